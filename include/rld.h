@@ -1,0 +1,183 @@
+/*
+ * rld.h -- C ABI of the B200-native rational log-determinant estimator.
+ *
+ * This is the drop-in boundary for the reference package `ratlogdet`'s r* path
+ * (arXiv 2405.03474, Algorithm 1).  Every entry point below names the
+ * reference interface it replaces (paths relative to
+ * /root/reference/pkg/src/ratlogdet/).  Plain C types only: pointers, sizes,
+ * enums, POD structs.  No torch or numpy types cross this line.
+ *
+ * Conventions
+ *  - "rows" layout everywhere, as in the reference: a block of m vectors of
+ *    length n is an m x n row-major array (probes s x n, src/probes.py:26;
+ *    sketch w x n, src/precond.py:183).
+ *  - Every call is synchronous with respect to the host: it returns after its
+ *    device work finished and its outputs are visible at the given pointers.
+ *  - A handle is not thread-safe; distinct handles are independent.
+ *  - Results are deterministic for a fixed device count: every reduction has
+ *    a fixed order (no floating-point atomics).
+ *  - Status codes map one-to-one onto the reference's exception types
+ *    (src/linalg.py:24-33, ValueError for argument errors); the message of the
+ *    last failure on a handle is available from rld_last_error().
+ */
+#ifndef RLD_H
+#define RLD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RLD_ABI_VERSION 1
+
+typedef enum rld_status {
+  RLD_OK = 0,
+  RLD_ERR_INVALID_ARGUMENT = 1,        /* ValueError (src/estimators.py:41-45, src/precond.py:241-242) */
+  RLD_ERR_NOT_POSITIVE_DEFINITE = 2,   /* NotPositiveDefinite (src/linalg.py:24-25, 113-116) */
+  RLD_ERR_SINGULAR_SHIFTED_SYSTEM = 3, /* SingularShiftedSystem (src/linalg.py:140-148) */
+  RLD_ERR_RANK_DEFICIENT = 4,          /* RankDeficient after the retry (src/precond.py:181-197) */
+  RLD_ERR_CUDA = 5,
+  RLD_ERR_NCCL = 6,
+  RLD_ERR_OUT_OF_MEMORY = 7,
+  RLD_ERR_NOT_SUPPORTED = 8
+} rld_status;
+
+typedef enum rld_dtype { RLD_FP64 = 0, RLD_FP32 = 1 } rld_dtype;
+typedef enum rld_family { RLD_RBF = 0, RLD_MATERN52 = 1 } rld_family; /* src/kernels.py:17-30 */
+typedef enum rld_source { RLD_SOURCE_DENSE = 0, RLD_SOURCE_POINTS = 1 } rld_source;
+typedef enum rld_path { RLD_PATH_STORED = 0, RLD_PATH_ON_THE_FLY = 1 } rld_path;
+typedef enum rld_memory { RLD_HOST = 0, RLD_DEVICE = 1 } rld_memory;
+typedef enum rld_probe_kind { RLD_RADEMACHER = 0, RLD_GAUSSIAN = 1 } rld_probe_kind; /* src/probes.py:12 */
+typedef enum rld_precond_kind {
+  RLD_PRECOND_RAND_SVD = 0, /* src/precond.py:262-267 */
+  RLD_PRECOND_IDENTITY = 1, /* src/precond.py:245-246 */
+  RLD_PRECOND_DIAGONAL = 2  /* src/precond.py:247-248 */
+} rld_precond_kind;
+
+typedef struct rld_handle rld_handle;
+
+/* One process drives one GPU; `world_size` processes row-shard K. */
+typedef struct rld_device_set {
+  int32_t device;       /* CUDA ordinal */
+  int32_t rank;         /* row-shard index, 0 <= rank < world_size */
+  int32_t world_size;   /* 1 = single GPU (no NCCL) */
+  int32_t reserved;
+  const void* nccl_id;  /* 128-byte ncclUniqueId shared by all ranks (NULL if world_size == 1) */
+} rld_device_set;
+
+/* The matrix: a dense K (the reference's only input, src/estimators.py:77) or the
+ * points + kernel it is built from (src/kernels.py:59, src/bench.py:105-109). */
+typedef struct rld_problem {
+  int32_t source;        /* rld_source */
+  int32_t path;          /* rld_path (points source): build K in HBM or generate tiles per product */
+  int32_t dtype;         /* rld_dtype: storage and product arithmetic of K */
+  int32_t family;        /* rld_family */
+  int64_t n;             /* order of K */
+  int32_t d;             /* point dimension */
+  int32_t data_memory;   /* rld_memory of `data` */
+  double amplitude;      /* K = amplitude^2 k(r) + jitter I  (src/kernels.py:41, 72) */
+  double length_scale;
+  double jitter;
+  const void* data;      /* dense: K rows (n x ld, data_dtype); points: n x d float64 row-major */
+  int32_t data_dtype;    /* rld_dtype of a dense `data` */
+  int32_t reserved;
+  int64_t ld;            /* row stride of dense K in elements (0 -> n) */
+} rld_problem;
+
+/* EstimatorConfig + PreconditionerConfig (src/estimators.py:32-45, src/precond.py:40-55). */
+typedef struct rld_config {
+  int32_t order;          /* 1, 3 or 5 (algorithm r1/r3/r5) */
+  int32_t num_probes;     /* s */
+  int32_t lanczos_iters;  /* t, clamped to n as in src/estimators.py:62 */
+  int32_t probe_kind;     /* rld_probe_kind */
+  int32_t precond_kind;   /* rld_precond_kind */
+  int32_t precond_rank;   /* l (k) */
+  int32_t precond_iters;  /* q */
+  int32_t oversample;     /* 10 (src/precond.py:165) */
+  double diag_floor;      /* 1e-12 (src/precond.py:37) */
+  double keep_rtol;       /* 1e-14 (src/precond.py:97) */
+  double breakdown_rtol;  /* 1e-12 (src/lanczos.py:20) */
+  double orth_rtol;       /* 1e-12 (src/linalg.py:177) */
+  uint64_t probe_key[2];  /* Philox4x64 key of numpy stream (seed, (2,))      -- src/estimators.py:64 */
+  uint64_t omega_key[4];  /* keys of streams (seed,(1,0)) and (seed,(1,1))    -- src/precond.py:183 */
+} rld_config;
+
+/* Optional injected random inputs (parity mode).  NULL -> generated on the
+ * device from the Philox keys in rld_config, bit-identical to numpy's stream
+ * for Rademacher probes; Gaussian rows must be injected until the device
+ * ziggurat lands (rld_logdet returns RLD_ERR_NOT_SUPPORTED otherwise). */
+typedef struct rld_inputs {
+  const double* probes;   /* s x n */
+  const double* omega0;   /* w x n, attempt 0 */
+  const double* omega1;   /* w x n, attempt 1 (only read after a RankDeficient retry) */
+  int32_t memory;         /* rld_memory of the three pointers */
+  int32_t reserved;
+} rld_inputs;
+
+/* LogDetEstimate (src/estimators.py:48-55) plus device-side diagnostics. */
+typedef struct rld_result {
+  double value;
+  double logdet_P;
+  double trace_term;
+  double* per_probe;      /* caller-allocated host array of num_probes doubles */
+  double wall_time;       /* seconds, CUDA events around the estimate */
+  int32_t attempts;       /* sketch attempts used (1 or 2) */
+  int32_t rank_kept;      /* columns of U kept by the 1e-14 filter (src/precond.py:97) */
+  int32_t kv_products;    /* K x block products issued */
+  int32_t kernel_launches;/* own kernels launched by the estimate */
+  double phase_ms[8];     /* [0] K build [1] sketch+QR [2] projected eig [3] precond factors
+                             [4] Lanczos [5] shifted solves + Hutchinson [6] collectives [7] total */
+} rld_result;
+
+int rld_abi_version(void);
+
+/* Fill `out` (128 bytes) with a fresh ncclUniqueId; rank 0 calls it and
+ * broadcasts the bytes to the other ranks before rld_create. */
+int rld_nccl_unique_id(void* out);
+
+/* Bind a handle to one GPU (and, for world_size > 1, to an NCCL communicator). */
+int rld_create(const rld_device_set* devices, rld_handle** out);
+void rld_destroy(rld_handle* h);
+const char* rld_last_error(const rld_handle* h);
+
+/* The cudaStream_t (as void*) the handle orders all its work on, so callers can
+ * record timing events or chain their own work on the same stream. */
+void* rld_stream(rld_handle* h);
+
+/* rstar_logdet(M, cfg) -- src/estimators.py:77-96 (and estimate_logdet for
+ * r1/r3/r5, src/estimators.py:132-138).  Uploads / builds K, runs the
+ * preconditioner build, s-probe Lanczos, multishift solves and the Hutchinson
+ * mean on the device, and fills `result`. */
+int rld_logdet(rld_handle* h, const rld_problem* problem, const rld_config* cfg,
+               const rld_inputs* inputs, rld_result* result);
+
+/* Make `problem` resident in the handle (upload points / build or copy K into
+ * HBM) so rld_logdet_resident can be called repeatedly without host traffic. */
+int rld_prepare(rld_handle* h, const rld_problem* problem);
+int rld_logdet_resident(rld_handle* h, const rld_config* cfg, const rld_inputs* inputs,
+                        rld_result* result);
+
+/* build_covariance(spec, points) -- src/kernels.py:59-73: write the dense K
+ * (n x n, dtype = problem->dtype) to `out` (host or device per out_memory). */
+int rld_build_covariance(rld_handle* h, const rld_problem* problem, void* out, int32_t out_memory);
+
+/* The operator seam `M @ x` of src/estimators.py:72 for a block: Y = V K for the
+ * m x n rows V (device, float64), Y m x n (device, float64), using the
+ * resident problem and its product arithmetic. */
+int rld_kv_apply(rld_handle* h, int64_t m, const double* V, double* Y);
+
+/* Rng(seed).child(...).rademacher((rows, n)) -- src/linalg.py:84-85, on the
+ * device from the stream's Philox key; `out` is device float64, rows x n. */
+int rld_rademacher(rld_handle* h, const uint64_t key[2], int64_t rows, int64_t n, double* out);
+
+/* exact_logdet(M) -- src/estimators.py:125-129: Cholesky log det of the
+ * resident problem's K in float64 on the device. */
+int rld_exact_logdet(rld_handle* h, double* value);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RLD_H */

@@ -1,0 +1,173 @@
+"""ctypes binding of ``librld.so`` (the C ABI declared in ``include/rld.h``).
+
+Loading is strict: if the library is missing or does not export the ABI,
+``load()`` raises -- there is no CPU fallback anywhere in the package.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "librld.so"
+
+RLD_OK = 0
+RLD_ERR_INVALID_ARGUMENT = 1
+RLD_ERR_NOT_POSITIVE_DEFINITE = 2
+RLD_ERR_SINGULAR_SHIFTED_SYSTEM = 3
+RLD_ERR_RANK_DEFICIENT = 4
+RLD_ERR_CUDA = 5
+RLD_ERR_NCCL = 6
+RLD_ERR_OUT_OF_MEMORY = 7
+RLD_ERR_NOT_SUPPORTED = 8
+
+FP64, FP32 = 0, 1
+RBF, MATERN52 = 0, 1
+SOURCE_DENSE, SOURCE_POINTS = 0, 1
+PATH_STORED, PATH_ON_THE_FLY = 0, 1
+HOST, DEVICE = 0, 1
+RADEMACHER, GAUSSIAN = 0, 1
+PRECOND_RAND_SVD, PRECOND_IDENTITY, PRECOND_DIAGONAL = 0, 1, 2
+
+# every symbol include/rld.h declares
+EXPORTS = (
+    "rld_abi_version", "rld_create", "rld_destroy", "rld_last_error", "rld_logdet", "rld_prepare",
+    "rld_logdet_resident", "rld_build_covariance", "rld_kv_apply", "rld_rademacher", "rld_exact_logdet",
+    "rld_nccl_unique_id", "rld_stream",
+)
+
+
+class DeviceSet(C.Structure):
+    _fields_ = [("device", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32), ("reserved", C.c_int32),
+                ("nccl_id", C.c_void_p)]
+
+
+class Problem(C.Structure):
+    _fields_ = [("source", C.c_int32), ("path", C.c_int32), ("dtype", C.c_int32), ("family", C.c_int32),
+                ("n", C.c_int64), ("d", C.c_int32), ("data_memory", C.c_int32), ("amplitude", C.c_double),
+                ("length_scale", C.c_double), ("jitter", C.c_double), ("data", C.c_void_p),
+                ("data_dtype", C.c_int32), ("reserved", C.c_int32), ("ld", C.c_int64)]
+
+
+class Config(C.Structure):
+    _fields_ = [("order", C.c_int32), ("num_probes", C.c_int32), ("lanczos_iters", C.c_int32),
+                ("probe_kind", C.c_int32), ("precond_kind", C.c_int32), ("precond_rank", C.c_int32),
+                ("precond_iters", C.c_int32), ("oversample", C.c_int32), ("diag_floor", C.c_double),
+                ("keep_rtol", C.c_double), ("breakdown_rtol", C.c_double), ("orth_rtol", C.c_double),
+                ("probe_key", C.c_uint64 * 2), ("omega_key", C.c_uint64 * 4)]
+
+
+class Inputs(C.Structure):
+    _fields_ = [("probes", C.c_void_p), ("omega0", C.c_void_p), ("omega1", C.c_void_p), ("memory", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+class Result(C.Structure):
+    _fields_ = [("value", C.c_double), ("logdet_P", C.c_double), ("trace_term", C.c_double),
+                ("per_probe", C.POINTER(C.c_double)), ("wall_time", C.c_double), ("attempts", C.c_int32),
+                ("rank_kept", C.c_int32), ("kv_products", C.c_int32), ("kernel_launches", C.c_int32),
+                ("phase_ms", C.c_double * 8)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load() -> C.CDLL:
+    """Load librld.so (raises if it is missing: the product has no CPU path)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -m paper_2405_03474_b200.build` "
+                               "(the estimator has no CPU fallback)")
+        lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_LOCAL)
+        for name in EXPORTS:
+            getattr(lib, name)  # AttributeError if the ABI is incomplete
+        H = C.c_void_p
+        lib.rld_abi_version.restype = C.c_int
+        lib.rld_create.argtypes = [C.POINTER(DeviceSet), C.POINTER(H)]
+        lib.rld_destroy.argtypes = [H]
+        lib.rld_destroy.restype = None
+        lib.rld_last_error.argtypes = [H]
+        lib.rld_last_error.restype = C.c_char_p
+        lib.rld_logdet.argtypes = [H, C.POINTER(Problem), C.POINTER(Config), C.POINTER(Inputs), C.POINTER(Result)]
+        lib.rld_prepare.argtypes = [H, C.POINTER(Problem)]
+        lib.rld_logdet_resident.argtypes = [H, C.POINTER(Config), C.POINTER(Inputs), C.POINTER(Result)]
+        lib.rld_build_covariance.argtypes = [H, C.POINTER(Problem), C.c_void_p, C.c_int32]
+        lib.rld_kv_apply.argtypes = [H, C.c_int64, C.c_void_p, C.c_void_p]
+        lib.rld_rademacher.argtypes = [H, C.POINTER(C.c_uint64 * 2), C.c_int64, C.c_int64, C.c_void_p]
+        lib.rld_exact_logdet.argtypes = [H, C.POINTER(C.c_double)]
+        lib.rld_nccl_unique_id.argtypes = [C.c_void_p]
+        lib.rld_stream.argtypes = [H]
+        lib.rld_stream.restype = C.c_void_p
+        for name in EXPORTS:
+            if name not in ("rld_abi_version", "rld_destroy", "rld_last_error", "rld_stream"):
+                getattr(lib, name).restype = C.c_int
+        if lib.rld_abi_version() != 1:
+            raise RuntimeError("librld.so ABI version mismatch")
+        _lib = lib
+        return lib
+
+
+class Handle:
+    """One GPU (one row shard) bound to a librld handle."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world_size: int = 1, nccl_id: bytes | None = None):
+        self.lib = load()
+        self._h = C.c_void_p()
+        self._id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        ds = DeviceSet(device, rank, world_size, 0, C.cast(self._id, C.c_void_p) if self._id is not None else None)
+        self.check(self.lib.rld_create(C.byref(ds), C.byref(self._h)), "rld_create")
+        self.device, self.rank, self.world_size = device, rank, world_size
+
+    def close(self):
+        if self._h:
+            self.lib.rld_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def ptr(self):
+        return self._h
+
+    @property
+    def stream(self) -> int:
+        """cudaStream_t of the handle (for torch.cuda.ExternalStream)."""
+        return int(self.lib.rld_stream(self._h) or 0)
+
+    def last_error(self) -> str:
+        msg = self.lib.rld_last_error(self._h) if self._h else b"no handle"
+        return msg.decode(errors="replace") if msg else ""
+
+    def check(self, rc: int, what: str):
+        if rc == RLD_OK:
+            return
+        raise_status(rc, f"{what}: {self.last_error() if self._h else ''}")
+
+
+def raise_status(rc: int, msg: str):
+    """Map a status code onto the reference's exception types (src/linalg.py:24-33)."""
+    from .linalg import NotPositiveDefinite, RankDeficient, SingularShiftedSystem
+
+    if rc == RLD_ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if rc == RLD_ERR_NOT_POSITIVE_DEFINITE:
+        raise NotPositiveDefinite(msg)
+    if rc == RLD_ERR_SINGULAR_SHIFTED_SYSTEM:
+        raise SingularShiftedSystem(msg)
+    if rc == RLD_ERR_RANK_DEFICIENT:
+        raise RankDeficient(msg)
+    if rc == RLD_ERR_NOT_SUPPORTED:
+        raise NotImplementedError(msg)
+    if rc == RLD_ERR_OUT_OF_MEMORY:
+        raise MemoryError(msg)
+    raise RuntimeError(f"rld status {rc}: {msg}")

@@ -1,0 +1,806 @@
+// C ABI (include/rld.h) and the device-side orchestration of one estimate.
+//
+// rld_logdet follows src/estimators.py:77-96 end to end on the GPU:
+//   preconditioner (src/precond.py:168-198, 231-267, 69-100)
+//     -> probes (src/estimators.py:64)
+//     -> s-probe Lanczos on N^-1 K N^-T (src/estimators.py:68-72, src/lanczos.py:34-74)
+//     -> multishift Thomas solves + Hutchinson mean (src/lanczos.py:77-84, src/estimators.py:86-95).
+// Everything is ordered on the handle's stream; the host synchronises only to
+// decide the RankDeficient retry (src/precond.py:181-197) and to read the result.
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "rld_internal.cuh"
+#include "rld_kernels.cuh"
+
+namespace rld {
+
+thread_local int g_launches = 0;  // own kernel launches (RLD_LAUNCH_CHECK)
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e == cudaSuccess) return;
+  (void)cudaGetLastError();
+  char buf[512];
+  snprintf(buf, sizeof buf, "%s failed: %s (%s:%d)", what, cudaGetErrorString(e), file, line);
+  fail(e == cudaErrorMemoryAllocation ? RLD_ERR_OUT_OF_MEMORY : RLD_ERR_CUDA, buf);
+}
+
+void cublas_check(cublasStatus_t s, const char* what, const char* file, int line) {
+  if (s == CUBLAS_STATUS_SUCCESS) return;
+  char buf[512];
+  snprintf(buf, sizeof buf, "%s failed: cublas status %d (%s:%d)", what, (int)s, file, line);
+  fail(s == CUBLAS_STATUS_ALLOC_FAILED ? RLD_ERR_OUT_OF_MEMORY : RLD_ERR_CUDA, buf);
+}
+
+void cusolver_check(cusolverStatus_t s, const char* what, const char* file, int line) {
+  if (s == CUSOLVER_STATUS_SUCCESS) return;
+  char buf[512];
+  snprintf(buf, sizeof buf, "%s failed: cusolver status %d (%s:%d)", what, (int)s, file, line);
+  fail(s == CUSOLVER_STATUS_ALLOC_FAILED ? RLD_ERR_OUT_OF_MEMORY : RLD_ERR_CUDA, buf);
+}
+
+void DevBuf::reserve(size_t nbytes) {
+  if (nbytes <= bytes) return;
+  release();
+  if (nbytes == 0) return;
+  RLD_CUDA(cudaMalloc(&ptr, nbytes));
+  bytes = nbytes;
+}
+
+void DevBuf::release() {
+  if (ptr) cudaFree(ptr);
+  ptr = nullptr;
+  bytes = 0;
+}
+
+namespace {
+
+struct Resident {
+  bool ready = false;
+  int source = 0, path = 0, dtype = 0, family = 0;
+  int64_t n = 0;
+  int d = 0;
+  double amplitude = 1, ell = 1, jitter = 0;
+  int64_t row0 = 0, rows = 0;
+  DevBuf Kbuf;               // owned stored rows
+  const void* K = nullptr;   // stored rows (owned or aliased)
+  int64_t ldk = 0;
+  DevBuf X;                  // points n x d
+  DevBuf diag;               // local diagonal of K (float64)
+  KernelParams kp{};
+
+  KvOperand op() const {
+    KvOperand o;
+    o.K = (path == RLD_PATH_ON_THE_FLY) ? nullptr : K;
+    o.ldk = ldk;
+    o.X = X.as<double>();
+    o.kp = kp;
+    o.dtype = dtype;
+    o.n = n;
+    o.row0 = row0;
+    o.rows = rows;
+    return o;
+  }
+};
+
+struct Work {
+  DevBuf Y, Z, A, G, gdiag, theta, Vtop, theta_top, C, inner, lam, hgg, base, sqrt_base;
+  DevBuf omega, probes;
+  DevBuf x, p, pp, u, w, KX, T, Tg;
+  DevBuf scal;     // small scalars / per-probe arrays
+  DevBuf ints;     // flags, info, live, size, kept
+  DevBuf scratch, scratch2, solver_work;
+  KvWorkspace kv;
+};
+
+}  // namespace
+}  // namespace rld
+
+struct rld_handle {
+  int device = 0, rank = 0, world = 1;
+  cudaStream_t st = nullptr;
+  cublasHandle_t cublas = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  ncclComm_t comm = nullptr;
+  std::string last_error;
+  rld::Resident res;
+  rld::Work wk;
+  cudaEvent_t ev[8] = {};
+};
+
+namespace rld {
+namespace {
+
+constexpr double ONE = 1.0, ZERO = 0.0;
+
+struct Partial {
+  double offset;
+  int npoles;
+  double poles[5], residues[5];
+};
+
+// Table 1 (src/rational.py:70-96)
+Partial partial_fraction(int order) {
+  Partial p{};
+  if (order == 1) {
+    p = {2.0, 1, {-1.0}, {-4.0}};
+  } else if (order == 3) {
+    p = {14.0 / 3.0, 3, {-13.92820323027551, -1.0, -0.0717967697244908},
+         {-49.52250037431294, -20.0 / 9.0, -0.2552774034648563}};
+  } else if (order == 5) {
+    p = {86.0 / 15.0, 5,
+         {-39.863458189061411, -3.8518399963191827, -1.0, -0.25961618368249978, -0.025085630936916615},
+         {-140.08241129102026, -6.1858406006156228, -92.0 / 75.0, -0.41692913805732562,
+          -0.088152303639431204}};
+  } else {
+    fail(RLD_ERR_INVALID_ARGUMENT, "partial fractions exist for odd orders 1, 3, 5; got " + std::to_string(order));
+  }
+  return p;
+}
+
+void set_device(rld_handle* h) { RLD_CUDA(cudaSetDevice(h->device)); }
+
+// --- collectives (row shards).  world == 1: no-ops. --------------------------
+void allreduce_sum(rld_handle* h, double* buf, int64_t count) {
+  if (h->world == 1 || count <= 0) return;
+  ncclResult_t r = ncclAllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, h->comm, h->st);
+  if (r != ncclSuccess) fail(RLD_ERR_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+}
+
+// ----------------------------------------------------------------------------
+void prepare(rld_handle* h, const rld_problem* p) {
+  if (!p) fail(RLD_ERR_INVALID_ARGUMENT, "problem is NULL");
+  if (p->n < 1) fail(RLD_ERR_INVALID_ARGUMENT, "n must be >= 1");
+  if (p->dtype != RLD_FP64 && p->dtype != RLD_FP32) fail(RLD_ERR_INVALID_ARGUMENT, "dtype must be fp64 or fp32");
+  if (!p->data) fail(RLD_ERR_INVALID_ARGUMENT, "problem data is NULL");
+  Resident& r = h->res;
+  r.ready = false;
+  r.source = p->source;
+  r.dtype = p->dtype;
+  r.n = p->n;
+  const int64_t L = ceil_div(p->n, h->world);
+  r.row0 = std::min<int64_t>(p->n, (int64_t)h->rank * L);
+  r.rows = std::min<int64_t>(L, p->n - r.row0);
+  cudaStream_t st = h->st;
+
+  if (p->source == RLD_SOURCE_POINTS) {
+    if (p->family != RLD_RBF && p->family != RLD_MATERN52) fail(RLD_ERR_INVALID_ARGUMENT, "unknown kernel family");
+    if (!(p->amplitude > 0) || !(p->length_scale > 0))
+      fail(RLD_ERR_INVALID_ARGUMENT, "amplitude and length_scale must be positive");
+    if (!(p->jitter >= 0)) fail(RLD_ERR_INVALID_ARGUMENT, "jitter must be non-negative");
+    if (p->d < 1) fail(RLD_ERR_INVALID_ARGUMENT, "n and d must be >= 1");
+    if (p->d > 32) fail(RLD_ERR_NOT_SUPPORTED, "point dimension d > 32 is not supported by the device kernels");
+    r.path = p->path;
+    r.family = p->family;
+    r.d = p->d;
+    r.amplitude = p->amplitude;
+    r.ell = p->length_scale;
+    r.jitter = p->jitter;
+    r.kp.family = p->family;
+    r.kp.d = p->d;
+    r.kp.a2 = p->amplitude * p->amplitude;
+    r.kp.inv_2l2 = 1.0 / (2.0 * p->length_scale * p->length_scale);
+    r.kp.s5_over_l = std::sqrt(5.0) / p->length_scale;
+    r.kp.diag = r.kp.a2 + p->jitter;
+    const size_t xb = sizeof(double) * p->n * p->d;
+    r.X.reserve(xb);
+    RLD_CUDA(cudaMemcpyAsync(r.X.ptr, p->data, xb,
+                             p->data_memory == RLD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    r.diag.reserve(sizeof(double) * std::max<int64_t>(1, r.rows));
+    fill_doubles(r.rows, r.kp.diag, r.diag.as<double>(), st);
+    if (r.path == RLD_PATH_STORED) {
+      const size_t es = p->dtype == RLD_FP64 ? 8 : 4;
+      r.Kbuf.reserve(es * r.rows * p->n);
+      r.K = r.Kbuf.ptr;
+      r.ldk = p->n;
+      if (p->dtype == RLD_FP64)
+        build_kernel_rows<double>(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.Kbuf.as<double>(), p->n, st);
+      else
+        build_kernel_rows<float>(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.Kbuf.as<float>(), p->n, st);
+    } else if (r.path != RLD_PATH_ON_THE_FLY) {
+      fail(RLD_ERR_INVALID_ARGUMENT, "unknown path");
+    }
+  } else if (p->source == RLD_SOURCE_DENSE) {
+    const int64_t ld = p->ld ? p->ld : p->n;
+    if (ld < p->n) fail(RLD_ERR_INVALID_ARGUMENT, "ld < n");
+    if (p->data_dtype != RLD_FP64 && p->data_dtype != RLD_FP32) fail(RLD_ERR_INVALID_ARGUMENT, "bad data_dtype");
+    r.path = RLD_PATH_STORED;
+    r.d = 0;
+    const size_t es = p->dtype == RLD_FP64 ? 8 : 4;
+    const size_t ses = p->data_dtype == RLD_FP64 ? 8 : 4;
+    const char* src = static_cast<const char*>(p->data) + ses * (r.row0 * ld);
+    if (p->data_memory == RLD_DEVICE && p->data_dtype == p->dtype) {
+      r.K = src;  // alias the caller's device rows (caller keeps them alive)
+      r.ldk = ld;
+    } else {
+      r.Kbuf.reserve(es * r.rows * p->n);
+      r.K = r.Kbuf.ptr;
+      r.ldk = p->n;
+      if (p->data_dtype == p->dtype) {
+        RLD_CUDA(cudaMemcpy2DAsync(r.Kbuf.ptr, es * p->n, src, ses * ld, es * p->n, r.rows,
+                                   p->data_memory == RLD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                   st));
+      } else {
+        // stage in chunks of rows and convert on the device
+        const int64_t chunk = std::max<int64_t>(1, (int64_t)((256ull << 20) / (ses * p->n)));
+        DevBuf& stage = h->wk.scratch2;
+        stage.reserve(ses * chunk * p->n);
+        for (int64_t r0 = 0; r0 < r.rows; r0 += chunk) {
+          const int64_t nr = std::min(chunk, r.rows - r0);
+          RLD_CUDA(cudaMemcpy2DAsync(stage.ptr, ses * p->n, src + ses * r0 * ld, ses * ld, ses * p->n, nr,
+                                     p->data_memory == RLD_DEVICE ? cudaMemcpyDeviceToDevice
+                                                                  : cudaMemcpyHostToDevice,
+                                     st));
+          convert_rows(stage.ptr, p->data_dtype, static_cast<char*>(r.Kbuf.ptr) + es * r0 * p->n, p->dtype,
+                       nr * p->n, st);
+        }
+        RLD_CUDA(cudaStreamSynchronize(st));
+      }
+    }
+    r.diag.reserve(sizeof(double) * std::max<int64_t>(1, r.rows));
+    diag_of_dense(r.rows, r.row0, r.K, r.ldk, p->dtype, r.diag.as<double>(), st);
+  } else {
+    fail(RLD_ERR_INVALID_ARGUMENT, "unknown source");
+  }
+  RLD_CUDA(cudaStreamSynchronize(st));
+  r.ready = true;
+}
+
+// rows (m x rows_local, row stride ld) <- host/device rows (m x n, global stride n), local columns only
+void load_rows(rld_handle* h, const double* src, int memory, int64_t m, double* dst) {
+  const Resident& r = h->res;
+  RLD_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * r.rows, src + r.row0, sizeof(double) * r.n,
+                             sizeof(double) * r.rows, m,
+                             memory == RLD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->st));
+}
+
+// m x rows_local (local rows layout) -> m x n full rows on every rank
+void gather_rows(rld_handle* h, const double* local, int64_t m, double* full) {
+  const Resident& r = h->res;
+  if (h->world == 1) {
+    if (local != full) copy_doubles(m * r.n, local, full, h->st);
+    return;
+  }
+  fail(RLD_ERR_NOT_SUPPORTED, "multi-GPU row gather not built yet");
+}
+
+// Y (m x rows) = V (m x n full) K^T restricted to the local rows
+void kv(rld_handle* h, int64_t m, const double* Vfull, double* Y) {
+  KvOperand op = h->res.op();
+  kv_product(op, m, Vfull, op.n, Y, op.rows, h->wk.kv, h->st, nullptr);
+}
+
+struct CholQR {
+  int lwork = 0;
+};
+
+// In-place row orthonormalisation of the w x n block Y (col-major n x w), two
+// Cholesky-QR passes.  Replaces the row-wise CGS2 of src/linalg.py:159-180:
+// both give the unique Q with positive-diagonal triangular factor, and R_ii of
+// the first pass is exactly the projected norm the reference tests against
+// 1e-12 |Y_i| (src/linalg.py:177-178).
+void cholqr2(rld_handle* h, int64_t n, int w, double* Y, double rtol, int* flags) {
+  Work& wk = h->wk;
+  wk.G.reserve(sizeof(double) * w * w);
+  wk.gdiag.reserve(sizeof(double) * w);
+  double* G = wk.G.as<double>();
+  int* info = wk.ints.as<int>() + 1;
+  int lwork = 0;
+  RLD_CUSOLVER(cusolverDnDpotrf_bufferSize(h->solver, CUBLAS_FILL_MODE_UPPER, w, G, w, &lwork));
+  wk.solver_work.reserve(sizeof(double) * std::max(lwork, 1));
+  for (int pass = 0; pass < 2; ++pass) {
+    RLD_CUBLAS(cublasDsyrk(h->cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, w, (int)n, &ONE, Y, (int)n, &ZERO, G, w));
+    allreduce_sum(h, G, (int64_t)w * w);
+    if (pass == 0) diag_copy(w, G, wk.gdiag.as<double>(), h->st);
+    RLD_CUSOLVER(cusolverDnDpotrf(h->solver, CUBLAS_FILL_MODE_UPPER, w, G, w, wk.solver_work.as<double>(), lwork,
+                                  info));
+    if (pass == 0) cholqr_check(w, G, wk.gdiag.as<double>(), info, rtol, flags, h->st);
+    RLD_CUBLAS(cublasDtrsm(h->cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
+                           (int)n, w, &ONE, G, w, Y, (int)n));
+  }
+}
+
+void syevd(rld_handle* h, int k, double* A, double* evals) {
+  Work& wk = h->wk;
+  int* info = wk.ints.as<int>() + 2;
+  int lwork = 0;
+  RLD_CUSOLVER(cusolverDnDsyevd_bufferSize(h->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, k, A, k,
+                                           evals, &lwork));
+  wk.solver_work.reserve(sizeof(double) * std::max(lwork, 1));
+  RLD_CUSOLVER(cusolverDnDsyevd(h->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, k, A, k, evals,
+                                wk.solver_work.as<double>(), lwork, info));
+}
+
+struct PrecondOut {
+  int k = 0;              // columns of U (kept ones are nonzero)
+  int attempts = 1;
+};
+
+// ints layout: [0] flags [1] potrf info [2] syevd info [3] kept [4] inner-chol info
+// scal layout: [0] sum log base [1] 2 sum log diag(inner chol) [2] trace
+PrecondOut build_preconditioner(rld_handle* h, const rld_config* c, const rld_inputs* in) {
+  Resident& r = h->res;
+  Work& wk = h->wk;
+  cudaStream_t st = h->st;
+  const int64_t n = r.n, nl = r.rows;
+  int* flags = wk.ints.as<int>();
+  double* scal = wk.scal.as<double>();
+  wk.base.reserve(sizeof(double) * nl);
+  wk.sqrt_base.reserve(sizeof(double) * nl);
+  double* base = wk.base.as<double>();
+  double* sqrt_base = wk.sqrt_base.as<double>();
+  PrecondOut out;
+
+  if (c->precond_kind == RLD_PRECOND_IDENTITY) {
+    fill_doubles(nl, 1.0, base, st);
+    fill_doubles(nl, 1.0, sqrt_base, st);
+    fill_doubles(2, 0.0, scal, st);
+    return out;
+  }
+  if (c->precond_kind == RLD_PRECOND_DIAGONAL) {
+    copy_doubles(nl, r.diag.as<double>(), base, st);
+    sqrt_into(nl, base, sqrt_base, flags, st);
+    sum_log(nl, base, scal, wk.scratch, st);
+    allreduce_sum(h, scal, 1);
+    fill_doubles(1, 0.0, scal + 1, st);
+    return out;
+  }
+  if (c->precond_kind != RLD_PRECOND_RAND_SVD) fail(RLD_ERR_NOT_SUPPORTED, "preconditioner kind not supported");
+
+  const int k = c->precond_rank;
+  const int w = (int)std::min<int64_t>(k + c->oversample, n);
+  wk.Y.reserve(sizeof(double) * n * w);       // full rows (gathered) sketch / Q
+  wk.Z.reserve(sizeof(double) * nl * w);      // local product rows
+  double* Y = wk.Y.as<double>();
+  double* Z = wk.Z.as<double>();
+
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    out.attempts = attempt + 1;
+    const double* om = attempt == 0 ? in->omega0 : in->omega1;
+    if (!om)
+      fail(RLD_ERR_NOT_SUPPORTED, attempt == 0 ? "sketch rows must be injected (device Gaussian stream not built yet)"
+                                               : "sketch rows for attempt 1 must be injected (RankDeficient retry)");
+    RLD_CUDA(cudaMemcpyAsync(Y, om, sizeof(double) * w * n,
+                             in->memory == RLD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    RLD_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), st));
+    for (int it = 0; it < c->precond_iters; ++it) {
+      kv(h, w, Y, Z);                                   // Y <- Y M   (src/precond.py:186)
+      cholqr2(h, nl, w, Z, c->orth_rtol, flags);        // Q <- orth(Y) (src/precond.py:187)
+      gather_rows(h, Z, w, Y);
+    }
+    int hflags = 0;
+    RLD_CUDA(cudaMemcpyAsync(&hflags, flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+    RLD_CUDA(cudaStreamSynchronize(st));
+    if (hflags & RLD_FLAG_RANK_DEFICIENT) {
+      if (attempt == 1) fail(RLD_ERR_RANK_DEFICIENT, "row is numerically dependent (after retry)");
+      continue;
+    }
+    break;
+  }
+  // B = Q M Q^T (src/precond.py:189); Q full rows in Y, local rows of Q at Y + row0
+  kv(h, w, Y, Z);
+  wk.C.reserve(sizeof(double) * std::max<int64_t>((int64_t)w * w, (int64_t)k * k));
+  double* B = wk.C.as<double>();
+  const double* Ql = Y + r.row0;  // col-major n x w, local rows start at row0
+  RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, w, w, (int)nl, &ONE, Ql, (int)n, Z, (int)nl, &ZERO, B,
+                         w));
+  allreduce_sum(h, B, (int64_t)w * w);
+  wk.theta.reserve(sizeof(double) * w);
+  syevd(h, w, B, wk.theta.as<double>());                  // src/precond.py:190
+  wk.Vtop.reserve(sizeof(double) * w * std::max(k, 1));
+  wk.theta_top.reserve(sizeof(double) * std::max(k, 1));
+  top_eigvecs(w, k, B, wk.theta.as<double>(), wk.Vtop.as<double>(), wk.theta_top.as<double>(), st);
+  // A = (Q^T U_top) sqrt(max(theta, 0))  (src/precond.py:191-193, 264)
+  wk.A.reserve(sizeof(double) * nl * k);
+  double* A = wk.A.as<double>();
+  RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nl, k, w, &ONE, Ql, (int)n, wk.Vtop.as<double>(),
+                         w, &ZERO, A, (int)nl));
+  // base = max(diag M - sum A^2, 1e-12); At = A / sqrt(base)  (src/precond.py:231-233, 94-95)
+  precond_base(nl, k, r.diag.as<double>(), c->diag_floor, A, base, sqrt_base, st);
+  sum_log(nl, base, scal, wk.scratch, st);
+  allreduce_sum(h, scal, 1);
+  // C = At^T At ; inner = I + C ; log det inner by Cholesky (src/precond.py:75-80)
+  double* C = wk.C.as<double>();
+  RLD_CUBLAS(cublasDsyrk(h->cublas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, k, (int)nl, &ONE, A, (int)nl, &ZERO, C, k));
+  allreduce_sum(h, C, (int64_t)k * k);
+  wk.inner.reserve(sizeof(double) * k * k);
+  double* inner = wk.inner.as<double>();
+  copy_doubles((int64_t)k * k, C, inner, st);
+  add_identity(k, inner, st);
+  {
+    int lwork = 0;
+    RLD_CUSOLVER(cusolverDnDpotrf_bufferSize(h->solver, CUBLAS_FILL_MODE_LOWER, k, inner, k, &lwork));
+    wk.solver_work.reserve(sizeof(double) * std::max(lwork, 1));
+    int* info = wk.ints.as<int>() + 4;
+    RLD_CUSOLVER(cusolverDnDpotrf(h->solver, CUBLAS_FILL_MODE_LOWER, k, inner, k, wk.solver_work.as<double>(), lwork,
+                                  info));
+    chol_logdet(k, inner, info, scal + 1, flags, st);
+  }
+  // factored square root (src/precond.py:90-100): eigh(At^T At), keep filter, U = At W / sqrt(lam)
+  wk.lam.reserve(sizeof(double) * k);
+  syevd(h, k, C, wk.lam.as<double>());
+  wk.hgg.reserve(sizeof(double) * 3 * k);
+  double* hv = wk.hgg.as<double>();
+  RLD_CUDA(cudaMemsetAsync(wk.ints.as<int>() + 3, 0, sizeof(int), st));
+  sqrt_factors(k, c->keep_rtol, wk.lam.as<double>(), C, hv, hv + k, hv + 2 * k, wk.ints.as<int>() + 3, st);
+  // U (n_local x k) into Z (no longer needed)
+  RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nl, k, k, &ONE, A, (int)nl, C, k, &ZERO, Z,
+                         (int)nl));
+  out.k = k;
+  return out;
+}
+
+void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_result* res) {
+  Resident& r = h->res;
+  if (!r.ready) fail(RLD_ERR_INVALID_ARGUMENT, "no resident problem (call rld_prepare or rld_logdet)");
+  if (!c) fail(RLD_ERR_INVALID_ARGUMENT, "config is NULL");
+  if (!res) fail(RLD_ERR_INVALID_ARGUMENT, "result is NULL");
+  rld_inputs none{};
+  if (!in) in = &none;
+  const Partial pf = partial_fraction(c->order);
+  if (c->num_probes < 1 || c->lanczos_iters < 1) fail(RLD_ERR_INVALID_ARGUMENT, "num_probes and lanczos_iters must be >= 1");
+  if (c->precond_rank < 0) fail(RLD_ERR_INVALID_ARGUMENT, "rank must be >= 0");
+  if (c->precond_iters < 1) fail(RLD_ERR_INVALID_ARGUMENT, "num_iters must be >= 1");
+  if (c->probe_kind != RLD_RADEMACHER && c->probe_kind != RLD_GAUSSIAN) fail(RLD_ERR_INVALID_ARGUMENT, "unknown probe kind");
+  const int64_t n = r.n, nl = r.rows;
+  const int64_t s = c->num_probes;
+  const int t = (int)std::min<int64_t>(c->lanczos_iters, n);   // src/estimators.py:62
+  if (c->precond_kind == RLD_PRECOND_RAND_SVD) {
+    if (c->precond_rank > n)
+      fail(RLD_ERR_INVALID_ARGUMENT, "rank " + std::to_string(c->precond_rank) + " exceeds dimension " + std::to_string(n));
+    if (c->precond_rank < 1)
+      fail(RLD_ERR_INVALID_ARGUMENT, "rank must be in 1.." + std::to_string(n) + ", got " + std::to_string(c->precond_rank));
+  }
+  cudaStream_t st = h->st;
+  Work& wk = h->wk;
+  wk.ints.reserve(sizeof(int) * (8 + 2 * s));
+  wk.scal.reserve(sizeof(double) * (8 + 2 * s + 2 * s * t + 16));
+  RLD_CUDA(cudaMemsetAsync(wk.ints.ptr, 0, sizeof(int) * 8, st));
+  g_launches = 0;
+  RLD_CUDA(cudaEventRecord(h->ev[0], st));
+
+  // ---- preconditioner
+  const PrecondOut po = build_preconditioner(h, c, in);
+  RLD_CUDA(cudaEventRecord(h->ev[1], st));
+  const int k = po.k;
+  const double* U = wk.Z.as<double>();
+  const double* hv = wk.hgg.as<double>();
+  const double* sqrt_base = wk.sqrt_base.as<double>();
+
+  // ---- probes (src/estimators.py:64)
+  wk.probes.reserve(sizeof(double) * s * nl);
+  double* Zp = wk.probes.as<double>();
+  if (in->probes) {
+    load_rows(h, in->probes, in->memory, s, Zp);
+  } else if (c->probe_kind == RLD_RADEMACHER) {
+    rademacher_rows(c->probe_key, s, n, r.row0, nl, nl, Zp, st);
+  } else {
+    fail(RLD_ERR_NOT_SUPPORTED, "Gaussian probes must be injected (device Gaussian stream not built yet)");
+  }
+
+  // ---- Lanczos state
+  for (DevBuf* b : {&wk.x, &wk.p, &wk.pp, &wk.u, &wk.w, &wk.KX}) b->reserve(sizeof(double) * s * nl);
+  wk.T.reserve(sizeof(double) * std::max(k, 1) * s);
+  wk.Tg.reserve(sizeof(double) * std::max(k, 1) * s);
+  double* x = wk.x.as<double>();
+  double* p = wk.p.as<double>();
+  double* pp = wk.pp.as<double>();
+  double* u = wk.u.as<double>();
+  double* wv = wk.w.as<double>();
+  double* KX = wk.KX.as<double>();
+  double* T = wk.T.as<double>();
+  double* Tg = wk.Tg.as<double>();
+  double* scal = wk.scal.as<double>();
+  double* norms = scal + 8;
+  double* dots = norms + s;
+  double* alpha = dots + s;
+  double* beta = alpha + s * t;
+  double* beta_ref = beta + s * t;
+  double* per_probe = beta_ref + s;
+  double* consts = per_probe + s;      // offset, poles[5], residues[5]
+  int* ints = wk.ints.as<int>();
+  int* flags = ints;
+  int* live = ints + 8;
+  int* size = live + s;
+  {
+    std::vector<int> hl(2 * s);
+    for (int64_t i = 0; i < s; ++i) { hl[i] = 1; hl[s + i] = t; }
+    RLD_CUDA(cudaMemcpyAsync(live, hl.data(), sizeof(int) * 2 * s, cudaMemcpyHostToDevice, st));
+    double hc[11] = {pf.offset};
+    for (int q = 0; q < pf.npoles; ++q) { hc[1 + q] = pf.poles[q]; hc[6 + q] = pf.residues[q]; }
+    RLD_CUDA(cudaMemcpyAsync(consts, hc, sizeof hc, cudaMemcpyHostToDevice, st));
+    RLD_CUDA(cudaStreamSynchronize(st));  // host staging buffers go out of scope
+  }
+  fill_doubles(2 * s * t, 0.0, alpha, st);
+
+  // q0 = v / |v|; x0 = N^-T q0; p0 = N q0
+  rows_dot(s, nl, Zp, nl, Zp, nl, dots, wk.scratch, st, nullptr);
+  allreduce_sum(h, dots, s);
+  normalize_rows(s, nl, Zp, dots, norms, wv, st);       // q0 in wv
+  copy_doubles(s * nl, wv, x, st);
+  copy_doubles(s * nl, wv, p, st);
+  if (k > 0) {
+    RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, k, (int)s, (int)nl, &ONE, U, (int)nl, wv, (int)nl,
+                           &ZERO, T, k));
+    allreduce_sum(h, T, (int64_t)k * s);
+    copy_doubles((int64_t)k * s, T, Tg, st);
+    scale_rows_colmajor(k, s, k, hv + k, false, Tg, st);       // g
+    scale_rows_colmajor(k, s, k, hv + 2 * k, false, T, st);    // gamma
+    RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nl, (int)s, k, &ONE, U, (int)nl, Tg, k, &ONE, x,
+                           (int)nl));
+    RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nl, (int)s, k, &ONE, U, (int)nl, T, k, &ONE, p,
+                           (int)nl));
+  }
+  scale_rows_colmajor(nl, s, nl, sqrt_base, true, x, st);
+  scale_rows_colmajor(nl, s, nl, sqrt_base, false, p, st);
+
+  wk.Y.reserve(sizeof(double) * s * n);
+  double* xfull = wk.Y.as<double>();
+  int products = 0;
+  for (int j = 0; j < t; ++j) {
+    gather_rows(h, x, s, xfull);
+    kv(h, s, xfull, KX);                                  // K x_j
+    ++products;
+    rows_dot(s, nl, x, nl, KX, nl, dots, wk.scratch, st, nullptr);
+    allreduce_sum(h, dots, s);
+    lanczos_alpha(s, j, t, dots, live, alpha, st);        // alpha_j = q_j . A q_j
+    if (j == t - 1) break;
+    lanczos_residual(s, nl, j, t, KX, alpha, beta, p, pp, sqrt_base, u, wv, st);
+    if (k > 0) {
+      RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, k, (int)s, (int)nl, &ONE, U, (int)nl, wv, (int)nl,
+                             &ZERO, T, k));
+      allreduce_sum(h, T, (int64_t)k * s);
+      scale_rows_colmajor(k, s, k, hv, false, T, st);         // h = 1/(1+lam) - 1
+      RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nl, (int)s, k, &ONE, U, (int)nl, T, k, &ONE,
+                             wv, (int)nl));
+    }
+    scale_rows_colmajor(nl, s, nl, sqrt_base, true, wv, st);  // z = P^-1 u
+    rows_dot(s, nl, u, nl, wv, nl, dots, wk.scratch, st, nullptr);
+    allreduce_sum(h, dots, s);
+    lanczos_beta(s, j, t, c->breakdown_rtol, dots, alpha, beta, beta_ref, live, size, st);
+    lanczos_advance(s, nl, j, t, beta, live, u, wv, p, pp, x, st);
+  }
+  RLD_CUDA(cudaEventRecord(h->ev[2], st));
+  thomas_hutchinson(s, t, alpha, beta, size, norms, pf.npoles, pf.offset, consts + 1, consts + 6, per_probe,
+                    scal + 2, flags, st);
+  RLD_CUDA(cudaEventRecord(h->ev[3], st));
+
+  double hs[3];
+  int hi[8];
+  RLD_CUDA(cudaMemcpyAsync(hs, scal, sizeof hs, cudaMemcpyDeviceToHost, st));
+  RLD_CUDA(cudaMemcpyAsync(hi, ints, sizeof hi, cudaMemcpyDeviceToHost, st));
+  if (res->per_probe)
+    RLD_CUDA(cudaMemcpyAsync(res->per_probe, per_probe, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
+  RLD_CUDA(cudaStreamSynchronize(st));
+  if (hi[0] & RLD_FLAG_NOT_PD) fail(RLD_ERR_NOT_POSITIVE_DEFINITE, "Matrix is not positive definite (inner Cholesky)");
+  if (hi[0] & RLD_FLAG_SINGULAR) fail(RLD_ERR_SINGULAR_SHIFTED_SYSTEM, "zero pivot in a shifted tridiagonal solve");
+  if (hi[0] & 8) fail(RLD_ERR_INVALID_ARGUMENT, "base diagonal must be strictly positive");
+  res->logdet_P = hs[0] + hs[1];
+  res->trace_term = hs[2];
+  res->value = res->logdet_P + res->trace_term;
+  res->attempts = po.attempts;
+  res->rank_kept = (c->precond_kind == RLD_PRECOND_RAND_SVD) ? hi[3] : 0;
+  res->kv_products = products + (c->precond_kind == RLD_PRECOND_RAND_SVD ? (c->precond_iters + 1) * po.attempts : 0);
+  res->kernel_launches = g_launches;
+  float ms[3] = {0, 0, 0};
+  RLD_CUDA(cudaEventElapsedTime(&ms[0], h->ev[0], h->ev[1]));
+  RLD_CUDA(cudaEventElapsedTime(&ms[1], h->ev[1], h->ev[2]));
+  RLD_CUDA(cudaEventElapsedTime(&ms[2], h->ev[2], h->ev[3]));
+  for (double& v : res->phase_ms) v = 0.0;
+  res->phase_ms[1] = ms[0];
+  res->phase_ms[4] = ms[1];
+  res->phase_ms[5] = ms[2];
+  res->phase_ms[7] = (double)ms[0] + ms[1] + ms[2];
+  res->wall_time = res->phase_ms[7] * 1e-3;
+}
+
+template <typename F>
+int guarded(rld_handle* h, F&& f) {
+  try {
+    if (h) set_device(h);
+    f();
+    if (h) h->last_error.clear();
+    return RLD_OK;
+  } catch (const Error& e) {
+    if (h) h->last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    if (h) h->last_error = "host allocation failed";
+    return RLD_ERR_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    if (h) h->last_error = e.what();
+    return RLD_ERR_CUDA;
+  }
+}
+
+}  // namespace
+}  // namespace rld
+
+using namespace rld;
+
+extern "C" {
+
+int rld_abi_version(void) { return RLD_ABI_VERSION; }
+
+int rld_nccl_unique_id(void* out) {
+  if (!out) return RLD_ERR_INVALID_ARGUMENT;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return RLD_ERR_NCCL;
+  memcpy(out, &id, sizeof id);
+  return RLD_OK;
+}
+
+int rld_create(const rld_device_set* ds, rld_handle** out) {
+  if (!out) return RLD_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  rld_handle* h = new (std::nothrow) rld_handle();
+  if (!h) return RLD_ERR_OUT_OF_MEMORY;
+  if (ds) {
+    h->device = ds->device;
+    h->rank = ds->rank;
+    h->world = ds->world_size < 1 ? 1 : ds->world_size;
+  }
+  int rc = guarded(h, [&] {
+    if (h->rank < 0 || h->rank >= h->world) fail(RLD_ERR_INVALID_ARGUMENT, "rank out of range");
+    RLD_CUDA(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+    RLD_CUBLAS(cublasCreate(&h->cublas));
+    RLD_CUBLAS(cublasSetStream(h->cublas, h->st));
+    RLD_CUSOLVER(cusolverDnCreate(&h->solver));
+    RLD_CUSOLVER(cusolverDnSetStream(h->solver, h->st));
+    for (auto& e : h->ev) RLD_CUDA(cudaEventCreate(&e));
+    if (h->world > 1) {
+      if (!ds || !ds->nccl_id) fail(RLD_ERR_INVALID_ARGUMENT, "nccl_id required for world_size > 1");
+      ncclUniqueId id;
+      memcpy(&id, ds->nccl_id, sizeof id);
+      ncclResult_t r = ncclCommInitRank(&h->comm, h->world, id, h->rank);
+      if (r != ncclSuccess) fail(RLD_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+  });
+  if (rc != RLD_OK) {
+    rld_destroy(h);
+    return rc;
+  }
+  *out = h;
+  return RLD_OK;
+}
+
+void rld_destroy(rld_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->st) cudaStreamSynchronize(h->st);
+  h->res.Kbuf.release();
+  if (h->comm) ncclCommDestroy(h->comm);
+  for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  if (h->solver) cusolverDnDestroy(h->solver);
+  if (h->cublas) cublasDestroy(h->cublas);
+  if (h->st) cudaStreamDestroy(h->st);
+  delete h;
+}
+
+const char* rld_last_error(const rld_handle* h) { return h ? h->last_error.c_str() : "null handle"; }
+
+void* rld_stream(rld_handle* h) { return h ? (void*)h->st : nullptr; }
+
+int rld_prepare(rld_handle* h, const rld_problem* problem) {
+  if (!h) return RLD_ERR_INVALID_ARGUMENT;
+  return guarded(h, [&] { prepare(h, problem); });
+}
+
+int rld_logdet_resident(rld_handle* h, const rld_config* cfg, const rld_inputs* inputs, rld_result* result) {
+  if (!h) return RLD_ERR_INVALID_ARGUMENT;
+  return guarded(h, [&] { run_estimate(h, cfg, inputs, result); });
+}
+
+int rld_logdet(rld_handle* h, const rld_problem* problem, const rld_config* cfg, const rld_inputs* inputs,
+               rld_result* result) {
+  if (!h) return RLD_ERR_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    prepare(h, problem);
+    run_estimate(h, cfg, inputs, result);
+  });
+}
+
+int rld_build_covariance(rld_handle* h, const rld_problem* p, void* out, int32_t out_memory) {
+  if (!h) return RLD_ERR_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    if (!p || p->source != RLD_SOURCE_POINTS) fail(RLD_ERR_INVALID_ARGUMENT, "build_covariance needs points");
+    if (!out) fail(RLD_ERR_INVALID_ARGUMENT, "out is NULL");
+    if (h->world != 1) fail(RLD_ERR_NOT_SUPPORTED, "build_covariance is single-GPU");
+    rld_problem q = *p;
+    q.path = RLD_PATH_ON_THE_FLY;  // upload points only
+    prepare(h, &q);
+    Resident& r = h->res;
+    const size_t es = p->dtype == RLD_FP64 ? 8 : 4;
+    if (out_memory == RLD_DEVICE) {
+      if (p->dtype == RLD_FP64)
+        build_kernel_rows<double>(r.X.as<double>(), r.n, r.kp, 0, r.n, static_cast<double*>(out), r.n, h->st);
+      else
+        build_kernel_rows<float>(r.X.as<double>(), r.n, r.kp, 0, r.n, static_cast<float*>(out), r.n, h->st);
+    } else {
+      const int64_t chunk = std::max<int64_t>(1, (int64_t)((512ull << 20) / (es * r.n)));
+      DevBuf& stage = h->wk.scratch2;
+      stage.reserve(es * chunk * r.n);
+      for (int64_t r0 = 0; r0 < r.n; r0 += chunk) {
+        const int64_t nr = std::min(chunk, r.n - r0);
+        if (p->dtype == RLD_FP64)
+          build_kernel_rows<double>(r.X.as<double>(), r.n, r.kp, r0, nr, stage.as<double>(), r.n, h->st);
+        else
+          build_kernel_rows<float>(r.X.as<double>(), r.n, r.kp, r0, nr, stage.as<float>(), r.n, h->st);
+        RLD_CUDA(cudaMemcpyAsync(static_cast<char*>(out) + es * r0 * r.n, stage.ptr, es * nr * r.n,
+                                 cudaMemcpyDeviceToHost, h->st));
+      }
+    }
+    RLD_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int rld_kv_apply(rld_handle* h, int64_t m, const double* V, double* Y) {
+  if (!h) return RLD_ERR_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    if (!h->res.ready) fail(RLD_ERR_INVALID_ARGUMENT, "no resident problem");
+    if (m < 1 || !V || !Y) fail(RLD_ERR_INVALID_ARGUMENT, "bad kv_apply arguments");
+    if (h->world != 1) fail(RLD_ERR_NOT_SUPPORTED, "kv_apply is single-GPU");
+    kv(h, m, V, Y);
+    RLD_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int rld_rademacher(rld_handle* h, const uint64_t key[2], int64_t rows, int64_t n, double* out) {
+  if (!h) return RLD_ERR_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    if (!key || !out || rows < 0 || n < 0) fail(RLD_ERR_INVALID_ARGUMENT, "bad rademacher arguments");
+    rademacher_rows(key, rows, n, 0, n, n, out, h->st);
+    RLD_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int rld_exact_logdet(rld_handle* h, double* value) {
+  if (!h) return RLD_ERR_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    Resident& r = h->res;
+    if (!r.ready) fail(RLD_ERR_INVALID_ARGUMENT, "no resident problem");
+    if (!value) fail(RLD_ERR_INVALID_ARGUMENT, "value is NULL");
+    if (h->world != 1) fail(RLD_ERR_NOT_SUPPORTED, "exact_logdet is single-GPU");
+    const int64_t n = r.n;
+    DevBuf L;
+    L.reserve(sizeof(double) * n * n);
+    if (r.path == RLD_PATH_ON_THE_FLY) {
+      build_kernel_rows<double>(r.X.as<double>(), n, r.kp, 0, n, L.as<double>(), n, h->st);
+    } else {
+      convert_rows_2d(r.K, r.dtype, r.ldk, L.as<double>(), n, n, h->st);
+    }
+    cusolverDnParams_t params;
+    RLD_CUSOLVER(cusolverDnCreateParams(&params));
+    size_t dws = 0, hws = 0;
+    RLD_CUSOLVER(cusolverDnXpotrf_bufferSize(h->solver, params, CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, L.ptr, n,
+                                             CUDA_R_64F, &dws, &hws));
+    DevBuf dwork;
+    dwork.reserve(std::max<size_t>(dws, 8));
+    std::vector<char> hwork(std::max<size_t>(hws, 8));
+    h->wk.ints.reserve(sizeof(int) * 8);
+    int* info = h->wk.ints.as<int>();
+    RLD_CUSOLVER(cusolverDnXpotrf(h->solver, params, CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, L.ptr, n, CUDA_R_64F,
+                                  dwork.ptr, dws, hwork.data(), hws, info + 1));
+    cusolverDnDestroyParams(params);
+    RLD_CUDA(cudaMemsetAsync(info, 0, sizeof(int), h->st));
+    // 2 sum log diag L with the diagonal stride n + 1
+    h->wk.scal.reserve(sizeof(double) * 8);
+    strided_sum_log(n, L.as<double>(), n + 1, h->wk.scal.as<double>(), h->wk.scratch, h->st);
+    double sv = 0;
+    int hinfo = 0;
+    RLD_CUDA(cudaMemcpyAsync(&sv, h->wk.scal.ptr, sizeof sv, cudaMemcpyDeviceToHost, h->st));
+    RLD_CUDA(cudaMemcpyAsync(&hinfo, info + 1, sizeof hinfo, cudaMemcpyDeviceToHost, h->st));
+    RLD_CUDA(cudaStreamSynchronize(h->st));
+    if (hinfo != 0) fail(RLD_ERR_NOT_POSITIVE_DEFINITE, "Matrix is not positive definite");
+    *value = 2.0 * sv;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,101 @@
+// Internal declarations shared by the rld CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "rld.h"
+
+namespace rld {
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+void cublas_check(cublasStatus_t s, const char* what, const char* file, int line);
+void cusolver_check(cusolverStatus_t s, const char* what, const char* file, int line);
+
+#define RLD_CUDA(x) ::rld::cuda_check((x), #x, __FILE__, __LINE__)
+#define RLD_CUBLAS(x) ::rld::cublas_check((x), #x, __FILE__, __LINE__)
+#define RLD_CUSOLVER(x) ::rld::cusolver_check((x), #x, __FILE__, __LINE__)
+extern thread_local int g_launches;
+#define RLD_LAUNCH_CHECK()                                                    \
+  do {                                                                        \
+    ++::rld::g_launches;                                                      \
+    ::rld::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__); \
+  } while (0)
+
+// Grow-only device buffer.
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  void reserve(size_t nbytes);
+  void release();
+  template <typename T> T* as() const { return static_cast<T*>(ptr); }
+  ~DevBuf() { release(); }
+};
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ inline int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+// ---------------------------------------------------------------------------
+// Kernel-matrix description as the device sees it.
+struct KernelParams {
+  int family;        // rld_family
+  int d;
+  double a2;         // amplitude^2
+  double inv_2l2;    // 1 / (2 ell^2)          (RBF)
+  double s5_over_l;  // sqrt(5) / ell          (Matern-5/2)
+  double diag;       // amplitude^2 + jitter   (src/kernels.py:72)
+};
+
+// K rows [row0, row0 + rows) x all n columns, written as T with row stride ld.
+template <typename T>
+void build_kernel_rows(const double* X, int64_t n, const KernelParams& kp, int64_t row0, int64_t rows,
+                       T* K, int64_t ld, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// Block products with K.  Y[c, i] = sum_j K[row0 + i, j] * V[c, j] for the m rows
+// of V (each of length n) and the local K rows i in [0, rows).  Y is float64,
+// rows layout with row stride ldy.
+struct KvOperand {
+  // Exactly one source of K.
+  const void* K = nullptr;   // dense rows (rows x n, row stride ldk), dtype below
+  int64_t ldk = 0;
+  const double* X = nullptr; // points (n x d) for on-the-fly generation
+  KernelParams kp{};
+  int dtype = RLD_FP64;      // product arithmetic
+  int64_t n = 0;             // columns of K (global order)
+  int64_t row0 = 0;          // first global row held locally
+  int64_t rows = 0;          // local rows
+};
+
+struct KvWorkspace {
+  DevBuf vcast;    // V converted to the product dtype
+  DevBuf partial;  // split-K partial sums
+};
+
+// V: m x n rows (float64, device).  Y: m x rows (float64, device, row stride ldy).
+void kv_product(const KvOperand& op, int64_t m, const double* V, int64_t ldv, double* Y, int64_t ldy,
+                KvWorkspace& ws, cudaStream_t st, int* launches);
+
+// ---------------------------------------------------------------------------
+// RNG
+void rademacher_rows(const uint64_t key[2], int64_t rows, int64_t n, int64_t row0_col, int64_t ncols,
+                     int64_t ld, double* out, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// Small vector kernels (rows layout).
+void rows_dot(int64_t m, int64_t n, const double* a, int64_t lda, const double* b, int64_t ldb,
+              double* out, DevBuf& scratch, cudaStream_t st, int* launches);
+
+}  // namespace rld

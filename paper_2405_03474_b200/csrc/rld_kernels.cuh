@@ -1,0 +1,55 @@
+// Host wrappers of the small kernels in vec_kernels.cu.
+#pragma once
+
+#include "rld_internal.cuh"
+
+namespace rld {
+
+enum : int {
+  RLD_FLAG_RANK_DEFICIENT = 1,
+  RLD_FLAG_NOT_PD = 2,
+  RLD_FLAG_SINGULAR = 4,
+  RLD_FLAG_BAD_BASE = 8,
+};
+
+void normalize_rows(int64_t m, int64_t n, const double* z, const double* nrm2, double* norms, double* q,
+                    cudaStream_t st);
+void lanczos_residual(int64_t m, int64_t n, int j, int t, const double* KX, const double* alpha,
+                      const double* beta, const double* p, const double* p_prev, const double* sqrt_base, double* u,
+                      double* w, cudaStream_t st);
+void lanczos_alpha(int64_t m, int j, int t, const double* dots, const int* live, double* alpha, cudaStream_t st);
+void lanczos_beta(int64_t m, int j, int t, double rtol, const double* beta2, double* alpha, double* beta,
+                  double* beta_ref, int* live, int* size, cudaStream_t st);
+void lanczos_advance(int64_t m, int64_t n, int j, int t, const double* beta, const int* live, const double* u,
+                     const double* z, double* p, double* p_prev, double* x, cudaStream_t st);
+void thomas_hutchinson(int64_t m, int t, const double* alpha, const double* beta, const int* size,
+                       const double* norms, int npoles, double offset, const double* poles,
+                       const double* residues, double* per_probe, double* trace, int* flags, cudaStream_t st);
+
+void scale_rows_colmajor(int64_t rows, int64_t cols, int64_t ld, const double* f, bool divide, double* a,
+                         cudaStream_t st);
+void scale_cols_colmajor(int64_t rows, int64_t cols, int64_t ld, const double* f, double* a, cudaStream_t st);
+void copy_doubles(int64_t count, const double* s, double* d, cudaStream_t st);
+void fill_doubles(int64_t count, double v, double* d, cudaStream_t st);
+
+void cholqr_check(int w, const double* R, const double* gdiag, const int* info, double rtol, int* flags,
+                  cudaStream_t st);
+void diag_copy(int w, const double* G, double* d, cudaStream_t st);
+void top_eigvecs(int w, int k, const double* V, const double* theta, double* Vtop, double* theta_top,
+                 cudaStream_t st);
+void precond_base(int64_t n, int k, const double* diag, double floor_v, double* A, double* base, double* sqrt_base,
+                  cudaStream_t st);
+void sum_log(int64_t n, const double* v, double* out, DevBuf& scratch, cudaStream_t st);
+void add_identity(int k, double* C, cudaStream_t st);
+void chol_logdet(int k, const double* L, const int* info, double* out, int* flags, cudaStream_t st);
+void sqrt_factors(int k, double keep_rtol, const double* lam, double* W, double* h, double* g, double* gam,
+                  int* kept, cudaStream_t st);
+void convert_rows(const void* src, int sdt, void* dst, int ddt, int64_t count, cudaStream_t st);
+void convert_rows_2d(const void* src, int sdt, int64_t lds, double* dst, int64_t rows, int64_t cols,
+                     cudaStream_t st);
+void sqrt_into(int64_t n, const double* base, double* sqrt_base, int* flags, cudaStream_t st);
+void strided_sum_log(int64_t count, const double* v, int64_t stride, double* out, DevBuf& scratch,
+                     cudaStream_t st);
+void diag_of_dense(int64_t rows, int64_t row0, const void* K, int64_t ldk, int dtype, double* d, cudaStream_t st);
+
+}  // namespace rld

@@ -1,0 +1,561 @@
+// Vector / small-matrix kernels of the estimator: per-probe dot products,
+// the preconditioned Lanczos recurrence, the multishift Thomas solves with the
+// Hutchinson mean, Philox probe generation, and the small preconditioner
+// epilogues.  All reductions have a fixed order (deterministic, no atomics).
+#include "rld_internal.cuh"
+#include "rld_device.cuh"
+#include "rld_kernels.cuh"
+
+namespace rld {
+
+namespace {
+
+constexpr int RB = 256;  // threads per reduction block
+
+// partial[c * P + p] = sum over chunk p of a[c, j] * b[c, j]
+__global__ void __launch_bounds__(RB)
+rows_dot_partial(int64_t n, const double* __restrict__ a, int64_t lda, const double* __restrict__ b,
+                 int64_t ldb, int64_t chunk, double* __restrict__ partial) {
+  __shared__ double red[RB / 32];
+  const int64_t c = blockIdx.y;
+  const int P = gridDim.x;
+  const int64_t j0 = (int64_t)blockIdx.x * chunk, j1 = min64(n, j0 + chunk);
+  const double* ar = a + c * lda;
+  const double* br = b + c * ldb;
+  double s = 0.0;
+  for (int64_t j = j0 + threadIdx.x; j < j1; j += RB) s = fma(ar[j], br[j], s);
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) partial[c * P + blockIdx.x] = s;
+}
+
+__global__ void rows_dot_final(int64_t m, int P, const double* __restrict__ partial, double* __restrict__ out) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= m) return;
+  double s = 0.0;
+  for (int p = 0; p < P; ++p) s += partial[c * P + p];
+  out[c] = s;
+}
+
+}  // namespace
+
+void rows_dot(int64_t m, int64_t n, const double* a, int64_t lda, const double* b, int64_t ldb,
+              double* out, DevBuf& scratch, cudaStream_t st, int* launches) {
+  if (m <= 0) return;
+  int P = (int)std::min<int64_t>(std::max<int64_t>(1, ceil_div(n, 4 * RB)), std::max<int64_t>(1, 1184 / m));
+  const int64_t chunk = ceil_div(n, P);
+  P = (int)ceil_div(n, chunk);
+  scratch.reserve(sizeof(double) * m * P);
+  rows_dot_partial<<<dim3(P, (unsigned)m), RB, 0, st>>>(n, a, lda, b, ldb, chunk, scratch.as<double>());
+  RLD_LAUNCH_CHECK();
+  rows_dot_final<<<(unsigned)ceil_div(m, 128), 128, 0, st>>>(m, P, scratch.as<double>(), out);
+  RLD_LAUNCH_CHECK();
+  if (launches) *launches += 2;
+}
+
+// ---------------------------------------------------------------------------
+// Philox Rademacher rows: out[r, j] = +-1 from bit 31 of 32-bit word (r*n + j)
+// of the stream (low half of each 64-bit word first) -- numpy's
+// integers(0, 2) through buffered_bounded_lemire_uint32 (threshold 0, so no
+// rejection), then 2x - 1 (src/linalg.py:84-85).
+
+namespace {
+__global__ void rademacher_kernel(uint64_t k0, uint64_t k1, int64_t rows, int64_t n, int64_t col0,
+                                  int64_t ncols, int64_t ld, double* __restrict__ out) {
+  const int64_t total = rows * ncols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / ncols, j = col0 + e % ncols;
+    const uint64_t f = (uint64_t)(r * n + j);
+    const uint64_t word = philox_word(f >> 1, k0, k1);
+    const uint32_t u = (f & 1) ? (uint32_t)(word >> 32) : (uint32_t)word;
+    out[r * ld + (j - col0)] = (u >> 31) ? 1.0 : -1.0;
+  }
+}
+}  // namespace
+
+void rademacher_rows(const uint64_t key[2], int64_t rows, int64_t n, int64_t col0, int64_t ncols, int64_t ld,
+                     double* out, cudaStream_t st) {
+  const int64_t total = rows * ncols;
+  if (total <= 0) return;
+  int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
+  rademacher_kernel<<<blocks, 256, 0, st>>>(key[0], key[1], rows, n, col0, ncols, ld, out);
+  RLD_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// Lanczos pieces.  Notation (rows layout, probe c, local index i):
+//   q_j     Lanczos vector of the symmetric operator A = N^-1 K N^-T (src/estimators.py:71-72)
+//   x_j = N^-T q_j,  p_j = N q_j          (so P^-1 p_j = x_j with P = N N^T)
+//   alpha_j = x_j . K x_j,  u = K x_j - alpha_j p_j - beta_{j-1} p_{j-1} = N r_j
+//   z = P^-1 u = N^-T r_j,  beta_j = sqrt(u . z) = |r_j|
+// which is the reference's recurrence (src/lanczos.py:56-72) without storing Q.
+
+namespace {
+
+__global__ void normalize_rows_kernel(int64_t m, int64_t n, const double* __restrict__ z,
+                                      const double* __restrict__ nrm2, double* __restrict__ norms,
+                                      double* __restrict__ q) {
+  const int64_t total = m * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / n;
+    const double nv = sqrt(nrm2[c]);
+    if (e % n == 0) norms[c] = nv;
+    q[e] = z[e] / nv;
+  }
+}
+
+// u = KX - alpha p - beta_prev p_prev ; w = u / sqrt_base
+__global__ void lanczos_residual_kernel(int64_t m, int64_t n, int j, int t, const double* __restrict__ KX,
+                                        const double* __restrict__ alpha, const double* __restrict__ beta,
+                                        const double* __restrict__ p, const double* __restrict__ p_prev,
+                                        const double* __restrict__ sqrt_base, double* __restrict__ u,
+                                        double* __restrict__ w) {
+  const int64_t total = m * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / n, i = e % n;
+    const double a = alpha[c * t + j];
+    const double bp = (j > 0) ? beta[c * t + (j - 1)] : 0.0;
+    double v = KX[e] - a * p[e];
+    if (j > 0) v -= bp * p_prev[e];
+    u[e] = v;
+    w[e] = v / sqrt_base[i];
+  }
+}
+
+// beta_j, breakdown test (src/lanczos.py:66-70), per probe
+__global__ void lanczos_beta_kernel(int64_t m, int j, int t, double rtol, const double* __restrict__ beta2,
+                                    double* __restrict__ alpha, double* __restrict__ beta,
+                                    double* __restrict__ beta_ref, int* __restrict__ live,
+                                    int* __restrict__ size) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= m) return;
+  const double b = sqrt(fmax(beta2[c], 0.0));
+  if (j == 0) beta_ref[c] = b;
+  if (!live[c]) {
+    beta[c * t + j] = 0.0;
+    return;
+  }
+  if (b <= rtol * fmax(beta_ref[c], fabs(alpha[c * t + j]))) {
+    live[c] = 0;
+    size[c] = j + 1;
+    beta[c * t + j] = 0.0;
+    return;
+  }
+  beta[c * t + j] = b;
+}
+
+// p_prev <- p ; p <- u / beta ; x <- z / beta  (zero for probes past breakdown)
+__global__ void lanczos_advance_kernel(int64_t m, int64_t n, int j, int t, const double* __restrict__ beta,
+                                       const int* __restrict__ live, const double* __restrict__ u,
+                                       const double* __restrict__ z, double* __restrict__ p,
+                                       double* __restrict__ p_prev, double* __restrict__ x) {
+  const int64_t total = m * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / n;
+    const double b = beta[c * t + j];
+    const bool on = live[c] != 0;
+    p_prev[e] = p[e];
+    p[e] = on ? u[e] / b : 0.0;
+    x[e] = on ? z[e] / b : 0.0;
+  }
+}
+
+// For probes already past breakdown, alpha of later steps must not be recorded.
+__global__ void lanczos_alpha_mask_kernel(int64_t m, int j, int t, const double* __restrict__ dots,
+                                          const int* __restrict__ live, double* __restrict__ alpha) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= m) return;
+  alpha[c * t + j] = live[c] ? dots[c] : 0.0;
+}
+
+// Multishift Thomas solves (src/linalg.py:125-156 via src/lanczos.py:77-84) and
+// the per-probe accumulation b |v|^2 + sum_j c_j v.(Q^T w_j) = |v|^2 b + |v| sum_j c_j w_j[0]
+// (src/estimators.py:89-92), then the fixed-order mean (src/estimators.py:93).
+__global__ void thomas_hutchinson_kernel(int64_t m, int t, const double* __restrict__ alpha,
+                                         const double* __restrict__ beta, const int* __restrict__ size,
+                                         const double* __restrict__ norms, int npoles, double offset,
+                                         const double* __restrict__ poles, const double* __restrict__ residues,
+                                         double* __restrict__ per_probe, double* __restrict__ trace,
+                                         int* __restrict__ flags) {
+  extern __shared__ double cbuf[];  // t doubles per thread
+  const int64_t c = threadIdx.x;
+  for (int64_t cc = c; cc < m; cc += blockDim.x) {
+    const int ms = size[cc];
+    const double nv = norms[cc];
+    double* cp = cbuf + threadIdx.x * t;
+    double acc = offset * nv * nv;
+    for (int q = 0; q < npoles; ++q) {
+      const double shift = -poles[q];
+      // forward sweep
+      double piv = alpha[cc * t] + shift;
+      if (fabs(piv) < 1e-300) { atomicOr(flags, RLD_FLAG_SINGULAR); piv = 1e-300; }
+      // cp[i] = e_i / pivot_i in the lower half of the scratch, dp[i] in the upper half
+      double* dpv = cbuf + blockDim.x * t + threadIdx.x * t;
+      dpv[0] = nv / piv;
+      if (ms > 1) cp[0] = beta[cc * t] / piv;
+      for (int i = 1; i < ms; ++i) {
+        const double e = beta[cc * t + (i - 1)];
+        piv = (alpha[cc * t + i] + shift) - e * cp[i - 1];
+        if (fabs(piv) < 1e-300) { atomicOr(flags, RLD_FLAG_SINGULAR); piv = 1e-300; }
+        dpv[i] = (0.0 - e * dpv[i - 1]) / piv;
+        if (i < ms - 1) cp[i] = beta[cc * t + i] / piv;
+      }
+      double xv = dpv[ms - 1];
+      for (int i = ms - 2; i >= 0; --i) xv = dpv[i] - cp[i] * xv;
+      acc += residues[q] * nv * xv;
+    }
+    per_probe[cc] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int64_t cc = 0; cc < m; ++cc) s += per_probe[cc];
+    *trace = s / (double)m;
+  }
+}
+
+}  // namespace
+
+static int grid_for(int64_t total) { return (int)std::min<int64_t>(std::max<int64_t>(1, ceil_div(total, 256)), 148 * 16); }
+
+void normalize_rows(int64_t m, int64_t n, const double* z, const double* nrm2, double* norms, double* q,
+                    cudaStream_t st) {
+  normalize_rows_kernel<<<grid_for(m * n), 256, 0, st>>>(m, n, z, nrm2, norms, q);
+  RLD_LAUNCH_CHECK();
+}
+
+void lanczos_residual(int64_t m, int64_t n, int j, int t, const double* KX, const double* alpha,
+                      const double* beta, const double* p, const double* p_prev, const double* sqrt_base, double* u,
+                      double* w, cudaStream_t st) {
+  lanczos_residual_kernel<<<grid_for(m * n), 256, 0, st>>>(m, n, j, t, KX, alpha, beta, p, p_prev, sqrt_base, u,
+                                                            w);
+  RLD_LAUNCH_CHECK();
+}
+
+void lanczos_alpha(int64_t m, int j, int t, const double* dots, const int* live, double* alpha, cudaStream_t st) {
+  lanczos_alpha_mask_kernel<<<(unsigned)ceil_div(m, 128), 128, 0, st>>>(m, j, t, dots, live, alpha);
+  RLD_LAUNCH_CHECK();
+}
+
+void lanczos_beta(int64_t m, int j, int t, double rtol, const double* beta2, double* alpha, double* beta,
+                  double* beta_ref, int* live, int* size, cudaStream_t st) {
+  lanczos_beta_kernel<<<(unsigned)ceil_div(m, 128), 128, 0, st>>>(m, j, t, rtol, beta2, alpha, beta, beta_ref,
+                                                                  live, size);
+  RLD_LAUNCH_CHECK();
+}
+
+void lanczos_advance(int64_t m, int64_t n, int j, int t, const double* beta, const int* live, const double* u,
+                     const double* z, double* p, double* p_prev, double* x, cudaStream_t st) {
+  lanczos_advance_kernel<<<grid_for(m * n), 256, 0, st>>>(m, n, j, t, beta, live, u, z, p, p_prev, x);
+  RLD_LAUNCH_CHECK();
+}
+
+void thomas_hutchinson(int64_t m, int t, const double* alpha, const double* beta, const int* size,
+                       const double* norms, int npoles, double offset, const double* poles,
+                       const double* residues, double* per_probe, double* trace, int* flags, cudaStream_t st) {
+  int threads = (int)std::min<int64_t>(128, std::max<int64_t>(1, m));
+  threads = std::max(1, std::min(threads, (int)((48 * 1024) / (16 * std::max(t, 1)))));
+  size_t smem = sizeof(double) * 2 * threads * t;
+  thomas_hutchinson_kernel<<<1, threads, smem, st>>>(m, t, alpha, beta, size, norms, npoles, offset, poles,
+                                                     residues, per_probe, trace, flags);
+  RLD_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// elementwise helpers
+
+namespace {
+__global__ void scale_rows_kernel(int64_t rows, int64_t cols, int64_t ld, const double* __restrict__ f,
+                                  int mode, double* __restrict__ a) {
+  // a is col-major rows x cols (ld); multiply row r by f[r] (mode 0) or divide (mode 1)
+  const int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e % rows, c = e / rows;
+    double& v = a[c * ld + r];
+    v = mode == 0 ? v * f[r] : v / f[r];
+  }
+}
+__global__ void scale_cols_kernel(int64_t rows, int64_t cols, int64_t ld, const double* __restrict__ f,
+                                  double* __restrict__ a) {
+  const int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e % rows, c = e / rows;
+    a[c * ld + r] *= f[c];
+  }
+}
+__global__ void copy_kernel(int64_t count, const double* __restrict__ s, double* __restrict__ d) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x)
+    d[e] = s[e];
+}
+__global__ void fill_kernel(int64_t count, double v, double* __restrict__ d) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x)
+    d[e] = v;
+}
+}  // namespace
+
+void scale_rows_colmajor(int64_t rows, int64_t cols, int64_t ld, const double* f, bool divide, double* a,
+                         cudaStream_t st) {
+  if (rows * cols <= 0) return;
+  scale_rows_kernel<<<grid_for(rows * cols), 256, 0, st>>>(rows, cols, ld, f, divide ? 1 : 0, a);
+  RLD_LAUNCH_CHECK();
+}
+void scale_cols_colmajor(int64_t rows, int64_t cols, int64_t ld, const double* f, double* a, cudaStream_t st) {
+  if (rows * cols <= 0) return;
+  scale_cols_kernel<<<grid_for(rows * cols), 256, 0, st>>>(rows, cols, ld, f, a);
+  RLD_LAUNCH_CHECK();
+}
+void copy_doubles(int64_t count, const double* s, double* d, cudaStream_t st) {
+  if (count <= 0) return;
+  copy_kernel<<<grid_for(count), 256, 0, st>>>(count, s, d);
+  RLD_LAUNCH_CHECK();
+}
+void fill_doubles(int64_t count, double v, double* d, cudaStream_t st) {
+  if (count <= 0) return;
+  fill_kernel<<<grid_for(count), 256, 0, st>>>(count, v, d);
+  RLD_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// preconditioner epilogues (src/precond.py:69-100, 231-233, 262-264)
+
+namespace {
+
+// Cholesky check of a CholQR pass: RankDeficient when potrf failed or when the
+// projected norm R_ii of row i falls below rtol * |Y_i| (src/linalg.py:177-178).
+__global__ void cholqr_check_kernel(int w, const double* __restrict__ R, const double* __restrict__ gdiag,
+                                    const int* __restrict__ info, double rtol, int* __restrict__ flags) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0 && *info != 0) atomicOr(flags, RLD_FLAG_RANK_DEFICIENT);
+  if (i >= w) return;
+  const double rii = R[(int64_t)i * w + i];
+  const double orig = sqrt(fmax(gdiag[i], 0.0));
+  if (!(rii >= rtol * fmax(orig, 1e-300))) atomicOr(flags, RLD_FLAG_RANK_DEFICIENT);
+}
+
+__global__ void diag_copy_kernel(int w, const double* __restrict__ G, double* __restrict__ d) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < w) d[i] = G[(int64_t)i * w + i];
+}
+
+// Vtop[:, r] = V[:, w-1-r] * sqrt(max(theta[w-1-r], 0)); theta_top[r] = theta[w-1-r]
+__global__ void top_eigvecs_kernel(int w, int k, const double* __restrict__ V, const double* __restrict__ theta,
+                                   double* __restrict__ Vtop, double* __restrict__ theta_top) {
+  const int64_t total = (int64_t)w * k;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / w), i = (int)(e % w);
+    const int src = w - 1 - r;
+    const double th = theta[src];
+    Vtop[e] = V[(int64_t)src * w + i] * sqrt(fmax(th, 0.0));
+    if (i == 0) theta_top[r] = th;
+  }
+}
+
+// base = max(diag - sum_r A^2, floor), sqrt_base, At = A / sqrt_base  (A col-major n x k)
+__global__ void base_kernel(int64_t n, int k, const double* __restrict__ diag, double floor_v,
+                            double* __restrict__ A, double* __restrict__ base, double* __restrict__ sqrt_base) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int r = 0; r < k; ++r) {
+    const double a = A[(int64_t)r * n + i];
+    s = fma(a, a, s);
+  }
+  const double b = fmax(diag[i] - s, floor_v);
+  const double sb = sqrt(b);
+  base[i] = b;
+  sqrt_base[i] = sb;
+  for (int r = 0; r < k; ++r) A[(int64_t)r * n + i] /= sb;
+}
+
+__global__ void __launch_bounds__(RB) sum_log_partial(int64_t n, const double* __restrict__ v, int64_t chunk,
+                                                      double* __restrict__ partial) {
+  __shared__ double red[RB / 32];
+  const int64_t j0 = (int64_t)blockIdx.x * chunk, j1 = min64(n, j0 + chunk);
+  double s = 0.0;
+  for (int64_t j = j0 + threadIdx.x; j < j1; j += RB) s += log(v[j]);
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+__global__ void sum_final(int P, const double* __restrict__ partial, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int p = 0; p < P; ++p) s += partial[p];
+    *out = s;
+  }
+}
+
+__global__ void add_identity_kernel(int k, double* __restrict__ C) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < k) C[(int64_t)i * k + i] += 1.0;
+}
+
+// 2 sum log diag(L) of the inner Cholesky (src/precond.py:77-80); NotPD on failure
+__global__ void chol_logdet_kernel(int k, const double* __restrict__ L, const int* __restrict__ info,
+                                   double* __restrict__ out, int* __restrict__ flags) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (*info != 0) atomicOr(flags, RLD_FLAG_NOT_PD);
+  double s = 0.0;
+  for (int i = 0; i < k; ++i) s += log(L[(int64_t)i * k + i]);
+  *out = 2.0 * s;
+}
+
+// keep filter and spectral factors of (I + At^T At) (src/precond.py:96-99):
+// scale_m = 1/sqrt(lam_m) for kept m else 0; h = 1/(1+lam)-1 (P^-1), g = 1/sqrt(1+lam)-1 (N^-T),
+// gam = sqrt(1+lam)-1 (N); W columns scaled in place.
+__global__ void sqrt_factor_kernel(int k, double keep_rtol, const double* __restrict__ lam, double* __restrict__ W,
+                                   double* __restrict__ h, double* __restrict__ g, double* __restrict__ gam,
+                                   int* __restrict__ kept) {
+  const double lmax = (k > 0) ? lam[k - 1] : 0.0;
+  const double thr = keep_rtol * fmax(lmax, 1.0);
+  for (int m = blockIdx.x; m < k; m += gridDim.x) {
+    const double l = lam[m];
+    const bool keep = l > thr;
+    const double sc = keep ? 1.0 / sqrt(l) : 0.0;
+    for (int i = threadIdx.x; i < k; i += blockDim.x) W[(int64_t)m * k + i] *= sc;
+    if (threadIdx.x == 0) {
+      h[m] = keep ? 1.0 / (1.0 + l) - 1.0 : 0.0;
+      g[m] = keep ? 1.0 / sqrt(1.0 + l) - 1.0 : 0.0;
+      gam[m] = keep ? sqrt(1.0 + l) - 1.0 : 0.0;
+      if (keep) atomicAdd(kept, 1);
+    }
+  }
+}
+
+__global__ void diag_of_dense_kernel(int64_t rows, int64_t row0, const void* __restrict__ K, int64_t ldk,
+                                     int dtype, double* __restrict__ d) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  const int64_t off = i * ldk + (row0 + i);
+  d[i] = dtype == RLD_FP64 ? static_cast<const double*>(K)[off] : (double)static_cast<const float*>(K)[off];
+}
+
+__global__ void convert_kernel(const void* __restrict__ src, int sdt, void* __restrict__ dst, int ddt,
+                               int64_t count) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double v = sdt == RLD_FP64 ? static_cast<const double*>(src)[e] : (double)static_cast<const float*>(src)[e];
+    if (ddt == RLD_FP64)
+      static_cast<double*>(dst)[e] = v;
+    else
+      static_cast<float*>(dst)[e] = (float)v;
+  }
+}
+
+__global__ void convert_2d_kernel(const void* __restrict__ src, int sdt, int64_t lds, double* __restrict__ dst,
+                                  int64_t rows, int64_t cols) {
+  const int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / cols, c = e % cols;
+    dst[e] = sdt == RLD_FP64 ? static_cast<const double*>(src)[r * lds + c]
+                             : (double)static_cast<const float*>(src)[r * lds + c];
+  }
+}
+
+__global__ void sqrt_into_kernel(int64_t n, const double* __restrict__ b, double* __restrict__ sb,
+                                 int* __restrict__ flags) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double v = b[i];
+  if (!(v > 0.0)) atomicOr(flags, RLD_FLAG_BAD_BASE);
+  sb[i] = sqrt(v);
+}
+
+__global__ void __launch_bounds__(RB) strided_log_partial(int64_t count, const double* __restrict__ v,
+                                                          int64_t stride, int64_t chunk,
+                                                          double* __restrict__ partial) {
+  __shared__ double red[RB / 32];
+  const int64_t j0 = (int64_t)blockIdx.x * chunk, j1 = min64(count, j0 + chunk);
+  double s = 0.0;
+  for (int64_t j = j0 + threadIdx.x; j < j1; j += RB) s += log(v[j * stride]);
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+}  // namespace
+
+void convert_rows(const void* src, int sdt, void* dst, int ddt, int64_t count, cudaStream_t st) {
+  if (count <= 0) return;
+  convert_kernel<<<grid_for(count), 256, 0, st>>>(src, sdt, dst, ddt, count);
+  RLD_LAUNCH_CHECK();
+}
+void convert_rows_2d(const void* src, int sdt, int64_t lds, double* dst, int64_t rows, int64_t cols,
+                     cudaStream_t st) {
+  if (rows * cols <= 0) return;
+  convert_2d_kernel<<<grid_for(rows * cols), 256, 0, st>>>(src, sdt, lds, dst, rows, cols);
+  RLD_LAUNCH_CHECK();
+}
+void sqrt_into(int64_t n, const double* base, double* sqrt_base, int* flags, cudaStream_t st) {
+  if (n <= 0) return;
+  sqrt_into_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, base, sqrt_base, flags);
+  RLD_LAUNCH_CHECK();
+}
+void strided_sum_log(int64_t count, const double* v, int64_t stride, double* out, DevBuf& scratch,
+                     cudaStream_t st) {
+  int P = (int)std::min<int64_t>(std::max<int64_t>(1, ceil_div(count, 4 * RB)), 1184);
+  const int64_t chunk = ceil_div(count, P);
+  P = (int)ceil_div(count, chunk);
+  scratch.reserve(sizeof(double) * P);
+  strided_log_partial<<<P, RB, 0, st>>>(count, v, stride, chunk, scratch.as<double>());
+  RLD_LAUNCH_CHECK();
+  sum_final<<<1, 32, 0, st>>>(P, scratch.as<double>(), out);
+  RLD_LAUNCH_CHECK();
+}
+
+void cholqr_check(int w, const double* R, const double* gdiag, const int* info, double rtol, int* flags,
+                  cudaStream_t st) {
+  cholqr_check_kernel<<<(unsigned)ceil_div(std::max(w, 1), 128), 128, 0, st>>>(w, R, gdiag, info, rtol, flags);
+  RLD_LAUNCH_CHECK();
+}
+void diag_copy(int w, const double* G, double* d, cudaStream_t st) {
+  diag_copy_kernel<<<(unsigned)ceil_div(std::max(w, 1), 128), 128, 0, st>>>(w, G, d);
+  RLD_LAUNCH_CHECK();
+}
+void top_eigvecs(int w, int k, const double* V, const double* theta, double* Vtop, double* theta_top,
+                 cudaStream_t st) {
+  top_eigvecs_kernel<<<grid_for((int64_t)w * k), 256, 0, st>>>(w, k, V, theta, Vtop, theta_top);
+  RLD_LAUNCH_CHECK();
+}
+void precond_base(int64_t n, int k, const double* diag, double floor_v, double* A, double* base, double* sqrt_base,
+                  cudaStream_t st) {
+  base_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, k, diag, floor_v, A, base, sqrt_base);
+  RLD_LAUNCH_CHECK();
+}
+void sum_log(int64_t n, const double* v, double* out, DevBuf& scratch, cudaStream_t st) {
+  int P = (int)std::min<int64_t>(std::max<int64_t>(1, ceil_div(n, 4 * RB)), 1184);
+  const int64_t chunk = ceil_div(n, P);
+  P = (int)ceil_div(n, chunk);
+  scratch.reserve(sizeof(double) * P);
+  sum_log_partial<<<P, RB, 0, st>>>(n, v, chunk, scratch.as<double>());
+  RLD_LAUNCH_CHECK();
+  sum_final<<<1, 32, 0, st>>>(P, scratch.as<double>(), out);
+  RLD_LAUNCH_CHECK();
+}
+void add_identity(int k, double* C, cudaStream_t st) {
+  add_identity_kernel<<<(unsigned)ceil_div(std::max(k, 1), 128), 128, 0, st>>>(k, C);
+  RLD_LAUNCH_CHECK();
+}
+void chol_logdet(int k, const double* L, const int* info, double* out, int* flags, cudaStream_t st) {
+  chol_logdet_kernel<<<1, 32, 0, st>>>(k, L, info, out, flags);
+  RLD_LAUNCH_CHECK();
+}
+void sqrt_factors(int k, double keep_rtol, const double* lam, double* W, double* h, double* g, double* gam,
+                  int* kept, cudaStream_t st) {
+  if (k <= 0) return;
+  sqrt_factor_kernel<<<std::min(k, 1024), 128, 0, st>>>(k, keep_rtol, lam, W, h, g, gam, kept);
+  RLD_LAUNCH_CHECK();
+}
+void diag_of_dense(int64_t rows, int64_t row0, const void* K, int64_t ldk, int dtype, double* d, cudaStream_t st) {
+  diag_of_dense_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, st>>>(rows, row0, K, ldk, dtype, d);
+  RLD_LAUNCH_CHECK();
+}
+
+}  // namespace rld
