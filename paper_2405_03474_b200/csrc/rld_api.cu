@@ -460,7 +460,7 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
   cudaStream_t st = h->st;
   Work& wk = h->wk;
   wk.ints.reserve(sizeof(int) * (8 + 2 * s));
-  wk.scal.reserve(sizeof(double) * (8 + 2 * s + 2 * s * t + 16));
+  wk.scal.reserve(sizeof(double) * (8 + 4 * s + 2 * s * t + 16));
   RLD_CUDA(cudaMemsetAsync(wk.ints.ptr, 0, sizeof(int) * 8, st));
   g_launches = 0;
   RLD_CUDA(cudaEventRecord(h->ev[0], st));
