@@ -11,6 +11,8 @@
 // The k range is split across CTAs so that small-m products still fill the
 // 148 SMs; partial sums land in a [split][m][rows] float64 buffer that a second
 // kernel reduces in fixed split order (deterministic, no atomics).
+#include <cstdlib>
+
 #include "rld_internal.cuh"
 #include "rld_device.cuh"
 
@@ -242,6 +244,10 @@ void kv_product(const KvOperand& op, int64_t m, const double* V, int64_t ldv, do
       launch_kv<double, double, 64, 32, 16, 4, 4, true>(op, m, V, ldv, Y, ldy, ws, st, launches);
     else
       launch_kv<double, double, 64, 32, 16, 4, 4, false>(op, m, V, ldv, Y, ldy, ws, st, launches);
+    return;
+  }
+  if (!otf && kv_tc_supported(op) && !getenv("RLD_NO_TC")) {
+    kv_product_tc(op, op.tc_mode, m, V, ldv, Y, ldy, ws, st);
     return;
   }
   // float32 arithmetic: cast the float64 operand rows once

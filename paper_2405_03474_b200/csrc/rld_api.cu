@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -196,13 +197,13 @@ void prepare(rld_handle* h, const rld_problem* p) {
     fill_doubles(r.rows, r.kp.diag, r.diag.as<double>(), st);
     if (r.path == RLD_PATH_STORED) {
       const size_t es = p->dtype == RLD_FP64 ? 8 : 4;
-      r.Kbuf.reserve(es * r.rows * p->n);
+      r.ldk = ceil_div(p->n, 4) * 4;  // 16-byte row pitch for TMA
+      r.Kbuf.reserve(es * r.rows * r.ldk);
       r.K = r.Kbuf.ptr;
-      r.ldk = p->n;
       if (p->dtype == RLD_FP64)
-        build_kernel_rows<double>(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.Kbuf.as<double>(), p->n, st);
+        build_kernel_rows<double>(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.Kbuf.as<double>(), r.ldk, st);
       else
-        build_kernel_rows<float>(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.Kbuf.as<float>(), p->n, st);
+        build_kernel_rows<float>(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.Kbuf.as<float>(), r.ldk, st);
     } else if (r.path != RLD_PATH_ON_THE_FLY) {
       fail(RLD_ERR_INVALID_ARGUMENT, "unknown path");
     }
@@ -219,26 +220,26 @@ void prepare(rld_handle* h, const rld_problem* p) {
       r.K = src;  // alias the caller's device rows (caller keeps them alive)
       r.ldk = ld;
     } else {
-      r.Kbuf.reserve(es * r.rows * p->n);
+      r.ldk = ceil_div(p->n, 4) * 4;
+      r.Kbuf.reserve(es * r.rows * r.ldk);
       r.K = r.Kbuf.ptr;
-      r.ldk = p->n;
       if (p->data_dtype == p->dtype) {
-        RLD_CUDA(cudaMemcpy2DAsync(r.Kbuf.ptr, es * p->n, src, ses * ld, es * p->n, r.rows,
+        RLD_CUDA(cudaMemcpy2DAsync(r.Kbuf.ptr, es * r.ldk, src, ses * ld, es * p->n, r.rows,
                                    p->data_memory == RLD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                                    st));
       } else {
         // stage in chunks of rows and convert on the device
         const int64_t chunk = std::max<int64_t>(1, (int64_t)((256ull << 20) / (ses * p->n)));
         DevBuf& stage = h->wk.scratch2;
-        stage.reserve(ses * chunk * p->n);
+        stage.reserve(ses * chunk * r.ldk);
         for (int64_t r0 = 0; r0 < r.rows; r0 += chunk) {
           const int64_t nr = std::min(chunk, r.rows - r0);
-          RLD_CUDA(cudaMemcpy2DAsync(stage.ptr, ses * p->n, src + ses * r0 * ld, ses * ld, ses * p->n, nr,
+          RLD_CUDA(cudaMemcpy2DAsync(stage.ptr, ses * r.ldk, src + ses * r0 * ld, ses * ld, ses * p->n, nr,
                                      p->data_memory == RLD_DEVICE ? cudaMemcpyDeviceToDevice
                                                                   : cudaMemcpyHostToDevice,
                                      st));
-          convert_rows(stage.ptr, p->data_dtype, static_cast<char*>(r.Kbuf.ptr) + es * r0 * p->n, p->dtype,
-                       nr * p->n, st);
+          convert_rows(stage.ptr, p->data_dtype, static_cast<char*>(r.Kbuf.ptr) + es * r0 * r.ldk, p->dtype,
+                       nr * r.ldk, st);
         }
         RLD_CUDA(cudaStreamSynchronize(st));
       }
@@ -271,21 +272,23 @@ void gather_rows(rld_handle* h, const double* local, int64_t m, double* full) {
 }
 
 // Y (m x rows) = V (m x n full) K^T restricted to the local rows
-void kv(rld_handle* h, int64_t m, const double* Vfull, double* Y) {
+// Y (m x rows) = V (m x n full) K^T restricted to the local rows.  tc_mode 1 =
+// single-pass TF32 on the tensor cores (power-iteration sketch products only),
+// 3 = 3xTF32 (everything whose value enters the estimate directly).
+void kv(rld_handle* h, int64_t m, const double* Vfull, double* Y, int tc_mode = 3) {
   KvOperand op = h->res.op();
+  op.tc_mode = tc_mode;
   kv_product(op, m, Vfull, op.n, Y, op.rows, h->wk.kv, h->st, nullptr);
 }
 
-struct CholQR {
-  int lwork = 0;
-};
-
 // In-place row orthonormalisation of the w x n block Y (col-major n x w), two
 // Cholesky-QR passes.  Replaces the row-wise CGS2 of src/linalg.py:159-180:
-// both give the unique Q with positive-diagonal triangular factor, and R_ii of
-// the first pass is exactly the projected norm the reference tests against
-// 1e-12 |Y_i| (src/linalg.py:177-178).
-void cholqr2(rld_handle* h, int64_t n, int w, double* Y, double rtol, int* flags) {
+// both give the unique Q with positive-diagonal triangular factor.  CholQR2 is
+// only accurate while cond(Y) stays below ~1e6 (it squares the condition
+// number), so pass 1 flags RLD_FLAG_QR_WEAK when any projected norm R_ii falls
+// below 1e-6 |Y_i| (or potrf fails); the caller then redoes the attempt with
+// Householder QR, which also decides the reference's RankDeficient test.
+void cholqr2(rld_handle* h, int64_t n, int w, double* Y, int* flags) {
   Work& wk = h->wk;
   wk.G.reserve(sizeof(double) * w * w);
   wk.gdiag.reserve(sizeof(double) * w);
@@ -300,10 +303,33 @@ void cholqr2(rld_handle* h, int64_t n, int w, double* Y, double rtol, int* flags
     if (pass == 0) diag_copy(w, G, wk.gdiag.as<double>(), h->st);
     RLD_CUSOLVER(cusolverDnDpotrf(h->solver, CUBLAS_FILL_MODE_UPPER, w, G, w, wk.solver_work.as<double>(), lwork,
                                   info));
-    if (pass == 0) cholqr_check(w, G, wk.gdiag.as<double>(), info, rtol, flags, h->st);
+    if (pass == 0) cholqr_check(w, G, wk.gdiag.as<double>(), info, 1e-6, flags, h->st);
     RLD_CUBLAS(cublasDtrsm(h->cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
                            (int)n, w, &ONE, G, w, Y, (int)n));
   }
+}
+
+// Householder QR of Y (col-major n x w, single shard), Q with positive R
+// diagonal -- the same Q CGS2 produces -- and the reference's rank test
+// |R_ii| < rtol |Y_i| (src/linalg.py:177-178).
+void qr_householder(rld_handle* h, int64_t n, int w, double* Y, double rtol, int* flags) {
+  if (h->world != 1) fail(RLD_ERR_RANK_DEFICIENT, "ill-conditioned sketch needs Householder QR (single GPU only)");
+  Work& wk = h->wk;
+  wk.gdiag.reserve(sizeof(double) * 2 * w);
+  wk.G.reserve(sizeof(double) * std::max<int64_t>((int64_t)w * w, 2 * w));
+  double* norms2 = wk.gdiag.as<double>();
+  double* tau = wk.G.as<double>();
+  double* sgn = norms2 + w;
+  int* info = wk.ints.as<int>() + 1;
+  rows_dot(w, n, Y, n, Y, n, norms2, wk.scratch, h->st, nullptr);
+  int l1 = 0, l2 = 0;
+  RLD_CUSOLVER(cusolverDnDgeqrf_bufferSize(h->solver, (int)n, w, Y, (int)n, &l1));
+  RLD_CUSOLVER(cusolverDnDorgqr_bufferSize(h->solver, (int)n, w, w, Y, (int)n, tau, &l2));
+  wk.solver_work.reserve(sizeof(double) * std::max(std::max(l1, l2), 1));
+  RLD_CUSOLVER(cusolverDnDgeqrf(h->solver, (int)n, w, Y, (int)n, tau, wk.solver_work.as<double>(), l1, info));
+  householder_check(w, Y, n, norms2, rtol, sgn, flags, h->st);
+  RLD_CUSOLVER(cusolverDnDorgqr(h->solver, (int)n, w, w, Y, (int)n, tau, wk.solver_work.as<double>(), l2, info));
+  scale_cols_colmajor(n, w, n, sgn, Y, h->st);
 }
 
 void syevd(rld_handle* h, int k, double* A, double* evals) {
@@ -320,7 +346,13 @@ void syevd(rld_handle* h, int k, double* A, double* evals) {
 struct PrecondOut {
   int k = 0;              // columns of U (kept ones are nonzero)
   int attempts = 1;
+  bool householder = false;
 };
+
+int sketch_tc_mode() {
+  static const int mode = getenv("RLD_SKETCH_TF32X1") ? 1 : 3;
+  return mode;
+}
 
 // ints layout: [0] flags [1] potrf info [2] syevd info [3] kept [4] inner-chol info
 // scal layout: [0] sum log base [1] 2 sum log diag(inner chol) [2] trace
@@ -360,23 +392,35 @@ PrecondOut build_preconditioner(rld_handle* h, const rld_config* c, const rld_in
   double* Y = wk.Y.as<double>();
   double* Z = wk.Z.as<double>();
 
+  auto read_flags = [&]() {
+    int hf = 0;
+    RLD_CUDA(cudaMemcpyAsync(&hf, flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+    RLD_CUDA(cudaStreamSynchronize(st));
+    return hf;
+  };
   for (int attempt = 0; attempt < 2; ++attempt) {
     out.attempts = attempt + 1;
     const double* om = attempt == 0 ? in->omega0 : in->omega1;
     if (!om)
       fail(RLD_ERR_NOT_SUPPORTED, attempt == 0 ? "sketch rows must be injected (device Gaussian stream not built yet)"
                                                : "sketch rows for attempt 1 must be injected (RankDeficient retry)");
-    RLD_CUDA(cudaMemcpyAsync(Y, om, sizeof(double) * w * n,
-                             in->memory == RLD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
-    RLD_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), st));
-    for (int it = 0; it < c->precond_iters; ++it) {
-      kv(h, w, Y, Z);                                   // Y <- Y M   (src/precond.py:186)
-      cholqr2(h, nl, w, Z, c->orth_rtol, flags);        // Q <- orth(Y) (src/precond.py:187)
-      gather_rows(h, Z, w, Y);
-    }
     int hflags = 0;
-    RLD_CUDA(cudaMemcpyAsync(&hflags, flags, sizeof(int), cudaMemcpyDeviceToHost, st));
-    RLD_CUDA(cudaStreamSynchronize(st));
+    for (int householder = 0; householder < 2; ++householder) {
+      RLD_CUDA(cudaMemcpyAsync(Y, om, sizeof(double) * w * n,
+                               in->memory == RLD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+      RLD_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), st));
+      for (int it = 0; it < c->precond_iters; ++it) {
+        kv(h, w, Y, Z, sketch_tc_mode());                 // Y <- Y M      (src/precond.py:186)
+        if (householder)
+          qr_householder(h, nl, w, Z, c->orth_rtol, flags);
+        else
+          cholqr2(h, nl, w, Z, flags);                    // Q <- orth(Y)  (src/precond.py:187)
+        gather_rows(h, Z, w, Y);
+      }
+      hflags = read_flags();
+      if (!householder && !(hflags & RLD_FLAG_QR_WEAK)) break;
+      out.householder = true;
+    }
     if (hflags & RLD_FLAG_RANK_DEFICIENT) {
       if (attempt == 1) fail(RLD_ERR_RANK_DEFICIENT, "row is numerically dependent (after retry)");
       continue;

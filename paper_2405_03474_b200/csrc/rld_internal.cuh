@@ -77,12 +77,19 @@ struct KvOperand {
   int64_t n = 0;             // columns of K (global order)
   int64_t row0 = 0;          // first global row held locally
   int64_t rows = 0;          // local rows
+  int tc_mode = 3;           // tensor-core product: 3 = 3xTF32 (Lanczos), 1 = 1xTF32 (sketch)
 };
 
 struct KvWorkspace {
-  DevBuf vcast;    // V converted to the product dtype
-  DevBuf partial;  // split-K partial sums
+  DevBuf vcast;       // V converted to the product dtype
+  DevBuf partial;     // split-K partial sums
+  DevBuf bhi, blo;    // tensor-core B operand (tf32 hi / lo rows)
+  DevBuf tc_partial;  // stream-K partial accumulators
 };
+
+bool kv_tc_supported(const KvOperand& op);
+void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, int64_t ldv, double* Y, int64_t ldy,
+                   KvWorkspace& ws, cudaStream_t st);
 
 // V: m x n rows (float64, device).  Y: m x rows (float64, device, row stride ldy).
 void kv_product(const KvOperand& op, int64_t m, const double* V, int64_t ldv, double* Y, int64_t ldy,

@@ -10,6 +10,7 @@ enum : int {
   RLD_FLAG_NOT_PD = 2,
   RLD_FLAG_SINGULAR = 4,
   RLD_FLAG_BAD_BASE = 8,
+  RLD_FLAG_QR_WEAK = 16,
 };
 
 void normalize_rows(int64_t m, int64_t n, const double* z, const double* nrm2, double* norms, double* q,
@@ -34,6 +35,8 @@ void fill_doubles(int64_t count, double v, double* d, cudaStream_t st);
 
 void cholqr_check(int w, const double* R, const double* gdiag, const int* info, double rtol, int* flags,
                   cudaStream_t st);
+void householder_check(int w, const double* R, int64_t ldr, const double* norms2, double rtol, double* sgn,
+                       int* flags, cudaStream_t st);
 void diag_copy(int w, const double* G, double* d, cudaStream_t st);
 void top_eigvecs(int w, int k, const double* V, const double* theta, double* Vtop, double* theta_top,
                  cudaStream_t st);

@@ -327,16 +327,27 @@ void fill_doubles(int64_t count, double v, double* d, cudaStream_t st) {
 
 namespace {
 
-// Cholesky check of a CholQR pass: RankDeficient when potrf failed or when the
-// projected norm R_ii of row i falls below rtol * |Y_i| (src/linalg.py:177-178).
+// Cholesky check of CholQR pass 1: flag QR_WEAK when potrf failed or a
+// projected norm R_ii fell below weak_rtol * |Y_i| (CholQR loses accuracy there).
 __global__ void cholqr_check_kernel(int w, const double* __restrict__ R, const double* __restrict__ gdiag,
-                                    const int* __restrict__ info, double rtol, int* __restrict__ flags) {
+                                    const int* __restrict__ info, double weak_rtol, int* __restrict__ flags) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i == 0 && *info != 0) atomicOr(flags, RLD_FLAG_RANK_DEFICIENT);
+  if (i == 0 && *info != 0) atomicOr(flags, RLD_FLAG_QR_WEAK);
   if (i >= w) return;
   const double rii = R[(int64_t)i * w + i];
   const double orig = sqrt(fmax(gdiag[i], 0.0));
-  if (!(rii >= rtol * fmax(orig, 1e-300))) atomicOr(flags, RLD_FLAG_RANK_DEFICIENT);
+  if (!(rii >= weak_rtol * fmax(orig, 1e-300))) atomicOr(flags, RLD_FLAG_QR_WEAK);
+}
+
+// Householder R: RankDeficient when |R_ii| < rtol |Y_i| (src/linalg.py:177-178); sign of R_ii
+__global__ void householder_check_kernel(int w, const double* __restrict__ R, int64_t ldr,
+                                         const double* __restrict__ norms2, double rtol, double* __restrict__ sgn,
+                                         int* __restrict__ flags) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= w) return;
+  const double rii = R[(int64_t)i * ldr + i];
+  if (!(fabs(rii) >= rtol * fmax(sqrt(fmax(norms2[i], 0.0)), 1e-300))) atomicOr(flags, RLD_FLAG_RANK_DEFICIENT);
+  sgn[i] = rii < 0.0 ? -1.0 : 1.0;
 }
 
 __global__ void diag_copy_kernel(int w, const double* __restrict__ G, double* __restrict__ d) {
@@ -513,6 +524,12 @@ void strided_sum_log(int64_t count, const double* v, int64_t stride, double* out
 void cholqr_check(int w, const double* R, const double* gdiag, const int* info, double rtol, int* flags,
                   cudaStream_t st) {
   cholqr_check_kernel<<<(unsigned)ceil_div(std::max(w, 1), 128), 128, 0, st>>>(w, R, gdiag, info, rtol, flags);
+  RLD_LAUNCH_CHECK();
+}
+void householder_check(int w, const double* R, int64_t ldr, const double* norms2, double rtol, double* sgn,
+                       int* flags, cudaStream_t st) {
+  householder_check_kernel<<<(unsigned)ceil_div(std::max(w, 1), 128), 128, 0, st>>>(w, R, ldr, norms2, rtol, sgn,
+                                                                                   flags);
   RLD_LAUNCH_CHECK();
 }
 void diag_copy(int w, const double* G, double* d, cudaStream_t st) {

@@ -100,6 +100,36 @@ def test_kv_apply_matches_numpy(rld, dtype, path, m):
     assert err <= (1e-13 if dtype == "fp64" else 2e-6), err
 
 
+@pytest.mark.parametrize("n,m", [(256, 32), (1000, 1), (4099, 64), (16384, 32), (3000, 300), (2048, 400),
+                                 (20000, 128), (700, 17)])
+def test_tcgen05_product_matches_float64(rld, n, m):
+    """fp32 stored K goes through the tcgen05 3xTF32 kernel (stream-K, TMEM A
+    operand); check it against float64 numpy and against the CUDA-core path."""
+    import os
+
+    import torch
+
+    g = np.random.default_rng(n + m)
+    pts = g.standard_normal((n, 4))
+    spec = rld.KernelSpec("rbf", 1.0, 1.5, 1e-3)
+    R = rld.ResidentMatrix(rld.KernelMatrix(spec, pts), dtype="fp32", path="stored")
+    V = g.standard_normal((m, n))
+    Vt = torch.from_numpy(V).cuda()
+    Y = R.kv_apply(Vt).cpu().numpy()
+    K = O.covariance_block("rbf", 1.0, 1.5, 1e-3, pts)
+    K32 = K.astype(np.float32).astype(np.float64)      # the stored matrix
+    scale = np.abs(V) @ np.abs(K)
+    err_tc = np.max(np.abs(Y - V @ K32) / scale)
+    tol = 2e-6 + 1e-7 * np.sqrt(n)     # fp32 accumulation over n terms
+    assert err_tc <= tol, err_tc
+    os.environ["RLD_NO_TC"] = "1"
+    try:
+        Ys = R.kv_apply(Vt).cpu().numpy()
+    finally:
+        del os.environ["RLD_NO_TC"]
+    assert np.max(np.abs(Ys - V @ K32) / scale) <= tol
+
+
 # ---------------------------------------------------------------- estimator parity
 
 @pytest.mark.parametrize("alg", ["r1", "r3", "r5"])
