@@ -46,17 +46,21 @@ constexpr int TC_BM = 128;          // K rows per tile (UMMA M)
 constexpr int TC_BK = 32;           // fp32 k-elements per step (one 128-byte swizzle row)
 constexpr int TC_THREADS = 256;
 constexpr int GROUP = 4;            // k-steps accumulated in TMEM before the register flush
+constexpr int NABUF = 4;            // TMEM A-operand buffers (converter runs up to 3 steps ahead)
 constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4;  // 16 KB
 
+// A launch covers `npass` column passes of NT vectors each: CTA b works on pass
+// b % npass over stream-K range b / npass, so the CTAs that need the same K rows
+// run concurrently and K streams from HBM about once (L2 serves the other passes).
 struct TcParams {
   int64_t total;    // tiles * ks
   int ks;           // k-steps per tile
   int tiles;
-  int b_row0;       // first vector of this pass
+  int npass;        // column passes in this launch
   int segs;         // partial slots per tile
   int stages;
   uint32_t tmem_cols;
-  float* partial;   // [tiles][segs][NT][128]
+  float* partial;   // [npass][tiles][segs][NT][128]
 };
 
 __host__ __device__ __forceinline__ int64_t cta_of_step(int64_t x, int64_t total, int64_t G) {
@@ -64,25 +68,46 @@ __host__ __device__ __forceinline__ int64_t cta_of_step(int64_t x, int64_t total
   return ((x + 1) * G - 1) / total;
 }
 
-struct StepInfo {
-  bool group_start, group_end, seg_end;
+// Walks a CTA's contiguous range of (tile, k-step) pairs with running counters
+// (no 64-bit divisions in the pipeline loops).
+struct StepIter {
+  int64_t g, end, j;
+  int ks, kstep, tile, gpos, s, S;
+  uint32_t ph;
+  __device__ __forceinline__ StepIter(int64_t beg, int64_t end_, int ks_, int S_)
+      : g(beg), end(end_), j(0), ks(ks_), gpos(0), s(0), S(S_), ph(0) {
+    tile = (int)(beg / ks_);
+    kstep = (int)(beg - (int64_t)tile * ks_);
+  }
+  __device__ __forceinline__ bool valid() const { return g < end; }
+  __device__ __forceinline__ bool group_start() const { return gpos == 0; }
+  __device__ __forceinline__ bool seg_end() const { return g + 1 == end || kstep + 1 == ks; }
+  __device__ __forceinline__ bool group_end() const { return seg_end() || gpos + 1 == GROUP; }
+  __device__ __forceinline__ int abuf() const { return (int)(j & (NABUF - 1)); }
+  __device__ __forceinline__ uint32_t aphase() const { return (uint32_t)((j / NABUF) & 1); }
+  __device__ __forceinline__ void next() {
+    gpos = group_end() ? 0 : gpos + 1;
+    ++g;
+    ++j;
+    if (++kstep == ks) {
+      kstep = 0;
+      ++tile;
+    }
+    if (++s == S) {
+      s = 0;
+      ph ^= 1;
+    }
+  }
 };
-
-__device__ __forceinline__ StepInfo step_info(int64_t g, int64_t beg, int64_t end, int ks) {
-  const int64_t tile_start = (g / ks) * ks;
-  const int64_t seg_start = beg > tile_start ? beg : tile_start;
-  StepInfo si;
-  si.seg_end = (g + 1 == end) || ((g + 1) % ks == 0);
-  si.group_start = ((g - seg_start) % GROUP) == 0;
-  si.group_end = si.seg_end || ((g + 1 - seg_start) % GROUP) == 0;
-  return si;
-}
 
 template <int MODE, int NT>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
              const __grid_constant__ CUtensorMap tmBlo, const TcParams p) {
-  static_assert(NT % 32 == 0 && NT <= 128, "NT");
+  static_assert(NT % 32 == 0 && (MODE == 3 ? NT <= 64 : NT <= 128), "NT");
+  // accumulator width: 3xTF32 multiplies [Bhi; Blo] (2 NT rows) in one instruction and
+  // folds the two halves in the drain; 1xTF32 multiplies Bhi (NT rows)
+  constexpr int DW = MODE == 3 ? 2 * NT : NT;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t B_BYTES = (uint32_t)NT * 128;
@@ -90,15 +115,18 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
   const int S = p.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * STAGE);
   uint64_t* empty = full + S;
-  uint64_t* afull = empty + S;       // [2]
-  uint64_t* aempty = afull + 2;      // [2]
-  uint64_t* accfull = aempty + 2;    // [2]
+  uint64_t* afull = empty + S;       // [NABUF]
+  uint64_t* aempty = afull + NABUF;  // [NABUF]
+  uint64_t* accfull = aempty + NABUF;  // [2]
   uint64_t* accempty = accfull + 2;  // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t G = gridDim.x, cta = blockIdx.x;
+  const int pass = (int)(blockIdx.x % p.npass);
+  const int64_t G = gridDim.x / p.npass, cta = blockIdx.x / p.npass;
   const int64_t beg = cta * p.total / G, end = (cta + 1) * p.total / G;
+  const int b_row0 = pass * NT;
+  float* const partial = p.partial + (size_t)pass * p.tiles * p.segs * NT * TC_BM;
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch_desc(&tmA);
@@ -108,9 +136,11 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NABUF; ++b) {
       ptx::mbar_init(&afull[b], 4);
       ptx::mbar_init(&aempty[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&accfull[b], 1);
       ptx::mbar_init(&accempty[b], 4);
     }
@@ -121,61 +151,53 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
-  // TMEM columns: accumulators [0, NT) and [NT, 2NT); A buffers [2NT + 64b, +32) hi, [+32, +64) lo
-  constexpr uint32_t A_COL0 = 2 * NT;
+  // TMEM columns: accumulators [0, DW) and [DW, 2DW); A buffer b at A_COL0 + ASTRIDE b: hi [+0, +32), lo [+32, +64)
+  constexpr uint32_t A_COL0 = 2 * DW;
+  constexpr uint32_t ASTRIDE = MODE == 3 ? 64 : 32;
 
   if (beg < end) {
     if (warp == 0) {
       if (lane == 0) {
         // ---------------- TMA producer
-        int64_t j = 0;
-        for (int64_t g = beg; g < end; ++g, ++j) {
-          const int s = (int)(j % S);
-          const uint32_t ph = (uint32_t)((j / S) & 1);
-          ptx::mbar_wait(&empty[s], ph ^ 1);
-          const int tile = (int)(g / p.ks), kstep = (int)(g % p.ks);
+        for (StepIter it(beg, end, p.ks, S); it.valid(); it.next()) {
+          const int s = it.s;
+          ptx::mbar_wait(&empty[s], it.ph ^ 1);
           uint8_t* st = smem + (size_t)s * STAGE;
           ptx::mbar_arrive_expect_tx(&full[s], STAGE);
-          ptx::tma_load_2d(st, &tmA, &full[s], kstep * TC_BK, tile * TC_BM);
-          ptx::tma_load_2d(st + A_BYTES, &tmBhi, &full[s], kstep * TC_BK, p.b_row0);
-          if (MODE == 3) ptx::tma_load_2d(st + A_BYTES + B_BYTES, &tmBlo, &full[s], kstep * TC_BK, p.b_row0);
+          ptx::tma_load_2d(st, &tmA, &full[s], it.kstep * TC_BK, it.tile * TC_BM);
+          ptx::tma_load_2d(st + A_BYTES, &tmBhi, &full[s], it.kstep * TC_BK, b_row0);
+          if (MODE == 3) ptx::tma_load_2d(st + A_BYTES + B_BYTES, &tmBlo, &full[s], it.kstep * TC_BK, b_row0);
         }
       }
     } else if (warp == 1) {
       if (lane == 0) {
         // ---------------- MMA issuer
-        constexpr uint32_t idesc = ptx::idesc_tf32(TC_BM, NT);
+        constexpr uint32_t idesc = ptx::idesc_tf32(TC_BM, DW);
         int64_t gi = -1;  // group index
-        int64_t j = 0;
-        for (int64_t g = beg; g < end; ++g, ++j) {
-          const int s = (int)(j % S);
-          const uint32_t ph = (uint32_t)((j / S) & 1);
-          const int b = (int)(j & 1);
-          const StepInfo si = step_info(g, beg, end, p.ks);
-          if (si.group_start) {
+        for (StepIter it(beg, end, p.ks, S); it.valid(); it.next()) {
+          const int s = it.s;
+          const int b = it.abuf();
+          const bool gstart = it.group_start(), gend = it.group_end();
+          if (gstart) {
             ++gi;
             if (gi >= 2) ptx::mbar_wait(&accempty[gi & 1], (uint32_t)(((gi >> 1) - 1) & 1));
           }
-          const uint32_t d = tmem + (uint32_t)(gi & 1) * NT;
-          ptx::mbar_wait(&full[s], ph);
-          ptx::mbar_wait(&afull[b], (uint32_t)((j >> 1) & 1));
+          const uint32_t d = tmem + (uint32_t)(gi & 1) * DW;
+          ptx::mbar_wait(&full[s], it.ph);
+          ptx::mbar_wait(&afull[b], it.aphase());
           ptx::tc_fence_after();
           const uint32_t sB = ptx::smem_u32(smem + (size_t)s * STAGE + A_BYTES);
 #pragma unroll
           for (int kk = 0; kk < TC_BK / 8; ++kk) {
-            const uint32_t a_hi = tmem + A_COL0 + 64 * b + 8 * kk;
-            const uint64_t bhi = ptx::smem_desc_sw128(sB + 32 * kk);
-            const uint32_t acc = (si.group_start && kk == 0) ? 0u : 1u;
-            ptx::mma_tf32_ts(d, a_hi, bhi, idesc, acc);
-            if (MODE == 3) {
-              const uint64_t blo = ptx::smem_desc_sw128(sB + B_BYTES + 32 * kk);
-              ptx::mma_tf32_ts(d, a_hi, blo, idesc, 1u);
-              ptx::mma_tf32_ts(d, a_hi + 32, bhi, idesc, 1u);
-            }
+            const uint32_t a_hi = tmem + A_COL0 + ASTRIDE * b + 8 * kk;
+            const uint64_t bd = ptx::smem_desc_sw128(sB + 32 * kk);   // [Bhi; Blo] rows (3xTF32) or Bhi
+            const uint32_t acc = (gstart && kk == 0) ? 0u : 1u;
+            ptx::mma_tf32_ts(d, a_hi, bd, idesc, acc);                 // D += Ahi [Bhi; Blo]
+            if (MODE == 3) ptx::mma_tf32_ts(d, a_hi + 32, bd, idesc, 1u);  // D += Alo [Bhi; Blo]
           }
           ptx::tc_commit(&empty[s]);
           ptx::tc_commit(&aempty[b]);
-          if (si.group_end) ptx::tc_commit(&accfull[gi & 1]);
+          if (gend) ptx::tc_commit(&accfull[gi & 1]);
         }
       }
     } else if (warp >= 4) {
@@ -198,17 +220,25 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
 #pragma unroll
         for (int c0 = 0; c0 < NT; c0 += 32) {
           uint32_t v[32];
-          ptx::tmem_ld_32x32b_x32(tmem + lane_base + (uint32_t)(buf * NT + c0), v);
-          ptx::tmem_wait_ld();
+          ptx::tmem_ld_32x32b_x32(tmem + lane_base + (uint32_t)(buf * DW + c0), v);
+          if (MODE == 3) {
+            uint32_t w[32];
+            ptx::tmem_ld_32x32b_x32(tmem + lane_base + (uint32_t)(buf * DW + NT + c0), w);
+            ptx::tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) acc[c0 + e] += __uint_as_float(v[e]);
+            for (int e = 0; e < 32; ++e) acc[c0 + e] += __uint_as_float(v[e]) + __uint_as_float(w[e]);
+          } else {
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) acc[c0 + e] += __uint_as_float(v[e]);
+          }
         }
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&accempty[buf]);
         if (seg_end) {
           const int seg = (int)(cta - cta_of_step(tile * (int64_t)p.ks, p.total, G));
-          float* P = p.partial + ((size_t)tile * p.segs + seg) * (size_t)NT * TC_BM;
+          float* P = partial + ((size_t)tile * p.segs + seg) * (size_t)NT * TC_BM;
 #pragma unroll
           for (int c = 0; c < NT; ++c) {
             P[(size_t)c * TC_BM + row] = acc[c];
@@ -218,19 +248,17 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       };
 
       int64_t gi = -1;
-      int64_t j = 0;
-      for (int64_t g = beg; g < end; ++g, ++j) {
-        const int s = (int)(j % S);
-        const uint32_t ph = (uint32_t)((j / S) & 1);
-        const int b = (int)(j & 1);
-        const StepInfo si = step_info(g, beg, end, p.ks);
-        if (si.group_start) ++gi;
-        ptx::mbar_wait(&full[s], ph);
-        const uint8_t* rowp = smem + (size_t)s * STAGE + row * 128;
+      for (StepIter it(beg, end, p.ks, S); it.valid(); it.next()) {
+        const int s = it.s;
+        const int b = it.abuf();
+        const int64_t j = it.j;
+        if (it.group_start()) ++gi;
+        ptx::mbar_wait(&full[s], it.ph);
+        const uint32_t rowp = ptx::smem_u32(smem + (size_t)s * STAGE + row * 128);
         uint32_t hi[32], lo[32];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (row & 7)) << 4));
+          const float4 v = ptx::lds128(rowp + ((c ^ (row & 7)) << 4));
           const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -244,9 +272,9 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             }
           }
         }
-        if (j >= 2) ptx::mbar_wait(&aempty[b], (uint32_t)(((j >> 1) - 1) & 1));
+        if (j >= NABUF) ptx::mbar_wait(&aempty[b], (uint32_t)(((j / NABUF) - 1) & 1));
         ptx::tc_fence_after();
-        const uint32_t ta = tmem + lane_base + A_COL0 + 64 * b;
+        const uint32_t ta = tmem + lane_base + A_COL0 + ASTRIDE * b;
         ptx::tmem_st_32x32b_x32(ta, hi);
         if (MODE == 3) ptx::tmem_st_32x32b_x32(ta + 32, lo);
         ptx::tmem_wait_st();
@@ -257,10 +285,10 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         // drain groups that finished at earlier steps (their MMAs do not wait on this step)
         for (int k = 0; k < npend; ++k) drain(pend_gi[k], pend_seg[k], pend_tile[k]);
         npend = 0;
-        if (si.group_end) {
+        if (it.group_end()) {
           pend_gi[npend] = gi;
-          pend_seg[npend] = si.seg_end;
-          pend_tile[npend] = g / p.ks;
+          pend_seg[npend] = it.seg_end();
+          pend_tile[npend] = it.tile;
           ++npend;
         }
       }
@@ -272,18 +300,20 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
   if (warp == 2) ptx::tmem_dealloc(tmem, p.tmem_cols);
 }
 
-// Y[(b_row0 + c) * ldy + i] = sum over the tile's segments of partial (float64 accumulation, fixed order)
-__global__ void kv_tc_reduce(const float* __restrict__ P, int64_t total, int64_t G, int ks, int segs, int nt,
-                             int ncols, int64_t rows, double* __restrict__ Y, int64_t ldy) {
-  const int64_t count = (int64_t)ncols * rows;
+// Y[c * ldy + i] = sum over the tile's segments of the partials (float64 accumulation, fixed order)
+__global__ void kv_tc_reduce(const float* __restrict__ P, int64_t total, int64_t G, int ks, int tiles, int segs,
+                             int nt, int64_t m, int64_t rows, double* __restrict__ Y, int64_t ldy) {
+  const int64_t count = m * rows;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = e / rows, i = e % rows;
+    const int64_t pass = c / nt, cc = c % nt;
     const int64_t tile = i / TC_BM, r = i % TC_BM;
     const int64_t x0 = tile * ks;
     const int nseg = (int)(cta_of_step(x0 + ks - 1, total, G) - cta_of_step(x0, total, G) + 1);
+    const float* Pp = P + (size_t)pass * tiles * segs * nt * TC_BM;
     double s = 0.0;
-    for (int k = 0; k < nseg; ++k) s += (double)P[(((size_t)tile * segs + k) * nt + c) * TC_BM + r];
+    for (int k = 0; k < nseg; ++k) s += (double)Pp[(((size_t)tile * segs + k) * nt + cc) * TC_BM + r];
     Y[c * ldy + i] = s;
   }
 }
@@ -360,21 +390,31 @@ void launch_tc(const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap&
   const size_t extra = 1024 + 8 * 64;
   const int smem_cap = max_smem_optin() - 1024;
   p.stages = (int)std::min<size_t>(8, (smem_cap - extra) / stage);
-  p.tmem_cols = (2 * NT + 128) <= 256 ? 256 : 512;
+  constexpr int DW = MODE == 3 ? 2 * NT : NT;
+  constexpr int cols = 2 * DW + NABUF * (MODE == 3 ? 64 : 32);
+  static_assert(cols <= 512, "TMEM budget");
+  p.tmem_cols = cols <= 256 ? 256 : 512;
   const size_t smem = p.stages * stage + extra;
   RLD_CUDA(cudaFuncSetAttribute(kv_tc_kernel<MODE, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kv_tc_kernel<MODE, NT><<<(unsigned)G, TC_THREADS, smem, st>>>(mA, mBh, mBl, p);
   RLD_LAUNCH_CHECK();
 }
 
-template <int MODE>
-void launch_tc_nt(int nt, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl, const TcParams& p,
-                  int64_t G, cudaStream_t st) {
+void launch_tc_3(int nt, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl, const TcParams& p,
+                 int64_t G, cudaStream_t st) {
+  if (nt == 32)
+    launch_tc<3, 32>(mA, mBh, mBl, p, G, st);
+  else
+    launch_tc<3, 64>(mA, mBh, mBl, p, G, st);
+}
+
+void launch_tc_1(int nt, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl, const TcParams& p,
+                 int64_t G, cudaStream_t st) {
   switch (nt) {
-    case 32: launch_tc<MODE, 32>(mA, mBh, mBl, p, G, st); break;
-    case 64: launch_tc<MODE, 64>(mA, mBh, mBl, p, G, st); break;
-    case 96: launch_tc<MODE, 96>(mA, mBh, mBl, p, G, st); break;
-    default: launch_tc<MODE, 128>(mA, mBh, mBl, p, G, st); break;
+    case 32: launch_tc<1, 32>(mA, mBh, mBl, p, G, st); break;
+    case 64: launch_tc<1, 64>(mA, mBh, mBl, p, G, st); break;
+    case 96: launch_tc<1, 96>(mA, mBh, mBl, p, G, st); break;
+    default: launch_tc<1, 128>(mA, mBh, mBl, p, G, st); break;
   }
 }
 
@@ -403,37 +443,35 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
   const int ks = (int)ceil_div(n, TC_BK);
   const int tiles = (int)ceil_div(rows, TC_BM);
   const int64_t total = (int64_t)tiles * ks;
-  const int64_t Gl = std::min<int64_t>(G, total);
+  // vectors per pass: <= 64 for 3xTF32 ([Bhi; Blo] is one N = 2 NT instruction), <= 128 for
+  // 1xTF32 (register-resident fp32 accumulators of the drain warps)
+  const int npass = (int)ceil_div(m, mode == 3 ? 64 : 128);
+  const int width = (int)(ceil_div(ceil_div(m, npass), 32) * 32);
+  const int64_t Gl = std::min<int64_t>(std::max(1, G / npass), total);
   int segs = 1;
   for (int t = 0; t < tiles; ++t) {
     const int64_t x0 = (int64_t)t * ks;
     segs = (int)std::max<int64_t>(segs, cta_of_step(x0 + ks - 1, total, Gl) - cta_of_step(x0, total, Gl) + 1);
   }
   const CUtensorMap mA = make_map(static_cast<const float*>(op.K), n, rows, op.ldk, TC_BM);
-  // vectors per pass: <= 128 (register-resident fp32 accumulators of the drain warps)
-  const int64_t npass = ceil_div(m, 128);
-  const int width = (int)(ceil_div(ceil_div(m, npass), 32) * 32);
-  for (int64_t c0 = 0; c0 < m; c0 += width) {
-    const int ncols = (int)std::min<int64_t>(width, m - c0);
-    TcParams p{};
-    p.total = total;
-    p.ks = ks;
-    p.tiles = tiles;
-    p.b_row0 = (int)c0;
-    p.segs = segs;
-    ws.tc_partial.reserve(sizeof(float) * (size_t)tiles * segs * width * TC_BM);
-    p.partial = ws.tc_partial.as<float>();
-    const CUtensorMap mBh = make_map(ws.bhi.as<float>(), n, m, ldb, width);
-    const CUtensorMap mBl = mode == 3 ? make_map(ws.blo.as<float>(), n, m, ldb, width) : mBh;
-    if (mode == 3)
-      launch_tc_nt<3>(width, mA, mBh, mBl, p, Gl, st);
-    else
-      launch_tc_nt<1>(width, mA, mBh, mBl, p, Gl, st);
-    const int64_t count = (int64_t)ncols * rows;
-    const int blocks = (int)std::min<int64_t>(ceil_div(count, 256), 148 * 16);
-    kv_tc_reduce<<<blocks, 256, 0, st>>>(p.partial, total, Gl, ks, segs, width, ncols, rows, Y + c0 * ldy, ldy);
-    RLD_LAUNCH_CHECK();
-  }
+  TcParams p{};
+  p.total = total;
+  p.ks = ks;
+  p.tiles = tiles;
+  p.npass = npass;
+  p.segs = segs;
+  ws.tc_partial.reserve(sizeof(float) * (size_t)npass * tiles * segs * width * TC_BM);
+  p.partial = ws.tc_partial.as<float>();
+  const CUtensorMap mBh = make_map(ws.bhi.as<float>(), n, m, ldb, width);
+  const CUtensorMap mBl = mode == 3 ? make_map(ws.blo.as<float>(), n, m, ldb, width) : mBh;
+  if (mode == 3)
+    launch_tc_3(width, mA, mBh, mBl, p, Gl * npass, st);
+  else
+    launch_tc_1(width, mA, mBh, mBl, p, Gl * npass, st);
+  const int64_t count = m * rows;
+  const int blocks = (int)std::min<int64_t>(ceil_div(count, 256), 148 * 16);
+  kv_tc_reduce<<<blocks, 256, 0, st>>>(p.partial, total, Gl, ks, tiles, segs, width, m, rows, Y, ldy);
+  RLD_LAUNCH_CHECK();
 }
 
 }  // namespace rld
