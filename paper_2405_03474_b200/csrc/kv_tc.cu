@@ -4,34 +4,40 @@
 // path of BASELINE configs 2-3; reference call sites src/estimators.py:72 and
 // src/precond.py:186, 189).
 //
-// Per CTA (one per SM, persistent, 8 warps):
-//   warp 0      TMA producer: K tile (128 rows x 32 fp32, 128B-swizzled) and the
-//               B tiles (NT vectors x 32 fp32: hi, and lo for 3xTF32) per k-step,
-//               into an S-stage shared-memory ring guarded by full/empty mbarriers.
-//   warps 4-7   converters: each thread owns one K row; it reads its 32 values
-//               from the swizzled tile, splits them into tf32 hi + lo (lo exact
-//               in fp32), and tcgen05.st's them into a double-buffered TMEM
-//               A-operand region (the tensor core never re-reads A from shared
-//               memory).  The same warps drain the accumulators (below).
-//   warp 1      MMA issuer (one thread): per 8-wide k chunk, D += Ahi*Bhi +
-//               Ahi*Blo + Alo*Bhi (3xTF32, ~fp32 accuracy) or D += A*B (1xTF32),
-//               A from TMEM, B from SMEM descriptors; tcgen05.commit releases
-//               the SMEM stage and the TMEM A buffer.
-//   warp 2      TMEM allocation owner.
+// One persistent CTA per SM, 16 warps:
+//   warp 0       TMA producer: K tile (128 rows x 32 fp32, 128B-swizzled) plus the
+//                B tiles (NT vectors x 32 fp32: tf32-hi, and lo for 3xTF32) per
+//                k-step into an S-stage shared-memory ring (full/empty mbarriers).
+//   warps 4-7    converters: thread = one K row; it reads its 32 values from the
+//                swizzled tile, splits them into tf32 hi + lo (lo exact in fp32)
+//                and tcgen05.st's them into one of NABUF TMEM A-operand buffers,
+//                so the tensor core never re-reads A from shared memory.
+//   warp 1       MMA issuer (whole warp walks the pipeline so every descriptor is
+//                warp-uniform; one elected lane issues).  3xTF32 per 8-wide k chunk:
+//                  NT == 32: D[2NT] += Ahi [Bhi; Blo] + Alo [Bhi; Blo] (two N = 64
+//                            instructions -- small N costs the same ~45 cycles as
+//                            N = 64, so stacking hi/lo B halves the issue count);
+//                  NT >= 64: D[NT] += Ahi Bhi + Ahi Blo + Alo Bhi.
+//                1xTF32 (optional sketch mode): D[NT] += A Bhi.
+//   warps 8-15   accumulator drain (two warps per TMEM lane quarter, one half of
+//                the columns each).
+//   warp 2       TMEM allocation owner.
 //
 // Accuracy: the tensor core rounds its fp32 accumulator toward zero, so a long
 // accumulation drifts (measured -2e-4 relative at n = 16384, -9e-4 at 65536).
-// The MMA therefore accumulates only GROUP k-steps into one of two TMEM
-// accumulators; the converter warps add each finished group into fp32
-// registers with round-to-nearest, one group behind (double buffering keeps
-// the tensor core busy meanwhile).
+// The MMAs therefore accumulate only GROUP k-steps into one of two TMEM
+// accumulators; the drain warps add each finished group into fp32 registers
+// with round-to-nearest while the tensor core fills the other accumulator.
 //
-// Work split: "stream-K" -- the tiles x k-steps space is cut into gridDim.x
-// contiguous ranges of equal length, so every SM streams the same number of K
-// bytes; a tile shared by several CTAs leaves per-CTA partial sums that
-// kv_tc_reduce adds in fixed CTA order, in float64 (deterministic).
+// Work split: "stream-K" -- the tiles x k-steps space is cut into equal
+// contiguous ranges, so every SM streams the same number of K bytes; a tile
+// shared by several CTAs leaves per-CTA partial sums that kv_tc_reduce adds in
+// fixed CTA order, in float64 (deterministic).  Column passes (more vectors than
+// one TMEM accumulator holds) run as concurrent CTA groups of the same launch so
+// K streams from HBM about once.
 #include <cuda.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "rld_device.cuh"
@@ -44,14 +50,12 @@ namespace {
 
 constexpr int TC_BM = 128;          // K rows per tile (UMMA M)
 constexpr int TC_BK = 32;           // fp32 k-elements per step (one 128-byte swizzle row)
-constexpr int TC_THREADS = 256;
+constexpr int TC_THREADS = 512;
 constexpr int GROUP = 4;            // k-steps accumulated in TMEM before the register flush
-constexpr int NABUF = 4;            // TMEM A-operand buffers (converter runs up to 3 steps ahead)
+constexpr int NABUF = 4;            // TMEM A-operand buffers (converters run up to 3 steps ahead)
 constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4;  // 16 KB
 
-// A launch covers `npass` column passes of NT vectors each: CTA b works on pass
-// b % npass over stream-K range b / npass, so the CTAs that need the same K rows
-// run concurrently and K streams from HBM about once (L2 serves the other passes).
+// CTA b works on column pass b % npass over stream-K range b / npass.
 struct TcParams {
   int64_t total;    // tiles * ks
   int ks;           // k-steps per tile
@@ -61,6 +65,7 @@ struct TcParams {
   int stages;
   uint32_t tmem_cols;
   float* partial;   // [npass][tiles][segs][NT][128]
+  int debug;        // profiling knob (RLD_TC_DEBUG): 1 = skip A stores, 2 = skip MMAs, 4 = skip A loads
 };
 
 __host__ __device__ __forceinline__ int64_t cta_of_step(int64_t x, int64_t total, int64_t G) {
@@ -101,24 +106,35 @@ struct StepIter {
 };
 
 template <int MODE, int NT>
+struct TcShape {
+  static constexpr bool STACK = MODE == 3 && NT == 32;  // [Bhi; Blo] as one N = 2 NT operand
+  static constexpr int DW = STACK ? 2 * NT : NT;       // accumulator columns
+  static constexpr uint32_t B_BYTES = (uint32_t)NT * 128;
+  static constexpr uint32_t STAGE = A_BYTES + B_BYTES * (MODE == 3 ? 2 : 1);
+  static constexpr uint32_t ASTRIDE = MODE == 3 ? 64 : 32;  // TMEM columns per A buffer (hi | lo)
+  static constexpr uint32_t A_COL0 = 2 * DW;
+  static constexpr int TMEM_NEED = 2 * DW + NABUF * (int)ASTRIDE;
+  static constexpr uint32_t TMEM_COLS = TMEM_NEED <= 256 ? 256 : 512;
+  static_assert(TMEM_NEED <= 512, "TMEM budget");
+  static_assert(NT % 32 == 0 && NT <= 128, "NT");
+};
+
+template <int MODE, int NT>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
              const __grid_constant__ CUtensorMap tmBlo, const TcParams p) {
-  static_assert(NT % 32 == 0 && (MODE == 3 ? NT <= 64 : NT <= 128), "NT");
-  // accumulator width: 3xTF32 multiplies [Bhi; Blo] (2 NT rows) in one instruction and
-  // folds the two halves in the drain; 1xTF32 multiplies Bhi (NT rows)
-  constexpr int DW = MODE == 3 ? 2 * NT : NT;
+  using Sh = TcShape<MODE, NT>;
+  constexpr int DW = Sh::DW;
+  constexpr uint32_t B_BYTES = Sh::B_BYTES, STAGE = Sh::STAGE, ASTRIDE = Sh::ASTRIDE, A_COL0 = Sh::A_COL0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr uint32_t B_BYTES = (uint32_t)NT * 128;
-  constexpr uint32_t STAGE = A_BYTES + B_BYTES * (MODE == 3 ? 2 : 1);
   const int S = p.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * STAGE);
   uint64_t* empty = full + S;
-  uint64_t* afull = empty + S;       // [NABUF]
-  uint64_t* aempty = afull + NABUF;  // [NABUF]
-  uint64_t* accfull = aempty + NABUF;  // [2]
-  uint64_t* accempty = accfull + 2;  // [2]
+  uint64_t* afull = empty + S;          // [NABUF]
+  uint64_t* aempty = afull + NABUF;     // [NABUF]
+  uint64_t* accfull = aempty + NABUF;   // [2]
+  uint64_t* accempty = accfull + 2;     // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -142,117 +158,84 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&accfull[b], 1);
-      ptx::mbar_init(&accempty[b], 4);
+      ptx::mbar_init(&accempty[b], 8);
     }
     ptx::fence_mbarrier_init();
   }
-  if (warp == 2) ptx::tmem_alloc(tmem_holder, p.tmem_cols);
+  if (warp == 2) ptx::tmem_alloc(tmem_holder, Sh::TMEM_COLS);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
-  // TMEM columns: accumulators [0, DW) and [DW, 2DW); A buffer b at A_COL0 + ASTRIDE b: hi [+0, +32), lo [+32, +64)
-  constexpr uint32_t A_COL0 = 2 * DW;
-  constexpr uint32_t ASTRIDE = MODE == 3 ? 64 : 32;
 
   if (beg < end) {
     if (warp == 0) {
-      if (lane == 0) {
-        // ---------------- TMA producer
-        for (StepIter it(beg, end, p.ks, S); it.valid(); it.next()) {
-          const int s = it.s;
-          ptx::mbar_wait(&empty[s], it.ph ^ 1);
+      // ---------------- TMA producer (whole warp walks the ring; one elected lane issues)
+      for (StepIter it(beg, end, p.ks, S); it.valid(); it.next()) {
+        const int s = it.s;
+        ptx::mbar_wait(&empty[s], it.ph ^ 1);
+        if (ptx::elect_one()) {
           uint8_t* st = smem + (size_t)s * STAGE;
-          ptx::mbar_arrive_expect_tx(&full[s], STAGE);
-          ptx::tma_load_2d(st, &tmA, &full[s], it.kstep * TC_BK, it.tile * TC_BM);
+          ptx::mbar_arrive_expect_tx(&full[s], p.debug == 4 ? STAGE - A_BYTES : STAGE);
+          if (p.debug != 4) ptx::tma_load_2d(st, &tmA, &full[s], it.kstep * TC_BK, it.tile * TC_BM);
           ptx::tma_load_2d(st + A_BYTES, &tmBhi, &full[s], it.kstep * TC_BK, b_row0);
           if (MODE == 3) ptx::tma_load_2d(st + A_BYTES + B_BYTES, &tmBlo, &full[s], it.kstep * TC_BK, b_row0);
         }
+        __syncwarp();
       }
     } else if (warp == 1) {
-      if (lane == 0) {
-        // ---------------- MMA issuer
-        constexpr uint32_t idesc = ptx::idesc_tf32(TC_BM, DW);
-        int64_t gi = -1;  // group index
-        for (StepIter it(beg, end, p.ks, S); it.valid(); it.next()) {
-          const int s = it.s;
-          const int b = it.abuf();
-          const bool gstart = it.group_start(), gend = it.group_end();
-          if (gstart) {
-            ++gi;
-            if (gi >= 2) ptx::mbar_wait(&accempty[gi & 1], (uint32_t)(((gi >> 1) - 1) & 1));
-          }
-          const uint32_t d = tmem + (uint32_t)(gi & 1) * DW;
-          ptx::mbar_wait(&full[s], it.ph);
-          ptx::mbar_wait(&afull[b], it.aphase());
-          ptx::tc_fence_after();
-          const uint32_t sB = ptx::smem_u32(smem + (size_t)s * STAGE + A_BYTES);
+      // ---------------- MMA issuer
+      constexpr uint32_t idesc = ptx::idesc_tf32(TC_BM, DW);
+      const uint64_t desc0 = ptx::smem_desc_sw128(ptx::smem_u32(smem + A_BYTES));
+      constexpr uint64_t LO_OFF = (uint64_t)(B_BYTES >> 4);   // Blo rows, in descriptor units
+      int64_t gi = -1;  // group index
+      for (StepIter it(beg, end, p.ks, S); it.valid(); it.next()) {
+        const int s = it.s;
+        const int b = it.abuf();
+        const bool gstart = it.group_start(), gend = it.group_end();
+        if (gstart) {
+          ++gi;
+          if (gi >= 2) ptx::mbar_wait(&accempty[gi & 1], (uint32_t)(((gi >> 1) - 1) & 1));
+        }
+        ptx::mbar_wait(&full[s], it.ph);
+        ptx::mbar_wait(&afull[b], it.aphase());
+        ptx::tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(gi & 1) * DW;
+        const uint32_t a0 = tmem + A_COL0 + ASTRIDE * b;
+        const uint64_t bdesc = desc0 + (uint64_t)((s * STAGE) >> 4);
+        if (ptx::elect_one()) {
+          if (p.debug != 2) {
 #pragma unroll
-          for (int kk = 0; kk < TC_BK / 8; ++kk) {
-            const uint32_t a_hi = tmem + A_COL0 + ASTRIDE * b + 8 * kk;
-            const uint64_t bd = ptx::smem_desc_sw128(sB + 32 * kk);   // [Bhi; Blo] rows (3xTF32) or Bhi
-            const uint32_t acc = (gstart && kk == 0) ? 0u : 1u;
-            ptx::mma_tf32_ts(d, a_hi, bd, idesc, acc);                 // D += Ahi [Bhi; Blo]
-            if (MODE == 3) ptx::mma_tf32_ts(d, a_hi + 32, bd, idesc, 1u);  // D += Alo [Bhi; Blo]
+            for (int kk = 0; kk < TC_BK / 8; ++kk) {
+              const uint64_t bd = bdesc + 2 * kk;  // +32 bytes along k
+              const uint32_t acc = (gstart && kk == 0) ? 0u : 1u;
+              if (MODE == 1) {
+                ptx::mma_tf32_ts(d, a0 + 8 * kk, bd, idesc, acc);
+              } else if (Sh::STACK) {
+                ptx::mma_tf32_ts(d, a0 + 8 * kk, bd, idesc, acc);        // D += Ahi [Bhi; Blo]
+                ptx::mma_tf32_ts(d, a0 + 32 + 8 * kk, bd, idesc, 1u);    // D += Alo [Bhi; Blo]
+              } else {
+                ptx::mma_tf32_ts(d, a0 + 8 * kk, bd, idesc, acc);            // D += Ahi Bhi
+                ptx::mma_tf32_ts(d, a0 + 8 * kk, bd + LO_OFF, idesc, 1u);    // D += Ahi Blo
+                ptx::mma_tf32_ts(d, a0 + 32 + 8 * kk, bd, idesc, 1u);        // D += Alo Bhi
+              }
+            }
           }
           ptx::tc_commit(&empty[s]);
           ptx::tc_commit(&aempty[b]);
           if (gend) ptx::tc_commit(&accfull[gi & 1]);
         }
+        __syncwarp();
       }
-    } else if (warp >= 4) {
-      // ---------------- converters + accumulator drain (warp q owns TMEM lanes 32q..32q+31)
+    } else if (warp >= 4 && warp < 8) {
+      // ---------------- converters (warp q owns TMEM lanes 32q..32q+31)
       const int q = warp - 4;
       const int row = q * 32 + lane;
       const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-      float acc[NT];
-#pragma unroll
-      for (int c = 0; c < NT; ++c) acc[c] = 0.f;
-      // finished groups waiting to be drained (at most two in flight)
-      int64_t pend_gi[2], pend_tile[2];
-      bool pend_seg[2];
-      int npend = 0;
-
-      auto drain = [&](int64_t gi, bool seg_end, int64_t tile) {
-        const int buf = (int)(gi & 1);
-        ptx::mbar_wait(&accfull[buf], (uint32_t)((gi >> 1) & 1));
-        ptx::tc_fence_after();
-#pragma unroll
-        for (int c0 = 0; c0 < NT; c0 += 32) {
-          uint32_t v[32];
-          ptx::tmem_ld_32x32b_x32(tmem + lane_base + (uint32_t)(buf * DW + c0), v);
-          if (MODE == 3) {
-            uint32_t w[32];
-            ptx::tmem_ld_32x32b_x32(tmem + lane_base + (uint32_t)(buf * DW + NT + c0), w);
-            ptx::tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) acc[c0 + e] += __uint_as_float(v[e]) + __uint_as_float(w[e]);
-          } else {
-            ptx::tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) acc[c0 + e] += __uint_as_float(v[e]);
-          }
-        }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&accempty[buf]);
-        if (seg_end) {
-          const int seg = (int)(cta - cta_of_step(tile * (int64_t)p.ks, p.total, G));
-          float* P = partial + ((size_t)tile * p.segs + seg) * (size_t)NT * TC_BM;
-#pragma unroll
-          for (int c = 0; c < NT; ++c) {
-            P[(size_t)c * TC_BM + row] = acc[c];
-            acc[c] = 0.f;
-          }
-        }
-      };
-
-      int64_t gi = -1;
       for (StepIter it(beg, end, p.ks, S); it.valid(); it.next()) {
         const int s = it.s;
         const int b = it.abuf();
         const int64_t j = it.j;
-        if (it.group_start()) ++gi;
         ptx::mbar_wait(&full[s], it.ph);
         const uint32_t rowp = ptx::smem_u32(smem + (size_t)s * STAGE + row * 128);
         uint32_t hi[32], lo[32];
@@ -275,29 +258,68 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         if (j >= NABUF) ptx::mbar_wait(&aempty[b], (uint32_t)(((j / NABUF) - 1) & 1));
         ptx::tc_fence_after();
         const uint32_t ta = tmem + lane_base + A_COL0 + ASTRIDE * b;
-        ptx::tmem_st_32x32b_x32(ta, hi);
-        if (MODE == 3) ptx::tmem_st_32x32b_x32(ta + 32, lo);
+        if (p.debug != 1) {
+          ptx::tmem_st_32x32b_x32(ta, hi);
+          if (MODE == 3) ptx::tmem_st_32x32b_x32(ta + 32, lo);
+        }
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&afull[b]);
-
-        // drain groups that finished at earlier steps (their MMAs do not wait on this step)
-        for (int k = 0; k < npend; ++k) drain(pend_gi[k], pend_seg[k], pend_tile[k]);
-        npend = 0;
-        if (it.group_end()) {
-          pend_gi[npend] = gi;
-          pend_seg[npend] = it.seg_end();
-          pend_tile[npend] = it.tile;
-          ++npend;
+      }
+    } else if (warp >= 8) {
+      // ---------------- accumulator drain: warp 8 + q + 4h owns TMEM lanes 32q..32q+31 and
+      // result columns [h NT/2, (h+1) NT/2); finished groups are added to fp32 registers
+      // (round-to-nearest), a finished segment is stored to the partial buffer
+      constexpr int HALF = NT / 2;
+      const int q = (warp - 8) & 3, hsel = (warp - 8) >> 2;
+      const int row = q * 32 + lane;
+      const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+      const int c_base = hsel * HALF;
+      float acc[HALF];
+#pragma unroll
+      for (int c = 0; c < HALF; ++c) acc[c] = 0.f;
+      int64_t gi = -1;
+      for (StepIter it(beg, end, p.ks, 1); it.valid(); it.next()) {
+        if (it.group_start()) ++gi;
+        if (!it.group_end()) continue;
+        const int buf = (int)(gi & 1);
+        ptx::mbar_wait(&accfull[buf], (uint32_t)((gi >> 1) & 1));
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < HALF; c0 += 16) {
+          uint32_t v[16];
+          ptx::tmem_ld_32x32b_x16(tmem + lane_base + (uint32_t)(buf * DW + c_base + c0), v);
+          if (Sh::STACK) {
+            uint32_t w[16];
+            ptx::tmem_ld_32x32b_x16(tmem + lane_base + (uint32_t)(buf * DW + NT + c_base + c0), w);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]) + __uint_as_float(w[e]);
+          } else {
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]);
+          }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&accempty[buf]);
+        if (it.seg_end()) {
+          const int seg = (int)(cta - cta_of_step((int64_t)it.tile * p.ks, p.total, G));
+          float* P = partial + ((size_t)it.tile * p.segs + seg) * (size_t)NT * TC_BM;
+#pragma unroll
+          for (int c = 0; c < HALF; ++c) {
+            P[(size_t)(c_base + c) * TC_BM + row] = acc[c];
+            acc[c] = 0.f;
+          }
         }
       }
-      for (int k = 0; k < npend; ++k) drain(pend_gi[k], pend_seg[k], pend_tile[k]);
     }
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 2) ptx::tmem_dealloc(tmem, p.tmem_cols);
+  if (warp == 2) ptx::tmem_dealloc(tmem, Sh::TMEM_COLS);
 }
 
 // Y[c * ldy + i] = sum over the tile's segments of the partials (float64 accumulation, fixed order)
@@ -384,37 +406,27 @@ int max_smem_optin() {
 }
 
 template <int MODE, int NT>
-void launch_tc(const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl, TcParams p, int64_t G,
+void launch_tc(const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl, TcParams p, int64_t grid,
                cudaStream_t st) {
-  constexpr size_t stage = A_BYTES + (size_t)NT * 128 * (MODE == 3 ? 2 : 1);
+  using Sh = TcShape<MODE, NT>;
   const size_t extra = 1024 + 8 * 64;
   const int smem_cap = max_smem_optin() - 1024;
-  p.stages = (int)std::min<size_t>(8, (smem_cap - extra) / stage);
-  constexpr int DW = MODE == 3 ? 2 * NT : NT;
-  constexpr int cols = 2 * DW + NABUF * (MODE == 3 ? 64 : 32);
-  static_assert(cols <= 512, "TMEM budget");
-  p.tmem_cols = cols <= 256 ? 256 : 512;
-  const size_t smem = p.stages * stage + extra;
+  p.stages = (int)std::min<size_t>(8, (smem_cap - extra) / Sh::STAGE);
+  p.tmem_cols = Sh::TMEM_COLS;
+  const size_t smem = p.stages * Sh::STAGE + extra;
   RLD_CUDA(cudaFuncSetAttribute(kv_tc_kernel<MODE, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kv_tc_kernel<MODE, NT><<<(unsigned)G, TC_THREADS, smem, st>>>(mA, mBh, mBl, p);
+  kv_tc_kernel<MODE, NT><<<(unsigned)grid, TC_THREADS, smem, st>>>(mA, mBh, mBl, p);
   RLD_LAUNCH_CHECK();
 }
 
-void launch_tc_3(int nt, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl, const TcParams& p,
-                 int64_t G, cudaStream_t st) {
-  if (nt == 32)
-    launch_tc<3, 32>(mA, mBh, mBl, p, G, st);
-  else
-    launch_tc<3, 64>(mA, mBh, mBl, p, G, st);
-}
-
-void launch_tc_1(int nt, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl, const TcParams& p,
-                 int64_t G, cudaStream_t st) {
+template <int MODE>
+void launch_tc_nt(int nt, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl, const TcParams& p,
+                  int64_t grid, cudaStream_t st) {
   switch (nt) {
-    case 32: launch_tc<1, 32>(mA, mBh, mBl, p, G, st); break;
-    case 64: launch_tc<1, 64>(mA, mBh, mBl, p, G, st); break;
-    case 96: launch_tc<1, 96>(mA, mBh, mBl, p, G, st); break;
-    default: launch_tc<1, 128>(mA, mBh, mBl, p, G, st); break;
+    case 32: launch_tc<MODE, 32>(mA, mBh, mBl, p, grid, st); break;
+    case 64: launch_tc<MODE, 64>(mA, mBh, mBl, p, grid, st); break;
+    case 96: launch_tc<MODE, 96>(mA, mBh, mBl, p, grid, st); break;
+    default: launch_tc<MODE, 128>(mA, mBh, mBl, p, grid, st); break;
   }
 }
 
@@ -443,9 +455,8 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
   const int ks = (int)ceil_div(n, TC_BK);
   const int tiles = (int)ceil_div(rows, TC_BM);
   const int64_t total = (int64_t)tiles * ks;
-  // vectors per pass: <= 64 for 3xTF32 ([Bhi; Blo] is one N = 2 NT instruction), <= 128 for
-  // 1xTF32 (register-resident fp32 accumulators of the drain warps)
-  const int npass = (int)ceil_div(m, mode == 3 ? 64 : 128);
+  // vectors per pass: <= 128 (two TMEM accumulators + A buffers within 512 columns)
+  const int npass = (int)ceil_div(m, 128);
   const int width = (int)(ceil_div(ceil_div(m, npass), 32) * 32);
   const int64_t Gl = std::min<int64_t>(std::max(1, G / npass), total);
   int segs = 1;
@@ -460,14 +471,18 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
   p.tiles = tiles;
   p.npass = npass;
   p.segs = segs;
+  {
+    static const int dbg = getenv("RLD_TC_DEBUG") ? atoi(getenv("RLD_TC_DEBUG")) : 0;
+    p.debug = dbg;
+  }
   ws.tc_partial.reserve(sizeof(float) * (size_t)npass * tiles * segs * width * TC_BM);
   p.partial = ws.tc_partial.as<float>();
   const CUtensorMap mBh = make_map(ws.bhi.as<float>(), n, m, ldb, width);
   const CUtensorMap mBl = mode == 3 ? make_map(ws.blo.as<float>(), n, m, ldb, width) : mBh;
   if (mode == 3)
-    launch_tc_3(width, mA, mBh, mBl, p, Gl * npass, st);
+    launch_tc_nt<3>(width, mA, mBh, mBl, p, Gl * npass, st);
   else
-    launch_tc_1(width, mA, mBh, mBl, p, Gl * npass, st);
+    launch_tc_nt<1>(width, mA, mBh, mBl, p, Gl * npass, st);
   const int64_t count = m * rows;
   const int blocks = (int)std::min<int64_t>(ceil_div(count, 256), 148 * 16);
   kv_tc_reduce<<<blocks, 256, 0, st>>>(p.partial, total, Gl, ks, tiles, segs, width, m, rows, Y, ldy);

@@ -7,13 +7,13 @@
 
 using namespace rld;
 
-template <int N, int NACC>
+template <int N, int NACC, int COMMIT_EVERY>
 __global__ void bench(int iters, long long* out) {
   __shared__ __align__(1024) uint8_t bsm[256 * 128];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar2;
   __shared__ uint32_t holder;
   for (int i = threadIdx.x; i < 256 * 128 / 4; i += blockDim.x) reinterpret_cast<float*>(bsm)[i] = 1.0f;
-  if (threadIdx.x == 0) { ptx::mbar_init(&bar, 1); ptx::fence_mbarrier_init(); }
+  if (threadIdx.x == 0) { ptx::mbar_init(&bar, 1); ptx::mbar_init(&bar2, 1); ptx::fence_mbarrier_init(); }
   if (threadIdx.x < 32) ptx::tmem_alloc(&holder, 512);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   ptx::tc_fence_before();
@@ -36,6 +36,7 @@ __global__ void bench(int iters, long long* out) {
           ptx::mma_tf32_ts(tmem + (k % NACC) * (256 / NACC), tmem + 256 + 8 * k, bd + 2 * k, idesc, 1u);
         }
       }
+      if (COMMIT_EVERY && (i % COMMIT_EVERY) == 0) ptx::tc_commit(&bar2);
     }
     ptx::tc_commit(&bar);
     ptx::mbar_wait(&bar, 0);
@@ -47,26 +48,27 @@ __global__ void bench(int iters, long long* out) {
   if (threadIdx.x < 32) ptx::tmem_dealloc(tmem, 512);
 }
 
-template <int N, int NACC>
+template <int N, int NACC, int CE>
 void run() {
   long long* d;
   cudaMalloc(&d, 8);
   const int iters = 2000;
-  bench<N, NACC><<<148, 128>>>(iters, d);
-  bench<N, NACC><<<148, 128>>>(iters, d);
+  bench<N, NACC, CE><<<148, 128>>>(iters, d);
+  bench<N, NACC, CE><<<148, 128>>>(iters, d);
   long long h = 0;
   cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
   cudaError_t e = cudaGetLastError();
-  printf("N=%3d acc=%d: %.1f cycles per MMA (128x%dx8 tf32, A in TMEM)  %s\n", N, NACC, (double)h / (iters * 4), N,
+  printf("N=%3d acc=%d commit_every=%d: %.1f cycles per MMA (128x%dx8 tf32, A in TMEM)  %s\n", N, NACC, CE, (double)h / (iters * 4), N,
          cudaGetErrorString(e));
   cudaFree(d);
 }
 
 int main() {
-  run<32, 1>();
-  run<32, 0>();
-  run<64, 0>();
-  run<128, 0>();
-  run<256, 0>();
+  run<64, 1, 0>();
+  run<64, 1, 1>();
+  run<64, 1, 2>();
+  run<64, 1, 8>();
+  run<128, 1, 0>();
+  run<128, 1, 1>();
   return 0;
 }
