@@ -246,7 +246,7 @@ void kv_product(const KvOperand& op, int64_t m, const double* V, int64_t ldv, do
       launch_kv<double, double, 64, 32, 16, 4, 4, false>(op, m, V, ldv, Y, ldy, ws, st, launches);
     return;
   }
-  if (!otf && kv_tc_supported(op) && !getenv("RLD_NO_TC")) {
+  if (kv_tc_supported(op) && !getenv("RLD_NO_TC")) {
     kv_product_tc(op, op.tc_mode, m, V, ldv, Y, ldy, ws, st);
     return;
   }

@@ -66,7 +66,57 @@ struct TcParams {
   uint32_t tmem_cols;
   float* partial;   // [npass][tiles][segs][NT][128]
   int debug;        // profiling knob (RLD_TC_DEBUG): 1 = skip A stores, 2 = skip MMAs, 4 = skip A loads
+  // on-the-fly kernel tiles (src/kernels.py:40-46, 72)
+  const float* pts;  // [8][ldp] float32: coordinate rows x,y,z,w (hi) then x,y,z,w (lo)
+  int64_t ldp;
+  int64_t n, row0, rows;
+  int family;
+  float a2, gscale, s5, diag;  // amplitude^2, log2(e) / (2 l^2), sqrt(5) / l, a^2 + jitter
 };
+
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// packed FP32x2 helpers (sm_100 FADD2 / FMUL2 / FFMA2), lanes = (lo 32 bits, hi 32 bits)
+__device__ __forceinline__ uint64_t pk(float a, float b) {
+  return (uint64_t)__float_as_uint(a) | ((uint64_t)__float_as_uint(b) << 32);
+}
+__device__ __forceinline__ float pk_lo(uint64_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float pk_hi(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// Two K entries from packed squared distances (src/kernels.py:40-46), float32.
+template <int FAM>
+__device__ __forceinline__ uint64_t kernel_pair(const TcParams& p, uint64_t r2) {
+  if (FAM == RLD_RBF) {
+    const uint64_t t = mul2(r2, pk(-p.gscale, -p.gscale));
+    return mul2(pk(fast_exp2(pk_lo(t)), fast_exp2(pk_hi(t))), pk(p.a2, p.a2));
+  }
+  const float a = pk_lo(r2), b = pk_hi(r2);
+  const float ra = a > 0.f ? a * rsqrtf(a) : 0.f, rb = b > 0.f ? b * rsqrtf(b) : 0.f;
+  const uint64_t u = mul2(pk(ra, rb), pk(p.s5, p.s5));
+  const uint64_t poly = fma2(u, fma2(u, pk(1.0f / 3.0f, 1.0f / 3.0f), pk(1.f, 1.f)), pk(1.f, 1.f));
+  const uint64_t t = mul2(u, pk(-1.4426950408889634f, -1.4426950408889634f));
+  const uint64_t e = pk(fast_exp2(pk_lo(t)), fast_exp2(pk_hi(t)));
+  return mul2(mul2(poly, e), pk(p.a2, p.a2));
+}
 
 __host__ __device__ __forceinline__ int64_t cta_of_step(int64_t x, int64_t total, int64_t G) {
   // the CTA whose range [c*total/G, (c+1)*total/G) contains step x
@@ -105,12 +155,20 @@ struct StepIter {
   }
 };
 
-template <int MODE, int NT>
+// On-the-fly K: the stage carries the 32 column points of the k-step (TMA box of
+// the coordinate-major point array [8][ldp]: rows x,y,z,w hi then x,y,z,w lo -- a
+// double-float split of the float64 coordinates, so differences of close points
+// keep ~48 bits) instead of a K tile; the converter warps generate the tile with
+// packed FP32x2 arithmetic (FFMA2/FADD2/FMUL2) and MUFU ex2/rsqrt.
+constexpr uint32_t PTS_BYTES = 1024;
+
+template <int MODE, int NT, bool OTF = false>
 struct TcShape {
   static constexpr bool STACK = MODE == 3 && NT == 32;  // [Bhi; Blo] as one N = 2 NT operand
   static constexpr int DW = STACK ? 2 * NT : NT;       // accumulator columns
   static constexpr uint32_t B_BYTES = (uint32_t)NT * 128;
-  static constexpr uint32_t STAGE = A_BYTES + B_BYTES * (MODE == 3 ? 2 : 1);
+  static constexpr uint32_t A_REGION = OTF ? PTS_BYTES : A_BYTES;
+  static constexpr uint32_t STAGE = A_REGION + B_BYTES * (MODE == 3 ? 2 : 1);
   static constexpr uint32_t ASTRIDE = MODE == 3 ? 64 : 32;  // TMEM columns per A buffer (hi | lo)
   static constexpr uint32_t A_COL0 = 2 * DW;
   static constexpr int TMEM_NEED = 2 * DW + NABUF * (int)ASTRIDE;
@@ -119,15 +177,18 @@ struct TcShape {
   static_assert(NT % 32 == 0 && NT <= 128, "NT");
 };
 
-template <int MODE, int NT>
+template <int MODE, int NT, bool OTF, int DIM, int FAM>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
              const __grid_constant__ CUtensorMap tmBlo, const TcParams p) {
-  using Sh = TcShape<MODE, NT>;
+  using Sh = TcShape<MODE, NT, OTF>;
   constexpr int DW = Sh::DW;
   constexpr uint32_t B_BYTES = Sh::B_BYTES, STAGE = Sh::STAGE, ASTRIDE = Sh::ASTRIDE, A_COL0 = Sh::A_COL0;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr uint32_t AR = Sh::A_REGION;   // K tile (stored) or column points (on the fly)
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  // 1024-byte aligned base, derived from smem_raw so the compiler keeps the shared
+  // address space (plain C++ loads compile to LDS and are ordered by the mbarrier asm)
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int S = p.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * STAGE);
   uint64_t* empty = full + S;
@@ -176,17 +237,22 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         ptx::mbar_wait(&empty[s], it.ph ^ 1);
         if (ptx::elect_one()) {
           uint8_t* st = smem + (size_t)s * STAGE;
-          ptx::mbar_arrive_expect_tx(&full[s], p.debug == 4 ? STAGE - A_BYTES : STAGE);
-          if (p.debug != 4) ptx::tma_load_2d(st, &tmA, &full[s], it.kstep * TC_BK, it.tile * TC_BM);
-          ptx::tma_load_2d(st + A_BYTES, &tmBhi, &full[s], it.kstep * TC_BK, b_row0);
-          if (MODE == 3) ptx::tma_load_2d(st + A_BYTES + B_BYTES, &tmBlo, &full[s], it.kstep * TC_BK, b_row0);
+          if (OTF) {
+            ptx::mbar_arrive_expect_tx(&full[s], STAGE);
+            ptx::tma_load_2d(st, &tmA, &full[s], it.kstep * TC_BK, 0);   // 32 column points, 8 coordinate rows
+          } else {
+            ptx::mbar_arrive_expect_tx(&full[s], p.debug == 4 ? STAGE - AR : STAGE);
+            if (p.debug != 4) ptx::tma_load_2d(st, &tmA, &full[s], it.kstep * TC_BK, it.tile * TC_BM);
+          }
+          ptx::tma_load_2d(st + AR, &tmBhi, &full[s], it.kstep * TC_BK, b_row0);
+          if (MODE == 3) ptx::tma_load_2d(st + AR + B_BYTES, &tmBlo, &full[s], it.kstep * TC_BK, b_row0);
         }
         __syncwarp();
       }
     } else if (warp == 1) {
       // ---------------- MMA issuer
       constexpr uint32_t idesc = ptx::idesc_tf32(TC_BM, DW);
-      const uint64_t desc0 = ptx::smem_desc_sw128(ptx::smem_u32(smem + A_BYTES));
+      const uint64_t desc0 = ptx::smem_desc_sw128(ptx::smem_u32(smem + AR));
       constexpr uint64_t LO_OFF = (uint64_t)(B_BYTES >> 4);   // Blo rows, in descriptor units
       int64_t gi = -1;  // group index
       for (StepIter it(beg, end, p.ks, S); it.valid(); it.next()) {
@@ -232,26 +298,80 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       const int q = warp - 4;
       const int row = q * 32 + lane;
       const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+      int cur_tile = -1;
+      uint64_t xh2[4] = {0, 0, 0, 0}, xl2[4] = {0, 0, 0, 0};   // this row's point, packed twice (on the fly)
+      int64_t grow = 0;
       for (StepIter it(beg, end, p.ks, S); it.valid(); it.next()) {
         const int s = it.s;
         const int b = it.abuf();
         const int64_t j = it.j;
-        ptx::mbar_wait(&full[s], it.ph);
-        const uint32_t rowp = ptx::smem_u32(smem + (size_t)s * STAGE + row * 128);
         uint32_t hi[32], lo[32];
+        if (OTF) {
+          if (it.tile != cur_tile) {
+            cur_tile = it.tile;
+            const int64_t lr = (int64_t)cur_tile * TC_BM + row;
+            grow = p.row0 + lr;
+            if (lr < p.rows) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float4 v = ptx::lds128(rowp + ((c ^ (row & 7)) << 4));
-          const float vv[4] = {v.x, v.y, v.z, v.w};
+              for (int k = 0; k < DIM; ++k) {
+                const float h = p.pts[k * p.ldp + grow], l = p.pts[(4 + k) * p.ldp + grow];
+                xh2[k] = pk(h, h);
+                xl2[k] = pk(l, l);
+              }
+            }
+          }
+          ptx::mbar_wait(&full[s], it.ph);
+          const float* pp = reinterpret_cast<const float*>(smem + (size_t)s * STAGE);   // [8][32]
+          const int64_t j0 = (int64_t)it.kstep * TC_BK;
+          const int64_t dd = grow - j0;                       // column of this row's diagonal entry
+          const int dcol = (dd >= 0 && dd < 32) ? (int)dd : -1;
+          const int64_t nn = p.n - j0;
+          const int ncol = nn < 32 ? (int)nn : 32;            // valid columns in this step
+          const uint64_t neg1 = pk(-1.f, -1.f);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const uint32_t ub = __float_as_uint(vv[e]);
+          for (int e = 0; e < 32; e += 2) {
+            uint64_t r2 = 0;
+#pragma unroll
+            for (int k = 0; k < DIM; ++k) {
+              const uint64_t ch = *reinterpret_cast<const uint64_t*>(pp + k * 32 + e);
+              const uint64_t cl = *reinterpret_cast<const uint64_t*>(pp + (4 + k) * 32 + e);
+              const uint64_t dk = add2(fma2(ch, neg1, xh2[k]), fma2(cl, neg1, xl2[k]));  // (xh-ch)+(xl-cl)
+              r2 = fma2(dk, dk, r2);
+            }
+            const uint64_t kv = kernel_pair<FAM>(p, r2);
+            float v0 = pk_lo(kv), v1 = pk_hi(kv);
+            v0 = (e == dcol) ? p.diag : (e < ncol ? v0 : 0.f);
+            v1 = (e + 1 == dcol) ? p.diag : (e + 1 < ncol ? v1 : 0.f);
+            const uint32_t u0 = __float_as_uint(v0), u1 = __float_as_uint(v1);
             if (MODE == 3) {
-              const uint32_t hb = ub & 0xFFFFE000u;
-              hi[4 * c + e] = hb;
-              lo[4 * c + e] = __float_as_uint(vv[e] - __uint_as_float(hb));
+              const uint32_t h0 = u0 & 0xFFFFE000u, h1 = u1 & 0xFFFFE000u;
+              hi[e] = h0;
+              hi[e + 1] = h1;
+              const uint64_t l2 = add2(pk(v0, v1), fma2(pk(__uint_as_float(h0), __uint_as_float(h1)), neg1, 0));
+              lo[e] = (uint32_t)l2;
+              lo[e + 1] = (uint32_t)(l2 >> 32);
             } else {
-              hi[4 * c + e] = ub;
+              hi[e] = u0;
+              hi[e + 1] = u1;
+            }
+          }
+        } else {
+          ptx::mbar_wait(&full[s], it.ph);
+          const uint8_t* rowp = smem + (size_t)s * STAGE + row * 128;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (row & 7)) << 4));
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const uint32_t ub = __float_as_uint(vv[e]);
+              if (MODE == 3) {
+                const uint32_t hb = ub & 0xFFFFE000u;
+                hi[4 * c + e] = hb;
+                lo[4 * c + e] = __float_as_uint(vv[e] - __uint_as_float(hb));
+              } else {
+                hi[4 * c + e] = ub;
+              }
             }
           }
         }
@@ -405,36 +525,77 @@ int max_smem_optin() {
   return v;
 }
 
-template <int MODE, int NT>
+template <int MODE, int NT, bool OTF, int DIM, int FAM>
 void launch_tc(const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl, TcParams p, int64_t grid,
                cudaStream_t st) {
-  using Sh = TcShape<MODE, NT>;
+  using Sh = TcShape<MODE, NT, OTF>;
   const size_t extra = 1024 + 8 * 64;
   const int smem_cap = max_smem_optin() - 1024;
   p.stages = (int)std::min<size_t>(8, (smem_cap - extra) / Sh::STAGE);
   p.tmem_cols = Sh::TMEM_COLS;
   const size_t smem = p.stages * Sh::STAGE + extra;
-  RLD_CUDA(cudaFuncSetAttribute(kv_tc_kernel<MODE, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kv_tc_kernel<MODE, NT><<<(unsigned)grid, TC_THREADS, smem, st>>>(mA, mBh, mBl, p);
+  RLD_CUDA(cudaFuncSetAttribute(kv_tc_kernel<MODE, NT, OTF, DIM, FAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+  kv_tc_kernel<MODE, NT, OTF, DIM, FAM><<<(unsigned)grid, TC_THREADS, smem, st>>>(mA, mBh, mBl, p);
   RLD_LAUNCH_CHECK();
 }
 
 template <int MODE>
-void launch_tc_nt(int nt, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl, const TcParams& p,
-                  int64_t grid, cudaStream_t st) {
+void launch_tc_stored(int nt, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl,
+                      const TcParams& p, int64_t grid, cudaStream_t st) {
   switch (nt) {
-    case 32: launch_tc<MODE, 32>(mA, mBh, mBl, p, grid, st); break;
-    case 64: launch_tc<MODE, 64>(mA, mBh, mBl, p, grid, st); break;
-    case 96: launch_tc<MODE, 96>(mA, mBh, mBl, p, grid, st); break;
-    default: launch_tc<MODE, 128>(mA, mBh, mBl, p, grid, st); break;
+    case 32: launch_tc<MODE, 32, false, 0, 0>(mA, mBh, mBl, p, grid, st); break;
+    case 64: launch_tc<MODE, 64, false, 0, 0>(mA, mBh, mBl, p, grid, st); break;
+    case 96: launch_tc<MODE, 96, false, 0, 0>(mA, mBh, mBl, p, grid, st); break;
+    default: launch_tc<MODE, 128, false, 0, 0>(mA, mBh, mBl, p, grid, st); break;
   }
+}
+
+template <int DIM, int FAM>
+void launch_tc_otf_nt(int nt, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl,
+                      const TcParams& p, int64_t grid, cudaStream_t st) {
+  switch (nt) {
+    case 32: launch_tc<3, 32, true, DIM, FAM>(mA, mBh, mBl, p, grid, st); break;
+    case 64: launch_tc<3, 64, true, DIM, FAM>(mA, mBh, mBl, p, grid, st); break;
+    default: launch_tc<3, 128, true, DIM, FAM>(mA, mBh, mBl, p, grid, st); break;
+  }
+}
+
+// on-the-fly tiles: 3xTF32 only; d = 1 runs as DIM 2 (zero padding)
+void launch_tc_otf(int d, int family, int nt, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl,
+                   const TcParams& p, int64_t grid, cudaStream_t st) {
+  if (family == RLD_RBF) {
+    if (d <= 2) launch_tc_otf_nt<2, RLD_RBF>(nt, mA, mBh, mBl, p, grid, st);
+    else if (d == 3) launch_tc_otf_nt<3, RLD_RBF>(nt, mA, mBh, mBl, p, grid, st);
+    else launch_tc_otf_nt<4, RLD_RBF>(nt, mA, mBh, mBl, p, grid, st);
+  } else {
+    if (d <= 2) launch_tc_otf_nt<2, RLD_MATERN52>(nt, mA, mBh, mBl, p, grid, st);
+    else if (d == 3) launch_tc_otf_nt<3, RLD_MATERN52>(nt, mA, mBh, mBl, p, grid, st);
+    else launch_tc_otf_nt<4, RLD_MATERN52>(nt, mA, mBh, mBl, p, grid, st);
+  }
+}
+
+// 2-D map over the coordinate-major split points [8][ldp] fp32: box {32, 8} = the
+// 32 column points of one k-step
+CUtensorMap make_points_map(const float* pts, int64_t n, int64_t ldp) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)n, 8};
+  cuuint64_t strides[1] = {(cuuint64_t)ldp * 4};
+  cuuint32_t box[2] = {(cuuint32_t)TC_BK, 8};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(pts), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(RLD_ERR_CUDA, "cuTensorMapEncodeTiled (points) failed (" + std::to_string((int)r) + ")");
+  return m;
 }
 
 }  // namespace
 
 bool kv_tc_supported(const KvOperand& op) {
-  return op.dtype == RLD_FP32 && op.K != nullptr && (op.ldk % 4) == 0 &&
-         (reinterpret_cast<uintptr_t>(op.K) % 16) == 0;
+  if (op.dtype != RLD_FP32) return false;
+  if (op.K == nullptr) return op.pts4 != nullptr && op.kp.d <= 4 && op.tc_mode == 3;   // on the fly
+  return (op.ldk % 4) == 0 && (reinterpret_cast<uintptr_t>(op.K) % 16) == 0;
 }
 
 // Y (m x rows, float64, row stride ldy) = V (m x n float64 rows) K^T on the tensor cores.
@@ -457,15 +618,29 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
   const int64_t total = (int64_t)tiles * ks;
   // vectors per pass: <= 128 (two TMEM accumulators + A buffers within 512 columns)
   const int npass = (int)ceil_div(m, 128);
-  const int width = (int)(ceil_div(ceil_div(m, npass), 32) * 32);
+  int width = (int)(ceil_div(ceil_div(m, npass), 32) * 32);
+  if (op.K == nullptr && width == 96) width = 128;   // on-the-fly kernels come in NT = 32, 64, 128
   const int64_t Gl = std::min<int64_t>(std::max(1, G / npass), total);
   int segs = 1;
   for (int t = 0; t < tiles; ++t) {
     const int64_t x0 = (int64_t)t * ks;
     segs = (int)std::max<int64_t>(segs, cta_of_step(x0 + ks - 1, total, Gl) - cta_of_step(x0, total, Gl) + 1);
   }
-  const CUtensorMap mA = make_map(static_cast<const float*>(op.K), n, rows, op.ldk, TC_BM);
+  const bool otf = op.K == nullptr;
+  const int64_t ldp = ceil_div(n, 4) * 4;
+  const CUtensorMap mA = otf ? make_points_map(op.pts4, n, ldp)
+                             : make_map(static_cast<const float*>(op.K), n, rows, op.ldk, TC_BM);
   TcParams p{};
+  p.pts = op.pts4;
+  p.ldp = ldp;
+  p.n = n;
+  p.row0 = op.row0;
+  p.rows = rows;
+  p.family = op.kp.family;
+  p.a2 = (float)op.kp.a2;
+  p.gscale = (float)(op.kp.inv_2l2 * 1.4426950408889634);
+  p.s5 = (float)op.kp.s5_over_l;
+  p.diag = (float)op.kp.diag;
   p.total = total;
   p.ks = ks;
   p.tiles = tiles;
@@ -479,10 +654,14 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
   p.partial = ws.tc_partial.as<float>();
   const CUtensorMap mBh = make_map(ws.bhi.as<float>(), n, m, ldb, width);
   const CUtensorMap mBl = mode == 3 ? make_map(ws.blo.as<float>(), n, m, ldb, width) : mBh;
-  if (mode == 3)
-    launch_tc_nt<3>(width, mA, mBh, mBl, p, Gl * npass, st);
-  else
-    launch_tc_nt<1>(width, mA, mBh, mBl, p, Gl * npass, st);
+  if (otf) {
+    launch_tc_otf(op.kp.d, op.kp.family, width, mA, mBh, mBl, p, Gl * npass, st);
+  } else {
+    if (mode == 3)
+      launch_tc_stored<3>(width, mA, mBh, mBl, p, Gl * npass, st);
+    else
+      launch_tc_stored<1>(width, mA, mBh, mBl, p, Gl * npass, st);
+  }
   const int64_t count = m * rows;
   const int blocks = (int)std::min<int64_t>(ceil_div(count, 256), 148 * 16);
   kv_tc_reduce<<<blocks, 256, 0, st>>>(p.partial, total, Gl, ks, tiles, segs, width, m, rows, Y, ldy);

@@ -73,6 +73,7 @@ struct Resident {
   const void* K = nullptr;   // stored rows (owned or aliased)
   int64_t ldk = 0;
   DevBuf X;                  // points n x d
+  DevBuf pts4;               // points split to n x 8 fp32 hi/lo (d <= 4; tensor-core on-the-fly tiles)
   DevBuf diag;               // local diagonal of K (float64)
   KernelParams kp{};
 
@@ -81,6 +82,7 @@ struct Resident {
     o.K = (path == RLD_PATH_ON_THE_FLY) ? nullptr : K;
     o.ldk = ldk;
     o.X = X.as<double>();
+    o.pts4 = (source == RLD_SOURCE_POINTS && d <= 4) ? pts4.as<float>() : nullptr;
     o.kp = kp;
     o.dtype = dtype;
     o.n = n;
@@ -195,6 +197,10 @@ void prepare(rld_handle* h, const rld_problem* p) {
                              p->data_memory == RLD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
     r.diag.reserve(sizeof(double) * std::max<int64_t>(1, r.rows));
     fill_doubles(r.rows, r.kp.diag, r.diag.as<double>(), st);
+    if (p->d <= 4) {
+      r.pts4.reserve(sizeof(float) * 8 * ceil_div(p->n, 4) * 4);
+      pad_points(r.X.as<double>(), p->n, p->d, r.pts4.as<float>(), st);
+    }
     if (r.path == RLD_PATH_STORED) {
       const size_t es = p->dtype == RLD_FP64 ? 8 : 4;
       r.ldk = ceil_div(p->n, 4) * 4;  // 16-byte row pitch for TMA

@@ -72,6 +72,7 @@ struct KvOperand {
   const void* K = nullptr;   // dense rows (rows x n, row stride ldk), dtype below
   int64_t ldk = 0;
   const double* X = nullptr; // points (n x d) for on-the-fly generation
+  const float* pts4 = nullptr;  // points as n x 8 fp32 (hi x,y,z,w; lo x,y,z,w) for the tensor-core on-the-fly path, d <= 4
   KernelParams kp{};
   int dtype = RLD_FP64;      // product arithmetic
   int64_t n = 0;             // columns of K (global order)

@@ -570,6 +570,26 @@ void sqrt_factors(int k, double keep_rtol, const double* lam, double* W, double*
   sqrt_factor_kernel<<<std::min(k, 1024), 128, 0, st>>>(k, keep_rtol, lam, W, h, g, gam, kept);
   RLD_LAUNCH_CHECK();
 }
+namespace {
+// coordinate-major split points [8][ldp]: row k = fp32(x_k) (hi), row 4 + k = fp32(x_k - hi) (lo)
+__global__ void pad_points_kernel(const double* __restrict__ X, int64_t n, int d, float* __restrict__ P) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= 4 * n) return;
+  const int64_t i = e >> 2;
+  const int k = (int)(e & 3);
+  const int64_t ldp = ceil_div(n, 4) * 4;
+  const double x = k < d ? X[i * d + k] : 0.0;
+  const float h = (float)x;
+  P[k * ldp + i] = h;
+  P[(4 + k) * ldp + i] = (float)(x - (double)h);
+}
+}  // namespace
+
+void pad_points(const double* X, int64_t n, int d, float* pts8, cudaStream_t st) {
+  pad_points_kernel<<<(unsigned)ceil_div(4 * n, 256), 256, 0, st>>>(X, n, d, pts8);
+  RLD_LAUNCH_CHECK();
+}
+
 void diag_of_dense(int64_t rows, int64_t row0, const void* K, int64_t ldk, int dtype, double* d, cudaStream_t st) {
   diag_of_dense_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, st>>>(rows, row0, K, ldk, dtype, d);
   RLD_LAUNCH_CHECK();
