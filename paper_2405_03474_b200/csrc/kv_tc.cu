@@ -4,14 +4,15 @@
 // path of BASELINE configs 2-3; reference call sites src/estimators.py:72 and
 // src/precond.py:186, 189).
 //
-// One persistent CTA per SM, 16 warps:
+// One persistent CTA per SM, 20 warps:
 //   warp 0       TMA producer: K tile (128 rows x 32 fp32, 128B-swizzled) plus the
 //                B tiles (NT vectors x 32 fp32: tf32-hi, and lo for 3xTF32) per
 //                k-step into an S-stage shared-memory ring (full/empty mbarriers).
-//   warps 4-7    converters: thread = one K row; it reads its 32 values from the
-//                swizzled tile, splits them into tf32 hi + lo (lo exact in fp32)
-//                and tcgen05.st's them into one of NABUF TMEM A-operand buffers,
-//                so the tensor core never re-reads A from shared memory.
+//   warps 4-11   converters (two per TMEM lane quarter, 16 of the 32 k-columns each):
+//                thread = one K row; it reads its values from the swizzled tile (or
+//                generates them from the points), splits them into tf32 hi + lo
+//                (lo exact in fp32) and tcgen05.st's them into one of NABUF TMEM
+//                A-operand buffers, so the tensor core never re-reads A from SMEM.
 //   warp 1       MMA issuer (whole warp walks the pipeline so every descriptor is
 //                warp-uniform; one elected lane issues).  3xTF32 per 8-wide k chunk:
 //                  NT == 32: D[2NT] += Ahi [Bhi; Blo] + Alo [Bhi; Blo] (two N = 64
@@ -19,8 +20,8 @@
 //                            N = 64, so stacking hi/lo B halves the issue count);
 //                  NT >= 64: D[NT] += Ahi Bhi + Ahi Blo + Alo Bhi.
 //                1xTF32 (optional sketch mode): D[NT] += A Bhi.
-//   warps 8-15   accumulator drain (two warps per TMEM lane quarter, one half of
-//                the columns each).
+//   warps 12-19  accumulator drain (two warps per TMEM lane quarter, one half of
+//                the result columns each).
 //   warp 2       TMEM allocation owner.
 //
 // Accuracy: the tensor core rounds its fp32 accumulator toward zero, so a long
@@ -37,6 +38,7 @@
 // K streams from HBM about once.
 #include <cuda.h>
 
+#include <cmath>
 #include <cstdlib>
 #include <mutex>
 
@@ -50,7 +52,7 @@ namespace {
 
 constexpr int TC_BM = 128;          // K rows per tile (UMMA M)
 constexpr int TC_BK = 32;           // fp32 k-elements per step (one 128-byte swizzle row)
-constexpr int TC_THREADS = 512;
+constexpr int TC_THREADS = 640;   // 20 warps: TMA, MMA, TMEM owner, idle, 8 converters, 8 drains
 constexpr int GROUP = 4;            // k-steps accumulated in TMEM before the register flush
 constexpr int NABUF = 4;            // TMEM A-operand buffers (converters run up to 3 steps ahead)
 constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4;  // 16 KB
@@ -72,6 +74,7 @@ struct TcParams {
   int64_t n, row0, rows;
   int family;
   float a2, gscale, s5, diag;  // amplitude^2, log2(e) / (2 l^2), sqrt(5) / l, a^2 + jitter
+  float la2;                   // log2(amplitude^2), folded into the exponent
 };
 
 __device__ __forceinline__ float fast_exp2(float x) {
@@ -105,17 +108,16 @@ __device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
 // Two K entries from packed squared distances (src/kernels.py:40-46), float32.
 template <int FAM>
 __device__ __forceinline__ uint64_t kernel_pair(const TcParams& p, uint64_t r2) {
-  if (FAM == RLD_RBF) {
-    const uint64_t t = mul2(r2, pk(-p.gscale, -p.gscale));
-    return mul2(pk(fast_exp2(pk_lo(t)), fast_exp2(pk_hi(t))), pk(p.a2, p.a2));
+  if (FAM == RLD_RBF) {   // a^2 2^(-g r^2) = 2^(log2 a^2 - g r^2)
+    const uint64_t t = fma2(r2, pk(-p.gscale, -p.gscale), pk(p.la2, p.la2));
+    return pk(fast_exp2(pk_lo(t)), fast_exp2(pk_hi(t)));
   }
   const float a = pk_lo(r2), b = pk_hi(r2);
   const float ra = a > 0.f ? a * rsqrtf(a) : 0.f, rb = b > 0.f ? b * rsqrtf(b) : 0.f;
   const uint64_t u = mul2(pk(ra, rb), pk(p.s5, p.s5));
   const uint64_t poly = fma2(u, fma2(u, pk(1.0f / 3.0f, 1.0f / 3.0f), pk(1.f, 1.f)), pk(1.f, 1.f));
-  const uint64_t t = mul2(u, pk(-1.4426950408889634f, -1.4426950408889634f));
-  const uint64_t e = pk(fast_exp2(pk_lo(t)), fast_exp2(pk_hi(t)));
-  return mul2(mul2(poly, e), pk(p.a2, p.a2));
+  const uint64_t t = fma2(u, pk(-1.4426950408889634f, -1.4426950408889634f), pk(p.la2, p.la2));
+  return mul2(poly, pk(fast_exp2(pk_lo(t)), fast_exp2(pk_hi(t))));
 }
 
 __host__ __device__ __forceinline__ int64_t cta_of_step(int64_t x, int64_t total, int64_t G) {
@@ -214,7 +216,7 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       ptx::mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < NABUF; ++b) {
-      ptx::mbar_init(&afull[b], 4);
+      ptx::mbar_init(&afull[b], 8);
       ptx::mbar_init(&aempty[b], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -234,7 +236,7 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       // ---------------- TMA producer (whole warp walks the ring; one elected lane issues)
       for (StepIter it(beg, end, p.ks, S); it.valid(); it.next()) {
         const int s = it.s;
-        ptx::mbar_wait(&empty[s], it.ph ^ 1);
+        ptx::mbar_wait_sleep(&empty[s], it.ph ^ 1);
         if (ptx::elect_one()) {
           uint8_t* st = smem + (size_t)s * STAGE;
           if (OTF) {
@@ -293,11 +295,13 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         }
         __syncwarp();
       }
-    } else if (warp >= 4 && warp < 8) {
-      // ---------------- converters (warp q owns TMEM lanes 32q..32q+31)
-      const int q = warp - 4;
+    } else if (warp >= 4 && warp < 12) {
+      // ---------------- converters: warp 4 + q + 4h owns TMEM lanes 32q..32q+31 (K rows) and
+      // the 16 k-columns [16h, 16h + 16) of every step
+      const int q = (warp - 4) & 3, hsel = (warp - 4) >> 2;
       const int row = q * 32 + lane;
       const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+      const int e0 = 16 * hsel;
       int cur_tile = -1;
       uint64_t xh2[4] = {0, 0, 0, 0}, xl2[4] = {0, 0, 0, 0};   // this row's point, packed twice (on the fly)
       int64_t grow = 0;
@@ -305,7 +309,7 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         const int s = it.s;
         const int b = it.abuf();
         const int64_t j = it.j;
-        uint32_t hi[32], lo[32];
+        uint32_t hi[16], lo[16];
         if (OTF) {
           if (it.tile != cur_tile) {
             cur_tile = it.tile;
@@ -321,46 +325,65 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             }
           }
           ptx::mbar_wait(&full[s], it.ph);
-          const float* pp = reinterpret_cast<const float*>(smem + (size_t)s * STAGE);   // [8][32]
-          const int64_t j0 = (int64_t)it.kstep * TC_BK;
-          const int64_t dd = grow - j0;                       // column of this row's diagonal entry
-          const int dcol = (dd >= 0 && dd < 32) ? (int)dd : -1;
-          const int64_t nn = p.n - j0;
-          const int ncol = nn < 32 ? (int)nn : 32;            // valid columns in this step
+          const float* pp = reinterpret_cast<const float*>(smem + (size_t)s * STAGE) + e0;   // [8][32] + half
+          const int64_t j0 = (int64_t)it.kstep * TC_BK + e0;
+          // warp-uniform: does this half step hold a diagonal entry of these rows, or columns >= n?
+          const int64_t wrow0 = p.row0 + (int64_t)cur_tile * TC_BM + q * 32;
+          const bool fix = (j0 < wrow0 + 32 && j0 + 16 > wrow0) || (j0 + 16 > p.n);
           const uint64_t neg1 = pk(-1.f, -1.f);
+          if (p.debug == 6) {   // profiling: skip the generation math
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            uint64_t r2 = 0;
+            for (int e = 0; e < 16; ++e) hi[e] = lo[e] = __float_as_uint(pp[e]);
+          } else
+#pragma unroll
+          for (int e = 0; e < 16; e += 4) {
+            uint64_t r2a = 0, r2b = 0;   // entries (e, e+1) and (e+2, e+3)
 #pragma unroll
             for (int k = 0; k < DIM; ++k) {
-              const uint64_t ch = *reinterpret_cast<const uint64_t*>(pp + k * 32 + e);
-              const uint64_t cl = *reinterpret_cast<const uint64_t*>(pp + (4 + k) * 32 + e);
-              const uint64_t dk = add2(fma2(ch, neg1, xh2[k]), fma2(cl, neg1, xl2[k]));  // (xh-ch)+(xl-cl)
-              r2 = fma2(dk, dk, r2);
+              const uint4 ch = *reinterpret_cast<const uint4*>(pp + k * 32 + e);
+              const uint4 cl = *reinterpret_cast<const uint4*>(pp + (4 + k) * 32 + e);
+              const uint64_t cha = (uint64_t)ch.x | ((uint64_t)ch.y << 32), chb = (uint64_t)ch.z | ((uint64_t)ch.w << 32);
+              const uint64_t cla = (uint64_t)cl.x | ((uint64_t)cl.y << 32), clb = (uint64_t)cl.z | ((uint64_t)cl.w << 32);
+              const uint64_t da = add2(fma2(cha, neg1, xh2[k]), fma2(cla, neg1, xl2[k]));  // (xh-ch)+(xl-cl)
+              const uint64_t db = add2(fma2(chb, neg1, xh2[k]), fma2(clb, neg1, xl2[k]));
+              r2a = fma2(da, da, r2a);
+              r2b = fma2(db, db, r2b);
             }
-            const uint64_t kv = kernel_pair<FAM>(p, r2);
-            float v0 = pk_lo(kv), v1 = pk_hi(kv);
-            v0 = (e == dcol) ? p.diag : (e < ncol ? v0 : 0.f);
-            v1 = (e + 1 == dcol) ? p.diag : (e + 1 < ncol ? v1 : 0.f);
-            const uint32_t u0 = __float_as_uint(v0), u1 = __float_as_uint(v1);
-            if (MODE == 3) {
-              const uint32_t h0 = u0 & 0xFFFFE000u, h1 = u1 & 0xFFFFE000u;
-              hi[e] = h0;
-              hi[e + 1] = h1;
-              const uint64_t l2 = add2(pk(v0, v1), fma2(pk(__uint_as_float(h0), __uint_as_float(h1)), neg1, 0));
-              lo[e] = (uint32_t)l2;
-              lo[e + 1] = (uint32_t)(l2 >> 32);
-            } else {
-              hi[e] = u0;
-              hi[e + 1] = u1;
+            uint64_t kv[2] = {kernel_pair<FAM>(p, r2a), kernel_pair<FAM>(p, r2b)};
+            if (fix) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                float v0 = pk_lo(kv[h]), v1 = pk_hi(kv[h]);
+                const int64_t c0 = j0 + e + 2 * h;
+                v0 = (c0 == grow) ? p.diag : (c0 < p.n ? v0 : 0.f);
+                v1 = (c0 + 1 == grow) ? p.diag : (c0 + 1 < p.n ? v1 : 0.f);
+                kv[h] = pk(v0, v1);
+              }
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t u0 = (uint32_t)kv[h], u1 = (uint32_t)(kv[h] >> 32);
+              const int ee = e + 2 * h;
+              if (MODE == 3) {
+                const uint32_t h0 = u0 & 0xFFFFE000u, h1 = u1 & 0xFFFFE000u;
+                hi[ee] = h0;
+                hi[ee + 1] = h1;
+                const uint64_t l2 = fma2((uint64_t)h0 | ((uint64_t)h1 << 32), neg1, kv[h]);   // v - hi (exact)
+                lo[ee] = (uint32_t)l2;
+                lo[ee + 1] = (uint32_t)(l2 >> 32);
+              } else {
+                hi[ee] = u0;
+                hi[ee + 1] = u1;
+              }
             }
           }
         } else {
           ptx::mbar_wait(&full[s], it.ph);
           const uint8_t* rowp = smem + (size_t)s * STAGE + row * 128;
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (row & 7)) << 4));
+          for (int c = 0; c < 4; ++c) {
+            const int cc = 4 * hsel + c;   // 16-byte chunk of the 128-byte row
+            const float4 v = *reinterpret_cast<const float4*>(rowp + ((cc ^ (row & 7)) << 4));
             const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -377,22 +400,22 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         }
         if (j >= NABUF) ptx::mbar_wait(&aempty[b], (uint32_t)(((j / NABUF) - 1) & 1));
         ptx::tc_fence_after();
-        const uint32_t ta = tmem + lane_base + A_COL0 + ASTRIDE * b;
+        const uint32_t ta = tmem + lane_base + A_COL0 + ASTRIDE * b + e0;
         if (p.debug != 1) {
-          ptx::tmem_st_32x32b_x32(ta, hi);
-          if (MODE == 3) ptx::tmem_st_32x32b_x32(ta + 32, lo);
+          ptx::tmem_st_32x32b_x16(ta, hi);
+          if (MODE == 3) ptx::tmem_st_32x32b_x16(ta + 32, lo);
         }
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&afull[b]);
       }
-    } else if (warp >= 8) {
-      // ---------------- accumulator drain: warp 8 + q + 4h owns TMEM lanes 32q..32q+31 and
+    } else if (warp >= 12) {
+      // ---------------- accumulator drain: warp 12 + q + 4h owns TMEM lanes 32q..32q+31 and
       // result columns [h NT/2, (h+1) NT/2); finished groups are added to fp32 registers
       // (round-to-nearest), a finished segment is stored to the partial buffer
       constexpr int HALF = NT / 2;
-      const int q = (warp - 8) & 3, hsel = (warp - 8) >> 2;
+      const int q = (warp - 12) & 3, hsel = (warp - 12) >> 2;
       const int row = q * 32 + lane;
       const uint32_t lane_base = (uint32_t)(q * 32) << 16;
       const int c_base = hsel * HALF;
@@ -400,11 +423,15 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
 #pragma unroll
       for (int c = 0; c < HALF; ++c) acc[c] = 0.f;
       int64_t gi = -1;
-      for (StepIter it(beg, end, p.ks, 1); it.valid(); it.next()) {
-        if (it.group_start()) ++gi;
-        if (!it.group_end()) continue;
+      int tile = (int)(beg / p.ks);
+      int64_t seg_lo = beg;
+      while (seg_lo < end) {
+        const int64_t seg_hi = std::min<int64_t>(end, (int64_t)(tile + 1) * p.ks);
+        for (int64_t gs = seg_lo; gs < seg_hi; gs += GROUP) {
+        ++gi;
+        const bool seg_end = gs + GROUP >= seg_hi;
         const int buf = (int)(gi & 1);
-        ptx::mbar_wait(&accfull[buf], (uint32_t)((gi >> 1) & 1));
+        ptx::mbar_wait_sleep(&accfull[buf], (uint32_t)((gi >> 1) & 1));
         ptx::tc_fence_after();
 #pragma unroll
         for (int c0 = 0; c0 < HALF; c0 += 16) {
@@ -425,15 +452,18 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&accempty[buf]);
-        if (it.seg_end()) {
-          const int seg = (int)(cta - cta_of_step((int64_t)it.tile * p.ks, p.total, G));
-          float* P = partial + ((size_t)it.tile * p.segs + seg) * (size_t)NT * TC_BM;
+        if (seg_end) {
+          const int seg = (int)(cta - cta_of_step((int64_t)tile * p.ks, p.total, G));
+          float* P = partial + ((size_t)tile * p.segs + seg) * (size_t)NT * TC_BM;
 #pragma unroll
           for (int c = 0; c < HALF; ++c) {
             P[(size_t)(c_base + c) * TC_BM + row] = acc[c];
             acc[c] = 0.f;
           }
         }
+        }
+        seg_lo = seg_hi;
+        ++tile;
       }
     }
   }
@@ -641,6 +671,7 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
   p.gscale = (float)(op.kp.inv_2l2 * 1.4426950408889634);
   p.s5 = (float)op.kp.s5_over_l;
   p.diag = (float)op.kp.diag;
+  p.la2 = (float)std::log2(op.kp.a2);
   p.total = total;
   p.ks = ks;
   p.tiles = tiles;
