@@ -104,10 +104,10 @@ typedef struct rld_config {
   uint64_t omega_key[4];  /* keys of streams (seed,(1,0)) and (seed,(1,1))    -- src/precond.py:183 */
 } rld_config;
 
-/* Optional injected random inputs (parity mode).  NULL -> generated on the
- * device from the Philox keys in rld_config, bit-identical to numpy's stream
- * for Rademacher probes; Gaussian rows must be injected until the device
- * ziggurat lands (rld_logdet returns RLD_ERR_NOT_SUPPORTED otherwise). */
+/* Optional injected random inputs.  NULL -> generated on the device from the
+ * Philox keys in rld_config, reproducing numpy's streams: Rademacher probes
+ * bit-identically, Gaussian rows (sketch, Gaussian probes) with numpy's
+ * ziggurat (rld_normal). */
 typedef struct rld_inputs {
   const double* probes;   /* s x n */
   const double* omega0;   /* w x n, attempt 0 */
@@ -171,6 +171,11 @@ int rld_kv_apply(rld_handle* h, int64_t m, const double* V, double* Y);
 /* Rng(seed).child(...).rademacher((rows, n)) -- src/linalg.py:84-85, on the
  * device from the stream's Philox key; `out` is device float64, rows x n. */
 int rld_rademacher(rld_handle* h, const uint64_t key[2], int64_t rows, int64_t n, double* out);
+
+/* Rng(...).normal((rows, n)) -- src/linalg.py:81-82: numpy's Generator.standard_normal
+ * (256-layer ziggurat over Philox4x64) reproduced on the device from the stream's key;
+ * `out` is device float64, rows x n. */
+int rld_normal(rld_handle* h, const uint64_t key[2], int64_t rows, int64_t n, double* out);
 
 /* exact_logdet(M) -- src/estimators.py:125-129: Cholesky log det of the
  * resident problem's K in float64 on the device. */

@@ -35,7 +35,7 @@ PRECOND_RAND_SVD, PRECOND_IDENTITY, PRECOND_DIAGONAL = 0, 1, 2
 EXPORTS = (
     "rld_abi_version", "rld_create", "rld_destroy", "rld_last_error", "rld_logdet", "rld_prepare",
     "rld_logdet_resident", "rld_build_covariance", "rld_kv_apply", "rld_rademacher", "rld_exact_logdet",
-    "rld_nccl_unique_id", "rld_stream",
+    "rld_nccl_unique_id", "rld_stream", "rld_normal",
 )
 
 
@@ -100,6 +100,7 @@ def load() -> C.CDLL:
         lib.rld_build_covariance.argtypes = [H, C.POINTER(Problem), C.c_void_p, C.c_int32]
         lib.rld_kv_apply.argtypes = [H, C.c_int64, C.c_void_p, C.c_void_p]
         lib.rld_rademacher.argtypes = [H, C.POINTER(C.c_uint64 * 2), C.c_int64, C.c_int64, C.c_void_p]
+        lib.rld_normal.argtypes = [H, C.POINTER(C.c_uint64 * 2), C.c_int64, C.c_int64, C.c_void_p]
         lib.rld_exact_logdet.argtypes = [H, C.POINTER(C.c_double)]
         lib.rld_nccl_unique_id.argtypes = [C.c_void_p]
         lib.rld_stream.argtypes = [H]

@@ -98,7 +98,7 @@ struct Work {
   DevBuf x, p, pp, u, w, KX, T, Tg;
   DevBuf scal;     // small scalars / per-probe arrays
   DevBuf ints;     // flags, info, live, size, kept
-  DevBuf scratch, scratch2, solver_work;
+  DevBuf scratch, scratch2, solver_work, rng_scratch;
   KvWorkspace kv;
 };
 
@@ -419,13 +419,14 @@ PrecondOut build_preconditioner(rld_handle* h, const rld_config* c, const rld_in
   for (int attempt = 0; attempt < 2; ++attempt) {
     out.attempts = attempt + 1;
     const double* om = attempt == 0 ? in->omega0 : in->omega1;
-    if (!om)
-      fail(RLD_ERR_NOT_SUPPORTED, attempt == 0 ? "sketch rows must be injected (device Gaussian stream not built yet)"
-                                               : "sketch rows for attempt 1 must be injected (RankDeficient retry)");
+    const uint64_t* okey = c->omega_key + 2 * attempt;   // stream (seed, (1, attempt))
     int hflags = 0;
     for (int householder = 0; householder < 2; ++householder) {
-      RLD_CUDA(cudaMemcpyAsync(Y, om, sizeof(double) * w * n,
-                               in->memory == RLD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+      if (om)
+        RLD_CUDA(cudaMemcpyAsync(Y, om, sizeof(double) * w * n,
+                                 in->memory == RLD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+      else  // numpy-exact Gaussian sketch rows, generated on the device (src/precond.py:183)
+        normal_rows(okey, w, n, 0, n, n, Y, wk.rng_scratch, wk.ints.as<int>() + 5, st);
       RLD_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), st));
       for (int it = 0; it < c->precond_iters; ++it) {
         const bool last = it + 1 == c->precond_iters;
@@ -543,8 +544,8 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
     load_rows(h, in->probes, in->memory, s, Zp);
   } else if (c->probe_kind == RLD_RADEMACHER) {
     rademacher_rows(c->probe_key, s, n, r.row0, nl, nl, Zp, st);
-  } else {
-    fail(RLD_ERR_NOT_SUPPORTED, "Gaussian probes must be injected (device Gaussian stream not built yet)");
+  } else {  // numpy-exact Gaussian probes on the device (src/probes.py:33-34)
+    normal_rows(c->probe_key, s, n, r.row0, nl, nl, Zp, wk.rng_scratch, wk.ints.as<int>() + 5, st);
   }
 
   // ---- Lanczos state
@@ -644,6 +645,7 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
   if (hi[0] & RLD_FLAG_NOT_PD) fail(RLD_ERR_NOT_POSITIVE_DEFINITE, "Matrix is not positive definite (inner Cholesky)");
   if (hi[0] & RLD_FLAG_SINGULAR) fail(RLD_ERR_SINGULAR_SHIFTED_SYSTEM, "zero pivot in a shifted tridiagonal solve");
   if (hi[0] & 8) fail(RLD_ERR_INVALID_ARGUMENT, "base diagonal must be strictly positive");
+  if (hi[5]) fail(RLD_ERR_CUDA, "device Gaussian stream generator overflow (flags " + std::to_string(hi[5]) + ")");
   res->logdet_P = hs[0] + hs[1];
   res->trace_term = hs[2];
   res->value = res->logdet_P + res->trace_term;
@@ -812,6 +814,21 @@ int rld_kv_apply(rld_handle* h, int64_t m, const double* V, double* Y) {
     if (h->world != 1) fail(RLD_ERR_NOT_SUPPORTED, "kv_apply is single-GPU");
     kv(h, m, V, Y);
     RLD_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int rld_normal(rld_handle* h, const uint64_t key[2], int64_t rows, int64_t n, double* out) {
+  if (!h) return RLD_ERR_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    if (!key || !out || rows < 0 || n < 0) fail(RLD_ERR_INVALID_ARGUMENT, "bad normal arguments");
+    h->wk.ints.reserve(sizeof(int) * 8);
+    int* f = h->wk.ints.as<int>() + 5;
+    RLD_CUDA(cudaMemsetAsync(f, 0, sizeof(int), h->st));
+    normal_rows(key, rows, n, 0, n, n, out, h->wk.rng_scratch, f, h->st);
+    int hf = 0;
+    RLD_CUDA(cudaMemcpyAsync(&hf, f, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    RLD_CUDA(cudaStreamSynchronize(h->st));
+    if (hf) fail(RLD_ERR_CUDA, "device Gaussian stream generator overflow (flags " + std::to_string(hf) + ")");
   });
 }
 

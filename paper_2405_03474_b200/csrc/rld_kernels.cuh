@@ -53,6 +53,10 @@ void convert_rows_2d(const void* src, int sdt, int64_t lds, double* dst, int64_t
 void sqrt_into(int64_t n, const double* base, double* sqrt_base, int* flags, cudaStream_t st);
 void strided_sum_log(int64_t count, const double* v, int64_t stride, double* out, DevBuf& scratch,
                      cudaStream_t st);
+// rows x n standard normals of numpy stream `key` (Generator(Philox).standard_normal, bit-exact),
+// columns [col0, col0 + ncols) of each row to out (row stride ld); dflags bit set on overflow
+void normal_rows(const uint64_t key[2], int64_t rows, int64_t n, int64_t col0, int64_t ncols, int64_t ld,
+                 double* out, DevBuf& scratch, int* dflags, cudaStream_t st);
 void pad_points(const double* X, int64_t n, int d, float* pts8, cudaStream_t st);
 void diag_of_dense(int64_t rows, int64_t row0, const void* K, int64_t ldk, int dtype, double* d, cudaStream_t st);
 

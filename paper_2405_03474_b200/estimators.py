@@ -12,12 +12,12 @@ Everything below the call runs in ``librld.so`` on the GPU: the rand-SVD
 preconditioner, all-probe Lanczos, the multishift solves and the Hutchinson
 mean.  There is no CPU fallback: a missing library raises.
 
-Random inputs follow the reference's streams exactly (``streams="reference"``):
-probes from ``Rng(seed).child(2)`` and the sketch from
-``Rng(seed).child(1).child(attempt)`` (``src/estimators.py:61-64``,
-``src/precond.py:183``).  Rademacher probes are generated on the GPU from the
-stream's Philox key, bit-identical to numpy; Gaussian rows are drawn by numpy
-on the host and uploaded.
+Random inputs follow the reference's streams exactly: probes from
+``Rng(seed).child(2)`` and the sketch from ``Rng(seed).child(1).child(attempt)``
+(``src/estimators.py:61-64``, ``src/precond.py:183``), regenerated on the GPU
+from the streams' Philox keys -- Rademacher rows bit-identical to numpy, Gaussian
+rows through a device port of numpy's ziggurat.  Explicit ``probes=`` /
+``omega=`` rows may still be injected.
 """
 
 from __future__ import annotations
@@ -119,30 +119,24 @@ def make_config(cfg: EstimatorConfig, n: int) -> N.Config:
 
 
 class _Inputs:
-    """Host-side random rows to inject (kept alive for the duration of a call)."""
+    """Random rows the caller injects explicitly (kept alive for the duration of a
+    call).  By default nothing is injected: the device regenerates the
+    reference's streams itself -- Rademacher probes and Gaussian rows (sketch,
+    Gaussian probes) bit-identical to numpy's Philox / ziggurat streams."""
 
     def __init__(self, cfg: EstimatorConfig, n: int, probes=None, omega=None):
         self.keep = []
         self.struct = N.Inputs()
         self.struct.memory = N.HOST
-        rng = Rng(cfg.seed)
         if probes is not None:
             P = np.ascontiguousarray(np.asarray(probes, dtype=np.float64))
             if P.shape != (cfg.num_probes, n):
                 raise ValueError(f"probes must be {cfg.num_probes} x {n}")
-        elif cfg.probe_kind == "gaussian":
-            P = make_probes("gaussian", cfg.num_probes, n, rng.child(2))
-        else:
-            P = None  # Rademacher: generated on the device from the Philox key
-        if P is not None:
             self.keep.append(P)
             self.struct.probes = P.ctypes.data
-        if cfg.precond.kind == "rand-svd":
+        if omega is not None and cfg.precond.kind == "rand-svd":
             w = _sketch_width(cfg, n)
-            if omega is not None:
-                om = [np.ascontiguousarray(np.asarray(o, dtype=np.float64)) for o in omega]
-            else:
-                om = [rng.child(1).child(0).normal((w, n))]
+            om = [np.ascontiguousarray(np.asarray(o, dtype=np.float64)) for o in omega]
             for o in om:
                 if o.shape != (w, n):
                     raise ValueError(f"sketch rows must be {w} x {n}")
@@ -150,19 +144,16 @@ class _Inputs:
             self.struct.omega0 = om[0].ctypes.data
             if len(om) > 1:
                 self.struct.omega1 = om[1].ctypes.data
-            self._rng, self._w, self._n = rng, w, n
+            self._seed, self._w, self._n = cfg.seed, w, n
 
     def add_retry_sketch(self):
-        o = self._rng.child(1).child(1).normal((self._w, self._n))
+        o = Rng(self._seed).child(1).child(1).normal((self._w, self._n))
         self.keep.append(o)
         self.struct.omega1 = o.ctypes.data
 
 
 def _call_with_retry(call, inputs: _Inputs, handle: N.Handle, what: str):
     rc = call()
-    if rc == N.RLD_ERR_NOT_SUPPORTED and "attempt 1" in handle.last_error() and not inputs.struct.omega1:
-        inputs.add_retry_sketch()   # the RankDeficient retry needs the second sketch stream
-        rc = call()
     handle.check(rc, what)
 
 
