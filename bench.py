@@ -12,9 +12,10 @@ multishift solves + Hutchinson mean) -- the reference's timer scope
 * ``value``: estimates/s with K, the sketch rows and the probes resident in HBM
   (K = 1.07 GB fp32 > 126 MB L2, so every product streams K from HBM), CUDA
   events on the handle's stream around exactly K steps, max over ranks.
-* ``e2e``: the same metric through the public API with host buffers -- every
-  step uploads the points and sketch rows from pinned memory, builds K on the
-  GPU, runs the estimate and reads the result back.
+* ``e2e``: the same metric through the C ABI call the public API makes, with host
+  buffers -- every step uploads the points from pinned memory, builds K on the
+  GPU, regenerates the reference's probe / sketch streams on the GPU, runs the
+  estimate and reads the result back.
 * ``roofline``: the dominant kernel (the K x block product, Lanczos shape),
   timed live with CUDA events; algorithmic bytes = 4 n^2 (K) + 4 n s (operand)
   + 8 n s (result) per launch.
@@ -23,8 +24,12 @@ multishift solves + Hutchinson mean) -- the reference's timer scope
   estimate of the same workload.
 * ``--impl reference``: that CPU implementation is the timed arm.
 
-Multi-GPU (torchrun): each rank runs an independent replica of the workload
-(``"scaling": "weak"``) until the row-sharded NCCL path lands.
+Multi-GPU (torchrun, one process per GPU): by default the rows of K and of every
+n-vector block are sharded across the ranks; one estimate per
+step for the whole job (``"scaling": "strong"``), NCCL all-gather of the direction
+block per Lanczos step and all-reduces of the dot products / Gram matrices.
+``--mode replicas`` instead runs an independent single-GPU estimate per rank
+(``"scaling": "weak"``).
 """
 
 from __future__ import annotations
@@ -61,6 +66,8 @@ def parse():
     ap.add_argument("--algorithm", choices=["r1", "r3", "r5"], default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", choices=["sharded", "replicas"], default="sharded",
+                    help="multi-GPU: row-shard one estimate (default) or run independent replicas")
     return ap.parse_args()
 
 
@@ -245,15 +252,20 @@ def run_ours(args):
     w = min(cfg.precond.rank + 10, n)
     es = 4 if cfg.dtype == "fp32" else 8
 
-    # ---- device-resident: K in HBM, sketch rows in HBM, probes generated on device
-    R = rld.ResidentMatrix(rld.KernelMatrix(wl.spec, wl.points), dtype=cfg.dtype, path="stored")
-    omega_host = Rng(cfg.seed).child(1).child(0).normal((w, n))
-    omega_dev = torch.from_numpy(omega_host).cuda()
+    # ---- device-resident: K in HBM; the probe and sketch streams are regenerated on the
+    # device every estimate (numpy-exact Philox Rademacher / ziggurat Gaussian rows), as the
+    # reference draws them inside its timed region (src/estimators.py:81-83)
+    sharded = world > 1 and args.mode == "sharded"
+    per_step = 1 if sharded else world       # estimates the whole job completes per step
+    R = rld.ResidentMatrix(rld.KernelMatrix(wl.spec, wl.points), dtype=cfg.dtype, path=wl.path, shard=sharded)
+    from paper_2405_03474_b200.parallel import shard_bounds
+    row0, row1 = shard_bounds(n, world, rank) if sharded else (0, n)
+    rows = row1 - row0
     inputs = N.Inputs()
-    inputs.omega0 = omega_dev.data_ptr()
     inputs.memory = N.DEVICE
     stream = torch.cuda.ExternalStream(R.sess.handle.stream)
 
+    clk = ClockSampler(local).__enter__()   # sampling starts before warm-up, covers the timed region
     for _ in range(args.warmup):
         est = R.estimate(cfg, inputs=inputs)
     barrier(world)
@@ -261,7 +273,7 @@ def run_ours(args):
     launches = 0
     products = 0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    if True:
         ev0.record(stream)
         for _ in range(args.steps):
             est = R.estimate(cfg, inputs=inputs)
@@ -269,10 +281,11 @@ def run_ours(args):
             products += est.kv_products
         ev1.record(stream)
         torch.cuda.synchronize()
+    clk.__exit__()
     barrier(world)
     ms = ev0.elapsed_time(ev1)
     ms = max_over_ranks(ms, world)
-    value = world * args.steps / (ms * 1e-3)
+    value = per_step * args.steps / (ms * 1e-3)
     clocks = clk.summary()
     phases = est.phase_ms
 
@@ -289,7 +302,7 @@ def run_ours(args):
     k1.record(stream)
     torch.cuda.synchronize()
     kv_ms = k0.elapsed_time(k1) / reps
-    alg_bytes = es * n * n + 4 * n * s + 8 * n * s
+    alg_bytes = es * rows * n + 4 * n * s + 8 * rows * s
     hbm_peak, _, peak_kind = load_peaks()
     achieved = alg_bytes / (kv_ms * 1e-3) / 1e9
 
@@ -297,12 +310,10 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         pts_pin = torch.from_numpy(np.ascontiguousarray(wl.points)).pin_memory()
-        om_pin = torch.from_numpy(omega_host).pin_memory()
         sess = R.sess
-        prob, keep = sess.problem_for(rld.KernelMatrix(wl.spec, pts_pin), cfg.dtype, "stored")
+        prob, keep = sess.problem_for(rld.KernelMatrix(wl.spec, pts_pin), cfg.dtype, wl.path)
         c = make_config(cfg, n)
         inp = N.Inputs()
-        inp.omega0 = om_pin.data_ptr()
         inp.memory = N.HOST
         per = np.empty(s)
         res = N.Result()
@@ -317,33 +328,37 @@ def run_ours(args):
         barrier(world)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
         for _ in range(args.steps):
             e2e_step()
+        e1.record(stream)
         torch.cuda.synchronize()
-        e2e_s = max_over_ranks(time.perf_counter() - t0, world)
-        e2e = {"value": world * args.steps / e2e_s, "unit": UNIT,
-               "h2d_bytes_per_step": int(pts_pin.numel() * 8 + om_pin.numel() * 8),
-               "d2h_bytes_per_step": int(8 * (s + 3) + 4 * 8)}
+        wall = time.perf_counter() - t0
+        e2e_s = max_over_ranks(e0.elapsed_time(e1) * 1e-3, world)   # device clock, max over ranks
+        e2e = {"value": per_step * args.steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int(pts_pin.numel() * 8),
+               "d2h_bytes_per_step": int(8 * (s + 3) + 4 * 8), "host_wall_s": wall}
         # restore the resident problem for any later use
         del keep
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32" if cfg.dtype == "fp32" else "f64",
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f32" if cfg.dtype == "fp32" else "f64",
         "data": "synthetic",
         "config": {"workload": f"{wl.name}: n={n} {wl.spec.family} d={wl.points.shape[1]} ell={wl.spec.length_scale} "
                                f"noise={wl.spec.jitter} {cfg.algorithm} l={cfg.precond.rank} s={s} "
                                f"{cfg.probe_kind} t={cfg.lanczos_iters} q={cfg.precond.num_iters} stored K "
                                f"({cfg.dtype})",
                    "l2": "inputs larger than L2 (K = %.2f GB)" % (es * n * n / 1e9),
-                   "parallelism": "replicas" if world > 1 else "single"},
+                   "parallelism": (f"rows{world}" if sharded else f"replicas{world}") if world > 1 else "single"},
         "e2e": e2e,
         "gpu_launches": launches,
         "kv_products_per_step": products // max(1, args.steps),
         "phase_ms_last_step": {"precond": phases[1], "lanczos": phases[4], "solves": phases[5]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None, "kernel": "kv_product (Lanczos shape m=s)",
+                     "frac": achieved / hbm_peak, "traffic": None, "kernel": f"kv_product (Lanczos shape m=s, {rows} rows of K)",
                      "kernel_ms": kv_ms, "alg_bytes": alg_bytes, "peak_source": peak_kind},
         "clocks": clocks,
         "estimate": est.value,

@@ -164,8 +164,10 @@ int rld_logdet_resident(rld_handle* h, const rld_config* cfg, const rld_inputs* 
 int rld_build_covariance(rld_handle* h, const rld_problem* problem, void* out, int32_t out_memory);
 
 /* The operator seam `M @ x` of src/estimators.py:72 for a block: Y = V K for the
- * m x n rows V (device, float64), Y m x n (device, float64), using the
- * resident problem and its product arithmetic. */
+ * m x n rows V (device, float64), using the resident problem and its product
+ * arithmetic.  Y (device, float64) is m x n on one GPU; with world_size > 1 it
+ * is this rank's row shard, m x rows (rows of K this rank holds, see
+ * rld_prepare).  Stream-ordered: enqueued on rld_stream(h), not synchronised. */
 int rld_kv_apply(rld_handle* h, int64_t m, const double* V, double* Y);
 
 /* Rng(seed).child(...).rademacher((rows, n)) -- src/linalg.py:84-85, on the

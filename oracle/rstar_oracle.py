@@ -20,7 +20,7 @@ Each function cites the reference file:line it follows.  Differences in
   points with the reference's r^2 = |x|^2 + |y|^2 - 2 x.y formula), which lets
   the oracle run past the n ~ 30k where a dense float64 K stops fitting in RAM.
 
-Pinning: ``tests/test_oracle_golden.py`` checks this module against golden
+Pinning: ``tests/test_oracle.py`` checks this module against golden
 vectors produced by the unmodified reference (``tests/golden/make_golden.py``)
 to <= 1e-10 relative on well-posed configurations, and bit-for-bit on the RNG
 streams.

@@ -99,6 +99,8 @@ struct Work {
   DevBuf scal;     // small scalars / per-probe arrays
   DevBuf ints;     // flags, info, live, size, kept
   DevBuf scratch, scratch2, solver_work, rng_scratch;
+  DevBuf gsend, grecv;   // row-shard all-gather staging
+  DevBuf flagbuf;        // flag OR over ranks
   KvWorkspace kv;
 };
 
@@ -154,6 +156,26 @@ void allreduce_sum(rld_handle* h, double* buf, int64_t count) {
   if (h->world == 1 || count <= 0) return;
   ncclResult_t r = ncclAllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, h->comm, h->st);
   if (r != ncclSuccess) fail(RLD_ERR_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+}
+
+// Bitwise OR of the host copies of the status flags over ranks.  Flags raised on
+// local rows only (BAD_BASE, generator overflow) must stop every rank alike.
+void allreduce_flags(rld_handle* h, int* hflags, int count) {
+  if (h->world == 1) return;
+  std::vector<int> bits(32 * count);
+  for (int i = 0; i < count; ++i)
+    for (int b = 0; b < 32; ++b) bits[32 * i + b] = (hflags[i] >> b) & 1;
+  DevBuf& d = h->wk.flagbuf;
+  d.reserve(sizeof(int) * bits.size());
+  RLD_CUDA(cudaMemcpyAsync(d.ptr, bits.data(), sizeof(int) * bits.size(), cudaMemcpyHostToDevice, h->st));
+  ncclResult_t r = ncclAllReduce(d.ptr, d.ptr, bits.size(), ncclInt32, ncclMax, h->comm, h->st);
+  if (r != ncclSuccess) fail(RLD_ERR_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+  RLD_CUDA(cudaMemcpyAsync(bits.data(), d.ptr, sizeof(int) * bits.size(), cudaMemcpyDeviceToHost, h->st));
+  RLD_CUDA(cudaStreamSynchronize(h->st));
+  for (int i = 0; i < count; ++i) {
+    hflags[i] = 0;
+    for (int b = 0; b < 32; ++b) hflags[i] |= bits[32 * i + b] << b;
+  }
 }
 
 // ----------------------------------------------------------------------------
@@ -268,13 +290,29 @@ void load_rows(rld_handle* h, const double* src, int memory, int64_t m, double* 
 }
 
 // m x rows_local (local rows layout) -> m x n full rows on every rank
+// Row shards: rank g owns columns [g L, g L + rows_g) of every n-vector, L = ceil(n / G).
+// The gather packs the local m x rows block into an m x L send buffer (zero pad),
+// ncclAllGather's it into [G][m][L], and a relayout kernel writes the m x n rows
+// layout every K x block product reads (the one per-iteration exchange).
 void gather_rows(rld_handle* h, const double* local, int64_t m, double* full) {
   const Resident& r = h->res;
   if (h->world == 1) {
     if (local != full) copy_doubles(m * r.n, local, full, h->st);
     return;
   }
-  fail(RLD_ERR_NOT_SUPPORTED, "multi-GPU row gather not built yet");
+  const int64_t L = ceil_div(r.n, h->world);
+  Work& wk = h->wk;
+  wk.gsend.reserve(sizeof(double) * m * L);
+  wk.grecv.reserve(sizeof(double) * m * L * h->world);
+  double* snd = wk.gsend.as<double>();
+  double* rcv = wk.grecv.as<double>();
+  if (r.rows < L) RLD_CUDA(cudaMemsetAsync(snd, 0, sizeof(double) * m * L, h->st));
+  if (r.rows > 0)
+    RLD_CUDA(cudaMemcpy2DAsync(snd, sizeof(double) * L, local, sizeof(double) * r.rows, sizeof(double) * r.rows, m,
+                               cudaMemcpyDeviceToDevice, h->st));
+  ncclResult_t e = ncclAllGather(snd, rcv, (size_t)(m * L), ncclDouble, h->comm, h->st);
+  if (e != ncclSuccess) fail(RLD_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(e));
+  relayout_gathered(rcv, h->world, m, L, r.n, full, h->st);
 }
 
 // Y (m x rows) = V (m x n full) K^T restricted to the local rows
@@ -642,6 +680,12 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
   if (res->per_probe)
     RLD_CUDA(cudaMemcpyAsync(res->per_probe, per_probe, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
   RLD_CUDA(cudaStreamSynchronize(st));
+  {
+    int fl[2] = {hi[0], hi[5]};
+    allreduce_flags(h, fl, 2);
+    hi[0] = fl[0];
+    hi[5] = fl[1];
+  }
   if (hi[0] & RLD_FLAG_NOT_PD) fail(RLD_ERR_NOT_POSITIVE_DEFINITE, "Matrix is not positive definite (inner Cholesky)");
   if (hi[0] & RLD_FLAG_SINGULAR) fail(RLD_ERR_SINGULAR_SHIFTED_SYSTEM, "zero pivot in a shifted tridiagonal solve");
   if (hi[0] & 8) fail(RLD_ERR_INVALID_ARGUMENT, "base diagonal must be strictly positive");
@@ -811,9 +855,7 @@ int rld_kv_apply(rld_handle* h, int64_t m, const double* V, double* Y) {
   return guarded(h, [&] {
     if (!h->res.ready) fail(RLD_ERR_INVALID_ARGUMENT, "no resident problem");
     if (m < 1 || !V || !Y) fail(RLD_ERR_INVALID_ARGUMENT, "bad kv_apply arguments");
-    if (h->world != 1) fail(RLD_ERR_NOT_SUPPORTED, "kv_apply is single-GPU");
-    kv(h, m, V, Y);
-    RLD_CUDA(cudaStreamSynchronize(h->st));
+    kv(h, m, V, Y);   // stream-ordered on rld_stream(h)
   });
 }
 

@@ -57,6 +57,8 @@ void strided_sum_log(int64_t count, const double* v, int64_t stride, double* out
 // columns [col0, col0 + ncols) of each row to out (row stride ld); dflags bit set on overflow
 void normal_rows(const uint64_t key[2], int64_t rows, int64_t n, int64_t col0, int64_t ncols, int64_t ld,
                  double* out, DevBuf& scratch, int* dflags, cudaStream_t st);
+// [G][m][L] (all-gathered shards) -> m x n rows, n <= G L
+void relayout_gathered(const double* src, int G, int64_t m, int64_t L, int64_t n, double* dst, cudaStream_t st);
 void pad_points(const double* X, int64_t n, int d, float* pts8, cudaStream_t st);
 void diag_of_dense(int64_t rows, int64_t row0, const void* K, int64_t ldk, int dtype, double* d, cudaStream_t st);
 

@@ -585,6 +585,26 @@ __global__ void pad_points_kernel(const double* __restrict__ X, int64_t n, int d
 }
 }  // namespace
 
+namespace {
+__global__ void relayout_kernel(const double* __restrict__ src, int64_t m, int64_t L, int64_t n,
+                                double* __restrict__ dst) {
+  const int64_t total = m * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / n, j = e % n;
+    const int64_t g = j / L, jj = j - g * L;
+    dst[e] = src[(g * m + c) * L + jj];
+  }
+}
+}  // namespace
+
+void relayout_gathered(const double* src, int G, int64_t m, int64_t L, int64_t n, double* dst, cudaStream_t st) {
+  (void)G;
+  if (m * n <= 0) return;
+  relayout_kernel<<<grid_for(m * n), 256, 0, st>>>(src, m, L, n, dst);
+  RLD_LAUNCH_CHECK();
+}
+
 void pad_points(const double* X, int64_t n, int d, float* pts8, cudaStream_t st) {
   pad_points_kernel<<<(unsigned)ceil_div(4 * n, 256), 256, 0, st>>>(X, n, d, pts8);
   RLD_LAUNCH_CHECK();

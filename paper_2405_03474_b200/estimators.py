@@ -212,11 +212,17 @@ class ResidentMatrix:
     that repeated estimates touch no host memory: the device-resident form
     ``bench.py`` times.  Owns its own librld handle."""
 
-    def __init__(self, M, dtype: str = "fp64", path: str = "auto", device: int | None = None):
+    def __init__(self, M, dtype: str = "fp64", path: str = "auto", device: int | None = None,
+                 shard: bool | None = None):
+        """``shard`` (default: True under torch.distributed with world size > 1)
+        joins the process-wide NCCL session and keeps only this rank's rows of K;
+        ``shard=False`` gives an independent single-GPU replica."""
         from ._session import Session, dist_world, session
 
         rank, world, local = dist_world()
-        if world > 1:
+        if shard is None:
+            shard = world > 1
+        if shard and world > 1:
             self.sess = session()
         else:
             self.sess = Session(local if device is None else device)
@@ -245,14 +251,34 @@ class ResidentMatrix:
         return _result(res, per, start)
 
     def kv_apply(self, V):
-        """Y = V K for device float64 rows V (m x n torch CUDA tensor)."""
+        """Y = V K for device float64 rows V (m x n torch CUDA tensor).  With a
+        row-sharded handle (world size > 1) Y holds this rank's columns only,
+        m x rows.  Ordered after torch's current stream and before its later work."""
         import torch
 
+        from .parallel import shard_bounds
+
         V = V.detach().to(torch.float64).contiguous()
-        Y = torch.empty_like(V)
+        if V.ndim != 2 or V.shape[1] != self.n:
+            raise ValueError(f"V must be m x {self.n}")
+        r0, r1 = shard_bounds(self.n, self.sess.world_size, self.sess.rank)
+        Y = torch.empty((V.shape[0], r1 - r0), dtype=torch.float64, device=V.device)
+        cur = torch.cuda.current_stream(V.device)
+        ext = self._ext_stream()
+        ext.wait_stream(cur)
         self.sess.handle.check(self.sess.lib.rld_kv_apply(self.sess.handle.ptr, V.shape[0], V.data_ptr(),
                                                           Y.data_ptr()), "rld_kv_apply")
+        V.record_stream(ext)
+        Y.record_stream(ext)
+        cur.wait_stream(ext)
         return Y
+
+    def _ext_stream(self):
+        import torch
+
+        if getattr(self, "_ext", None) is None:
+            self._ext = torch.cuda.ExternalStream(self.sess.handle.stream)
+        return self._ext
 
     def exact_logdet(self) -> float:
         v = C.c_double()
