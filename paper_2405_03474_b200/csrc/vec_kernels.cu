@@ -370,20 +370,39 @@ __global__ void top_eigvecs_kernel(int w, int k, const double* __restrict__ V, c
 }
 
 // base = max(diag - sum_r A^2, floor), sqrt_base, At = A / sqrt_base  (A col-major n x k)
-__global__ void base_kernel(int64_t n, int k, const double* __restrict__ diag, double floor_v,
-                            double* __restrict__ A, double* __restrict__ base, double* __restrict__ sqrt_base) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+// 32 rows per block, the 8 warps split the k columns; lanes walk adjacent rows (coalesced)
+__global__ void __launch_bounds__(256) base_kernel(int64_t n, int k, const double* __restrict__ diag, double floor_v,
+                                                   double* __restrict__ A, double* __restrict__ base,
+                                                   double* __restrict__ sqrt_base) {
+  __shared__ double part[8][33];
+  __shared__ double sbs[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * 32 + lane;
   double s = 0.0;
-  for (int r = 0; r < k; ++r) {
-    const double a = A[(int64_t)r * n + i];
-    s = fma(a, a, s);
+  if (i < n)
+    for (int r = wid; r < k; r += 8) {
+      const double a = A[(int64_t)r * n + i];
+      s = fma(a, a, s);
+    }
+  part[wid][lane] = s;
+  __syncthreads();
+  if (wid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += part[w][lane];
+    double sb = 1.0;
+    if (i < n) {
+      const double b = fmax(diag[i] - t, floor_v);
+      sb = sqrt(b);
+      base[i] = b;
+      sqrt_base[i] = sb;
+    }
+    sbs[lane] = sb;
   }
-  const double b = fmax(diag[i] - s, floor_v);
-  const double sb = sqrt(b);
-  base[i] = b;
-  sqrt_base[i] = sb;
-  for (int r = 0; r < k; ++r) A[(int64_t)r * n + i] /= sb;
+  __syncthreads();
+  if (i < n) {
+    const double inv = sbs[lane];
+    for (int r = wid; r < k; r += 8) A[(int64_t)r * n + i] /= inv;
+  }
 }
 
 __global__ void __launch_bounds__(RB) sum_log_partial(int64_t n, const double* __restrict__ v, int64_t chunk,
@@ -411,11 +430,14 @@ __global__ void add_identity_kernel(int k, double* __restrict__ C) {
 // 2 sum log diag(L) of the inner Cholesky (src/precond.py:77-80); NotPD on failure
 __global__ void chol_logdet_kernel(int k, const double* __restrict__ L, const int* __restrict__ info,
                                    double* __restrict__ out, int* __restrict__ flags) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  if (*info != 0) atomicOr(flags, RLD_FLAG_NOT_PD);
+  // one warp: lane-strided logs of the diagonal, then a shuffle reduction
   double s = 0.0;
-  for (int i = 0; i < k; ++i) s += log(L[(int64_t)i * k + i]);
-  *out = 2.0 * s;
+  for (int i = threadIdx.x; i < k; i += 32) s += log(L[(int64_t)i * k + i]);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (threadIdx.x == 0) {
+    if (*info != 0) atomicOr(flags, RLD_FLAG_NOT_PD);
+    *out = 2.0 * s;
+  }
 }
 
 // keep filter and spectral factors of (I + At^T At) (src/precond.py:96-99):
@@ -543,7 +565,7 @@ void top_eigvecs(int w, int k, const double* V, const double* theta, double* Vto
 }
 void precond_base(int64_t n, int k, const double* diag, double floor_v, double* A, double* base, double* sqrt_base,
                   cudaStream_t st) {
-  base_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, k, diag, floor_v, A, base, sqrt_base);
+  base_kernel<<<(unsigned)ceil_div(n, 32), 256, 0, st>>>(n, k, diag, floor_v, A, base, sqrt_base);
   RLD_LAUNCH_CHECK();
 }
 void sum_log(int64_t n, const double* v, double* out, DevBuf& scratch, cudaStream_t st) {

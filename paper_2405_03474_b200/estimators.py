@@ -268,8 +268,9 @@ class ResidentMatrix:
         ext.wait_stream(cur)
         self.sess.handle.check(self.sess.lib.rld_kv_apply(self.sess.handle.ptr, V.shape[0], V.data_ptr(),
                                                           Y.data_ptr()), "rld_kv_apply")
-        V.record_stream(ext)
-        Y.record_stream(ext)
+        # V and Y belong to torch's current stream; it waits for the product here, so
+        # no later reuse of their blocks can overtake it (no record_stream: the handle's
+        # stream may be destroyed before the tensors are freed)
         cur.wait_stream(ext)
         return Y
 
