@@ -41,6 +41,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
+#include <vector>
+#include <cstdio>
 
 #include "rld_device.cuh"
 #include "rld_internal.cuh"
@@ -54,7 +56,7 @@ constexpr int TC_BM = 128;          // K rows per tile (UMMA M)
 constexpr int TC_BK = 32;           // fp32 k-elements per step (one 128-byte swizzle row)
 constexpr int TC_THREADS = 640;   // 20 warps: TMA, MMA, TMEM owner, idle, 8 converters, 8 drains
 constexpr int GROUP = 4;            // k-steps accumulated in TMEM before the register flush
-constexpr int NABUF = 4;            // TMEM A-operand buffers (converters run up to 3 steps ahead)
+constexpr int NABUF_MAX = 8;        // pipeline stages = TMEM A-operand buffers: as many as the 512 columns leave (<= 8)
 constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4;  // 16 KB
 
 // CTA b works on column pass b % npass over stream-K range b / npass.
@@ -67,19 +69,29 @@ struct TcParams {
   int stages;
   uint32_t tmem_cols;
   float* partial;   // [npass][tiles][segs][NT][128]
-  int debug;        // profiling knob (RLD_TC_DEBUG): 1 = skip A stores, 2 = skip MMAs, 4 = skip A loads
+  int wait_mode;    // producer / drain wait strategy (RLD_TC_WAIT, see ptx::mbar_wait_idle)
+  uint32_t wait_ns;  // back-off of wait_mode 1 (RLD_TC_WAIT_NS)
+  unsigned long long* prof;   // RLD_TC_PROFILE: per-CTA cycle counters [grid][16], else null
+  int debug;        // profiling bitmask (RLD_TC_DEBUG): 1 skip A stores, 2 skip MMAs, 4 skip K-tile loads,
+                    // 8 skip tile generation math, 16 converters only arrive, 32 drains skip TMEM loads
   // on-the-fly kernel tiles (src/kernels.py:40-46, 72)
   const float* pts;  // [8][ldp] float32: coordinate rows x,y,z,w (hi) then x,y,z,w (lo)
   int64_t ldp;
   int64_t n, row0, rows;
   int family;
-  float a2, gscale, s5, diag;  // amplitude^2, log2(e) / (2 l^2), sqrt(5) / l, a^2 + jitter
+  float diag;                  // a^2 + jitter
   float la2;                   // log2(amplitude^2), folded into the exponent
 };
 
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float fast_sqrt(float x) {   // MUFU; sqrt(0) = 0
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
@@ -105,16 +117,16 @@ __device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
   return d;
 }
 
-// Two K entries from packed squared distances (src/kernels.py:40-46), float32.
+// Two K entries from packed scaled squared distances (src/kernels.py:40-46), float32:
+// RBF a^2 2^(-r2') with r2' = r^2 log2(e) / (2 l^2); Matern-5/2 a^2 (1 + u + u^2/3) e^-u
+// with u = sqrt(r2') = sqrt(5) r / l.  a^2 is folded into the exponent (la2 = log2 a^2).
 template <int FAM>
 __device__ __forceinline__ uint64_t kernel_pair(const TcParams& p, uint64_t r2) {
-  if (FAM == RLD_RBF) {   // a^2 2^(-g r^2) = 2^(log2 a^2 - g r^2)
-    const uint64_t t = fma2(r2, pk(-p.gscale, -p.gscale), pk(p.la2, p.la2));
+  if (FAM == RLD_RBF) {
+    const uint64_t t = fma2(r2, pk(-1.f, -1.f), pk(p.la2, p.la2));
     return pk(fast_exp2(pk_lo(t)), fast_exp2(pk_hi(t)));
   }
-  const float a = pk_lo(r2), b = pk_hi(r2);
-  const float ra = a > 0.f ? a * rsqrtf(a) : 0.f, rb = b > 0.f ? b * rsqrtf(b) : 0.f;
-  const uint64_t u = mul2(pk(ra, rb), pk(p.s5, p.s5));
+  const uint64_t u = pk(fast_sqrt(pk_lo(r2)), fast_sqrt(pk_hi(r2)));
   const uint64_t poly = fma2(u, fma2(u, pk(1.0f / 3.0f, 1.0f / 3.0f), pk(1.f, 1.f)), pk(1.f, 1.f));
   const uint64_t t = fma2(u, pk(-1.4426950408889634f, -1.4426950408889634f), pk(p.la2, p.la2));
   return mul2(poly, pk(fast_exp2(pk_lo(t)), fast_exp2(pk_hi(t))));
@@ -131,8 +143,11 @@ struct StepIter {
   int64_t g, end, j;
   int ks, kstep, tile, gpos, s, S;
   uint32_t ph;
-  __device__ __forceinline__ StepIter(int64_t beg, int64_t end_, int ks_, int S_)
-      : g(beg), end(end_), j(0), ks(ks_), gpos(0), s(0), S(S_), ph(0) {
+  int ab, NA;            // TMEM A buffer of step j (j % NA)
+  int ls;                // stage of step j - NA (valid for j >= NA) and its phase parity
+  uint32_t lph;
+  __device__ __forceinline__ StepIter(int64_t beg, int64_t end_, int ks_, int S_, int NA_)
+      : g(beg), end(end_), j(0), ks(ks_), gpos(0), s(0), S(S_), ph(0), ab(0), NA(NA_), ls(0), lph(0) {
     tile = (int)(beg / ks_);
     kstep = (int)(beg - (int64_t)tile * ks_);
   }
@@ -140,8 +155,6 @@ struct StepIter {
   __device__ __forceinline__ bool group_start() const { return gpos == 0; }
   __device__ __forceinline__ bool seg_end() const { return g + 1 == end || kstep + 1 == ks; }
   __device__ __forceinline__ bool group_end() const { return seg_end() || gpos + 1 == GROUP; }
-  __device__ __forceinline__ int abuf() const { return (int)(j & (NABUF - 1)); }
-  __device__ __forceinline__ uint32_t aphase() const { return (uint32_t)((j / NABUF) & 1); }
   __device__ __forceinline__ void next() {
     gpos = group_end() ? 0 : gpos + 1;
     ++g;
@@ -154,14 +167,91 @@ struct StepIter {
       s = 0;
       ph ^= 1;
     }
+    if (++ab == NA) ab = 0;
+    if (j > NA && ++ls == S) {   // the lagged ring starts at stage 0, parity 0 when j == NA
+      ls = 0;
+      lph ^= 1;
+    }
   }
 };
 
+// 16 on-the-fly K entries of one converter thread: its row x 16 column points of
+// the stage (columns [e0, e0 + 16) of the k-step), split into tf32 hi + lo.
+// Coordinates arrive pre-scaled in float32 (x sqrt(5)/l for Matern-5/2, x
+// sqrt(log2(e)/(2 l^2)) for RBF), so r2 is the kernel's argument directly.  FIX:
+// the half step holds a diagonal entry (a^2 + jitter, src/kernels.py:72) or
+// padding columns >= n (zero) -- warp-uniform, so the common path has no selects.
+template <int DIM, int FAM, bool FIX>
+__device__ __forceinline__ void gen16(const TcParams& p, uint32_t pp, const uint64_t (&xr2)[DIM], int j0,
+                                      int grow, int n32, uint32_t (&hi)[16], uint32_t (&lo)[16]) {
+  const uint64_t neg1 = pk(-1.f, -1.f);
+#pragma unroll
+  for (int e = 0; e < 16; e += 4) {
+    uint64_t r2a = 0, r2b = 0;   // entries (e, e+1) and (e+2, e+3)
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) {
+      const float4 c = ptx::lds128(pp + 4u * (k * 32 + e));
+      const uint64_t da = fma2(pk(c.x, c.y), neg1, xr2[k]);
+      const uint64_t db = fma2(pk(c.z, c.w), neg1, xr2[k]);
+      r2a = fma2(da, da, r2a);
+      r2b = fma2(db, db, r2b);
+    }
+    uint64_t kv[2] = {kernel_pair<FAM>(p, r2a), kernel_pair<FAM>(p, r2b)};
+    if (FIX) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float v0 = pk_lo(kv[h]), v1 = pk_hi(kv[h]);
+        const int c0 = j0 + e + 2 * h;
+        v0 = (c0 == grow) ? p.diag : (c0 < n32 ? v0 : 0.f);
+        v1 = (c0 + 1 == grow) ? p.diag : (c0 + 1 < n32 ? v1 : 0.f);
+        kv[h] = pk(v0, v1);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t u0 = (uint32_t)kv[h], u1 = (uint32_t)(kv[h] >> 32);
+      const int ee = e + 2 * h;
+      const uint32_t h0 = u0 & 0xFFFFE000u, h1 = u1 & 0xFFFFE000u;
+      hi[ee] = h0;
+      hi[ee + 1] = h1;
+      const uint64_t l2 = fma2((uint64_t)h0 | ((uint64_t)h1 << 32), neg1, kv[h]);   // v - hi (exact)
+      lo[ee] = (uint32_t)l2;
+      lo[ee + 1] = (uint32_t)(l2 >> 32);
+    }
+  }
+}
+
+// 16 stored K entries of one converter thread (its row, columns [16 half, +16) of
+// the 128-byte-swizzled tile), split into tf32 hi + lo (3xTF32) or passed (1xTF32).
+template <int MODE>
+__device__ __forceinline__ void load16(const uint8_t* rowp, int row, int half, uint32_t (&hi)[16],
+                                       uint32_t (&lo)[16]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int cc = 4 * half + c;   // 16-byte chunk of the 128-byte row
+    const float4 v = *reinterpret_cast<const float4*>(rowp + ((cc ^ (row & 7)) << 4));
+    const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t ub = __float_as_uint(vv[e]);
+      if (MODE == 3) {
+        const uint32_t hb = ub & 0xFFFFE000u;
+        hi[4 * c + e] = hb;
+        lo[4 * c + e] = __float_as_uint(vv[e] - __uint_as_float(hb));
+      } else {
+        hi[4 * c + e] = ub;
+      }
+    }
+  }
+}
+
 // On-the-fly K: the stage carries the 32 column points of the k-step (TMA box of
-// the coordinate-major point array [8][ldp]: rows x,y,z,w hi then x,y,z,w lo -- a
-// double-float split of the float64 coordinates, so differences of close points
-// keep ~48 bits) instead of a K tile; the converter warps generate the tile with
-// packed FP32x2 arithmetic (FFMA2/FADD2/FMUL2) and MUFU ex2/rsqrt.
+// the coordinate-major point array [8][ldp]: rows x,y,z,w of the pre-scaled
+// float32 coordinates, rows 4-7 zero padding so the B tiles stay 1024-byte
+// aligned) instead of a K tile; the converter warps generate the tile with packed
+// FP32x2 arithmetic (FFMA2/FMUL2) and MUFU sqrt/ex2.  Rounding the coordinates to
+// float32 moved reduced config-4/5 estimates by 4e-10 / 1e-8 relative in float64
+// (scripts/otf_points_fp32.py), far inside the 1e-4 fp32 budget.
 constexpr uint32_t PTS_BYTES = 1024;
 
 template <int MODE, int NT, bool OTF = false>
@@ -173,6 +263,7 @@ struct TcShape {
   static constexpr uint32_t STAGE = A_REGION + B_BYTES * (MODE == 3 ? 2 : 1);
   static constexpr uint32_t ASTRIDE = MODE == 3 ? 64 : 32;  // TMEM columns per A buffer (hi | lo)
   static constexpr uint32_t A_COL0 = 2 * DW;
+  static constexpr int NABUF = (512 - 2 * DW) / (int)ASTRIDE < NABUF_MAX ? (512 - 2 * DW) / (int)ASTRIDE : NABUF_MAX;
   static constexpr int TMEM_NEED = 2 * DW + NABUF * (int)ASTRIDE;
   static constexpr uint32_t TMEM_COLS = TMEM_NEED <= 256 ? 256 : 512;
   static_assert(TMEM_NEED <= 512, "TMEM budget");
@@ -191,13 +282,23 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
   // 1024-byte aligned base, derived from smem_raw so the compiler keeps the shared
   // address space (plain C++ loads compile to LDS and are ordered by the mbarrier asm)
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  // Step j uses ring stage s = j % S and TMEM A buffer b = j % NA:
+  //   full[s]   TMA bytes landed                      (producer -> converters)
+  //   afull[s]  A tile converted into TMEM buffer b   (4 converter warps -> MMA)
+  //   empty[s]  MMAs of the step completed            (tcgen05.commit -> producer, converters)
+  // Buffer b is free for step j once the MMAs of step j - NA completed: the converters
+  // wait on empty[] of that step's stage (implied by full[s] when S <= NA, since the
+  // producer waited for step j - S).  The MMA warp needs only afull[s]: the converters
+  // arrive after they observed full[s].  One wait and one commit per step keep the
+  // serial MMA-issue loop short (each mbarrier wait costs ~90 cycles and each commit
+  // ~100 even when nothing blocks).
   const int S = p.stages;
+  constexpr int NA = Sh::NABUF;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * STAGE);
   uint64_t* empty = full + S;
-  uint64_t* afull = empty + S;          // [NABUF]
-  uint64_t* aempty = afull + NABUF;     // [NABUF]
-  uint64_t* accfull = aempty + NABUF;   // [2]
-  uint64_t* accempty = accfull + 2;     // [2]
+  uint64_t* afull = empty + S;
+  uint64_t* accfull = afull + S;     // [2]
+  uint64_t* accempty = accfull + 2;  // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -206,6 +307,7 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
   const int64_t beg = cta * p.total / G, end = (cta + 1) * p.total / G;
   const int b_row0 = pass * NT;
   float* const partial = p.partial + (size_t)pass * p.tiles * p.segs * NT * TC_BM;
+  unsigned long long* const prof = p.prof ? p.prof + blockIdx.x * 16 : nullptr;
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch_desc(&tmA);
@@ -214,13 +316,10 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     for (int s = 0; s < S; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
-    }
-    for (int b = 0; b < NABUF; ++b) {
-      ptx::mbar_init(&afull[b], 8);
-      ptx::mbar_init(&aempty[b], 1);
+      ptx::mbar_init(&afull[s], 4);   // one arrive per lane-quarter converter warp
     }
     for (int b = 0; b < 2; ++b) {
-      ptx::mbar_init(&accfull[b], 1);
+      ptx::mbar_init(&accfull[b], 2);   // one commit per MMA-issuing warp
       ptx::mbar_init(&accempty[b], 8);
     }
     ptx::fence_mbarrier_init();
@@ -234,45 +333,63 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
   if (beg < end) {
     if (warp == 0) {
       // ---------------- TMA producer (whole warp walks the ring; one elected lane issues)
-      for (StepIter it(beg, end, p.ks, S); it.valid(); it.next()) {
+      unsigned long long t_wait = 0;
+      const unsigned long long t_start = prof ? clock64() : 0;
+      for (StepIter it(beg, end, p.ks, S, NA); it.valid(); it.next()) {
         const int s = it.s;
-        ptx::mbar_wait_sleep(&empty[s], it.ph ^ 1);
+        const unsigned long long t0 = prof ? clock64() : 0;
+        ptx::mbar_wait_idle(&empty[s], it.ph ^ 1, p.wait_mode, p.wait_ns);
+        if (prof) t_wait += clock64() - t0;
         if (ptx::elect_one()) {
           uint8_t* st = smem + (size_t)s * STAGE;
           if (OTF) {
             ptx::mbar_arrive_expect_tx(&full[s], STAGE);
             ptx::tma_load_2d(st, &tmA, &full[s], it.kstep * TC_BK, 0);   // 32 column points, 8 coordinate rows
           } else {
-            ptx::mbar_arrive_expect_tx(&full[s], p.debug == 4 ? STAGE - AR : STAGE);
-            if (p.debug != 4) ptx::tma_load_2d(st, &tmA, &full[s], it.kstep * TC_BK, it.tile * TC_BM);
+            ptx::mbar_arrive_expect_tx(&full[s], (p.debug & 4) ? STAGE - AR : STAGE);
+            if (!(p.debug & 4)) ptx::tma_load_2d(st, &tmA, &full[s], it.kstep * TC_BK, it.tile * TC_BM);
           }
           ptx::tma_load_2d(st + AR, &tmBhi, &full[s], it.kstep * TC_BK, b_row0);
           if (MODE == 3) ptx::tma_load_2d(st + AR + B_BYTES, &tmBlo, &full[s], it.kstep * TC_BK, b_row0);
         }
         __syncwarp();
       }
-    } else if (warp == 1) {
-      // ---------------- MMA issuer
+      if (prof && lane == 0) {
+        prof[0] = t_wait;
+        prof[1] = clock64() - t_start;
+      }
+    } else if (warp == 1 || warp == 3) {
+      // ---------------- MMA issuers: warps 1 and 3 take alternate steps (whole warp walks
+      // the pipeline so every descriptor is warp-uniform; one elected lane issues).  A
+      // named-barrier baton hands the issue slot from step j's warp to step j+1's, so the
+      // tensor core sees one deterministic instruction order, while each warp's
+      // per-step mbarrier wait and commit overlap the other warp's MMAs.  Each warp
+      // commits accfull at every group end (count 2): together the two commits cover
+      // all MMAs of the group.
+      const int mpar = warp == 3;
       constexpr uint32_t idesc = ptx::idesc_tf32(TC_BM, DW);
       const uint64_t desc0 = ptx::smem_desc_sw128(ptx::smem_u32(smem + AR));
       constexpr uint64_t LO_OFF = (uint64_t)(B_BYTES >> 4);   // Blo rows, in descriptor units
       int64_t gi = -1;  // group index
-      for (StepIter it(beg, end, p.ks, S); it.valid(); it.next()) {
-        const int s = it.s;
-        const int b = it.abuf();
+      unsigned long long t_acc = 0, t_afull = 0, t_iss = 0, nsteps = 0;
+      const unsigned long long t_start = prof ? clock64() : 0;
+      for (StepIter it(beg, end, p.ks, S, NA); it.valid(); it.next()) {
         const bool gstart = it.group_start(), gend = it.group_end();
-        if (gstart) {
-          ++gi;
-          if (gi >= 2) ptx::mbar_wait(&accempty[gi & 1], (uint32_t)(((gi >> 1) - 1) & 1));
-        }
-        ptx::mbar_wait(&full[s], it.ph);
-        ptx::mbar_wait(&afull[b], it.aphase());
-        ptx::tc_fence_after();
-        const uint32_t d = tmem + (uint32_t)(gi & 1) * DW;
-        const uint32_t a0 = tmem + A_COL0 + ASTRIDE * b;
-        const uint64_t bdesc = desc0 + (uint64_t)((s * STAGE) >> 4);
-        if (ptx::elect_one()) {
-          if (p.debug != 2) {
+        if (gstart) ++gi;
+        if ((int)(it.j & 1) == mpar) {
+          const int s = it.s;
+          const unsigned long long t0 = prof ? clock64() : 0;
+          if (gstart && gi >= 2) ptx::mbar_wait(&accempty[gi & 1], (uint32_t)(((gi >> 1) - 1) & 1));
+          ptx::mbar_wait(&afull[s], it.ph);
+          const unsigned long long t1 = prof ? clock64() : 0;
+          if (it.j > 0) ptx::named_bar_sync(mpar ? 1 : 2, 64);   // baton from step j - 1
+          const unsigned long long t2 = prof ? clock64() : 0;
+          ptx::tc_fence_after();
+          const uint32_t d = tmem + (uint32_t)(gi & 1) * DW;
+          const uint32_t a0 = tmem + A_COL0 + ASTRIDE * it.ab;
+          const uint64_t bdesc = desc0 + (uint64_t)((s * STAGE) >> 4);
+          const bool leader = ptx::elect_one();
+          if (leader && !(p.debug & 2)) {
 #pragma unroll
             for (int kk = 0; kk < TC_BK / 8; ++kk) {
               const uint64_t bd = bdesc + 2 * kk;  // +32 bytes along k
@@ -289,126 +406,110 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
               }
             }
           }
-          ptx::tc_commit(&empty[s]);
-          ptx::tc_commit(&aempty[b]);
-          if (gend) ptx::tc_commit(&accfull[gi & 1]);
+          __syncwarp();
+          if (it.g + 1 < end) ptx::named_bar_arrive(mpar ? 2 : 1, 64);   // baton to step j + 1
+          if (leader) ptx::tc_commit(&empty[s]);
+          if (prof) {
+            t_acc += t1 - t0;
+            t_afull += t2 - t1;
+            t_iss += clock64() - t2;
+            ++nsteps;
+          }
         }
-        __syncwarp();
+        if (gend) {
+          if (ptx::elect_one()) ptx::tc_commit(&accfull[gi & 1]);
+          __syncwarp();
+        }
+      }
+      if (prof && lane == 0 && warp == 1) {
+        prof[2] = t_acc; prof[4] = t_afull; prof[5] = t_iss; prof[6] = clock64() - t_start; prof[13] = 2 * nsteps;
       }
     } else if (warp >= 4 && warp < 12) {
-      // ---------------- converters: warp 4 + q + 4h owns TMEM lanes 32q..32q+31 (K rows) and
-      // the 16 k-columns [16h, 16h + 16) of every step
-      const int q = (warp - 4) & 3, hsel = (warp - 4) >> 2;
+      // ---------------- converters: warp 4 + q + 4 par owns TMEM lanes 32q..32q+31 (K rows)
+      // and the steps j with j % 2 == par (all 32 k-columns of each).  The two warps of
+      // a sub-partition work on alternate steps, so one's generation overlaps the
+      // other's TMEM stores; and each warp posts the afull arrive of a step only after
+      // generating the first half of its next step, so tcgen05.wait::st rarely waits.
+      const int q = (warp - 4) & 3, par = (warp - 4) >> 2;
       const int row = q * 32 + lane;
       const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-      const int e0 = 16 * hsel;
       int cur_tile = -1;
-      uint64_t xh2[4] = {0, 0, 0, 0}, xl2[4] = {0, 0, 0, 0};   // this row's point, packed twice (on the fly)
-      int64_t grow = 0;
-      for (StepIter it(beg, end, p.ks, S); it.valid(); it.next()) {
-        const int s = it.s;
-        const int b = it.abuf();
-        const int64_t j = it.j;
-        uint32_t hi[16], lo[16];
-        if (OTF) {
-          if (it.tile != cur_tile) {
-            cur_tile = it.tile;
-            const int64_t lr = (int64_t)cur_tile * TC_BM + row;
-            grow = p.row0 + lr;
-            if (lr < p.rows) {
+      uint64_t xr2[DIM > 0 ? DIM : 1];   // this row's scaled point, packed twice (on the fly)
 #pragma unroll
-              for (int k = 0; k < DIM; ++k) {
-                const float h = p.pts[k * p.ldp + grow], l = p.pts[(4 + k) * p.ldp + grow];
-                xh2[k] = pk(h, h);
-                xl2[k] = pk(l, l);
-              }
-            }
-          }
-          ptx::mbar_wait(&full[s], it.ph);
-          const float* pp = reinterpret_cast<const float*>(smem + (size_t)s * STAGE) + e0;   // [8][32] + half
-          const int64_t j0 = (int64_t)it.kstep * TC_BK + e0;
-          // warp-uniform: does this half step hold a diagonal entry of these rows, or columns >= n?
-          const int64_t wrow0 = p.row0 + (int64_t)cur_tile * TC_BM + q * 32;
-          const bool fix = (j0 < wrow0 + 32 && j0 + 16 > wrow0) || (j0 + 16 > p.n);
-          const uint64_t neg1 = pk(-1.f, -1.f);
-          if (p.debug == 6) {   // profiling: skip the generation math
-#pragma unroll
-            for (int e = 0; e < 16; ++e) hi[e] = lo[e] = __float_as_uint(pp[e]);
-          } else
-#pragma unroll
-          for (int e = 0; e < 16; e += 4) {
-            uint64_t r2a = 0, r2b = 0;   // entries (e, e+1) and (e+2, e+3)
-#pragma unroll
-            for (int k = 0; k < DIM; ++k) {
-              const uint4 ch = *reinterpret_cast<const uint4*>(pp + k * 32 + e);
-              const uint4 cl = *reinterpret_cast<const uint4*>(pp + (4 + k) * 32 + e);
-              const uint64_t cha = (uint64_t)ch.x | ((uint64_t)ch.y << 32), chb = (uint64_t)ch.z | ((uint64_t)ch.w << 32);
-              const uint64_t cla = (uint64_t)cl.x | ((uint64_t)cl.y << 32), clb = (uint64_t)cl.z | ((uint64_t)cl.w << 32);
-              const uint64_t da = add2(fma2(cha, neg1, xh2[k]), fma2(cla, neg1, xl2[k]));  // (xh-ch)+(xl-cl)
-              const uint64_t db = add2(fma2(chb, neg1, xh2[k]), fma2(clb, neg1, xl2[k]));
-              r2a = fma2(da, da, r2a);
-              r2b = fma2(db, db, r2b);
-            }
-            uint64_t kv[2] = {kernel_pair<FAM>(p, r2a), kernel_pair<FAM>(p, r2b)};
-            if (fix) {
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                float v0 = pk_lo(kv[h]), v1 = pk_hi(kv[h]);
-                const int64_t c0 = j0 + e + 2 * h;
-                v0 = (c0 == grow) ? p.diag : (c0 < p.n ? v0 : 0.f);
-                v1 = (c0 + 1 == grow) ? p.diag : (c0 + 1 < p.n ? v1 : 0.f);
-                kv[h] = pk(v0, v1);
-              }
-            }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const uint32_t u0 = (uint32_t)kv[h], u1 = (uint32_t)(kv[h] >> 32);
-              const int ee = e + 2 * h;
-              if (MODE == 3) {
-                const uint32_t h0 = u0 & 0xFFFFE000u, h1 = u1 & 0xFFFFE000u;
-                hi[ee] = h0;
-                hi[ee + 1] = h1;
-                const uint64_t l2 = fma2((uint64_t)h0 | ((uint64_t)h1 << 32), neg1, kv[h]);   // v - hi (exact)
-                lo[ee] = (uint32_t)l2;
-                lo[ee + 1] = (uint32_t)(l2 >> 32);
-              } else {
-                hi[ee] = u0;
-                hi[ee + 1] = u1;
-              }
-            }
-          }
-        } else {
-          ptx::mbar_wait(&full[s], it.ph);
-          const uint8_t* rowp = smem + (size_t)s * STAGE + row * 128;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const int cc = 4 * hsel + c;   // 16-byte chunk of the 128-byte row
-            const float4 v = *reinterpret_cast<const float4*>(rowp + ((cc ^ (row & 7)) << 4));
-            const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const uint32_t ub = __float_as_uint(vv[e]);
-              if (MODE == 3) {
-                const uint32_t hb = ub & 0xFFFFE000u;
-                hi[4 * c + e] = hb;
-                lo[4 * c + e] = __float_as_uint(vv[e] - __uint_as_float(hb));
-              } else {
-                hi[4 * c + e] = ub;
-              }
-            }
-          }
-        }
-        if (j >= NABUF) ptx::mbar_wait(&aempty[b], (uint32_t)(((j / NABUF) - 1) & 1));
-        ptx::tc_fence_after();
-        const uint32_t ta = tmem + lane_base + A_COL0 + ASTRIDE * b + e0;
-        if (p.debug != 1) {
-          ptx::tmem_st_32x32b_x16(ta, hi);
-          if (MODE == 3) ptx::tmem_st_32x32b_x16(ta + 32, lo);
-        }
+      for (int k = 0; k < (DIM > 0 ? DIM : 1); ++k) xr2[k] = 0;
+      int grow = 0, wrow0 = 0;   // global row of this lane / of lane 0 (n < 2^31)
+      const int n32 = (int)p.n;
+      int pend = -1;             // A buffer whose TMEM stores are in flight
+      auto post = [&](int buf) {
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&afull[b]);
+        if (lane == 0) ptx::mbar_arrive(&afull[buf]);
+      };
+      unsigned long long cv_full = 0;
+      const unsigned long long cv_start = prof ? clock64() : 0;
+      StepIter it(beg, end, p.ks, S, NA);
+      if (par) it.next();
+      for (; it.valid(); it.next(), it.next()) {
+        const int s = it.s;
+        if constexpr (OTF) if (it.tile != cur_tile) {
+          cur_tile = it.tile;
+          const int lr = cur_tile * TC_BM + row;
+          wrow0 = (int)p.row0 + cur_tile * TC_BM + q * 32;
+          grow = wrow0 + lane;
+          if (lr < p.rows) {
+#pragma unroll
+            for (int k = 0; k < DIM; ++k) {
+              const float x = p.pts[k * p.ldp + grow];
+              xr2[k] = pk(x, x);
+            }
+          }
+        }
+        const unsigned long long c0 = prof ? clock64() : 0;
+        ptx::mbar_wait(&full[s], it.ph);
+        if (S > NA && it.j >= NA) ptx::mbar_wait(&empty[it.ls], it.lph);   // TMEM buffer free
+        if (prof) cv_full += clock64() - c0;
+        ptx::tc_fence_after();
+        const uint32_t ta = tmem + lane_base + A_COL0 + ASTRIDE * it.ab;
+        if (p.debug & 16) {   // profiling: no converter work at all
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&afull[s]);
+          continue;
+        }
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          uint32_t hi[16], lo[16];
+          if constexpr (OTF) {
+            const uint32_t pp = ptx::smem_u32(smem + (size_t)s * STAGE) + 64u * half;   // [8][32] fp32
+            const int j0 = it.kstep * TC_BK + 16 * half;
+            // warp-uniform: a diagonal entry of these rows, or columns >= n?
+            const bool fix = (j0 < wrow0 + 32 && j0 + 16 > wrow0) || (j0 + 16 > n32);
+            if (p.debug & 8) {   // profiling: raw stage words, no generation math
+#pragma unroll
+              for (int c = 0; c < 16; c += 4) {
+                const float4 v = ptx::lds128(pp + 4u * c);
+                hi[c] = lo[c] = __float_as_uint(v.x); hi[c + 1] = lo[c + 1] = __float_as_uint(v.y);
+                hi[c + 2] = lo[c + 2] = __float_as_uint(v.z); hi[c + 3] = lo[c + 3] = __float_as_uint(v.w);
+              }
+            } else if (!fix) {
+              gen16<DIM, FAM, false>(p, pp, xr2, 0, 0, 0, hi, lo);
+            } else {
+              gen16<DIM, FAM, true>(p, pp, xr2, j0, grow, n32, hi, lo);
+            }
+          } else {
+            load16<MODE>(smem + (size_t)s * STAGE + row * 128, row, half, hi, lo);
+          }
+          if (half == 0 && pend >= 0) post(pend);
+          if (!(p.debug & 1)) {
+            ptx::tmem_st_32x32b_x16(ta + 16 * half, hi);
+            if (MODE == 3) ptx::tmem_st_32x32b_x16(ta + 32 + 16 * half, lo);
+          }
+        }
+        pend = s;
+      }
+      if (pend >= 0) post(pend);
+      if (prof && warp == 4 && lane == 0) {
+        prof[7] = cv_full; prof[10] = clock64() - cv_start;
       }
     } else if (warp >= 12) {
       // ---------------- accumulator drain: warp 12 + q + 4h owns TMEM lanes 32q..32q+31 and
@@ -425,45 +526,54 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       int64_t gi = -1;
       int tile = (int)(beg / p.ks);
       int64_t seg_lo = beg;
+      unsigned long long dr_wait = 0;
+      const unsigned long long dr_start = prof ? clock64() : 0;
       while (seg_lo < end) {
         const int64_t seg_hi = std::min<int64_t>(end, (int64_t)(tile + 1) * p.ks);
         for (int64_t gs = seg_lo; gs < seg_hi; gs += GROUP) {
-        ++gi;
-        const bool seg_end = gs + GROUP >= seg_hi;
-        const int buf = (int)(gi & 1);
-        ptx::mbar_wait_sleep(&accfull[buf], (uint32_t)((gi >> 1) & 1));
-        ptx::tc_fence_after();
+          ++gi;
+          const bool seg_end = gs + GROUP >= seg_hi;
+          const int buf = (int)(gi & 1);
+          const unsigned long long d0 = prof ? clock64() : 0;
+          ptx::mbar_wait_idle(&accfull[buf], (uint32_t)((gi >> 1) & 1), p.wait_mode, p.wait_ns);
+          if (prof) dr_wait += clock64() - d0;
+          ptx::tc_fence_after();
+          if (!(p.debug & 32)) {
 #pragma unroll
-        for (int c0 = 0; c0 < HALF; c0 += 16) {
-          uint32_t v[16];
-          ptx::tmem_ld_32x32b_x16(tmem + lane_base + (uint32_t)(buf * DW + c_base + c0), v);
-          if (Sh::STACK) {
-            uint32_t w[16];
-            ptx::tmem_ld_32x32b_x16(tmem + lane_base + (uint32_t)(buf * DW + NT + c_base + c0), w);
-            ptx::tmem_wait_ld();
+            for (int c0 = 0; c0 < HALF; c0 += 16) {
+              uint32_t v[16];
+              ptx::tmem_ld_32x32b_x16(tmem + lane_base + (uint32_t)(buf * DW + c_base + c0), v);
+              if (Sh::STACK) {
+                uint32_t w[16];
+                ptx::tmem_ld_32x32b_x16(tmem + lane_base + (uint32_t)(buf * DW + NT + c_base + c0), w);
+                ptx::tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]) + __uint_as_float(w[e]);
-          } else {
-            ptx::tmem_wait_ld();
+                for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]) + __uint_as_float(w[e]);
+              } else {
+                ptx::tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]);
+                for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]);
+              }
+            }
           }
-        }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&accempty[buf]);
-        if (seg_end) {
-          const int seg = (int)(cta - cta_of_step((int64_t)tile * p.ks, p.total, G));
-          float* P = partial + ((size_t)tile * p.segs + seg) * (size_t)NT * TC_BM;
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&accempty[buf]);
+          if (seg_end) {
+            const int seg = (int)(cta - cta_of_step((int64_t)tile * p.ks, p.total, G));
+            float* P = partial + ((size_t)tile * p.segs + seg) * (size_t)NT * TC_BM;
 #pragma unroll
-          for (int c = 0; c < HALF; ++c) {
-            P[(size_t)(c_base + c) * TC_BM + row] = acc[c];
-            acc[c] = 0.f;
+            for (int c = 0; c < HALF; ++c) {
+              P[(size_t)(c_base + c) * TC_BM + row] = acc[c];
+              acc[c] = 0.f;
+            }
           }
-        }
         }
         seg_lo = seg_hi;
         ++tile;
+      }
+      if (prof && warp == 12 && lane == 0) {
+        prof[11] = dr_wait; prof[12] = clock64() - dr_start;
       }
     }
   }
@@ -559,9 +669,10 @@ template <int MODE, int NT, bool OTF, int DIM, int FAM>
 void launch_tc(const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl, TcParams p, int64_t grid,
                cudaStream_t st) {
   using Sh = TcShape<MODE, NT, OTF>;
-  const size_t extra = 1024 + 8 * 64;
+  const size_t extra = 1024 + 8 * 96;   // alignment slack + barriers (<= 32 stages)
   const int smem_cap = max_smem_optin() - 1024;
-  p.stages = (int)std::min<size_t>(8, (smem_cap - extra) / Sh::STAGE);
+  static const int max_stages = getenv("RLD_TC_STAGES") ? atoi(getenv("RLD_TC_STAGES")) : NABUF_MAX;
+  p.stages = (int)std::min<size_t>(max_stages, (smem_cap - extra) / Sh::STAGE);
   p.tmem_cols = Sh::TMEM_COLS;
   const size_t smem = p.stages * Sh::STAGE + extra;
   RLD_CUDA(cudaFuncSetAttribute(kv_tc_kernel<MODE, NT, OTF, DIM, FAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -667,9 +778,6 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
   p.row0 = op.row0;
   p.rows = rows;
   p.family = op.kp.family;
-  p.a2 = (float)op.kp.a2;
-  p.gscale = (float)(op.kp.inv_2l2 * 1.4426950408889634);
-  p.s5 = (float)op.kp.s5_over_l;
   p.diag = (float)op.kp.diag;
   p.la2 = (float)std::log2(op.kp.a2);
   p.total = total;
@@ -680,6 +788,17 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
   {
     static const int dbg = getenv("RLD_TC_DEBUG") ? atoi(getenv("RLD_TC_DEBUG")) : 0;
     p.debug = dbg;
+    static const int wm = getenv("RLD_TC_WAIT") ? atoi(getenv("RLD_TC_WAIT")) : 1;
+    static const int wns = getenv("RLD_TC_WAIT_NS") ? atoi(getenv("RLD_TC_WAIT_NS")) : 256;
+    p.wait_mode = wm;
+    p.wait_ns = (uint32_t)wns;
+  }
+  static const bool prof_on = getenv("RLD_TC_PROFILE") != nullptr;
+  static DevBuf prof_buf;
+  if (prof_on) {
+    prof_buf.reserve(sizeof(unsigned long long) * 16 * (size_t)(Gl * npass));
+    RLD_CUDA(cudaMemsetAsync(prof_buf.ptr, 0, sizeof(unsigned long long) * 16 * (size_t)(Gl * npass), st));
+    p.prof = prof_buf.as<unsigned long long>();
   }
   ws.tc_partial.reserve(sizeof(float) * (size_t)npass * tiles * segs * width * TC_BM);
   p.partial = ws.tc_partial.as<float>();
@@ -692,6 +811,20 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
       launch_tc_stored<3>(width, mA, mBh, mBl, p, Gl * npass, st);
     else
       launch_tc_stored<1>(width, mA, mBh, mBl, p, Gl * npass, st);
+  }
+  if (prof_on) {
+    std::vector<unsigned long long> h(16 * (size_t)(Gl * npass));
+    RLD_CUDA(cudaMemcpyAsync(h.data(), prof_buf.ptr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, st));
+    RLD_CUDA(cudaStreamSynchronize(st));
+    double a[16] = {0};
+    for (int64_t c = 0; c < Gl * npass; ++c)
+      for (int k = 0; k < 16; ++k) a[k] += (double)h[c * 16 + k];
+    const double steps = a[13] > 0 ? a[13] : 1;
+    fprintf(stderr,
+            "[kv_tc prof] m=%ld n=%ld nt=%d otf=%d per k-step cycles: producer wait %.0f / loop %.0f | mma wait acc %.0f "
+            "afull %.0f issue %.0f loop %.0f | conv(w4) wait full %.0f loop %.0f | drain wait %.0f loop %.0f\n",
+            (long)m, (long)n, width, (int)otf, a[0] / steps, a[1] / steps, a[2] / steps, a[4] / steps,
+            a[5] / steps, a[6] / steps, a[7] / steps, a[10] / steps, a[11] / steps, a[12] / steps);
   }
   const int64_t count = m * rows;
   const int blocks = (int)std::min<int64_t>(ceil_div(count, 256), 148 * 16);

@@ -221,7 +221,9 @@ void prepare(rld_handle* h, const rld_problem* p) {
     fill_doubles(r.rows, r.kp.diag, r.diag.as<double>(), st);
     if (p->d <= 4) {
       r.pts4.reserve(sizeof(float) * 8 * ceil_div(p->n, 4) * 4);
-      pad_points(r.X.as<double>(), p->n, p->d, r.pts4.as<float>(), st);
+      // coordinates pre-scaled so the tile generator's r^2 is the kernel argument
+      const double scale = p->family == RLD_MATERN52 ? r.kp.s5_over_l : std::sqrt(r.kp.inv_2l2 * 1.4426950408889634);
+      pad_points(r.X.as<double>(), p->n, p->d, scale, r.pts4.as<float>(), st);
     }
     if (r.path == RLD_PATH_STORED) {
       const size_t es = p->dtype == RLD_FP64 ? 8 : 4;

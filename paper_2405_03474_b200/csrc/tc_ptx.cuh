@@ -51,13 +51,19 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 }
 
 // Wait for the phase of parity `parity` to complete.  A watchdog traps after
-// 20 s instead of hanging the GPU if a pipeline invariant is ever broken.
+// ~20 s (4e10 SM cycles) instead of hanging the GPU if a pipeline invariant is
+// ever broken; it reads the SM cycle counter only every 1024 failed probes
+// (%globaltimer reads are slow enough to serialise the pipelines).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
-  const uint64_t t0 = globaltimer_ns();
   uint32_t spins = 0;
+  uint64_t t0 = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if ((++spins & 1023u) == 0 && globaltimer_ns() - t0 > 20000000000ull) __trap();
+    if ((++spins & 1023u) == 0) {
+      const uint64_t now = clock64();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 40000000000ull) __trap();
+    }
   }
 }
 
@@ -86,6 +92,25 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
   }
 }
 
+// Waits of warps with slack (producer ring, accumulator drain) that share the SM
+// sub-partitions with the converter warps: `mode` 0 = try_wait loop (hardware
+// suspend), 1 = try_wait + nanosleep back-off (no issue slots while parked),
+// 2 = try_wait with a suspend-time hint.
+__device__ __forceinline__ void mbar_wait_idle(uint64_t* bar, uint32_t parity, int mode, uint32_t ns) {
+  if (mode == 2) return mbar_wait_sleep(bar, parity);
+  if (mbar_try_wait(bar, parity)) return;
+  uint32_t spins = 0;
+  uint64_t t0 = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    if (mode == 1) __nanosleep(ns);
+    if ((++spins & 255u) == 0) {
+      const uint64_t now = clock64();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 40000000000ull) __trap();
+    }
+  }
+}
+
 __device__ __forceinline__ float4 lds128(uint32_t saddr) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(saddr));
@@ -109,6 +134,14 @@ __device__ __forceinline__ double2 lds128d(uint32_t saddr) {
   double2 v;
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(saddr));
   return v;
+}
+
+// ---------------------------------------------------------------- named barriers
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 // ---------------------------------------------------------------- TMA
@@ -181,6 +214,12 @@ __device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_
       "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
       "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
       : "memory");
+}
+
+__device__ __forceinline__ void tmem_st_32x32b_x8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&v)[32]) {

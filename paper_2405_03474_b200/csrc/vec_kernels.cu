@@ -594,16 +594,18 @@ void sqrt_factors(int k, double keep_rtol, const double* lam, double* W, double*
 }
 namespace {
 // coordinate-major split points [8][ldp]: row k = fp32(x_k) (hi), row 4 + k = fp32(x_k - hi) (lo)
-__global__ void pad_points_kernel(const double* __restrict__ X, int64_t n, int d, float* __restrict__ P) {
+// Coordinate-major float32 points for the on-the-fly tensor-core tiles: rows 0-3
+// hold x_k * scale (zero for k >= d), rows 4-7 zero padding.
+__global__ void pad_points_kernel(const double* __restrict__ X, int64_t n, int d, double scale,
+                                  float* __restrict__ P) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= 4 * n) return;
   const int64_t i = e >> 2;
   const int k = (int)(e & 3);
   const int64_t ldp = ceil_div(n, 4) * 4;
   const double x = k < d ? X[i * d + k] : 0.0;
-  const float h = (float)x;
-  P[k * ldp + i] = h;
-  P[(4 + k) * ldp + i] = (float)(x - (double)h);
+  P[k * ldp + i] = (float)(x * scale);
+  P[(4 + k) * ldp + i] = 0.f;
 }
 }  // namespace
 
@@ -627,8 +629,8 @@ void relayout_gathered(const double* src, int G, int64_t m, int64_t L, int64_t n
   RLD_LAUNCH_CHECK();
 }
 
-void pad_points(const double* X, int64_t n, int d, float* pts8, cudaStream_t st) {
-  pad_points_kernel<<<(unsigned)ceil_div(4 * n, 256), 256, 0, st>>>(X, n, d, pts8);
+void pad_points(const double* X, int64_t n, int d, double scale, float* pts8, cudaStream_t st) {
+  pad_points_kernel<<<(unsigned)ceil_div(4 * n, 256), 256, 0, st>>>(X, n, d, scale, pts8);
   RLD_LAUNCH_CHECK();
 }
 
