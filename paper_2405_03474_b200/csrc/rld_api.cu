@@ -98,7 +98,7 @@ struct Work {
   DevBuf x, p, pp, u, w, KX, T, Tg;
   DevBuf scal;     // small scalars / per-probe arrays
   DevBuf ints;     // flags, info, live, size, kept
-  DevBuf scratch, scratch2, solver_work, rng_scratch;
+  DevBuf scratch, scratch2, solver_work, rng_scratch, gram_scratch;
   DevBuf gsend, grecv;   // row-shard all-gather staging
   DevBuf flagbuf;        // flag OR over ranks
   KvWorkspace kv;
@@ -327,6 +327,27 @@ void kv(rld_handle* h, int64_t m, const double* Vfull, double* Y, int tc_mode = 
   kv_product(op, m, Vfull, op.n, Y, op.rows, h->wk.kv, h->st, nullptr);
 }
 
+// G (w x w, full) = Y^T Y for the rows x w column-major block.  The rows are cut
+// into fixed chunks, one DGEMM per chunk in a strided batch (FP64 tensor cores,
+// enough CTAs to fill the GPU; a single SYRK has only ~w^2/2048 output tiles),
+// then the chunk Grams are summed in fixed order (deterministic).
+void gram_blas(rld_handle* h, int64_t rows, int w, const double* Y, int64_t ldy, double* G) {
+  Work& wk = h->wk;
+  const int64_t chunk = std::max<int64_t>(512, ceil_div(rows, 16));
+  const int64_t nb = ceil_div(rows, chunk);
+  const int64_t full = rows / chunk;   // equal chunks in the batch; a ragged tail gets its own GEMM
+  wk.gram_scratch.reserve(sizeof(double) * (size_t)w * w * nb);
+  double* P = wk.gram_scratch.as<double>();
+  if (full > 0)
+    RLD_CUBLAS(cublasDgemmStridedBatched(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, w, w, (int)chunk, &ONE, Y, (int)ldy,
+                                         chunk, Y, (int)ldy, chunk, &ZERO, P, w, (int64_t)w * w, (int)full));
+  const int64_t tail = rows - full * chunk;
+  if (tail > 0)
+    RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, w, w, (int)tail, &ONE, Y + full * chunk, (int)ldy,
+                           Y + full * chunk, (int)ldy, &ZERO, P + (size_t)full * w * w, w));
+  sum_blocks(nb, (int64_t)w * w, P, G, h->st);
+}
+
 // In-place row orthonormalisation of the w x n block Y (col-major n x w), two
 // Cholesky-QR passes.  Replaces the row-wise CGS2 of src/linalg.py:159-180:
 // both give the unique Q with positive-diagonal triangular factor.  CholQR2 is
@@ -347,7 +368,7 @@ void cholqr2(rld_handle* h, int64_t n, int w, double* Y, int* flags, int passes 
   RLD_CUSOLVER(cusolverDnDpotrf_bufferSize(h->solver, CUBLAS_FILL_MODE_UPPER, w, G, w, &lwork));
   wk.solver_work.reserve(sizeof(double) * std::max(lwork, 1));
   for (int pass = 0; pass < passes; ++pass) {
-    RLD_CUBLAS(cublasDsyrk(h->cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, w, (int)n, &ONE, Y, (int)n, &ZERO, G, w));
+    gram_blas(h, n, w, Y, n, G);
     allreduce_sum(h, G, (int64_t)w * w);
     if (pass == 0) diag_copy(w, G, wk.gdiag.as<double>(), h->st);
     RLD_CUSOLVER(cusolverDnDpotrf(h->solver, CUBLAS_FILL_MODE_UPPER, w, G, w, wk.solver_work.as<double>(), lwork,
@@ -511,17 +532,17 @@ PrecondOut build_preconditioner(rld_handle* h, const rld_config* c, const rld_in
   allreduce_sum(h, scal, 1);
   // C = At^T At ; inner = I + C ; log det inner by Cholesky (src/precond.py:75-80)
   double* C = wk.C.as<double>();
-  RLD_CUBLAS(cublasDsyrk(h->cublas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, k, (int)nl, &ONE, A, (int)nl, &ZERO, C, k));
+  gram_blas(h, nl, k, A, nl, C);
   allreduce_sum(h, C, (int64_t)k * k);
   wk.inner.reserve(sizeof(double) * k * k);
   double* inner = wk.inner.as<double>();
   copy_doubles((int64_t)k * k, C, inner, st);
   add_identity(k, inner, st);
   {
+    int* info = wk.ints.as<int>() + 4;
     int lwork = 0;
     RLD_CUSOLVER(cusolverDnDpotrf_bufferSize(h->solver, CUBLAS_FILL_MODE_LOWER, k, inner, k, &lwork));
     wk.solver_work.reserve(sizeof(double) * std::max(lwork, 1));
-    int* info = wk.ints.as<int>() + 4;
     RLD_CUSOLVER(cusolverDnDpotrf(h->solver, CUBLAS_FILL_MODE_LOWER, k, inner, k, wk.solver_work.as<double>(), lwork,
                                   info));
     chol_logdet(k, inner, info, scal + 1, flags, st);

@@ -59,6 +59,8 @@ void normal_rows(const uint64_t key[2], int64_t rows, int64_t n, int64_t col0, i
                  double* out, DevBuf& scratch, int* dflags, cudaStream_t st);
 // [G][m][L] (all-gathered shards) -> m x n rows, n <= G L
 void relayout_gathered(const double* src, int G, int64_t m, int64_t L, int64_t n, double* dst, cudaStream_t st);
+// out[e] = sum_{b < nb} in[b * count + e] (fixed order)
+void sum_blocks(int64_t nb, int64_t count, const double* in, double* out, cudaStream_t st);
 void pad_points(const double* X, int64_t n, int d, double scale, float* pts8, cudaStream_t st);
 void diag_of_dense(int64_t rows, int64_t row0, const void* K, int64_t ldk, int dtype, double* d, cudaStream_t st);
 

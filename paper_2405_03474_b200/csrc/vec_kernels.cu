@@ -629,6 +629,22 @@ void relayout_gathered(const double* src, int G, int64_t m, int64_t L, int64_t n
   RLD_LAUNCH_CHECK();
 }
 
+namespace {
+__global__ void sum_blocks_kernel(int64_t nb, int64_t count, const double* __restrict__ in, double* __restrict__ out) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t b = 0; b < nb; ++b) s += in[b * count + e];
+    out[e] = s;
+  }
+}
+}  // namespace
+
+void sum_blocks(int64_t nb, int64_t count, const double* in, double* out, cudaStream_t st) {
+  if (count <= 0) return;
+  sum_blocks_kernel<<<(unsigned)std::min<int64_t>(ceil_div(count, 256), 148 * 8), 256, 0, st>>>(nb, count, in, out);
+  RLD_LAUNCH_CHECK();
+}
+
 void pad_points(const double* X, int64_t n, int d, double scale, float* pts8, cudaStream_t st) {
   pad_points_kernel<<<(unsigned)ceil_div(4 * n, 256), 256, 0, st>>>(X, n, d, scale, pts8);
   RLD_LAUNCH_CHECK();
