@@ -59,9 +59,26 @@ constexpr int GROUP = 4;            // k-steps accumulated in TMEM before the re
 constexpr int NABUF_MAX = 8;        // pipeline stages = TMEM A-operand buffers: as many as the 512 columns leave (<= 8)
 constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4;  // 16 KB
 
+// Work schedule of one CTA (G CTAs per column pass).  Phase 1: R = tiles / G full
+// rounds -- CTA c takes tile c + r G over all k-steps, so every CTA sweeps the B
+// operand (V) in the same k order at about the same time and L2 serves the reuse
+// (with per-CTA stream-K ranges the CTAs sat at unrelated k offsets and re-read B
+// from HBM once per tile: ~8.8 TB per config-5 product).  Phase 2: the remaining
+// tiles' (tile, k-step) space is cut into G equal contiguous ranges ("stream-K"),
+// whose per-CTA partial tiles kv_tc_reduce adds in fixed order.
+struct Sched {
+  int ks, G, R;          // k-steps per tile, CTAs per pass, full rounds
+  int64_t tail_total;    // (tiles - R G) * ks
+  __host__ __device__ int64_t tail_beg(int64_t c) const { return c * tail_total / G; }
+  __host__ __device__ int64_t tail_end(int64_t c) const { return (c + 1) * tail_total / G; }
+};
+
 // CTA b works on column pass b % npass over stream-K range b / npass.
 struct TcParams {
-  int64_t total;    // tiles * ks
+  Sched sched;      // work schedule (per column pass)
+  int mp;           // B rows per k-step block (vectors padded to npass x NT)
+  unsigned int* sync;   // per-pass arrival counters of the phase-1 epoch barrier (zeroed per launch)
+  int sync_k;           // k-steps per epoch (0: no barrier)
   int ks;           // k-steps per tile
   int tiles;
   int npass;        // column passes in this launch
@@ -75,8 +92,7 @@ struct TcParams {
   int debug;        // profiling bitmask (RLD_TC_DEBUG): 1 skip A stores, 2 skip MMAs, 4 skip K-tile loads,
                     // 8 skip tile generation math, 16 converters only arrive, 32 drains skip TMEM loads
   // on-the-fly kernel tiles (src/kernels.py:40-46, 72)
-  const float* pts;  // [8][ldp] float32: coordinate rows x,y,z,w (hi) then x,y,z,w (lo)
-  int64_t ldp;
+  const float* pts;  // [ceil(n/32)][8][32] float32 k-step blocks: scaled x,y,z,w rows, rows 4-7 zero
   int64_t n, row0, rows;
   int family;
   float diag;                  // a^2 + jitter
@@ -137,31 +153,62 @@ __host__ __device__ __forceinline__ int64_t cta_of_step(int64_t x, int64_t total
   return ((x + 1) * G - 1) / total;
 }
 
-// Walks a CTA's contiguous range of (tile, k-step) pairs with running counters
-// (no 64-bit divisions in the pipeline loops).
+// Walks a CTA's steps with running counters (no 64-bit divisions in the loops).
 struct StepIter {
-  int64_t g, end, j;
-  int ks, kstep, tile, gpos, s, S;
+  int64_t v, vend;       // virtual step index and end: [0, R ks) phase 1, then the tail range
+  int64_t j;             // step counter (== v)
+  int64_t tail_x;        // position in the tail space (phase 2)
+  int ks, kstep, tile, gpos, s, S, G, R, round;
+  int64_t cta, tail_end;
   uint32_t ph;
   int ab, NA;            // TMEM A buffer of step j (j % NA)
   int ls;                // stage of step j - NA (valid for j >= NA) and its phase parity
   uint32_t lph;
-  __device__ __forceinline__ StepIter(int64_t beg, int64_t end_, int ks_, int S_, int NA_)
-      : g(beg), end(end_), j(0), ks(ks_), gpos(0), s(0), S(S_), ph(0), ab(0), NA(NA_), ls(0), lph(0) {
-    tile = (int)(beg / ks_);
-    kstep = (int)(beg - (int64_t)tile * ks_);
+  int64_t tail_total;
+  __device__ __forceinline__ StepIter(const Sched& sc, int64_t cta_, int S_, int NA_)
+      : v(0), j(0), ks(sc.ks), kstep(0), gpos(0), s(0), S(S_), G(sc.G), R(sc.R), round(0), cta(cta_), ph(0),
+        ab(0), NA(NA_), ls(0), lph(0), tail_total(sc.tail_total) {
+    const int64_t tb = sc.tail_beg(cta_);
+    tail_end = sc.tail_end(cta_);
+    vend = (int64_t)R * ks + (tail_end - tb);
+    tail_x = tb;
+    if (R > 0) {
+      tile = (int)cta_;
+    } else {
+      tile = R * G + (int)(tb / ks);
+      kstep = (int)(tb - (int64_t)(tile - R * G) * ks);
+    }
   }
-  __device__ __forceinline__ bool valid() const { return g < end; }
+  __device__ __forceinline__ bool valid() const { return v < vend; }
+  __device__ __forceinline__ bool in_tail() const { return round >= R; }
   __device__ __forceinline__ bool group_start() const { return gpos == 0; }
-  __device__ __forceinline__ bool seg_end() const { return g + 1 == end || kstep + 1 == ks; }
+  __device__ __forceinline__ bool seg_end() const { return v + 1 == vend || kstep + 1 == ks; }
   __device__ __forceinline__ bool group_end() const { return seg_end() || gpos + 1 == GROUP; }
+  // partial-sum slot of this step's tile segment
+  __device__ __forceinline__ int seg() const {
+    if (!in_tail()) return 0;
+    const int64_t x0 = (int64_t)(tile - R * G) * ks;
+    return (int)(cta - cta_of_step(x0, tail_total, G));
+  }
   __device__ __forceinline__ void next() {
     gpos = group_end() ? 0 : gpos + 1;
-    ++g;
+    ++v;
     ++j;
+    if (in_tail()) ++tail_x;
     if (++kstep == ks) {
       kstep = 0;
-      ++tile;
+      if (!in_tail()) {
+        ++round;
+        if (round < R) {
+          tile += G;
+        } else {   // enter the tail range
+          const int64_t tb = tail_x;
+          tile = R * G + (int)(tb / ks);
+          kstep = (int)(tb - (int64_t)(tile - R * G) * ks);
+        }
+      } else {
+        ++tile;
+      }
     }
     if (++s == S) {
       s = 0;
@@ -303,8 +350,7 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pass = (int)(blockIdx.x % p.npass);
-  const int64_t G = gridDim.x / p.npass, cta = blockIdx.x / p.npass;
-  const int64_t beg = cta * p.total / G, end = (cta + 1) * p.total / G;
+  const int64_t cta = blockIdx.x / p.npass;
   const int b_row0 = pass * NT;
   float* const partial = p.partial + (size_t)pass * p.tiles * p.segs * NT * TC_BM;
   unsigned long long* const prof = p.prof ? p.prof + blockIdx.x * 16 : nullptr;
@@ -330,13 +376,27 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
-  if (beg < end) {
+  if (StepIter(p.sched, cta, 1, 1).valid()) {
     if (warp == 0) {
       // ---------------- TMA producer (whole warp walks the ring; one elected lane issues)
       unsigned long long t_wait = 0;
       const unsigned long long t_start = prof ? clock64() : 0;
-      for (StepIter it(beg, end, p.ks, S, NA); it.valid(); it.next()) {
+      int64_t epoch = 0;
+      for (StepIter it(p.sched, cta, S, NA); it.valid(); it.next()) {
         const int s = it.s;
+        // phase-1 epoch barrier: the CTAs' producers meet every sync_k k-steps, so all
+        // CTAs stream the same window of B and L2 serves it (their drift otherwise
+        // accumulates tile after tile until B comes from HBM once per tile)
+        if (p.sync_k > 0 && !it.in_tail() && it.v > 0 && it.kstep % p.sync_k == 0) {
+          ++epoch;
+          if (lane == 0) {
+            unsigned int* ctr = p.sync + pass;
+            atomicAdd(ctr, 1u);
+            const unsigned int target = (unsigned int)(epoch * p.sched.G);
+            while (*(volatile unsigned int*)ctr < target) __nanosleep(100);
+          }
+          __syncwarp();
+        }
         const unsigned long long t0 = prof ? clock64() : 0;
         ptx::mbar_wait_idle(&empty[s], it.ph ^ 1, p.wait_mode, p.wait_ns);
         if (prof) t_wait += clock64() - t0;
@@ -344,13 +404,14 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
           uint8_t* st = smem + (size_t)s * STAGE;
           if (OTF) {
             ptx::mbar_arrive_expect_tx(&full[s], STAGE);
-            ptx::tma_load_2d(st, &tmA, &full[s], it.kstep * TC_BK, 0);   // 32 column points, 8 coordinate rows
+            ptx::tma_load_2d(st, &tmA, &full[s], 0, it.kstep * 8);   // 32 column points, 8 coordinate rows
           } else {
             ptx::mbar_arrive_expect_tx(&full[s], (p.debug & 4) ? STAGE - AR : STAGE);
             if (!(p.debug & 4)) ptx::tma_load_2d(st, &tmA, &full[s], it.kstep * TC_BK, it.tile * TC_BM);
           }
-          ptx::tma_load_2d(st + AR, &tmBhi, &full[s], it.kstep * TC_BK, b_row0);
-          if (MODE == 3) ptx::tma_load_2d(st + AR + B_BYTES, &tmBlo, &full[s], it.kstep * TC_BK, b_row0);
+          // B in k-step blocks [ks][mp][32]: one contiguous NT x 128-byte box per step
+          ptx::tma_load_2d(st + AR, &tmBhi, &full[s], 0, it.kstep * p.mp + b_row0);
+          if (MODE == 3) ptx::tma_load_2d(st + AR + B_BYTES, &tmBlo, &full[s], 0, it.kstep * p.mp + b_row0);
         }
         __syncwarp();
       }
@@ -373,7 +434,7 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       int64_t gi = -1;  // group index
       unsigned long long t_acc = 0, t_afull = 0, t_iss = 0, nsteps = 0;
       const unsigned long long t_start = prof ? clock64() : 0;
-      for (StepIter it(beg, end, p.ks, S, NA); it.valid(); it.next()) {
+      for (StepIter it(p.sched, cta, S, NA); it.valid(); it.next()) {
         const bool gstart = it.group_start(), gend = it.group_end();
         if (gstart) ++gi;
         if ((int)(it.j & 1) == mpar) {
@@ -407,7 +468,7 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             }
           }
           __syncwarp();
-          if (it.g + 1 < end) ptx::named_bar_arrive(mpar ? 2 : 1, 64);   // baton to step j + 1
+          if (it.v + 1 < it.vend) ptx::named_bar_arrive(mpar ? 2 : 1, 64);   // baton to step j + 1
           if (leader) ptx::tc_commit(&empty[s]);
           if (prof) {
             t_acc += t1 - t0;
@@ -448,7 +509,7 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       };
       unsigned long long cv_full = 0;
       const unsigned long long cv_start = prof ? clock64() : 0;
-      StepIter it(beg, end, p.ks, S, NA);
+      StepIter it(p.sched, cta, S, NA);
       if (par) it.next();
       for (; it.valid(); it.next(), it.next()) {
         const int s = it.s;
@@ -460,7 +521,7 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
           if (lr < p.rows) {
 #pragma unroll
             for (int k = 0; k < DIM; ++k) {
-              const float x = p.pts[k * p.ldp + grow];
+              const float x = p.pts[(((int64_t)(grow >> 5) * 8 + k) << 5) + (grow & 31)];
               xr2[k] = pk(x, x);
             }
           }
@@ -524,53 +585,45 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
 #pragma unroll
       for (int c = 0; c < HALF; ++c) acc[c] = 0.f;
       int64_t gi = -1;
-      int tile = (int)(beg / p.ks);
-      int64_t seg_lo = beg;
       unsigned long long dr_wait = 0;
       const unsigned long long dr_start = prof ? clock64() : 0;
-      while (seg_lo < end) {
-        const int64_t seg_hi = std::min<int64_t>(end, (int64_t)(tile + 1) * p.ks);
-        for (int64_t gs = seg_lo; gs < seg_hi; gs += GROUP) {
-          ++gi;
-          const bool seg_end = gs + GROUP >= seg_hi;
-          const int buf = (int)(gi & 1);
-          const unsigned long long d0 = prof ? clock64() : 0;
-          ptx::mbar_wait_idle(&accfull[buf], (uint32_t)((gi >> 1) & 1), p.wait_mode, p.wait_ns);
-          if (prof) dr_wait += clock64() - d0;
-          ptx::tc_fence_after();
-          if (!(p.debug & 32)) {
+      for (StepIter it(p.sched, cta, 1, 1); it.valid(); it.next()) {
+        if (!it.group_end()) continue;
+        ++gi;
+        const int buf = (int)(gi & 1);
+        const unsigned long long d0 = prof ? clock64() : 0;
+        ptx::mbar_wait_idle(&accfull[buf], (uint32_t)((gi >> 1) & 1), p.wait_mode, p.wait_ns);
+        if (prof) dr_wait += clock64() - d0;
+        ptx::tc_fence_after();
+        if (!(p.debug & 32)) {
 #pragma unroll
-            for (int c0 = 0; c0 < HALF; c0 += 16) {
-              uint32_t v[16];
-              ptx::tmem_ld_32x32b_x16(tmem + lane_base + (uint32_t)(buf * DW + c_base + c0), v);
-              if (Sh::STACK) {
-                uint32_t w[16];
-                ptx::tmem_ld_32x32b_x16(tmem + lane_base + (uint32_t)(buf * DW + NT + c_base + c0), w);
-                ptx::tmem_wait_ld();
+          for (int c0 = 0; c0 < HALF; c0 += 16) {
+            uint32_t v[16];
+            ptx::tmem_ld_32x32b_x16(tmem + lane_base + (uint32_t)(buf * DW + c_base + c0), v);
+            if (Sh::STACK) {
+              uint32_t w[16];
+              ptx::tmem_ld_32x32b_x16(tmem + lane_base + (uint32_t)(buf * DW + NT + c_base + c0), w);
+              ptx::tmem_wait_ld();
 #pragma unroll
-                for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]) + __uint_as_float(w[e]);
-              } else {
-                ptx::tmem_wait_ld();
+              for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]) + __uint_as_float(w[e]);
+            } else {
+              ptx::tmem_wait_ld();
 #pragma unroll
-                for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]);
-              }
-            }
-          }
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&accempty[buf]);
-          if (seg_end) {
-            const int seg = (int)(cta - cta_of_step((int64_t)tile * p.ks, p.total, G));
-            float* P = partial + ((size_t)tile * p.segs + seg) * (size_t)NT * TC_BM;
-#pragma unroll
-            for (int c = 0; c < HALF; ++c) {
-              P[(size_t)(c_base + c) * TC_BM + row] = acc[c];
-              acc[c] = 0.f;
+              for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]);
             }
           }
         }
-        seg_lo = seg_hi;
-        ++tile;
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&accempty[buf]);
+        if (it.seg_end()) {
+          float* P = partial + ((size_t)it.tile * p.segs + it.seg()) * (size_t)NT * TC_BM;
+#pragma unroll
+          for (int c = 0; c < HALF; ++c) {
+            P[(size_t)(c_base + c) * TC_BM + row] = acc[c];
+            acc[c] = 0.f;
+          }
+        }
       }
       if (prof && warp == 12 && lane == 0) {
         prof[11] = dr_wait; prof[12] = clock64() - dr_start;
@@ -583,16 +636,20 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
 }
 
 // Y[c * ldy + i] = sum over the tile's segments of the partials (float64 accumulation, fixed order)
-__global__ void kv_tc_reduce(const float* __restrict__ P, int64_t total, int64_t G, int ks, int tiles, int segs,
-                             int nt, int64_t m, int64_t rows, double* __restrict__ Y, int64_t ldy) {
+__global__ void kv_tc_reduce(const float* __restrict__ P, Sched sc, int tiles, int segs, int nt, int64_t m,
+                             int64_t rows, double* __restrict__ Y, int64_t ldy) {
   const int64_t count = m * rows;
+  const int full = sc.R * sc.G;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = e / rows, i = e % rows;
     const int64_t pass = c / nt, cc = c % nt;
     const int64_t tile = i / TC_BM, r = i % TC_BM;
-    const int64_t x0 = tile * ks;
-    const int nseg = (int)(cta_of_step(x0 + ks - 1, total, G) - cta_of_step(x0, total, G) + 1);
+    int nseg = 1;
+    if (tile >= full) {
+      const int64_t x0 = (tile - full) * sc.ks;
+      nseg = (int)(cta_of_step(x0 + sc.ks - 1, sc.tail_total, sc.G) - cta_of_step(x0, sc.tail_total, sc.G) + 1);
+    }
     const float* Pp = P + (size_t)pass * tiles * segs * nt * TC_BM;
     double s = 0.0;
     for (int k = 0; k < nseg; ++k) s += (double)Pp[(((size_t)tile * segs + k) * nt + cc) * TC_BM + r];
@@ -600,20 +657,25 @@ __global__ void kv_tc_reduce(const float* __restrict__ P, int64_t total, int64_t
   }
 }
 
-// B operand rows from float64 V: hi = tf32(v) (3xTF32) or fp32(v) (1xTF32), lo = fp32(v - hi)
-__global__ void kv_tc_split(const double* __restrict__ V, int64_t ldv, int64_t m, int64_t n, int64_t ldb, int mode,
-                            float* __restrict__ Bhi, float* __restrict__ Blo) {
-  const int64_t count = m * n;
+// B operand from float64 V (m rows of length n) in k-step blocks Bt[ks][mp][32]
+// (contiguous 128-byte rows per vector and k-step, zero padded for c >= m, j >= n):
+// hi = tf32(v) (3xTF32) or fp32(v) (1xTF32), lo = fp32(v - hi).  The blocked layout
+// makes every pipeline step's TMA box one contiguous NT x 128-byte range, instead of
+// NT rows n*4 bytes apart (256 distinct 2 MB pages per box at n = 2^20).
+__global__ void kv_tc_split(const double* __restrict__ V, int64_t ldv, int64_t m, int64_t n, int64_t mp, int64_t ks,
+                            int mode, float* __restrict__ Bhi, float* __restrict__ Blo) {
+  const int64_t count = mp * ks * 32;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = e / n, j = e % n;
-    const double v = V[c * ldv + j];
+    const int64_t c = e / (ks * 32), j = e % (ks * 32);
+    const double v = (c < m && j < n) ? V[c * ldv + j] : 0.0;
+    const int64_t o = ((j >> 5) * mp + c) * 32 + (j & 31);
     float h = (float)v;
     if (mode == 3) {
       h = __uint_as_float(__float_as_uint(h) & 0xFFFFE000u);
-      Blo[c * ldb + j] = (float)(v - (double)h);
+      Blo[o] = (float)(v - (double)h);
     }
-    Bhi[c * ldb + j] = h;
+    Bhi[o] = h;
   }
 }
 
@@ -716,12 +778,13 @@ void launch_tc_otf(int d, int family, int nt, const CUtensorMap& mA, const CUten
   }
 }
 
-// 2-D map over the coordinate-major split points [8][ldp] fp32: box {32, 8} = the
-// 32 column points of one k-step
-CUtensorMap make_points_map(const float* pts, int64_t n, int64_t ldp) {
+// 2-D map over the blocked points [ceil(n/32) * 8][32] fp32: box {32, 8} = the 32
+// column points of one k-step (1 KB contiguous)
+CUtensorMap make_points_map(const float* pts, int64_t n) {
   CUtensorMap m;
-  cuuint64_t dims[2] = {(cuuint64_t)n, 8};
-  cuuint64_t strides[1] = {(cuuint64_t)ldp * 4};
+  const int64_t ks = ceil_div(n, TC_BK);
+  cuuint64_t dims[2] = {(cuuint64_t)TC_BK, (cuuint64_t)(ks * 8)};
+  cuuint64_t strides[1] = {(cuuint64_t)TC_BK * 4};
   cuuint32_t box[2] = {(cuuint32_t)TC_BK, 8};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(pts), dims, strides, box, estr,
@@ -743,44 +806,52 @@ bool kv_tc_supported(const KvOperand& op) {
 void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, int64_t ldv, double* Y, int64_t ldy,
                    KvWorkspace& ws, cudaStream_t st) {
   const int64_t n = op.n, rows = op.rows;
-  const int64_t ldb = ceil_div(n, 4) * 4;
-  ws.bhi.reserve(sizeof(float) * ldb * m);
-  if (mode == 3) ws.blo.reserve(sizeof(float) * ldb * m);
-  {
-    const int64_t count = m * n;
-    const int blocks = (int)std::min<int64_t>(ceil_div(count, 256), 148 * 16);
-    kv_tc_split<<<blocks, 256, 0, st>>>(V, ldv, m, n, ldb, mode, ws.bhi.as<float>(),
-                                        mode == 3 ? ws.blo.as<float>() : nullptr);
-    RLD_LAUNCH_CHECK();
-  }
-  const int G = sm_count();
   const int ks = (int)ceil_div(n, TC_BK);
-  const int tiles = (int)ceil_div(rows, TC_BM);
-  const int64_t total = (int64_t)tiles * ks;
   // vectors per pass: <= 128 (two TMEM accumulators + A buffers within 512 columns)
   const int npass = (int)ceil_div(m, 128);
   int width = (int)(ceil_div(ceil_div(m, npass), 32) * 32);
   if (op.K == nullptr && width == 96) width = 128;   // on-the-fly kernels come in NT = 32, 64, 128
+  const int64_t mp = (int64_t)npass * width;
+  ws.bhi.reserve(sizeof(float) * mp * ks * 32);
+  if (mode == 3) ws.blo.reserve(sizeof(float) * mp * ks * 32);
+  {
+    const int64_t count = mp * ks * 32;
+    const int blocks = (int)std::min<int64_t>(ceil_div(count, 256), 148 * 16);
+    kv_tc_split<<<blocks, 256, 0, st>>>(V, ldv, m, n, mp, ks, mode, ws.bhi.as<float>(),
+                                        mode == 3 ? ws.blo.as<float>() : nullptr);
+    RLD_LAUNCH_CHECK();
+  }
+  const int G = sm_count();
+  const int tiles = (int)ceil_div(rows, TC_BM);
+  const int64_t total = (int64_t)tiles * ks;
   const int64_t Gl = std::min<int64_t>(std::max(1, G / npass), total);
+  Sched sc{};
+  sc.ks = ks;
+  sc.G = (int)Gl;
+  {
+    static const bool streamk_only = getenv("RLD_TC_STREAMK") && getenv("RLD_TC_STREAMK")[0] == '1';
+    sc.R = streamk_only ? 0 : (int)(tiles / Gl);
+  }
+  sc.tail_total = (int64_t)(tiles - sc.R * Gl) * ks;
   int segs = 1;
-  for (int t = 0; t < tiles; ++t) {
-    const int64_t x0 = (int64_t)t * ks;
-    segs = (int)std::max<int64_t>(segs, cta_of_step(x0 + ks - 1, total, Gl) - cta_of_step(x0, total, Gl) + 1);
+  for (int t = sc.R * (int)Gl; t < tiles; ++t) {
+    const int64_t x0 = (int64_t)(t - sc.R * Gl) * ks;
+    segs = (int)std::max<int64_t>(
+        segs, cta_of_step(x0 + ks - 1, sc.tail_total, Gl) - cta_of_step(x0, sc.tail_total, Gl) + 1);
   }
   const bool otf = op.K == nullptr;
-  const int64_t ldp = ceil_div(n, 4) * 4;
-  const CUtensorMap mA = otf ? make_points_map(op.pts4, n, ldp)
+  const CUtensorMap mA = otf ? make_points_map(op.pts4, n)
                              : make_map(static_cast<const float*>(op.K), n, rows, op.ldk, TC_BM);
   TcParams p{};
   p.pts = op.pts4;
-  p.ldp = ldp;
+  p.mp = (int)mp;
   p.n = n;
   p.row0 = op.row0;
   p.rows = rows;
   p.family = op.kp.family;
   p.diag = (float)op.kp.diag;
   p.la2 = (float)std::log2(op.kp.a2);
-  p.total = total;
+  p.sched = sc;
   p.ks = ks;
   p.tiles = tiles;
   p.npass = npass;
@@ -800,10 +871,17 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
     RLD_CUDA(cudaMemsetAsync(prof_buf.ptr, 0, sizeof(unsigned long long) * 16 * (size_t)(Gl * npass), st));
     p.prof = prof_buf.as<unsigned long long>();
   }
+  {
+    static const int sync_k = getenv("RLD_TC_SYNC_K") ? atoi(getenv("RLD_TC_SYNC_K")) : 2048;
+    p.sync_k = (sc.R > 1 || (sc.R == 1 && sc.tail_total > 0)) ? sync_k : 0;
+    ws.tc_sync.reserve(sizeof(unsigned int) * npass);
+    p.sync = ws.tc_sync.as<unsigned int>();
+    if (p.sync_k > 0) RLD_CUDA(cudaMemsetAsync(p.sync, 0, sizeof(unsigned int) * npass, st));
+  }
   ws.tc_partial.reserve(sizeof(float) * (size_t)npass * tiles * segs * width * TC_BM);
   p.partial = ws.tc_partial.as<float>();
-  const CUtensorMap mBh = make_map(ws.bhi.as<float>(), n, m, ldb, width);
-  const CUtensorMap mBl = mode == 3 ? make_map(ws.blo.as<float>(), n, m, ldb, width) : mBh;
+  const CUtensorMap mBh = make_map(ws.bhi.as<float>(), TC_BK, mp * ks, TC_BK, width);
+  const CUtensorMap mBl = mode == 3 ? make_map(ws.blo.as<float>(), TC_BK, mp * ks, TC_BK, width) : mBh;
   if (otf) {
     launch_tc_otf(op.kp.d, op.kp.family, width, mA, mBh, mBl, p, Gl * npass, st);
   } else {
@@ -828,7 +906,7 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
   }
   const int64_t count = m * rows;
   const int blocks = (int)std::min<int64_t>(ceil_div(count, 256), 148 * 16);
-  kv_tc_reduce<<<blocks, 256, 0, st>>>(p.partial, total, Gl, ks, tiles, segs, width, m, rows, Y, ldy);
+  kv_tc_reduce<<<blocks, 256, 0, st>>>(p.partial, sc, tiles, segs, width, m, rows, Y, ldy);
   RLD_LAUNCH_CHECK();
 }
 

@@ -86,6 +86,7 @@ struct KvWorkspace {
   DevBuf partial;     // split-K partial sums
   DevBuf bhi, blo;    // tensor-core B operand (tf32 hi / lo rows)
   DevBuf tc_partial;  // stream-K partial accumulators
+  DevBuf tc_sync;     // epoch-barrier counters of the tensor-core kernel
 };
 
 bool kv_tc_supported(const KvOperand& op);

@@ -594,18 +594,17 @@ void sqrt_factors(int k, double keep_rtol, const double* lam, double* W, double*
 }
 namespace {
 // coordinate-major split points [8][ldp]: row k = fp32(x_k) (hi), row 4 + k = fp32(x_k - hi) (lo)
-// Coordinate-major float32 points for the on-the-fly tensor-core tiles: rows 0-3
-// hold x_k * scale (zero for k >= d), rows 4-7 zero padding.
+// Float32 points for the on-the-fly tensor-core tiles in k-step blocks
+// P[ceil(n/32)][8][32]: rows 0-3 hold x_k * scale (zero for k >= d), rows 4-7 and
+// the padding columns are zero (the buffer is cleared first).
 __global__ void pad_points_kernel(const double* __restrict__ X, int64_t n, int d, double scale,
                                   float* __restrict__ P) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= 4 * n) return;
   const int64_t i = e >> 2;
   const int k = (int)(e & 3);
-  const int64_t ldp = ceil_div(n, 4) * 4;
   const double x = k < d ? X[i * d + k] : 0.0;
-  P[k * ldp + i] = (float)(x * scale);
-  P[(4 + k) * ldp + i] = 0.f;
+  P[(((i >> 5) * 8 + k) << 5) + (i & 31)] = (float)(x * scale);
 }
 }  // namespace
 
@@ -646,6 +645,7 @@ void sum_blocks(int64_t nb, int64_t count, const double* in, double* out, cudaSt
 }
 
 void pad_points(const double* X, int64_t n, int d, double scale, float* pts8, cudaStream_t st) {
+  RLD_CUDA(cudaMemsetAsync(pts8, 0, sizeof(float) * 8 * ceil_div(n, 32) * 32, st));
   pad_points_kernel<<<(unsigned)ceil_div(4 * n, 256), 256, 0, st>>>(X, n, d, scale, pts8);
   RLD_LAUNCH_CHECK();
 }
