@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define RLD_ABI_VERSION 1
+#define RLD_ABI_VERSION 2
 
 typedef enum rld_status {
   RLD_OK = 0,
@@ -55,6 +55,13 @@ typedef enum rld_precond_kind {
   RLD_PRECOND_IDENTITY = 1, /* src/precond.py:245-246 */
   RLD_PRECOND_DIAGONAL = 2  /* src/precond.py:247-248 */
 } rld_precond_kind;
+
+/* The stochastic estimators of src/estimators.py behind rld_logdet. */
+typedef enum rld_estimator {
+  RLD_ESTIMATOR_RSTAR = 0, /* rstar_logdet r1/r3/r5 (src/estimators.py:77-96) */
+  RLD_ESTIMATOR_SLQ = 1    /* slq_logdet: Lanczos on K itself with full reorthogonalisation, no
+                              preconditioner, Gauss quadrature of log (src/estimators.py:99-122) */
+} rld_estimator;
 
 typedef struct rld_handle rld_handle;
 
@@ -102,6 +109,8 @@ typedef struct rld_config {
   double orth_rtol;       /* 1e-12 (src/linalg.py:177) */
   uint64_t probe_key[2];  /* Philox4x64 key of numpy stream (seed, (2,))      -- src/estimators.py:64 */
   uint64_t omega_key[4];  /* keys of streams (seed,(1,0)) and (seed,(1,1))    -- src/precond.py:183 */
+  int32_t estimator;      /* rld_estimator: r* (order above) or SLQ (src/estimators.py:99-122) */
+  int32_t reserved2;
 } rld_config;
 
 /* Optional injected random inputs.  NULL -> generated on the device from the
@@ -129,6 +138,8 @@ typedef struct rld_result {
   int32_t kernel_launches;/* own kernels launched by the estimate */
   double phase_ms[8];     /* [0] K build [1] sketch+QR [2] projected eig [3] precond factors
                              [4] Lanczos [5] shifted solves + Hutchinson [6] collectives [7] total */
+  int32_t clamped_eigs;   /* SLQ: Ritz values <= 0 floored before the log (src/estimators.py:113-115) */
+  int32_t reserved;
 } rld_result;
 
 int rld_abi_version(void);
@@ -146,8 +157,9 @@ const char* rld_last_error(const rld_handle* h);
  * record timing events or chain their own work on the same stream. */
 void* rld_stream(rld_handle* h);
 
-/* rstar_logdet(M, cfg) -- src/estimators.py:77-96 (and estimate_logdet for
- * r1/r3/r5, src/estimators.py:132-138).  Uploads / builds K, runs the
+/* rstar_logdet(M, cfg) -- src/estimators.py:77-96 -- or, with
+ * cfg->estimator == RLD_ESTIMATOR_SLQ, slq_logdet(M, cfg) -- src/estimators.py:99-122
+ * (estimate_logdet for r1/r3/r5/slq, src/estimators.py:132-138).  Uploads / builds K, runs the
  * preconditioner build, s-probe Lanczos, multishift solves and the Hutchinson
  * mean on the device, and fills `result`. */
 int rld_logdet(rld_handle* h, const rld_problem* problem, const rld_config* cfg,

@@ -424,6 +424,43 @@ def rstar_points(family, amplitude, ell, jitter, X, order=3, s=35, t=20, probe_k
     return rstar(op, op.n, order, s, t, probe_kind, k, q, seed, **kw)
 
 
+# ----------------------------------------------------------------------------
+# stochastic Lanczos quadrature (src/estimators.py:99-122) -- SURVEY.md §8(f) row 1
+
+SLQ_EIG_FLOOR = 1e-300   # src/estimators.py:29
+
+
+def slq(op, n, s, t, probe_kind, seed, V=None, per_probe=False) -> OracleEstimate:
+    """mean_i |z_i|^2 sum_j Y[0,j]^2 log(max(theta_j, floor)) over the Ritz pairs of
+    each probe's t-step Lanczos on K itself (no preconditioner, src/estimators.py:106),
+    with the reference's two-pass full reorthogonalisation (lanczos_block)."""
+    start = time.perf_counter()
+    t = min(t, n)                                                       # estimators.py:62
+    Z = probes(probe_kind, s, n, seed) if V is None else np.asarray(V, dtype=np.float64)
+    per = np.empty(s)
+    clamped = 0
+    groups = [slice(i, i + 1) for i in range(s)] if per_probe else [slice(0, s)]
+    for g in groups:
+        Zg = Z[g].T
+        _, al, be, sizes, norms = lanczos_block(op, Zg, t)
+        for c in range(Zg.shape[1]):
+            m = sizes[c]
+            T = np.diag(al[c, :m]) + np.diag(be[c, : m - 1], 1) + np.diag(be[c, : m - 1], -1)
+            theta, Y = np.linalg.eigh(T)                                  # estimators.py:111
+            clamped += int(np.count_nonzero(theta <= 0.0))
+            theta = np.maximum(theta, SLQ_EIG_FLOOR)
+            per[g.start + c] = norms[c] ** 2 * float((Y[0, :] ** 2) @ np.log(theta))
+    trace = float(np.mean(per))
+    est = OracleEstimate(trace, 0.0, trace, per, time.perf_counter() - start)
+    est.clamped_eigs = clamped
+    return est
+
+
+def slq_dense(K, s=35, t=20, probe_kind="rademacher", seed=0, **kw):
+    op = DenseOperator(K)
+    return slq(op, op.n, s, t, probe_kind, seed, **kw)
+
+
 def eval_partial(order, z):
     """b + sum_j c_j/(z - a_j) -- src/rational.py:151-160."""
     b, poles, residues = PARTIAL_FRACTIONS[order]

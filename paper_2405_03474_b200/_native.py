@@ -30,6 +30,8 @@ PATH_STORED, PATH_ON_THE_FLY = 0, 1
 HOST, DEVICE = 0, 1
 RADEMACHER, GAUSSIAN = 0, 1
 PRECOND_RAND_SVD, PRECOND_IDENTITY, PRECOND_DIAGONAL = 0, 1, 2
+ESTIMATOR_RSTAR, ESTIMATOR_SLQ = 0, 1
+ABI_VERSION = 2
 
 # every symbol include/rld.h declares
 EXPORTS = (
@@ -56,7 +58,8 @@ class Config(C.Structure):
                 ("probe_kind", C.c_int32), ("precond_kind", C.c_int32), ("precond_rank", C.c_int32),
                 ("precond_iters", C.c_int32), ("oversample", C.c_int32), ("diag_floor", C.c_double),
                 ("keep_rtol", C.c_double), ("breakdown_rtol", C.c_double), ("orth_rtol", C.c_double),
-                ("probe_key", C.c_uint64 * 2), ("omega_key", C.c_uint64 * 4)]
+                ("probe_key", C.c_uint64 * 2), ("omega_key", C.c_uint64 * 4), ("estimator", C.c_int32),
+                ("reserved2", C.c_int32)]
 
 
 class Inputs(C.Structure):
@@ -68,7 +71,7 @@ class Result(C.Structure):
     _fields_ = [("value", C.c_double), ("logdet_P", C.c_double), ("trace_term", C.c_double),
                 ("per_probe", C.POINTER(C.c_double)), ("wall_time", C.c_double), ("attempts", C.c_int32),
                 ("rank_kept", C.c_int32), ("kv_products", C.c_int32), ("kernel_launches", C.c_int32),
-                ("phase_ms", C.c_double * 8)]
+                ("phase_ms", C.c_double * 8), ("clamped_eigs", C.c_int32), ("reserved", C.c_int32)]
 
 
 _lib = None
@@ -108,7 +111,7 @@ def load() -> C.CDLL:
         for name in EXPORTS:
             if name not in ("rld_abi_version", "rld_destroy", "rld_last_error", "rld_stream"):
                 getattr(lib, name).restype = C.c_int
-        if lib.rld_abi_version() != 1:
+        if lib.rld_abi_version() != ABI_VERSION:
             raise RuntimeError("librld.so ABI version mismatch")
         _lib = lib
         return lib

@@ -100,6 +100,7 @@ struct Work {
   DevBuf ints;     // flags, info, live, size, kept
   DevBuf scratch, scratch2, solver_work, rng_scratch, gram_scratch;
   DevBuf gsend, grecv;   // row-shard all-gather staging
+  DevBuf qbasis, coef;   // SLQ: Lanczos basis (t x s x rows) and reorthogonalisation coefficients
   DevBuf flagbuf;        // flag OR over ranks
   KvWorkspace kv;
 };
@@ -568,7 +569,13 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
   if (!res) fail(RLD_ERR_INVALID_ARGUMENT, "result is NULL");
   rld_inputs none{};
   if (!in) in = &none;
-  const Partial pf = partial_fraction(c->order);
+  if (c->estimator != RLD_ESTIMATOR_RSTAR && c->estimator != RLD_ESTIMATOR_SLQ)
+    fail(RLD_ERR_INVALID_ARGUMENT, "unknown estimator " + std::to_string(c->estimator));
+  const bool slq = c->estimator == RLD_ESTIMATOR_SLQ;
+  rld_config cs = *c;
+  if (slq) cs.precond_kind = RLD_PRECOND_IDENTITY;   // SLQ runs on K itself (src/estimators.py:106)
+  c = &cs;
+  const Partial pf = slq ? Partial{0.0, 0, {}, {}} : partial_fraction(c->order);
   if (c->num_probes < 1 || c->lanczos_iters < 1) fail(RLD_ERR_INVALID_ARGUMENT, "num_probes and lanczos_iters must be >= 1");
   if (c->precond_rank < 0) fail(RLD_ERR_INVALID_ARGUMENT, "rank must be >= 0");
   if (c->precond_iters < 1) fail(RLD_ERR_INVALID_ARGUMENT, "num_iters must be >= 1");
@@ -667,8 +674,20 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
 
   wk.Y.reserve(sizeof(double) * s * n);
   double* xfull = wk.Y.as<double>();
+  // SLQ keeps the Lanczos basis for the full reorthogonalisation of src/lanczos.py:60-62:
+  // Qb[j] = q_j rows (s x nl); probe c's basis is the nl x (j+1) column-major block at
+  // Qb + c nl with leading dimension s nl
+  double* Qb = nullptr;
+  double* coef = nullptr;
+  if (slq) {
+    wk.qbasis.reserve(sizeof(double) * (size_t)t * s * nl);
+    wk.coef.reserve(sizeof(double) * (size_t)s * t);
+    Qb = wk.qbasis.as<double>();
+    coef = wk.coef.as<double>();
+  }
   int products = 0;
   for (int j = 0; j < t; ++j) {
+    if (slq) copy_doubles(s * nl, x, Qb + (size_t)j * s * nl, st);
     gather_rows(h, x, s, xfull);
     kv(h, s, xfull, KX);                                  // K x_j
     ++products;
@@ -676,6 +695,23 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
     allreduce_sum(h, dots, s);
     lanczos_alpha(s, j, t, dots, live, alpha, st);        // alpha_j = q_j . A q_j
     if (j == t - 1) break;
+    if (slq) {
+      // w = K q_j; two passes w -= Q_j (Q_j^T w) over q_0..q_j (src/lanczos.py:58-62)
+      copy_doubles(s * nl, KX, u, st);
+      const double MONE = -1.0;
+      for (int pass = 0; pass < 2; ++pass) {
+        RLD_CUBLAS(cublasDgemvStridedBatched(h->cublas, CUBLAS_OP_T, (int)nl, j + 1, &ONE, Qb, (int)(s * nl), nl, u,
+                                             1, nl, &ZERO, coef, 1, t, (int)s));
+        if (h->world > 1) allreduce_sum(h, coef, s * t);
+        RLD_CUBLAS(cublasDgemvStridedBatched(h->cublas, CUBLAS_OP_N, (int)nl, j + 1, &MONE, Qb, (int)(s * nl), nl,
+                                             coef, 1, t, &ONE, u, 1, nl, (int)s));
+      }
+      rows_dot(s, nl, u, nl, u, nl, dots, wk.scratch, st, nullptr);
+      allreduce_sum(h, dots, s);
+      lanczos_beta(s, j, t, c->breakdown_rtol, dots, alpha, beta, beta_ref, live, size, st);
+      lanczos_advance(s, nl, j, t, beta, live, u, u, p, pp, x, st);
+      continue;
+    }
     lanczos_residual(s, nl, j, t, KX, alpha, beta, p, pp, sqrt_base, u, wv, st);
     if (k > 0) {
       RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, k, (int)s, (int)nl, &ONE, U, (int)nl, wv, (int)nl,
@@ -692,8 +728,11 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
     lanczos_advance(s, nl, j, t, beta, live, u, wv, p, pp, x, st);
   }
   RLD_CUDA(cudaEventRecord(h->ev[2], st));
-  thomas_hutchinson(s, t, alpha, beta, size, norms, pf.npoles, pf.offset, consts + 1, consts + 6, per_probe,
-                    scal + 2, flags, st);
+  if (slq)   // Gauss quadrature of log on each probe's T (src/estimators.py:110-116)
+    slq_epilogue(s, t, alpha, beta, size, norms, 1e-300, per_probe, scal + 2, ints + 6, flags, st);
+  else
+    thomas_hutchinson(s, t, alpha, beta, size, norms, pf.npoles, pf.offset, consts + 1, consts + 6, per_probe,
+                      scal + 2, flags, st);
   RLD_CUDA(cudaEventRecord(h->ev[3], st));
 
   double hs[3];
@@ -713,6 +752,8 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
   if (hi[0] & RLD_FLAG_SINGULAR) fail(RLD_ERR_SINGULAR_SHIFTED_SYSTEM, "zero pivot in a shifted tridiagonal solve");
   if (hi[0] & 8) fail(RLD_ERR_INVALID_ARGUMENT, "base diagonal must be strictly positive");
   if (hi[5]) fail(RLD_ERR_CUDA, "device Gaussian stream generator overflow (flags " + std::to_string(hi[5]) + ")");
+  if (hi[0] & RLD_FLAG_EIG_NOCONV) fail(RLD_ERR_CUDA, "tridiagonal eigensolver did not converge (SLQ)");
+  res->clamped_eigs = slq ? hi[6] : 0;
   res->logdet_P = hs[0] + hs[1];
   res->trace_term = hs[2];
   res->value = res->logdet_P + res->trace_term;

@@ -11,6 +11,7 @@ enum : int {
   RLD_FLAG_SINGULAR = 4,
   RLD_FLAG_BAD_BASE = 8,
   RLD_FLAG_QR_WEAK = 16,
+  RLD_FLAG_EIG_NOCONV = 32,
 };
 
 void normalize_rows(int64_t m, int64_t n, const double* z, const double* nrm2, double* norms, double* q,
@@ -26,6 +27,9 @@ void lanczos_advance(int64_t m, int64_t n, int j, int t, const double* beta, con
 void thomas_hutchinson(int64_t m, int t, const double* alpha, const double* beta, const int* size,
                        const double* norms, int npoles, double offset, const double* poles,
                        const double* residues, double* per_probe, double* trace, int* flags, cudaStream_t st);
+
+void slq_epilogue(int64_t m, int t, const double* alpha, const double* beta, const int* size, const double* norms,
+                  double eig_floor, double* per_probe, double* trace, int* clamped, int* flags, cudaStream_t st);
 
 void scale_rows_colmajor(int64_t rows, int64_t cols, int64_t ld, const double* f, bool divide, double* a,
                          cudaStream_t st);

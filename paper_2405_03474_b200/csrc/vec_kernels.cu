@@ -253,6 +253,104 @@ void lanczos_advance(int64_t m, int64_t n, int j, int t, const double* beta, con
   RLD_LAUNCH_CHECK();
 }
 
+namespace {
+// Stochastic Lanczos quadrature epilogue (src/estimators.py:110-120): per probe,
+// the eigenvalues theta and first eigenvector components Y[0, :] of its t x t
+// tridiagonal T (implicit-shift QL, EISPACK tql2, tracking only the first row
+// of the eigenvector matrix), then |v|^2 sum_i Y[0,i]^2 log(max(theta_i, floor))
+// and the count of theta_i <= 0; fixed-order mean over probes.  One thread per probe.
+__global__ void slq_epilogue_kernel(int64_t m, int t, const double* __restrict__ alpha,
+                                    const double* __restrict__ beta, const int* __restrict__ size,
+                                    const double* __restrict__ norms, double eig_floor,
+                                    double* __restrict__ per_probe, double* __restrict__ trace,
+                                    int* __restrict__ clamped, int* __restrict__ flags) {
+  extern __shared__ double sbuf[];   // 3 t doubles per thread: d, e, z
+  for (int64_t c = threadIdx.x; c < m; c += blockDim.x) {
+    double* d = sbuf + (size_t)threadIdx.x * 3 * t;
+    double* e = d + t;
+    double* z = e + t;
+    const int ms = size[c];
+    for (int i = 0; i < ms; ++i) {
+      d[i] = alpha[c * t + i];
+      e[i] = (i + 1 < ms) ? beta[c * t + i] : 0.0;
+      z[i] = (i == 0) ? 1.0 : 0.0;
+    }
+    // tql2 (implicit QL with Wilkinson-type shifts); e[i] couples d[i], d[i+1]
+    for (int l = 0; l < ms; ++l) {
+      int iter = 0;
+      for (;;) {
+        int mm = l;
+        for (; mm < ms - 1; ++mm) {
+          const double dd = fabs(d[mm]) + fabs(d[mm + 1]);
+          if (fabs(e[mm]) <= 2.220446049250313e-16 * dd) break;
+        }
+        if (mm == l) break;
+        if (++iter > 60) {
+          atomicOr(flags, RLD_FLAG_EIG_NOCONV);
+          break;
+        }
+        double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+        double r = hypot(g, 1.0);
+        g = d[mm] - d[l] + e[l] / (g + (g >= 0.0 ? fabs(r) : -fabs(r)));
+        double sn = 1.0, cs = 1.0, p = 0.0;
+        int i = mm - 1;
+        for (; i >= l; --i) {
+          double f = sn * e[i];
+          const double b = cs * e[i];
+          r = hypot(f, g);
+          e[i + 1] = r;
+          if (r == 0.0) {
+            d[i + 1] -= p;
+            e[mm] = 0.0;
+            break;
+          }
+          sn = f / r;
+          cs = g / r;
+          g = d[i + 1] - p;
+          r = (d[i] - g) * sn + 2.0 * cs * b;
+          p = sn * r;
+          d[i + 1] = g + p;
+          g = cs * r - b;
+          // first row of the accumulated rotations
+          f = z[i + 1];
+          z[i + 1] = sn * z[i] + cs * f;
+          z[i] = cs * z[i] - sn * f;
+        }
+        if (r == 0.0 && i >= l) continue;
+        d[l] -= p;
+        e[l] = g;
+        e[mm] = 0.0;
+      }
+    }
+    double acc = 0.0;
+    int bad = 0;
+    for (int i = 0; i < ms; ++i) {
+      if (d[i] <= 0.0) ++bad;
+      acc += z[i] * z[i] * log(fmax(d[i], eig_floor));
+    }
+    const double nv = norms[c];
+    per_probe[c] = nv * nv * acc;
+    if (bad) atomicAdd(clamped, bad);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int64_t c = 0; c < m; ++c) s += per_probe[c];
+    *trace = s / (double)m;
+  }
+}
+}  // namespace
+
+void slq_epilogue(int64_t m, int t, const double* alpha, const double* beta, const int* size, const double* norms,
+                  double eig_floor, double* per_probe, double* trace, int* clamped, int* flags, cudaStream_t st) {
+  int threads = (int)std::min<int64_t>(128, std::max<int64_t>(1, m));
+  threads = std::max(1, std::min(threads, (int)((48 * 1024) / (24 * std::max(t, 1)))));
+  const size_t smem = sizeof(double) * 3 * threads * t;
+  slq_epilogue_kernel<<<1, threads, smem, st>>>(m, t, alpha, beta, size, norms, eig_floor, per_probe, trace,
+                                                clamped, flags);
+  RLD_LAUNCH_CHECK();
+}
+
 void thomas_hutchinson(int64_t m, int t, const double* alpha, const double* beta, const int* size,
                        const double* norms, int npoles, double offset, const double* poles,
                        const double* residues, double* per_probe, double* trace, int* flags, cudaStream_t st) {

@@ -33,8 +33,8 @@ from .linalg import Rng, philox_key
 from .precond import DEVICE_PRECOND_KINDS, OVERSAMPLE, DIAG_FLOOR, PreconditionerConfig
 from .probes import DEVICE_PROBE_KINDS, PROBE_KINDS, make_probes
 
-__all__ = ["ALGORITHMS", "EstimatorConfig", "LogDetEstimate", "estimate_logdet", "rstar_logdet", "exact_logdet",
-           "ResidentMatrix"]
+__all__ = ["ALGORITHMS", "EstimatorConfig", "LogDetEstimate", "estimate_logdet", "rstar_logdet", "slq_logdet",
+           "exact_logdet", "ResidentMatrix"]
 
 ALGORITHMS = ("r1", "r3", "r5", "slq", "exact")
 DTYPES = ("fp64", "fp32")
@@ -86,23 +86,28 @@ def _sketch_width(cfg: EstimatorConfig, n: int) -> int:
 
 
 def make_config(cfg: EstimatorConfig, n: int) -> N.Config:
-    """EstimatorConfig -> rld_config (validation mirrors src/estimators.py:41-45, src/precond.py:241-242)."""
-    if cfg.algorithm not in ("r1", "r3", "r5"):
-        raise ValueError(f"rstar_logdet got algorithm {cfg.algorithm!r}")
+    """EstimatorConfig -> rld_config (validation mirrors src/estimators.py:41-45, src/precond.py:241-242).
+
+    ``slq`` runs on K itself (src/estimators.py:106): the preconditioner fields are
+    not used, exactly as the reference ignores them."""
+    slq = cfg.algorithm == "slq"
+    if cfg.algorithm not in ("r1", "r3", "r5", "slq"):
+        raise ValueError(f"estimator got algorithm {cfg.algorithm!r}")
     if cfg.probe_kind not in PROBE_KINDS:
         raise ValueError(f"unknown probe kind {cfg.probe_kind!r}")
     if cfg.probe_kind not in DEVICE_PROBE_KINDS:
         raise NotImplementedError(f"probe kind {cfg.probe_kind!r} is outside the r* hot path")
-    if cfg.precond.kind not in DEVICE_PRECOND_KINDS:
+    if not slq and cfg.precond.kind not in DEVICE_PRECOND_KINDS:
         if cfg.precond.kind not in ("identity", "diagonal", "rank-one") and cfg.precond.rank > n:
             raise ValueError(f"rank {cfg.precond.rank} exceeds dimension {n}")
         raise NotImplementedError(f"preconditioner kind {cfg.precond.kind!r} is outside the r* hot path")
     c = N.Config()
-    c.order = int(cfg.algorithm[1])
+    c.estimator = N.ESTIMATOR_SLQ if slq else N.ESTIMATOR_RSTAR
+    c.order = 3 if slq else int(cfg.algorithm[1])
     c.num_probes = cfg.num_probes
     c.lanczos_iters = cfg.lanczos_iters
     c.probe_kind = DEVICE_PROBE_KINDS[cfg.probe_kind]
-    c.precond_kind = DEVICE_PRECOND_KINDS[cfg.precond.kind]
+    c.precond_kind = N.PRECOND_IDENTITY if slq else DEVICE_PRECOND_KINDS[cfg.precond.kind]
     c.precond_rank = cfg.precond.rank
     c.precond_iters = cfg.precond.num_iters
     c.oversample = OVERSAMPLE
@@ -159,16 +164,31 @@ def _call_with_retry(call, inputs: _Inputs, handle: N.Handle, what: str):
 
 def _result(res: N.Result, per: np.ndarray, start: float) -> LogDetEstimate:
     return LogDetEstimate(res.value, res.logdet_P, res.trace_term, per, time.perf_counter() - start,
-                          device_time=res.wall_time, phase_ms=tuple(res.phase_ms), kv_products=res.kv_products,
+                          clamped_eigs=int(res.clamped_eigs), device_time=res.wall_time, phase_ms=tuple(res.phase_ms), kv_products=res.kv_products,
                           kernel_launches=res.kernel_launches, rank_kept=res.rank_kept, attempts=res.attempts)
 
 
 def rstar_logdet(M, cfg: EstimatorConfig, probes=None, omega=None) -> LogDetEstimate:
     """Rational-approximation estimate of log det M (algorithms r1/r3/r5) on the GPU."""
-    from ._session import session
-
     if cfg.algorithm not in ("r1", "r3", "r5"):
         raise ValueError(f"rstar_logdet got algorithm {cfg.algorithm!r}")
+    return _run(M, cfg, probes, omega)
+
+
+def slq_logdet(M, cfg: EstimatorConfig, probes=None) -> LogDetEstimate:
+    """Stochastic Lanczos quadrature estimate of log det M (``src/estimators.py:99-122``):
+    Lanczos on M itself with full two-pass reorthogonalisation (no preconditioner),
+    the same probe stream as the rational estimators, Gauss quadrature of log on
+    each probe's tridiagonal (Ritz values <= 0 floored at 1e-300 and counted in
+    ``clamped_eigs``).  ``logdet_P`` is 0 and ``value == trace_term``."""
+    if cfg.algorithm != "slq":
+        raise ValueError(f"slq_logdet got algorithm {cfg.algorithm!r}")
+    return _run(M, cfg, probes, None)
+
+
+def _run(M, cfg: EstimatorConfig, probes, omega) -> LogDetEstimate:
+    from ._session import session
+
     start = time.perf_counter()
     sess = session()
     prob, keep = sess.problem_for(M, cfg.dtype, cfg.path)
@@ -202,9 +222,9 @@ def estimate_logdet(M, cfg: EstimatorConfig) -> LogDetEstimate:
     """Dispatch on cfg.algorithm (``src/estimators.py:132-138``)."""
     if cfg.algorithm in ("r1", "r3", "r5"):
         return rstar_logdet(M, cfg)
-    if cfg.algorithm == "exact":
-        return exact_logdet(M)
-    raise NotImplementedError("slq is a 'next' row (SURVEY.md §8(f)); not on this hot path yet")
+    if cfg.algorithm == "slq":
+        return slq_logdet(M, cfg)
+    return exact_logdet(M)
 
 
 class ResidentMatrix:

@@ -33,7 +33,7 @@ def test_library_loads_and_exports_every_symbol():
     lib = N.load()
     for name in declared_symbols():
         assert hasattr(lib, name), name
-    assert lib.rld_abi_version() == 1
+    assert lib.rld_abi_version() == N.ABI_VERSION == 2
 
 
 def test_library_is_sm100a():
@@ -52,6 +52,7 @@ int main(void) {
   P(rld_device_set) P(rld_problem) P(rld_config) P(rld_inputs) P(rld_result)
   O(rld_problem, data) O(rld_problem, ld) O(rld_config, probe_key) O(rld_config, omega_key)
   O(rld_config, diag_floor) O(rld_result, per_probe) O(rld_result, phase_ms) O(rld_inputs, memory)
+  O(rld_config, estimator) O(rld_result, clamped_eigs)
   return 0;
 }
 """
@@ -103,7 +104,7 @@ def test_config_validation_mirrors_reference():
     with pytest.raises(ValueError):
         KernelSpec(length_scale=0.0)
     with pytest.raises(ValueError):
-        make_config(EstimatorConfig(algorithm="slq"), 10)
+        make_config(EstimatorConfig(algorithm="exact"), 10)
     with pytest.raises(NotImplementedError):
         make_config(EstimatorConfig(precond=PreconditionerConfig("partial-cholesky", 5)), 10)
     with pytest.raises(ValueError):
@@ -117,6 +118,13 @@ def test_make_config_fields():
         (5, 16, 20, 64, 5, 10)
     assert (c.probe_key[0], c.probe_key[1]) == philox_key(7, (2,))
     assert (c.omega_key[2], c.omega_key[3]) == philox_key(7, (1, 1))
+
+
+def test_make_config_slq_runs_without_preconditioner():
+    # src/estimators.py:106: SLQ ignores the preconditioner config
+    c = make_config(EstimatorConfig("slq", 8, 20, precond=PreconditionerConfig("partial-cholesky", 5)), 100)
+    assert c.estimator == N.ESTIMATOR_SLQ and c.precond_kind == N.PRECOND_IDENTITY
+    assert make_config(EstimatorConfig("r3"), 100).estimator == N.ESTIMATOR_RSTAR
 
 
 def test_philox_key_is_numpy_state():

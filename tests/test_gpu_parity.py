@@ -310,3 +310,64 @@ def test_config3_full_size_properties(rld):
         k = O.covariance_block("matern52", 1.0, 0.05, 1e-2, wl.points, rows=slice(i, i + 1))[0]
         ref = V @ k
         assert np.max(np.abs(Y[:, i] - ref) / (np.abs(V) @ np.abs(k))) <= 2e-6
+
+
+# ---------------------------------------------------------------- SLQ
+
+def _slq_cases():
+    from conftest import load_golden
+
+    return load_golden("golden_slq.json")
+
+
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+@pytest.mark.parametrize("case", _slq_cases(), ids=lambda c: c["name"])
+def test_slq_matches_reference(rld, case, dtype):
+    """slq_logdet (src/estimators.py:99-122) on the device: Lanczos on K with full
+    reorthogonalisation, Gauss quadrature of log per probe, against the unmodified
+    reference's outputs (tests/golden/make_golden_slq.py)."""
+    from paper_2405_03474_b200.workloads import baseline
+
+    wl = baseline(case["config_index"], n=case["n"], num_probes=case["num_probes"])
+    cfg = replace(wl.config, algorithm="slq", dtype=dtype)
+    est = rld.estimate_logdet(rld.KernelMatrix(wl.spec, wl.points), cfg)
+    assert est.logdet_P == 0.0 and est.value == est.trace_term
+    assert rel(est.value, case["value"]) <= TOL[dtype], (est.value, case["value"])
+    if dtype == "fp64":
+        np.testing.assert_allclose(est.per_probe_values, case["per_probe"], rtol=1e-6)
+        assert est.clamped_eigs == case["clamped_eigs"]
+
+
+def test_slq_dense_input_deterministic(rld):
+    from paper_2405_03474_b200.workloads import baseline
+
+    wl = baseline(1, n=1024, num_probes=8)
+    K = O.covariance_block(wl.spec.family, wl.spec.amplitude, wl.spec.length_scale, wl.spec.jitter, wl.points)
+    cfg = replace(wl.config, algorithm="slq")
+    a = rld.slq_logdet(K, cfg)
+    b = rld.slq_logdet(K, cfg)
+    assert a.value == b.value
+    ref = O.slq_dense(K, s=8, t=20, probe_kind="rademacher", seed=0)
+    assert rel(a.value, ref.value) <= 1e-9
+
+
+def test_slq_on_the_fly_fp32(rld):
+    from paper_2405_03474_b200.workloads import baseline
+
+    wl = baseline(5, n=4096)
+    ref = [c for c in _slq_cases() if c["name"] == "slq_config5_n4096"][0]
+    cfg = replace(wl.config, algorithm="slq", dtype="fp32", path="on_the_fly")
+    est = rld.estimate_logdet(rld.KernelMatrix(wl.spec, wl.points), cfg)
+    assert rel(est.value, ref["value"]) <= TOL["fp32"]
+
+
+def test_slq_t_equals_n_is_exact(rld):
+    """t = n: the Gauss quadrature is exact, so SLQ returns mean |z|^2 e1^T log(K) e1
+    -- checked against the oracle at n = 20 (src/lanczos.py full-space reconstruction)."""
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((20, 20))
+    K = A @ A.T + 20 * np.eye(20)
+    cfg = rld.EstimatorConfig("slq", 4, 20)
+    est = rld.slq_logdet(K, cfg)
+    ref = O.slq_dense(K, s=4, t=20, seed=0)
+    assert rel(est.value, ref.value) <= 1e-10
