@@ -167,6 +167,20 @@ def barrier(world):
         dist.barrier()
 
 
+def ncu_traffic(name="kv_c2_m32"):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the newest
+    committed ncu --set full summary (profiles/*_kv_ncu.json, scripts/summarize_profiles.py)."""
+    files = sorted((ROOT / "profiles").glob("*_kv_ncu.json"), key=lambda p: p.stat().st_mtime)
+    for f in reversed(files):
+        try:
+            rec = json.loads(f.read_text()).get(name)
+        except Exception:
+            continue
+        if rec and "dram_bytes_total" in rec:
+            return rec["dram_bytes_total"], f.name
+    return None, None
+
+
 def workload_for(args):
     from paper_2405_03474_b200.workloads import baseline
 
@@ -304,6 +318,8 @@ def run_ours(args):
     kv_ms = k0.elapsed_time(k1) / reps
     alg_bytes = es * rows * n + 4 * n * s + 8 * rows * s
     hbm_peak, _, peak_kind = load_peaks()
+    traffic, traffic_src = (ncu_traffic() if (args.config == 2 and world == 1 and args.dtype in (None, "fp32"))
+                            else (None, None))
     achieved = alg_bytes / (kv_ms * 1e-3) / 1e9
 
     # ---- end to end through the public API (host buffers, pinned)
@@ -358,7 +374,9 @@ def run_ours(args):
         "kv_products_per_step": products // max(1, args.steps),
         "phase_ms_last_step": {"precond": phases[1], "lanczos": phases[4], "solves": phases[5]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None, "kernel": f"kv_product (Lanczos shape m=s, {rows} rows of K)",
+                     "frac": achieved / hbm_peak, "traffic": traffic,
+                     "traffic_source": traffic_src,
+                     "kernel": f"kv_product (Lanczos shape m=s, {rows} rows of K)",
                      "kernel_ms": kv_ms, "alg_bytes": alg_bytes, "peak_source": peak_kind},
         "clocks": clocks,
         "estimate": est.value,
