@@ -54,7 +54,7 @@ namespace {
 
 constexpr int TC_BM = 128;          // K rows per tile (UMMA M)
 constexpr int TC_BK = 32;           // fp32 k-elements per step (one 128-byte swizzle row)
-constexpr int TC_THREADS = 640;   // 20 warps: TMA, MMA, TMEM owner, idle, 8 converters, 8 drains
+constexpr int TC_THREADS = 640;   // 20 warps: TMA, 2 MMA, TMEM owner, 4 CP converters, 4 DP drains (CP + DP = 4)
 constexpr int GROUP = 4;            // k-steps accumulated in TMEM before the register flush
 constexpr int NABUF_MAX = 8;        // pipeline stages = TMEM A-operand buffers: as many as the 512 columns leave (<= 8)
 constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4;  // 16 KB
@@ -310,6 +310,12 @@ struct TcShape {
   static constexpr uint32_t STAGE = A_REGION + B_BYTES * (MODE == 3 ? 2 : 1);
   static constexpr uint32_t ASTRIDE = MODE == 3 ? 64 : 32;  // TMEM columns per A buffer (hi | lo)
   static constexpr uint32_t A_COL0 = 2 * DW;
+  // warps per TMEM lane quarter: drains (DP; each holds NT / DP fp32 running sums in
+  // registers) and converters (CP = 4 - DP), within the 20-warp CTA.  A third
+  // converter warp per quarter measured +6 % at NT = 64 (config 4 on the fly) and
+  // -10 % at NT = 32, where the extra polling warps cost more than they hide
+  static constexpr int DP = NT == 64 ? 1 : 2;
+  static constexpr int CP = 4 - DP;
   static constexpr int NABUF = (512 - 2 * DW) / (int)ASTRIDE < NABUF_MAX ? (512 - 2 * DW) / (int)ASTRIDE : NABUF_MAX;
   static constexpr int TMEM_NEED = 2 * DW + NABUF * (int)ASTRIDE;
   static constexpr uint32_t TMEM_COLS = TMEM_NEED <= 256 ? 256 : 512;
@@ -366,7 +372,7 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&accfull[b], 2);   // one commit per MMA-issuing warp
-      ptx::mbar_init(&accempty[b], 8);
+      ptx::mbar_init(&accempty[b], 4 * Sh::DP);
     }
     ptx::fence_mbarrier_init();
   }
@@ -485,13 +491,13 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       if (prof && lane == 0 && warp == 1) {
         prof[2] = t_acc; prof[4] = t_afull; prof[5] = t_iss; prof[6] = clock64() - t_start; prof[13] = 2 * nsteps;
       }
-    } else if (warp >= 4 && warp < 12) {
+    } else if (warp >= 4 && warp < 4 + 4 * Sh::CP) {
       // ---------------- converters: warp 4 + q + 4 par owns TMEM lanes 32q..32q+31 (K rows)
       // and the steps j with j % 2 == par (all 32 k-columns of each).  The two warps of
       // a sub-partition work on alternate steps, so one's generation overlaps the
       // other's TMEM stores; and each warp posts the afull arrive of a step only after
       // generating the first half of its next step, so tcgen05.wait::st rarely waits.
-      const int q = (warp - 4) & 3, par = (warp - 4) >> 2;
+      const int q = (warp - 4) & 3, par = (warp - 4) >> 2;   // steps j with j % CP == par
       const int row = q * 32 + lane;
       const uint32_t lane_base = (uint32_t)(q * 32) << 16;
       int cur_tile = -1;
@@ -510,8 +516,8 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       unsigned long long cv_full = 0;
       const unsigned long long cv_start = prof ? clock64() : 0;
       StepIter it(p.sched, cta, S, NA);
-      if (par) it.next();
-      for (; it.valid(); it.next(), it.next()) {
+      for (int k = 0; k < par; ++k) it.next();
+      for (; it.valid(); [&] { for (int k = 0; k < Sh::CP; ++k) it.next(); }()) {
         const int s = it.s;
         if constexpr (OTF) if (it.tile != cur_tile) {
           cur_tile = it.tile;
@@ -572,12 +578,13 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       if (prof && warp == 4 && lane == 0) {
         prof[7] = cv_full; prof[10] = clock64() - cv_start;
       }
-    } else if (warp >= 12) {
+    } else if (warp >= 4 + 4 * Sh::CP) {
       // ---------------- accumulator drain: warp 12 + q + 4h owns TMEM lanes 32q..32q+31 and
       // result columns [h NT/2, (h+1) NT/2); finished groups are added to fp32 registers
       // (round-to-nearest), a finished segment is stored to the partial buffer
-      constexpr int HALF = NT / 2;
-      const int q = (warp - 12) & 3, hsel = (warp - 12) >> 2;
+      constexpr int HALF = NT / Sh::DP;
+      const int dw = warp - (4 + 4 * Sh::CP);
+      const int q = dw & 3, hsel = dw >> 2;
       const int row = q * 32 + lane;
       const uint32_t lane_base = (uint32_t)(q * 32) << 16;
       const int c_base = hsel * HALF;
@@ -625,7 +632,7 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
           }
         }
       }
-      if (prof && warp == 12 && lane == 0) {
+      if (prof && dw == 0 && lane == 0) {
         prof[11] = dr_wait; prof[12] = clock64() - dr_start;
       }
     }
