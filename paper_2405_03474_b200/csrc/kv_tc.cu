@@ -1,28 +1,30 @@
 // K x block products on the 5th-generation tensor cores (tcgen05, kind::tf32).
 //
 // Y[c, i] = sum_j K[i, j] V[c, j] for a stored float32 K (the HBM-streaming
-// path of BASELINE configs 2-3; reference call sites src/estimators.py:72 and
-// src/precond.py:186, 189).
+// path of BASELINE configs 2-3) or for K tiles generated on the fly from the
+// points (configs 4-5); reference call sites src/estimators.py:72 and
+// src/precond.py:186, 189.
 //
 // One persistent CTA per SM, 20 warps:
-//   warp 0       TMA producer: K tile (128 rows x 32 fp32, 128B-swizzled) plus the
-//                B tiles (NT vectors x 32 fp32: tf32-hi, and lo for 3xTF32) per
-//                k-step into an S-stage shared-memory ring (full/empty mbarriers).
-//   warps 4-11   converters (two per TMEM lane quarter, 16 of the 32 k-columns each):
-//                thread = one K row; it reads its values from the swizzled tile (or
-//                generates them from the points), splits them into tf32 hi + lo
-//                (lo exact in fp32) and tcgen05.st's them into one of NABUF TMEM
-//                A-operand buffers, so the tensor core never re-reads A from SMEM.
-//   warp 1       MMA issuer (whole warp walks the pipeline so every descriptor is
-//                warp-uniform; one elected lane issues).  3xTF32 per 8-wide k chunk:
+//   warp 0       TMA producer: per k-step, the K tile (128 rows x 32 fp32,
+//                128B-swizzled) or the 32 column points (on the fly), plus the B
+//                tiles (NT vectors x 32 fp32: tf32-hi, and lo for 3xTF32, stored in
+//                k-step blocks so each box is contiguous) into an S-stage ring.
+//   warps 1, 3   MMA issuers, alternate k-steps, handing a named-barrier baton so
+//                the tensor core sees one fixed instruction order while each warp's
+//                mbarrier wait and commit overlap the other's MMAs.  3xTF32 per
+//                8-wide k chunk:
 //                  NT == 32: D[2NT] += Ahi [Bhi; Blo] + Alo [Bhi; Blo] (two N = 64
-//                            instructions -- small N costs the same ~45 cycles as
-//                            N = 64, so stacking hi/lo B halves the issue count);
+//                            instructions: small N costs the same as N = 64);
 //                  NT >= 64: D[NT] += Ahi Bhi + Ahi Blo + Alo Bhi.
 //                1xTF32 (optional sketch mode): D[NT] += A Bhi.
-//   warps 12-19  accumulator drain (two warps per TMEM lane quarter, one half of
-//                the result columns each).
 //   warp 2       TMEM allocation owner.
+//   4 CP warps   converters (CP per TMEM lane quarter, alternate k-steps): thread = one
+//                K row; it reads its 32 values from the swizzled tile or generates
+//                them from the points (FFMA2 + MUFU sqrt/ex2), splits them into tf32
+//                hi + lo (lo exact in fp32) and tcgen05.st's them into a TMEM
+//                A-operand buffer, so the tensor core never re-reads A from SMEM.
+//   4 DP warps   accumulator drains (CP + DP = 4 per quarter).
 //
 // Accuracy: the tensor core rounds its fp32 accumulator toward zero, so a long
 // accumulation drifts (measured -2e-4 relative at n = 16384, -9e-4 at 65536).
@@ -30,12 +32,12 @@
 // accumulators; the drain warps add each finished group into fp32 registers
 // with round-to-nearest while the tensor core fills the other accumulator.
 //
-// Work split: "stream-K" -- the tiles x k-steps space is cut into equal
-// contiguous ranges, so every SM streams the same number of K bytes; a tile
-// shared by several CTAs leaves per-CTA partial sums that kv_tc_reduce adds in
-// fixed CTA order, in float64 (deterministic).  Column passes (more vectors than
-// one TMEM accumulator holds) run as concurrent CTA groups of the same launch so
-// K streams from HBM about once.
+// Work split (Sched): full rounds of G row tiles, all CTAs sweeping k in step
+// (kept within an epoch of each other by a producer barrier) so L2 serves the B
+// operand to every CTA; the tail tiles are cut into equal stream-K ranges whose
+// per-CTA partial sums kv_tc_reduce adds in fixed order, in float64
+// (deterministic).  Column passes (more vectors than one TMEM accumulator holds)
+// run as concurrent CTA groups of the same launch so K streams from HBM once.
 #include <cuda.h>
 
 #include <cmath>
