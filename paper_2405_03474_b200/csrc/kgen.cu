@@ -8,6 +8,8 @@
 //
 // One CTA writes a 32-row x 256-column tile; each thread owns one column and
 // walks the 32 rows, so every row store is a coalesced 256-element segment.
+// Point dimension and kernel family are template parameters (no per-entry
+// branches, the column point stays in registers).
 #include "rld_internal.cuh"
 #include "rld_device.cuh"
 
@@ -18,12 +20,13 @@ namespace {
 constexpr int KG_ROWS = 32;
 constexpr int KG_COLS = 256;
 
-template <typename T>
+// DIM > 0: compile-time point dimension (registers only); DIM == 0: runtime d <= RLD_MAX_DIM.
+template <typename T, int DIM, int FAM>
 __global__ void __launch_bounds__(KG_COLS)
 kgen_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, int64_t row0, int64_t rows,
             T* __restrict__ K, int64_t ld) {
   extern __shared__ double sm[];
-  const int d = kp.d;
+  const int d = DIM > 0 ? DIM : kp.d;
   double* xr = sm;                       // KG_ROWS x d
   const int64_t i0 = (int64_t)blockIdx.y * KG_ROWS;
   const int64_t j = (int64_t)blockIdx.x * KG_COLS + threadIdx.x;
@@ -33,23 +36,42 @@ kgen_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, int64_t ro
   }
   __syncthreads();
   if (j >= n) return;
-  double xc[RLD_MAX_DIM];
+  constexpr int DD = DIM > 0 ? DIM : RLD_MAX_DIM;
+  double xc[DD];
 #pragma unroll
-  for (int k = 0; k < RLD_MAX_DIM; ++k) xc[k] = (k < d) ? X[j * d + k] : 0.0;
+  for (int k = 0; k < DD; ++k) xc[k] = (k < d) ? X[j * d + k] : 0.0;
   const int rmax = (int)min64(KG_ROWS, rows - i0);
+  T* out = K + i0 * ld + j;
+  const int64_t gi0 = row0 + i0;
   for (int r = 0; r < rmax; ++r) {
     double r2 = 0.0;
 #pragma unroll
-    for (int k = 0; k < RLD_MAX_DIM; ++k) {
-      if (k < d) {
-        double diff = xr[r * d + k] - xc[k];
+    for (int k = 0; k < DD; ++k) {
+      if (DIM > 0 || k < d) {
+        const double diff = xr[r * d + k] - xc[k];
         r2 = fma(diff, diff, r2);
       }
     }
-    const int64_t gi = row0 + i0 + r;
-    double v = (gi == j) ? kp.diag : kernel_value_f64(kp, r2);
-    K[(i0 + r) * ld + j] = (T)v;
+    double v;
+    if (FAM == RLD_RBF) {
+      v = kp.a2 * exp(-r2 * kp.inv_2l2);
+    } else {
+      const double u = sqrt(r2) * kp.s5_over_l;
+      v = kp.a2 * (1.0 + u + u * u * (1.0 / 3.0)) * exp(-u);
+    }
+    if (gi0 + r == j) v = kp.diag;
+    out[(int64_t)r * ld] = (T)v;
   }
+}
+
+template <typename T, int DIM>
+void launch_kgen(dim3 grid, size_t smem, const double* X, int64_t n, const KernelParams& kp, int64_t row0,
+                 int64_t rows, T* K, int64_t ld, cudaStream_t st) {
+  if (kp.family == RLD_RBF)
+    kgen_kernel<T, DIM, RLD_RBF><<<grid, KG_COLS, smem, st>>>(X, n, kp, row0, rows, K, ld);
+  else
+    kgen_kernel<T, DIM, RLD_MATERN52><<<grid, KG_COLS, smem, st>>>(X, n, kp, row0, rows, K, ld);
+  RLD_LAUNCH_CHECK();
 }
 
 }  // namespace
@@ -60,8 +82,14 @@ void build_kernel_rows(const double* X, int64_t n, const KernelParams& kp, int64
   if (rows <= 0) return;
   dim3 grid((unsigned)ceil_div(n, KG_COLS), (unsigned)ceil_div(rows, KG_ROWS));
   size_t smem = sizeof(double) * KG_ROWS * kp.d;
-  kgen_kernel<T><<<grid, KG_COLS, smem, st>>>(X, n, kp, row0, rows, K, ld);
-  RLD_LAUNCH_CHECK();
+  switch (kp.d) {   // the BASELINE configs use d = 2, 3, 8
+    case 1: launch_kgen<T, 1>(grid, smem, X, n, kp, row0, rows, K, ld, st); break;
+    case 2: launch_kgen<T, 2>(grid, smem, X, n, kp, row0, rows, K, ld, st); break;
+    case 3: launch_kgen<T, 3>(grid, smem, X, n, kp, row0, rows, K, ld, st); break;
+    case 4: launch_kgen<T, 4>(grid, smem, X, n, kp, row0, rows, K, ld, st); break;
+    case 8: launch_kgen<T, 8>(grid, smem, X, n, kp, row0, rows, K, ld, st); break;
+    default: launch_kgen<T, 0>(grid, smem, X, n, kp, row0, rows, K, ld, st); break;
+  }
 }
 
 template void build_kernel_rows<double>(const double*, int64_t, const KernelParams&, int64_t, int64_t,

@@ -79,6 +79,7 @@ struct Sched {
 struct TcParams {
   Sched sched;      // work schedule (per column pass)
   int mp;           // B rows per k-step block (vectors padded to npass x NT)
+  int bcol_step, brow_step;   // TMA coordinates of B per k-step: blocked (0, mp) or row-major (32, 0)
   unsigned int* sync;   // per-pass arrival counters of the phase-1 epoch barrier (zeroed per launch)
   int sync_k;           // k-steps per epoch (0: no barrier)
   int ks;           // k-steps per tile
@@ -155,30 +156,31 @@ __host__ __device__ __forceinline__ int64_t cta_of_step(int64_t x, int64_t total
   return ((x + 1) * G - 1) / total;
 }
 
-// Walks a CTA's steps with running counters (no 64-bit divisions in the loops).
+// Walks a CTA's steps with running 32-bit counters (no divisions in the loops:
+// the pipeline warps run this once per k-step, inside their critical loops, and
+// each role pays only for the counters it uses: GRP = group boundaries (MMA),
+// ABUF = TMEM A buffer and the lagged stage ring (MMA, converters)).
+template <bool GRP, bool ABUF>
 struct StepIter {
-  int64_t v, vend;       // virtual step index and end: [0, R ks) phase 1, then the tail range
-  int64_t j;             // step counter (== v)
-  int64_t tail_x;        // position in the tail space (phase 2)
-  int ks, kstep, tile, gpos, s, S, G, R, round;
-  int64_t cta, tail_end;
+  int v, vend;           // step index (== pipeline slot j) and end: [0, R ks) phase 1, then the tail range
+  int ks, kstep, tile, s, S, G, R, round;
+  int tail_next, tail_k0;   // where the tail range starts (tile, k-step)
   uint32_t ph;
-  int ab, NA;            // TMEM A buffer of step j (j % NA)
-  int ls;                // stage of step j - NA (valid for j >= NA) and its phase parity
-  uint32_t lph;
-  int64_t tail_total;
-  __device__ __forceinline__ StepIter(const Sched& sc, int64_t cta_, int S_, int NA_)
-      : v(0), j(0), ks(sc.ks), kstep(0), gpos(0), s(0), S(S_), G(sc.G), R(sc.R), round(0), cta(cta_), ph(0),
-        ab(0), NA(NA_), ls(0), lph(0), tail_total(sc.tail_total) {
-    const int64_t tb = sc.tail_beg(cta_);
-    tail_end = sc.tail_end(cta_);
-    vend = (int64_t)R * ks + (tail_end - tb);
-    tail_x = tb;
+  int gpos = 0;          // GRP: position in the accumulation group
+  int ab = 0, NA = 1;    // ABUF: TMEM A buffer of step j (j % NA)
+  int ls = 0;            // ABUF: stage of step j - NA (valid for j >= NA) and its phase parity
+  uint32_t lph = 0;
+  __device__ __forceinline__ StepIter(const Sched& sc, int64_t cta, int S_, int NA_ = 1)
+      : v(0), ks(sc.ks), kstep(0), s(0), S(S_), G(sc.G), R(sc.R), round(0), ph(0), NA(NA_) {
+    const int64_t tb = sc.tail_beg(cta), te = sc.tail_end(cta);
+    vend = R * ks + (int)(te - tb);
+    tail_next = R * G + (int)(tb / ks);
+    tail_k0 = (int)(tb - (int64_t)(tb / ks) * ks);
     if (R > 0) {
-      tile = (int)cta_;
+      tile = (int)cta;
     } else {
-      tile = R * G + (int)(tb / ks);
-      kstep = (int)(tb - (int64_t)(tile - R * G) * ks);
+      tile = tail_next;
+      kstep = tail_k0;
     }
   }
   __device__ __forceinline__ bool valid() const { return v < vend; }
@@ -186,27 +188,17 @@ struct StepIter {
   __device__ __forceinline__ bool group_start() const { return gpos == 0; }
   __device__ __forceinline__ bool seg_end() const { return v + 1 == vend || kstep + 1 == ks; }
   __device__ __forceinline__ bool group_end() const { return seg_end() || gpos + 1 == GROUP; }
-  // partial-sum slot of this step's tile segment
-  __device__ __forceinline__ int seg() const {
-    if (!in_tail()) return 0;
-    const int64_t x0 = (int64_t)(tile - R * G) * ks;
-    return (int)(cta - cta_of_step(x0, tail_total, G));
-  }
   __device__ __forceinline__ void next() {
-    gpos = group_end() ? 0 : gpos + 1;
+    if (GRP) gpos = group_end() ? 0 : gpos + 1;
     ++v;
-    ++j;
-    if (in_tail()) ++tail_x;
     if (++kstep == ks) {
       kstep = 0;
-      if (!in_tail()) {
-        ++round;
-        if (round < R) {
+      if (round < R) {
+        if (++round < R) {
           tile += G;
-        } else {   // enter the tail range
-          const int64_t tb = tail_x;
-          tile = R * G + (int)(tb / ks);
-          kstep = (int)(tb - (int64_t)(tile - R * G) * ks);
+        } else {   // phase 1 done: continue in the tail range
+          tile = tail_next;
+          kstep = tail_k0;
         }
       } else {
         ++tile;
@@ -216,11 +208,44 @@ struct StepIter {
       s = 0;
       ph ^= 1;
     }
-    if (++ab == NA) ab = 0;
-    if (j > NA && ++ls == S) {   // the lagged ring starts at stage 0, parity 0 when j == NA
-      ls = 0;
-      lph ^= 1;
+    if (ABUF) {
+      if (++ab == NA) ab = 0;
+      if (v > NA && ++ls == S) {   // the lagged ring starts at stage 0, parity 0 when j == NA
+        ls = 0;
+        lph ^= 1;
+      }
     }
+  }
+};
+
+// Segment (tile, first step, steps) iteration for the drain warps: one call per
+// segment instead of one StepIter advance per k-step.
+struct SegIter {
+  int64_t cta;
+  const Sched* sc;
+  int r;                 // phase-1 round, then R for the tail
+  int64_t x, xe;         // tail-space position and end
+  __device__ __forceinline__ SegIter(const Sched& s, int64_t c) : cta(c), sc(&s), r(0) {
+    x = s.tail_beg(c);
+    xe = s.tail_end(c);
+  }
+  // next segment: tile, its length in k-steps and its partial-sum slot; false when done
+  __device__ __forceinline__ bool next(int& tile, int& len, int& seg) {
+    if (r < sc->R) {
+      tile = (int)cta + r * sc->G;
+      len = sc->ks;
+      seg = 0;
+      ++r;
+      return true;
+    }
+    if (x >= xe) return false;
+    const int64_t u = x / sc->ks;
+    const int64_t x0 = u * sc->ks;
+    tile = sc->R * sc->G + (int)u;
+    len = (int)(std::min<int64_t>(xe, x0 + sc->ks) - x);
+    seg = (int)(cta - cta_of_step(x0, sc->tail_total, sc->G));
+    x += len;
+    return true;
   }
 };
 
@@ -384,18 +409,18 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
-  if (StepIter(p.sched, cta, 1, 1).valid()) {
+  if (StepIter<false, false>(p.sched, cta, 1).valid()) {
     if (warp == 0) {
       // ---------------- TMA producer (whole warp walks the ring; one elected lane issues)
       unsigned long long t_wait = 0;
       const unsigned long long t_start = prof ? clock64() : 0;
       int64_t epoch = 0;
-      for (StepIter it(p.sched, cta, S, NA); it.valid(); it.next()) {
+      for (StepIter<false, false> it(p.sched, cta, S); it.valid(); it.next()) {
         const int s = it.s;
         // phase-1 epoch barrier: the CTAs' producers meet every sync_k k-steps, so all
         // CTAs stream the same window of B and L2 serves it (their drift otherwise
         // accumulates tile after tile until B comes from HBM once per tile)
-        if (p.sync_k > 0 && !it.in_tail() && it.v > 0 && it.kstep % p.sync_k == 0) {
+        if (p.sync_k > 0 && !it.in_tail() && it.v > 0 && (it.kstep & (p.sync_k - 1)) == 0) {
           ++epoch;
           if (lane == 0) {
             unsigned int* ctr = p.sync + pass;
@@ -418,8 +443,10 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             if (!(p.debug & 4)) ptx::tma_load_2d(st, &tmA, &full[s], it.kstep * TC_BK, it.tile * TC_BM);
           }
           // B in k-step blocks [ks][mp][32]: one contiguous NT x 128-byte box per step
-          ptx::tma_load_2d(st + AR, &tmBhi, &full[s], 0, it.kstep * p.mp + b_row0);
-          if (MODE == 3) ptx::tma_load_2d(st + AR + B_BYTES, &tmBlo, &full[s], 0, it.kstep * p.mp + b_row0);
+          ptx::tma_load_2d(st + AR, &tmBhi, &full[s], it.kstep * p.bcol_step, it.kstep * p.brow_step + b_row0);
+          if (MODE == 3)
+            ptx::tma_load_2d(st + AR + B_BYTES, &tmBlo, &full[s], it.kstep * p.bcol_step,
+                             it.kstep * p.brow_step + b_row0);
         }
         __syncwarp();
       }
@@ -442,16 +469,16 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       int64_t gi = -1;  // group index
       unsigned long long t_acc = 0, t_afull = 0, t_iss = 0, nsteps = 0;
       const unsigned long long t_start = prof ? clock64() : 0;
-      for (StepIter it(p.sched, cta, S, NA); it.valid(); it.next()) {
+      for (StepIter<true, true> it(p.sched, cta, S, NA); it.valid(); it.next()) {
         const bool gstart = it.group_start(), gend = it.group_end();
         if (gstart) ++gi;
-        if ((int)(it.j & 1) == mpar) {
+        if ((it.v & 1) == mpar) {
           const int s = it.s;
           const unsigned long long t0 = prof ? clock64() : 0;
           if (gstart && gi >= 2) ptx::mbar_wait(&accempty[gi & 1], (uint32_t)(((gi >> 1) - 1) & 1));
           ptx::mbar_wait(&afull[s], it.ph);
           const unsigned long long t1 = prof ? clock64() : 0;
-          if (it.j > 0) ptx::named_bar_sync(mpar ? 1 : 2, 64);   // baton from step j - 1
+          if (it.v > 0) ptx::named_bar_sync(mpar ? 1 : 2, 64);   // baton from step j - 1
           const unsigned long long t2 = prof ? clock64() : 0;
           ptx::tc_fence_after();
           const uint32_t d = tmem + (uint32_t)(gi & 1) * DW;
@@ -517,7 +544,7 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       };
       unsigned long long cv_full = 0;
       const unsigned long long cv_start = prof ? clock64() : 0;
-      StepIter it(p.sched, cta, S, NA);
+      StepIter<false, true> it(p.sched, cta, S, NA);
       for (int k = 0; k < par; ++k) it.next();
       for (; it.valid(); [&] { for (int k = 0; k < Sh::CP; ++k) it.next(); }()) {
         const int s = it.s;
@@ -536,7 +563,7 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         }
         const unsigned long long c0 = prof ? clock64() : 0;
         ptx::mbar_wait(&full[s], it.ph);
-        if (S > NA && it.j >= NA) ptx::mbar_wait(&empty[it.ls], it.lph);   // TMEM buffer free
+        if (S > NA && it.v >= NA) ptx::mbar_wait(&empty[it.ls], it.lph);   // TMEM buffer free
         if (prof) cv_full += clock64() - c0;
         ptx::tc_fence_after();
         const uint32_t ta = tmem + lane_base + A_COL0 + ASTRIDE * it.ab;
@@ -596,42 +623,43 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       int64_t gi = -1;
       unsigned long long dr_wait = 0;
       const unsigned long long dr_start = prof ? clock64() : 0;
-      for (StepIter it(p.sched, cta, 1, 1); it.valid(); it.next()) {
-        if (!it.group_end()) continue;
-        ++gi;
-        const int buf = (int)(gi & 1);
-        const unsigned long long d0 = prof ? clock64() : 0;
-        ptx::mbar_wait_idle(&accfull[buf], (uint32_t)((gi >> 1) & 1), p.wait_mode, p.wait_ns);
-        if (prof) dr_wait += clock64() - d0;
-        ptx::tc_fence_after();
-        if (!(p.debug & 32)) {
+      SegIter si(p.sched, cta);
+      int tile = 0, len = 0, seg = 0;
+      while (si.next(tile, len, seg)) {
+        for (int g0 = 0; g0 < len; g0 += GROUP) {
+          ++gi;
+          const int buf = (int)(gi & 1);
+          const unsigned long long d0 = prof ? clock64() : 0;
+          ptx::mbar_wait_idle(&accfull[buf], (uint32_t)((gi >> 1) & 1), p.wait_mode, p.wait_ns);
+          if (prof) dr_wait += clock64() - d0;
+          ptx::tc_fence_after();
+          if (!(p.debug & 32)) {
 #pragma unroll
-          for (int c0 = 0; c0 < HALF; c0 += 16) {
-            uint32_t v[16];
-            ptx::tmem_ld_32x32b_x16(tmem + lane_base + (uint32_t)(buf * DW + c_base + c0), v);
-            if (Sh::STACK) {
-              uint32_t w[16];
-              ptx::tmem_ld_32x32b_x16(tmem + lane_base + (uint32_t)(buf * DW + NT + c_base + c0), w);
-              ptx::tmem_wait_ld();
+            for (int c0 = 0; c0 < HALF; c0 += 16) {
+              uint32_t v[16];
+              ptx::tmem_ld_32x32b_x16(tmem + lane_base + (uint32_t)(buf * DW + c_base + c0), v);
+              if (Sh::STACK) {
+                uint32_t w[16];
+                ptx::tmem_ld_32x32b_x16(tmem + lane_base + (uint32_t)(buf * DW + NT + c_base + c0), w);
+                ptx::tmem_wait_ld();
 #pragma unroll
-              for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]) + __uint_as_float(w[e]);
-            } else {
-              ptx::tmem_wait_ld();
+                for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]) + __uint_as_float(w[e]);
+              } else {
+                ptx::tmem_wait_ld();
 #pragma unroll
-              for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]);
+                for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]);
+              }
             }
           }
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&accempty[buf]);
         }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&accempty[buf]);
-        if (it.seg_end()) {
-          float* P = partial + ((size_t)it.tile * p.segs + it.seg()) * (size_t)NT * TC_BM;
+        float* P = partial + ((size_t)tile * p.segs + seg) * (size_t)NT * TC_BM;
 #pragma unroll
-          for (int c = 0; c < HALF; ++c) {
-            P[(size_t)(c_base + c) * TC_BM + row] = acc[c];
-            acc[c] = 0.f;
-          }
+        for (int c = 0; c < HALF; ++c) {
+          P[(size_t)(c_base + c) * TC_BM + row] = acc[c];
+          acc[c] = 0.f;
         }
       }
       if (prof && dw == 0 && lane == 0) {
@@ -672,13 +700,13 @@ __global__ void kv_tc_reduce(const float* __restrict__ P, Sched sc, int tiles, i
 // makes every pipeline step's TMA box one contiguous NT x 128-byte range, instead of
 // NT rows n*4 bytes apart (256 distinct 2 MB pages per box at n = 2^20).
 __global__ void kv_tc_split(const double* __restrict__ V, int64_t ldv, int64_t m, int64_t n, int64_t mp, int64_t ks,
-                            int mode, float* __restrict__ Bhi, float* __restrict__ Blo) {
+                            int mode, int blocked, float* __restrict__ Bhi, float* __restrict__ Blo) {
   const int64_t count = mp * ks * 32;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = e / (ks * 32), j = e % (ks * 32);
     const double v = (c < m && j < n) ? V[c * ldv + j] : 0.0;
-    const int64_t o = ((j >> 5) * mp + c) * 32 + (j & 31);
+    const int64_t o = blocked ? ((j >> 5) * mp + c) * 32 + (j & 31) : c * (ks * 32) + j;
     float h = (float)v;
     if (mode == 3) {
       h = __uint_as_float(__float_as_uint(h) & 0xFFFFE000u);
@@ -803,6 +831,13 @@ CUtensorMap make_points_map(const float* pts, int64_t n) {
   return m;
 }
 
+// B operand layout: k-step blocks (default; contiguous TMA boxes) or row-major
+// vectors (RLD_TC_BLAYOUT=0), for A/B measurements.
+bool blocked_b() {
+  static const bool b = !(getenv("RLD_TC_BLAYOUT") && getenv("RLD_TC_BLAYOUT")[0] == '0');
+  return b;
+}
+
 }  // namespace
 
 bool kv_tc_supported(const KvOperand& op) {
@@ -826,7 +861,7 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
   {
     const int64_t count = mp * ks * 32;
     const int blocks = (int)std::min<int64_t>(ceil_div(count, 256), 148 * 16);
-    kv_tc_split<<<blocks, 256, 0, st>>>(V, ldv, m, n, mp, ks, mode, ws.bhi.as<float>(),
+    kv_tc_split<<<blocks, 256, 0, st>>>(V, ldv, m, n, mp, ks, mode, blocked_b(), ws.bhi.as<float>(),
                                         mode == 3 ? ws.blo.as<float>() : nullptr);
     RLD_LAUNCH_CHECK();
   }
@@ -881,7 +916,12 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
     p.prof = prof_buf.as<unsigned long long>();
   }
   {
-    static const int sync_k = getenv("RLD_TC_SYNC_K") ? atoi(getenv("RLD_TC_SYNC_K")) : 2048;
+    static const int sync_k = [] {   // power of two (the producer tests kstep & (sync_k - 1))
+      int v = getenv("RLD_TC_SYNC_K") ? atoi(getenv("RLD_TC_SYNC_K")) : 2048;
+      int pw = 0;
+      while (v > 1 && (1 << (pw + 1)) <= v) ++pw;
+      return v > 0 ? (1 << pw) : 0;
+    }();
     p.sync_k = (sc.R > 1 || (sc.R == 1 && sc.tail_total > 0)) ? sync_k : 0;
     ws.tc_sync.reserve(sizeof(unsigned int) * npass);
     p.sync = ws.tc_sync.as<unsigned int>();
@@ -889,8 +929,12 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
   }
   ws.tc_partial.reserve(sizeof(float) * (size_t)npass * tiles * segs * width * TC_BM);
   p.partial = ws.tc_partial.as<float>();
-  const CUtensorMap mBh = make_map(ws.bhi.as<float>(), TC_BK, mp * ks, TC_BK, width);
-  const CUtensorMap mBl = mode == 3 ? make_map(ws.blo.as<float>(), TC_BK, mp * ks, TC_BK, width) : mBh;
+  const bool blk = blocked_b();
+  const int64_t bcols = blk ? TC_BK : (int64_t)ks * TC_BK, brows = blk ? mp * ks : mp;
+  const CUtensorMap mBh = make_map(ws.bhi.as<float>(), bcols, brows, bcols, width);
+  const CUtensorMap mBl = mode == 3 ? make_map(ws.blo.as<float>(), bcols, brows, bcols, width) : mBh;
+  p.bcol_step = blk ? 0 : TC_BK;
+  p.brow_step = blk ? (int)mp : 0;
   if (otf) {
     launch_tc_otf(op.kp.d, op.kp.family, width, mA, mBh, mBl, p, Gl * npass, st);
   } else {

@@ -688,8 +688,12 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
   int products = 0;
   for (int j = 0; j < t; ++j) {
     if (slq) copy_doubles(s * nl, x, Qb + (size_t)j * s * nl, st);
-    gather_rows(h, x, s, xfull);
-    kv(h, s, xfull, KX);                                  // K x_j
+    const double* xin = x;                                // one GPU: the local rows are the full rows
+    if (h->world > 1) {
+      gather_rows(h, x, s, xfull);
+      xin = xfull;
+    }
+    kv(h, s, xin, KX);                                    // K x_j
     ++products;
     rows_dot(s, nl, x, nl, KX, nl, dots, wk.scratch, st, nullptr);
     allreduce_sum(h, dots, s);
