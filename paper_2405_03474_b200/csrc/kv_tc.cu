@@ -86,7 +86,7 @@ struct TcParams {
   int tiles;
   int npass;        // column passes in this launch
   int segs;         // partial slots per tile
-  int stages;
+  int sa, sb;       // A-source ring and B ring (= TMEM A buffers) depths
   uint32_t tmem_cols;
   float* partial;   // [npass][tiles][segs][NT][128]
   int wait_mode;    // producer / drain wait strategy (RLD_TC_WAIT, see ptx::mbar_wait_idle)
@@ -159,19 +159,19 @@ __host__ __device__ __forceinline__ int64_t cta_of_step(int64_t x, int64_t total
 // Walks a CTA's steps with running 32-bit counters (no divisions in the loops:
 // the pipeline warps run this once per k-step, inside their critical loops, and
 // each role pays only for the counters it uses: GRP = group boundaries (MMA),
-// ABUF = TMEM A buffer and the lagged stage ring (MMA, converters)).
-template <bool GRP, bool ABUF>
+// BR = a second ring (the converters walk the A-source ring in (s, ph) and the
+// B / TMEM-buffer ring in (sb, phb))).
+template <bool GRP, bool BR>
 struct StepIter {
   int v, vend;           // step index (== pipeline slot j) and end: [0, R ks) phase 1, then the tail range
   int ks, kstep, tile, s, S, G, R, round;
   int tail_next, tail_k0;   // where the tail range starts (tile, k-step)
   uint32_t ph;
   int gpos = 0;          // GRP: position in the accumulation group
-  int ab = 0, NA = 1;    // ABUF: TMEM A buffer of step j (j % NA)
-  int ls = 0;            // ABUF: stage of step j - NA (valid for j >= NA) and its phase parity
-  uint32_t lph = 0;
-  __device__ __forceinline__ StepIter(const Sched& sc, int64_t cta, int S_, int NA_ = 1)
-      : v(0), ks(sc.ks), kstep(0), s(0), S(S_), G(sc.G), R(sc.R), round(0), ph(0), NA(NA_) {
+  int sb = 0, SB = 1;    // BR: second ring
+  uint32_t phb = 0;
+  __device__ __forceinline__ StepIter(const Sched& sc, int64_t cta, int S_, int SB_ = 1)
+      : v(0), ks(sc.ks), kstep(0), s(0), S(S_), G(sc.G), R(sc.R), round(0), ph(0), SB(SB_) {
     const int64_t tb = sc.tail_beg(cta), te = sc.tail_end(cta);
     vend = R * ks + (int)(te - tb);
     tail_next = R * G + (int)(tb / ks);
@@ -208,12 +208,9 @@ struct StepIter {
       s = 0;
       ph ^= 1;
     }
-    if (ABUF) {
-      if (++ab == NA) ab = 0;
-      if (v > NA && ++ls == S) {   // the lagged ring starts at stage 0, parity 0 when j == NA
-        ls = 0;
-        lph ^= 1;
-      }
+    if (BR && ++sb == SB) {
+      sb = 0;
+      phb ^= 1;
     }
   }
 };
@@ -356,28 +353,32 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
              const __grid_constant__ CUtensorMap tmBlo, const TcParams p) {
   using Sh = TcShape<MODE, NT, OTF>;
   constexpr int DW = Sh::DW;
-  constexpr uint32_t B_BYTES = Sh::B_BYTES, STAGE = Sh::STAGE, ASTRIDE = Sh::ASTRIDE, A_COL0 = Sh::A_COL0;
+  constexpr uint32_t B_BYTES = Sh::B_BYTES, ASTRIDE = Sh::ASTRIDE, A_COL0 = Sh::A_COL0;
   constexpr uint32_t AR = Sh::A_REGION;   // K tile (stored) or column points (on the fly)
   extern __shared__ __align__(16) uint8_t smem_raw[];
   // 1024-byte aligned base, derived from smem_raw so the compiler keeps the shared
   // address space (plain C++ loads compile to LDS and are ordered by the mbarrier asm)
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-  // Step j uses ring stage s = j % S and TMEM A buffer b = j % NA:
-  //   full[s]   TMA bytes landed                      (producer -> converters)
-  //   afull[s]  A tile converted into TMEM buffer b   (4 converter warps -> MMA)
-  //   empty[s]  MMAs of the step completed            (tcgen05.commit -> producer, converters)
-  // Buffer b is free for step j once the MMAs of step j - NA completed: the converters
-  // wait on empty[] of that step's stage (implied by full[s] when S <= NA, since the
-  // producer waited for step j - S).  The MMA warp needs only afull[s]: the converters
-  // arrive after they observed full[s].  One wait and one commit per step keep the
-  // serial MMA-issue loop short (each mbarrier wait costs ~90 cycles and each commit
-  // ~100 even when nothing blocks).
-  const int S = p.stages;
-  constexpr int NA = Sh::NABUF;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * STAGE);
-  uint64_t* empty = full + S;
-  uint64_t* afull = empty + S;
-  uint64_t* accfull = afull + S;     // [2]
+  // Two rings.  Step j reads its A source (K tile, or the 32 column points on the
+  // fly) from A-ring stage j % SA and its B tiles from B-ring stage j % SB; TMEM A
+  // buffer j % SB goes with the B stage (NA == SB):
+  //   kfull/kempty[SA]   K tile landed / read by the 4 converter warps of the step --
+  //                      released right after conversion, so the HBM stream of K can
+  //                      run up to SA steps ahead of the tensor core;
+  //   bfull/bempty[SB]   B tiles landed (producer warp 2) / MMAs of the step done
+  //                      (tcgen05.commit); bempty also frees TMEM A buffer j % SB;
+  //   afull[SB]          A tile converted into TMEM (4 converter warps -> MMA).
+  // One wait on afull + one on bfull and one commit per step keep the serial
+  // MMA-issue loops short.
+  const int SA = p.sa, SB = p.sb;
+  constexpr uint32_t BST = B_BYTES * (MODE == 3 ? 2 : 1);
+  uint8_t* const bring = smem + (size_t)SA * AR;
+  uint64_t* kfull = reinterpret_cast<uint64_t*>(bring + (size_t)SB * BST);
+  uint64_t* kempty = kfull + SA;
+  uint64_t* bfull = kempty + SA;
+  uint64_t* bempty = bfull + SB;
+  uint64_t* afull = bempty + SB;
+  uint64_t* accfull = afull + SB;    // [2]
   uint64_t* accempty = accfull + 2;  // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accempty + 2);
 
@@ -392,14 +393,18 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     ptx::tma_prefetch_desc(&tmA);
     ptx::tma_prefetch_desc(&tmBhi);
     if (MODE == 3) ptx::tma_prefetch_desc(&tmBlo);
-    for (int s = 0; s < S; ++s) {
-      ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
-      ptx::mbar_init(&afull[s], 4);   // one arrive per lane-quarter converter warp
+    for (int i = 0; i < SA; ++i) {
+      ptx::mbar_init(&kfull[i], 1);
+      ptx::mbar_init(&kempty[i], 4);   // one arrive per lane-quarter converter warp
     }
-    for (int b = 0; b < 2; ++b) {
-      ptx::mbar_init(&accfull[b], 2);   // one commit per MMA-issuing warp
-      ptx::mbar_init(&accempty[b], 4 * Sh::DP);
+    for (int i = 0; i < SB; ++i) {
+      ptx::mbar_init(&bfull[i], 1);
+      ptx::mbar_init(&bempty[i], 1);
+      ptx::mbar_init(&afull[i], 4);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&accfull[i], 2);   // one commit per MMA-issuing warp
+      ptx::mbar_init(&accempty[i], 4 * Sh::DP);
     }
     ptx::fence_mbarrier_init();
   }
@@ -411,13 +416,38 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
 
   if (StepIter<false, false>(p.sched, cta, 1).valid()) {
     if (warp == 0) {
-      // ---------------- TMA producer (whole warp walks the ring; one elected lane issues)
+      // ---------------- A-source producer: K tiles from HBM (or the column points)
       unsigned long long t_wait = 0;
       const unsigned long long t_start = prof ? clock64() : 0;
-      int64_t epoch = 0;
-      for (StepIter<false, false> it(p.sched, cta, S); it.valid(); it.next()) {
+      for (StepIter<false, false> it(p.sched, cta, SA); it.valid(); it.next()) {
         const int s = it.s;
-        // phase-1 epoch barrier: the CTAs' producers meet every sync_k k-steps, so all
+        const unsigned long long t0 = prof ? clock64() : 0;
+        ptx::mbar_wait_idle(&kempty[s], it.ph ^ 1, p.wait_mode, p.wait_ns);
+        if (prof) t_wait += clock64() - t0;
+        if (ptx::elect_one()) {
+          uint8_t* st = smem + (size_t)s * AR;
+          if (OTF) {
+            ptx::mbar_arrive_expect_tx(&kfull[s], AR);
+            ptx::tma_load_2d(st, &tmA, &kfull[s], 0, it.kstep * 8);   // 32 column points, 8 coordinate rows
+          } else if (p.debug & 4) {
+            ptx::mbar_arrive(&kfull[s]);
+          } else {
+            ptx::mbar_arrive_expect_tx(&kfull[s], AR);
+            ptx::tma_load_2d(st, &tmA, &kfull[s], it.kstep * TC_BK, it.tile * TC_BM);
+          }
+        }
+        __syncwarp();
+      }
+      if (prof && lane == 0) {
+        prof[0] = t_wait;
+        prof[1] = clock64() - t_start;
+      }
+    } else if (warp == 2) {
+      // ---------------- B producer (after the TMEM allocation)
+      int64_t epoch = 0;
+      for (StepIter<false, false> it(p.sched, cta, SB); it.valid(); it.next()) {
+        const int s = it.s;
+        // phase-1 epoch barrier: the CTAs' B producers meet every sync_k k-steps, so all
         // CTAs stream the same window of B and L2 serves it (their drift otherwise
         // accumulates tile after tile until B comes from HBM once per tile)
         if (p.sync_k > 0 && !it.in_tail() && it.v > 0 && (it.kstep & (p.sync_k - 1)) == 0) {
@@ -430,46 +460,33 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
           }
           __syncwarp();
         }
-        const unsigned long long t0 = prof ? clock64() : 0;
-        ptx::mbar_wait_idle(&empty[s], it.ph ^ 1, p.wait_mode, p.wait_ns);
-        if (prof) t_wait += clock64() - t0;
+        ptx::mbar_wait_idle(&bempty[s], it.ph ^ 1, p.wait_mode, p.wait_ns);
         if (ptx::elect_one()) {
-          uint8_t* st = smem + (size_t)s * STAGE;
-          if (OTF) {
-            ptx::mbar_arrive_expect_tx(&full[s], STAGE);
-            ptx::tma_load_2d(st, &tmA, &full[s], 0, it.kstep * 8);   // 32 column points, 8 coordinate rows
-          } else {
-            ptx::mbar_arrive_expect_tx(&full[s], (p.debug & 4) ? STAGE - AR : STAGE);
-            if (!(p.debug & 4)) ptx::tma_load_2d(st, &tmA, &full[s], it.kstep * TC_BK, it.tile * TC_BM);
-          }
+          uint8_t* st = bring + (size_t)s * BST;
+          ptx::mbar_arrive_expect_tx(&bfull[s], BST);
           // B in k-step blocks [ks][mp][32]: one contiguous NT x 128-byte box per step
-          ptx::tma_load_2d(st + AR, &tmBhi, &full[s], it.kstep * p.bcol_step, it.kstep * p.brow_step + b_row0);
+          ptx::tma_load_2d(st, &tmBhi, &bfull[s], it.kstep * p.bcol_step, it.kstep * p.brow_step + b_row0);
           if (MODE == 3)
-            ptx::tma_load_2d(st + AR + B_BYTES, &tmBlo, &full[s], it.kstep * p.bcol_step,
-                             it.kstep * p.brow_step + b_row0);
+            ptx::tma_load_2d(st + B_BYTES, &tmBlo, &bfull[s], it.kstep * p.bcol_step, it.kstep * p.brow_step + b_row0);
         }
         __syncwarp();
-      }
-      if (prof && lane == 0) {
-        prof[0] = t_wait;
-        prof[1] = clock64() - t_start;
       }
     } else if (warp == 1 || warp == 3) {
       // ---------------- MMA issuers: warps 1 and 3 take alternate steps (whole warp walks
       // the pipeline so every descriptor is warp-uniform; one elected lane issues).  A
       // named-barrier baton hands the issue slot from step j's warp to step j+1's, so the
       // tensor core sees one deterministic instruction order, while each warp's
-      // per-step mbarrier wait and commit overlap the other warp's MMAs.  Each warp
+      // per-step mbarrier waits and commit overlap the other warp's MMAs.  Each warp
       // commits accfull at every group end (count 2): together the two commits cover
       // all MMAs of the group.
       const int mpar = warp == 3;
       constexpr uint32_t idesc = ptx::idesc_tf32(TC_BM, DW);
-      const uint64_t desc0 = ptx::smem_desc_sw128(ptx::smem_u32(smem + AR));
+      const uint64_t desc0 = ptx::smem_desc_sw128(ptx::smem_u32(bring));
       constexpr uint64_t LO_OFF = (uint64_t)(B_BYTES >> 4);   // Blo rows, in descriptor units
       int64_t gi = -1;  // group index
       unsigned long long t_acc = 0, t_afull = 0, t_iss = 0, nsteps = 0;
       const unsigned long long t_start = prof ? clock64() : 0;
-      for (StepIter<true, true> it(p.sched, cta, S, NA); it.valid(); it.next()) {
+      for (StepIter<true, false> it(p.sched, cta, SB); it.valid(); it.next()) {
         const bool gstart = it.group_start(), gend = it.group_end();
         if (gstart) ++gi;
         if ((it.v & 1) == mpar) {
@@ -477,13 +494,14 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
           const unsigned long long t0 = prof ? clock64() : 0;
           if (gstart && gi >= 2) ptx::mbar_wait(&accempty[gi & 1], (uint32_t)(((gi >> 1) - 1) & 1));
           ptx::mbar_wait(&afull[s], it.ph);
+          ptx::mbar_wait(&bfull[s], it.ph);
           const unsigned long long t1 = prof ? clock64() : 0;
           if (it.v > 0) ptx::named_bar_sync(mpar ? 1 : 2, 64);   // baton from step j - 1
           const unsigned long long t2 = prof ? clock64() : 0;
           ptx::tc_fence_after();
           const uint32_t d = tmem + (uint32_t)(gi & 1) * DW;
-          const uint32_t a0 = tmem + A_COL0 + ASTRIDE * it.ab;
-          const uint64_t bdesc = desc0 + (uint64_t)((s * STAGE) >> 4);
+          const uint32_t a0 = tmem + A_COL0 + ASTRIDE * s;
+          const uint64_t bdesc = desc0 + (uint64_t)((s * BST) >> 4);
           const bool leader = ptx::elect_one();
           if (leader && !(p.debug & 2)) {
 #pragma unroll
@@ -504,7 +522,7 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
           }
           __syncwarp();
           if (it.v + 1 < it.vend) ptx::named_bar_arrive(mpar ? 2 : 1, 64);   // baton to step j + 1
-          if (leader) ptx::tc_commit(&empty[s]);
+          if (leader) ptx::tc_commit(&bempty[s]);
           if (prof) {
             t_acc += t1 - t0;
             t_afull += t2 - t1;
@@ -522,11 +540,11 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       }
     } else if (warp >= 4 && warp < 4 + 4 * Sh::CP) {
       // ---------------- converters: warp 4 + q + 4 par owns TMEM lanes 32q..32q+31 (K rows)
-      // and the steps j with j % 2 == par (all 32 k-columns of each).  The two warps of
-      // a sub-partition work on alternate steps, so one's generation overlaps the
-      // other's TMEM stores; and each warp posts the afull arrive of a step only after
-      // generating the first half of its next step, so tcgen05.wait::st rarely waits.
-      const int q = (warp - 4) & 3, par = (warp - 4) >> 2;   // steps j with j % CP == par
+      // and the steps j with j % CP == par (all 32 k-columns of each), so the warps of a
+      // sub-partition work on different steps and one's generation overlaps another's
+      // TMEM stores; each warp posts the afull arrive of a step only after generating
+      // the first half of its next step, so tcgen05.wait::st rarely waits.
+      const int q = (warp - 4) & 3, par = (warp - 4) >> 2;
       const int row = q * 32 + lane;
       const uint32_t lane_base = (uint32_t)(q * 32) << 16;
       int cur_tile = -1;
@@ -544,10 +562,10 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       };
       unsigned long long cv_full = 0;
       const unsigned long long cv_start = prof ? clock64() : 0;
-      StepIter<false, true> it(p.sched, cta, S, NA);
+      StepIter<false, true> it(p.sched, cta, SA, SB);
       for (int k = 0; k < par; ++k) it.next();
       for (; it.valid(); [&] { for (int k = 0; k < Sh::CP; ++k) it.next(); }()) {
-        const int s = it.s;
+        const int s = it.s, sb = it.sb;
         if constexpr (OTF) if (it.tile != cur_tile) {
           cur_tile = it.tile;
           const int lr = cur_tile * TC_BM + row;
@@ -562,21 +580,25 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
           }
         }
         const unsigned long long c0 = prof ? clock64() : 0;
-        ptx::mbar_wait(&full[s], it.ph);
-        if (S > NA && it.v >= NA) ptx::mbar_wait(&empty[it.ls], it.lph);   // TMEM buffer free
+        ptx::mbar_wait(&kfull[s], it.ph);
+        // TMEM A buffer sb is free once the MMAs of step j - SB completed
+        if (it.v >= SB) ptx::mbar_wait(&bempty[sb], it.phb ^ 1);
         if (prof) cv_full += clock64() - c0;
         ptx::tc_fence_after();
-        const uint32_t ta = tmem + lane_base + A_COL0 + ASTRIDE * it.ab;
+        const uint32_t ta = tmem + lane_base + A_COL0 + ASTRIDE * sb;
         if (p.debug & 16) {   // profiling: no converter work at all
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&afull[s]);
+          if (lane == 0) {
+            ptx::mbar_arrive(&kempty[s]);
+            ptx::mbar_arrive(&afull[sb]);
+          }
           continue;
         }
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           uint32_t hi[16], lo[16];
           if constexpr (OTF) {
-            const uint32_t pp = ptx::smem_u32(smem + (size_t)s * STAGE) + 64u * half;   // [8][32] fp32
+            const uint32_t pp = ptx::smem_u32(smem + (size_t)s * AR) + 64u * half;   // [8][32] fp32
             const int j0 = it.kstep * TC_BK + 16 * half;
             // warp-uniform: a diagonal entry of these rows, or columns >= n?
             const bool fix = (j0 < wrow0 + 32 && j0 + 16 > wrow0) || (j0 + 16 > n32);
@@ -593,7 +615,11 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
               gen16<DIM, FAM, true>(p, pp, xr2, j0, grow, n32, hi, lo);
             }
           } else {
-            load16<MODE>(smem + (size_t)s * STAGE + row * 128, row, half, hi, lo);
+            load16<MODE>(smem + (size_t)s * AR + row * 128, row, half, hi, lo);
+          }
+          if (half == 1) {   // the stage is read: release it to the producer
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&kempty[s]);
           }
           if (half == 0 && pend >= 0) post(pend);
           if (!(p.debug & 1)) {
@@ -601,7 +627,7 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             if (MODE == 3) ptx::tmem_st_32x32b_x16(ta + 32 + 16 * half, lo);
           }
         }
-        pend = s;
+        pend = sb;
       }
       if (pend >= 0) post(pend);
       if (prof && warp == 4 && lane == 0) {
@@ -768,12 +794,18 @@ template <int MODE, int NT, bool OTF, int DIM, int FAM>
 void launch_tc(const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl, TcParams p, int64_t grid,
                cudaStream_t st) {
   using Sh = TcShape<MODE, NT, OTF>;
-  const size_t extra = 1024 + 8 * 96;   // alignment slack + barriers (<= 32 stages)
-  const int smem_cap = max_smem_optin() - 1024;
-  static const int max_stages = getenv("RLD_TC_STAGES") ? atoi(getenv("RLD_TC_STAGES")) : NABUF_MAX;
-  p.stages = (int)std::min<size_t>(max_stages, (smem_cap - extra) / Sh::STAGE);
+  const size_t extra = 1024 + 8 * 96;   // alignment slack + barriers
+  const size_t smem_cap = (size_t)max_smem_optin() - 1024 - extra;
+  constexpr size_t BST = (size_t)Sh::B_BYTES * (MODE == 3 ? 2 : 1);
+  static const int max_sa = getenv("RLD_TC_STAGES") ? atoi(getenv("RLD_TC_STAGES")) : 12;
+  // B ring = TMEM A buffers (as many as TMEM leaves, <= 8); the A-source ring (K tiles
+  // from HBM) takes the rest of shared memory, at least 3 stages
+  int sb = Sh::NABUF;
+  while (sb > 2 && smem_cap < sb * BST + 3 * (size_t)Sh::A_REGION) --sb;
+  p.sb = sb;
+  p.sa = (int)std::min<size_t>(max_sa, (smem_cap - sb * BST) / Sh::A_REGION);
   p.tmem_cols = Sh::TMEM_COLS;
-  const size_t smem = p.stages * Sh::STAGE + extra;
+  const size_t smem = (size_t)p.sa * Sh::A_REGION + (size_t)p.sb * BST + extra;
   RLD_CUDA(cudaFuncSetAttribute(kv_tc_kernel<MODE, NT, OTF, DIM, FAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
   kv_tc_kernel<MODE, NT, OTF, DIM, FAM><<<(unsigned)grid, TC_THREADS, smem, st>>>(mA, mBh, mBl, p);
