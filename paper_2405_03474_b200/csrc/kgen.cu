@@ -21,7 +21,8 @@ constexpr int KG_ROWS = 32;
 constexpr int KG_COLS = 256;
 
 // DIM > 0: compile-time point dimension (registers only); DIM == 0: runtime d <= RLD_MAX_DIM.
-template <typename T, int DIM, int FAM>
+// TILED: K is the tiled fp32 layout [ceil(rows/128)][ceil(n/32)][128][32] (ld unused).
+template <typename T, int DIM, int FAM, bool TILED = false>
 __global__ void __launch_bounds__(KG_COLS)
 kgen_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, int64_t row0, int64_t rows,
             T* __restrict__ K, int64_t ld) {
@@ -43,6 +44,7 @@ kgen_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, int64_t ro
   const int rmax = (int)min64(KG_ROWS, rows - i0);
   T* out = K + i0 * ld + j;
   const int64_t gi0 = row0 + i0;
+  const int64_t ks = (n + 31) >> 5;
   for (int r = 0; r < rmax; ++r) {
     double r2 = 0.0;
 #pragma unroll
@@ -60,17 +62,22 @@ kgen_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, int64_t ro
       v = kp.a2 * (1.0 + u + u * u * (1.0 / 3.0)) * exp(-u);
     }
     if (gi0 + r == j) v = kp.diag;
-    out[(int64_t)r * ld] = (T)v;
+    if (TILED) {
+      const int64_t i = i0 + r;
+      K[(((i >> 7) * ks + (j >> 5)) << 12) + ((i & 127) << 5) + (j & 31)] = (T)v;
+    } else {
+      out[(int64_t)r * ld] = (T)v;
+    }
   }
 }
 
-template <typename T, int DIM>
+template <typename T, int DIM, bool TILED = false>
 void launch_kgen(dim3 grid, size_t smem, const double* X, int64_t n, const KernelParams& kp, int64_t row0,
                  int64_t rows, T* K, int64_t ld, cudaStream_t st) {
   if (kp.family == RLD_RBF)
-    kgen_kernel<T, DIM, RLD_RBF><<<grid, KG_COLS, smem, st>>>(X, n, kp, row0, rows, K, ld);
+    kgen_kernel<T, DIM, RLD_RBF, TILED><<<grid, KG_COLS, smem, st>>>(X, n, kp, row0, rows, K, ld);
   else
-    kgen_kernel<T, DIM, RLD_MATERN52><<<grid, KG_COLS, smem, st>>>(X, n, kp, row0, rows, K, ld);
+    kgen_kernel<T, DIM, RLD_MATERN52, TILED><<<grid, KG_COLS, smem, st>>>(X, n, kp, row0, rows, K, ld);
   RLD_LAUNCH_CHECK();
 }
 
@@ -89,6 +96,22 @@ void build_kernel_rows(const double* X, int64_t n, const KernelParams& kp, int64
     case 4: launch_kgen<T, 4>(grid, smem, X, n, kp, row0, rows, K, ld, st); break;
     case 8: launch_kgen<T, 8>(grid, smem, X, n, kp, row0, rows, K, ld, st); break;
     default: launch_kgen<T, 0>(grid, smem, X, n, kp, row0, rows, K, ld, st); break;
+  }
+}
+
+void build_kernel_tiles(const double* X, int64_t n, const KernelParams& kp, int64_t row0, int64_t rows, float* Kt,
+                        cudaStream_t st) {
+  if (rows <= 0) return;
+  RLD_CUDA(cudaMemsetAsync(Kt, 0, sizeof(float) * tiled_elems(rows, n), st));   // padding rows / columns
+  dim3 grid((unsigned)ceil_div(n, KG_COLS), (unsigned)ceil_div(rows, KG_ROWS));
+  size_t smem = sizeof(double) * KG_ROWS * kp.d;
+  switch (kp.d) {
+    case 1: launch_kgen<float, 1, true>(grid, smem, X, n, kp, row0, rows, Kt, 0, st); break;
+    case 2: launch_kgen<float, 2, true>(grid, smem, X, n, kp, row0, rows, Kt, 0, st); break;
+    case 3: launch_kgen<float, 3, true>(grid, smem, X, n, kp, row0, rows, Kt, 0, st); break;
+    case 4: launch_kgen<float, 4, true>(grid, smem, X, n, kp, row0, rows, Kt, 0, st); break;
+    case 8: launch_kgen<float, 8, true>(grid, smem, X, n, kp, row0, rows, Kt, 0, st); break;
+    default: launch_kgen<float, 0, true>(grid, smem, X, n, kp, row0, rows, Kt, 0, st); break;
   }
 }
 

@@ -246,10 +246,11 @@ void kv_product(const KvOperand& op, int64_t m, const double* V, int64_t ldv, do
       launch_kv<double, double, 64, 32, 16, 4, 4, false>(op, m, V, ldv, Y, ldy, ws, st, launches);
     return;
   }
-  if (kv_tc_supported(op) && !getenv("RLD_NO_TC")) {
+  if (kv_tc_supported(op) && (op.tiled || !getenv("RLD_NO_TC"))) {
     kv_product_tc(op, op.tc_mode, m, V, ldv, Y, ldy, ws, st);
     return;
   }
+  if (op.tiled) fail(RLD_ERR_NOT_SUPPORTED, "tiled fp32 K needs the tensor-core product");
   // float32 arithmetic: cast the float64 operand rows once
   ws.vcast.reserve(sizeof(float) * m * op.n);
   float* Vf = ws.vcast.as<float>();

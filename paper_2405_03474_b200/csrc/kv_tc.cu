@@ -79,6 +79,7 @@ struct Sched {
 struct TcParams {
   Sched sched;      // work schedule (per column pass)
   int mp;           // B rows per k-step block (vectors padded to npass x NT)
+  int a_tiled;      // stored K in 16 KB tiles (box row (tile ks + kstep) 128) instead of row-major
   int bcol_step, brow_step;   // TMA coordinates of B per k-step: blocked (0, mp) or row-major (32, 0)
   unsigned int* sync;   // per-pass arrival counters of the phase-1 epoch barrier (zeroed per launch)
   int sync_k;           // k-steps per epoch (0: no barrier)
@@ -433,7 +434,10 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             ptx::mbar_arrive(&kfull[s]);
           } else {
             ptx::mbar_arrive_expect_tx(&kfull[s], AR);
-            ptx::tma_load_2d(st, &tmA, &kfull[s], it.kstep * TC_BK, it.tile * TC_BM);
+            if (p.a_tiled)
+              ptx::tma_load_2d(st, &tmA, &kfull[s], 0, (it.tile * p.ks + it.kstep) * TC_BM);
+            else
+              ptx::tma_load_2d(st, &tmA, &kfull[s], it.kstep * TC_BK, it.tile * TC_BM);
           }
         }
         __syncwarp();
@@ -875,6 +879,7 @@ bool blocked_b() {
 bool kv_tc_supported(const KvOperand& op) {
   if (op.dtype != RLD_FP32) return false;
   if (op.K == nullptr) return op.pts4 != nullptr && op.kp.d <= 4 && op.tc_mode == 3;   // on the fly
+  if (op.tiled) return true;
   return (op.ldk % 4) == 0 && (reinterpret_cast<uintptr_t>(op.K) % 16) == 0;
 }
 
@@ -916,11 +921,15 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
         segs, cta_of_step(x0 + ks - 1, sc.tail_total, Gl) - cta_of_step(x0, sc.tail_total, Gl) + 1);
   }
   const bool otf = op.K == nullptr;
+  // tiled K: one 16 KB box = 128 contiguous rows of 128 bytes of the [tiles * ks * 128][32] view
   const CUtensorMap mA = otf ? make_points_map(op.pts4, n)
-                             : make_map(static_cast<const float*>(op.K), n, rows, op.ldk, TC_BM);
+                             : op.tiled ? make_map(static_cast<const float*>(op.K), TC_BK,
+                                                   (int64_t)ceil_div(rows, TC_BM) * ks * TC_BM, TC_BK, TC_BM)
+                                        : make_map(static_cast<const float*>(op.K), n, rows, op.ldk, TC_BM);
   TcParams p{};
   p.pts = op.pts4;
   p.mp = (int)mp;
+  p.a_tiled = op.tiled ? 1 : 0;
   p.n = n;
   p.row0 = op.row0;
   p.rows = rows;

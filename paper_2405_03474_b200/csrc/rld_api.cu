@@ -72,6 +72,7 @@ struct Resident {
   DevBuf Kbuf;               // owned stored rows
   const void* K = nullptr;   // stored rows (owned or aliased)
   int64_t ldk = 0;
+  bool tiled = false;        // fp32 K in the 16 KB-tile layout (kgen.cu build_kernel_tiles)
   DevBuf X;                  // points n x d
   DevBuf pts4;               // points split to n x 8 fp32 hi/lo (d <= 4; tensor-core on-the-fly tiles)
   DevBuf diag;               // local diagonal of K (float64)
@@ -81,6 +82,7 @@ struct Resident {
     KvOperand o;
     o.K = (path == RLD_PATH_ON_THE_FLY) ? nullptr : K;
     o.ldk = ldk;
+    o.tiled = tiled;
     o.X = X.as<double>();
     o.pts4 = (source == RLD_SOURCE_POINTS && d <= 4) ? pts4.as<float>() : nullptr;
     o.kp = kp;
@@ -98,7 +100,7 @@ struct Work {
   DevBuf x, p, pp, u, w, KX, T, Tg;
   DevBuf scal;     // small scalars / per-probe arrays
   DevBuf ints;     // flags, info, live, size, kept
-  DevBuf scratch, scratch2, solver_work, rng_scratch, gram_scratch;
+  DevBuf scratch, scratch2, solver_work, rng_scratch, gram_scratch, qtile;
   DevBuf gsend, grecv;   // row-shard all-gather staging
   DevBuf qbasis, coef;   // SLQ: Lanczos basis (t x s x rows) and reorthogonalisation coefficients
   DevBuf flagbuf;        // flag OR over ranks
@@ -187,6 +189,7 @@ void prepare(rld_handle* h, const rld_problem* p) {
   if (!p->data) fail(RLD_ERR_INVALID_ARGUMENT, "problem data is NULL");
   Resident& r = h->res;
   r.ready = false;
+  r.tiled = false;
   r.source = p->source;
   r.dtype = p->dtype;
   r.n = p->n;
@@ -227,14 +230,18 @@ void prepare(rld_handle* h, const rld_problem* p) {
       pad_points(r.X.as<double>(), p->n, p->d, scale, r.pts4.as<float>(), st);
     }
     if (r.path == RLD_PATH_STORED) {
-      const size_t es = p->dtype == RLD_FP64 ? 8 : 4;
-      r.ldk = ceil_div(p->n, 4) * 4;  // 16-byte row pitch for TMA
-      r.Kbuf.reserve(es * r.rows * r.ldk);
-      r.K = r.Kbuf.ptr;
-      if (p->dtype == RLD_FP64)
+      if (p->dtype == RLD_FP64) {
+        r.ldk = ceil_div(p->n, 4) * 4;
+        r.Kbuf.reserve(sizeof(double) * r.rows * r.ldk);
+        r.K = r.Kbuf.ptr;
         build_kernel_rows<double>(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.Kbuf.as<double>(), r.ldk, st);
-      else
-        build_kernel_rows<float>(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.Kbuf.as<float>(), r.ldk, st);
+      } else {   // fp32: 16 KB tiles, one contiguous TMA box per tensor-core step
+        r.tiled = true;
+        r.ldk = 0;
+        r.Kbuf.reserve(sizeof(float) * tiled_elems(r.rows, p->n));
+        r.K = r.Kbuf.ptr;
+        build_kernel_tiles(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.Kbuf.as<float>(), st);
+      }
     } else if (r.path != RLD_PATH_ON_THE_FLY) {
       fail(RLD_ERR_INVALID_ARGUMENT, "unknown path");
     }
@@ -247,7 +254,31 @@ void prepare(rld_handle* h, const rld_problem* p) {
     const size_t es = p->dtype == RLD_FP64 ? 8 : 4;
     const size_t ses = p->data_dtype == RLD_FP64 ? 8 : 4;
     const char* src = static_cast<const char*>(p->data) + ses * (r.row0 * ld);
-    if (p->data_memory == RLD_DEVICE && p->data_dtype == p->dtype) {
+    const cudaMemcpyKind kind = p->data_memory == RLD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (p->dtype == RLD_FP32) {
+      // fp32 products read K in 16 KB tiles: stage 128-row chunks, convert, relayout
+      r.tiled = true;
+      r.ldk = 0;
+      r.Kbuf.reserve(sizeof(float) * tiled_elems(r.rows, p->n));
+      r.K = r.Kbuf.ptr;
+      RLD_CUDA(cudaMemsetAsync(r.Kbuf.ptr, 0, sizeof(float) * tiled_elems(r.rows, p->n), st));
+      const int64_t chunk = std::max<int64_t>(128, ((256ll << 20) / (int64_t)(ses * p->n)) / 128 * 128);
+      DevBuf& stage = h->wk.scratch2;
+      DevBuf& stage32 = h->wk.qtile;
+      stage.reserve(ses * chunk * p->n);
+      if (ses == 8) stage32.reserve(sizeof(float) * chunk * p->n);
+      for (int64_t r0 = 0; r0 < r.rows; r0 += chunk) {
+        const int64_t nr = std::min(chunk, r.rows - r0);
+        RLD_CUDA(cudaMemcpy2DAsync(stage.ptr, ses * p->n, src + ses * r0 * ld, ses * ld, ses * p->n, nr, kind, st));
+        const float* t = stage.as<float>();
+        if (ses == 8) {
+          convert_rows(stage.ptr, RLD_FP64, stage32.ptr, RLD_FP32, nr * p->n, st);
+          t = stage32.as<float>();
+        }
+        tile_rows(t, p->n, r0, nr, p->n, r.Kbuf.as<float>(), st);
+      }
+      RLD_CUDA(cudaStreamSynchronize(st));
+    } else if (p->data_memory == RLD_DEVICE && p->data_dtype == p->dtype) {
       r.K = src;  // alias the caller's device rows (caller keeps them alive)
       r.ldk = ld;
     } else {
@@ -276,7 +307,10 @@ void prepare(rld_handle* h, const rld_problem* p) {
       }
     }
     r.diag.reserve(sizeof(double) * std::max<int64_t>(1, r.rows));
-    diag_of_dense(r.rows, r.row0, r.K, r.ldk, p->dtype, r.diag.as<double>(), st);
+    if (r.tiled)
+      diag_of_tiled(r.rows, r.row0, p->n, static_cast<const float*>(r.K), r.diag.as<double>(), st);
+    else
+      diag_of_dense(r.rows, r.row0, r.K, r.ldk, p->dtype, r.diag.as<double>(), st);
   } else {
     fail(RLD_ERR_INVALID_ARGUMENT, "unknown source");
   }
@@ -964,7 +998,10 @@ int rld_exact_logdet(rld_handle* h, double* value) {
     if (r.path == RLD_PATH_ON_THE_FLY) {
       build_kernel_rows<double>(r.X.as<double>(), n, r.kp, 0, n, L.as<double>(), n, h->st);
     } else {
-      convert_rows_2d(r.K, r.dtype, r.ldk, L.as<double>(), n, n, h->st);
+      if (r.tiled)
+        untile_to_f64(static_cast<const float*>(r.K), n, n, L.as<double>(), n, h->st);
+      else
+        convert_rows_2d(r.K, r.dtype, r.ldk, L.as<double>(), n, n, h->st);
     }
     cusolverDnParams_t params;
     RLD_CUSOLVER(cusolverDnCreateParams(&params));

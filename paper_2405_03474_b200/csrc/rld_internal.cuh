@@ -59,6 +59,12 @@ struct KernelParams {
 };
 
 // K rows [row0, row0 + rows) x all n columns, written as T with row stride ld.
+// fp32 K rows [row0, row0 + rows) in the tiled layout Kt[ceil(rows/128)][ceil(n/32)][128][32]
+// (zero padded): every tensor-core pipeline step streams one contiguous 16 KB tile.
+void build_kernel_tiles(const double* X, int64_t n, const KernelParams& kp, int64_t row0, int64_t rows, float* Kt,
+                        cudaStream_t st);
+inline int64_t tiled_elems(int64_t rows, int64_t n) { return ceil_div(rows, 128) * 128 * ceil_div(n, 32) * 32; }
+
 template <typename T>
 void build_kernel_rows(const double* X, int64_t n, const KernelParams& kp, int64_t row0, int64_t rows,
                        T* K, int64_t ld, cudaStream_t st);
@@ -71,6 +77,7 @@ struct KvOperand {
   // Exactly one source of K.
   const void* K = nullptr;   // dense rows (rows x n, row stride ldk), dtype below
   int64_t ldk = 0;
+  bool tiled = false;        // fp32 K in 16 KB tiles [ceil(rows/128)][ceil(n/32)][128][32] (see kgen.cu)
   const double* X = nullptr; // points (n x d) for on-the-fly generation
   const float* pts4 = nullptr;  // points as n x 8 fp32 (hi x,y,z,w; lo x,y,z,w) for the tensor-core on-the-fly path, d <= 4
   KernelParams kp{};

@@ -63,6 +63,10 @@ void normal_rows(const uint64_t key[2], int64_t rows, int64_t n, int64_t col0, i
                  double* out, DevBuf& scratch, int* dflags, cudaStream_t st);
 // [G][m][L] (all-gathered shards) -> m x n rows, n <= G L
 void relayout_gathered(const double* src, int G, int64_t m, int64_t L, int64_t n, double* dst, cudaStream_t st);
+// tiled fp32 K (kgen.cu layout): relayout of row-major rows, back to float64 rows, diagonal
+void tile_rows(const float* src, int64_t lds, int64_t r0, int64_t nr, int64_t n, float* Kt, cudaStream_t st);
+void untile_to_f64(const float* Kt, int64_t rows, int64_t n, double* out, int64_t ldo, cudaStream_t st);
+void diag_of_tiled(int64_t rows, int64_t row0, int64_t n, const float* Kt, double* d, cudaStream_t st);
 // out[e] = sum_{b < nb} in[b * count + e] (fixed order)
 void sum_blocks(int64_t nb, int64_t count, const double* in, double* out, cudaStream_t st);
 void pad_points(const double* X, int64_t n, int d, double scale, float* pts8, cudaStream_t st);

@@ -736,6 +736,51 @@ __global__ void sum_blocks_kernel(int64_t nb, int64_t count, const double* __res
 }
 }  // namespace
 
+namespace {
+// rows r0 .. r0 + nr - 1 (r0 multiple of 128) of row-major fp32 src (row stride lds) into the tiled layout
+__global__ void tile_rows_kernel(const float* __restrict__ src, int64_t lds, int64_t r0, int64_t nr, int64_t n,
+                                 float* __restrict__ Kt) {
+  const int64_t ks = (n + 31) >> 5;
+  const int64_t total = nr * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / n, j = e % n, i = r0 + r;
+    Kt[(((i >> 7) * ks + (j >> 5)) << 12) + ((i & 127) << 5) + (j & 31)] = src[r * lds + j];
+  }
+}
+__global__ void untile_kernel(const float* __restrict__ Kt, int64_t rows, int64_t n, double* __restrict__ out,
+                              int64_t ldo) {
+  const int64_t ks = (n + 31) >> 5;
+  const int64_t total = rows * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e % n;
+    out[i * ldo + j] = (double)Kt[(((i >> 7) * ks + (j >> 5)) << 12) + ((i & 127) << 5) + (j & 31)];
+  }
+}
+__global__ void diag_of_tiled_kernel(int64_t rows, int64_t row0, int64_t n, const float* __restrict__ Kt,
+                                     double* __restrict__ d) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  const int64_t ks = (n + 31) >> 5, j = row0 + i;
+  d[i] = (double)Kt[(((i >> 7) * ks + (j >> 5)) << 12) + ((i & 127) << 5) + (j & 31)];
+}
+}  // namespace
+
+void tile_rows(const float* src, int64_t lds, int64_t r0, int64_t nr, int64_t n, float* Kt, cudaStream_t st) {
+  if (nr <= 0) return;
+  tile_rows_kernel<<<(unsigned)std::min<int64_t>(ceil_div(nr * n, 256), 148 * 16), 256, 0, st>>>(src, lds, r0, nr, n,
+                                                                                                Kt);
+  RLD_LAUNCH_CHECK();
+}
+void untile_to_f64(const float* Kt, int64_t rows, int64_t n, double* out, int64_t ldo, cudaStream_t st) {
+  untile_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows * n, 256), 148 * 16), 256, 0, st>>>(Kt, rows, n, out, ldo);
+  RLD_LAUNCH_CHECK();
+}
+void diag_of_tiled(int64_t rows, int64_t row0, int64_t n, const float* Kt, double* d, cudaStream_t st) {
+  if (rows <= 0) return;
+  diag_of_tiled_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, st>>>(rows, row0, n, Kt, d);
+  RLD_LAUNCH_CHECK();
+}
+
 void sum_blocks(int64_t nb, int64_t count, const double* in, double* out, cudaStream_t st) {
   if (count <= 0) return;
   sum_blocks_kernel<<<(unsigned)std::min<int64_t>(ceil_div(count, 256), 148 * 8), 256, 0, st>>>(nb, count, in, out);
