@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define RLD_ABI_VERSION 2
+#define RLD_ABI_VERSION 3
 
 typedef enum rld_status {
   RLD_OK = 0,
@@ -50,10 +50,16 @@ typedef enum rld_source { RLD_SOURCE_DENSE = 0, RLD_SOURCE_POINTS = 1 } rld_sour
 typedef enum rld_path { RLD_PATH_STORED = 0, RLD_PATH_ON_THE_FLY = 1 } rld_path;
 typedef enum rld_memory { RLD_HOST = 0, RLD_DEVICE = 1 } rld_memory;
 typedef enum rld_probe_kind { RLD_RADEMACHER = 0, RLD_GAUSSIAN = 1 } rld_probe_kind; /* src/probes.py:12 */
-typedef enum rld_precond_kind {
-  RLD_PRECOND_RAND_SVD = 0, /* src/precond.py:262-267 */
-  RLD_PRECOND_IDENTITY = 1, /* src/precond.py:245-246 */
-  RLD_PRECOND_DIAGONAL = 2  /* src/precond.py:247-248 */
+typedef enum rld_precond_kind {  /* the nine kinds of src/precond.py:25-35 */
+  RLD_PRECOND_RAND_SVD = 0,                /* randomized truncated SVD, src/precond.py:262-267 (the r* default) */
+  RLD_PRECOND_IDENTITY = 1,                /* src/precond.py:245-246 */
+  RLD_PRECOND_DIAGONAL = 2,                /* src/precond.py:247-248 */
+  RLD_PRECOND_RAND_SVD_SCALED = 3,         /* rand-svd low rank, base = scale, src/precond.py:265-266 */
+  RLD_PRECOND_PARTIAL_CHOLESKY = 4,        /* pivoted partial Cholesky, src/precond.py:215-228, 253-258 */
+  RLD_PRECOND_PARTIAL_CHOLESKY_SCALED = 5, /* src/precond.py:259 */
+  RLD_PRECOND_TRUNC_SVD = 6,               /* dense eigh of K (one GPU), src/precond.py:260-263 */
+  RLD_PRECOND_TRUNC_SVD_SCALED = 7,
+  RLD_PRECOND_RANK_ONE = 8                 /* power iteration, src/precond.py:201-213, 249-251 */
 } rld_precond_kind;
 
 /* The stochastic estimators of src/estimators.py behind rld_logdet. */
@@ -111,6 +117,8 @@ typedef struct rld_config {
   uint64_t omega_key[4];  /* keys of streams (seed,(1,0)) and (seed,(1,1))    -- src/precond.py:183 */
   int32_t estimator;      /* rld_estimator: r* (order above) or SLQ (src/estimators.py:99-122) */
   int32_t reserved2;
+  double precond_scale;   /* base scalar a of the "-scaled" kinds (PreconditionerConfig.scale, src/precond.py:45) */
+  uint64_t precond_key[2];/* Philox key of stream (seed, (1,)): the rank-one power-iteration start (src/precond.py:202) */
 } rld_config;
 
 /* Optional injected random inputs.  NULL -> generated on the device from the

@@ -288,6 +288,79 @@ def range_svd(op, n, k, q, seed, omega=None):
     raise AssertionError("unreachable")
 
 
+def _finish_preconditioner(A, base, theta=None, attempts=1) -> OraclePreconditioner:
+    """Determinant lemma and factored square root of P = diag(base) + A A^T -- src/precond.py:69-100."""
+    inner = np.eye(A.shape[1]) + A.T @ (A / base[:, None])
+    try:
+        L = np.linalg.cholesky(inner)
+    except np.linalg.LinAlgError as exc:
+        raise OracleNotPD(str(exc)) from exc
+    log_det = float(np.sum(np.log(base)) + 2.0 * np.sum(np.log(np.diag(L))))
+    sqrt_base = np.sqrt(base)
+    At = A / sqrt_base[:, None]
+    lam, W = np.linalg.eigh(At.T @ At)
+    keep = lam > KEEP_RTOL * max(lam[-1] if lam.size else 0.0, 1.0)
+    U = At @ (W[:, keep] / np.sqrt(lam[keep]))
+    return OraclePreconditioner(base, A, log_det, sqrt_base, U, lam[keep],
+                                np.zeros(0) if theta is None else theta, attempts)
+
+
+def other_preconditioner(kind, K, k, q, seed, scale) -> OraclePreconditioner:
+    """The non-default kinds of build_preconditioner for a dense K -- src/precond.py:201-267:
+    diagonal, rank-one (power iteration from stream (seed, (1,))), partial-cholesky(-scaled)
+    (greedy largest-diagonal pivots), trunc-svd(-scaled) (dense eigh), rand-svd-scaled."""
+    K = np.asarray(K, dtype=np.float64)
+    n = K.shape[0]
+    if kind not in ("identity", "diagonal", "rank-one") and k > n:
+        raise ValueError(f"rank {k} exceeds dimension {n}")                 # precond.py:241-242
+    d0 = np.diag(K).copy()
+
+    def floored(A):                                                         # precond.py:231-233
+        return np.maximum(d0 - np.sum(A * A, axis=1), DIAG_FLOOR)
+
+    if kind == "diagonal":
+        return _finish_preconditioner(np.zeros((n, 0)), d0)
+    if kind == "rank-one":                                                  # precond.py:201-213, 249-251
+        g = stream(seed, (1,))
+        v = g.standard_normal(n)
+        v /= np.linalg.norm(v)
+        lam = 0.0
+        for _ in range(max(100, q * max(k, 1))):
+            w = K @ v
+            new_lam = float(v @ w)
+            v = w / np.linalg.norm(w)
+            if lam != 0.0 and abs(new_lam - lam) <= 1e-10 * abs(new_lam):
+                lam = new_lam
+                break
+            lam = new_lam
+        A = np.sqrt(max(lam, DIAG_FLOOR)) * v[:, None]
+        return _finish_preconditioner(A, floored(A))
+    if kind in ("partial-cholesky", "partial-cholesky-scaled"):             # precond.py:215-228
+        d = d0.copy()
+        C = np.zeros((n, k))
+        for j in range(k):
+            p = int(np.argmax(d))
+            if d[p] <= 0.0:
+                C = C[:, :j]
+                break
+            col = K[:, p] - C[:, :j] @ C[p, :j]
+            C[:, j] = col / np.sqrt(d[p])
+            d -= C[:, j] ** 2
+        base = floored(C) if kind == "partial-cholesky" else np.full(n, scale)
+        return _finish_preconditioner(C, base)
+    if kind in ("trunc-svd", "trunc-svd-scaled"):                           # precond.py:260-263
+        theta, vecs = np.linalg.eigh(K)
+        top = np.argsort(theta)[::-1][:k]
+        A = vecs[:, top] * np.sqrt(np.maximum(theta[top], 0.0))
+    elif kind == "rand-svd-scaled":
+        theta, rows, _ = range_svd(DenseOperator(K), n, k, q, seed)
+        A = rows.T * np.sqrt(np.maximum(theta, 0.0))
+    else:
+        raise ValueError(f"unknown preconditioner kind {kind!r}")
+    base = np.full(n, scale) if kind.endswith("-scaled") else floored(A)
+    return _finish_preconditioner(A, base)
+
+
 def rand_svd_preconditioner(op, diagK, n, k, q, seed, omega=None) -> OraclePreconditioner:
     """rand-svd branch of build_preconditioner -- src/precond.py:236-267."""
     if k > n:
@@ -374,7 +447,7 @@ def identity_preconditioner(n) -> OraclePreconditioner:
 
 
 def rstar(op, n, order, s, t, probe_kind, k, q, seed, V=None, omega=None, per_probe=False,
-          diagK=None, precond="rand-svd") -> OracleEstimate:
+          diagK=None, precond="rand-svd", scale=1e-6) -> OracleEstimate:
     """log det P + mean_i z_i^T r_k(N^-1 K N^-T) z_i -- src/estimators.py:77-96.
 
     ``op`` maps an n x m block to K @ block.  ``V`` optionally injects the s x n
@@ -384,8 +457,10 @@ def rstar(op, n, order, s, t, probe_kind, k, q, seed, V=None, omega=None, per_pr
     t = min(t, n)                                                       # estimators.py:62
     if precond == "identity":
         P = identity_preconditioner(n)
-    else:
+    elif precond == "rand-svd":
         P = rand_svd_preconditioner(op, op.diag() if diagK is None else diagK, n, k, q, seed, omega)
+    else:   # dense K only (the other kinds of src/precond.py:236-267)
+        P = other_preconditioner(precond, op.K, k, q, seed, scale)
     Z = probes(probe_kind, s, n, seed) if V is None else np.asarray(V, dtype=np.float64)
 
     def aop(X):

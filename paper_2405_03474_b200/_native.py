@@ -30,8 +30,10 @@ PATH_STORED, PATH_ON_THE_FLY = 0, 1
 HOST, DEVICE = 0, 1
 RADEMACHER, GAUSSIAN = 0, 1
 PRECOND_RAND_SVD, PRECOND_IDENTITY, PRECOND_DIAGONAL = 0, 1, 2
+PRECOND_RAND_SVD_SCALED, PRECOND_PARTIAL_CHOLESKY, PRECOND_PARTIAL_CHOLESKY_SCALED = 3, 4, 5
+PRECOND_TRUNC_SVD, PRECOND_TRUNC_SVD_SCALED, PRECOND_RANK_ONE = 6, 7, 8
 ESTIMATOR_RSTAR, ESTIMATOR_SLQ = 0, 1
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 # every symbol include/rld.h declares
 EXPORTS = (
@@ -59,7 +61,7 @@ class Config(C.Structure):
                 ("precond_iters", C.c_int32), ("oversample", C.c_int32), ("diag_floor", C.c_double),
                 ("keep_rtol", C.c_double), ("breakdown_rtol", C.c_double), ("orth_rtol", C.c_double),
                 ("probe_key", C.c_uint64 * 2), ("omega_key", C.c_uint64 * 4), ("estimator", C.c_int32),
-                ("reserved2", C.c_int32)]
+                ("reserved2", C.c_int32), ("precond_scale", C.c_double), ("precond_key", C.c_uint64 * 2)]
 
 
 class Inputs(C.Structure):

@@ -470,35 +470,14 @@ int sketch_tc_mode() {
 
 // ints layout: [0] flags [1] potrf info [2] syevd info [3] kept [4] inner-chol info
 // scal layout: [0] sum log base [1] 2 sum log diag(inner chol) [2] trace
-PrecondOut build_preconditioner(rld_handle* h, const rld_config* c, const rld_inputs* in) {
+// Low-rank factor A (n_local x ka, column-major in wk.A) of the randomized truncated SVD
+// (src/precond.py:168-198, 264-267).  Returns ka = k.
+int lowrank_randsvd(rld_handle* h, const rld_config* c, const rld_inputs* in, PrecondOut& out) {
   Resident& r = h->res;
   Work& wk = h->wk;
   cudaStream_t st = h->st;
   const int64_t n = r.n, nl = r.rows;
   int* flags = wk.ints.as<int>();
-  double* scal = wk.scal.as<double>();
-  wk.base.reserve(sizeof(double) * nl);
-  wk.sqrt_base.reserve(sizeof(double) * nl);
-  double* base = wk.base.as<double>();
-  double* sqrt_base = wk.sqrt_base.as<double>();
-  PrecondOut out;
-
-  if (c->precond_kind == RLD_PRECOND_IDENTITY) {
-    fill_doubles(nl, 1.0, base, st);
-    fill_doubles(nl, 1.0, sqrt_base, st);
-    fill_doubles(2, 0.0, scal, st);
-    return out;
-  }
-  if (c->precond_kind == RLD_PRECOND_DIAGONAL) {
-    copy_doubles(nl, r.diag.as<double>(), base, st);
-    sqrt_into(nl, base, sqrt_base, flags, st);
-    sum_log(nl, base, scal, wk.scratch, st);
-    allreduce_sum(h, scal, 1);
-    fill_doubles(1, 0.0, scal + 1, st);
-    return out;
-  }
-  if (c->precond_kind != RLD_PRECOND_RAND_SVD) fail(RLD_ERR_NOT_SUPPORTED, "preconditioner kind not supported");
-
   const int k = c->precond_rank;
   const int w = (int)std::min<int64_t>(k + c->oversample, n);
   wk.Y.reserve(sizeof(double) * n * w);       // full rows (gathered) sketch / Q
@@ -561,11 +540,204 @@ PrecondOut build_preconditioner(rld_handle* h, const rld_config* c, const rld_in
   double* A = wk.A.as<double>();
   RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nl, k, w, &ONE, Ql, (int)n, wk.Vtop.as<double>(),
                          w, &ZERO, A, (int)nl));
-  // base = max(diag M - sum A^2, 1e-12); At = A / sqrt(base)  (src/precond.py:231-233, 94-95)
-  precond_base(nl, k, r.diag.as<double>(), c->diag_floor, A, base, sqrt_base, st);
+  return k;
+}
+
+// All-rank (value, index) of the first largest local-row entry of d (np.argmax rule) into pv[0..1]
+void global_argmax(rld_handle* h, const double* d, double* pv) {
+  Resident& r = h->res;
+  Work& wk = h->wk;
+  if (h->world == 1) {
+    argmax_first(r.rows, d, r.row0, pv, wk.scratch, h->st);
+    return;
+  }
+  wk.gsend.reserve(sizeof(double) * 2);
+  wk.grecv.reserve(sizeof(double) * 2 * h->world);
+  argmax_first(r.rows, d, r.row0, wk.gsend.as<double>(), wk.scratch, h->st);
+  ncclResult_t e = ncclAllGather(wk.gsend.ptr, wk.grecv.ptr, 2, ncclDouble, h->comm, h->st);
+  if (e != ncclSuccess) fail(RLD_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(e));
+  pick_first_max(h->world, wk.grecv.as<double>(), pv, h->st);   // ranks hold increasing row ranges
+}
+
+// Rank-k pivoted partial Cholesky with greedy largest-diagonal pivoting (src/precond.py:215-228):
+// A = C (n_local x ka), ka < k when the residual diagonal runs out (d[p] <= 0).
+int lowrank_pchol(rld_handle* h, const rld_config* c) {
+  Resident& r = h->res;
+  Work& wk = h->wk;
+  cudaStream_t st = h->st;
+  const int64_t nl = r.rows;
+  const int k = c->precond_rank;
+  wk.A.reserve(sizeof(double) * std::max<int64_t>(1, nl) * std::max(k, 1));
+  wk.Tg.reserve(sizeof(double) * std::max<int64_t>(2 * nl, k + 2));   // residual diagonal d + column buffer
+  wk.coef.reserve(sizeof(double) * (k + 2));
+  double* C = wk.A.as<double>();
+  double* d = wk.Tg.as<double>();
+  double* col = d + nl;
+  double* crow = wk.coef.as<double>();
+  double* pv = wk.scal.as<double>() + 4;   // (value, index) of the pivot
+  copy_doubles(nl, r.diag.as<double>(), d, st);
+  const KvOperand op = r.op();
+  int ka = k;
+  for (int j = 0; j < k; ++j) {
+    global_argmax(h, d, pv);
+    double hp[2];
+    RLD_CUDA(cudaMemcpyAsync(hp, pv, sizeof hp, cudaMemcpyDeviceToHost, st));
+    RLD_CUDA(cudaStreamSynchronize(st));
+    if (!(hp[0] > 0.0)) {   // src/precond.py:221-223
+      ka = j;
+      break;
+    }
+    const int64_t p = (int64_t)hp[1];
+    kernel_column(nl, r.row0, r.n, p, op.K, op.ldk, op.dtype, op.tiled, r.X.as<double>(), r.kp, col, st);
+    if (j > 0) {   // col -= C[:, :j] C[p, :j]
+      row_of_owner(nl, r.row0, pv, C, j, crow, st);
+      allreduce_sum(h, crow, j);
+      const double MONE = -1.0;
+      RLD_CUBLAS(cublasDgemv(h->cublas, CUBLAS_OP_N, (int)nl, j, &MONE, C, (int)std::max<int64_t>(1, nl), crow, 1,
+                             &ONE, col, 1));
+    }
+    pchol_update(nl, col, pv, C + (size_t)j * nl, d, st);
+  }
+  return ka;
+}
+
+// Top-k eigenpairs of the dense K in float64 (src/precond.py:260-263), one GPU.
+int lowrank_truncsvd(rld_handle* h, const rld_config* c) {
+  Resident& r = h->res;
+  Work& wk = h->wk;
+  cudaStream_t st = h->st;
+  if (h->world != 1) fail(RLD_ERR_NOT_SUPPORTED, "trunc-svd needs the dense K on one GPU");
+  const int64_t n = r.n;
+  const int k = c->precond_rank;
+  DevBuf L, W;
+  L.reserve(sizeof(double) * n * n);
+  W.reserve(sizeof(double) * n);
+  if (r.path == RLD_PATH_ON_THE_FLY)
+    build_kernel_rows<double>(r.X.as<double>(), n, r.kp, 0, n, L.as<double>(), n, st);
+  else if (r.tiled)
+    untile_to_f64(static_cast<const float*>(r.K), n, n, L.as<double>(), n, st);
+  else
+    convert_rows_2d(r.K, r.dtype, r.ldk, L.as<double>(), n, n, st);
+  cusolverDnParams_t params;
+  RLD_CUSOLVER(cusolverDnCreateParams(&params));
+  size_t dws = 0, hws = 0;
+  RLD_CUSOLVER(cusolverDnXsyevd_bufferSize(h->solver, params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n,
+                                           CUDA_R_64F, L.ptr, n, CUDA_R_64F, W.ptr, CUDA_R_64F, &dws, &hws));
+  DevBuf dwork;
+  dwork.reserve(std::max<size_t>(dws, 8));
+  std::vector<char> hwork(std::max<size_t>(hws, 8));
+  RLD_CUSOLVER(cusolverDnXsyevd(h->solver, params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F,
+                                L.ptr, n, CUDA_R_64F, W.ptr, CUDA_R_64F, dwork.ptr, dws, hwork.data(), hws,
+                                wk.ints.as<int>() + 2));
+  cusolverDnDestroyParams(params);
+  wk.A.reserve(sizeof(double) * n * std::max(k, 1));
+  wk.theta_top.reserve(sizeof(double) * std::max(k, 1));
+  // A[:, r] = V[:, n-1-r] sqrt(max(theta, 0)) (descending order, src/precond.py:262-263)
+  if (k > 0) top_eigvecs((int)n, k, L.as<double>(), W.as<double>(), wk.A.as<double>(), wk.theta_top.as<double>(), st);
+  RLD_CUDA(cudaStreamSynchronize(st));   // L, W go out of scope
+  return k;
+}
+
+// Dominant eigenpair by power iteration (src/precond.py:201-213, 249-251): A = sqrt(max(lam, floor)) v.
+int lowrank_rankone(rld_handle* h, const rld_config* c) {
+  Resident& r = h->res;
+  Work& wk = h->wk;
+  cudaStream_t st = h->st;
+  const int64_t n = r.n, nl = r.rows;
+  const int max_iters = std::max(100, c->precond_iters * std::max(c->precond_rank, 1));
+  wk.Y.reserve(sizeof(double) * std::max<int64_t>(n, 1));
+  wk.A.reserve(sizeof(double) * std::max<int64_t>(nl, 1));
+  wk.Tg.reserve(sizeof(double) * std::max<int64_t>(nl, 1));
+  double* vfull = wk.Y.as<double>();
+  double* v = wk.A.as<double>();     // local rows of v, and finally A
+  double* w = wk.Tg.as<double>();
+  double* dd = wk.scal.as<double>() + 4;   // [0] v.w  [1] w.w  [2] v.v
+  normal_rows(c->precond_key, 1, n, 0, n, n, vfull, wk.rng_scratch, wk.ints.as<int>() + 5, st);   // rng.normal(n)
+  rows_dot(1, n, vfull, n, vfull, n, dd + 2, wk.scratch, st, nullptr);
+  scale_by(n, vfull, dd + 2, 0, st);                                   // v /= |v|
+  copy_doubles(nl, vfull + r.row0, v, st);
+  double lam = 0.0;
+  for (int it = 0; it < max_iters; ++it) {
+    kv(h, 1, vfull, w);                                                // w = M v
+    rows_dot(1, nl, v, nl, w, nl, dd, wk.scratch, st, nullptr);
+    rows_dot(1, nl, w, nl, w, nl, dd + 1, wk.scratch, st, nullptr);
+    allreduce_sum(h, dd, 2);
+    copy_doubles(nl, w, v, st);
+    scale_by(nl, v, dd + 1, 0, st);                                    // v = w / |w|
+    gather_rows(h, v, 1, vfull);
+    double hv = 0.0;
+    RLD_CUDA(cudaMemcpyAsync(&hv, dd, sizeof hv, cudaMemcpyDeviceToHost, st));
+    RLD_CUDA(cudaStreamSynchronize(st));
+    const bool done = lam != 0.0 && std::fabs(hv - lam) <= 1e-10 * std::fabs(hv);
+    lam = hv;
+    if (done) break;
+  }
+  fill_doubles(1, lam, dd, st);
+  scale_by(nl, v, dd, 1, st);                                          // A = sqrt(max(lam, 1e-12)) v
+  RLD_CUDA(cudaStreamSynchronize(st));
+  return 1;
+}
+
+PrecondOut build_preconditioner(rld_handle* h, const rld_config* c, const rld_inputs* in) {
+  Resident& r = h->res;
+  Work& wk = h->wk;
+  cudaStream_t st = h->st;
+  const int64_t nl = r.rows;
+  int* flags = wk.ints.as<int>();
+  double* scal = wk.scal.as<double>();
+  wk.base.reserve(sizeof(double) * std::max<int64_t>(1, nl));
+  wk.sqrt_base.reserve(sizeof(double) * std::max<int64_t>(1, nl));
+  double* base = wk.base.as<double>();
+  double* sqrt_base = wk.sqrt_base.as<double>();
+  PrecondOut out;
+  const int kind = c->precond_kind;
+
+  if (kind == RLD_PRECOND_IDENTITY) {
+    fill_doubles(nl, 1.0, base, st);
+    fill_doubles(nl, 1.0, sqrt_base, st);
+    fill_doubles(2, 0.0, scal, st);
+    return out;
+  }
+  if (kind == RLD_PRECOND_DIAGONAL) {
+    copy_doubles(nl, r.diag.as<double>(), base, st);
+    sqrt_into(nl, base, sqrt_base, flags, st);
+    sum_log(nl, base, scal, wk.scratch, st);
+    allreduce_sum(h, scal, 1);
+    fill_doubles(1, 0.0, scal + 1, st);
+    return out;
+  }
+  int k = 0;
+  bool scaled = false;
+  switch (kind) {
+    case RLD_PRECOND_RAND_SVD_SCALED: scaled = true; [[fallthrough]];
+    case RLD_PRECOND_RAND_SVD: k = lowrank_randsvd(h, c, in, out); break;
+    case RLD_PRECOND_PARTIAL_CHOLESKY_SCALED: scaled = true; [[fallthrough]];
+    case RLD_PRECOND_PARTIAL_CHOLESKY: k = lowrank_pchol(h, c); break;
+    case RLD_PRECOND_TRUNC_SVD_SCALED: scaled = true; [[fallthrough]];
+    case RLD_PRECOND_TRUNC_SVD: k = lowrank_truncsvd(h, c); break;
+    case RLD_PRECOND_RANK_ONE: k = lowrank_rankone(h, c); break;
+    default: fail(RLD_ERR_NOT_SUPPORTED, "unknown preconditioner kind " + std::to_string(kind));
+  }
+  wk.A.reserve(sizeof(double) * std::max<int64_t>(1, nl) * std::max(k, 1));
+  wk.Z.reserve(sizeof(double) * std::max<int64_t>(1, nl) * std::max(k, 1));
+  double* A = wk.A.as<double>();
+  double* Z = wk.Z.as<double>();
+  // base: floored residual diagonal max(diag M - sum A^2, 1e-12) (src/precond.py:231-233) or the
+  // scale of the "-scaled" kinds; At = A / sqrt(base) (src/precond.py:94-95)
+  if (scaled)
+    precond_base_scaled(nl, k, c->precond_scale, A, base, sqrt_base, st);
+  else
+    precond_base(nl, k, r.diag.as<double>(), c->diag_floor, A, base, sqrt_base, st);
   sum_log(nl, base, scal, wk.scratch, st);
   allreduce_sum(h, scal, 1);
+  RLD_CUDA(cudaMemsetAsync(wk.ints.as<int>() + 3, 0, sizeof(int), st));
+  if (k == 0) {   // P = diag(base)
+    fill_doubles(1, 0.0, scal + 1, st);
+    out.k = 0;
+    return out;
+  }
   // C = At^T At ; inner = I + C ; log det inner by Cholesky (src/precond.py:75-80)
+  wk.C.reserve(sizeof(double) * k * k);
   double* C = wk.C.as<double>();
   gram_blas(h, nl, k, A, nl, C);
   allreduce_sum(h, C, (int64_t)k * k);
@@ -587,7 +759,6 @@ PrecondOut build_preconditioner(rld_handle* h, const rld_config* c, const rld_in
   syevd(h, k, C, wk.lam.as<double>());
   wk.hgg.reserve(sizeof(double) * 3 * k);
   double* hv = wk.hgg.as<double>();
-  RLD_CUDA(cudaMemsetAsync(wk.ints.as<int>() + 3, 0, sizeof(int), st));
   sqrt_factors(k, c->keep_rtol, wk.lam.as<double>(), C, hv, hv + k, hv + 2 * k, wk.ints.as<int>() + 3, st);
   // U (n_local x k) into Z (no longer needed)
   RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nl, k, k, &ONE, A, (int)nl, C, k, &ZERO, Z,
@@ -617,12 +788,15 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
   const int64_t n = r.n, nl = r.rows;
   const int64_t s = c->num_probes;
   const int t = (int)std::min<int64_t>(c->lanczos_iters, n);   // src/estimators.py:62
-  if (c->precond_kind == RLD_PRECOND_RAND_SVD) {
-    if (c->precond_rank > n)
-      fail(RLD_ERR_INVALID_ARGUMENT, "rank " + std::to_string(c->precond_rank) + " exceeds dimension " + std::to_string(n));
-    if (c->precond_rank < 1)
-      fail(RLD_ERR_INVALID_ARGUMENT, "rank must be in 1.." + std::to_string(n) + ", got " + std::to_string(c->precond_rank));
-  }
+  const int pk = c->precond_kind;
+  if (pk != RLD_PRECOND_IDENTITY && pk != RLD_PRECOND_DIAGONAL && pk != RLD_PRECOND_RANK_ONE && c->precond_rank > n)
+    fail(RLD_ERR_INVALID_ARGUMENT, "rank " + std::to_string(c->precond_rank) + " exceeds dimension " + std::to_string(n));
+  const bool randsvd = pk == RLD_PRECOND_RAND_SVD || pk == RLD_PRECOND_RAND_SVD_SCALED;
+  if (randsvd && c->precond_rank < 1)   // randomized_range_svd (src/precond.py:176-177)
+    fail(RLD_ERR_INVALID_ARGUMENT, "rank must be in 1.." + std::to_string(n) + ", got " + std::to_string(c->precond_rank));
+  if (!(c->precond_scale > 0) && (pk == RLD_PRECOND_RAND_SVD_SCALED || pk == RLD_PRECOND_PARTIAL_CHOLESKY_SCALED ||
+                                  pk == RLD_PRECOND_TRUNC_SVD_SCALED))
+    fail(RLD_ERR_INVALID_ARGUMENT, "scale must be positive");
   cudaStream_t st = h->st;
   Work& wk = h->wk;
   wk.ints.reserve(sizeof(int) * (8 + 2 * s));
@@ -796,8 +970,9 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
   res->trace_term = hs[2];
   res->value = res->logdet_P + res->trace_term;
   res->attempts = po.attempts;
-  res->rank_kept = (c->precond_kind == RLD_PRECOND_RAND_SVD) ? hi[3] : 0;
-  res->kv_products = products + (c->precond_kind == RLD_PRECOND_RAND_SVD ? (c->precond_iters + 1) * po.attempts : 0);
+  res->rank_kept = po.k > 0 ? hi[3] : 0;
+  res->kv_products = products + (c->precond_kind == RLD_PRECOND_RAND_SVD || c->precond_kind == RLD_PRECOND_RAND_SVD_SCALED
+                                     ? (c->precond_iters + 1) * po.attempts : 0);
   res->kernel_launches = g_launches;
   float ms[3] = {0, 0, 0};
   RLD_CUDA(cudaEventElapsedTime(&ms[0], h->ev[0], h->ev[1]));

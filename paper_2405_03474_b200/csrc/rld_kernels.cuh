@@ -67,6 +67,18 @@ void relayout_gathered(const double* src, int G, int64_t m, int64_t L, int64_t n
 void tile_rows(const float* src, int64_t lds, int64_t r0, int64_t nr, int64_t n, float* Kt, cudaStream_t st);
 void untile_to_f64(const float* Kt, int64_t rows, int64_t n, double* out, int64_t ldo, cudaStream_t st);
 void diag_of_tiled(int64_t rows, int64_t row0, int64_t n, const float* Kt, double* d, cudaStream_t st);
+// preconditioner kinds beyond rand-svd (src/precond.py:201-267)
+void precond_base_scaled(int64_t n, int k, double scale, double* A, double* base, double* sqrt_base,
+                         cudaStream_t st);
+void argmax_first(int64_t n, const double* d, int64_t offset, double* out, DevBuf& scratch, cudaStream_t st);
+// out = the (value, index) pair with the largest value, first on ties, of P pairs ordered by index
+void pick_first_max(int P, const double* pairs, double* out, cudaStream_t st);
+void kernel_column(int64_t rows, int64_t row0, int64_t n, int64_t p, const void* K, int64_t ldk, int kdtype,
+                   bool tiled, const double* X, const KernelParams& kp, double* out, cudaStream_t st);
+void pchol_update(int64_t rows, const double* col, const double* dp, double* Cj, double* d, cudaStream_t st);
+void row_of_owner(int64_t rows, int64_t row0, const double* pv, const double* C, int j, double* out,
+                  cudaStream_t st);
+void scale_by(int64_t n, double* v, const double* f, int mode, cudaStream_t st);
 // out[e] = sum_{b < nb} in[b * count + e] (fixed order)
 void sum_blocks(int64_t nb, int64_t count, const double* in, double* out, cudaStream_t st);
 void pad_points(const double* X, int64_t n, int d, double scale, float* pts8, cudaStream_t st);

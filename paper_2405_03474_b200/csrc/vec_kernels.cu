@@ -781,6 +781,164 @@ void diag_of_tiled(int64_t rows, int64_t row0, int64_t n, const float* Kt, doubl
   RLD_LAUNCH_CHECK();
 }
 
+namespace {
+// base = scale (the "-scaled" kinds, src/precond.py:260-261, 266), sqrt_base, At = A / sqrt(scale)
+__global__ void base_scaled_kernel(int64_t n, int k, double scale, double* __restrict__ A, double* __restrict__ base,
+                                   double* __restrict__ sqrt_base) {
+  const double sb = sqrt(scale), inv = 1.0 / sb;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * (int64_t)(k + 1);
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < n) {
+      base[e] = scale;
+      sqrt_base[e] = sb;
+    } else {
+      A[e - n] *= inv;
+    }
+  }
+}
+
+// first largest entry of d[0..n) (np.argmax tie rule: smallest index), one block per chunk then a final pick;
+// out[0] = value, out[1] = global index (row0 + i) as double
+__global__ void argmax_partial_kernel(int64_t n, const double* __restrict__ d, int64_t chunk,
+                                      double* __restrict__ part) {
+  __shared__ double sv[256];
+  __shared__ int64_t si[256];
+  const int64_t j0 = (int64_t)blockIdx.x * chunk, j1 = min64(n, j0 + chunk);
+  double bv = -INFINITY;
+  int64_t bi = -1;
+  for (int64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+    const double v = d[j];
+    if (v > bv) { bv = v; bi = j; }   // strided walk visits increasing j: keeps the first max
+  }
+  sv[threadIdx.x] = bv;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double v2 = sv[threadIdx.x + o];
+      const int64_t i2 = si[threadIdx.x + o];
+      if (v2 > sv[threadIdx.x] || (v2 == sv[threadIdx.x] && i2 >= 0 && (si[threadIdx.x] < 0 || i2 < si[threadIdx.x]))) {
+        sv[threadIdx.x] = v2;
+        si[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = sv[0];
+    part[2 * blockIdx.x + 1] = (double)si[0];
+  }
+}
+__global__ void argmax_final_kernel(int P, const double* __restrict__ part, int64_t offset, double* __restrict__ out) {
+  double bv = -INFINITY, bi = -1.0;
+  for (int b = 0; b < P; ++b) {   // pairs in increasing index order: strict > keeps the first max
+    const double v = part[2 * b], i = part[2 * b + 1];
+    if (i >= 0 && v > bv) { bv = v; bi = i; }
+  }
+  out[0] = bv;
+  out[1] = bi >= 0 ? bi + (double)offset : -1.0;
+}
+
+// column p of K for the local rows (K symmetric: K[row0 + i, p]) from the resident form
+__global__ void kernel_column_kernel(int64_t rows, int64_t row0, int64_t n, int64_t p, const void* __restrict__ K,
+                                     int64_t ldk, int kdtype, int tiled, const double* __restrict__ X,
+                                     KernelParams kp, double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  double v;
+  if (K == nullptr) {   // from the points (src/kernels.py:40-46, 72)
+    if (row0 + i == p) {
+      v = kp.diag;
+    } else {
+      double r2 = 0.0;
+      for (int c = 0; c < kp.d; ++c) {
+        const double df = X[(row0 + i) * kp.d + c] - X[p * kp.d + c];
+        r2 = fma(df, df, r2);
+      }
+      v = kernel_value_f64(kp, r2);
+    }
+  } else if (tiled) {
+    const int64_t ks = (n + 31) >> 5;
+    v = (double)static_cast<const float*>(K)[(((i >> 7) * ks + (p >> 5)) << 12) + ((i & 127) << 5) + (p & 31)];
+  } else if (kdtype == RLD_FP64) {
+    v = static_cast<const double*>(K)[i * ldk + p];
+  } else {
+    v = (double)static_cast<const float*>(K)[i * ldk + p];
+  }
+  out[i] = v;
+}
+
+// partial-Cholesky column j (src/precond.py:215-228): C[:, j] = col / sqrt(dp); d -= C[:, j]^2
+__global__ void pchol_update_kernel(int64_t rows, const double* __restrict__ col, const double* __restrict__ dp,
+                                    double* __restrict__ Cj, double* __restrict__ d) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  const double c = col[i] / sqrt(dp[0]);
+  Cj[i] = c;
+  d[i] -= c * c;
+}
+
+// C[p, 0..j) of the owner rank's rows, zeros elsewhere (then all-reduced)
+__global__ void row_of_owner_kernel(int64_t rows, int64_t row0, const double* __restrict__ pv, const double* __restrict__ C,
+                                    int j, double* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= j) return;
+  const int64_t p = (int64_t)pv[1] - row0;
+  out[c] = (p >= 0 && p < rows) ? C[(int64_t)c * rows + p] : 0.0;
+}
+
+__global__ void scale_by_kernel(int64_t n, double* __restrict__ v, const double* __restrict__ f, int mode) {
+  // mode 0: v *= 1/sqrt(f[0]) ; mode 1: v *= sqrt(max(f[0], 1e-12))
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  v[i] *= mode == 0 ? 1.0 / sqrt(f[0]) : sqrt(fmax(f[0], 1e-12));
+}
+}  // namespace
+
+void precond_base_scaled(int64_t n, int k, double scale, double* A, double* base, double* sqrt_base,
+                         cudaStream_t st) {
+  base_scaled_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n * (k + 1), 256), 148 * 16), 256, 0, st>>>(
+      n, k, scale, A, base, sqrt_base);
+  RLD_LAUNCH_CHECK();
+}
+void argmax_first(int64_t n, const double* d, int64_t offset, double* out, DevBuf& scratch, cudaStream_t st) {
+  int P = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 2048), 512));
+  const int64_t chunk = ceil_div(std::max<int64_t>(n, 1), P);
+  P = (int)ceil_div(std::max<int64_t>(n, 1), chunk);
+  scratch.reserve(sizeof(double) * 2 * P);
+  argmax_partial_kernel<<<P, 256, 0, st>>>(n, d, chunk, scratch.as<double>());
+  RLD_LAUNCH_CHECK();
+  argmax_final_kernel<<<1, 1, 0, st>>>(P, scratch.as<double>(), offset, out);
+  RLD_LAUNCH_CHECK();
+}
+void pick_first_max(int P, const double* pairs, double* out, cudaStream_t st) {
+  argmax_final_kernel<<<1, 1, 0, st>>>(P, pairs, 0, out);
+  RLD_LAUNCH_CHECK();
+}
+void kernel_column(int64_t rows, int64_t row0, int64_t n, int64_t p, const void* K, int64_t ldk, int kdtype,
+                   bool tiled, const double* X, const KernelParams& kp, double* out, cudaStream_t st) {
+  if (rows <= 0) return;
+  kernel_column_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, st>>>(rows, row0, n, p, K, ldk, kdtype, tiled ? 1 : 0,
+                                                                      X, kp, out);
+  RLD_LAUNCH_CHECK();
+}
+void pchol_update(int64_t rows, const double* col, const double* dp, double* Cj, double* d, cudaStream_t st) {
+  if (rows <= 0) return;
+  pchol_update_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, st>>>(rows, col, dp, Cj, d);
+  RLD_LAUNCH_CHECK();
+}
+void row_of_owner(int64_t rows, int64_t row0, const double* pv, const double* C, int j, double* out,
+                  cudaStream_t st) {
+  if (j <= 0) return;
+  row_of_owner_kernel<<<(unsigned)ceil_div(j, 128), 128, 0, st>>>(rows, row0, pv, C, j, out);
+  RLD_LAUNCH_CHECK();
+}
+void scale_by(int64_t n, double* v, const double* f, int mode, cudaStream_t st) {
+  if (n <= 0) return;
+  scale_by_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, v, f, mode);
+  RLD_LAUNCH_CHECK();
+}
+
 void sum_blocks(int64_t nb, int64_t count, const double* in, double* out, cudaStream_t st) {
   if (count <= 0) return;
   sum_blocks_kernel<<<(unsigned)std::min<int64_t>(ceil_div(count, 256), 148 * 8), 256, 0, st>>>(nb, count, in, out);

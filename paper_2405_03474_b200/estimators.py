@@ -97,10 +97,8 @@ def make_config(cfg: EstimatorConfig, n: int) -> N.Config:
         raise ValueError(f"unknown probe kind {cfg.probe_kind!r}")
     if cfg.probe_kind not in DEVICE_PROBE_KINDS:
         raise NotImplementedError(f"probe kind {cfg.probe_kind!r} is outside the r* hot path")
-    if not slq and cfg.precond.kind not in DEVICE_PRECOND_KINDS:
-        if cfg.precond.kind not in ("identity", "diagonal", "rank-one") and cfg.precond.rank > n:
-            raise ValueError(f"rank {cfg.precond.rank} exceeds dimension {n}")
-        raise NotImplementedError(f"preconditioner kind {cfg.precond.kind!r} is outside the r* hot path")
+    if not slq and cfg.precond.kind not in ("identity", "diagonal", "rank-one") and cfg.precond.rank > n:
+        raise ValueError(f"rank {cfg.precond.rank} exceeds dimension {n}")     # src/precond.py:241-242
     c = N.Config()
     c.estimator = N.ESTIMATOR_SLQ if slq else N.ESTIMATOR_RSTAR
     c.order = 3 if slq else int(cfg.algorithm[1])
@@ -120,6 +118,9 @@ def make_config(cfg: EstimatorConfig, n: int) -> N.Config:
     for a in range(2):
         o0, o1 = philox_key(cfg.seed, (1, a))
         c.omega_key[2 * a], c.omega_key[2 * a + 1] = o0, o1
+    c.precond_scale = cfg.precond.scale
+    p0, p1 = philox_key(cfg.seed, (1,))
+    c.precond_key[0], c.precond_key[1] = p0, p1
     return c
 
 
@@ -139,7 +140,7 @@ class _Inputs:
                 raise ValueError(f"probes must be {cfg.num_probes} x {n}")
             self.keep.append(P)
             self.struct.probes = P.ctypes.data
-        if omega is not None and cfg.precond.kind == "rand-svd":
+        if omega is not None and cfg.precond.kind in ("rand-svd", "rand-svd-scaled"):
             w = _sketch_width(cfg, n)
             om = [np.ascontiguousarray(np.asarray(o, dtype=np.float64)) for o in omega]
             for o in om:

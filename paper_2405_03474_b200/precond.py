@@ -1,11 +1,11 @@
 """Preconditioner configuration (``src/precond.py:25-55``).
 
-The device builds the randomized truncated-SVD preconditioner
-P = diag(base) + A A^T (``src/precond.py:168-198, 231-267``) together with its
-determinant-lemma log det (69-80) and factored square root (90-115).  The
-``identity`` and ``diagonal`` kinds are also built (test doubles for the
-reference's own identities); the remaining kinds are out of scope for this
-hot path and raise ``NotImplementedError`` when an estimate asks for them.
+The device builds all nine kinds of P = diag(base) + A A^T
+(``src/precond.py:201-267``): the randomized truncated SVD of the r* hot path
+(168-198) and its ``-scaled`` variant, identity, diagonal, the rank-one power
+iteration, the pivoted partial Cholesky (``-scaled``), and the dense truncated
+eigendecomposition (``-scaled``; one GPU, K materialised in float64), each with
+its determinant-lemma log det (69-80) and factored square root (90-115).
 """
 
 from __future__ import annotations
@@ -25,7 +25,8 @@ PRECOND_KINDS = (
     "rand-svd",
     "rand-svd-scaled",
 )
-DEVICE_PRECOND_KINDS = {"rand-svd": 0, "identity": 1, "diagonal": 2}
+DEVICE_PRECOND_KINDS = {"rand-svd": 0, "identity": 1, "diagonal": 2, "rand-svd-scaled": 3, "partial-cholesky": 4,
+                        "partial-cholesky-scaled": 5, "trunc-svd": 6, "trunc-svd-scaled": 7, "rank-one": 8}
 
 OVERSAMPLE = 10          # src/precond.py:165
 DIAG_FLOOR = 1e-12       # src/precond.py:37

@@ -1,0 +1,54 @@
+"""Golden vectors for the nine preconditioner kinds from the
+UNMODIFIED reference ``ratlogdet.rstar_logdet`` with ``PreconditionerConfig(kind, ...)``
+(src/precond.py:201-267), run in this container only.
+
+Usage:  OPENBLAS_NUM_THREADS=1 python tests/golden/make_golden_precond.py
+"""
+
+from __future__ import annotations
+
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parent.parent
+sys.path.insert(0, str(REF))
+sys.path.insert(0, str(ROOT))
+
+import ratlogdet  # noqa: E402  (the unmodified reference)
+
+from paper_2405_03474_b200.workloads import baseline  # noqa: E402  (point sets only)
+
+KINDS = ("identity", "diagonal", "rank-one", "partial-cholesky", "partial-cholesky-scaled", "trunc-svd",
+         "trunc-svd-scaled", "rand-svd", "rand-svd-scaled")
+
+
+def main():
+    out = []
+    for idx, n, rank, scale in [(1, 768, 48, 5e-3), (3, 1024, 64, 5e-3)]:
+        wl = baseline(idx, n=n)
+        spec = ratlogdet.KernelSpec(wl.spec.family, wl.spec.amplitude, wl.spec.length_scale, wl.spec.jitter)
+        M = ratlogdet.build_covariance(spec, wl.points)
+        for kind in KINDS:
+            cfg = ratlogdet.EstimatorConfig("r3", 8, 20, "rademacher",
+                                            ratlogdet.PreconditionerConfig(kind, rank, 5, scale), seed=0)
+            est = ratlogdet.rstar_logdet(M, cfg)
+            g = np.random.default_rng(12345)
+            E = g.standard_normal(M.shape)
+            E = 0.5 * (E + E.T)
+            pert = ratlogdet.rstar_logdet(M * (1.0 + 1e-15 * E), cfg).value
+            rec = dict(name=f"{kind}_{wl.name}_n{n}", kind=kind, config_index=idx, n=n, rank=rank, num_iters=5,
+                       scale=scale, num_probes=8, algorithm="r3", seed=0, value=est.value, logdet_P=est.logdet_P,
+                       trace_term=est.trace_term, per_probe=[float(x) for x in est.per_probe_values],
+                       screen=abs(pert - est.value) / abs(est.value))
+            print(rec["name"], rec["value"], rec["logdet_P"], "screen", rec["screen"], flush=True)
+            out.append(rec)
+    (HERE / "golden_precond.json").write_text(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()

@@ -33,7 +33,7 @@ def test_library_loads_and_exports_every_symbol():
     lib = N.load()
     for name in declared_symbols():
         assert hasattr(lib, name), name
-    assert lib.rld_abi_version() == N.ABI_VERSION == 2
+    assert lib.rld_abi_version() == N.ABI_VERSION == 3
 
 
 def test_library_is_sm100a():
@@ -52,7 +52,7 @@ int main(void) {
   P(rld_device_set) P(rld_problem) P(rld_config) P(rld_inputs) P(rld_result)
   O(rld_problem, data) O(rld_problem, ld) O(rld_config, probe_key) O(rld_config, omega_key)
   O(rld_config, diag_floor) O(rld_result, per_probe) O(rld_result, phase_ms) O(rld_inputs, memory)
-  O(rld_config, estimator) O(rld_result, clamped_eigs)
+  O(rld_config, estimator) O(rld_result, clamped_eigs) O(rld_config, precond_scale) O(rld_config, precond_key)
   return 0;
 }
 """
@@ -105,8 +105,10 @@ def test_config_validation_mirrors_reference():
         KernelSpec(length_scale=0.0)
     with pytest.raises(ValueError):
         make_config(EstimatorConfig(algorithm="exact"), 10)
-    with pytest.raises(NotImplementedError):
-        make_config(EstimatorConfig(precond=PreconditionerConfig("partial-cholesky", 5)), 10)
+    with pytest.raises(ValueError):
+        make_config(EstimatorConfig(precond=PreconditionerConfig("partial-cholesky", 11)), 10)
+    assert make_config(EstimatorConfig(precond=PreconditionerConfig("rank-one", 50)), 10).precond_kind == \
+        N.PRECOND_RANK_ONE
     with pytest.raises(ValueError):
         make_config(EstimatorConfig(precond=PreconditionerConfig("trunc-svd", 11)), 10)
 

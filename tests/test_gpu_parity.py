@@ -371,3 +371,73 @@ def test_slq_t_equals_n_is_exact(rld):
     est = rld.slq_logdet(K, cfg)
     ref = O.slq_dense(K, s=4, t=20, seed=0)
     assert rel(est.value, ref.value) <= 1e-10
+
+
+# ---------------------------------------------------------------- preconditioner kinds
+
+def _precond_cases():
+    from conftest import load_golden
+
+    return load_golden("golden_precond.json")
+
+
+@pytest.mark.parametrize("case", _precond_cases(), ids=lambda c: c["name"])
+def test_precond_kinds_match_reference(rld, case):
+    """All nine kinds of src/precond.py:236-267 on the device (dense float64 K, the
+    reference's own input) against the unmodified reference."""
+    from paper_2405_03474_b200.workloads import baseline
+
+    wl = baseline(case["config_index"], n=case["n"])
+    K = O.covariance_block(wl.spec.family, wl.spec.amplitude, wl.spec.length_scale, wl.spec.jitter, wl.points)
+    cfg = rld.EstimatorConfig("r3", case["num_probes"], 20, "rademacher",
+                              rld.PreconditionerConfig(case["kind"], case["rank"], case["num_iters"], case["scale"]),
+                              case["seed"], dtype="fp64")
+    est = rld.rstar_logdet(K, cfg)
+    tol = max(TOL["fp64"], 20 * case["screen"])   # partial Cholesky: pivot near-ties (screen ~1e-2)
+    assert rel(est.value, case["value"]) <= tol, (est.value, case["value"])
+    if case["screen"] < 1e-12:
+        assert rel(est.logdet_P + 1.0, case["logdet_P"] + 1.0) <= 1e-8
+
+
+@pytest.mark.parametrize("kind", ["rand-svd-scaled", "trunc-svd", "trunc-svd-scaled", "rank-one", "diagonal"])
+def test_precond_kinds_fp32_points(rld, kind):
+    """The same kinds from the points with K stored in float32 (tiled) on the device."""
+    from paper_2405_03474_b200.workloads import baseline
+
+    case = [c for c in _precond_cases() if c["kind"] == kind and c["config_index"] == 1][0]
+    wl = baseline(1, n=case["n"])
+    cfg = rld.EstimatorConfig("r3", case["num_probes"], 20, "rademacher",
+                              rld.PreconditionerConfig(kind, case["rank"], case["num_iters"], case["scale"]),
+                              case["seed"], dtype="fp32", path="stored")
+    est = rld.rstar_logdet(rld.KernelMatrix(wl.spec, wl.points), cfg)
+    assert rel(est.value, case["value"]) <= TOL["fp32"]
+
+
+@pytest.mark.parametrize("kind", ["trunc-svd", "partial-cholesky"])
+@pytest.mark.parametrize("path", ["stored", "on_the_fly"])
+def test_perfect_preconditioner_kills_stochastic_part(rld, kind, path):
+    """test_estimators.py:45-56: a rank-n preconditioner reproduces K, so the trace term
+    vanishes and the estimate is the Cholesky log det."""
+    rng = np.random.default_rng(4)
+    pts = rng.standard_normal((60, 2))
+    spec = rld.KernelSpec("rbf", jitter=1e-3)
+    cfg = rld.EstimatorConfig("r3", 35, 20, "rademacher", rld.PreconditionerConfig(kind, 60), 4)
+    if kind == "trunc-svd" and path == "on_the_fly":
+        path = "stored"
+    est = rld.rstar_logdet(rld.KernelMatrix(spec, pts), replace(cfg, path=path))
+    K = O.covariance_block("rbf", 1.0, 1.0, 1e-3, pts)
+    assert abs(est.trace_term) <= 1e-8 * max(abs(est.logdet_P), 1.0)
+    assert rel(est.value, O.cholesky_logdet(K)) <= 1e-8
+
+
+def test_partial_cholesky_on_the_fly_matches_stored(rld):
+    """The pivoted partial Cholesky reads K columns from the stored K or generates them
+    from the points: same pivots and estimate (float64)."""
+    from paper_2405_03474_b200.workloads import baseline
+
+    wl = baseline(5, n=2048)
+    cfg = replace(wl.config, dtype="fp64", num_probes=8,
+                  precond=rld.PreconditionerConfig("partial-cholesky", 64, 5))
+    a = rld.rstar_logdet(rld.KernelMatrix(wl.spec, wl.points), replace(cfg, path="stored"))
+    b = rld.rstar_logdet(rld.KernelMatrix(wl.spec, wl.points), replace(cfg, path="on_the_fly"))
+    assert rel(a.logdet_P, b.logdet_P) <= 1e-9 and rel(a.value, b.value) <= 1e-9
