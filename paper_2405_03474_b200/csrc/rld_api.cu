@@ -102,7 +102,7 @@ struct Work {
   DevBuf ints;     // flags, info, live, size, kept
   DevBuf scratch, scratch2, solver_work, rng_scratch, gram_scratch, qtile;
   DevBuf gsend, grecv;   // row-shard all-gather staging
-  DevBuf qbasis, coef;   // SLQ: Lanczos basis (t x s x rows) and reorthogonalisation coefficients
+  DevBuf qbasis, pbasis, coef;   // reorthogonalised Lanczos: bases (t x s x rows) and coefficients
   DevBuf flagbuf;        // flag OR over ranks
   KvWorkspace kv;
 };
@@ -885,17 +885,28 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
   // SLQ keeps the Lanczos basis for the full reorthogonalisation of src/lanczos.py:60-62:
   // Qb[j] = q_j rows (s x nl); probe c's basis is the nl x (j+1) column-major block at
   // Qb + c nl with leading dimension s nl
+  // r* with any preconditioner but the hot path's rand-svd keeps both bases (x_j in Qb, p_j in
+  // Pb) for the reference's full reorthogonalisation: weak or "-scaled" preconditioners leave
+  // N^-1 K N^-T ill-conditioned, where the three-term recurrence loses orthogonality (fp32 K:
+  // 2.7e-3 relative at config 1 with the diagonal P).  rand-svd does not need it.
+  const bool reorth = !slq && c->precond_kind != RLD_PRECOND_RAND_SVD;
   double* Qb = nullptr;
+  double* Pb = nullptr;
   double* coef = nullptr;
-  if (slq) {
+  if (slq || reorth) {
     wk.qbasis.reserve(sizeof(double) * (size_t)t * s * nl);
     wk.coef.reserve(sizeof(double) * (size_t)s * t);
     Qb = wk.qbasis.as<double>();
     coef = wk.coef.as<double>();
   }
+  if (reorth) {
+    wk.pbasis.reserve(sizeof(double) * (size_t)t * s * nl);
+    Pb = wk.pbasis.as<double>();
+  }
   int products = 0;
   for (int j = 0; j < t; ++j) {
-    if (slq) copy_doubles(s * nl, x, Qb + (size_t)j * s * nl, st);
+    if (slq || reorth) copy_doubles(s * nl, x, Qb + (size_t)j * s * nl, st);
+    if (reorth) copy_doubles(s * nl, p, Pb + (size_t)j * s * nl, st);
     const double* xin = x;                                // one GPU: the local rows are the full rows
     if (h->world > 1) {
       gather_rows(h, x, s, xfull);
@@ -924,7 +935,7 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
       lanczos_advance(s, nl, j, t, beta, live, u, u, p, pp, x, st);
       continue;
     }
-    lanczos_residual(s, nl, j, t, KX, alpha, beta, p, pp, sqrt_base, u, wv, st);
+    lanczos_residual(s, nl, j, t, KX, alpha, beta, p, pp, sqrt_base, u, wv, st, !reorth);
     if (k > 0) {
       RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, k, (int)s, (int)nl, &ONE, U, (int)nl, wv, (int)nl,
                              &ZERO, T, k));
@@ -934,6 +945,21 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
                              wv, (int)nl));
     }
     scale_rows_colmajor(nl, s, nl, sqrt_base, true, wv, st);  // z = P^-1 u
+    if (reorth) {
+      // full two-pass reorthogonalisation of src/lanczos.py:60-62 in the two-sequence form:
+      // with q_i = N^T x_i = N^-1 p_i and w = A q_j (u = N w, z = N^-T w), q_i.w = p_i.z, so
+      // u -= sum_i (p_i.z) p_i and z -= sum_i (p_i.z) x_i keep u = N w and z = N^-T w
+      const double MONE = -1.0;
+      for (int pass = 0; pass < 2; ++pass) {
+        RLD_CUBLAS(cublasDgemvStridedBatched(h->cublas, CUBLAS_OP_T, (int)nl, j + 1, &ONE, Pb, (int)(s * nl), nl, wv,
+                                             1, nl, &ZERO, coef, 1, t, (int)s));
+        if (h->world > 1) allreduce_sum(h, coef, s * t);
+        RLD_CUBLAS(cublasDgemvStridedBatched(h->cublas, CUBLAS_OP_N, (int)nl, j + 1, &MONE, Pb, (int)(s * nl), nl,
+                                             coef, 1, t, &ONE, u, 1, nl, (int)s));
+        RLD_CUBLAS(cublasDgemvStridedBatched(h->cublas, CUBLAS_OP_N, (int)nl, j + 1, &MONE, Qb, (int)(s * nl), nl,
+                                             coef, 1, t, &ONE, wv, 1, nl, (int)s));
+      }
+    }
     rows_dot(s, nl, u, nl, wv, nl, dots, wk.scratch, st, nullptr);
     allreduce_sum(h, dots, s);
     lanczos_beta(s, j, t, c->breakdown_rtol, dots, alpha, beta, beta_ref, live, size, st);

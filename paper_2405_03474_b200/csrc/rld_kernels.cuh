@@ -16,9 +16,11 @@ enum : int {
 
 void normalize_rows(int64_t m, int64_t n, const double* z, const double* nrm2, double* norms, double* q,
                     cudaStream_t st);
+// u = KX - alpha_j p - beta_{j-1} p_prev (or u = KX when !three_term: the residual is then
+// reorthogonalised against the whole basis, src/lanczos.py:58-62); w = u / sqrt_base
 void lanczos_residual(int64_t m, int64_t n, int j, int t, const double* KX, const double* alpha,
                       const double* beta, const double* p, const double* p_prev, const double* sqrt_base, double* u,
-                      double* w, cudaStream_t st);
+                      double* w, cudaStream_t st, bool three_term = true);
 void lanczos_alpha(int64_t m, int j, int t, const double* dots, const int* live, double* alpha, cudaStream_t st);
 void lanczos_beta(int64_t m, int j, int t, double rtol, const double* beta2, double* alpha, double* beta,
                   double* beta_ref, int* live, int* size, cudaStream_t st);

@@ -109,16 +109,17 @@ __global__ void normalize_rows_kernel(int64_t m, int64_t n, const double* __rest
 __global__ void lanczos_residual_kernel(int64_t m, int64_t n, int j, int t, const double* __restrict__ KX,
                                         const double* __restrict__ alpha, const double* __restrict__ beta,
                                         const double* __restrict__ p, const double* __restrict__ p_prev,
-                                        const double* __restrict__ sqrt_base, double* __restrict__ u,
+                                        const double* __restrict__ sqrt_base, int three_term, double* __restrict__ u,
                                         double* __restrict__ w) {
   const int64_t total = m * n;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = e / n, i = e % n;
-    const double a = alpha[c * t + j];
-    const double bp = (j > 0) ? beta[c * t + (j - 1)] : 0.0;
-    double v = KX[e] - a * p[e];
-    if (j > 0) v -= bp * p_prev[e];
+    double v = KX[e];
+    if (three_term) {
+      v -= alpha[c * t + j] * p[e];
+      if (j > 0) v -= beta[c * t + (j - 1)] * p_prev[e];
+    }
     u[e] = v;
     w[e] = v / sqrt_base[i];
   }
@@ -229,9 +230,9 @@ void normalize_rows(int64_t m, int64_t n, const double* z, const double* nrm2, d
 
 void lanczos_residual(int64_t m, int64_t n, int j, int t, const double* KX, const double* alpha,
                       const double* beta, const double* p, const double* p_prev, const double* sqrt_base, double* u,
-                      double* w, cudaStream_t st) {
-  lanczos_residual_kernel<<<grid_for(m * n), 256, 0, st>>>(m, n, j, t, KX, alpha, beta, p, p_prev, sqrt_base, u,
-                                                            w);
+                      double* w, cudaStream_t st, bool three_term) {
+  lanczos_residual_kernel<<<grid_for(m * n), 256, 0, st>>>(m, n, j, t, KX, alpha, beta, p, p_prev, sqrt_base,
+                                                           three_term ? 1 : 0, u, w);
   RLD_LAUNCH_CHECK();
 }
 
