@@ -49,7 +49,12 @@ typedef enum rld_family { RLD_RBF = 0, RLD_MATERN52 = 1 } rld_family; /* src/ker
 typedef enum rld_source { RLD_SOURCE_DENSE = 0, RLD_SOURCE_POINTS = 1 } rld_source;
 typedef enum rld_path { RLD_PATH_STORED = 0, RLD_PATH_ON_THE_FLY = 1 } rld_path;
 typedef enum rld_memory { RLD_HOST = 0, RLD_DEVICE = 1 } rld_memory;
-typedef enum rld_probe_kind { RLD_RADEMACHER = 0, RLD_GAUSSIAN = 1 } rld_probe_kind; /* src/probes.py:12 */
+typedef enum rld_probe_kind {   /* src/probes.py:12 */
+  RLD_RADEMACHER = 0,
+  RLD_GAUSSIAN = 1,
+  RLD_NORMAL_ORTHOGONAL = 2   /* orthonormalised Gaussian blocks scaled by chi(n) radii, src/probes.py:15-22 */
+} rld_probe_kind;
+#define RLD_MAX_PROBE_BLOCKS 4  /* normal-orthogonal: s <= 4 n */
 typedef enum rld_precond_kind {  /* the nine kinds of src/precond.py:25-35 */
   RLD_PRECOND_RAND_SVD = 0,                /* randomized truncated SVD, src/precond.py:262-267 (the r* default) */
   RLD_PRECOND_IDENTITY = 1,                /* src/precond.py:245-246 */
@@ -119,6 +124,7 @@ typedef struct rld_config {
   int32_t reserved2;
   double precond_scale;   /* base scalar a of the "-scaled" kinds (PreconditionerConfig.scale, src/precond.py:45) */
   uint64_t precond_key[2];/* Philox key of stream (seed, (1,)): the rank-one power-iteration start (src/precond.py:202) */
+  uint64_t probe_block_keys[2 * RLD_MAX_PROBE_BLOCKS]; /* normal-orthogonal: keys of streams (seed, (2, i)) */
 } rld_config;
 
 /* Optional injected random inputs.  NULL -> generated on the device from the
@@ -198,6 +204,12 @@ int rld_rademacher(rld_handle* h, const uint64_t key[2], int64_t rows, int64_t n
  * (256-layer ziggurat over Philox4x64) reproduced on the device from the stream's key;
  * `out` is device float64, rows x n. */
 int rld_normal(rld_handle* h, const uint64_t key[2], int64_t rows, int64_t n, double* out);
+
+/* Rng.chi(df, count) -- src/linalg.py:87-88 (sqrt of numpy's Generator.chisquare) -- drawn on the
+ * host from the numpy Philox stream `key` starting at 64-bit word `word0`: the continuation of the
+ * stream after Gaussian rows the device generated (normal-orthogonal probes, src/probes.py:15-22).
+ * Host only; needs no GPU. */
+int rld_chi_radii(const uint64_t key[2], uint64_t word0, int64_t df, int64_t count, double* out);
 
 /* exact_logdet(M) -- src/estimators.py:125-129: Cholesky log det of the
  * resident problem's K in float64 on the device. */

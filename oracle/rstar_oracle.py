@@ -86,7 +86,17 @@ def probes(kind: str, s: int, n: int, seed: int) -> np.ndarray:
         return 2.0 * g.integers(0, 2, size=(s, n)).astype(np.float64) - 1.0   # src/linalg.py:84-85
     if kind == "gaussian":
         return g.standard_normal((s, n))                                     # src/linalg.py:81-82
-    raise ValueError(f"oracle supports rademacher/gaussian probes, not {kind!r}")
+    if kind == "normal-orthogonal":                                          # src/probes.py:15-22, 36-44
+        blocks, left, i = [], s, 0
+        while left > 0:
+            sb = min(left, n)
+            gb = stream(seed, (2, i))
+            Q = cgs2_rows(gb.standard_normal((sb, n)))
+            blocks.append(Q * np.sqrt(gb.chisquare(n, sb))[:, None])          # Rng.chi, src/linalg.py:87-88
+            left -= sb
+            i += 1
+        return np.vstack(blocks)
+    raise ValueError(f"unknown probe kind {kind!r}")
 
 
 def sketch(seed: int, attempt: int, w: int, n: int) -> np.ndarray:

@@ -28,7 +28,8 @@ RBF, MATERN52 = 0, 1
 SOURCE_DENSE, SOURCE_POINTS = 0, 1
 PATH_STORED, PATH_ON_THE_FLY = 0, 1
 HOST, DEVICE = 0, 1
-RADEMACHER, GAUSSIAN = 0, 1
+RADEMACHER, GAUSSIAN, NORMAL_ORTHOGONAL = 0, 1, 2
+MAX_PROBE_BLOCKS = 4
 PRECOND_RAND_SVD, PRECOND_IDENTITY, PRECOND_DIAGONAL = 0, 1, 2
 PRECOND_RAND_SVD_SCALED, PRECOND_PARTIAL_CHOLESKY, PRECOND_PARTIAL_CHOLESKY_SCALED = 3, 4, 5
 PRECOND_TRUNC_SVD, PRECOND_TRUNC_SVD_SCALED, PRECOND_RANK_ONE = 6, 7, 8
@@ -39,7 +40,7 @@ ABI_VERSION = 3
 EXPORTS = (
     "rld_abi_version", "rld_create", "rld_destroy", "rld_last_error", "rld_logdet", "rld_prepare",
     "rld_logdet_resident", "rld_build_covariance", "rld_kv_apply", "rld_rademacher", "rld_exact_logdet",
-    "rld_nccl_unique_id", "rld_stream", "rld_normal",
+    "rld_nccl_unique_id", "rld_stream", "rld_normal", "rld_chi_radii",
 )
 
 
@@ -61,7 +62,8 @@ class Config(C.Structure):
                 ("precond_iters", C.c_int32), ("oversample", C.c_int32), ("diag_floor", C.c_double),
                 ("keep_rtol", C.c_double), ("breakdown_rtol", C.c_double), ("orth_rtol", C.c_double),
                 ("probe_key", C.c_uint64 * 2), ("omega_key", C.c_uint64 * 4), ("estimator", C.c_int32),
-                ("reserved2", C.c_int32), ("precond_scale", C.c_double), ("precond_key", C.c_uint64 * 2)]
+                ("reserved2", C.c_int32), ("precond_scale", C.c_double), ("precond_key", C.c_uint64 * 2),
+                ("probe_block_keys", C.c_uint64 * 8)]
 
 
 class Inputs(C.Structure):
@@ -107,6 +109,7 @@ def load() -> C.CDLL:
         lib.rld_rademacher.argtypes = [H, C.POINTER(C.c_uint64 * 2), C.c_int64, C.c_int64, C.c_void_p]
         lib.rld_normal.argtypes = [H, C.POINTER(C.c_uint64 * 2), C.c_int64, C.c_int64, C.c_void_p]
         lib.rld_exact_logdet.argtypes = [H, C.POINTER(C.c_double)]
+        lib.rld_chi_radii.argtypes = [C.POINTER(C.c_uint64 * 2), C.c_uint64, C.c_int64, C.c_int64, C.c_void_p]
         lib.rld_nccl_unique_id.argtypes = [C.c_void_p]
         lib.rld_stream.argtypes = [H]
         lib.rld_stream.restype = C.c_void_p

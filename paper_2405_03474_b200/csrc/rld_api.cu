@@ -103,6 +103,7 @@ struct Work {
   DevBuf scratch, scratch2, solver_work, rng_scratch, gram_scratch, qtile;
   DevBuf gsend, grecv;   // row-shard all-gather staging
   DevBuf qbasis, pbasis, coef;   // reorthogonalised Lanczos: bases (t x s x rows) and coefficients
+  DevBuf endw, radii;            // normal-orthogonal probes: stream position, chi radii
   DevBuf flagbuf;        // flag OR over ranks
   KvWorkspace kv;
 };
@@ -784,7 +785,8 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
   if (c->num_probes < 1 || c->lanczos_iters < 1) fail(RLD_ERR_INVALID_ARGUMENT, "num_probes and lanczos_iters must be >= 1");
   if (c->precond_rank < 0) fail(RLD_ERR_INVALID_ARGUMENT, "rank must be >= 0");
   if (c->precond_iters < 1) fail(RLD_ERR_INVALID_ARGUMENT, "num_iters must be >= 1");
-  if (c->probe_kind != RLD_RADEMACHER && c->probe_kind != RLD_GAUSSIAN) fail(RLD_ERR_INVALID_ARGUMENT, "unknown probe kind");
+  if (c->probe_kind != RLD_RADEMACHER && c->probe_kind != RLD_GAUSSIAN && c->probe_kind != RLD_NORMAL_ORTHOGONAL)
+    fail(RLD_ERR_INVALID_ARGUMENT, "unknown probe kind");
   const int64_t n = r.n, nl = r.rows;
   const int64_t s = c->num_probes;
   const int t = (int)std::min<int64_t>(c->lanczos_iters, n);   // src/estimators.py:62
@@ -820,6 +822,30 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
     load_rows(h, in->probes, in->memory, s, Zp);
   } else if (c->probe_kind == RLD_RADEMACHER) {
     rademacher_rows(c->probe_key, s, n, r.row0, nl, nl, Zp, st);
+  } else if (c->probe_kind == RLD_NORMAL_ORTHOGONAL) {
+    // src/probes.py:15-22, 36-44: block i of min(s_left, n) rows from stream (seed, (2, i)):
+    // Gaussian rows, orthonormalised (CholQR = the CGS2 Q), scaled by chi(n) radii drawn from
+    // the same stream right after the rows (host continuation, rng_host.cu)
+    wk.endw.reserve(sizeof(int64_t));
+    wk.radii.reserve(sizeof(double) * s);
+    int64_t done = 0;
+    for (int b = 0; done < s; ++b) {
+      if (b >= RLD_MAX_PROBE_BLOCKS) fail(RLD_ERR_NOT_SUPPORTED, "normal-orthogonal probes need s <= 4 n");
+      const int64_t sb = std::min<int64_t>(s - done, n);
+      double* blk = Zp + done * nl;
+      const uint64_t* key = c->probe_block_keys + 2 * b;
+      normal_rows(key, sb, n, r.row0, nl, nl, blk, wk.rng_scratch, wk.ints.as<int>() + 5, st, wk.endw.as<int64_t>());
+      cholqr2(h, nl, (int)sb, blk, wk.ints.as<int>(), 2);
+      int64_t ew = 0;
+      RLD_CUDA(cudaMemcpyAsync(&ew, wk.endw.ptr, sizeof ew, cudaMemcpyDeviceToHost, st));
+      RLD_CUDA(cudaStreamSynchronize(st));
+      std::vector<double> rad((size_t)sb);
+      chi_radii_host(key, (uint64_t)ew, n, sb, rad.data());
+      RLD_CUDA(cudaMemcpyAsync(wk.radii.ptr, rad.data(), sizeof(double) * sb, cudaMemcpyHostToDevice, st));
+      scale_cols_colmajor(nl, sb, nl, wk.radii.as<double>(), blk, st);
+      RLD_CUDA(cudaStreamSynchronize(st));   // rad goes out of scope
+      done += sb;
+    }
   } else {  // numpy-exact Gaussian probes on the device (src/probes.py:33-34)
     normal_rows(c->probe_key, s, n, r.row0, nl, nl, Zp, wk.rng_scratch, wk.ints.as<int>() + 5, st);
   }

@@ -61,8 +61,11 @@ void strided_sum_log(int64_t count, const double* v, int64_t stride, double* out
                      cudaStream_t st);
 // rows x n standard normals of numpy stream `key` (Generator(Philox).standard_normal, bit-exact),
 // columns [col0, col0 + ncols) of each row to out (row stride ld); dflags bit set on overflow
+// end_word (device, optional): the stream word index following the last draw (where a
+// host continuation of the same numpy stream starts, see rng_host.cu)
 void normal_rows(const uint64_t key[2], int64_t rows, int64_t n, int64_t col0, int64_t ncols, int64_t ld,
-                 double* out, DevBuf& scratch, int* dflags, cudaStream_t st);
+                 double* out, DevBuf& scratch, int* dflags, cudaStream_t st, int64_t* end_word = nullptr);
+void chi_radii_host(const uint64_t key[2], uint64_t word0, int64_t df, int64_t count, double* out);
 // [G][m][L] (all-gathered shards) -> m x n rows, n <= G L
 void relayout_gathered(const double* src, int G, int64_t m, int64_t L, int64_t n, double* dst, cudaStream_t st);
 // tiled fp32 K (kgen.cu layout): relayout of row-major rows, back to float64 rows, diagonal

@@ -267,7 +267,8 @@ __global__ void __launch_bounds__(ZL) zig_link_kernel(int64_t nchunks, int64_t c
 __global__ void __launch_bounds__(ZT) zig_emit_kernel(uint64_t k0, uint64_t k1, const int* __restrict__ entry,
                                                       const int64_t* __restrict__ base, int64_t count, int64_t ncols,
                                                       int64_t col0, int64_t ldo, int64_t nout_cols,
-                                                      double* __restrict__ out, int* __restrict__ flags) {
+                                                      double* __restrict__ out, int* __restrict__ flags,
+                                                      int64_t* __restrict__ end_word) {
   extern __shared__ __align__(16) unsigned char zsm_raw[];
   ChunkSmem& sm = *reinterpret_cast<ChunkSmem*>(zsm_raw);
   const int64_t chunk = blockIdx.x;
@@ -318,6 +319,7 @@ __global__ void __launch_bounds__(ZT) zig_emit_kernel(uint64_t k0, uint64_t k1, 
     const Attempt a = attempt_at(sm.words, t * 16 + i, ZC + ZM, true);
     const int64_t r = k / ncols, jj = k % ncols;
     if (jj >= col0 && jj < col0 + nout_cols) out[r * ldo + (jj - col0)] = a.value;
+    if (end_word && k == count - 1) *end_word = chunk * ZC + t * 16 + i + a.len;   // stream word after the last draw
     ++k;
   }
 }
@@ -327,7 +329,7 @@ __global__ void __launch_bounds__(ZT) zig_emit_kernel(uint64_t k0, uint64_t k1, 
 // rows x n standard normals of numpy stream `key`, columns [col0, col0 + ncols_out) of
 // each row written to out (row stride ld).  Scratch is grown as needed.
 void normal_rows(const uint64_t key[2], int64_t rows, int64_t n, int64_t col0, int64_t ncols_out, int64_t ld,
-                 double* out, DevBuf& scratch, int* dflags, cudaStream_t st) {
+                 double* out, DevBuf& scratch, int* dflags, cudaStream_t st, int64_t* end_word) {
   const int64_t count = rows * n;
   if (count <= 0) return;
   // words: ~1.007 per draw on average; generous margin, checked below
@@ -350,7 +352,7 @@ void normal_rows(const uint64_t key[2], int64_t rows, int64_t n, int64_t col0, i
   zig_link_kernel<<<1, ZL, 0, st>>>(nchunks, count, exits, naccs, entry, base, dflags);
   RLD_LAUNCH_CHECK();
   zig_emit_kernel<<<(unsigned)nchunks, ZT, smem, st>>>(key[0], key[1], entry, base, count, n, col0, ld, ncols_out,
-                                                        out, dflags);
+                                                        out, dflags, end_word);
   RLD_LAUNCH_CHECK();
 }
 

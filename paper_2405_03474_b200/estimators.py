@@ -118,6 +118,13 @@ def make_config(cfg: EstimatorConfig, n: int) -> N.Config:
     for a in range(2):
         o0, o1 = philox_key(cfg.seed, (1, a))
         c.omega_key[2 * a], c.omega_key[2 * a + 1] = o0, o1
+    if cfg.probe_kind == "normal-orthogonal":
+        nb = -(-cfg.num_probes // n)
+        if nb > N.MAX_PROBE_BLOCKS:
+            raise NotImplementedError(f"normal-orthogonal probes need s <= {N.MAX_PROBE_BLOCKS} n")
+        for b in range(nb):
+            b0, b1 = philox_key(cfg.seed, (2, b))
+            c.probe_block_keys[2 * b], c.probe_block_keys[2 * b + 1] = b0, b1
     c.precond_scale = cfg.precond.scale
     p0, p1 = philox_key(cfg.seed, (1,))
     c.precond_key[0], c.precond_key[1] = p0, p1

@@ -151,3 +151,25 @@ def test_shard_bounds_cover_rows():
             assert spans[0][0] == 0 and spans[-1][1] == n
             for (a, b), (c, d) in zip(spans, spans[1:]):
                 assert b == c and a <= b
+
+
+def _words_consumed(bg):
+    st = bg.state
+    ctr = int(st["state"]["counter"][0])
+    return 0 if ctr == 0 else 4 * (ctr - 1) + int(st["buffer_pos"])
+
+
+@pytest.mark.parametrize("seed,path,k,df,m", [(0, (2, 0), 4096 * 3, 4096, 3), (7, (2, 1), 12345, 12345, 8),
+                                              (3, (2, 0), 100, 5, 50), (11, (1,), 0, 1000, 4)])
+def test_host_chi_radii_continue_numpy_stream(seed, path, k, df, m):
+    """rld_chi_radii (host port of numpy's chisquare) continues the Philox stream where
+    the device's Gaussian rows stopped: bit-identical to Generator.chisquare (src/linalg.py:87-88)."""
+    g = np.random.Generator(np.random.Philox(np.random.SeedSequence(seed, spawn_key=path)))
+    g.standard_normal(k)
+    w0 = _words_consumed(g.bit_generator)
+    want = np.sqrt(g.chisquare(df, m))
+    lib = N.load()
+    key = (C.c_uint64 * 2)(*philox_key(seed, path))
+    out = np.empty(m)
+    assert lib.rld_chi_radii(C.byref(key), w0, df, m, out.ctypes.data) == 0
+    np.testing.assert_array_equal(out, want)

@@ -441,3 +441,38 @@ def test_partial_cholesky_on_the_fly_matches_stored(rld):
     a = rld.rstar_logdet(rld.KernelMatrix(wl.spec, wl.points), replace(cfg, path="stored"))
     b = rld.rstar_logdet(rld.KernelMatrix(wl.spec, wl.points), replace(cfg, path="on_the_fly"))
     assert rel(a.logdet_P, b.logdet_P) <= 1e-9 and rel(a.value, b.value) <= 1e-9
+
+
+# ---------------------------------------------------------------- normal-orthogonal probes
+
+def _probe_cases():
+    from conftest import load_golden
+
+    return load_golden("golden_probes.json")["estimates"]
+
+
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+@pytest.mark.parametrize("case", _probe_cases(), ids=lambda c: c["name"])
+def test_normal_orthogonal_probes_match_reference(rld, case, dtype):
+    """Device Gaussian blocks (stream (seed, (2, i))), device orthonormalisation, chi radii
+    continuing the same stream on the host (rld_chi_radii) -- src/probes.py:15-44."""
+    from paper_2405_03474_b200.workloads import baseline
+
+    wl = baseline(case["config_index"], n=case["n"])
+    cfg = rld.EstimatorConfig(case["algorithm"], case["num_probes"], 20, "normal-orthogonal",
+                              rld.PreconditionerConfig("rand-svd", case["rank"], 5), case["seed"], dtype=dtype)
+    est = rld.estimate_logdet(rld.KernelMatrix(wl.spec, wl.points), cfg)
+    assert rel(est.value, case["value"]) <= TOL[dtype], (est.value, case["value"])
+    if dtype == "fp64":
+        np.testing.assert_allclose(est.per_probe_values, case["per_probe"], rtol=1e-6)
+
+
+def test_normal_orthogonal_several_blocks(rld):
+    """s > n: independent blocks from streams (seed, (2, 0)), (seed, (2, 1)), ... (src/probes.py:38-44)."""
+    rng = np.random.default_rng(5)
+    pts = rng.uniform(0, 1, (20, 2))
+    K = O.covariance_block("matern52", 1.0, 0.3, 1e-2, pts)
+    cfg = rld.EstimatorConfig("r3", 50, 20, "normal-orthogonal", rld.PreconditionerConfig("identity"), 3)
+    est = rld.rstar_logdet(K, cfg)
+    ref = O.rstar_dense(K, order=3, s=50, t=20, probe_kind="normal-orthogonal", k=0, q=5, seed=3, precond="identity")
+    assert rel(est.value, ref.value) <= 1e-9
