@@ -1,0 +1,217 @@
+// Whole-GPU pipe peaks on this box ("re-measure FP32, FP64, TF32 and MUFU"):
+// FFMA, packed FFMA2 (fma.rn.f32x2), DFMA, MUFU ex2.approx / sqrt.approx, and tcgen05.mma
+// kind::tf32 (M = 128, K = 8, N = 64/128/256; A from SMEM "ss" and from TMEM "ts").
+// Each test runs on every SM, timed with CUDA events (best of 5 after a warm-up), and prints
+// one JSON object.  The SM clock during the run is sampled by the caller (nvidia-smi).
+//
+//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -I../paper_2405_03474_b200/csrc pipe_peaks.cu -o pipe_peaks
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "tc_ptx.cuh"
+
+using namespace rld;
+
+constexpr int CHAINS = 8;
+
+__global__ void ffma_kernel(int iters, float seed, float* out) {
+  float a[CHAINS];
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) a[c] = seed + c * 1e-3f + threadIdx.x * 1e-6f;
+  const float m = 0.999999f, k = 1e-7f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+#pragma unroll
+      for (int c = 0; c < CHAINS; ++c) a[c] = fmaf(a[c], m, k);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) s += a[c];
+  if (s == 12345.f) out[0] = s;
+}
+
+__global__ void ffma2_kernel(int iters, float seed, float* out) {
+  uint64_t a[CHAINS];
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) {
+    float2 f = make_float2(seed + c * 1e-3f, seed - threadIdx.x * 1e-6f);
+    a[c] = *reinterpret_cast<uint64_t*>(&f);
+  }
+  float2 mf = make_float2(0.999999f, 0.999998f), kf = make_float2(1e-7f, 2e-7f);
+  const uint64_t m = *reinterpret_cast<uint64_t*>(&mf), k = *reinterpret_cast<uint64_t*>(&kf);
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+#pragma unroll
+      for (int c = 0; c < CHAINS; ++c) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(a[c]) : "l"(m), "l"(k));
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) {
+    float2 f = *reinterpret_cast<float2*>(&a[c]);
+    s += f.x + f.y;
+  }
+  if (s == 12345.f) out[0] = s;
+}
+
+__global__ void dfma_kernel(int iters, double seed, double* out) {
+  double a[CHAINS];
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) a[c] = seed + c * 1e-3 + threadIdx.x * 1e-6;
+  const double m = 0.9999999, k = 1e-9;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+#pragma unroll
+      for (int c = 0; c < CHAINS; ++c) a[c] = fma(a[c], m, k);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) s += a[c];
+  if (s == 12345.0) out[0] = s;
+}
+
+template <int OP>   // 0 ex2.approx.ftz, 1 sqrt.approx.ftz
+__global__ void mufu_kernel(int iters, float seed, float* out) {
+  float a[CHAINS];
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) a[c] = seed + c * 1e-3f + threadIdx.x * 1e-6f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+#pragma unroll
+      for (int c = 0; c < CHAINS; ++c) {
+        if (OP == 0)
+          asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[c]));
+        else
+          asm volatile("sqrt.approx.ftz.f32 %0, %0;" : "+f"(a[c]));
+      }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) s += a[c];
+  if (s == 12345.f) out[0] = s;
+}
+
+// One issuing thread per CTA, one CTA per SM, back-to-back MMAs into one accumulator.
+template <int N, bool TS>
+__global__ void __launch_bounds__(128) mma_kernel(int iters, long long* out) {
+  __shared__ __align__(1024) uint8_t bsm[256 * 128];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t holder;
+  for (int i = threadIdx.x; i < 256 * 128 / 4; i += blockDim.x) reinterpret_cast<float*>(bsm)[i] = 1.0f;
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_mbarrier_init();
+  }
+  if (threadIdx.x < 32) ptx::tmem_alloc(&holder, 512);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = holder;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = ptx::idesc_tf32(128, N);
+    const uint64_t bd = ptx::smem_desc_sw128(ptx::smem_u32(bsm));
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (TS) {
+          ptx::mma_tf32_ts(tmem, tmem + 256 + 8 * k, bd + 2 * k, idesc, 1u);
+        } else {
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+              "l"(bd + 2 * k), "l"(bd + 2 * k), "r"(idesc), "r"(1u)
+              : "memory");
+        }
+      }
+    }
+    ptx::tc_commit(&bar);
+    ptx::mbar_wait(&bar, 0);
+    if (blockIdx.x == 0) out[0] = clock64() - t0;
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) ptx::tmem_dealloc(tmem, 512);
+}
+
+template <typename F>
+float best_ms(F launch) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  launch();
+  cudaDeviceSynchronize();
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(e0);
+    launch();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = ms < best ? ms : best;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return best;
+}
+
+int main() {
+  int sms = 0, clk_khz = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
+  float* fo;
+  double* dd;
+  long long* lo;
+  cudaMalloc(&fo, 16);
+  cudaMalloc(&dd, 16);
+  cudaMalloc(&lo, 16);
+  const int blocks = sms * 8, threads = 256, iters = 4096;
+  const double ops = (double)blocks * threads * iters * 16 * CHAINS;   // instructions (per lane)
+  printf("{\n \"sms\": %d, \"clock_attr_mhz\": %.0f,\n", sms, clk_khz / 1e3);
+  {
+    float ms = best_ms([&] { ffma_kernel<<<blocks, threads>>>(iters, 1.0f, fo); });
+    printf(" \"ffma_tflops\": %.2f,\n", 2 * ops / (ms * 1e-3) / 1e12);
+  }
+  {
+    float ms = best_ms([&] { ffma2_kernel<<<blocks, threads>>>(iters, 1.0f, fo); });
+    printf(" \"ffma2_tflops\": %.2f,\n", 4 * ops / (ms * 1e-3) / 1e12);
+  }
+  {
+    float ms = best_ms([&] { dfma_kernel<<<blocks, threads>>>(iters / 4, 1.0, dd); });
+    printf(" \"dfma_tflops\": %.2f,\n", 2 * ops / 4 / (ms * 1e-3) / 1e12);
+  }
+  {
+    float ms = best_ms([&] { mufu_kernel<0><<<blocks, threads>>>(iters / 4, 0.5f, fo); });
+    printf(" \"mufu_ex2_gops\": %.1f,\n", ops / 4 / (ms * 1e-3) / 1e9);
+  }
+  {
+    float ms = best_ms([&] { mufu_kernel<1><<<blocks, threads>>>(iters / 4, 0.5f, fo); });
+    printf(" \"mufu_sqrt_gops\": %.1f,\n", ops / 4 / (ms * 1e-3) / 1e9);
+  }
+  const int mi = 20000;
+  auto mma = [&](auto kern, int N, const char* name, bool last) {
+    float ms = best_ms([&] { kern<<<sms, 128>>>(mi, lo); });
+    long long cyc = 0;
+    cudaMemcpy(&cyc, lo, 8, cudaMemcpyDeviceToHost);
+    const double fl = (double)sms * mi * 4 * 2.0 * 128 * N * 8;
+    printf(" \"%s\": {\"tflops\": %.1f, \"cycles_per_mma\": %.1f}%s\n", name, fl / (ms * 1e-3) / 1e12,
+           (double)cyc / (mi * 4.0), last ? "" : ",");
+  };
+  mma(mma_kernel<64, false>, 64, "tf32_ss_n64", false);
+  mma(mma_kernel<128, false>, 128, "tf32_ss_n128", false);
+  mma(mma_kernel<256, false>, 256, "tf32_ss_n256", false);
+  mma(mma_kernel<64, true>, 64, "tf32_ts_n64", false);
+  mma(mma_kernel<128, true>, 128, "tf32_ts_n128", false);
+  mma(mma_kernel<256, true>, 256, "tf32_ts_n256", true);
+  printf("}\n");
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "CUDA error: %s\n", cudaGetErrorString(e));
+    return 1;
+  }
+  return 0;
+}
