@@ -211,6 +211,13 @@ int rld_normal(rld_handle* h, const uint64_t key[2], int64_t rows, int64_t n, do
  * Host only; needs no GPU. */
 int rld_chi_radii(const uint64_t key[2], uint64_t word0, int64_t df, int64_t count, double* out);
 
+/* The dense Cholesky the preconditioner build uses (CholQR's w x w Gram, src/linalg.py:159-180
+ * restated; the k x k inner factor, src/precond.py:75-80): G = R^T R in place on the n x n
+ * column-major float64 device matrix G (upper triangle read and overwritten with R).  *info
+ * (host) = 0, or the 1-based index of the first non-positive pivot as LAPACK's potrf.
+ * Synchronous. */
+int rld_dense_cholesky(rld_handle* h, int32_t n, double* G, int32_t* info);
+
 /* exact_logdet(M) -- src/estimators.py:125-129: Cholesky log det of the
  * resident problem's K in float64 on the device. */
 int rld_exact_logdet(rld_handle* h, double* value);

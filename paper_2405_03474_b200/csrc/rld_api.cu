@@ -394,21 +394,32 @@ void gram_blas(rld_handle* h, int64_t rows, int w, const double* Y, int64_t ldy,
 // Intermediate power iterations use one pass (`passes` = 1): any triangular
 // re-basis keeps the final Q = qr(K^q Omega) unchanged, so only the last
 // iteration needs the second pass for orthogonality.
+// Upper Cholesky of the w x w fp64 matrix G (ld w): the one-cluster kernel for w <= 640
+// (small_chol.cu), cuSOLVER potrf above that.  RLD_SMALL_CHOL=0 forces cuSOLVER.
+void potrf_upper(rld_handle* h, int w, double* G, int* info) {
+  static const bool small = [] {
+    const char* e = getenv("RLD_SMALL_CHOL");
+    return !(e && e[0] == '0');
+  }();
+  if (small && small_potrf_upper(w, G, w, info, h->st)) return;
+  Work& wk = h->wk;
+  int lwork = 0;
+  RLD_CUSOLVER(cusolverDnDpotrf_bufferSize(h->solver, CUBLAS_FILL_MODE_UPPER, w, G, w, &lwork));
+  wk.solver_work.reserve(sizeof(double) * std::max(lwork, 1));
+  RLD_CUSOLVER(cusolverDnDpotrf(h->solver, CUBLAS_FILL_MODE_UPPER, w, G, w, wk.solver_work.as<double>(), lwork, info));
+}
+
 void cholqr2(rld_handle* h, int64_t n, int w, double* Y, int* flags, int passes = 2) {
   Work& wk = h->wk;
   wk.G.reserve(sizeof(double) * w * w);
   wk.gdiag.reserve(sizeof(double) * w);
   double* G = wk.G.as<double>();
   int* info = wk.ints.as<int>() + 1;
-  int lwork = 0;
-  RLD_CUSOLVER(cusolverDnDpotrf_bufferSize(h->solver, CUBLAS_FILL_MODE_UPPER, w, G, w, &lwork));
-  wk.solver_work.reserve(sizeof(double) * std::max(lwork, 1));
   for (int pass = 0; pass < passes; ++pass) {
     gram_blas(h, n, w, Y, n, G);
     allreduce_sum(h, G, (int64_t)w * w);
     if (pass == 0) diag_copy(w, G, wk.gdiag.as<double>(), h->st);
-    RLD_CUSOLVER(cusolverDnDpotrf(h->solver, CUBLAS_FILL_MODE_UPPER, w, G, w, wk.solver_work.as<double>(), lwork,
-                                  info));
+    potrf_upper(h, w, G, info);
     if (pass == 0) cholqr_check(w, G, wk.gdiag.as<double>(), info, 1e-6, flags, h->st);
     RLD_CUBLAS(cublasDtrsm(h->cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
                            (int)n, w, &ONE, G, w, Y, (int)n));
@@ -748,11 +759,7 @@ PrecondOut build_preconditioner(rld_handle* h, const rld_config* c, const rld_in
   add_identity(k, inner, st);
   {
     int* info = wk.ints.as<int>() + 4;
-    int lwork = 0;
-    RLD_CUSOLVER(cusolverDnDpotrf_bufferSize(h->solver, CUBLAS_FILL_MODE_LOWER, k, inner, k, &lwork));
-    wk.solver_work.reserve(sizeof(double) * std::max(lwork, 1));
-    RLD_CUSOLVER(cusolverDnDpotrf(h->solver, CUBLAS_FILL_MODE_LOWER, k, inner, k, wk.solver_work.as<double>(), lwork,
-                                  info));
+    potrf_upper(h, k, inner, info);   // only the diagonal of the factor is used
     chol_logdet(k, inner, info, scal + 1, flags, st);
   }
   // factored square root (src/precond.py:90-100): eigh(At^T At), keep filter, U = At W / sqrt(lam)
@@ -1185,6 +1192,18 @@ int rld_kv_apply(rld_handle* h, int64_t m, const double* V, double* Y) {
     if (!h->res.ready) fail(RLD_ERR_INVALID_ARGUMENT, "no resident problem");
     if (m < 1 || !V || !Y) fail(RLD_ERR_INVALID_ARGUMENT, "bad kv_apply arguments");
     kv(h, m, V, Y);   // stream-ordered on rld_stream(h)
+  });
+}
+
+int rld_dense_cholesky(rld_handle* h, int32_t n, double* G, int32_t* info) {
+  if (!h) return RLD_ERR_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    if (n < 1 || !G || !info) fail(RLD_ERR_INVALID_ARGUMENT, "bad dense_cholesky arguments");
+    h->wk.ints.reserve(sizeof(int) * 8);
+    int* dinfo = h->wk.ints.as<int>() + 1;
+    potrf_upper(h, n, G, dinfo);
+    RLD_CUDA(cudaMemcpyAsync(info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    RLD_CUDA(cudaStreamSynchronize(h->st));
   });
 }
 

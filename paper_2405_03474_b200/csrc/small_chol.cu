@@ -1,0 +1,271 @@
+// Small dense Cholesky G = R^T R (upper, float64, column-major, in place) on one thread-block
+// cluster -- the w x w Gram factorisations of CholQR (src/linalg.py:159-180 restated as
+// Cholesky-QR) and the k x k inner factor of the preconditioner
+// (src/precond.py:75-80).  cuSOLVER's potrf at these sizes is a chain of ~20 small kernels
+// (0.21 ms at n = 256, 0.27 ms at 266); this is one launch.
+//
+// Right-looking, 32-column panels, CL CTAs of one cluster; column j belongs to CTA j % CL.
+// Per panel p (rows/cols [k0, k1)):
+//   1. every CTA loads the diagonal block from global, applies the previous panel's update to
+//      it redundantly (owners skip those columns), and factors it in one warp with the columns
+//      in registers (identical arithmetic in every CTA, so a non-positive pivot is seen by all
+//      and they leave together);
+//   2. each CTA solves R_pp^T x = G[k0:k1, j] for its columns j >= k1 (forward substitution,
+//      one warp per column) and writes the panel row R[k0:k1, j] over G;
+//   3. one cluster barrier, then every CTA pulls the whole panel row into shared memory and
+//      applies the rank-32 update G[k1:j, j] -= R[p, k1:j]^T R[p, j] to its columns.
+// The matrix stays in global memory (L2-resident at these sizes); cross-CTA data is read with
+// ld.global.cg after the barrier (release / acquire at cluster scope, plus a gpu fence).
+// info = first failing pivot (1-based), 0 on success, as LAPACK's potrf.
+#include "rld_internal.cuh"
+#include "rld_device.cuh"
+
+namespace rld {
+
+namespace {
+
+constexpr int CL = 8;            // CTAs per cluster
+constexpr int NB = 32;           // panel width
+constexpr int THREADS = 256;
+constexpr int SMALL_CHOL_MAX = 640;
+constexpr int CMAX = (SMALL_CHOL_MAX + CL - 1) / CL;   // columns per CTA
+
+// barrier.cluster release / acquire orders the global-memory writes before it for every thread of
+// the cluster; the cross-CTA reads after it go to L2 (ld.global.cg) anyway.
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Pivot J of the register-resident 32 x 32 factorisation (lane c holds column c); templated so
+// every a[] index is a compile-time constant (the array stays in registers).
+__device__ __forceinline__ double rsqrt_nr(double d) {
+  // MUFU approximation + two Newton steps (relative error ~1 ulp); the IEEE sqrt and division
+  // sequences are several times longer on the serial pivot chain
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  const double hd = 0.5 * d;
+  y = y * fma(-hd * y, y, 1.5);
+  y = y * fma(-hd * y, y, 1.5);
+  return y;
+}
+
+// Pivot J of the register-resident 32 x 32 factorisation (lane c holds column c); templated so
+// every a[] index is a compile-time constant.  d = the (already updated) pivot, broadcast.
+// The serial chain is d -> 1/sqrt(d) -> scale -> next pivot (lane J+1 updates its own two
+// entries and broadcasts the result); the rank-1 update of the other entries goes through a
+// shared-memory row broadcast off that chain.  No per-lane predicates: lane c's entries below
+// its diagonal (a[i], i > c) are scratch that is never read.
+template <int J>
+__device__ __forceinline__ void chol_pivot(double (&a)[NB], double d, int lane, int& bad, double* Ri,
+                                           double* rowbuf) {
+  if (!(d > 0.0) && bad < 0) bad = J;   // warp-uniform; finish on dummies
+  if (bad >= 0) d = 1.0;
+  const double ri = rsqrt_nr(d);
+  const double r = d * ri;
+  a[J] = (lane == J) ? r : a[J] * ri;
+  double dn = 0.0;
+  if constexpr (J + 1 < NB) dn = __shfl_sync(0xffffffffu, fma(-a[J], a[J], a[J + 1]), J + 1);
+  if (lane == 0) Ri[J] = ri;
+  double* rb = rowbuf + (J & 1) * NB;   // double-buffered row J of R
+  rb[lane] = a[J];
+  __syncwarp();
+#pragma unroll
+  for (int i = J + 1; i < NB; ++i) a[i] = fma(-rb[i], a[J], a[i]);
+  if constexpr (J + 1 < NB) chol_pivot<J + 1>(a, dn, lane, bad, Ri, rowbuf);
+}
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+
+// Warp 0: factor the diagonal block in Ds (upper part valid, lower part zero / identity pad) into
+// R_pp (upper part of Ds), 1/R_ii (Ri) and R_pp^-1 (upper part of Rv).  Returns via Ri[0] < 0 a
+// failure marker -1 - j for a non-positive pivot j.
+__device__ __forceinline__ void factor_block(double* Ds, double* Ri, double* Rv, double* rowbuf, int lane) {
+  double a[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) a[i] = Ds[i * (NB + 1) + lane];
+  int bad = -1;
+  chol_pivot<0>(a, __shfl_sync(0xffffffffu, a[0], 0), lane, bad, Ri, rowbuf);
+#pragma unroll
+  for (int i = 0; i < NB; ++i) Ds[i * (NB + 1) + lane] = a[i];
+  __syncwarp();
+  // R^-1, column c = lane, by column-oriented back substitution: x_m = 1/R_mm (m == c) or
+  // s_m / R_mm (m < c), then s_i -= R_im x_m for i < m (independent updates, short chains)
+  double x[NB], sacc[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) sacc[i] = 0.0;
+#pragma unroll
+  for (int m = NB - 1; m >= 0; --m) {
+    x[m] = (m > lane) ? 0.0 : Ri[m] * ((m == lane) ? 1.0 : sacc[m]);
+#pragma unroll
+    for (int i = 0; i < m; ++i) sacc[i] = fma(-Ds[i * (NB + 1) + m], x[m], sacc[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < NB; ++i) Rv[i * (NB + 1) + lane] = x[i];
+  if (bad >= 0 && lane == 0) Ri[0] = -1.0 - (double)bad;
+}
+
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(THREADS)
+chol_upper_kernel(int n, double* __restrict__ G, int ld, int* __restrict__ info, long long* __restrict__ prof) {
+  extern __shared__ double sm[];
+  constexpr int LDB = NB + 1;
+  double* Ds = sm;                  // NB x LDB: diagonal block / its factor R_pp (upper part)
+  double* Rv = Ds + NB * LDB;       // NB x LDB: R_pp^-1 (upper part)
+  double* Dn = Rv + NB * LDB;       // NB x LDB: next diagonal block as loaded from global
+  double* Ri = Dn + NB * LDB;       // NB: 1 / R_ii
+  double* rowbuf = Ri + NB;         // 2 x NB: pivot-row broadcast of the diagonal factorisation
+  double* Gs = rowbuf + 2 * NB;     // CMAX x LDB: this CTA's columns of the panel rows (step 2 input)
+  double* Pt = Gs + CMAX * LDB;     // n x LDB: panel row, Pt[j * LDB + m] = R[k0 + m, j]
+  const int cta = (int)blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int npanels = (n + NB - 1) / NB;
+  long long t_prev = clock64();
+  auto mark = [&](int slot) {   // RLD_CHOL_PROFILE: per-phase cycles of CTA 0
+    if (prof && cta == 0) {
+      __syncthreads();
+      const long long t = clock64();
+      if (tid == 0) prof[slot] += t - t_prev;
+      t_prev = t;
+    }
+  };
+
+  // ---- prologue: the first diagonal block straight from global
+  {
+    const int kb = min(NB, n);
+    for (int e = tid; e < NB * NB; e += THREADS) {
+      const int i = e % NB, c = e / NB;
+      Ds[i * LDB + c] = (i < kb && c < kb) ? ((i <= c) ? __ldcg(G + (size_t)c * ld + i) : 0.0) : (i == c ? 1.0 : 0.0);
+    }
+    __syncthreads();
+    if (warp == 0) factor_block(Ds, Ri, Rv, rowbuf, lane);
+    __syncthreads();
+  }
+  mark(0);
+
+  for (int p = 0; p < npanels; ++p) {
+    const int k0 = p * NB, kb = min(NB, n - k0), k1 = k0 + kb;
+    if (Ri[0] < 0.0) {   // identical in every CTA: leave together
+      if (cta == 0 && tid == 0) *info = k0 + (int)(-Ri[0] - 1.0) + 1;
+      return;
+    }
+    // R_pp goes over the diagonal block only after the cluster barrier: until then the other CTAs
+    // may still be reading that block
+    auto write_rpp = [&]() {
+      if (cta == 0)
+        for (int e = tid; e < kb * kb; e += THREADS) {
+          const int i = e % kb, c = e / kb;
+          if (i <= c) G[(size_t)(k0 + c) * ld + k0 + i] = Ds[i * LDB + c];
+        }
+    };
+    if (k1 >= n) {
+      cluster_sync_all();
+      write_rpp();
+      break;
+    }
+    // ---- 2. panel row for this CTA's columns j >= k1: R[p, j] = R_pp^-T g_j
+    const int jstart = k1 + ((cta - k1 % CL) + CL) % CL;   // first column j >= k1 with j % CL == cta
+    const int ncol = jstart < n ? (n - 1 - jstart) / CL + 1 : 0;
+    for (int e = tid; e < ncol * NB; e += THREADS) {
+      const int m = e % NB, q = e / NB;
+      if (m < kb)
+        cp_async8(Gs + q * LDB + m, G + (size_t)(jstart + q * CL) * ld + k0 + m);
+      else
+        Gs[q * LDB + m] = 0.0;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    for (int e = tid; e < ncol * NB; e += THREADS) {
+      const int m = e % NB, q = e / NB;
+      double x = 0.0;
+#pragma unroll 8
+      for (int l = 0; l < NB; ++l) x = fma(Rv[l * LDB + m], Gs[q * LDB + l], x);   // Rv lower part is 0
+      if (m < kb) G[(size_t)(jstart + q * CL) * ld + k0 + m] = x;
+    }
+    mark(1);
+    cluster_sync_all();
+    mark(2);
+    write_rpp();
+    // ---- 3. panel row (all columns) and the next diagonal block into shared memory
+    const int k2 = min(n, k1 + NB), kb2 = k2 - k1;
+    for (int e = tid; e < NB * (n - k1); e += THREADS) {
+      const int m = e % NB, j = k1 + e / NB;
+      if (m < kb)
+        cp_async8(Pt + j * LDB + m, G + (size_t)j * ld + k0 + m);
+      else
+        Pt[j * LDB + m] = 0.0;
+    }
+    for (int e = tid; e < NB * NB; e += THREADS) {
+      const int i = e % NB, c = e / NB;
+      if (i < kb2 && c < kb2 && i <= c)
+        cp_async8(Dn + i * LDB + c, G + (size_t)(k1 + c) * ld + k1 + i);
+      else
+        Dn[i * LDB + c] = (i < kb2 && c < kb2) ? 0.0 : (i == c ? 1.0 : 0.0);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    mark(3);
+    // ---- 4a. next diagonal block = Dn - panel-row update (all threads), then warp 0 factors it
+    for (int e = tid; e < NB * NB; e += THREADS) {
+      const int i = e % NB, c = e / NB;
+      double v = Dn[i * LDB + c];
+      if (i <= c && c < kb2) {
+#pragma unroll 8
+        for (int m = 0; m < NB; ++m) v = fma(-Pt[(k1 + i) * LDB + m], Pt[(k1 + c) * LDB + m], v);
+      }
+      Ds[i * LDB + c] = v;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      factor_block(Ds, Ri, Rv, rowbuf, lane);
+    } else {
+      // ---- 4b. rank-kb update of this CTA's columns beyond the next diagonal block
+      const int js2 = k2 + ((cta - k2 % CL) + CL) % CL;
+      for (int j = js2 + (warp - 1) * CL; j < n; j += CL * (THREADS / 32 - 1)) {
+        double pj[NB];
+#pragma unroll
+        for (int m = 0; m < NB; ++m) pj[m] = Pt[j * LDB + m];
+        for (int i = k1 + lane; i <= j; i += 32) {
+          double s = 0.0;
+#pragma unroll
+          for (int m = 0; m < NB; ++m) s = fma(Pt[i * LDB + m], pj[m], s);
+          G[(size_t)j * ld + i] -= s;
+        }
+      }
+    }
+    __syncthreads();
+    mark(4);
+  }
+  if (cta == 0 && tid == 0) *info = 0;
+}
+
+}  // namespace
+
+bool small_potrf_upper(int n, double* G, int ld, int* info, cudaStream_t st) {
+  if (n < 1 || n > SMALL_CHOL_MAX) return false;
+  auto smem_for = [](int nn) { return sizeof(double) * ((size_t)3 * NB * (NB + 1) + 3 * NB + (size_t)(CMAX + nn) * (NB + 1)); };
+  static bool attr_set = false;
+  if (!attr_set) {
+    RLD_CUDA(cudaFuncSetAttribute(chol_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem_for(SMALL_CHOL_MAX)));
+    attr_set = true;
+  }
+  const size_t smem = smem_for(n);
+  static const bool profile = getenv("RLD_CHOL_PROFILE") != nullptr;
+  long long* prof = nullptr;
+  if (profile) RLD_CUDA(cudaMallocAsync(&prof, 8 * sizeof(long long), st)), RLD_CUDA(cudaMemsetAsync(prof, 0, 64, st));
+  chol_upper_kernel<<<CL, THREADS, smem, st>>>(n, G, ld, info, prof);
+  RLD_LAUNCH_CHECK();
+  if (profile) {
+    long long hp[8];
+    RLD_CUDA(cudaMemcpyAsync(hp, prof, sizeof hp, cudaMemcpyDeviceToHost, st));
+    RLD_CUDA(cudaStreamSynchronize(st));
+    RLD_CUDA(cudaFree(prof));
+    fprintf(stderr, "small_chol n=%d cycles: prologue %lld panel-row %lld barrier %lld load %lld factor||update %lld\n",
+            n, hp[0], hp[1], hp[2], hp[3], hp[4]);
+  }
+  return true;
+}
+
+}  // namespace rld

@@ -476,3 +476,50 @@ def test_normal_orthogonal_several_blocks(rld):
     est = rld.rstar_logdet(K, cfg)
     ref = O.rstar_dense(K, order=3, s=50, t=20, probe_kind="normal-orthogonal", k=0, q=5, seed=3, precond="identity")
     assert rel(est.value, ref.value) <= 1e-9
+
+
+# ---------------------------------------------------------------- dense Cholesky of the preconditioner build
+
+def _dense_cholesky(G):
+    import ctypes as C
+    import torch
+
+    from paper_2405_03474_b200._session import session
+
+    s = session()
+    t = torch.from_numpy(np.ascontiguousarray(G)).cuda()
+    info = C.c_int32(-7)
+    s.handle.check(s.lib.rld_dense_cholesky(s.handle.ptr, G.shape[0], t.data_ptr(), C.byref(info)), "dense_cholesky")
+    return np.tril(t.cpu().numpy()), info.value   # device column-major upper R = tril of the row-major view
+
+
+@pytest.mark.parametrize("n", [1, 5, 31, 32, 33, 64, 100, 255, 266, 522, 640, 700])
+@pytest.mark.parametrize("spectrum", ["wishart", "decaying"])
+def test_dense_cholesky_matches_lapack(rld, n, spectrum):
+    """One-cluster Cholesky (n <= 640) / cuSOLVER potrf (above) vs LAPACK: the Gram factor of
+    CholQR and the inner factor of src/precond.py:75-80."""
+    g = np.random.default_rng(n)
+    if spectrum == "wishart":
+        X = g.standard_normal((n + 8, n))
+        G = X.T @ X
+    else:
+        Q, _ = np.linalg.qr(g.standard_normal((n, n)))
+        G = (Q * np.logspace(6, -3, n)) @ Q.T
+        G = (G + G.T) / 2 + 1e-3 * np.eye(n)
+    L, info = _dense_cholesky(G)
+    assert info == 0
+    Lref = np.linalg.cholesky(G)
+    assert np.linalg.norm(L @ L.T - G) <= 1e-14 * np.linalg.norm(G) * max(1, n / 64)
+    assert np.linalg.norm(L - Lref) <= 1e-10 * np.linalg.norm(Lref)
+
+
+@pytest.mark.parametrize("n,bad", [(1, 0), (40, 0), (40, 5), (266, 37), (266, 265), (522, 300), (700, 650)])
+def test_dense_cholesky_reports_first_bad_pivot(rld, n, bad):
+    """info = 1-based index of the first non-positive pivot (LAPACK potrf), which the CholQR weak
+    test and the NotPositiveDefinite check read."""
+    g = np.random.default_rng(1)
+    X = g.standard_normal((n + 8, n))
+    G = X.T @ X
+    G[bad, bad] = -1.0
+    _, info = _dense_cholesky(G)
+    assert info == bad + 1
