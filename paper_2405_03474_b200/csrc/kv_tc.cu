@@ -83,6 +83,7 @@ struct TcParams {
   int bcol_step, brow_step;   // TMA coordinates of B per k-step: blocked (0, mp) or row-major (32, 0)
   unsigned int* sync;   // per-pass arrival counters of the phase-1 epoch barrier (zeroed per launch)
   int sync_k;           // k-steps per epoch (0: no barrier)
+  int sync_all;         // 1: the epoch barrier spans all passes (one counter)
   int ks;           // k-steps per tile
   int tiles;
   int npass;        // column passes in this launch
@@ -345,7 +346,7 @@ struct TcShape {
   static constexpr int TMEM_NEED = 2 * DW + NABUF * (int)ASTRIDE;
   static constexpr uint32_t TMEM_COLS = TMEM_NEED <= 256 ? 256 : 512;
   static_assert(TMEM_NEED <= 512, "TMEM budget");
-  static_assert(NT % 32 == 0 && NT <= 128, "NT");
+  static_assert(NT % 16 == 0 && (NT / DP) % 8 == 0 && NT <= 144 && (NT <= 128 || !OTF), "NT");
 };
 
 template <int MODE, int NT, bool OTF, int DIM, int FAM>
@@ -457,9 +458,11 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         if (p.sync_k > 0 && !it.in_tail() && it.v > 0 && (it.kstep & (p.sync_k - 1)) == 0) {
           ++epoch;
           if (lane == 0) {
-            unsigned int* ctr = p.sync + pass;
+            // one counter for all passes (p.sync_all): CTA c of every pass streams the same
+            // row tiles of K, so aligned passes read each K tile from HBM once, not npass times
+            unsigned int* ctr = p.sync + (p.sync_all ? 0 : pass);
             atomicAdd(ctr, 1u);
-            const unsigned int target = (unsigned int)(epoch * p.sched.G);
+            const unsigned int target = (unsigned int)(epoch * p.sched.G * (p.sync_all ? p.npass : 1));
             while (*(volatile unsigned int*)ctr < target) __nanosleep(100);
           }
           __syncwarp();
@@ -665,7 +668,7 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
           ptx::tc_fence_after();
           if (!(p.debug & 32)) {
 #pragma unroll
-            for (int c0 = 0; c0 < HALF; c0 += 16) {
+            for (int c0 = 0; c0 + 16 <= HALF; c0 += 16) {
               uint32_t v[16];
               ptx::tmem_ld_32x32b_x16(tmem + lane_base + (uint32_t)(buf * DW + c_base + c0), v);
               if (Sh::STACK) {
@@ -679,6 +682,14 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
 #pragma unroll
                 for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]);
               }
+            }
+            if constexpr (HALF % 16 == 8) {   // NT = 144: a last 8-column chunk (never stacked)
+              constexpr int c0 = HALF - 8;
+              uint32_t v[8];
+              ptx::tmem_ld_32x32b_x8(tmem + lane_base + (uint32_t)(buf * DW + c_base + c0), v);
+              ptx::tmem_wait_ld();
+#pragma unroll
+              for (int e = 0; e < 8; ++e) acc[c0 + e] += __uint_as_float(v[e]);
             }
           }
           ptx::tc_fence_before();
@@ -823,6 +834,7 @@ void launch_tc_stored(int nt, const CUtensorMap& mA, const CUtensorMap& mBh, con
     case 32: launch_tc<MODE, 32, false, 0, 0>(mA, mBh, mBl, p, grid, st); break;
     case 64: launch_tc<MODE, 64, false, 0, 0>(mA, mBh, mBl, p, grid, st); break;
     case 96: launch_tc<MODE, 96, false, 0, 0>(mA, mBh, mBl, p, grid, st); break;
+    case 144: launch_tc<MODE, 144, false, 0, 0>(mA, mBh, mBl, p, grid, st); break;
     default: launch_tc<MODE, 128, false, 0, 0>(mA, mBh, mBl, p, grid, st); break;
   }
 }
@@ -888,10 +900,23 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
                    KvWorkspace& ws, cudaStream_t st) {
   const int64_t n = op.n, rows = op.rows;
   const int ks = (int)ceil_div(n, TC_BK);
-  // vectors per pass: <= 128 (two TMEM accumulators + A buffers within 512 columns)
-  const int npass = (int)ceil_div(m, 128);
-  int width = (int)(ceil_div(ceil_div(m, npass), 32) * 32);
-  if (op.K == nullptr && width == 96) width = 128;   // on-the-fly kernels come in NT = 32, 64, 128
+  // vectors per pass (two TMEM accumulators + A buffers within 512 columns): NT = 32..128 in
+  // steps of 32, or 144 when that saves a pass of a stored-K product with 129..144 vectors
+  // (0.43 vs 0.47 ms at n = 16384, m = 140).  For more vectors NT = 144 measured slower than
+  // passes of 96 / 128 (config 2 sketch, m = 266: 0.82 vs 0.72 ms; RLD_TC_NT144=1 forces it).
+  static const int wide_env = getenv("RLD_TC_NT144") ? atoi(getenv("RLD_TC_NT144")) : -1;
+  const bool otf = op.K == nullptr;
+  const bool wide = wide_env == 1 || (wide_env < 0 && m > 128 && m <= 144);
+  int npass, width;
+  if (m > 128 && !otf && wide) {
+    npass = (int)ceil_div(m, 144);
+    width = (int)(ceil_div(ceil_div(m, npass), 16) * 16);
+    width = width > 128 ? 144 : (int)(ceil_div(width, 32) * 32);
+  } else {
+    npass = (int)ceil_div(m, 128);
+    width = (int)(ceil_div(ceil_div(m, npass), 32) * 32);
+    if (otf && width == 96) width = 128;   // on-the-fly kernels come in NT = 32, 64, 128
+  }
   const int64_t mp = (int64_t)npass * width;
   ws.bhi.reserve(sizeof(float) * mp * ks * 32);
   if (mode == 3) ws.blo.reserve(sizeof(float) * mp * ks * 32);
@@ -920,7 +945,6 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
     segs = (int)std::max<int64_t>(
         segs, cta_of_step(x0 + ks - 1, sc.tail_total, Gl) - cta_of_step(x0, sc.tail_total, Gl) + 1);
   }
-  const bool otf = op.K == nullptr;
   // tiled K: one 16 KB box = 128 contiguous rows of 128 bytes of the [tiles * ks * 128][32] view
   const CUtensorMap mA = otf ? make_points_map(op.pts4, n)
                              : op.tiled ? make_map(static_cast<const float*>(op.K), TC_BK,
@@ -964,6 +988,10 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
       return v > 0 ? (1 << pw) : 0;
     }();
     p.sync_k = (sc.R > 1 || (sc.R == 1 && sc.tail_total > 0)) ? sync_k : 0;
+    static const int sync_all = getenv("RLD_TC_SYNC_ALL") ? atoi(getenv("RLD_TC_SYNC_ALL")) : 0;
+    static const int sync_k_multi = getenv("RLD_TC_SYNC_K_MULTI") ? atoi(getenv("RLD_TC_SYNC_K_MULTI")) : 0;
+    p.sync_all = (npass > 1 && sync_all) ? 1 : 0;
+    if (p.sync_all && sync_k_multi > 0 && p.sync_k > 0) p.sync_k = sync_k_multi;
     ws.tc_sync.reserve(sizeof(unsigned int) * npass);
     p.sync = ws.tc_sync.as<unsigned int>();
     if (p.sync_k > 0) RLD_CUDA(cudaMemsetAsync(p.sync, 0, sizeof(unsigned int) * npass, st));

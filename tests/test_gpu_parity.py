@@ -125,7 +125,7 @@ def test_kv_apply_matches_numpy(rld, dtype, path, m):
 
 
 @pytest.mark.parametrize("n,m", [(256, 32), (1000, 1), (4099, 64), (16384, 32), (3000, 300), (2048, 400),
-                                 (20000, 128), (700, 17)])
+                                 (20000, 128), (700, 17), (5000, 266), (1500, 140), (3001, 522)])
 def test_tcgen05_product_matches_float64(rld, n, m):
     """fp32 stored K goes through the tcgen05 3xTF32 kernel (stream-K, TMEM A
     operand); check it against float64 numpy and against the CUDA-core path."""
