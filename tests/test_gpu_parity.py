@@ -312,6 +312,54 @@ def test_config3_full_size_properties(rld):
         assert np.max(np.abs(Y[:, i] - ref) / (np.abs(V) @ np.abs(k))) <= 2e-6
 
 
+def test_config3_on_the_fly_matches_stored(rld):
+    """Full config 3 (n = 65536): the on-the-fly path (K tiles generated from float32 points on
+    the tensor-core kernel) against the stored fp32 K -- two independent fp32 routes to the same
+    float64 estimate; each is within ~1e-6 of it, so they must agree far inside the 1e-4 budget."""
+    from paper_2405_03474_b200.workloads import baseline
+
+    wl = baseline(3)
+    M = rld.KernelMatrix(wl.spec, wl.points)
+    a = rld.estimate_logdet(M, replace(wl.config, path="stored"))
+    b = rld.estimate_logdet(M, replace(wl.config, path="on_the_fly"))
+    assert rel(a.value, b.value) <= 1e-5, (a.value, b.value)
+    assert rel(a.logdet_P, b.logdet_P) <= 1e-5
+
+
+def _otf_rows_check(rld, index, m, nrows, seed):
+    import torch
+
+    from paper_2405_03474_b200.workloads import baseline
+
+    wl = baseline(index)
+    R = rld.ResidentMatrix(rld.KernelMatrix(wl.spec, wl.points), dtype="fp32", path="on_the_fly")
+    g = np.random.default_rng(seed)
+    V = g.standard_normal((m, wl.n))
+    Y = R.kv_apply(torch.from_numpy(V).cuda()).cpu().numpy()
+    for i in g.choice(wl.n, nrows, replace=False):
+        k = O.covariance_block(wl.spec.family, wl.spec.amplitude, wl.spec.length_scale, wl.spec.jitter, wl.points,
+                               rows=slice(i, i + 1))[0]
+        assert np.max(np.abs(Y[:, i] - V @ k) / (np.abs(V) @ np.abs(k))) <= 2e-6
+    return R, wl
+
+
+def test_config4_full_size_properties(rld):
+    """Full config 4 (n = 262144, on the fly, r5, l = 1024, 64 probes): K cannot be stored,
+    so check size-independent properties -- bit-identical repeat, value = log det P + trace
+    term -- and row-sampled K.V against float64."""
+    R, wl = _otf_rows_check(rld, 4, 3, 16, 1)
+    a = R.estimate(wl.config)
+    b = R.estimate(wl.config)
+    assert np.isfinite(a.value) and a.value == b.value
+    assert a.value == pytest.approx(a.logdet_P + a.trace_term, rel=1e-12)
+    assert a.kv_products == 26
+
+
+def test_config5_full_size_products(rld):
+    """Full config 5 (n = 2^20, Matern-5/2 on the fly): row-sampled K.V against float64."""
+    _otf_rows_check(rld, 5, 2, 12, 2)
+
+
 # ---------------------------------------------------------------- SLQ (SURVEY.md §8(f) row 1)
 
 def _slq_cases():
