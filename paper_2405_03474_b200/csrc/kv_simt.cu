@@ -236,7 +236,7 @@ void launch_kv(const KvOperand& op, int64_t m, const T* V, int64_t ldv, double* 
 }  // namespace
 
 void kv_product(const KvOperand& op, int64_t m, const double* V, int64_t ldv, double* Y, int64_t ldy,
-                KvWorkspace& ws, cudaStream_t st, int* launches) {
+                KvWorkspace& ws, cudaStream_t st, int* launches, bool presplit) {
   if (m <= 0 || op.rows <= 0) return;
   const bool otf = (op.K == nullptr);
   if (op.dtype == RLD_FP64) {
@@ -247,7 +247,7 @@ void kv_product(const KvOperand& op, int64_t m, const double* V, int64_t ldv, do
     return;
   }
   if (kv_tc_supported(op) && (op.tiled || !getenv("RLD_NO_TC"))) {
-    kv_product_tc(op, op.tc_mode, m, V, ldv, Y, ldy, ws, st);
+    kv_product_tc(op, op.tc_mode, m, V, ldv, Y, ldy, ws, st, presplit);
     return;
   }
   if (op.tiled) fail(RLD_ERR_NOT_SUPPORTED, "tiled fp32 K needs the tensor-core product");

@@ -896,18 +896,15 @@ bool kv_tc_supported(const KvOperand& op) {
 }
 
 // Y (m x rows, float64, row stride ldy) = V (m x n float64 rows) K^T on the tensor cores.
-void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, int64_t ldv, double* Y, int64_t ldy,
-                   KvWorkspace& ws, cudaStream_t st) {
-  const int64_t n = op.n, rows = op.rows;
-  const int ks = (int)ceil_div(n, TC_BK);
-  // vectors per pass (two TMEM accumulators + A buffers within 512 columns): NT = 32..128 in
-  // steps of 32, or 144 when that saves a pass of a stored-K product with 129..144 vectors
-  // (0.43 vs 0.47 ms at n = 16384, m = 140).  For more vectors NT = 144 measured slower than
-  // passes of 96 / 128 (config 2 sketch, m = 266: 0.82 vs 0.72 ms; RLD_TC_NT144=1 forces it).
+namespace {
+// vectors per pass (two TMEM accumulators + A buffers within 512 columns): NT = 32..128 in
+// steps of 32, or 144 when that saves a pass of a stored-K product with 129..144 vectors
+// (0.43 vs 0.47 ms at n = 16384, m = 140).  For more vectors NT = 144 measured slower than
+// passes of 96 / 128 (config 2 sketch, m = 266: 0.82 vs 0.72 ms; RLD_TC_NT144=1 forces it).
+void tc_passes(const KvOperand& op, int64_t m, int& npass, int& width) {
   static const int wide_env = getenv("RLD_TC_NT144") ? atoi(getenv("RLD_TC_NT144")) : -1;
   const bool otf = op.K == nullptr;
   const bool wide = wide_env == 1 || (wide_env < 0 && m > 128 && m <= 144);
-  int npass, width;
   if (m > 128 && !otf && wide) {
     npass = (int)ceil_div(m, 144);
     width = (int)(ceil_div(ceil_div(m, npass), 16) * 16);
@@ -917,10 +914,36 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
     width = (int)(ceil_div(ceil_div(m, npass), 32) * 32);
     if (otf && width == 96) width = 128;   // on-the-fly kernels come in NT = 32, 64, 128
   }
+}
+}  // namespace
+
+bool kv_tc_b_layout(const KvOperand& op, int64_t m, KvWorkspace& ws, TcBLayout& out) {
+  if (!kv_tc_supported(op) || (!op.tiled && getenv("RLD_NO_TC"))) return false;
+  int npass = 0, width = 0;
+  tc_passes(op, m, npass, width);
+  const int64_t ks = ceil_div(op.n, TC_BK);
+  out.mp = (int64_t)npass * width;
+  out.ks = ks;
+  out.blocked = blocked_b() ? 1 : 0;
+  out.mode = op.tc_mode;
+  ws.bhi.reserve(sizeof(float) * out.mp * ks * 32);
+  if (op.tc_mode == 3) ws.blo.reserve(sizeof(float) * out.mp * ks * 32);
+  out.bhi = ws.bhi.as<float>();
+  out.blo = op.tc_mode == 3 ? ws.blo.as<float>() : nullptr;
+  return true;
+}
+
+void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, int64_t ldv, double* Y, int64_t ldy,
+                   KvWorkspace& ws, cudaStream_t st, bool presplit) {
+  const int64_t n = op.n, rows = op.rows;
+  const int ks = (int)ceil_div(n, TC_BK);
+  int npass = 0, width = 0;
+  tc_passes(op, m, npass, width);
+  const bool otf = op.K == nullptr;
   const int64_t mp = (int64_t)npass * width;
   ws.bhi.reserve(sizeof(float) * mp * ks * 32);
   if (mode == 3) ws.blo.reserve(sizeof(float) * mp * ks * 32);
-  {
+  if (!presplit) {
     const int64_t count = mp * ks * 32;
     const int blocks = (int)std::min<int64_t>(ceil_div(count, 256), 148 * 16);
     kv_tc_split<<<blocks, 256, 0, st>>>(V, ldv, m, n, mp, ks, mode, blocked_b(), ws.bhi.as<float>(),

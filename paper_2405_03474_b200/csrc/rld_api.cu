@@ -52,6 +52,13 @@ void DevBuf::reserve(size_t nbytes) {
   if (nbytes == 0) return;
   RLD_CUDA(cudaMalloc(&ptr, nbytes));
   bytes = nbytes;
+  // RLD_POISON=1 (debugging): fresh workspace is filled with NaN bytes, so a kernel that reads
+  // memory nothing wrote shows up as a NaN / wrong result instead of silently reusing stale values
+  static const bool poison = getenv("RLD_POISON") && getenv("RLD_POISON")[0] == '1';
+  if (poison) {   // the handle's stream does not order against the legacy stream: wait here
+    RLD_CUDA(cudaMemset(ptr, 0xFF, nbytes));
+    RLD_CUDA(cudaDeviceSynchronize());
+  }
 }
 
 void DevBuf::release() {
@@ -104,6 +111,7 @@ struct Work {
   DevBuf gsend, grecv;   // row-shard all-gather staging
   DevBuf qbasis, pbasis, coef;   // reorthogonalised Lanczos: bases (t x s x rows) and coefficients
   DevBuf endw, radii;            // normal-orthogonal probes: stream position, chi radii
+  DevBuf lz_dotp, lz_dotp2;      // fused Lanczos step: per-chunk dot partials
   DevBuf flagbuf;        // flag OR over ranks
   KvWorkspace kv;
 };
@@ -357,10 +365,18 @@ void gather_rows(rld_handle* h, const double* local, int64_t m, double* full) {
 // Y (m x rows) = V (m x n full) K^T restricted to the local rows.  tc_mode 1 =
 // single-pass TF32 on the tensor cores (power-iteration sketch products only),
 // 3 = 3xTF32 (everything whose value enters the estimate directly).
-void kv(rld_handle* h, int64_t m, const double* Vfull, double* Y, int tc_mode = 3) {
+void kv(rld_handle* h, int64_t m, const double* Vfull, double* Y, int tc_mode = 3, bool presplit = false) {
   KvOperand op = h->res.op();
   op.tc_mode = tc_mode;
-  kv_product(op, m, Vfull, op.n, Y, op.rows, h->wk.kv, h->st, nullptr);
+  kv_product(op, m, Vfull, op.n, Y, op.rows, h->wk.kv, h->st, nullptr, presplit);
+}
+
+// The fused Lanczos step (lanczos_fused.cu) covers one GPU, the three-term recurrence (no
+// reorthogonalisation) and s <= 64 probes.  Opt-in (RLD_FUSED_LANCZOS=1): it measured no faster
+// than the separate kernels at config 2 (19.43 vs 19.32 ms per estimate).
+bool fused_enabled_for(int64_t s, int k) {
+  static const bool on = getenv("RLD_FUSED_LANCZOS") && getenv("RLD_FUSED_LANCZOS")[0] == '1';
+  return on && lanczos_fused_fits(s, k);
 }
 
 // G (w x w, full) = Y^T Y for the rows x w column-major block.  The rows are cut
@@ -937,7 +953,44 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
     Pb = wk.pbasis.as<double>();
   }
   int products = 0;
+  const bool fused = h->world == 1 && !slq && !reorth && fused_enabled_for(s, k);
+  LanczosFusedArgs fa;
+  if (fused) {
+    const int64_t nch = ceil_div(nl, 128);
+    wk.lz_dotp.reserve(sizeof(double) * nch * s);
+    wk.lz_dotp2.reserve(sizeof(double) * nch * s);
+    KvOperand op = r.op();
+    op.tc_mode = 3;
+    static const bool presplit_on = !(getenv("RLD_FUSED_PRESPLIT") && getenv("RLD_FUSED_PRESPLIT")[0] == '0');
+    if (!presplit_on || !kv_tc_b_layout(op, s, wk.kv, fa.bl)) fa.bl = TcBLayout{};
+    fa.n = nl; fa.m = (int)s; fa.t = t; fa.rtol = c->breakdown_rtol;
+    fa.dotp = wk.lz_dotp.as<double>(); fa.dotp2 = wk.lz_dotp2.as<double>();
+    fa.live = live; fa.live_rw = live; fa.size = size;
+    fa.alpha = alpha; fa.beta = beta; fa.beta_ref = beta_ref;
+    fa.KX = KX; fa.sqrt_base = sqrt_base;
+    fa.p = p; fa.pp = pp; fa.u = u; fa.w = wv; fa.x = x;
+  }
   for (int j = 0; j < t; ++j) {
+    if (fused) {
+      kv(h, s, x, KX, 3, j > 0 && fa.bl.bhi != nullptr);   // x_j's operand written by the previous step
+      ++products;
+      lanczos_chunk_dots(nl, (int)s, x, KX, wk.lz_dotp.as<double>(), st);
+      if (j == t - 1) {
+        lanczos_alpha_chunks((int)s, nl, j, t, wk.lz_dotp.as<double>(), live, alpha, st);
+        break;
+      }
+      fa.j = j;
+      lanczos_fused_residual(fa, st);
+      if (k > 0) {   // w += U (h o (U^T w))
+        RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, k, (int)s, (int)nl, &ONE, U, (int)nl, wv,
+                               (int)nl, &ZERO, T, k));
+        scale_rows_colmajor(k, s, k, hv, false, T, st);
+        RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nl, (int)s, k, &ONE, U, (int)nl, T, k, &ONE,
+                               wv, (int)nl));
+      }
+      lanczos_fused_finish(fa, st);
+      continue;
+    }
     if (slq || reorth) copy_doubles(s * nl, x, Qb + (size_t)j * s * nl, st);
     if (reorth) copy_doubles(s * nl, p, Pb + (size_t)j * s * nl, st);
     const double* xin = x;                                // one GPU: the local rows are the full rows

@@ -97,12 +97,26 @@ struct KvWorkspace {
 };
 
 bool kv_tc_supported(const KvOperand& op);
+// presplit: the B operand (tf32 hi / lo of V in the k-step blocked layout) was already written
+// into ws.bhi / ws.blo by the caller (see kv_tc_b_layout); V is then unused.
 void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, int64_t ldv, double* Y, int64_t ldy,
-                   KvWorkspace& ws, cudaStream_t st);
+                   KvWorkspace& ws, cudaStream_t st, bool presplit = false);
+
+// Layout of the tensor-core B operand of an m-vector product: element (vector c, column j) at
+// ((j >> 5) * mp + c) * 32 + (j & 31) when blocked (else c * ks * 32 + j); hi = tf32(v) (mode 3)
+// or fp32(v) (mode 1), lo = fp32(v - hi).  Reserves the buffers; false if the product does not
+// run on the tensor cores.
+struct TcBLayout {
+  float* bhi = nullptr;
+  float* blo = nullptr;
+  int64_t mp = 0, ks = 0;
+  int blocked = 1, mode = 3;
+};
+bool kv_tc_b_layout(const KvOperand& op, int64_t m, KvWorkspace& ws, TcBLayout& out);
 
 // V: m x n rows (float64, device).  Y: m x rows (float64, device, row stride ldy).
 void kv_product(const KvOperand& op, int64_t m, const double* V, int64_t ldv, double* Y, int64_t ldy,
-                KvWorkspace& ws, cudaStream_t st, int* launches);
+                KvWorkspace& ws, cudaStream_t st, int* launches, bool presplit = false);
 
 // ---------------------------------------------------------------------------
 // RNG

@@ -14,8 +14,8 @@
 //      one warp per column) and writes the panel row R[k0:k1, j] over G;
 //   3. one cluster barrier, then every CTA pulls the whole panel row into shared memory and
 //      applies the rank-32 update G[k1:j, j] -= R[p, k1:j]^T R[p, j] to its columns.
-// The matrix stays in global memory (L2-resident at these sizes); cross-CTA data is read with
-// ld.global.cg after the barrier (release / acquire at cluster scope, plus a gpu fence).
+// The matrix stays in global memory (L2-resident at these sizes); data other CTAs wrote is read
+// with ld.global.cg after the barrier (release / acquire at cluster scope, plus a gpu fence).
 // info = first failing pivot (1-based), 0 on success, as LAPACK's potrf.
 #include "rld_internal.cuh"
 #include "rld_device.cuh"
@@ -30,9 +30,10 @@ constexpr int THREADS = 256;
 constexpr int SMALL_CHOL_MAX = 640;
 constexpr int CMAX = (SMALL_CHOL_MAX + CL - 1) / CL;   // columns per CTA
 
-// barrier.cluster release / acquire orders the global-memory writes before it for every thread of
-// the cluster; the cross-CTA reads after it go to L2 (ld.global.cg) anyway.
+// Global-memory writes of one CTA become visible to the others: gpu-scope fence, then the
+// cluster barrier (release / acquire); the reads after it go to L2 (ld.global.cg).
 __device__ __forceinline__ void cluster_sync_all() {
+  __threadfence();
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
@@ -74,10 +75,6 @@ __device__ __forceinline__ void chol_pivot(double (&a)[NB], double d, int lane, 
   if constexpr (J + 1 < NB) chol_pivot<J + 1>(a, dn, lane, bad, Ri, rowbuf);
 }
 
-__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
-               : "memory");
-}
 
 // Warp 0: factor the diagonal block in Ds (upper part valid, lower part zero / identity pad) into
 // R_pp (upper part of Ds), 1/R_ii (Ri) and R_pp^-1 (upper part of Rv).  Returns via Ri[0] < 0 a
@@ -167,14 +164,10 @@ chol_upper_kernel(int n, double* __restrict__ G, int ld, int* __restrict__ info,
     // ---- 2. panel row for this CTA's columns j >= k1: R[p, j] = R_pp^-T g_j
     const int jstart = k1 + ((cta - k1 % CL) + CL) % CL;   // first column j >= k1 with j % CL == cta
     const int ncol = jstart < n ? (n - 1 - jstart) / CL + 1 : 0;
-    for (int e = tid; e < ncol * NB; e += THREADS) {
+    for (int e = tid; e < ncol * NB; e += THREADS) {   // this CTA's own columns: plain loads are coherent
       const int m = e % NB, q = e / NB;
-      if (m < kb)
-        cp_async8(Gs + q * LDB + m, G + (size_t)(jstart + q * CL) * ld + k0 + m);
-      else
-        Gs[q * LDB + m] = 0.0;
+      Gs[q * LDB + m] = (m < kb) ? G[(size_t)(jstart + q * CL) * ld + k0 + m] : 0.0;
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     for (int e = tid; e < ncol * NB; e += THREADS) {
       const int m = e % NB, q = e / NB;
@@ -189,21 +182,31 @@ chol_upper_kernel(int n, double* __restrict__ G, int ld, int* __restrict__ info,
     write_rpp();
     // ---- 3. panel row (all columns) and the next diagonal block into shared memory
     const int k2 = min(n, k1 + NB), kb2 = k2 - k1;
-    for (int e = tid; e < NB * (n - k1); e += THREADS) {
-      const int m = e % NB, j = k1 + e / NB;
-      if (m < kb)
-        cp_async8(Pt + j * LDB + m, G + (size_t)j * ld + k0 + m);
-      else
-        Pt[j * LDB + m] = 0.0;
+    // other CTAs wrote these: L2 loads (ld.global.cg), never a possibly stale L1 line (a column's
+    // 128-byte lines straddle panels, so this SM may hold an old copy from the previous panel)
+    {
+      const int tot = NB * (n - k1);
+      constexpr int UNR = 8;
+      for (int e0 = tid; e0 < tot; e0 += THREADS * UNR) {
+        double v[UNR];
+#pragma unroll
+        for (int q = 0; q < UNR; ++q) {
+          const int e = e0 + q * THREADS;
+          const int m = e % NB, j = k1 + e / NB;
+          v[q] = (e < tot && m < kb) ? __ldcg(G + (size_t)j * ld + k0 + m) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < UNR; ++q) {
+          const int e = e0 + q * THREADS;
+          if (e < tot) Pt[(k1 + e / NB) * LDB + e % NB] = v[q];
+        }
+      }
     }
     for (int e = tid; e < NB * NB; e += THREADS) {
       const int i = e % NB, c = e / NB;
-      if (i < kb2 && c < kb2 && i <= c)
-        cp_async8(Dn + i * LDB + c, G + (size_t)(k1 + c) * ld + k1 + i);
-      else
-        Dn[i * LDB + c] = (i < kb2 && c < kb2) ? 0.0 : (i == c ? 1.0 : 0.0);
+      Dn[i * LDB + c] = (i < kb2 && c < kb2) ? ((i <= c) ? __ldcg(G + (size_t)(k1 + c) * ld + k1 + i) : 0.0)
+                                             : (i == c ? 1.0 : 0.0);
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     mark(3);
     // ---- 4a. next diagonal block = Dn - panel-row update (all threads), then warp 0 factors it
