@@ -3,8 +3,8 @@
 // Follows src/kernels.py:40-73 (RBF and Matern-5/2 values, diagonal set to
 // a^2 + jitter exactly) but forms r^2 from direct coordinate differences
 // instead of |x|^2 + |y|^2 - 2 x.y: same value up to rounding, and no
-// cancellation for close pairs.  Arithmetic is float64; the
-// fp32 store rounds the float64 value once.
+// cancellation for close pairs.  r^2 is float64; the kernel
+// function is float64 for a float64 K and float32 (MUFU exp) for a float32 K.
 //
 // One CTA writes a 32-row x 256-column tile; each thread owns one column and
 // walks the 32 rows, so every row store is a coalesced 256-element segment.
@@ -55,7 +55,17 @@ kgen_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, int64_t ro
       }
     }
     double v;
-    if (FAM == RLD_RBF) {
+    if constexpr (sizeof(T) == 4) {
+      // float32 K: r^2 from float64 differences as above, the kernel function in float32
+      // (relative error ~3e-7, about the float32 rounding of the stored value itself; the fp64
+      // exp made this kernel FP64-bound at 3-4x the time of writing K)
+      if (FAM == RLD_RBF) {
+        v = (double)((float)kp.a2 * __expf(-(float)(r2 * kp.inv_2l2)));
+      } else {
+        const float u = sqrtf((float)r2) * (float)kp.s5_over_l;
+        v = (double)((float)kp.a2 * (1.0f + u + u * u * (1.0f / 3.0f)) * __expf(-u));
+      }
+    } else if (FAM == RLD_RBF) {
       v = kp.a2 * exp(-r2 * kp.inv_2l2);
     } else {
       const double u = sqrt(r2) * kp.s5_over_l;
