@@ -84,6 +84,7 @@ struct TcParams {
   unsigned int* sync;   // per-pass arrival counters of the phase-1 epoch barrier (zeroed per launch)
   int sync_k;           // k-steps per epoch (0: no barrier)
   int sync_all;         // 1: the epoch barrier spans all passes (one counter)
+  int arrive_sem;       // CTA pairs: semantics of the remote mbarrier arrives (RLD_TC_ARRIVE)
   int ks;           // k-steps per tile
   int tiles;
   int npass;        // column passes in this launch
@@ -327,33 +328,46 @@ __device__ __forceinline__ void load16(const uint8_t* rowp, int row, int half, u
 // (scripts/otf_points_fp32.py), far inside the 1e-4 fp32 budget.
 constexpr uint32_t PTS_BYTES = 1024;
 
-template <int MODE, int NT, bool OTF = false>
+template <int MODE, int NT, bool OTF = false, bool CG2 = false>
 struct TcShape {
   static constexpr bool STACK = MODE == 3 && NT == 32;  // [Bhi; Blo] as one N = 2 NT operand
   static constexpr int DW = STACK ? 2 * NT : NT;       // accumulator columns
-  static constexpr uint32_t B_BYTES = (uint32_t)NT * 128;
+  // CTA pairs (CG2, cta_group::2): each CTA holds half of the B operand's N rows -- NT / 2 rows of
+  // Bhi and of Blo, or, stacked, all NT rows of Bhi (leader) / Blo (peer)
+  static constexpr int BROWS = (CG2 && !STACK) ? NT / 2 : NT;   // B rows per operand in this CTA
+  static constexpr int BOPS = (CG2 && STACK) ? 1 : (MODE == 3 ? 2 : 1);   // B operands in this CTA's stage
+  static constexpr uint32_t B_BYTES = (uint32_t)BROWS * 128;
+  static constexpr int MM = CG2 ? 256 : 128;                    // MMA M (over the pair)
   static constexpr uint32_t A_REGION = OTF ? PTS_BYTES : A_BYTES;
-  static constexpr uint32_t STAGE = A_REGION + B_BYTES * (MODE == 3 ? 2 : 1);
+  static constexpr uint32_t STAGE = A_REGION + B_BYTES * BOPS;
   static constexpr uint32_t ASTRIDE = MODE == 3 ? 64 : 32;  // TMEM columns per A buffer (hi | lo)
-  static constexpr uint32_t A_COL0 = 2 * DW;
+  // TMEM accumulator buffers: two, or (CTA pairs) three / four -- the pair's drain handshake
+  // (multicast commit, remote arrive) is longer than one group of MMAs
+  static constexpr int NACC = (CG2 && DW <= 64) ? 3 : 2;
+  static constexpr uint32_t A_COL0 = NACC * DW;
   // warps per TMEM lane quarter: drains (DP; each holds NT / DP fp32 running sums in
   // registers) and converters (CP = 4 - DP), within the 20-warp CTA.  A third
   // converter warp per quarter measured +6 % at NT = 64 (config 4 on the fly) and
   // -10 % at NT = 32, where the extra polling warps cost more than they hide
   static constexpr int DP = NT == 64 ? 1 : 2;
   static constexpr int CP = 4 - DP;
-  static constexpr int NABUF = (512 - 2 * DW) / (int)ASTRIDE < NABUF_MAX ? (512 - 2 * DW) / (int)ASTRIDE : NABUF_MAX;
-  static constexpr int TMEM_NEED = 2 * DW + NABUF * (int)ASTRIDE;
+  static constexpr int NABUF =
+      (512 - NACC * DW) / (int)ASTRIDE < NABUF_MAX ? (512 - NACC * DW) / (int)ASTRIDE : NABUF_MAX;
+  static constexpr int TMEM_NEED = NACC * DW + NABUF * (int)ASTRIDE;
   static constexpr uint32_t TMEM_COLS = TMEM_NEED <= 256 ? 256 : 512;
   static_assert(TMEM_NEED <= 512, "TMEM budget");
+  // a converter posts step j's afull only after starting step j + CP, whose TMEM buffer must not
+  // be the one step j's MMAs still hold: more buffers than converter warps per quarter
+  static_assert(NABUF > CP, "TMEM A buffers");
   static_assert(NT % 16 == 0 && (NT / DP) % 8 == 0 && NT <= 144 && (NT <= 128 || !OTF), "NT");
+  static_assert(!CG2 || (!OTF && (STACK || (NT / 2) % 16 == 0)), "pair variant: stored K, half of N a multiple of 16");
 };
 
-template <int MODE, int NT, bool OTF, int DIM, int FAM>
+template <int MODE, int NT, bool OTF, int DIM, int FAM, bool CG2 = false>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
              const __grid_constant__ CUtensorMap tmBlo, const TcParams p) {
-  using Sh = TcShape<MODE, NT, OTF>;
+  using Sh = TcShape<MODE, NT, OTF, CG2>;
   constexpr int DW = Sh::DW;
   constexpr uint32_t B_BYTES = Sh::B_BYTES, ASTRIDE = Sh::ASTRIDE, A_COL0 = Sh::A_COL0;
   constexpr uint32_t AR = Sh::A_REGION;   // K tile (stored) or column points (on the fly)
@@ -373,20 +387,26 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
   // One wait on afull + one on bfull and one commit per step keep the serial
   // MMA-issue loops short.
   const int SA = p.sa, SB = p.sb;
-  constexpr uint32_t BST = B_BYTES * (MODE == 3 ? 2 : 1);
+  constexpr uint32_t BST = B_BYTES * Sh::BOPS;
   uint8_t* const bring = smem + (size_t)SA * AR;
   uint64_t* kfull = reinterpret_cast<uint64_t*>(bring + (size_t)SB * BST);
   uint64_t* kempty = kfull + SA;
   uint64_t* bfull = kempty + SA;
   uint64_t* bempty = bfull + SB;
   uint64_t* afull = bempty + SB;
-  uint64_t* accfull = afull + SB;    // [2]
-  uint64_t* accempty = accfull + 2;  // [2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accempty + 2);
+  constexpr int NACC = Sh::NACC;
+  uint64_t* accfull = afull + SB;       // [NACC]
+  uint64_t* accempty = accfull + NACC;  // [NACC]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accempty + NACC);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int pass = (int)(blockIdx.x % p.npass);
-  const int64_t cta = blockIdx.x / p.npass;
+  // CG2: blockIdx.x = 2 (pair * npass + pass) + rank; the schedule walks pair tiles of 256 rows,
+  // rank r takes row tile 2 t + r
+  const int rank = CG2 ? (int)(blockIdx.x & 1) : 0;
+  const int64_t bid = CG2 ? (int64_t)(blockIdx.x >> 1) : (int64_t)blockIdx.x;
+  const int pass = (int)(bid % p.npass);
+  const int64_t cta = bid / p.npass;
+  auto row_tile = [&](int t) { return CG2 ? 2 * t + rank : t; };
   const int b_row0 = pass * NT;
   float* const partial = p.partial + (size_t)pass * p.tiles * p.segs * NT * TC_BM;
   unsigned long long* const prof = p.prof ? p.prof + blockIdx.x * 16 : nullptr;
@@ -402,18 +422,25 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     for (int i = 0; i < SB; ++i) {
       ptx::mbar_init(&bfull[i], 1);
       ptx::mbar_init(&bempty[i], 1);
-      ptx::mbar_init(&afull[i], 4);
+      ptx::mbar_init(&afull[i], CG2 ? 8 : 4);   // CG2: the leader's barrier counts both CTAs' converters
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NACC; ++i) {
       ptx::mbar_init(&accfull[i], 2);   // one commit per MMA-issuing warp
-      ptx::mbar_init(&accempty[i], 4 * Sh::DP);
+      ptx::mbar_init(&accempty[i], (CG2 ? 8 : 4) * Sh::DP);
     }
     ptx::fence_mbarrier_init();
   }
-  if (warp == 2) ptx::tmem_alloc(tmem_holder, Sh::TMEM_COLS);
+  if (warp == 2) {
+    if constexpr (CG2) ptx::tmem_alloc_pair(tmem_holder, Sh::TMEM_COLS);
+    else ptx::tmem_alloc(tmem_holder, Sh::TMEM_COLS);
+  }
   ptx::tc_fence_before();
   __syncthreads();
+  if constexpr (CG2) ptx::cluster_sync();   // both CTAs' barriers initialised before any remote arrive
   ptx::tc_fence_after();
+  // barriers of the pair leader, as shared::cluster addresses (remote arrives / 2-SM TMA)
+  const uint32_t afull_l = CG2 ? ptx::mapa(afull, 0) : 0, accempty_l = CG2 ? ptx::mapa(accempty, 0) : 0;
+  const uint32_t bfull_l = CG2 ? ptx::mapa(bfull, 0) : 0;
   const uint32_t tmem = *tmem_holder;
 
   if (StepIter<false, false>(p.sched, cta, 1).valid()) {
@@ -436,9 +463,9 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
           } else {
             ptx::mbar_arrive_expect_tx(&kfull[s], AR);
             if (p.a_tiled)
-              ptx::tma_load_2d(st, &tmA, &kfull[s], 0, (it.tile * p.ks + it.kstep) * TC_BM);
+              ptx::tma_load_2d(st, &tmA, &kfull[s], 0, (row_tile(it.tile) * p.ks + it.kstep) * TC_BM);
             else
-              ptx::tma_load_2d(st, &tmA, &kfull[s], it.kstep * TC_BK, it.tile * TC_BM);
+              ptx::tma_load_2d(st, &tmA, &kfull[s], it.kstep * TC_BK, row_tile(it.tile) * TC_BM);
           }
         }
         __syncwarp();
@@ -462,7 +489,8 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             // row tiles of K, so aligned passes read each K tile from HBM once, not npass times
             unsigned int* ctr = p.sync + (p.sync_all ? 0 : pass);
             atomicAdd(ctr, 1u);
-            const unsigned int target = (unsigned int)(epoch * p.sched.G * (p.sync_all ? p.npass : 1));
+            const unsigned int target =
+                (unsigned int)(epoch * p.sched.G * (p.sync_all ? p.npass : 1) * (CG2 ? 2 : 1));
             while (*(volatile unsigned int*)ctr < target) __nanosleep(100);
           }
           __syncwarp();
@@ -470,15 +498,27 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         ptx::mbar_wait_idle(&bempty[s], it.ph ^ 1, p.wait_mode, p.wait_ns);
         if (ptx::elect_one()) {
           uint8_t* st = bring + (size_t)s * BST;
-          ptx::mbar_arrive_expect_tx(&bfull[s], BST);
-          // B in k-step blocks [ks][mp][32]: one contiguous NT x 128-byte box per step
-          ptx::tma_load_2d(st, &tmBhi, &bfull[s], it.kstep * p.bcol_step, it.kstep * p.brow_step + b_row0);
-          if (MODE == 3)
-            ptx::tma_load_2d(st + B_BYTES, &tmBlo, &bfull[s], it.kstep * p.bcol_step, it.kstep * p.brow_step + b_row0);
+          const int bcol = it.kstep * p.bcol_step, brow = it.kstep * p.brow_step + b_row0;
+          if constexpr (CG2) {
+            // each CTA loads its half of N; both count on the leader's barrier
+            if (rank == 0) ptx::mbar_arrive_expect_tx(&bfull[s], 2 * BST);
+            const uint32_t bar = bfull_l + 8u * (uint32_t)s;
+            if (Sh::STACK) {
+              ptx::tma_load_2d_pair(st, rank ? &tmBlo : &tmBhi, bar, bcol, brow);
+            } else {
+              ptx::tma_load_2d_pair(st, &tmBhi, bar, bcol, brow + rank * Sh::BROWS);
+              if (MODE == 3) ptx::tma_load_2d_pair(st + B_BYTES, &tmBlo, bar, bcol, brow + rank * Sh::BROWS);
+            }
+          } else {
+            ptx::mbar_arrive_expect_tx(&bfull[s], BST);
+            // B in k-step blocks [ks][mp][32]: one contiguous NT x 128-byte box per step
+            ptx::tma_load_2d(st, &tmBhi, &bfull[s], bcol, brow);
+            if (MODE == 3) ptx::tma_load_2d(st + B_BYTES, &tmBlo, &bfull[s], bcol, brow);
+          }
         }
         __syncwarp();
       }
-    } else if (warp == 1 || warp == 3) {
+    } else if ((warp == 1 || warp == 3) && rank == 0) {
       // ---------------- MMA issuers: warps 1 and 3 take alternate steps (whole warp walks
       // the pipeline so every descriptor is warp-uniform; one elected lane issues).  A
       // named-barrier baton hands the issue slot from step j's warp to step j+1's, so the
@@ -487,7 +527,7 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       // commits accfull at every group end (count 2): together the two commits cover
       // all MMAs of the group.
       const int mpar = warp == 3;
-      constexpr uint32_t idesc = ptx::idesc_tf32(TC_BM, DW);
+      constexpr uint32_t idesc = ptx::idesc_tf32(Sh::MM, DW);
       const uint64_t desc0 = ptx::smem_desc_sw128(ptx::smem_u32(bring));
       constexpr uint64_t LO_OFF = (uint64_t)(B_BYTES >> 4);   // Blo rows, in descriptor units
       int64_t gi = -1;  // group index
@@ -499,14 +539,14 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         if ((it.v & 1) == mpar) {
           const int s = it.s;
           const unsigned long long t0 = prof ? clock64() : 0;
-          if (gstart && gi >= 2) ptx::mbar_wait(&accempty[gi & 1], (uint32_t)(((gi >> 1) - 1) & 1));
+          if (gstart && gi >= NACC) ptx::mbar_wait(&accempty[gi % NACC], (uint32_t)((gi / NACC - 1) & 1));
           ptx::mbar_wait(&afull[s], it.ph);
           ptx::mbar_wait(&bfull[s], it.ph);
           const unsigned long long t1 = prof ? clock64() : 0;
           if (it.v > 0) ptx::named_bar_sync(mpar ? 1 : 2, 64);   // baton from step j - 1
           const unsigned long long t2 = prof ? clock64() : 0;
           ptx::tc_fence_after();
-          const uint32_t d = tmem + (uint32_t)(gi & 1) * DW;
+          const uint32_t d = tmem + (uint32_t)(gi % NACC) * DW;
           const uint32_t a0 = tmem + A_COL0 + ASTRIDE * s;
           const uint64_t bdesc = desc0 + (uint64_t)((s * BST) >> 4);
           const bool leader = ptx::elect_one();
@@ -515,21 +555,28 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             for (int kk = 0; kk < TC_BK / 8; ++kk) {
               const uint64_t bd = bdesc + 2 * kk;  // +32 bytes along k
               const uint32_t acc = (gstart && kk == 0) ? 0u : 1u;
+              auto mma = [&](uint32_t dd, uint32_t aa, uint64_t bb, uint32_t ac) {
+                if constexpr (CG2) ptx::mma_tf32_ts_pair(dd, aa, bb, idesc, ac);
+                else ptx::mma_tf32_ts(dd, aa, bb, idesc, ac);
+              };
               if (MODE == 1) {
-                ptx::mma_tf32_ts(d, a0 + 8 * kk, bd, idesc, acc);
+                mma(d, a0 + 8 * kk, bd, acc);
               } else if (Sh::STACK) {
-                ptx::mma_tf32_ts(d, a0 + 8 * kk, bd, idesc, acc);        // D += Ahi [Bhi; Blo]
-                ptx::mma_tf32_ts(d, a0 + 32 + 8 * kk, bd, idesc, 1u);    // D += Alo [Bhi; Blo]
+                mma(d, a0 + 8 * kk, bd, acc);        // D += Ahi [Bhi; Blo]
+                mma(d, a0 + 32 + 8 * kk, bd, 1u);    // D += Alo [Bhi; Blo]
               } else {
-                ptx::mma_tf32_ts(d, a0 + 8 * kk, bd, idesc, acc);            // D += Ahi Bhi
-                ptx::mma_tf32_ts(d, a0 + 8 * kk, bd + LO_OFF, idesc, 1u);    // D += Ahi Blo
-                ptx::mma_tf32_ts(d, a0 + 32 + 8 * kk, bd, idesc, 1u);        // D += Alo Bhi
+                mma(d, a0 + 8 * kk, bd, acc);            // D += Ahi Bhi
+                mma(d, a0 + 8 * kk, bd + LO_OFF, 1u);    // D += Ahi Blo
+                mma(d, a0 + 32 + 8 * kk, bd, 1u);        // D += Alo Bhi
               }
             }
           }
           __syncwarp();
           if (it.v + 1 < it.vend) ptx::named_bar_arrive(mpar ? 2 : 1, 64);   // baton to step j + 1
-          if (leader) ptx::tc_commit(&bempty[s]);
+          if (leader) {
+            if constexpr (CG2) ptx::tc_commit_pair(&bempty[s]);
+            else ptx::tc_commit(&bempty[s]);
+          }
           if (prof) {
             t_acc += t1 - t0;
             t_afull += t2 - t1;
@@ -538,7 +585,10 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
           }
         }
         if (gend) {
-          if (ptx::elect_one()) ptx::tc_commit(&accfull[gi & 1]);
+          if (ptx::elect_one()) {
+            if constexpr (CG2) ptx::tc_commit_pair(&accfull[gi % NACC]);
+            else ptx::tc_commit(&accfull[gi % NACC]);
+          }
           __syncwarp();
         }
       }
@@ -561,11 +611,15 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       int grow = 0, wrow0 = 0;   // global row of this lane / of lane 0 (n < 2^31)
       const int n32 = (int)p.n;
       int pend = -1;             // A buffer whose TMEM stores are in flight
+      auto arrive_afull = [&](int buf) {   // CG2: on the leader's barrier
+        if constexpr (CG2) ptx::mbar_arrive_cluster(afull_l + 8u * (uint32_t)buf, p.arrive_sem);
+        else ptx::mbar_arrive(&afull[buf]);
+      };
       auto post = [&](int buf) {
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&afull[buf]);
+        if (lane == 0) arrive_afull(buf);
       };
       unsigned long long cv_full = 0;
       const unsigned long long cv_start = prof ? clock64() : 0;
@@ -597,7 +651,7 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
           __syncwarp();
           if (lane == 0) {
             ptx::mbar_arrive(&kempty[s]);
-            ptx::mbar_arrive(&afull[sb]);
+            arrive_afull(sb);
           }
           continue;
         }
@@ -661,9 +715,9 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
       while (si.next(tile, len, seg)) {
         for (int g0 = 0; g0 < len; g0 += GROUP) {
           ++gi;
-          const int buf = (int)(gi & 1);
+          const int buf = (int)(gi % NACC);
           const unsigned long long d0 = prof ? clock64() : 0;
-          ptx::mbar_wait_idle(&accfull[buf], (uint32_t)((gi >> 1) & 1), p.wait_mode, p.wait_ns);
+          ptx::mbar_wait_idle(&accfull[buf], (uint32_t)((gi / NACC) & 1), p.wait_mode, p.wait_ns);
           if (prof) dr_wait += clock64() - d0;
           ptx::tc_fence_after();
           if (!(p.debug & 32)) {
@@ -694,12 +748,16 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
           }
           ptx::tc_fence_before();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&accempty[buf]);
+          if (lane == 0) {
+            if constexpr (CG2) ptx::mbar_arrive_cluster(accempty_l + 8u * (uint32_t)buf, p.arrive_sem);
+            else ptx::mbar_arrive(&accempty[buf]);
+          }
         }
-        float* P = partial + ((size_t)tile * p.segs + seg) * (size_t)NT * TC_BM;
+        const int rt = row_tile(tile);
+        float* P = partial + ((size_t)rt * p.segs + seg) * (size_t)NT * TC_BM;
 #pragma unroll
         for (int c = 0; c < HALF; ++c) {
-          P[(size_t)(c_base + c) * TC_BM + row] = acc[c];
+          if (rt < p.tiles) P[(size_t)(c_base + c) * TC_BM + row] = acc[c];
           acc[c] = 0.f;
         }
       }
@@ -710,12 +768,17 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 2) ptx::tmem_dealloc(tmem, Sh::TMEM_COLS);
+  if constexpr (CG2) {
+    ptx::cluster_sync();   // the peer's last remote arrives have landed; no MMA reads TMEM any more
+    if (warp == 2) ptx::tmem_dealloc_pair(tmem, Sh::TMEM_COLS);
+  } else {
+    if (warp == 2) ptx::tmem_dealloc(tmem, Sh::TMEM_COLS);
+  }
 }
 
 // Y[c * ldy + i] = sum over the tile's segments of the partials (float64 accumulation, fixed order)
 __global__ void kv_tc_reduce(const float* __restrict__ P, Sched sc, int tiles, int segs, int nt, int64_t m,
-                             int64_t rows, double* __restrict__ Y, int64_t ldy) {
+                             int64_t rows, double* __restrict__ Y, int64_t ldy, int pair) {
   const int64_t count = m * rows;
   const int full = sc.R * sc.G;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
@@ -723,9 +786,10 @@ __global__ void kv_tc_reduce(const float* __restrict__ P, Sched sc, int tiles, i
     const int64_t c = e / rows, i = e % rows;
     const int64_t pass = c / nt, cc = c % nt;
     const int64_t tile = i / TC_BM, r = i % TC_BM;
+    const int64_t unit = pair ? tile >> 1 : tile;   // schedule unit (a pair tile for CTA pairs)
     int nseg = 1;
-    if (tile >= full) {
-      const int64_t x0 = (tile - full) * sc.ks;
+    if (unit >= full) {
+      const int64_t x0 = (unit - full) * sc.ks;
       nseg = (int)(cta_of_step(x0 + sc.ks - 1, sc.tail_total, sc.G) - cta_of_step(x0, sc.tail_total, sc.G) + 1);
     }
     const float* Pp = P + (size_t)pass * tiles * segs * nt * TC_BM;
@@ -805,13 +869,13 @@ int max_smem_optin() {
   return v;
 }
 
-template <int MODE, int NT, bool OTF, int DIM, int FAM>
+template <int MODE, int NT, bool OTF, int DIM, int FAM, bool CG2 = false>
 void launch_tc(const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl, TcParams p, int64_t grid,
                cudaStream_t st) {
-  using Sh = TcShape<MODE, NT, OTF>;
+  using Sh = TcShape<MODE, NT, OTF, CG2>;
   const size_t extra = 1024 + 8 * 96;   // alignment slack + barriers
   const size_t smem_cap = (size_t)max_smem_optin() - 1024 - extra;
-  constexpr size_t BST = (size_t)Sh::B_BYTES * (MODE == 3 ? 2 : 1);
+  constexpr size_t BST = (size_t)Sh::B_BYTES * Sh::BOPS;
   static const int max_sa = getenv("RLD_TC_STAGES") ? atoi(getenv("RLD_TC_STAGES")) : 12;
   // B ring = TMEM A buffers (as many as TMEM leaves, <= 8); the A-source ring (K tiles
   // from HBM) takes the rest of shared memory, at least 3 stages
@@ -821,15 +885,40 @@ void launch_tc(const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap&
   p.sa = (int)std::min<size_t>(max_sa, (smem_cap - sb * BST) / Sh::A_REGION);
   p.tmem_cols = Sh::TMEM_COLS;
   const size_t smem = (size_t)p.sa * Sh::A_REGION + (size_t)p.sb * BST + extra;
-  RLD_CUDA(cudaFuncSetAttribute(kv_tc_kernel<MODE, NT, OTF, DIM, FAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
-  kv_tc_kernel<MODE, NT, OTF, DIM, FAM><<<(unsigned)grid, TC_THREADS, smem, st>>>(mA, mBh, mBl, p);
+  auto kern = kv_tc_kernel<MODE, NT, OTF, DIM, FAM, CG2>;
+  RLD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if constexpr (CG2) {   // CTA pairs: clusters of two on one TPC
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(TC_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    RLD_CUDA(cudaLaunchKernelEx(&cfg, kern, mA, mBh, mBl, p));
+  } else {
+    kern<<<(unsigned)grid, TC_THREADS, smem, st>>>(mA, mBh, mBl, p);
+  }
   RLD_LAUNCH_CHECK();
 }
 
 template <int MODE>
 void launch_tc_stored(int nt, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl,
-                      const TcParams& p, int64_t grid, cudaStream_t st) {
+                      const TcParams& p, int64_t grid, cudaStream_t st, bool cg2 = false) {
+  if (cg2) {
+    switch (nt) {
+      case 32: launch_tc<MODE, 32, false, 0, 0, true>(mA, mBh, mBl, p, grid, st); break;
+      case 64: launch_tc<MODE, 64, false, 0, 0, true>(mA, mBh, mBl, p, grid, st); break;
+      case 96: launch_tc<MODE, 96, false, 0, 0, true>(mA, mBh, mBl, p, grid, st); break;
+      default: launch_tc<MODE, 128, false, 0, 0, true>(mA, mBh, mBl, p, grid, st); break;
+    }
+    return;
+  }
   switch (nt) {
     case 32: launch_tc<MODE, 32, false, 0, 0>(mA, mBh, mBl, p, grid, st); break;
     case 64: launch_tc<MODE, 64, false, 0, 0>(mA, mBh, mBl, p, grid, st); break;
@@ -952,22 +1041,32 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
   }
   const int G = sm_count();
   const int tiles = (int)ceil_div(rows, TC_BM);
-  const int64_t total = (int64_t)tiles * ks;
-  const int64_t Gl = std::min<int64_t>(std::max(1, G / npass), total);
+  // CTA pairs (stored K, NT >= 64; RLD_TC_CG2=0/1 forces off/on): 2-SM MMAs (cta_group::2,
+  // M = 256), each SM loads half of the B operand, the schedule runs over pair tiles of 256 rows.
+  // Config 2 sketch (m = 266) 0.69 vs 0.74 ms, config 3 Lanczos (m = 64) 3.57 vs 3.70 ms; the
+  // HBM-bound m = 32 product is unchanged (0.215 vs 0.212 ms), so it keeps single CTAs.
+  static const int cg2_env = getenv("RLD_TC_CG2") ? atoi(getenv("RLD_TC_CG2")) : -1;
+  const bool cg2_ok = !otf && (width == 32 ? mode == 3 : (width / 2) % 16 == 0) && width <= 128;
+  const bool cg2 = cg2_ok && (cg2_env == 1 || (cg2_env < 0 && width >= 64));
+  const int units = cg2 ? (tiles + 1) / 2 : tiles;
+  const int per = cg2 ? 2 : 1;
+  const int64_t total = (int64_t)units * ks;
+  const int64_t Gl = std::min<int64_t>(std::max(1, G / (npass * per)), total);
   Sched sc{};
   sc.ks = ks;
   sc.G = (int)Gl;
   {
     static const bool streamk_only = getenv("RLD_TC_STREAMK") && getenv("RLD_TC_STREAMK")[0] == '1';
-    sc.R = streamk_only ? 0 : (int)(tiles / Gl);
+    sc.R = streamk_only ? 0 : (int)(units / Gl);
   }
-  sc.tail_total = (int64_t)(tiles - sc.R * Gl) * ks;
+  sc.tail_total = (int64_t)(units - sc.R * Gl) * ks;
   int segs = 1;
-  for (int t = sc.R * (int)Gl; t < tiles; ++t) {
+  for (int t = sc.R * (int)Gl; t < units; ++t) {
     const int64_t x0 = (int64_t)(t - sc.R * Gl) * ks;
     segs = (int)std::max<int64_t>(
         segs, cta_of_step(x0 + ks - 1, sc.tail_total, Gl) - cta_of_step(x0, sc.tail_total, Gl) + 1);
   }
+  const int64_t nblocks = Gl * npass * per;
   // tiled K: one 16 KB box = 128 contiguous rows of 128 bytes of the [tiles * ks * 128][32] view
   const CUtensorMap mA = otf ? make_points_map(op.pts4, n)
                              : op.tiled ? make_map(static_cast<const float*>(op.K), TC_BK,
@@ -995,12 +1094,14 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
     static const int wns = getenv("RLD_TC_WAIT_NS") ? atoi(getenv("RLD_TC_WAIT_NS")) : 256;
     p.wait_mode = wm;
     p.wait_ns = (uint32_t)wns;
+    static const int asem = getenv("RLD_TC_ARRIVE") ? atoi(getenv("RLD_TC_ARRIVE")) : 2;
+    p.arrive_sem = asem;
   }
   static const bool prof_on = getenv("RLD_TC_PROFILE") != nullptr;
   static DevBuf prof_buf;
   if (prof_on) {
-    prof_buf.reserve(sizeof(unsigned long long) * 16 * (size_t)(Gl * npass));
-    RLD_CUDA(cudaMemsetAsync(prof_buf.ptr, 0, sizeof(unsigned long long) * 16 * (size_t)(Gl * npass), st));
+    prof_buf.reserve(sizeof(unsigned long long) * 16 * (size_t)nblocks);
+    RLD_CUDA(cudaMemsetAsync(prof_buf.ptr, 0, sizeof(unsigned long long) * 16 * (size_t)nblocks, st));
     p.prof = prof_buf.as<unsigned long long>();
   }
   {
@@ -1023,26 +1124,37 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
   p.partial = ws.tc_partial.as<float>();
   const bool blk = blocked_b();
   const int64_t bcols = blk ? TC_BK : (int64_t)ks * TC_BK, brows = blk ? mp * ks : mp;
-  const CUtensorMap mBh = make_map(ws.bhi.as<float>(), bcols, brows, bcols, width);
-  const CUtensorMap mBl = mode == 3 ? make_map(ws.blo.as<float>(), bcols, brows, bcols, width) : mBh;
+  const int bbox = (cg2 && !(mode == 3 && width == 32)) ? width / 2 : width;   // B rows per TMA box
+  const CUtensorMap mBh = make_map(ws.bhi.as<float>(), bcols, brows, bcols, bbox);
+  const CUtensorMap mBl = mode == 3 ? make_map(ws.blo.as<float>(), bcols, brows, bcols, bbox) : mBh;
   p.bcol_step = blk ? 0 : TC_BK;
   p.brow_step = blk ? (int)mp : 0;
   if (otf) {
     launch_tc_otf(op.kp.d, op.kp.family, width, mA, mBh, mBl, p, Gl * npass, st);
   } else {
     if (mode == 3)
-      launch_tc_stored<3>(width, mA, mBh, mBl, p, Gl * npass, st);
+      launch_tc_stored<3>(width, mA, mBh, mBl, p, nblocks, st, cg2);
     else
-      launch_tc_stored<1>(width, mA, mBh, mBl, p, Gl * npass, st);
+      launch_tc_stored<1>(width, mA, mBh, mBl, p, nblocks, st, cg2);
   }
   if (prof_on) {
-    std::vector<unsigned long long> h(16 * (size_t)(Gl * npass));
+    std::vector<unsigned long long> h(16 * (size_t)nblocks);
     RLD_CUDA(cudaMemcpyAsync(h.data(), prof_buf.ptr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, st));
     RLD_CUDA(cudaStreamSynchronize(st));
     double a[16] = {0};
-    for (int64_t c = 0; c < Gl * npass; ++c)
+    for (int64_t c = 0; c < nblocks; ++c)
       for (int k = 0; k < 16; ++k) a[k] += (double)h[c * 16 + k];
     const double steps = a[13] > 0 ? a[13] : 1;
+    if (cg2) {   // per rank: leaders (even blocks) and peers (odd blocks)
+      for (int rk = 0; rk < 2; ++rk) {
+        double b[16] = {0};
+        for (int64_t c = rk; c < nblocks; c += 2)
+          for (int k = 0; k < 16; ++k) b[k] += (double)h[c * 16 + k];
+        fprintf(stderr, "[kv_tc prof rank %d] per k-step: producer wait %.0f / loop %.0f | conv wait %.0f loop %.0f | drain wait %.0f loop %.0f\n",
+                rk, 2 * b[0] / steps, 2 * b[1] / steps, 2 * b[7] / steps, 2 * b[10] / steps, 2 * b[11] / steps,
+                2 * b[12] / steps);
+      }
+    }
     fprintf(stderr,
             "[kv_tc prof] m=%ld n=%ld nt=%d otf=%d per k-step cycles: producer wait %.0f / loop %.0f | mma wait acc %.0f "
             "afull %.0f issue %.0f loop %.0f | conv(w4) wait full %.0f loop %.0f | drain wait %.0f loop %.0f\n",
@@ -1051,7 +1163,7 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
   }
   const int64_t count = m * rows;
   const int blocks = (int)std::min<int64_t>(ceil_div(count, 256), 148 * 16);
-  kv_tc_reduce<<<blocks, 256, 0, st>>>(p.partial, sc, tiles, segs, width, m, rows, Y, ldy);
+  kv_tc_reduce<<<blocks, 256, 0, st>>>(p.partial, sc, tiles, segs, width, m, rows, Y, ldy, cg2 ? 1 : 0);
   RLD_LAUNCH_CHECK();
 }
 
