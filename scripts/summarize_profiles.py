@@ -58,7 +58,8 @@ def main(tag, what):
 
 WHAT = {
     "kv_c2_m32": "config 2 Lanczos shape: n=16384 fp32 stored K, m=s=32 vectors, 3xTF32",
-    "kv_c2_m266": "config 2 sketch shape: n=16384 fp32 stored K, m=w=266 (3 column passes of 96), 3xTF32",
+    "kv_c2_m266": "config 2 sketch shape: n=16384 fp32 stored K, m=w=266 (3 column passes of 96, CTA pairs: cta_group::2 M=256), 3xTF32",
+    "kv_c3_m64": "config 3 Lanczos shape: n=65536 fp32 stored K (17.2 GB), m=s=64, CTA pairs, 3xTF32",
     "otf_c5_n262144": "config 5 on-the-fly Matern-5/2 d=3 tiles, n=262144 (reduced), m=128",
     "otf_c4_n262144": "config 4 on-the-fly RBF d=3 tiles, n=262144 (full), m=64",
 }
