@@ -112,6 +112,7 @@ struct Work {
   DevBuf qbasis, pbasis, coef;   // reorthogonalised Lanczos: bases (t x s x rows) and coefficients
   DevBuf endw, radii;            // normal-orthogonal probes: stream position, chi radii
   DevBuf lz_dotp, lz_dotp2;      // fused Lanczos step: per-chunk dot partials
+  DevBuf rinv;                   // CholQR: explicit R^-1
   DevBuf flagbuf;        // flag OR over ranks
   KvWorkspace kv;
 };
@@ -442,6 +443,45 @@ void cholqr2(rld_handle* h, int64_t n, int w, double* Y, int* flags, int passes 
   }
 }
 
+// One GPU: the same CholQR with the basis change as a DGEMM with an explicit R^-1 (a w x w
+// triangular solve on the identity), written straight into `dst` (the full-rows buffer, so no
+// gather copy): dst = src R^-1 (one pass) or dst = (src R1^-1) R2^-1 (two passes, through `src`).
+// cuBLAS DTRSM on the n x w block was ~143 us at config 2 (n = 16384, w = 266).
+void cholqr_gemm(rld_handle* h, int64_t n, int w, double* src, double* dst, int* flags, int passes) {
+  Work& wk = h->wk;
+  wk.G.reserve(sizeof(double) * w * w);
+  wk.gdiag.reserve(sizeof(double) * w);
+  wk.rinv.reserve(sizeof(double) * w * w);
+  double* G = wk.G.as<double>();
+  double* Ri = wk.rinv.as<double>();
+  int* info = wk.ints.as<int>() + 1;
+  double* cur = src;
+  for (int pass = 0; pass < passes; ++pass) {
+    double* out = (pass == passes - 1) ? dst : (cur == src ? dst : src);
+    if (passes == 2 && pass == 0) out = dst;
+    if (passes == 2 && pass == 1) out = src;
+    gram_blas(h, n, w, cur, n, G);
+    if (pass == 0) diag_copy(w, G, wk.gdiag.as<double>(), h->st);
+    potrf_upper(h, w, G, info);
+    if (pass == 0) cholqr_check(w, G, wk.gdiag.as<double>(), info, 1e-6, flags, h->st);
+    RLD_CUDA(cudaMemsetAsync(Ri, 0, sizeof(double) * w * w, h->st));
+    add_identity(w, Ri, h->st);
+    RLD_CUBLAS(cublasDtrsm(h->cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, w, w,
+                           &ONE, G, w, Ri, w));
+    RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)n, w, w, &ONE, cur, (int)n, Ri, w, &ZERO, out,
+                           (int)n));
+    cur = out;
+  }
+  if (cur != dst) copy_doubles(n * (int64_t)w, cur, dst, h->st);
+}
+
+// Opt-in (RLD_CHOLQR_GEMM=1): cuBLAS's triangular solve on the w x w identity costs ~96 us at
+// w = 266, so the estimate measured the same (19.33 vs 19.35 ms at config 2).
+bool cholqr_gemm_enabled() {
+  static const bool on = getenv("RLD_CHOLQR_GEMM") && getenv("RLD_CHOLQR_GEMM")[0] == '1';
+  return on;
+}
+
 // Householder QR of Y (col-major n x w, single shard), Q with positive R
 // diagonal -- the same Q CGS2 produces -- and the reference's rank test
 // |R_ii| < rtol |Y_i| (src/linalg.py:177-178).
@@ -534,11 +574,15 @@ int lowrank_randsvd(rld_handle* h, const rld_config* c, const rld_inputs* in, Pr
       for (int it = 0; it < c->precond_iters; ++it) {
         const bool last = it + 1 == c->precond_iters;
         kv(h, w, Y, Z, last ? 3 : sketch_tc_mode());      // Y <- Y M      (src/precond.py:186)
-        if (householder)
+        if (householder) {
           qr_householder(h, nl, w, Z, c->orth_rtol, flags);
-        else
+          gather_rows(h, Z, w, Y);
+        } else if (h->world == 1 && cholqr_gemm_enabled()) {
+          cholqr_gemm(h, nl, w, Z, Y, flags, last ? 2 : 1);   // Q <- orth(Y), straight into Y
+        } else {
           cholqr2(h, nl, w, Z, flags, last ? 2 : 1);      // Q <- orth(Y)  (src/precond.py:187)
-        gather_rows(h, Z, w, Y);
+          gather_rows(h, Z, w, Y);
+        }
       }
       hflags = read_flags();
       if (!householder && !(hflags & RLD_FLAG_QR_WEAK)) break;
