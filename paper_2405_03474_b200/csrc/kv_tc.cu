@@ -776,26 +776,33 @@ kv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
   }
 }
 
-// Y[c * ldy + i] = sum over the tile's segments of the partials (float64 accumulation, fixed order)
-__global__ void kv_tc_reduce(const float* __restrict__ P, Sched sc, int tiles, int segs, int nt, int64_t m,
-                             int64_t rows, double* __restrict__ Y, int64_t ldy, int pair) {
-  const int64_t count = m * rows;
+// Y[c * ldy + i] = sum over the tile's segments of the partials (float64 accumulation, fixed order).
+// One block per (row tile, 8 columns): the segment count is computed once per block.
+constexpr int RED_COLS = 8;
+__global__ void __launch_bounds__(256)
+kv_tc_reduce(const float* __restrict__ P, Sched sc, int tiles, int segs, int nt, int64_t m, int64_t rows,
+             double* __restrict__ Y, int64_t ldy, int pair) {
+  const int tile = blockIdx.x;
+  const int r = threadIdx.x & 127;
+  const int64_t i = (int64_t)tile * TC_BM + r;
+  const int unit = pair ? tile >> 1 : tile;   // schedule unit (a pair tile for CTA pairs)
   const int full = sc.R * sc.G;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = e / rows, i = e % rows;
-    const int64_t pass = c / nt, cc = c % nt;
-    const int64_t tile = i / TC_BM, r = i % TC_BM;
-    const int64_t unit = pair ? tile >> 1 : tile;   // schedule unit (a pair tile for CTA pairs)
-    int nseg = 1;
-    if (unit >= full) {
-      const int64_t x0 = (unit - full) * sc.ks;
-      nseg = (int)(cta_of_step(x0 + sc.ks - 1, sc.tail_total, sc.G) - cta_of_step(x0, sc.tail_total, sc.G) + 1);
-    }
-    const float* Pp = P + (size_t)pass * tiles * segs * nt * TC_BM;
+  int nseg = 1;
+  if (unit >= full) {
+    const int64_t x0 = (int64_t)(unit - full) * sc.ks;
+    nseg = (int)(cta_of_step(x0 + sc.ks - 1, sc.tail_total, sc.G) - cta_of_step(x0, sc.tail_total, sc.G) + 1);
+  }
+  if (i >= rows) return;
+  const int c0 = blockIdx.y * RED_COLS;
+#pragma unroll
+  for (int q = threadIdx.x >> 7; q < RED_COLS; q += 2) {
+    const int c = c0 + q;
+    if (c >= m) break;
+    const int pass = c / nt, cc = c - pass * nt;
+    const float* Pp = P + (size_t)pass * tiles * segs * nt * TC_BM + ((size_t)tile * segs * nt + cc) * TC_BM + r;
     double s = 0.0;
-    for (int k = 0; k < nseg; ++k) s += (double)Pp[(((size_t)tile * segs + k) * nt + cc) * TC_BM + r];
-    Y[c * ldy + i] = s;
+    for (int k = 0; k < nseg; ++k) s += (double)Pp[(size_t)k * nt * TC_BM];
+    Y[(int64_t)c * ldy + i] = s;
   }
 }
 
@@ -806,19 +813,18 @@ __global__ void kv_tc_reduce(const float* __restrict__ P, Sched sc, int tiles, i
 // NT rows n*4 bytes apart (256 distinct 2 MB pages per box at n = 2^20).
 __global__ void kv_tc_split(const double* __restrict__ V, int64_t ldv, int64_t m, int64_t n, int64_t mp, int64_t ks,
                             int mode, int blocked, float* __restrict__ Bhi, float* __restrict__ Blo) {
-  const int64_t count = mp * ks * 32;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = e / (ks * 32), j = e % (ks * 32);
-    const double v = (c < m && j < n) ? V[c * ldv + j] : 0.0;
-    const int64_t o = blocked ? ((j >> 5) * mp + c) * 32 + (j & 31) : c * (ks * 32) + j;
-    float h = (float)v;
-    if (mode == 3) {
-      h = __uint_as_float(__float_as_uint(h) & 0xFFFFE000u);
-      Blo[o] = (float)(v - (double)h);
-    }
-    Bhi[o] = h;
+  // grid (ceil(ks * 32 / 256), mp): one vector per block row, contiguous columns per warp
+  const int64_t c = blockIdx.y;
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= ks * 32) return;
+  const double v = (c < m && j < n) ? V[c * ldv + j] : 0.0;
+  const int64_t o = blocked ? ((j >> 5) * mp + c) * 32 + (j & 31) : c * (ks * 32) + j;
+  float h = (float)v;
+  if (mode == 3) {
+    h = __uint_as_float(__float_as_uint(h) & 0xFFFFE000u);
+    Blo[o] = (float)(v - (double)h);
   }
+  Bhi[o] = h;
 }
 
 // ---------------------------------------------------------------- host side
@@ -1033,9 +1039,8 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
   ws.bhi.reserve(sizeof(float) * mp * ks * 32);
   if (mode == 3) ws.blo.reserve(sizeof(float) * mp * ks * 32);
   if (!presplit) {
-    const int64_t count = mp * ks * 32;
-    const int blocks = (int)std::min<int64_t>(ceil_div(count, 256), 148 * 16);
-    kv_tc_split<<<blocks, 256, 0, st>>>(V, ldv, m, n, mp, ks, mode, blocked_b(), ws.bhi.as<float>(),
+    const dim3 sgrid((unsigned)ceil_div((int64_t)ks * 32, 256), (unsigned)mp);
+    kv_tc_split<<<sgrid, 256, 0, st>>>(V, ldv, m, n, mp, ks, mode, blocked_b(), ws.bhi.as<float>(),
                                         mode == 3 ? ws.blo.as<float>() : nullptr);
     RLD_LAUNCH_CHECK();
   }
@@ -1161,9 +1166,8 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
             (long)m, (long)n, width, (int)otf, a[0] / steps, a[1] / steps, a[2] / steps, a[4] / steps,
             a[5] / steps, a[6] / steps, a[7] / steps, a[10] / steps, a[11] / steps, a[12] / steps);
   }
-  const int64_t count = m * rows;
-  const int blocks = (int)std::min<int64_t>(ceil_div(count, 256), 148 * 16);
-  kv_tc_reduce<<<blocks, 256, 0, st>>>(p.partial, sc, tiles, segs, width, m, rows, Y, ldy, cg2 ? 1 : 0);
+  const dim3 rgrid((unsigned)tiles, (unsigned)ceil_div(m, RED_COLS));
+  kv_tc_reduce<<<rgrid, 256, 0, st>>>(p.partial, sc, tiles, segs, width, m, rows, Y, ldy, cg2 ? 1 : 0);
   RLD_LAUNCH_CHECK();
 }
 
