@@ -359,7 +359,7 @@ struct TcShape {
   // a converter posts step j's afull only after starting step j + CP, whose TMEM buffer must not
   // be the one step j's MMAs still hold: more buffers than converter warps per quarter
   static_assert(NABUF > CP, "TMEM A buffers");
-  static_assert(NT % 16 == 0 && (NT / DP) % 8 == 0 && NT <= 144 && (NT <= 128 || !OTF), "NT");
+  static_assert(NT % 16 == 0 && (NT / DP) % 8 == 0 && NT <= 144, "NT");
   static_assert(!CG2 || (!OTF && (STACK || (NT / 2) % 16 == 0)), "pair variant: stored K, half of N a multiple of 16");
 };
 
@@ -940,6 +940,7 @@ void launch_tc_otf_nt(int nt, const CUtensorMap& mA, const CUtensorMap& mBh, con
   switch (nt) {
     case 32: launch_tc<3, 32, true, DIM, FAM>(mA, mBh, mBl, p, grid, st); break;
     case 64: launch_tc<3, 64, true, DIM, FAM>(mA, mBh, mBl, p, grid, st); break;
+    case 144: launch_tc<3, 144, true, DIM, FAM>(mA, mBh, mBl, p, grid, st); break;
     default: launch_tc<3, 128, true, DIM, FAM>(mA, mBh, mBl, p, grid, st); break;
   }
 }
@@ -999,6 +1000,15 @@ namespace {
 void tc_passes(const KvOperand& op, int64_t m, int& npass, int& width) {
   static const int wide_env = getenv("RLD_TC_NT144") ? atoi(getenv("RLD_TC_NT144")) : -1;
   const bool otf = op.K == nullptr;
+  // on the fly every pass regenerates its K tiles; passes of 144 would save one at configs 4/5
+  // (8 instead of 9, 15 instead of 17) but measured slower per pass (3 TMEM A buffers): 988 vs
+  // 754 ms (config 4 sketch), 2091 vs 1639 ms (config 5, n = 262144).  Opt-in RLD_TC_OTF144=1.
+  static const bool otf_wide = getenv("RLD_TC_OTF144") && getenv("RLD_TC_OTF144")[0] == '1';
+  if (m > 128 && otf && otf_wide && ceil_div(m, 144) < ceil_div(m, 128)) {
+    npass = (int)ceil_div(m, 144);
+    width = 144;
+    return;
+  }
   const bool wide = wide_env == 1 || (wide_env < 0 && m > 128 && m <= 144);
   if (m > 128 && !otf && wide) {
     npass = (int)ceil_div(m, 144);
