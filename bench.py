@@ -66,6 +66,7 @@ def parse():
     ap.add_argument("--algorithm", choices=["r1", "r3", "r5"], default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-concurrent", action="store_true", help="skip the informational concurrent-estimates run")
     ap.add_argument("--mode", choices=["sharded", "replicas"], default="sharded",
                     help="multi-GPU: row-shard one estimate (default) or run independent replicas")
     return ap.parse_args()
@@ -358,6 +359,29 @@ def run_ours(args):
         # restore the resident problem for any later use
         del keep
 
+    # ---- informational: independent estimates from several host threads, each with its own
+    # handle / stream / K copy (the harness's run_sweep(jobs=J)); not the headline value
+    concurrent = None
+    if world == 1 and not args.no_concurrent:
+        import threading
+
+        J, per = 4, max(2, args.steps // 2)
+        Rs = [rld.ResidentMatrix(rld.KernelMatrix(wl.spec, wl.points), dtype=cfg.dtype, path=wl.path)
+              for _ in range(J)]
+        for Rj in Rs:
+            Rj.estimate(cfg)
+        torch.cuda.synchronize()
+        ths = [threading.Thread(target=lambda Rj=Rj: [Rj.estimate(cfg) for _ in range(per)]) for Rj in Rs]
+        t0 = time.perf_counter()
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+        dtc = time.perf_counter() - t0
+        concurrent = {"jobs": J, "value": J * per / dtc, "unit": UNIT, "clock": "host wall",
+                      "what": "J independent estimates at a time, one device handle per host thread"}
+        del Rs
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -381,6 +405,8 @@ def run_ours(args):
         "clocks": clocks,
         "estimate": est.value,
     }
+    if concurrent is not None:
+        line["concurrent"] = concurrent
 
     # ---- CPU baseline (rank 0, N = 1 only)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

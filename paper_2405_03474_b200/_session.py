@@ -139,10 +139,36 @@ class Session:
 
 _session = None
 _session_lock = threading.Lock()
+_local = threading.local()
+
+
+class worker_session:
+    """Context manager: this thread's calls use their own handle (own stream, workspace and
+    resident problem) instead of the process-wide one, so independent estimates can run
+    concurrently from several host threads (``harness.run_sweep(jobs=J)``).  One GPU only."""
+
+    def __init__(self, device: int | None = None):
+        self.device = device
+        self.sess = None
+
+    def __enter__(self):
+        self.sess = Session(self.device)
+        self.prev = getattr(_local, "sess", None)
+        _local.sess = self.sess
+        return self.sess
+
+    def __exit__(self, *exc):
+        _local.sess = self.prev
+        self.sess.handle.close()
+        return False
 
 
 def session() -> Session:
-    """The process-wide session (created on first use)."""
+    """The calling thread's worker session if one is active, else the process-wide session
+    (created on first use)."""
+    mine = getattr(_local, "sess", None)
+    if mine is not None:
+        return mine
     global _session
     with _session_lock:
         if _session is None:

@@ -131,3 +131,19 @@ def test_sweep_is_deterministic_and_paired():
     # algorithms of one (value, trial) share the seed and the exact log det
     for r1, r2 in zip(a[0::2], a[1::2]):
         assert r1.seed == r2.seed and r1.exact == r2.exact
+
+
+@pytest.mark.gpu
+def test_sweep_jobs_run_concurrently_with_identical_records():
+    """jobs > 1: worker threads with their own device handles (the reference's --jobs runs
+    processes, src/bench.py:209-215); every record equals the serial one, in the same order."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    spec = H.SweepSpec("probes", (4, 8, 12), ("r1", "r3"), base=H.RunConfig(n=400, jitter=1e-3), trials=2)
+    serial = H.run_sweep(spec)
+    par = H.run_sweep(spec, jobs=3)
+    key = lambda r: (r.n, r.s, r.seed, r.algorithm, r.estimate, r.exact, r.error)   # noqa: E731
+    assert [key(r) for r in par] == [key(r) for r in serial]
+    assert all(r.error is None for r in par)
