@@ -413,17 +413,19 @@ void gram_blas(rld_handle* h, int64_t rows, int w, const double* Y, int64_t ldy,
 // iteration needs the second pass for orthogonality.
 // Upper Cholesky of the w x w fp64 matrix G (ld w): the one-cluster kernel for w <= 640
 // (small_chol.cu), cuSOLVER potrf above that.  RLD_SMALL_CHOL=0 forces cuSOLVER.
-void potrf_upper(rld_handle* h, int w, double* G, int* info) {
+// Returns true when R^-1 was written to `rinv` as well (only the one-cluster kernel does).
+bool potrf_upper(rld_handle* h, int w, double* G, int* info, double* rinv = nullptr) {
   static const bool small = [] {
     const char* e = getenv("RLD_SMALL_CHOL");
     return !(e && e[0] == '0');
   }();
-  if (small && small_potrf_upper(w, G, w, info, h->st)) return;
+  if (small && small_potrf_upper(w, G, w, info, h->st, rinv)) return rinv != nullptr;
   Work& wk = h->wk;
   int lwork = 0;
   RLD_CUSOLVER(cusolverDnDpotrf_bufferSize(h->solver, CUBLAS_FILL_MODE_UPPER, w, G, w, &lwork));
   wk.solver_work.reserve(sizeof(double) * std::max(lwork, 1));
   RLD_CUSOLVER(cusolverDnDpotrf(h->solver, CUBLAS_FILL_MODE_UPPER, w, G, w, wk.solver_work.as<double>(), lwork, info));
+  return false;
 }
 
 void cholqr2(rld_handle* h, int64_t n, int w, double* Y, int* flags, int passes = 2) {
@@ -462,12 +464,14 @@ void cholqr_gemm(rld_handle* h, int64_t n, int w, double* src, double* dst, int*
     if (passes == 2 && pass == 1) out = src;
     gram_blas(h, n, w, cur, n, G);
     if (pass == 0) diag_copy(w, G, wk.gdiag.as<double>(), h->st);
-    potrf_upper(h, w, G, info);
+    const bool have_rinv = potrf_upper(h, w, G, info, Ri);   // the cluster kernel also writes R^-1
     if (pass == 0) cholqr_check(w, G, wk.gdiag.as<double>(), info, 1e-6, flags, h->st);
-    RLD_CUDA(cudaMemsetAsync(Ri, 0, sizeof(double) * w * w, h->st));
-    add_identity(w, Ri, h->st);
-    RLD_CUBLAS(cublasDtrsm(h->cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, w, w,
-                           &ONE, G, w, Ri, w));
+    if (!have_rinv) {
+      RLD_CUDA(cudaMemsetAsync(Ri, 0, sizeof(double) * w * w, h->st));
+      add_identity(w, Ri, h->st);
+      RLD_CUBLAS(cublasDtrsm(h->cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, w,
+                             w, &ONE, G, w, Ri, w));
+    }
     RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)n, w, w, &ONE, cur, (int)n, Ri, w, &ZERO, out,
                            (int)n));
     cur = out;
@@ -475,10 +479,11 @@ void cholqr_gemm(rld_handle* h, int64_t n, int w, double* src, double* dst, int*
   if (cur != dst) copy_doubles(n * (int64_t)w, cur, dst, h->st);
 }
 
-// Opt-in (RLD_CHOLQR_GEMM=1): cuBLAS's triangular solve on the w x w identity costs ~96 us at
-// w = 266, so the estimate measured the same (19.33 vs 19.35 ms at config 2).
+// Default on (RLD_CHOLQR_GEMM=0 restores the DTRSM path): with R^-1 from the cluster Cholesky
+// kernel the config-2 estimate takes 18.8 vs 19.2 ms (with cuBLAS's triangular solve on the w x w
+// identity instead it measured even, 19.33 vs 19.35 ms).
 bool cholqr_gemm_enabled() {
-  static const bool on = getenv("RLD_CHOLQR_GEMM") && getenv("RLD_CHOLQR_GEMM")[0] == '1';
+  static const bool on = !(getenv("RLD_CHOLQR_GEMM") && getenv("RLD_CHOLQR_GEMM")[0] == '0');
   return on;
 }
 

@@ -77,7 +77,8 @@ void add_identity(int k, double* C, cudaStream_t st);
 void chol_logdet(int k, const double* L, const int* info, double* out, int* flags, cudaStream_t st);
 // One-cluster Cholesky G = R^T R (upper, in place, info as LAPACK potrf) for n <= 640; false if n is
 // out of range (caller falls back to cuSOLVER).  small_chol.cu
-bool small_potrf_upper(int n, double* G, int ld, int* info, cudaStream_t st);
+// With Rinv != nullptr also writes R^-1 (upper, n x n, ld n, lower part zero).
+bool small_potrf_upper(int n, double* G, int ld, int* info, cudaStream_t st, double* Rinv = nullptr);
 void sqrt_factors(int k, double keep_rtol, const double* lam, double* W, double* h, double* g, double* gam,
                   int* kept, cudaStream_t st);
 void convert_rows(const void* src, int sdt, void* dst, int ddt, int64_t count, cudaStream_t st);

@@ -105,7 +105,8 @@ __device__ __forceinline__ void factor_block(double* Ds, double* Ri, double* Rv,
 }
 
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(THREADS)
-chol_upper_kernel(int n, double* __restrict__ G, int ld, int* __restrict__ info, long long* __restrict__ prof) {
+chol_upper_kernel(int n, double* __restrict__ G, int ld, int* __restrict__ info, double* __restrict__ X,
+                  long long* __restrict__ prof) {
   extern __shared__ double sm[];
   constexpr int LDB = NB + 1;
   double* Ds = sm;                  // NB x LDB: diagonal block / its factor R_pp (upper part)
@@ -149,11 +150,14 @@ chol_upper_kernel(int n, double* __restrict__ G, int ld, int* __restrict__ info,
     }
     // R_pp goes over the diagonal block only after the cluster barrier: until then the other CTAs
     // may still be reading that block
-    auto write_rpp = [&]() {
+    auto write_rpp = [&]() {   // also R_pp^-1 into X's diagonal block when R^-1 is wanted
       if (cta == 0)
         for (int e = tid; e < kb * kb; e += THREADS) {
           const int i = e % kb, c = e / kb;
-          if (i <= c) G[(size_t)(k0 + c) * ld + k0 + i] = Ds[i * LDB + c];
+          if (i <= c) {
+            G[(size_t)(k0 + c) * ld + k0 + i] = Ds[i * LDB + c];
+            if (X) X[(size_t)(k0 + c) * n + k0 + i] = Rv[i * LDB + c];
+          }
         }
     };
     if (k1 >= n) {
@@ -241,13 +245,71 @@ chol_upper_kernel(int n, double* __restrict__ G, int ld, int* __restrict__ info,
     mark(4);
   }
   if (cta == 0 && tid == 0) *info = 0;
+  if (!X) return;
+  // ---- R^-1 (upper, n x n, ld n; lower part left as the caller's zeros), block column J by this
+  // CTA (J % CL == cta): X_JJ = R_JJ^-1 is in place; X_IJ = -R_II^-1 sum_{K=I+1..J} R_IK X_KJ for
+  // I = J-1 .. 0 (block back substitution), the column's blocks kept in shared memory
+  cluster_sync_all();   // every panel row of R and every diagonal inverse is in global memory
+  double* Xc = Pt;      // npanels x NB x NB: this column's blocks, Xc[K][m][c]
+  double* S = Dn;       // NB x LDB
+  const int ri = tid & 31, cg = tid >> 5;   // output row, 4-column group
+  for (int J = cta; J < npanels; J += CL) {
+    const int cJ = J * NB, wJ = min(NB, n - cJ);
+    for (int e = tid; e < NB * NB; e += THREADS) {
+      const int m = e % NB, c = e / NB;
+      Xc[(size_t)J * NB * NB + m * NB + c] = (m < wJ && c < wJ && m <= c) ? __ldcg(X + (size_t)(cJ + c) * n + cJ + m) : 0.0;
+    }
+    __syncthreads();
+    for (int I = J - 1; I >= 0; --I) {
+      const int rI = I * NB;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int K = I + 1; K <= J; ++K) {
+        const int cK = K * NB, wK = min(NB, n - cK);
+        const double* Xk = Xc + (size_t)K * NB * NB;
+        for (int m0 = 0; m0 < wK; m0 += 8) {   // 8 independent L2 loads in flight per thread
+          double r[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            r[u] = (m0 + u < wK) ? __ldcg(G + (size_t)(cK + m0 + u) * ld + rI + ri) : 0.0;   // R[rI + ri, cK + m]
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] = fma(r[u], Xk[(m0 + u) * NB + cg * 4 + q], acc[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) S[ri * LDB + cg * 4 + q] = acc[q];
+      __syncthreads();
+      double x[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int m0 = 0; m0 < NB; m0 += 8) {   // R_II^-1 is upper: row ri, columns m >= ri (zeros below)
+        double rv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) rv[u] = (m0 + u >= ri) ? __ldcg(X + (size_t)(rI + m0 + u) * n + rI + ri) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) x[q] = fma(rv[u], S[(m0 + u) * LDB + cg * 4 + q], x[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = cg * 4 + q;
+        Xc[(size_t)I * NB * NB + ri * NB + c] = -x[q];
+        if (c < wJ) X[(size_t)(cJ + c) * n + rI + ri] = -x[q];
+      }
+      __syncthreads();
+    }
+  }
 }
 
 }  // namespace
 
-bool small_potrf_upper(int n, double* G, int ld, int* info, cudaStream_t st) {
+bool small_potrf_upper(int n, double* G, int ld, int* info, cudaStream_t st, double* Rinv) {
   if (n < 1 || n > SMALL_CHOL_MAX) return false;
-  auto smem_for = [](int nn) { return sizeof(double) * ((size_t)3 * NB * (NB + 1) + 3 * NB + (size_t)(CMAX + nn) * (NB + 1)); };
+  // the panel-row buffer doubles as the R^-1 column blocks (ceil(n / 32) 32 x 32 blocks)
+  auto smem_for = [](int nn) {
+    const size_t tail = std::max((size_t)nn * (NB + 1), (size_t)NB * NB * ((nn + NB - 1) / NB));
+    return sizeof(double) * ((size_t)3 * NB * (NB + 1) + 3 * NB + (size_t)CMAX * (NB + 1)) + sizeof(double) * tail;
+  };
   static bool attr_set = false;
   if (!attr_set) {
     RLD_CUDA(cudaFuncSetAttribute(chol_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -258,7 +320,8 @@ bool small_potrf_upper(int n, double* G, int ld, int* info, cudaStream_t st) {
   static const bool profile = getenv("RLD_CHOL_PROFILE") != nullptr;
   long long* prof = nullptr;
   if (profile) RLD_CUDA(cudaMallocAsync(&prof, 8 * sizeof(long long), st)), RLD_CUDA(cudaMemsetAsync(prof, 0, 64, st));
-  chol_upper_kernel<<<CL, THREADS, smem, st>>>(n, G, ld, info, prof);
+  if (Rinv) RLD_CUDA(cudaMemsetAsync(Rinv, 0, sizeof(double) * (size_t)n * n, st));
+  chol_upper_kernel<<<CL, THREADS, smem, st>>>(n, G, ld, info, Rinv, prof);
   RLD_LAUNCH_CHECK();
   if (profile) {
     long long hp[8];
