@@ -573,3 +573,38 @@ def test_dense_cholesky_reports_first_bad_pivot(rld, n, bad):
     G[bad, bad] = -1.0
     _, info = _dense_cholesky(G)
     assert info == bad + 1
+
+
+def test_fresh_workspace_poisoned_with_nan_changes_nothing(rld):
+    """Every device workspace is written before it is read: with RLD_POISON=1 each new buffer is
+    filled with NaN bytes (a fresh process, since the flag is read once) and the estimates of
+    configs 1-3 (stored, on the fly, CTA pairs, several preconditioners, normal-orthogonal probes)
+    must equal the ones computed here without it."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    code = r"""
+import json, sys
+sys.path.insert(0, %r)
+import paper_2405_03474_b200 as rld
+from paper_2405_03474_b200.workloads import baseline
+from dataclasses import replace
+out = []
+for idx, n, path, kind, probe in [(1, 1024, "stored", "rand-svd", "rademacher"), (2, 4096, "stored", "rand-svd", "rademacher"),
+                                  (3, 4096, "on_the_fly", "rand-svd", "gaussian"), (2, 2048, "stored", "partial-cholesky", "normal-orthogonal")]:
+    wl = baseline(idx, n=n)
+    cfg = replace(wl.config, probe_kind=probe, precond=replace(wl.config.precond, kind=kind), path=path)
+    out.append(rld.estimate_logdet(rld.KernelMatrix(wl.spec, wl.points), cfg).value)
+print(json.dumps(out))
+""" % str(Path(__file__).resolve().parent.parent)
+    runs = []
+    for poison in ("1", "0"):
+        env = dict(os.environ, RLD_POISON=poison)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        runs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert runs[0] == runs[1], runs
+    assert all(np.isfinite(v) for v in runs[0])
