@@ -216,6 +216,19 @@ def cpu_model():
     return "unknown"
 
 
+def workload_config(wl, world=1, sharded=False):
+    """The `config` object both arms print (the driver compares the reference arm on our arm's config)."""
+    cfg = wl.config
+    n, s = wl.n, cfg.num_probes
+    es = 4 if cfg.dtype == "fp32" else 8
+    return {"workload": f"{wl.name}: n={n} {wl.spec.family} d={wl.points.shape[1]} ell={wl.spec.length_scale} "
+                        f"noise={wl.spec.jitter} {cfg.algorithm} l={cfg.precond.rank} s={s} "
+                        f"{cfg.probe_kind} t={cfg.lanczos_iters} q={cfg.precond.num_iters} stored K "
+                        f"({cfg.dtype})",
+            "l2": "inputs larger than L2 (K = %.2f GB)" % (es * n * n / 1e9),
+            "parallelism": (f"rows{world}" if sharded else f"replicas{world}") if world > 1 else "single"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -223,6 +236,7 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     os.environ["OPENBLAS_NUM_THREADS"] = str(threads)
     wl = workload_for(args)
+    arm_config = workload_config(wl)
     cfg = replace(wl.config, dtype="fp64")
     wl = replace(wl, config=cfg)
     warm = min(args.warmup, 1)
@@ -236,9 +250,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
         "warmup": warm, "ms_per_step": 1e3 * total / steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{wl.name} n={wl.n} {wl.spec.family} r={cfg.algorithm} l={cfg.precond.rank} "
-                               f"s={cfg.num_probes} t={cfg.lanczos_iters} stored-K",
-                   "note": "reference has no fp32 mode; CPU arm computes in float64"},
+        "config": {**arm_config, "note": "the reference has no fp32 mode: this CPU arm computes in float64"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{steps} full estimate(s) of the workload, oracle port (numpy/OpenBLAS, "
                                    f"per-probe loop), K build excluded", "cpu": cpu_model()},
@@ -387,12 +399,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f32" if cfg.dtype == "fp32" else "f64",
         "data": "synthetic",
-        "config": {"workload": f"{wl.name}: n={n} {wl.spec.family} d={wl.points.shape[1]} ell={wl.spec.length_scale} "
-                               f"noise={wl.spec.jitter} {cfg.algorithm} l={cfg.precond.rank} s={s} "
-                               f"{cfg.probe_kind} t={cfg.lanczos_iters} q={cfg.precond.num_iters} stored K "
-                               f"({cfg.dtype})",
-                   "l2": "inputs larger than L2 (K = %.2f GB)" % (es * n * n / 1e9),
-                   "parallelism": (f"rows{world}" if sharded else f"replicas{world}") if world > 1 else "single"},
+        "config": workload_config(wl, world, sharded),
         "e2e": e2e,
         "gpu_launches": launches,
         "kv_products_per_step": products // max(1, args.steps),
