@@ -46,16 +46,32 @@ struct Attempt {
   double value;
 };
 
-__device__ Attempt attempt_at(const uint64_t* words, int qi, int limit, bool want_value) {
+// Ziggurat tables in shared memory: the layer index is random per lane, and __constant__ reads
+// with 32 different addresses serialise (the emit kernel spent 40 % of its stalls there).
+struct ZigTables {
+  uint64_t ki[256];
+  double wi[256];
+  double fi[256];
+};
+
+__device__ __forceinline__ void load_zig_tables(ZigTables& z) {
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    z.ki[i] = rld_zig_ki[i];
+    z.wi[i] = rld_zig_wi[i];
+    z.fi[i] = rld_zig_fi[i];
+  }
+}
+
+__device__ Attempt attempt_at(const uint64_t* words, int qi, int limit, bool want_value, const ZigTables& z) {
   Attempt a{1, true, 0.0};
   uint64_t r = words[qi];
   const int idx = (int)(r & 0xff);
   r >>= 8;
   const int sign = (int)(r & 1);
   const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
-  double x = (double)rabs * rld_zig_wi[idx];
+  double x = (double)rabs * z.wi[idx];
   if (sign) x = -x;
-  if (rabs < rld_zig_ki[idx]) {
+  if (rabs < z.ki[idx]) {
     a.value = x;
     return a;
   }
@@ -81,7 +97,7 @@ __device__ Attempt attempt_at(const uint64_t* words, int qi, int limit, bool wan
     return a;
   }
   a.len = 2;
-  a.acc = ((rld_zig_fi[idx - 1] - rld_zig_fi[idx]) * u01(words[qi + 1]) + rld_zig_fi[idx]) < exp(-0.5 * x * x);
+  a.acc = ((z.fi[idx - 1] - z.fi[idx]) * u01(words[qi + 1]) + z.fi[idx]) < exp(-0.5 * x * x);
   a.value = x;
   (void)want_value;
   return a;
@@ -90,7 +106,8 @@ __device__ Attempt attempt_at(const uint64_t* words, int qi, int limit, bool wan
 // Fill sm_words[0 .. ZC + ZM) with stream words chunk*ZC + i, and build the ordered
 // list of slow words (attempt length != 1 or rejecting) with their lengths / accept bits.
 __device__ void load_chunk(int64_t chunk, uint64_t k0, uint64_t k1, uint64_t* sm_words, int* sm_slow_pos,
-                           short* sm_slow_len, unsigned char* sm_slow_acc, int* sm_nslow, int* sm_cnt, int* flags) {
+                           short* sm_slow_len, unsigned char* sm_slow_acc, int* sm_nslow, int* sm_cnt, int* flags,
+                           const ZigTables& z) {
   const int t = threadIdx.x;
   const uint64_t q0 = (uint64_t)chunk * ZC;
   // 16 words per thread = 4 Philox blocks; margin words by the first ZM/4 threads
@@ -132,8 +149,8 @@ __device__ void load_chunk(int64_t chunk, uint64_t k0, uint64_t k1, uint64_t* sm
     const uint64_t r = sm_words[qi];
     const int idx = (int)(r & 0xff);
     const uint64_t rabs = (r >> 9) & 0x000fffffffffffffULL;
-    if (rabs >= rld_zig_ki[idx]) {
-      const Attempt a = attempt_at(sm_words, qi, ZC + ZM, false);
+    if (rabs >= z.ki[idx]) {
+      const Attempt a = attempt_at(sm_words, qi, ZC + ZM, false, z);
       if (a.len < 0) atomicOr(flags, 1);
       pos[ns] = qi;
       len[ns] = (short)(a.len < 0 ? 1 : a.len);
@@ -168,6 +185,7 @@ __device__ void load_chunk(int64_t chunk, uint64_t k0, uint64_t k1, uint64_t* sm
 }
 
 struct ChunkSmem {
+  ZigTables zig;
   uint64_t words[ZC + ZM];
   int slow_pos[MAXSLOW];
   short slow_len[MAXSLOW];
@@ -183,7 +201,8 @@ __global__ void __launch_bounds__(ZT) zig_chunk_kernel(uint64_t k0, uint64_t k1,
   extern __shared__ __align__(16) unsigned char zsm_raw[];
   ChunkSmem& sm = *reinterpret_cast<ChunkSmem*>(zsm_raw);
   const int64_t chunk = blockIdx.x;
-  load_chunk(chunk, k0, k1, sm.words, sm.slow_pos, sm.slow_len, sm.slow_acc, &sm.nslow, sm.cnt, flags);
+  load_zig_tables(sm.zig);
+  load_chunk(chunk, k0, k1, sm.words, sm.slow_pos, sm.slow_len, sm.slow_acc, &sm.nslow, sm.cnt, flags, sm.zig);
   const int ns = min(sm.nslow, MAXSLOW);
   if (threadIdx.x < EMAX) {
     const int e = threadIdx.x;
@@ -274,7 +293,8 @@ __global__ void __launch_bounds__(ZT) zig_emit_kernel(uint64_t k0, uint64_t k1, 
   const int64_t chunk = blockIdx.x;
   const int64_t b0 = base[chunk];
   if (b0 >= count) return;
-  load_chunk(chunk, k0, k1, sm.words, sm.slow_pos, sm.slow_len, sm.slow_acc, &sm.nslow, sm.cnt, flags);
+  load_zig_tables(sm.zig);
+  load_chunk(chunk, k0, k1, sm.words, sm.slow_pos, sm.slow_len, sm.slow_acc, &sm.nslow, sm.cnt, flags, sm.zig);
   const int t = threadIdx.x;
   const int e = entry[chunk];
   // start mask: every word >= e, minus words covered by slow attempts
@@ -316,7 +336,7 @@ __global__ void __launch_bounds__(ZT) zig_emit_kernel(uint64_t k0, uint64_t k1, 
   for (int i = 0; i < 16; ++i) {
     if (!((mine >> i) & 1)) continue;
     if (k >= count) break;
-    const Attempt a = attempt_at(sm.words, t * 16 + i, ZC + ZM, true);
+    const Attempt a = attempt_at(sm.words, t * 16 + i, ZC + ZM, true, sm.zig);
     const int64_t r = k / ncols, jj = k % ncols;
     if (jj >= col0 && jj < col0 + nout_cols) out[r * ldo + (jj - col0)] = a.value;
     if (end_word && k == count - 1) *end_word = chunk * ZC + t * 16 + i + a.len;   // stream word after the last draw
