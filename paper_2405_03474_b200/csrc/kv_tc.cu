@@ -1126,7 +1126,7 @@ void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, in
       while (v > 1 && (1 << (pw + 1)) <= v) ++pw;
       return v > 0 ? (1 << pw) : 0;
     }();
-    p.sync_k = (sc.R > 1 || (sc.R == 1 && sc.tail_total > 0)) ? sync_k : 0;
+    p.sync_k = (sc.R > 1 || (sc.R == 1 && sc.tail_total > 0)) && g_live_handles.load() <= 1 ? sync_k : 0;
     static const int sync_all = getenv("RLD_TC_SYNC_ALL") ? atoi(getenv("RLD_TC_SYNC_ALL")) : 0;
     static const int sync_k_multi = getenv("RLD_TC_SYNC_K_MULTI") ? atoi(getenv("RLD_TC_SYNC_K_MULTI")) : 0;
     p.sync_all = (npass > 1 && sync_all) ? 1 : 0;

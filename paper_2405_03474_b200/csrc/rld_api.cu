@@ -20,7 +20,8 @@
 
 namespace rld {
 
-thread_local int g_launches = 0;  // own kernel launches (RLD_LAUNCH_CHECK)
+thread_local int g_launches = 0;
+std::atomic<int> g_live_handles{0};  // own kernel launches (RLD_LAUNCH_CHECK)
 
 [[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
 
@@ -122,6 +123,7 @@ struct Work {
 
 struct rld_handle {
   int device = 0, rank = 0, world = 1;
+  bool counted = false;   // included in rld::g_live_handles
   cudaStream_t st = nullptr;
   cublasHandle_t cublas = nullptr;
   cusolverDnHandle_t solver = nullptr;
@@ -1213,12 +1215,15 @@ int rld_create(const rld_device_set* ds, rld_handle** out) {
     rld_destroy(h);
     return rc;
   }
+  h->counted = true;
+  rld::g_live_handles.fetch_add(1);
   *out = h;
   return RLD_OK;
 }
 
 void rld_destroy(rld_handle* h) {
   if (!h) return;
+  if (h->counted) rld::g_live_handles.fetch_sub(1);
   cudaSetDevice(h->device);
   if (h->st) cudaStreamSynchronize(h->st);
   h->res.Kbuf.release();

@@ -6,6 +6,7 @@
 #include <cusolverDn.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -32,6 +33,11 @@ extern thread_local int g_launches;
     ++::rld::g_launches;                                                      \
     ::rld::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__); \
   } while (0)
+
+// Live handles in the process.  With more than one, K x V launches from different streams may
+// run concurrently and interleave on the SMs, so the tensor-core kernel drops its inter-CTA epoch
+// barrier (a spin on CTAs that another kernel's blocks could keep off the SMs).
+extern std::atomic<int> g_live_handles;
 
 // Grow-only device buffer.
 struct DevBuf {
