@@ -132,6 +132,8 @@ struct rld_handle {
   rld::Resident res;
   rld::Work wk;
   cudaEvent_t ev[8] = {};
+  cudaStream_t st2 = nullptr;        // side stream for independent small work (joined before use)
+  cudaEvent_t fork = nullptr, join = nullptr;
 };
 
 namespace rld {
@@ -824,10 +826,21 @@ PrecondOut build_preconditioner(rld_handle* h, const rld_config* c, const rld_in
   double* inner = wk.inner.as<double>();
   copy_doubles((int64_t)k * k, C, inner, st);
   add_identity(k, inner, st);
+  // log det of the inner factor on the side stream, overlapping the eigensolve of C below (both
+  // only read C / inner); joined at the end of this function
+  const bool side = k <= 640 && h->world == 1;
   {
     int* info = wk.ints.as<int>() + 4;
-    potrf_upper(h, k, inner, info);   // only the diagonal of the factor is used
-    chol_logdet(k, inner, info, scal + 1, flags, st);
+    if (side) {
+      RLD_CUDA(cudaEventRecord(h->fork, st));
+      RLD_CUDA(cudaStreamWaitEvent(h->st2, h->fork, 0));
+      small_potrf_upper(k, inner, k, info, h->st2);   // only the diagonal of the factor is used
+      chol_logdet(k, inner, info, scal + 1, flags, h->st2);
+      RLD_CUDA(cudaEventRecord(h->join, h->st2));
+    } else {
+      potrf_upper(h, k, inner, info);
+      chol_logdet(k, inner, info, scal + 1, flags, st);
+    }
   }
   // factored square root (src/precond.py:90-100): eigh(At^T At), keep filter, U = At W / sqrt(lam)
   wk.lam.reserve(sizeof(double) * k);
@@ -838,6 +851,7 @@ PrecondOut build_preconditioner(rld_handle* h, const rld_config* c, const rld_in
   // U (n_local x k) into Z (no longer needed)
   RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nl, k, k, &ONE, A, (int)nl, C, k, &ZERO, Z,
                          (int)nl));
+  if (side) RLD_CUDA(cudaStreamWaitEvent(st, h->join, 0));
   out.k = k;
   return out;
 }
@@ -1203,6 +1217,9 @@ int rld_create(const rld_device_set* ds, rld_handle** out) {
     RLD_CUSOLVER(cusolverDnCreate(&h->solver));
     RLD_CUSOLVER(cusolverDnSetStream(h->solver, h->st));
     for (auto& e : h->ev) RLD_CUDA(cudaEventCreate(&e));
+    RLD_CUDA(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
+    RLD_CUDA(cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming));
+    RLD_CUDA(cudaEventCreateWithFlags(&h->join, cudaEventDisableTiming));
     if (h->world > 1) {
       if (!ds || !ds->nccl_id) fail(RLD_ERR_INVALID_ARGUMENT, "nccl_id required for world_size > 1");
       ncclUniqueId id;
@@ -1230,6 +1247,9 @@ void rld_destroy(rld_handle* h) {
   if (h->comm) ncclCommDestroy(h->comm);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
+  if (h->st2) cudaStreamSynchronize(h->st2), cudaStreamDestroy(h->st2);
+  if (h->fork) cudaEventDestroy(h->fork);
+  if (h->join) cudaEventDestroy(h->join);
   if (h->solver) cusolverDnDestroy(h->solver);
   if (h->cublas) cublasDestroy(h->cublas);
   if (h->st) cudaStreamDestroy(h->st);
