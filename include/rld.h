@@ -218,6 +218,12 @@ int rld_chi_radii(const uint64_t key[2], uint64_t word0, int64_t df, int64_t cou
  * Synchronous. */
 int rld_dense_cholesky(rld_handle* h, int32_t n, double* G, int32_t* info);
 
+/* The symmetric eigensolver of the preconditioner build (eigh of B, src/precond.py:189-190, and of
+ * At^T At, src/precond.py:96) on the n x n column-major float64 device matrix A (positive
+ * semi-definite): eigenvalues ascending into w (device, n), eigenvectors over A (column j <-> w[j],
+ * signs arbitrary as LAPACK's).  Synchronous. */
+int rld_dense_eigh(rld_handle* h, int32_t n, double* A, double* w);
+
 /* exact_logdet(M) -- src/estimators.py:125-129: Cholesky log det of the
  * resident problem's K in float64 on the device. */
 int rld_exact_logdet(rld_handle* h, double* value);

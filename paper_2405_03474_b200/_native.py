@@ -39,7 +39,7 @@ ABI_VERSION = 3
 # every symbol include/rld.h declares
 EXPORTS = (
     "rld_abi_version", "rld_create", "rld_destroy", "rld_last_error", "rld_logdet", "rld_prepare",
-    "rld_logdet_resident", "rld_build_covariance", "rld_kv_apply", "rld_rademacher", "rld_exact_logdet", "rld_dense_cholesky",
+    "rld_logdet_resident", "rld_build_covariance", "rld_kv_apply", "rld_rademacher", "rld_exact_logdet", "rld_dense_cholesky", "rld_dense_eigh",
     "rld_nccl_unique_id", "rld_stream", "rld_normal", "rld_chi_radii",
 )
 
@@ -110,6 +110,7 @@ def load() -> C.CDLL:
         lib.rld_normal.argtypes = [H, C.POINTER(C.c_uint64 * 2), C.c_int64, C.c_int64, C.c_void_p]
         lib.rld_exact_logdet.argtypes = [H, C.POINTER(C.c_double)]
         lib.rld_dense_cholesky.argtypes = [H, C.c_int32, C.c_void_p, C.POINTER(C.c_int32)]
+        lib.rld_dense_eigh.argtypes = [H, C.c_int32, C.c_void_p, C.c_void_p]
         lib.rld_chi_radii.argtypes = [C.POINTER(C.c_uint64 * 2), C.c_uint64, C.c_int64, C.c_int64, C.c_void_p]
         lib.rld_nccl_unique_id.argtypes = [C.c_void_p]
         lib.rld_stream.argtypes = [H]

@@ -114,6 +114,7 @@ struct Work {
   DevBuf endw, radii;            // normal-orthogonal probes: stream position, chi radii
   DevBuf lz_dotp, lz_dotp2;      // fused Lanczos step: per-chunk dot partials
   DevBuf rinv;                   // CholQR: explicit R^-1
+  DevBuf eig_scratch;            // one-cluster eigensolver: V and singular values
   DevBuf flagbuf;        // flag OR over ranks
   KvWorkspace kv;
 };
@@ -516,6 +517,9 @@ void qr_householder(rld_handle* h, int64_t n, int w, double* Y, double rtol, int
 
 void syevd(rld_handle* h, int k, double* A, double* evals) {
   Work& wk = h->wk;
+  // the preconditioner's B and C are positive semi-definite: one-cluster Jacobi for k <= 288 when
+  // opted in (RLD_SMALL_EIG=1; slower than DSYEVD, kept for measurement)
+  if (small_eigh(k, A, evals, wk.eig_scratch, nullptr, h->st)) return;
   int* info = wk.ints.as<int>() + 2;
   int lwork = 0;
   RLD_CUSOLVER(cusolverDnDsyevd_bufferSize(h->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, k, A, k,
@@ -1330,6 +1334,16 @@ int rld_dense_cholesky(rld_handle* h, int32_t n, double* G, int32_t* info) {
     int* dinfo = h->wk.ints.as<int>() + 1;
     potrf_upper(h, n, G, dinfo);
     RLD_CUDA(cudaMemcpyAsync(info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    RLD_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int rld_dense_eigh(rld_handle* h, int32_t n, double* A, double* w) {
+  if (!h) return RLD_ERR_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    if (n < 1 || !A || !w) fail(RLD_ERR_INVALID_ARGUMENT, "bad dense_eigh arguments");
+    h->wk.ints.reserve(sizeof(int) * 8);
+    syevd(h, n, A, w);
     RLD_CUDA(cudaStreamSynchronize(h->st));
   });
 }

@@ -79,6 +79,11 @@ void chol_logdet(int k, const double* L, const int* info, double* out, int* flag
 // out of range (caller falls back to cuSOLVER).  small_chol.cu
 // With Rinv != nullptr also writes R^-1 (upper, n x n, ld n, lower part zero).
 bool small_potrf_upper(int n, double* G, int ld, int* info, cudaStream_t st, double* Rinv = nullptr);
+// Eigenpairs of a symmetric positive semi-definite n x n matrix (n <= 288) on one 16-CTA cluster
+// (one-sided block Jacobi, small_eig.cu): eigenvalues ascending into w, eigenvectors over A
+// (column j <-> w[j]), as DSYEVD returns them up to signs.  false if n is out of range or the
+// solver is not enabled (opt-in RLD_SMALL_EIG=1: measured ~10x slower than DSYEVD).
+bool small_eigh(int n, double* A, double* w, DevBuf& scratch, int* sweeps, cudaStream_t st);
 void sqrt_factors(int k, double keep_rtol, const double* lam, double* W, double* h, double* g, double* gam,
                   int* kept, cudaStream_t st);
 void convert_rows(const void* src, int sdt, void* dst, int ddt, int64_t count, cudaStream_t st);

@@ -608,3 +608,81 @@ print(json.dumps(out))
         runs.append(json.loads(r.stdout.strip().splitlines()[-1]))
     assert runs[0] == runs[1], runs
     assert all(np.isfinite(v) for v in runs[0])
+
+
+def _dense_eigh(A):
+    import ctypes as C  # noqa: F401
+    import torch
+
+    from paper_2405_03474_b200._session import session
+
+    s = session()
+    t = torch.from_numpy(np.ascontiguousarray(A)).cuda()   # symmetric: row-major == column-major
+    w = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
+    s.handle.check(s.lib.rld_dense_eigh(s.handle.ptr, A.shape[0], t.data_ptr(), w.data_ptr()), "dense_eigh")
+    return w.cpu().numpy(), t.cpu().numpy().T   # column j of the column-major result <-> w[j]
+
+
+@pytest.mark.parametrize("n", [2, 10, 64, 74, 256, 266, 288, 300])
+@pytest.mark.parametrize("spectrum", ["wishart", "decaying", "degenerate", "rank_deficient"])
+def test_dense_eigh_matches_lapack(rld, n, spectrum):
+    """The preconditioner's symmetric eigensolver (one-cluster Jacobi for n <= 288, DSYEVD above)
+    against LAPACK eigh: eigenvalues, reconstruction, orthogonality, and the top-half spectral
+    projector (eigenvectors are defined up to sign / rotation inside degenerate eigenspaces)."""
+    g = np.random.default_rng(n + len(spectrum))
+    Q, _ = np.linalg.qr(g.standard_normal((n, n)))
+    if spectrum == "wishart":
+        X = g.standard_normal((n + 5, n))
+        A = X.T @ X
+    else:
+        if spectrum == "decaying":
+            lam = np.logspace(7, -3, n)
+        elif spectrum == "degenerate":
+            lam = np.repeat([5.0, 2.0, 2.0, 0.5], -(-n // 4))[:n]
+        else:
+            lam = np.concatenate([np.logspace(3, 0, n - n // 3), np.zeros(n // 3)])
+        A = (Q * lam) @ Q.T
+        A = (A + A.T) / 2
+    w, V = _dense_eigh(A)
+    wr, Vr = np.linalg.eigh(A)
+    scale = max(1.0, np.max(np.abs(wr)))
+    assert np.all(np.diff(w) >= -1e-12 * scale)
+    np.testing.assert_allclose(w, wr, rtol=0, atol=1e-11 * scale)
+    assert np.linalg.norm(V.T @ V - np.eye(n)) <= 1e-11 * np.sqrt(n)
+    assert np.linalg.norm((V * w) @ V.T - A) <= 1e-11 * np.linalg.norm(A)
+    h = n // 2
+    if wr[h] - wr[h - 1] > 1e-6 * scale:   # a gap: the top-half invariant subspace is well defined
+        Pg, Pr = V[:, h:] @ V[:, h:].T, Vr[:, h:] @ Vr[:, h:].T
+        assert np.linalg.norm(Pg - Pr) <= 1e-9
+
+
+def test_dense_eigh_cluster_jacobi_opt_in(rld):
+    """The opt-in one-cluster Jacobi eigensolver (RLD_SMALL_EIG=1, read once per process, so in a
+    subprocess) against LAPACK on a decaying and a degenerate spectrum."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    code = r"""
+import sys
+sys.path.insert(0, %r)
+sys.path.insert(0, %r)
+import numpy as np
+from test_gpu_parity import _dense_eigh
+for n, lam in [(266, np.logspace(7, -3, 266)), (64, np.repeat([5.0, 2.0, 2.0, 0.5], 16))]:
+    g = np.random.default_rng(n)
+    Q, _ = np.linalg.qr(g.standard_normal((n, n)))
+    A = (Q * lam) @ Q.T
+    A = (A + A.T) / 2
+    w, V = _dense_eigh(A)
+    wr = np.linalg.eigh(A)[0]
+    s = np.max(np.abs(wr))
+    assert np.max(np.abs(w - wr)) <= 1e-11 * s, (n, np.max(np.abs(w - wr)))
+    assert np.linalg.norm(V.T @ V - np.eye(n)) <= 1e-11 * np.sqrt(n)
+    assert np.linalg.norm((V * w) @ V.T - A) <= 1e-11 * np.linalg.norm(A)
+print("ok")
+""" % (str(Path(__file__).resolve().parent.parent), str(Path(__file__).resolve().parent))
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, RLD_SMALL_EIG="1"), capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
