@@ -686,3 +686,36 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, RLD_SMALL_EIG="1"), capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
+
+
+def test_opt_in_fused_lanczos_and_cholqr_paths_agree(rld):
+    """The opt-in / alternative one-GPU paths (RLD_FUSED_LANCZOS=1: fused Lanczos step with the
+    pre-split tensor-core operand; RLD_CHOLQR_GEMM=0: DTRSM CholQR; RLD_TC_CG2=0: single-CTA
+    products) give the default estimate to fp32 accuracy (flags are read once: subprocesses)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    code = r"""
+import json, sys
+sys.path.insert(0, %r)
+import paper_2405_03474_b200 as rld
+from paper_2405_03474_b200.workloads import baseline
+out = []
+for idx, n in [(1, 1024), (2, 4096)]:
+    wl = baseline(idx, n=n)
+    out.append(rld.estimate_logdet(rld.KernelMatrix(wl.spec, wl.points), wl.config).value)
+print(json.dumps(out))
+""" % str(Path(__file__).resolve().parent.parent)
+    runs = {}
+    for name, env in [("default", {}), ("fused", {"RLD_FUSED_LANCZOS": "1"}), ("trsm", {"RLD_CHOLQR_GEMM": "0"}),
+                      ("single_cta", {"RLD_TC_CG2": "0"})]:
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, (name, r.stderr[-2000:])
+        runs[name] = json.loads(r.stdout.strip().splitlines()[-1])
+    for name, vals in runs.items():
+        for v, d, tol in zip(vals, runs["default"], (1e-9, 1e-5)):   # config 1 runs in fp64, config 2 in fp32
+            assert rel(v, d) <= tol, (name, v, d)
