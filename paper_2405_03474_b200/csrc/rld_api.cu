@@ -135,6 +135,7 @@ struct rld_handle {
   cudaEvent_t ev[8] = {};
   cudaStream_t st2 = nullptr;        // side stream for independent small work (joined before use)
   cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t efork = nullptr, ejoin = nullptr;   // the eigensolver's own side-stream branch
 };
 
 namespace rld {
@@ -520,6 +521,43 @@ void syevd(rld_handle* h, int k, double* A, double* evals) {
   // the preconditioner's B and C are positive semi-definite: one-cluster Jacobi for k <= 288 when
   // opted in (RLD_SMALL_EIG=1; slower than DSYEVD, kept for measurement)
   if (small_eigh(k, A, evals, wk.eig_scratch, nullptr, h->st)) return;
+  // tridiagonalisation + multisection + inverse iteration (tri_eig.cu) for k <= 288, then
+  // Newton-Schulz orthogonalisation of T's eigenvectors, Z <- 1.5 Z - 0.5 Z (Z^T Z) (symmetric in
+  // the columns; the defect E = Z^T Z - I goes to ~0.75 E^2 per step), and the back-transformation,
+  // all on FP64 DGEMMs.  Inverse-iteration vectors are orthogonal to ~eps |T| / gap; the defect is
+  // read back (one sync per eigensolve) to pick 1-4 steps, and when it exceeds 0.05 (eigenvalues
+  // inside one unreduced block of T closer than that allows) the matrix, still untouched, goes to
+  // DSYEVD instead.
+  double *Z, *Q, *sp;
+  if (tri_eigh(k, A, evals, wk.eig_scratch, &Z, &Q, &sp, h->st, h->st2, h->efork, h->ejoin)) {
+    const size_t kk = (size_t)k * k;
+    double* G = sp;
+    double* Z2 = sp + kk;
+    double* defect = sp + 2 * kk;
+    RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, k, k, k, &ONE, Z, k, Z, k, &ZERO, G, k));
+    orth_defect(k, G, defect, h->st);
+    double hd = 0.0;
+    RLD_CUDA(cudaMemcpyAsync(&hd, defect, sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    RLD_CUDA(cudaStreamSynchronize(h->st));
+    if (hd <= 0.05) {
+      int steps = 0;
+      for (double e = hd; e > 1e-15 && steps < 6; e = 0.75 * e * e + 2e-16) ++steps;
+      const double HALF_NEG = -0.5, THREE_HALF = 1.5;
+      double* cur = Z;
+      double* nxt = Z2;
+      for (int it = 0; it < steps; ++it) {
+        if (it > 0)
+          RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, k, k, k, &ONE, cur, k, cur, k, &ZERO, G, k));
+        copy_doubles((int64_t)kk, cur, nxt, h->st);
+        RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, k, k, k, &HALF_NEG, cur, k, G, k, &THREE_HALF,
+                               nxt, k));
+        std::swap(cur, nxt);
+      }
+      RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, k, k, k, &ONE, Q, k, cur, k, &ZERO, A, k));
+      return;
+    }
+    if (getenv("RLD_TRI_EIG_DEBUG")) fprintf(stderr, "rld: tri_eigh fallback to DSYEVD (k = %d, defect %.2e)\n", k, hd);
+  }
   int* info = wk.ints.as<int>() + 2;
   int lwork = 0;
   RLD_CUSOLVER(cusolverDnDsyevd_bufferSize(h->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, k, A, k,
@@ -1224,6 +1262,8 @@ int rld_create(const rld_device_set* ds, rld_handle** out) {
     RLD_CUDA(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
     RLD_CUDA(cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming));
     RLD_CUDA(cudaEventCreateWithFlags(&h->join, cudaEventDisableTiming));
+    RLD_CUDA(cudaEventCreateWithFlags(&h->efork, cudaEventDisableTiming));
+    RLD_CUDA(cudaEventCreateWithFlags(&h->ejoin, cudaEventDisableTiming));
     if (h->world > 1) {
       if (!ds || !ds->nccl_id) fail(RLD_ERR_INVALID_ARGUMENT, "nccl_id required for world_size > 1");
       ncclUniqueId id;
@@ -1254,6 +1294,8 @@ void rld_destroy(rld_handle* h) {
   if (h->st2) cudaStreamSynchronize(h->st2), cudaStreamDestroy(h->st2);
   if (h->fork) cudaEventDestroy(h->fork);
   if (h->join) cudaEventDestroy(h->join);
+  if (h->efork) cudaEventDestroy(h->efork);
+  if (h->ejoin) cudaEventDestroy(h->ejoin);
   if (h->solver) cusolverDnDestroy(h->solver);
   if (h->cublas) cublasDestroy(h->cublas);
   if (h->st) cudaStreamDestroy(h->st);

@@ -84,6 +84,16 @@ bool small_potrf_upper(int n, double* G, int ld, int* info, cudaStream_t st, dou
 // (column j <-> w[j]), as DSYEVD returns them up to signs.  false if n is out of range or the
 // solver is not enabled (opt-in RLD_SMALL_EIG=1: measured ~10x slower than DSYEVD).
 bool small_eigh(int n, double* A, double* w, DevBuf& scratch, int* sweeps, cudaStream_t st);
+// Eigen-decomposition of a symmetric n x n matrix (3 <= n <= 288) up to the last two steps
+// (tri_eig.cu): eigenvalues ascending into w; Z (n x n) = eigenvectors of the tridiagonal T from
+// inverse iteration (orthogonal up to eps |T| / gap: the caller runs one Cholesky-QR pass) and
+// Q (n x n) with A = Q T Q^T, both in `scratch`; eigenvectors of A = Q orth(Z).  `spare` points to
+// 3 n^2 free doubles.  Q is formed on st2 (fork / join events), joined into st before returning.
+// false if n is out of range or RLD_TRI_EIG=0.
+bool tri_eigh(int n, const double* A, double* w, DevBuf& scratch, double** Z, double** Q, double** spare,
+              cudaStream_t st, cudaStream_t st2, cudaEvent_t fork, cudaEvent_t join);
+// *out = max |G - I| of the n x n matrix G (NaN reads as 1e300)
+void orth_defect(int n, const double* G, double* out, cudaStream_t st);
 void sqrt_factors(int k, double keep_rtol, const double* lam, double* W, double* h, double* g, double* gam,
                   int* kept, cudaStream_t st);
 void convert_rows(const void* src, int sdt, void* dst, int ddt, int64_t count, cudaStream_t st);
