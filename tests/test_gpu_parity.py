@@ -623,22 +623,31 @@ def _dense_eigh(A):
     return w.cpu().numpy(), t.cpu().numpy().T   # column j of the column-major result <-> w[j]
 
 
-@pytest.mark.parametrize("n", [2, 10, 64, 74, 256, 266, 288, 300])
-@pytest.mark.parametrize("spectrum", ["wishart", "decaying", "degenerate", "rank_deficient"])
+@pytest.mark.parametrize("n", [2, 3, 10, 64, 74, 256, 266, 288, 300])
+@pytest.mark.parametrize("spectrum", ["wishart", "decaying", "degenerate", "rank_deficient", "indefinite",
+                                      "clustered", "diagonal"])
 def test_dense_eigh_matches_lapack(rld, n, spectrum):
-    """The preconditioner's symmetric eigensolver (one-cluster Jacobi for n <= 288, DSYEVD above)
-    against LAPACK eigh: eigenvalues, reconstruction, orthogonality, and the top-half spectral
-    projector (eigenvectors are defined up to sign / rotation inside degenerate eigenspaces)."""
+    """The preconditioner's symmetric eigensolver (tri_eig.cu for 3 <= n <= 288, DSYEVD otherwise
+    and as the fallback on degenerate unreduced blocks) against LAPACK eigh: eigenvalues,
+    reconstruction, orthogonality, and the top-half spectral projector (eigenvectors are defined
+    up to sign / rotation inside degenerate eigenspaces)."""
     g = np.random.default_rng(n + len(spectrum))
     Q, _ = np.linalg.qr(g.standard_normal((n, n)))
     if spectrum == "wishart":
         X = g.standard_normal((n + 5, n))
         A = X.T @ X
+    elif spectrum == "diagonal":   # already tridiagonal and fully split: one-row blocks
+        A = np.diag(g.permutation(np.repeat(np.arange(1.0, 1 + -(-n // 2)), 2)[:n]))
     else:
         if spectrum == "decaying":
             lam = np.logspace(7, -3, n)
         elif spectrum == "degenerate":
             lam = np.repeat([5.0, 2.0, 2.0, 0.5], -(-n // 4))[:n]
+        elif spectrum == "indefinite":
+            lam = np.linspace(-3.0, 2.0, n) ** 3
+        elif spectrum == "clustered":   # pairs 1e-9 apart (relative): close but not degenerate
+            base = np.repeat(np.logspace(2, -1, -(-n // 2)), 2)[:n]
+            lam = base * (1 + 1e-9 * (np.arange(n) % 2))
         else:
             lam = np.concatenate([np.logspace(3, 0, n - n // 3), np.zeros(n // 3)])
         A = (Q * lam) @ Q.T
@@ -688,10 +697,53 @@ print("ok")
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
 
 
+def test_tri_eigh_fallback_and_dsyevd_path(rld):
+    """tri_eig.cu hands degenerate unreduced blocks to DSYEVD (reported with RLD_TRI_EIG_DEBUG=1)
+    and keeps a well-separated spectrum; RLD_TRI_EIG=0 (DSYEVD always) agrees to rounding.  Flags
+    are read once per process: subprocesses."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    code = r"""
+import sys
+sys.path.insert(0, %r)
+sys.path.insert(0, %r)
+import numpy as np
+from test_gpu_parity import _dense_eigh
+out = []
+for n, lam in [(266, np.logspace(4, -2, 266)), (64, np.repeat([5.0, 2.0, 2.0, 0.5], 16))]:
+    g = np.random.default_rng(n)
+    Q, _ = np.linalg.qr(g.standard_normal((n, n)))
+    A = (Q * lam) @ Q.T
+    A = (A + A.T) / 2
+    w, V = _dense_eigh(A)
+    out.append(np.linalg.norm((V * w) @ V.T - A) / np.linalg.norm(A))
+    out.append(float(w.sum()))
+print("res", *out)
+""" % (str(Path(__file__).resolve().parent.parent), str(Path(__file__).resolve().parent))
+    runs = {}
+    for flag in ("1", "0"):
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, RLD_TRI_EIG=flag, RLD_TRI_EIG_DEBUG="1"),
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        runs[flag] = (r.stdout, r.stderr)
+    fallbacks = [ln for ln in runs["1"][1].splitlines() if "tri_eigh fallback" in ln]
+    assert len(fallbacks) == 1 and "k = 64" in fallbacks[0], runs["1"][1][-2000:]
+    assert not [ln for ln in runs["0"][1].splitlines() if "tri_eigh fallback" in ln]
+    a = [float(x) for x in runs["1"][0].split("res")[1].split()]
+    b = [float(x) for x in runs["0"][0].split("res")[1].split()]
+    assert a[0] < 1e-13 and b[0] < 1e-13 and a[2] < 1e-13
+    np.testing.assert_allclose(a[1], b[1], rtol=1e-12)
+    np.testing.assert_allclose(a[3], b[3], rtol=1e-12)
+
+
 def test_opt_in_fused_lanczos_and_cholqr_paths_agree(rld):
     """The opt-in / alternative one-GPU paths (RLD_FUSED_LANCZOS=1: fused Lanczos step with the
     pre-split tensor-core operand; RLD_CHOLQR_GEMM=0: DTRSM CholQR; RLD_TC_CG2=0: single-CTA
-    products) give the default estimate to fp32 accuracy (flags are read once: subprocesses)."""
+    products; RLD_TRI_EIG=0: cuSOLVER DSYEVD instead of tri_eig.cu) give the default estimate to
+    fp32 accuracy (flags are read once: subprocesses)."""
     import json
     import os
     import subprocess
@@ -711,7 +763,7 @@ print(json.dumps(out))
 """ % str(Path(__file__).resolve().parent.parent)
     runs = {}
     for name, env in [("default", {}), ("fused", {"RLD_FUSED_LANCZOS": "1"}), ("trsm", {"RLD_CHOLQR_GEMM": "0"}),
-                      ("single_cta", {"RLD_TC_CG2": "0"})]:
+                      ("single_cta", {"RLD_TC_CG2": "0"}), ("dsyevd", {"RLD_TRI_EIG": "0"})]:
         r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
                            timeout=600)
         assert r.returncode == 0, (name, r.stderr[-2000:])
