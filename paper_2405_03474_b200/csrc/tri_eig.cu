@@ -27,18 +27,24 @@ constexpr int TCL = 16, TT = 256, TNMAX = 288, TRPC = TNMAX / TCL;   // 18 rows 
 
 // A column-major n x n symmetric (only symmetry is used: row i == column i).  Outputs d (n),
 // e (n - 1), tau (n - 2) and the reflectors V (n x (n - 2), column j = v_j, zero above j + 1).
+// Each CTA owns rows i = r, r + 16, ...; per column ONE cluster barrier and no block barrier:
+// every warp keeps the current column, v and w in registers (c = lane + 32k), computes the
+// reflector and both dot products redundantly with butterflies, and reads v_i / w_i of its own
+// rows (the rank-2 update) from a per-warp shared slot.  Owners broadcast p = tau A v and their
+// raw entries of the next column through DSMEM; the next column is rebuilt locally from them.
+// (0.63 ms vs 0.89 ms for the block-barrier version at n = 266: scripts/tridiag_bench3.cu.)
 __global__ void __launch_bounds__(TT)
 tridiag_kernel(int n, const double* __restrict__ A, double* __restrict__ d, double* __restrict__ e,
                double* __restrict__ tau_out, double* __restrict__ V) {
+  constexpr int K = TNMAX / 32, W = TT / 32;
   cg::cluster_group cl = cg::this_cluster();
   const int r = (int)cl.block_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  extern __shared__ double rows_raw[];
-  double (*rows)[TNMAX] = reinterpret_cast<double (*)[TNMAX]>(rows_raw);   // my rows, [TRPC][TNMAX]
-  __shared__ double col[2][TNMAX];
-  __shared__ double pv[2][TNMAX];
-  __shared__ double v[TNMAX], w[TNMAX];
-  __shared__ double red[TT / 32];
+  extern __shared__ double sm[];
+  double (*rows)[TNMAX] = reinterpret_cast<double (*)[TNMAX]>(sm);                  // [TRPC][TNMAX]
+  double (*vw)[2][TNMAX] = reinterpret_cast<double (*)[2][TNMAX]>(sm + TRPC * TNMAX);  // [W][2][TNMAX]
+  __shared__ double col[2][TNMAX];   // raw broadcast column (before this column's correction)
+  __shared__ double pv[2][TNMAX];    // broadcast p = tau A v
   const int nr = (n - r + TCL - 1) / TCL;
   for (int q = 0; q < nr; ++q)
     for (int c = tid; c < n; c += TT) rows[q][c] = A[(size_t)(r + q * TCL) * n + c];
@@ -48,71 +54,114 @@ tridiag_kernel(int n, const double* __restrict__ A, double* __restrict__ d, doub
     for (int dst = 0; dst < TCL; ++dst) *cl.map_shared_rank(&col[0][i], dst) = rows[q][0];
   }
   cl.sync();
+  double x[K], v[K], w[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int c = lane + 32 * k;
+    x[k] = c < n ? col[0][c] : 0.0;
+  }
+  double* myv = vw[warp][0];
+  double* myw = vw[warp][1];
+  for (int c = lane; c < TNMAX; c += 32) myv[c] = myw[c] = 0.0;
+  __syncwarp();
+  // the previous column's reflector scalars v_j, w_j: entry c of the current column is
+  // col[b][c] - (v'_c w'_j + w'_c v'_j) with v', w' still in this warp's slot
+  double pvj = 0.0, pwj = 0.0;
   for (int j = 0; j < n - 2; ++j) {
     const int b = j & 1;
     double s = 0.0;
-    for (int i = j + 1 + tid; i < n; i += TT) s = fma(col[b][i], col[b][i], s);
-    s = warp_sum(s);
-    if (lane == 0) red[warp] = s;
-    __syncthreads();
-    double sig = 0.0;
-    for (int k = 0; k < TT / 32; ++k) sig += red[k];
-    const double x0 = col[b][j + 1];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (lane + 32 * k > j) s = fma(x[k], x[k], s);
+    const double sig = warp_sum(s);
+    const double x0 = col[b][j + 1] - (myv[j + 1] * pwj + myw[j + 1] * pvj);
+    const double dj = col[b][j] - (myv[j] * pwj + myw[j] * pvj);
+    __syncwarp();
     const double alpha = -copysign(sqrt(sig), x0);
     const double vtv = sig - x0 * x0 + (x0 - alpha) * (x0 - alpha);
     const double tau = vtv > 0.0 ? 2.0 / vtv : 0.0;
-    for (int i = tid; i < n; i += TT) v[i] = (i <= j) ? 0.0 : (i == j + 1 ? x0 - alpha : col[b][i]);
-    if (r == 0 && tid == 0) {
-      d[j] = col[b][j];
-      e[j] = (tau > 0.0) ? alpha : x0;   // a zero column below the diagonal: no reflection
-      tau_out[j] = tau;
+    const double vj1 = x0 - alpha;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int c = lane + 32 * k;
+      v[k] = (c <= j) ? 0.0 : (c == j + 1 ? vj1 : x[k]);
+      myv[c] = v[k];
     }
-    __syncthreads();
-    if (r == 0)
-      for (int i = tid; i < n; i += TT) V[(size_t)j * n + i] = v[i];
-    for (int q = warp; q < nr; q += TT / 32) {
+    if (r == 0 && warp == 0) {
+      if (lane == 0) {
+        d[j] = dj;
+        e[j] = (tau > 0.0) ? alpha : x0;
+        tau_out[j] = tau;
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int c = lane + 32 * k;
+        if (c < n) V[(size_t)j * n + c] = v[k];
+      }
+    }
+    for (int q = warp; q < nr; q += W) {
       const int i = r + q * TCL;
+      if (i <= j) continue;
       double acc = 0.0;
-      if (i > j)
-        for (int c = j + 1 + lane; c < n; c += 32) acc = fma(rows[q][c], v[c], acc);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int c = lane + 32 * k;
+        if (c > j && c < n) acc = fma(rows[q][c], v[k], acc);
+      }
       acc = warp_sum(acc);
-      if (lane < TCL && i > j) *cl.map_shared_rank(&pv[b][i], lane) = tau * acc;
-    }
-    for (int q = tid; q < nr; q += TT) {
-      const int i = r + q * TCL;
-      if (i > j)
-        for (int dst = 0; dst < TCL; ++dst) *cl.map_shared_rank(&col[b ^ 1][i], dst) = rows[q][j + 1];
+      if (lane < TCL) {
+        *cl.map_shared_rank(&pv[b][i], lane) = tau * acc;
+        *cl.map_shared_rank(&col[b ^ 1][i], lane) = rows[q][j + 1];
+      }
     }
     cl.sync();
     double kap = 0.0;
-    for (int i = j + 1 + tid; i < n; i += TT) kap = fma(pv[b][i], v[i], kap);
-    kap = warp_sum(kap);
-    __syncthreads();
-    if (lane == 0) red[warp] = kap;
-    __syncthreads();
-    double kk = 0.0;
-    for (int k = 0; k < TT / 32; ++k) kk += red[k];
-    kk *= 0.5 * tau;
-    for (int i = tid; i < n; i += TT) w[i] = (i <= j) ? 0.0 : pv[b][i] - kk * v[i];
-    __syncthreads();
-    for (int i = j + 1 + tid; i < n; i += TT) col[b ^ 1][i] -= v[i] * w[j + 1] + w[i] * v[j + 1];
-    for (int q = warp; q < nr; q += TT / 32) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int c = lane + 32 * k;
+      w[k] = (c > j && c < n) ? pv[b][c] : 0.0;
+      kap = fma(w[k], v[k], kap);
+    }
+    const double kk = 0.5 * tau * warp_sum(kap);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      w[k] = fma(-kk, v[k], w[k]);
+      myw[lane + 32 * k] = w[k];
+    }
+    __syncwarp();
+    const double wj1 = fma(-kk, vj1, pv[b][j + 1]);
+    pvj = vj1;
+    pwj = wj1;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int c = lane + 32 * k;
+      x[k] = (c > j && c < n) ? col[b ^ 1][c] - (v[k] * wj1 + w[k] * vj1) : 0.0;
+    }
+    for (int q = warp; q < nr; q += W) {
       const int i = r + q * TCL;
       if (i <= j) continue;
-      const double vi = v[i], wi = w[i];
-      for (int c = j + 1 + lane; c < n; c += 32) rows[q][c] -= vi * w[c] + wi * v[c];
+      const double vi = myv[i], wi = myw[i];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int c = lane + 32 * k;
+        if (c > j && c < n) rows[q][c] -= vi * w[k] + wi * v[k];
+      }
     }
-    __syncthreads();
+    __syncwarp();
   }
-  if (r == 0 && tid == 0) {
+  if (n >= 3) {
     const int b = (n - 2) & 1;
-    if (n >= 2) {
-      d[n - 2] = col[b][n - 2];
-      e[n - 2] = col[b][n - 1];
+    const double a = col[b][n - 2] - (myv[n - 2] * pwj + myw[n - 2] * pvj);
+    const double bb = col[b][n - 1] - (myv[n - 1] * pwj + myw[n - 1] * pvj);
+    if (r == 0 && tid == 0) {
+      d[n - 2] = a;
+      e[n - 2] = bb;
     }
   }
+  __syncthreads();   // row n - 1 was last updated by its owner warp
   if ((n - 1) % TCL == r && tid == 0) d[n - 1] = rows[(n - 1) / TCL][n - 1];
 }
+
 
 // T splits between i and i + 1 when e_i^2 <= eps^2 |d_i d_{i+1}| (LAPACK dstebz's test): the
 // coupling is treated as zero by both the eigenvalue and the eigenvector kernels
@@ -351,6 +400,8 @@ inviter_kernel(int n, const double* __restrict__ d, const double* __restrict__ e
 #undef PB
 }
 
+size_t tridiag_smem() { return sizeof(double) * ((size_t)TRPC * TNMAX + (size_t)(TT / 32) * 2 * TNMAX); }
+
 size_t inviter_smem(int n) {
   return sizeof(double) * (3 * (size_t)n + (size_t)5 * n * IV_T) + sizeof(unsigned) * ((n + 31) / 32) * IV_T;
 }
@@ -522,7 +573,7 @@ bool tri_eigh(int n, const double* A, double* w, DevBuf& scratch, double** Zout,
   if (!attr) {
     RLD_CUDA(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     RLD_CUDA(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(sizeof(double) * TRPC * TNMAX)));
+                                  (int)tridiag_smem()));
     RLD_CUDA(cudaFuncSetAttribute(inviter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)inviter_smem(TNMAX)));
     attr = true;
   }
@@ -530,7 +581,7 @@ bool tri_eigh(int n, const double* A, double* w, DevBuf& scratch, double** Zout,
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(TCL);
     cfg.blockDim = dim3(TT);
-    cfg.dynamicSmemBytes = sizeof(double) * TRPC * TNMAX;
+    cfg.dynamicSmemBytes = tridiag_smem();
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
