@@ -175,10 +175,10 @@ chol_upper_kernel(int n, double* __restrict__ G, int ld, int* __restrict__ info,
     __syncthreads();
     for (int e = tid; e < ncol * NB; e += THREADS) {
       const int m = e % NB, q = e / NB;
-      double x = 0.0;
-#pragma unroll 8
-      for (int l = 0; l < NB; ++l) x = fma(Rv[l * LDB + m], Gs[q * LDB + l], x);   // Rv lower part is 0
-      if (m < kb) G[(size_t)(jstart + q * CL) * ld + k0 + m] = x;
+      double x4[4] = {0.0, 0.0, 0.0, 0.0};   // four short chains instead of one of length 32
+#pragma unroll
+      for (int l = 0; l < NB; ++l) x4[l & 3] = fma(Rv[l * LDB + m], Gs[q * LDB + l], x4[l & 3]);   // Rv lower part is 0
+      if (m < kb) G[(size_t)(jstart + q * CL) * ld + k0 + m] = (x4[0] + x4[1]) + (x4[2] + x4[3]);
     }
     mark(1);
     cluster_sync_all();
@@ -190,7 +190,7 @@ chol_upper_kernel(int n, double* __restrict__ G, int ld, int* __restrict__ info,
     // 128-byte lines straddle panels, so this SM may hold an old copy from the previous panel)
     {
       const int tot = NB * (n - k1);
-      constexpr int UNR = 8;
+      constexpr int UNR = 16;
       for (int e0 = tid; e0 < tot; e0 += THREADS * UNR) {
         double v[UNR];
 #pragma unroll
@@ -218,14 +218,18 @@ chol_upper_kernel(int n, double* __restrict__ G, int ld, int* __restrict__ info,
       const int i = e % NB, c = e / NB;
       double v = Dn[i * LDB + c];
       if (i <= c && c < kb2) {
-#pragma unroll 8
-        for (int m = 0; m < NB; ++m) v = fma(-Pt[(k1 + i) * LDB + m], Pt[(k1 + c) * LDB + m], v);
+        double u4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int m = 0; m < NB; ++m) u4[m & 3] = fma(Pt[(k1 + i) * LDB + m], Pt[(k1 + c) * LDB + m], u4[m & 3]);
+        v -= (u4[0] + u4[1]) + (u4[2] + u4[3]);
       }
       Ds[i * LDB + c] = v;
     }
     __syncthreads();
     if (warp == 0) {
+      const long long tf = clock64();
       factor_block(Ds, Ri, Rv, rowbuf, lane);
+      if (prof && cta == 0 && lane == 0) prof[5] += clock64() - tf;
     } else {
       // ---- 4b. rank-kb update of this CTA's columns beyond the next diagonal block
       const int js2 = k2 + ((cta - k2 % CL) + CL) % CL;
@@ -233,11 +237,26 @@ chol_upper_kernel(int n, double* __restrict__ G, int ld, int* __restrict__ info,
         double pj[NB];
 #pragma unroll
         for (int m = 0; m < NB; ++m) pj[m] = Pt[j * LDB + m];
-        for (int i = k1 + lane; i <= j; i += 32) {
-          double s = 0.0;
+        // this column's rows in chunks of 8 per lane: all 8 L2 loads of G issued before the FMAs
+        // (one round trip per chunk instead of one per row: the update was L2-latency bound)
+        for (int ib = k1; ib <= j; ib += 256) {
+          double g[8];
 #pragma unroll
-          for (int m = 0; m < NB; ++m) s = fma(Pt[i * LDB + m], pj[m], s);
-          G[(size_t)j * ld + i] -= s;
+          for (int u = 0; u < 8; ++u) {
+            const int i = ib + lane + 32 * u;
+            g[u] = (i <= j) ? G[(size_t)j * ld + i] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int i = ib + lane + 32 * u;
+            if (i <= j) {
+              const double* P1 = Pt + i * LDB;
+              double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+              for (int m = 0; m < NB; ++m) s4[m & 3] = fma(P1[m], pj[m], s4[m & 3]);
+              G[(size_t)j * ld + i] = g[u] - ((s4[0] + s4[1]) + (s4[2] + s4[3]));
+            }
+          }
         }
       }
     }
@@ -328,8 +347,8 @@ bool small_potrf_upper(int n, double* G, int ld, int* info, cudaStream_t st, dou
     RLD_CUDA(cudaMemcpyAsync(hp, prof, sizeof hp, cudaMemcpyDeviceToHost, st));
     RLD_CUDA(cudaStreamSynchronize(st));
     RLD_CUDA(cudaFree(prof));
-    fprintf(stderr, "small_chol n=%d cycles: prologue %lld panel-row %lld barrier %lld load %lld factor||update %lld\n",
-            n, hp[0], hp[1], hp[2], hp[3], hp[4]);
+    fprintf(stderr, "small_chol n=%d cycles: prologue %lld panel-row %lld barrier %lld load %lld factor||update %lld "
+            "(factor alone %lld)\n", n, hp[0], hp[1], hp[2], hp[3], hp[4], hp[5]);
   }
   return true;
 }
