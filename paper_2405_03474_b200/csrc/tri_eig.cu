@@ -205,6 +205,32 @@ __device__ __forceinline__ int sturm_block(int s, int t, const double* __restric
   return cnt;
 }
 
+// Two Sturm counts of rows [0, n) at xa and xb, interleaved (two independent recurrences per
+// thread: the chain is latency-bound, so the second count is nearly free).
+__device__ __forceinline__ void sturm_pair(int n, const double* __restrict__ d, const double* __restrict__ e2,
+                                           double xa, double xb, int& ca, int& cb) {
+  double a2 = 1.0, a1 = d[0] - xa, b2 = 1.0, b1 = d[0] - xb;
+  if (a1 == 0.0) a1 = -0x1p-900;
+  if (b1 == 0.0) b1 = -0x1p-900;
+  ca = a1 < 0.0;
+  cb = b1 < 0.0;
+  int i = 1;
+  for (; i + 7 <= n - 1; i += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double di = d[i + u], ei = e2[i + u - 1];
+      sturm_step(di - xa, ei, a1, a2, ca);
+      sturm_step(di - xb, ei, b1, b2, cb);
+    }
+    sturm_renorm(a1, a2);
+    sturm_renorm(b1, b2);
+  }
+  for (; i <= n - 1; ++i) {
+    sturm_step(d[i] - xa, e2[i - 1], a1, a2, ca);
+    sturm_step(d[i] - xb, e2[i - 1], b1, b2, cb);
+  }
+}
+
 // d, e of T scaled by a power of two to |T|_inf <= 1 (exact), squared couplings with splits zeroed.
 // Staged through shared memory first (the norm loop would otherwise walk global memory serially).
 __device__ __forceinline__ double load_scaled(int n, const double* __restrict__ d, const double* __restrict__ e,
@@ -230,7 +256,7 @@ __device__ __forceinline__ double load_scaled(int n, const double* __restrict__ 
 }
 
 // eigenvalue k (ascending) of T by multisection, one warp per eigenvalue: each iteration the lanes
-// test 31 interior points of [lo, hi] (~5 bits), down to 2 eps |T| or 2 ulp of the eigenvalue
+// test 63 interior points of [lo, hi] (~6 bits), down to 2 eps |T| or 2 ulp of the eigenvalue
 __global__ void bisect_kernel(int n, const double* __restrict__ d, const double* __restrict__ e,
                               double* __restrict__ lam) {
   extern __shared__ double sh[];
@@ -250,14 +276,19 @@ __global__ void bisect_kernel(int n, const double* __restrict__ d, const double*
   if (k >= n) return;
   double lo = glo - atol, hi = ghi + atol;
   for (int it = 0; it < 200 && hi - lo > fmax(atol, 4.4e-16 * fmax(fabs(lo), fabs(hi))); ++it) {
-    const double x = lo + (hi - lo) * (double)(lane + 1) / 32.0;   // lanes 0..30 interior, 31 = hi
-    const int c = (lane < 31) ? sturm_block(0, n - 1, ds, e2, x) : n;
-    // smallest lane whose count exceeds k: the eigenvalue lies below its point
-    const unsigned above = __ballot_sync(0xffffffffu, c > k);
-    const int first = __ffs(above) - 1;   // exists: lane 31 has count n > k
-    const double nhi = lo + (hi - lo) * (double)(first + 1) / 32.0;
-    const double nlo = lo + (hi - lo) * (double)first / 32.0;
-    hi = (first == 31) ? hi : nhi;
+    // 64 points lo + (hi - lo) q / 64, q = 1..64 (~6 bits per iteration): lane l tests q = l + 1
+    // and q = l + 33; q = 64 is hi itself (count n)
+    const double xa = lo + (hi - lo) * (double)(lane + 1) / 64.0;
+    const double xb = lo + (hi - lo) * (double)(lane + 33) / 64.0;
+    int ca, cb;
+    sturm_pair(n, ds, e2, xa, xb, ca, cb);
+    if (lane == 31) cb = n;
+    // smallest point whose count exceeds k: the eigenvalue lies below it
+    const unsigned aa = __ballot_sync(0xffffffffu, ca > k), ab = __ballot_sync(0xffffffffu, cb > k);
+    const int first = aa ? __ffs(aa) - 1 : 32 + __ffs(ab) - 1;   // exists: q = 64 has count n > k
+    const double nhi = lo + (hi - lo) * (double)(first + 1) / 64.0;
+    const double nlo = lo + (hi - lo) * (double)first / 64.0;
+    hi = (first == 63) ? hi : nhi;
     lo = nlo;
   }
   if (lane == 0) lam[k] = 0.5 * (lo + hi) / sc;
