@@ -365,17 +365,19 @@ inviter_kernel(int n, const double* __restrict__ d, const double* __restrict__ e
     for (int i = bs; i < bt; ++i) {
       const double sub = es[i] * sc;
       const double a1 = ds[i + 1] - shs, b1 = (i + 1 < bt) ? es[i + 1] * sc : 0.0;
-      if (fabs(a) >= fabs(sub)) {   // no interchange
-        const double m = (a == 0.0) ? 0.0 : sub / a;
-        FW(0, i) = 1.0 / ((fabs(a) < tiny) ? copysign(tiny, a) : a);
+      if (fabs(a) >= fabs(sub)) {   // no interchange (one reciprocal per row on the chain, not two divisions)
+        const double ra = 1.0 / ((fabs(a) < tiny) ? copysign(tiny, a) : a);
+        const double m = (a == 0.0) ? 0.0 : sub * ra;
+        FW(0, i) = ra;
         FW(1, i) = bsup;
         FW(2, i) = m;
         FW(3, i) = 0.0;
         a = a1 - m * bsup;
         bsup = b1;
       } else {                      // rows i and i+1 swap
-        const double m = a / sub;
-        FW(0, i) = 1.0 / sub;
+        const double rs = 1.0 / sub;
+        const double m = a * rs;
+        FW(0, i) = rs;
         FW(1, i) = a1;
         FW(2, i) = m;
         FW(3, i) = b1;
