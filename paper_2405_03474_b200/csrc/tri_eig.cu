@@ -25,6 +25,25 @@ namespace {
 namespace cg = cooperative_groups;
 constexpr int TCL = 16, TT = 256, TNMAX = 288, TRPC = TNMAX / TCL;   // 18 rows per CTA
 
+// sqrt and reciprocal on the per-column chain from the MUFU approximations plus two Newton steps
+// (~1 ulp): the IEEE FP64 sqrt / division sequences are several times longer.  Normal inputs only
+// (callers keep the IEEE path below 1e-300).
+__device__ __forceinline__ double sqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return x * y;
+}
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = fma(y, fma(-x, y, 1.0), y);
+  y = fma(y, fma(-x, y, 1.0), y);
+  return y;
+}
+
 // A column-major n x n symmetric (only symmetry is used: row i == column i).  Outputs d (n),
 // e (n - 1), tau (n - 2) and the reflectors V (n x (n - 2), column j = v_j, zero above j + 1).
 // Each CTA owns rows i = r, r + 16, ...; per column ONE cluster barrier and no block barrier:
@@ -77,9 +96,9 @@ tridiag_kernel(int n, const double* __restrict__ A, double* __restrict__ d, doub
     const double x0 = col[b][j + 1] - (myv[j + 1] * pwj + myw[j + 1] * pvj);
     const double dj = col[b][j] - (myv[j] * pwj + myw[j] * pvj);
     __syncwarp();
-    const double alpha = -copysign(sqrt(sig), x0);
+    const double alpha = -copysign(sig > 1e-300 ? sqrt_nr(sig) : sqrt(sig), x0);
     const double vtv = sig - x0 * x0 + (x0 - alpha) * (x0 - alpha);
-    const double tau = vtv > 0.0 ? 2.0 / vtv : 0.0;
+    const double tau = vtv > 1e-300 ? 2.0 * rcp_nr(vtv) : (vtv > 0.0 ? 2.0 / vtv : 0.0);
     const double vj1 = x0 - alpha;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
