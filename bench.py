@@ -80,6 +80,12 @@ def load_peaks():
     return 6650.0, 1590.0, "fallback"
 
 
+def load_pipe_peaks():
+    """Measured compute-pipe peaks of this pool's B200 (scripts/pipe_peaks.cu, committed)."""
+    p = ROOT / "profiles" / "r01_pipe_peaks.json"
+    return json.loads(p.read_text()) if p.exists() else {}
+
+
 class ClockSampler:
     """nvidia-smi clocks and throttle reasons during the timed region."""
 
@@ -334,6 +340,24 @@ def run_ours(args):
     traffic, traffic_src = (ncu_traffic() if (args.config == 2 and world == 1 and args.dtype in (None, "fp32"))
                             else (None, None))
     achieved = alg_bytes / (kv_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                "traffic": traffic, "traffic_source": traffic_src,
+                "kernel": f"kv_product (Lanczos shape m=s, {rows} rows of K)", "kernel_ms": kv_ms,
+                "alg_bytes": alg_bytes, "peak_source": peak_kind}
+    pipe = load_pipe_peaks()
+    if wl.path == "on_the_fly" or cfg.dtype == "fp64":
+        # no stored K (on the fly) or an FP64-pipe-bound product (fp64, 8 flop/B > the DFMA ridge):
+        # the bound is a compute pipe, SURVEY.md §8(d)
+        useful = 2.0 * rows * n * s
+        if cfg.dtype == "fp64":
+            kind, work, peak, src = "fp64", useful, pipe.get("dfma_tflops", 36.36), "profiles/r01_pipe_peaks.json dfma"
+        else:   # 3xTF32 tensor-core MMAs: three products per useful one
+            kind, work = "tensor", 3.0 * useful
+            peak, src = pipe.get("tf32_ts_n128", {}).get("tflops", 1115.0), "profiles/r01_pipe_peaks.json tf32 N=128"
+        ach = work / (kv_ms * 1e-3) / 1e12
+        roofline = {"bound": kind, "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                    "traffic": None, "kernel": f"kv_product ({wl.path}, m=s={s}, {rows} rows)", "kernel_ms": kv_ms,
+                    "alg_flops": work, "useful_flops": useful, "peak_source": src}
 
     # ---- end to end through the public API (host buffers, pinned)
     e2e = None
@@ -404,11 +428,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "kv_products_per_step": products // max(1, args.steps),
         "phase_ms_last_step": {"precond": phases[1], "lanczos": phases[4], "solves": phases[5]},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": traffic,
-                     "traffic_source": traffic_src,
-                     "kernel": f"kv_product (Lanczos shape m=s, {rows} rows of K)",
-                     "kernel_ms": kv_ms, "alg_bytes": alg_bytes, "peak_source": peak_kind},
+        "roofline": roofline,
         "clocks": clocks,
         "estimate": est.value,
     }

@@ -240,6 +240,17 @@ void kv_product(const KvOperand& op, int64_t m, const double* V, int64_t ldv, do
   if (m <= 0 || op.rows <= 0) return;
   const bool otf = (op.K == nullptr);
   if (op.dtype == RLD_FP64) {
+    // Stored float64 K: a plain GEMM, Y^T = K V^T, on cuBLAS DGEMM (the FP64 tensor-core DMMA path;
+    // tcgen05 has no f64 kind).  Measured 146 -> ~40 ms of K.V per config-2 fp64 estimate against
+    // this file's SIMT DFMA kernel (23 % of the DFMA peak), which stays for the on-the-fly fp64 path
+    // and behind RLD_FP64_SIMT=1.  Deterministic: cuBLAS without atomics, fixed configuration.
+    static const bool simt = getenv("RLD_FP64_SIMT") && getenv("RLD_FP64_SIMT")[0] == '1';
+    if (!otf && ws.blas && !simt) {
+      const double one = 1.0, zero = 0.0;
+      RLD_CUBLAS(cublasDgemm(ws.blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)op.rows, (int)m, (int)op.n, &one,
+                             static_cast<const double*>(op.K), (int)op.ldk, V, (int)ldv, &zero, Y, (int)ldy));
+      return;
+    }
     if (otf)
       launch_kv<double, double, 64, 32, 16, 4, 4, true>(op, m, V, ldv, Y, ldy, ws, st, launches);
     else

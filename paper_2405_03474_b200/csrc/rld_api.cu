@@ -1256,6 +1256,7 @@ int rld_create(const rld_device_set* ds, rld_handle** out) {
     RLD_CUDA(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
     RLD_CUBLAS(cublasCreate(&h->cublas));
     RLD_CUBLAS(cublasSetStream(h->cublas, h->st));
+    h->wk.kv.blas = h->cublas;
     RLD_CUSOLVER(cusolverDnCreate(&h->solver));
     RLD_CUSOLVER(cusolverDnSetStream(h->solver, h->st));
     for (auto& e : h->ev) RLD_CUDA(cudaEventCreate(&e));

@@ -100,6 +100,7 @@ struct KvWorkspace {
   DevBuf bhi, blo;    // tensor-core B operand (tf32 hi / lo rows)
   DevBuf tc_partial;  // stream-K partial accumulators
   DevBuf tc_sync;     // epoch-barrier counters of the tensor-core kernel
+  cublasHandle_t blas = nullptr;   // the handle's cuBLAS (bound to the same stream): fp64 stored K
 };
 
 bool kv_tc_supported(const KvOperand& op);
