@@ -482,7 +482,10 @@ def test_perfect_preconditioner_kills_stochastic_part(rld, kind, path):
 
 def test_partial_cholesky_on_the_fly_matches_stored(rld):
     """The pivoted partial Cholesky reads K columns from the stored K or generates them
-    from the points: same pivots and estimate (float64)."""
+    from the points: same pivots, so log det P agrees to 1e-9 (float64).  The stochastic
+    part agrees to 1e-6 only: stored fp64 K.V runs on cuBLAS DGEMM while the on-the-fly
+    product sums in the SIMT kernel's order, and Lanczos carries that ulp-level
+    difference through t steps (fp64 stored K.V)."""
     from paper_2405_03474_b200.workloads import baseline
 
     wl = baseline(5, n=2048)
@@ -490,7 +493,8 @@ def test_partial_cholesky_on_the_fly_matches_stored(rld):
                   precond=rld.PreconditionerConfig("partial-cholesky", 64, 5))
     a = rld.rstar_logdet(rld.KernelMatrix(wl.spec, wl.points), replace(cfg, path="stored"))
     b = rld.rstar_logdet(rld.KernelMatrix(wl.spec, wl.points), replace(cfg, path="on_the_fly"))
-    assert rel(a.logdet_P, b.logdet_P) <= 1e-9 and rel(a.value, b.value) <= 1e-9
+    assert rel(a.logdet_P, b.logdet_P) <= 1e-9
+    assert rel(a.value, b.value) <= 1e-6
 
 
 # ---------------------------------------------------------------- normal-orthogonal probes
