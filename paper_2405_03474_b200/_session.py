@@ -48,10 +48,12 @@ def dist_world():
 
 
 def hbm_bytes(device: int) -> int:
+    """Total HBM of the device: the 'auto' path choice depends on the problem and the GPU only,
+    never on what this process (or another) happens to have allocated, so every trial of a
+    sweep takes the same path."""
     t = _torch()
     if t is not None and t.cuda.is_available():
-        free, total = t.cuda.mem_get_info(device)
-        return int(free)
+        return int(t.cuda.get_device_properties(device).total_memory)
     return 180 * (1 << 30)
 
 
@@ -62,6 +64,33 @@ class Session:
         self.handle = N.Handle(device, rank, world_size, nccl_id)
         self.lib = self.handle.lib
         self.rank, self.world_size, self.device = rank, world_size, device
+
+    # -- stream ordering against torch ---------------------------------------
+    def torch_stream(self):
+        """The handle's stream as a torch ExternalStream (None without CUDA torch)."""
+        t = _torch()
+        if t is None or not t.cuda.is_available():
+            return None
+        if getattr(self, "_ext", None) is None:
+            self._ext = t.cuda.ExternalStream(self.handle.stream, device=self.device)
+        return self._ext
+
+    def after_torch(self):
+        """Order the handle's stream after everything torch has queued on its current stream
+        (the handle's stream is non-blocking: without this, a C call could read a torch tensor
+        before the kernel producing it ran, or write a block the caching allocator just handed
+        out while its previous owner's kernels are still pending)."""
+        t = _torch()
+        if t is None or not t.cuda.is_available() or not t.cuda.is_initialized():
+            return
+        self.torch_stream().wait_stream(t.cuda.current_stream(self.device))
+
+    def before_torch(self):
+        """Order torch's current stream after the handle's queued work (results it wrote)."""
+        t = _torch()
+        if t is None or not t.cuda.is_available() or not t.cuda.is_initialized():
+            return
+        t.cuda.current_stream(self.device).wait_stream(self.torch_stream())
 
     # -- problem translation -------------------------------------------------
     def resolve_path(self, M, dtype: str, path: str) -> str:
@@ -74,7 +103,7 @@ class Session:
         n = M.n
         rows = -(-n // self.world_size)
         es = 8 if dtype == "fp64" else 4
-        return "stored" if rows * n * es <= 0.6 * hbm_bytes(self.device) else "on_the_fly"
+        return "stored" if rows * n * es <= 0.5 * hbm_bytes(self.device) else "on_the_fly"
 
     def problem_for(self, M, dtype: str, path: str = "auto"):
         """(rld_problem, keepalive) for a dense matrix or a KernelMatrix."""
@@ -101,6 +130,7 @@ class Session:
             p.n, p.d = int(pts.shape[0]), int(pts.shape[1])
             p.amplitude, p.length_scale, p.jitter = spec.amplitude, spec.length_scale, spec.jitter
             p.data, p.data_memory, p.data_dtype, p.ld = ptr, mem, N.FP64, 0
+            self.after_torch()
             return p, pts
         if _is_torch(M):
             T = M.detach()
@@ -121,6 +151,7 @@ class Session:
                 a = T.numpy()
                 p.data, p.data_memory = a.ctypes.data, N.HOST
                 T = a
+            self.after_torch()
             return p, T
         A = np.asarray(M)
         if A.ndim != 2 or A.shape[0] != A.shape[1]:

@@ -240,15 +240,22 @@ void kv_product(const KvOperand& op, int64_t m, const double* V, int64_t ldv, do
   if (m <= 0 || op.rows <= 0) return;
   const bool otf = (op.K == nullptr);
   if (op.dtype == RLD_FP64) {
-    // Stored float64 K: a plain GEMM, Y^T = K V^T, on cuBLAS DGEMM (the FP64 tensor-core DMMA path;
-    // tcgen05 has no f64 kind).  Measured 146 -> ~40 ms of K.V per config-2 fp64 estimate against
-    // this file's SIMT DFMA kernel (23 % of the DFMA peak), which stays for the on-the-fly fp64 path
-    // and behind RLD_FP64_SIMT=1.  Deterministic: cuBLAS without atomics, fixed configuration.
+    // Stored float64 K: Y = V K^T on the FP64 tensor cores (kv_dmma.cu: TMA-fed DMMA, fixed-order
+    // split-k).  Operand rows must start 16-byte aligned: V is re-pitched into the workspace when
+    // it is not; a K aliased from a caller's odd-pitched matrix takes this file's DFMA kernel.
     static const bool simt = getenv("RLD_FP64_SIMT") && getenv("RLD_FP64_SIMT")[0] == '1';
-    if (!otf && ws.blas && !simt) {
-      const double one = 1.0, zero = 0.0;
-      RLD_CUBLAS(cublasDgemm(ws.blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)op.rows, (int)m, (int)op.n, &one,
-                             static_cast<const double*>(op.K), (int)op.ldk, V, (int)ldv, &zero, Y, (int)ldy));
+    const double* K = static_cast<const double*>(op.K);
+    if (!otf && !simt && gemm_nt_f64_ok(K, op.ldk, K, op.ldk)) {
+      const double* Vp = V;
+      int64_t ldvp = ldv;
+      if (!gemm_nt_f64_ok(V, ldv, V, ldv)) {
+        ldvp = (op.n + 1) / 2 * 2;
+        ws.vcast.reserve(sizeof(double) * m * ldvp);
+        RLD_CUDA(cudaMemcpy2DAsync(ws.vcast.ptr, sizeof(double) * ldvp, V, sizeof(double) * ldv,
+                                   sizeof(double) * op.n, m, cudaMemcpyDeviceToDevice, st));
+        Vp = ws.vcast.as<double>();
+      }
+      gemm_nt_f64(K, op.ldk, op.rows, Vp, ldvp, m, op.n, Y, ldy, 0.0, ws.partial, st);
       return;
     }
     if (otf)

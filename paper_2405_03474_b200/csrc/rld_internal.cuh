@@ -125,6 +125,13 @@ bool kv_tc_b_layout(const KvOperand& op, int64_t m, KvWorkspace& ws, TcBLayout& 
 void kv_product(const KvOperand& op, int64_t m, const double* V, int64_t ldv, double* Y, int64_t ldy,
                 KvWorkspace& ws, cudaStream_t st, int* launches, bool presplit = false);
 
+// Float64 products on the FP64 tensor cores (kv_dmma.cu):
+// C (q x p, ld ldc) = beta C + A B^T for A: p x n (ld lda), B: q x n (ld ldb), rows layout.
+// Rows must start 16-byte aligned (gemm_nt_f64_ok); deterministic split-k.
+bool gemm_nt_f64_ok(const double* A, int64_t lda, const double* B, int64_t ldb);
+void gemm_nt_f64(const double* A, int64_t lda, int64_t p, const double* B, int64_t ldb, int64_t q, int64_t n,
+                 double* C, int64_t ldc, double beta, DevBuf& partial, cudaStream_t st);
+
 // ---------------------------------------------------------------------------
 // RNG
 void rademacher_rows(const uint64_t key[2], int64_t rows, int64_t n, int64_t row0_col, int64_t ncols,

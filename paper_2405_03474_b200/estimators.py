@@ -79,6 +79,7 @@ class LogDetEstimate:
     kernel_launches: int = 0
     rank_kept: int = 0
     attempts: int = 1
+    path: str = "stored"      # where K lived for this estimate: "stored" in HBM or "on_the_fly"
 
 
 def _sketch_width(cfg: EstimatorConfig, n: int) -> int:
@@ -170,10 +171,15 @@ def _call_with_retry(call, inputs: _Inputs, handle: N.Handle, what: str):
     handle.check(rc, what)
 
 
-def _result(res: N.Result, per: np.ndarray, start: float) -> LogDetEstimate:
+def _path_of(prob) -> str:
+    return "on_the_fly" if (prob.source == N.SOURCE_POINTS and prob.path == N.PATH_ON_THE_FLY) else "stored"
+
+
+def _result(res: N.Result, per: np.ndarray, start: float, path: str = "stored") -> LogDetEstimate:
     return LogDetEstimate(res.value, res.logdet_P, res.trace_term, per, time.perf_counter() - start,
-                          clamped_eigs=int(res.clamped_eigs), device_time=res.wall_time, phase_ms=tuple(res.phase_ms), kv_products=res.kv_products,
-                          kernel_launches=res.kernel_launches, rank_kept=res.rank_kept, attempts=res.attempts)
+                          clamped_eigs=int(res.clamped_eigs), device_time=res.wall_time, phase_ms=tuple(res.phase_ms),
+                          kv_products=res.kv_products, kernel_launches=res.kernel_launches, rank_kept=res.rank_kept,
+                          attempts=res.attempts, path=path)
 
 
 def rstar_logdet(M, cfg: EstimatorConfig, probes=None, omega=None) -> LogDetEstimate:
@@ -210,7 +216,7 @@ def _run(M, cfg: EstimatorConfig, probes, omega) -> LogDetEstimate:
                                                  C.byref(inputs.struct), C.byref(res)),
                      inputs, sess.handle, "rld_logdet")
     del keep
-    return _result(res, per, start)
+    return _result(res, per, start, _path_of(prob))
 
 
 def exact_logdet(M, dtype: str = "fp64") -> LogDetEstimate:
@@ -257,7 +263,7 @@ class ResidentMatrix:
         self.dtype = dtype
         prob, self._keep = self.sess.problem_for(M, dtype, path)
         self.n = int(prob.n)
-        self.path = "on_the_fly" if (prob.source == N.SOURCE_POINTS and prob.path == N.PATH_ON_THE_FLY) else "stored"
+        self.path = _path_of(prob)
         self.sess.handle.check(self.sess.lib.rld_prepare(self.sess.handle.ptr, C.byref(prob)), "rld_prepare")
 
     def estimate(self, cfg: EstimatorConfig, probes=None, omega=None, inputs: N.Inputs | None = None) -> LogDetEstimate:
@@ -276,7 +282,7 @@ class ResidentMatrix:
             _call_with_retry(lambda: self.sess.lib.rld_logdet_resident(self.sess.handle.ptr, C.byref(c),
                                                                        C.byref(inp.struct), C.byref(res)),
                              inp, self.sess.handle, "rld_logdet_resident")
-        return _result(res, per, start)
+        return _result(res, per, start, self.path)
 
     def kv_apply(self, V):
         """Y = V K for device float64 rows V (m x n torch CUDA tensor).  With a
@@ -292,7 +298,7 @@ class ResidentMatrix:
         r0, r1 = shard_bounds(self.n, self.sess.world_size, self.sess.rank)
         Y = torch.empty((V.shape[0], r1 - r0), dtype=torch.float64, device=V.device)
         cur = torch.cuda.current_stream(V.device)
-        ext = self._ext_stream()
+        ext = self.sess.torch_stream()
         ext.wait_stream(cur)
         self.sess.handle.check(self.sess.lib.rld_kv_apply(self.sess.handle.ptr, V.shape[0], V.data_ptr(),
                                                           Y.data_ptr()), "rld_kv_apply")
@@ -301,13 +307,6 @@ class ResidentMatrix:
         # stream may be destroyed before the tensors are freed)
         cur.wait_stream(ext)
         return Y
-
-    def _ext_stream(self):
-        import torch
-
-        if getattr(self, "_ext", None) is None:
-            self._ext = torch.cuda.ExternalStream(self.sess.handle.stream)
-        return self._ext
 
     def exact_logdet(self) -> float:
         v = C.c_double()

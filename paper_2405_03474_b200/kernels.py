@@ -97,6 +97,8 @@ def build_covariance(spec: KernelSpec, points, dtype: str = "fp64", device: str 
 
     out = torch.empty((n, n), dtype=torch.float64 if dtype == "fp64" else torch.float32,
                       device=f"cuda:{sess.handle.device}")
+    sess.after_torch()    # the block may still be in use by pending torch kernels
     sess.handle.check(sess.lib.rld_build_covariance(sess.handle.ptr, C.byref(prob), out.data_ptr(), DEVICE),
                       "rld_build_covariance")
+    sess.before_torch()   # later torch work on `out` sees the build
     return out

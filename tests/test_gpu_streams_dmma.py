@@ -1,0 +1,100 @@
+"""GPU: stream ordering against torch, and the float64 tensor-core product (kv_dmma.cu).
+
+* Inputs produced by torch kernels still queued on torch's current stream must be seen by
+  librld's (non-blocking) stream: ``Session.after_torch`` orders the handle's stream after
+  them.
+* The FP64 DMMA product (stored float64 K, the estimate's ``M @ y`` of src/estimators.py:72)
+  against numpy float64 at ragged shapes: n odd / not a multiple of the 16-double k-step,
+  m = 1 .. 300 vectors (one, two and several column tiles, split-k and not).
+"""
+
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+from conftest import rel
+from oracle import rstar_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rld():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2405_03474_b200 as rld
+
+    return rld
+
+
+def test_points_from_pending_torch_kernels_are_seen(rld):
+    """Points written by a torch copy queued behind ~100 ms of GEMMs on the default stream."""
+    import torch
+
+    from paper_2405_03474_b200.workloads import baseline
+
+    wl = baseline(1, n=1024, rank=32, num_probes=8)
+    ref = rld.rstar_logdet(rld.KernelMatrix(wl.spec, wl.points), wl.config)
+    src = torch.from_numpy(wl.points).cuda()
+    torch.cuda.synchronize()
+    for trial in range(3):
+        big = torch.randn(4096, 4096, device="cuda")
+        pts = torch.zeros_like(src)
+        for _ in range(40):                       # keep the current stream busy
+            big = (big @ big) * 1e-4
+        pts.copy_(src)                            # queued behind the GEMMs
+        est = rld.rstar_logdet(rld.KernelMatrix(wl.spec, pts), wl.config)
+        assert est.value == ref.value, (trial, est.value, ref.value)
+
+
+def test_build_covariance_then_torch_reads_it(rld):
+    import torch
+
+    from paper_2405_03474_b200.workloads import baseline
+
+    wl = baseline(2, n=3000)
+    K = rld.build_covariance(wl.spec, wl.points, dtype="fp64")
+    s = K.sum()                                   # torch work on the current stream
+    ref = O.covariance_block(wl.spec.family, wl.spec.amplitude, wl.spec.length_scale, wl.spec.jitter, wl.points)
+    assert rel(float(s), float(ref.sum())) <= 1e-12
+
+
+@pytest.mark.parametrize("n,m", [(16, 1), (17, 3), (1000, 33), (4099, 37), (4096, 64), (3001, 65), (2048, 129),
+                                 (5000, 300), (20000, 8)])
+def test_fp64_tensor_core_product(rld, n, m):
+    import torch
+
+    from paper_2405_03474_b200.workloads import baseline
+
+    wl = baseline(2, n=n)
+    R = rld.ResidentMatrix(rld.KernelMatrix(wl.spec, wl.points), dtype="fp64", path="stored")
+    g = np.random.default_rng(n + m)
+    V = g.standard_normal((m, n))
+    Y = R.kv_apply(torch.from_numpy(V).cuda()).cpu().numpy()
+    K = O.covariance_block(wl.spec.family, wl.spec.amplitude, wl.spec.length_scale, wl.spec.jitter, wl.points)
+    ref = V @ K.T
+    scale = np.abs(V) @ np.abs(K).T
+    assert np.max(np.abs(Y - ref) / scale) <= 1e-14
+    # deterministic: a second product is bit-identical
+    Y2 = R.kv_apply(torch.from_numpy(V).cuda()).cpu().numpy()
+    assert np.array_equal(Y, Y2)
+
+
+def test_fp64_product_misaligned_operand(rld):
+    """V rows with an odd pitch (a column slice of a wider tensor) are re-pitched, not misread."""
+    import torch
+
+    from paper_2405_03474_b200.workloads import baseline
+
+    n, m = 1001, 5
+    wl = baseline(2, n=n)
+    R = rld.ResidentMatrix(rld.KernelMatrix(wl.spec, wl.points), dtype="fp64", path="stored")
+    wide = torch.randn(m, n + 1, dtype=torch.float64, device="cuda")
+    V = wide[:, 1:]
+    Y = R.kv_apply(V).cpu().numpy()
+    K = O.covariance_block(wl.spec.family, wl.spec.amplitude, wl.spec.length_scale, wl.spec.jitter, wl.points)
+    ref = V.cpu().numpy() @ K.T
+    assert np.max(np.abs(Y - ref)) <= 1e-12 * np.max(np.abs(ref))
