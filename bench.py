@@ -1,9 +1,13 @@
-"""Benchmark: log-det estimates per second on BASELINE config 2 (n = 16384,
-RBF in R^8, stored K in HBM, rand-SVD l = 256, 32 Rademacher probes, t = 20),
-one JSON line on rank 0.
+"""Benchmark: log-det estimates per second on BASELINE config 3 (n = 65536 points
+uniform in [0,1]^2, Matern-5/2 l = 0.05, noise 1e-2, stored K in HBM, r3, rand-SVD
+l = 512, 64 Gaussian probes, t = 20), in float64 -- the reference's arithmetic, so the
+reference arm is like-for-like -- one JSON line on rank 0.  Config 3 is the largest
+BASELINE configuration a single B200 completes within the driver's limits (config 5
+takes minutes per estimate); the line also carries config 3 in fp32 (BASELINE's
+stated precision) as an extra key.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config 2] [--dtype fp32|fp64] [--algorithm r3] [--n N]
+                  [--config 3] [--dtype fp32|fp64] [--algorithm r3] [--n N]
 
 A step is one full estimate (preconditioner build + s-probe Lanczos +
 multishift solves + Hutchinson mean) -- the reference's timer scope
@@ -17,11 +21,13 @@ multishift solves + Hutchinson mean) -- the reference's timer scope
   GPU, regenerates the reference's probe / sketch streams on the GPU, runs the
   estimate and reads the result back.
 * ``roofline``: the dominant kernel (the K x block product, Lanczos shape),
-  timed live with CUDA events; algorithmic bytes = 4 n^2 (K) + 4 n s (operand)
-  + 8 n s (result) per launch.
+  timed live with CUDA events.  float64: FP64 tensor cores (DMMA), algorithmic
+  flops 2 n^2 s per launch against the measured DMMA peak; float32 stored:
+  HBM, algorithmic bytes 4 n^2 (K) + 4 n s (operand) + 8 n s (result).
 * ``cpu_baseline``: the oracle port (float64 numpy restatement of the
-  reference, per-probe loop like the reference) on this host's cores, one
-  estimate of the same workload.
+  reference, per-probe loop like the reference) on this host's cores.  The
+  reference's dense K does not fit host RAM at n = 65536, so the
+  sample is the same configuration at n = 16384, extrapolated by n^2 (labelled).
 * ``--impl reference``: that CPU implementation is the timed arm.
 
 Multi-GPU (torchrun, one process per GPU): by default the rows of K and of every
@@ -60,7 +66,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--dtype", choices=["fp32", "fp64"], default=None)
     ap.add_argument("--algorithm", choices=["r1", "r3", "r5"], default=None)
@@ -69,6 +75,9 @@ def parse():
     ap.add_argument("--no-concurrent", action="store_true", help="skip the informational concurrent-estimates run")
     ap.add_argument("--mode", choices=["sharded", "replicas"], default="sharded",
                     help="multi-GPU: row-shard one estimate (default) or run independent replicas")
+    ap.add_argument("--no-extra", action="store_true", help="skip the extra config-3 fp32 measurement")
+    ap.add_argument("--cpu-sample-n", type=int, default=16384,
+                    help="n of the CPU sample (extrapolated by n^2 to the workload's n)")
     return ap.parse_args()
 
 
@@ -174,25 +183,25 @@ def barrier(world):
         dist.barrier()
 
 
-def ncu_traffic(name="kv_c2_m32"):
-    """DRAM bytes (read + write) per launch of the dominant kernel from the newest
-    committed ncu --set full summary (profiles/*_kv_ncu.json, scripts/summarize_profiles.py)."""
-    files = sorted((ROOT / "profiles").glob("*_kv_ncu.json"), key=lambda p: p.stat().st_mtime)
-    for f in reversed(files):
-        try:
-            rec = json.loads(f.read_text()).get(name)
-        except Exception:
-            continue
-        if rec and "dram_bytes_total" in rec:
-            return rec["dram_bytes_total"], f.name
+def ncu_traffic(key):
+    """DRAM bytes (read + write) per launch of the dominant kernel at exactly this shape, from the
+    committed ncu --set full summary (profiles/traffic.json: {key: {"dram_bytes": B, "source": f}}).
+    The key names the kernel, dtype, path and shape; no entry -> None (never a neighbour's number)."""
+    f = ROOT / "profiles" / "traffic.json"
+    try:
+        rec = json.loads(f.read_text()).get(key)
+    except Exception:
+        return None, None
+    if rec and "dram_bytes" in rec:
+        return rec["dram_bytes"], rec.get("source", f.name)
     return None, None
 
 
-def workload_for(args):
+def workload_for(args, dtype=None):
     from paper_2405_03474_b200.workloads import baseline
 
-    wl = baseline(args.config, n=args.n, algorithm=args.algorithm, dtype=args.dtype)
-    return wl
+    dtype = dtype or args.dtype or ("fp64" if args.config == 3 else None)
+    return baseline(args.config, n=args.n, algorithm=args.algorithm, dtype=dtype)
 
 
 # --------------------------------------------------------------------------- CPU (oracle port)
@@ -210,6 +219,22 @@ def cpu_estimate(wl, threads: int):
                         probe_kind=cfg.probe_kind, k=cfg.precond.rank, q=cfg.precond.num_iters, seed=cfg.seed,
                         per_probe=True)
     return time.perf_counter() - t0, est
+
+
+def cpu_sample(wl, args):
+    """(workload to time on the CPU, factor from its seconds to the full workload's seconds, label)."""
+    from paper_2405_03474_b200.workloads import baseline
+
+    cfg = wl.config
+    ns = args.cpu_sample_n
+    if wl.n <= ns:
+        return replace(wl, config=replace(cfg, dtype="fp64")), 1.0, "the full workload"
+    idx = int(wl.name.replace("config", ""))
+    sw = baseline(idx, n=ns, algorithm=cfg.algorithm, dtype="fp64", rank=cfg.precond.rank,
+                  num_probes=cfg.num_probes)
+    f = (wl.n / ns) ** 2
+    return sw, f, (f"the same configuration at n = {ns} (the reference's dense float64 K does not fit host RAM "
+                   f"at n = {wl.n}), seconds extrapolated by (n / {ns})^2 = {f:.0f}: EXTRAPOLATED")
 
 
 def cpu_model():
@@ -243,23 +268,23 @@ def run_reference(args):
     os.environ["OPENBLAS_NUM_THREADS"] = str(threads)
     wl = workload_for(args)
     arm_config = workload_config(wl)
-    cfg = replace(wl.config, dtype="fp64")
-    wl = replace(wl, config=cfg)
+    sw, factor, label = cpu_sample(wl, args)
     warm = min(args.warmup, 1)
-    steps = max(1, min(args.steps, 3))
+    steps = max(1, min(args.steps, 2 if factor > 1 else 3))
     for _ in range(warm):
-        cpu_estimate(wl, threads)
-    times = [cpu_estimate(wl, threads)[0] for _ in range(steps)]
+        cpu_estimate(sw, threads)
+    times = [cpu_estimate(sw, threads)[0] * factor for _ in range(steps)]
     total = sum(times)
     v = steps / total
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
         "warmup": warm, "ms_per_step": 1e3 * total / steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {**arm_config, "note": "the reference has no fp32 mode: this CPU arm computes in float64"},
+        "config": arm_config,
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{steps} full estimate(s) of the workload, oracle port (numpy/OpenBLAS, "
-                                   f"per-probe loop), K build excluded", "cpu": cpu_model()},
+                         "sample": f"{steps} estimate(s) of {label}; oracle port (numpy/OpenBLAS float64, "
+                                   f"per-probe loop like the reference), K build excluded",
+                         "cpu": cpu_model()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -335,29 +360,7 @@ def run_ours(args):
     k1.record(stream)
     torch.cuda.synchronize()
     kv_ms = k0.elapsed_time(k1) / reps
-    alg_bytes = es * rows * n + 4 * n * s + 8 * rows * s
-    hbm_peak, _, peak_kind = load_peaks()
-    traffic, traffic_src = (ncu_traffic() if (args.config == 2 and world == 1 and args.dtype in (None, "fp32"))
-                            else (None, None))
-    achieved = alg_bytes / (kv_ms * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                "traffic": traffic, "traffic_source": traffic_src,
-                "kernel": f"kv_product (Lanczos shape m=s, {rows} rows of K)", "kernel_ms": kv_ms,
-                "alg_bytes": alg_bytes, "peak_source": peak_kind}
-    pipe = load_pipe_peaks()
-    if wl.path == "on_the_fly" or cfg.dtype == "fp64":
-        # no stored K (on the fly) or an FP64-pipe-bound product (fp64, 8 flop/B > the DFMA ridge):
-        # the bound is a compute pipe, SURVEY.md §8(d)
-        useful = 2.0 * rows * n * s
-        if cfg.dtype == "fp64":
-            kind, work, peak, src = "fp64", useful, pipe.get("dfma_tflops", 36.36), "profiles/r01_pipe_peaks.json dfma"
-        else:   # 3xTF32 tensor-core MMAs: three products per useful one
-            kind, work = "tensor", 3.0 * useful
-            peak, src = pipe.get("tf32_ts_n128", {}).get("tflops", 1115.0), "profiles/r01_pipe_peaks.json tf32 N=128"
-        ach = work / (kv_ms * 1e-3) / 1e12
-        roofline = {"bound": kind, "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                    "traffic": None, "kernel": f"kv_product ({wl.path}, m=s={s}, {rows} rows)", "kernel_ms": kv_ms,
-                    "alg_flops": work, "useful_flops": useful, "peak_source": src}
+    roofline = roofline_for(wl, cfg, rows, n, s, kv_ms, world)
 
     # ---- end to end through the public API (host buffers, pinned)
     e2e = None
@@ -396,9 +399,10 @@ def run_ours(args):
         del keep
 
     # ---- informational: independent estimates from several host threads, each with its own
-    # handle / stream / K copy (the harness's run_sweep(jobs=J)); not the headline value
+    # handle / stream / K copy (the harness's run_sweep(jobs=J)); not the headline value.  Only
+    # where J copies of K fit in HBM.
     concurrent = None
-    if world == 1 and not args.no_concurrent:
+    if world == 1 and not args.no_concurrent and 4 * es * n * n < 0.5 * torch.cuda.get_device_properties(0).total_memory:
         import threading
 
         J, per = 4, max(2, args.steps // 2)
@@ -434,26 +438,156 @@ def run_ours(args):
     }
     if concurrent is not None:
         line["concurrent"] = concurrent
+    line["parity"] = parity_vs_golden(wl, est.value)
+    del R
+    torch.cuda.empty_cache()
+
+    # ---- extra: the same configuration in BASELINE's stated fp32 (stored fp32 K, 3xTF32 products)
+    if args.config == 3 and cfg.dtype == "fp64" and not args.no_extra:
+        line["extra_fp32"] = extra_fp32(args, rld, world, sharded, per_step)
 
     # ---- CPU baseline (rank 0, N = 1 only)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        secs, oest = cpu_estimate(wl, threads)
-        line["cpu_baseline"] = {"value": 1.0 / secs, "unit": UNIT, "cores": threads, "kind": "port",
-                                "sample": "1 full estimate of the same workload in float64 (oracle port, "
-                                          "numpy/OpenBLAS, per-probe loop), K build excluded",
-                                "cpu": cpu_model()}
-        line["parity"] = {"oracle_value": oest.value, "gpu_value": est.value,
-                          "rel_diff": abs(est.value - oest.value) / abs(oest.value),
-                          "tol": 1e-4 if cfg.dtype == "fp32" else 1e-6}
+        sw, factor, label = cpu_sample(wl, args)
+        secs, oest = cpu_estimate(sw, threads)
+        line["cpu_baseline"] = {"value": 1.0 / (secs * factor), "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": f"1 estimate of {label}; oracle port (numpy/OpenBLAS float64, per-probe "
+                                          f"loop like the reference), K build excluded",
+                                "sample_seconds": secs, "cpu": cpu_model()}
     if rank == 0:
         print(json.dumps(line), flush=True)
     barrier(world)
     return 0
 
 
+def roofline_for(wl, cfg, rows, n, s, kv_ms, world):
+    """Roofline of the dominant kernel (K x block, Lanczos shape m = s), SURVEY.md §8(d)."""
+    es = 4 if cfg.dtype == "fp32" else 8
+    pipe = load_pipe_peaks()
+    key = f"kv_product|{cfg.dtype}|{wl.path}|n={n}|rows={rows}|m={s}"
+    traffic, traffic_src = ncu_traffic(key)
+    if wl.path == "stored" and cfg.dtype == "fp32":
+        alg_bytes = es * rows * n + 4 * n * s + 8 * rows * s
+        hbm_peak, _, peak_kind = load_peaks()
+        achieved = alg_bytes / (kv_ms * 1e-3) / 1e9
+        return {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                "traffic": traffic, "traffic_source": traffic_src, "traffic_key": key,
+                "kernel": f"kv_product (tcgen05 3xTF32, Lanczos shape m=s={s}, {rows} rows of K)", "kernel_ms": kv_ms,
+                "alg_bytes": alg_bytes, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}
+    useful = 2.0 * rows * n * s
+    if cfg.dtype == "fp64":
+        # FP64 tensor cores (DMMA, kv_dmma.cu): 2 n^2 s flops per product (8 flop/B at s = 32:
+        # above the FP64 ridge, so the FP64 pipe bounds it, not HBM)
+        kind, work = "fp64-tensor", useful
+        if "dmma_tflops" in pipe:
+            peak, src = pipe["dmma_tflops"], "profiles/r02_pipe_peaks.json dmma (measured)"
+        else:
+            peak, src = pipe.get("dfma_tflops", 36.36), "profiles/r01_pipe_peaks.json dfma (measured)"
+        alg_bytes = es * rows * n + 8 * n * s + 8 * rows * s
+    else:   # on the fly, 3xTF32 tensor-core MMAs: three products per useful one
+        kind, work = "tensor", 3.0 * useful
+        peak, src = pipe.get("tf32_ts_n128", {}).get("tflops", 1115.0), "pipe peaks tf32 N=128 (measured)"
+        alg_bytes = None
+    ach = work / (kv_ms * 1e-3) / 1e12
+    return {"bound": kind, "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+            "traffic": traffic, "traffic_source": traffic_src, "traffic_key": key, "alg_bytes": alg_bytes,
+            "kernel": f"kv_product ({wl.path}, {cfg.dtype}, m=s={s}, {rows} rows)", "kernel_ms": kv_ms,
+            "alg_flops": work, "useful_flops": useful, "peak_source": src}
+
+
+def parity_vs_golden(wl, value):
+    """The estimate against the committed float64 oracle value of the same workload (full-size
+    configs 3-5: tests/golden/golden_large.json, matrix-free oracle; configs 1-2: golden.json,
+    the unmodified reference)."""
+    g = ROOT / "tests" / "golden"
+    cfg = wl.config
+    ref = None
+    try:
+        if wl.n == {1: 2048, 2: 16384}.get(int(wl.name[-1])):
+            for c in json.loads((g / "golden.json").read_text()):
+                if c["name"] == f"{wl.name}_{cfg.algorithm}":
+                    ref, src = c["value"], "tests/golden/golden.json (unmodified reference)"
+        else:
+            c = json.loads((g / "golden_large.json").read_text()).get(f"{wl.name}_full")
+            if (c and c["n"] == wl.n and c["rank"] == cfg.precond.rank and c["num_probes"] == cfg.num_probes
+                    and c["algorithm"] == cfg.algorithm and c["lanczos_iters"] == cfg.lanczos_iters
+                    and c["num_iters"] == cfg.precond.num_iters):
+                ref, src = c["value"], "tests/golden/golden_large.json (matrix-free float64 oracle)"
+    except Exception:
+        ref = None
+    if ref is None:
+        return None
+    return {"oracle_value": ref, "gpu_value": value, "rel_diff": abs(value - ref) / abs(ref),
+            "tol": 1e-4 if cfg.dtype == "fp32" else 1e-6, "source": src}
+
+
+def extra_fp32(args, rld, world, sharded, per_step):
+    """Config 3 in fp32 (BASELINE's stated precision): stored fp32 K, 3xTF32 tensor-core products;
+    3 timed estimates after 2 warm-ups, CUDA events, max over ranks."""
+    import torch
+
+    wl = workload_for(args, dtype="fp32")
+    cfg = wl.config
+    R = rld.ResidentMatrix(rld.KernelMatrix(wl.spec, wl.points), dtype="fp32", path=wl.path, shard=sharded)
+    st = torch.cuda.ExternalStream(R.sess.handle.stream)
+    for _ in range(2):
+        est = R.estimate(cfg)
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    K = 3
+    for _ in range(K):
+        est = R.estimate(cfg)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), world)
+    from paper_2405_03474_b200.parallel import shard_bounds
+
+    r0, r1 = shard_bounds(wl.n, world, int(os.environ.get("RANK", "0"))) if sharded else (0, wl.n)
+    V = torch.randn(cfg.num_probes, wl.n, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        R.kv_apply(V)
+    torch.cuda.synchronize()
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record(st)
+    for _ in range(10):
+        R.kv_apply(V)
+    k1.record(st)
+    torch.cuda.synchronize()
+    out = {"value": per_step * K / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms / K, "dtype": "f32",
+           "config": workload_config(wl, world, sharded),
+           "roofline": roofline_for(wl, cfg, r1 - r0, wl.n, cfg.num_probes, k0.elapsed_time(k1) / 10, world),
+           "parity": parity_vs_golden(wl, est.value)}
+    del R
+    torch.cuda.empty_cache()
+    return out
+
+
+def spawn_ranks(args):
+    """`--gpus N` outside torchrun: launch N ranks with torch.distributed.run on this node (one
+    process per GPU, NCCL), after checking N GPUs are visible.  Rank 0's JSON line passes through."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but only {have} CUDA device(s) visible"}), flush=True)
+        return 2
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define RLD_ABI_VERSION 3
+#define RLD_ABI_VERSION 4
 
 typedef enum rld_status {
   RLD_OK = 0,
@@ -75,14 +75,22 @@ typedef enum rld_estimator {
 } rld_estimator;
 
 typedef struct rld_handle rld_handle;
+typedef struct rld_vgroup rld_vgroup;   /* "virtual shards": G ranks of one process (rld_vgroup_create) */
 
-/* One process drives one GPU; `world_size` processes row-shard K. */
+typedef enum rld_comm_kind {
+  RLD_COMM_NCCL = 0,     /* one process (or thread) per GPU, NCCL over NVLink / NVSwitch */
+  RLD_COMM_THREADS = 1   /* G handles of one process, one host thread each, host-barrier exchange
+                            through device staging slots: runs the row-sharded path on one GPU */
+} rld_comm_kind;
+
+/* `world_size` ranks row-shard K; world_size 1 = single GPU, no collectives. */
 typedef struct rld_device_set {
   int32_t device;       /* CUDA ordinal */
   int32_t rank;         /* row-shard index, 0 <= rank < world_size */
   int32_t world_size;   /* 1 = single GPU (no NCCL) */
-  int32_t reserved;
-  const void* nccl_id;  /* 128-byte ncclUniqueId shared by all ranks (NULL if world_size == 1) */
+  int32_t comm_kind;    /* rld_comm_kind (was `reserved`, 0 = NCCL) */
+  const void* nccl_id;  /* RLD_COMM_NCCL: 128-byte ncclUniqueId shared by all ranks (NULL if world_size == 1) */
+  rld_vgroup* group;    /* RLD_COMM_THREADS: the group every rank's handle joins */
 } rld_device_set;
 
 /* The matrix: a dense K (the reference's only input, src/estimators.py:77) or the
@@ -164,6 +172,11 @@ int rld_nccl_unique_id(void* out);
 
 /* Bind a handle to one GPU (and, for world_size > 1, to an NCCL communicator). */
 int rld_create(const rld_device_set* devices, rld_handle** out);
+/* Virtual-shard group for RLD_COMM_THREADS: create once, pass to every rank's rld_create, destroy
+ * after every handle of the group is destroyed.  No reference counterpart (the reference has no
+ * parallel path); test / single-GPU plumbing of the row-sharded estimate. */
+int rld_vgroup_create(int32_t world_size, rld_vgroup** out);
+void rld_vgroup_destroy(rld_vgroup* group);
 void rld_destroy(rld_handle* h);
 const char* rld_last_error(const rld_handle* h);
 

@@ -34,19 +34,20 @@ PRECOND_RAND_SVD, PRECOND_IDENTITY, PRECOND_DIAGONAL = 0, 1, 2
 PRECOND_RAND_SVD_SCALED, PRECOND_PARTIAL_CHOLESKY, PRECOND_PARTIAL_CHOLESKY_SCALED = 3, 4, 5
 PRECOND_TRUNC_SVD, PRECOND_TRUNC_SVD_SCALED, PRECOND_RANK_ONE = 6, 7, 8
 ESTIMATOR_RSTAR, ESTIMATOR_SLQ = 0, 1
-ABI_VERSION = 3
+ABI_VERSION = 4
+COMM_NCCL, COMM_THREADS = 0, 1
 
 # every symbol include/rld.h declares
 EXPORTS = (
     "rld_abi_version", "rld_create", "rld_destroy", "rld_last_error", "rld_logdet", "rld_prepare",
     "rld_logdet_resident", "rld_build_covariance", "rld_kv_apply", "rld_rademacher", "rld_exact_logdet", "rld_dense_cholesky", "rld_dense_eigh",
-    "rld_nccl_unique_id", "rld_stream", "rld_normal", "rld_chi_radii",
+    "rld_nccl_unique_id", "rld_stream", "rld_normal", "rld_chi_radii", "rld_vgroup_create", "rld_vgroup_destroy",
 )
 
 
 class DeviceSet(C.Structure):
-    _fields_ = [("device", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32), ("reserved", C.c_int32),
-                ("nccl_id", C.c_void_p)]
+    _fields_ = [("device", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32), ("comm_kind", C.c_int32),
+                ("nccl_id", C.c_void_p), ("group", C.c_void_p)]
 
 
 class Problem(C.Structure):
@@ -115,8 +116,11 @@ def load() -> C.CDLL:
         lib.rld_nccl_unique_id.argtypes = [C.c_void_p]
         lib.rld_stream.argtypes = [H]
         lib.rld_stream.restype = C.c_void_p
+        lib.rld_vgroup_create.argtypes = [C.c_int32, C.POINTER(C.c_void_p)]
+        lib.rld_vgroup_destroy.argtypes = [C.c_void_p]
+        lib.rld_vgroup_destroy.restype = None
         for name in EXPORTS:
-            if name not in ("rld_abi_version", "rld_destroy", "rld_last_error", "rld_stream"):
+            if name not in ("rld_abi_version", "rld_destroy", "rld_last_error", "rld_stream", "rld_vgroup_destroy"):
                 getattr(lib, name).restype = C.c_int
         if lib.rld_abi_version() != ABI_VERSION:
             raise RuntimeError("librld.so ABI version mismatch")
@@ -127,11 +131,15 @@ def load() -> C.CDLL:
 class Handle:
     """One GPU (one row shard) bound to a librld handle."""
 
-    def __init__(self, device: int = 0, rank: int = 0, world_size: int = 1, nccl_id: bytes | None = None):
+    def __init__(self, device: int = 0, rank: int = 0, world_size: int = 1, nccl_id: bytes | None = None,
+                 group: "VirtualGroup | None" = None):
         self.lib = load()
         self._h = C.c_void_p()
         self._id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
-        ds = DeviceSet(device, rank, world_size, 0, C.cast(self._id, C.c_void_p) if self._id is not None else None)
+        self.group = group   # keeps the group alive while this handle uses it
+        ds = DeviceSet(device, rank, world_size, COMM_THREADS if group is not None else COMM_NCCL,
+                       C.cast(self._id, C.c_void_p) if self._id is not None else None,
+                       group.ptr if group is not None else None)
         self.check(self.lib.rld_create(C.byref(ds), C.byref(self._h)), "rld_create")
         self.device, self.rank, self.world_size = device, rank, world_size
 
@@ -163,6 +171,33 @@ class Handle:
         if rc == RLD_OK:
             return
         raise_status(rc, f"{what}: {self.last_error() if self._h else ''}")
+
+
+class VirtualGroup:
+    """rld_vgroup: G ranks of one process sharing host-barrier collectives (RLD_COMM_THREADS)."""
+
+    def __init__(self, world_size: int):
+        self.lib = load()
+        self._g = C.c_void_p()
+        rc = self.lib.rld_vgroup_create(int(world_size), C.byref(self._g))
+        if rc != RLD_OK:
+            raise_status(rc, "rld_vgroup_create")
+        self.world_size = int(world_size)
+
+    @property
+    def ptr(self):
+        return self._g
+
+    def close(self):
+        if self._g:
+            self.lib.rld_vgroup_destroy(self._g)
+            self._g = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def raise_status(rc: int, msg: str):

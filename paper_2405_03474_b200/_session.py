@@ -58,10 +58,11 @@ def hbm_bytes(device: int) -> int:
 
 
 class Session:
-    def __init__(self, device: int | None = None, rank: int = 0, world_size: int = 1, nccl_id: bytes | None = None):
+    def __init__(self, device: int | None = None, rank: int = 0, world_size: int = 1, nccl_id: bytes | None = None,
+                 group: "N.VirtualGroup | None" = None):
         if device is None:
             _, _, device = dist_world()
-        self.handle = N.Handle(device, rank, world_size, nccl_id)
+        self.handle = N.Handle(device, rank, world_size, nccl_id, group)
         self.lib = self.handle.lib
         self.rank, self.world_size, self.device = rank, world_size, device
 
@@ -176,21 +177,26 @@ _local = threading.local()
 class worker_session:
     """Context manager: this thread's calls use their own handle (own stream, workspace and
     resident problem) instead of the process-wide one, so independent estimates can run
-    concurrently from several host threads (``harness.run_sweep(jobs=J)``).  One GPU only."""
+    concurrently from several host threads (``harness.run_sweep(jobs=J)``).  One GPU only.
+    ``sess=`` binds an existing session instead (a virtual-shard rank, ``parallel.py``); it is
+    then not closed on exit."""
 
-    def __init__(self, device: int | None = None):
+    def __init__(self, device: int | None = None, sess: "Session | None" = None):
         self.device = device
-        self.sess = None
+        self.sess = sess
+        self.own = sess is None
 
     def __enter__(self):
-        self.sess = Session(self.device)
+        if self.sess is None:
+            self.sess = Session(self.device)
         self.prev = getattr(_local, "sess", None)
         _local.sess = self.sess
         return self.sess
 
     def __exit__(self, *exc):
         _local.sess = self.prev
-        self.sess.handle.close()
+        if self.own:
+            self.sess.handle.close()
         return False
 
 

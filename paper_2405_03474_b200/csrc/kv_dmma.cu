@@ -24,6 +24,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <climits>
 #include <mutex>
 
 #include "rld_internal.cuh"
@@ -41,7 +42,7 @@ constexpr int DM_THREADS = (DM_MMA_WARPS + 1) * 32;
 
 template <int BM, int BN>
 struct DmmaShape {
-  static constexpr int WARPS_N = BN >= 64 ? 2 : 1;
+  static constexpr int WARPS_N = (BN >= 64 && BN % 16 == 0) ? 2 : 1;
   static constexpr int WARPS_M = DM_MMA_WARPS / WARPS_N;
   static constexpr int WM = BM / WARPS_M;
   static constexpr int WN = BN / WARPS_N;
@@ -294,12 +295,25 @@ void gemm_nt_f64(const double* A, int64_t lda, int64_t p, const double* B, int64
     return;
   }
   if (!gemm_nt_f64_ok(A, lda, B, ldb)) fail(RLD_ERR_NOT_SUPPORTED, "gemm_nt_f64 needs 16-byte aligned rows");
-  if (q <= 32)
-    launch_nt<128, 32>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st);
-  else if (q <= 64 || p <= 64)
-    launch_nt<128, 64>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st);
-  else
-    launch_nt<128, 128>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st);
+  // column-tile width with the least padding of q (ties: the wider tile, fewer A re-reads)
+  static const int widths[] = {128, 96, 64, 48, 32, 16};
+  int bn = 128;
+  int64_t best = INT64_MAX;
+  for (int w : widths) {
+    const int64_t padded = ceil_div(q, w) * w;
+    if (padded < best) {
+      best = padded;
+      bn = w;
+    }
+  }
+  switch (bn) {
+    case 128: launch_nt<128, 128>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st); break;
+    case 96: launch_nt<128, 96>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st); break;
+    case 64: launch_nt<128, 64>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st); break;
+    case 48: launch_nt<128, 48>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st); break;
+    case 32: launch_nt<128, 32>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st); break;
+    default: launch_nt<128, 16>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st); break;
+  }
 }
 
 }  // namespace rld

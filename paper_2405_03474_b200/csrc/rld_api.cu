@@ -15,6 +15,7 @@
 #include <cstring>
 #include <new>
 
+#include "comm.cuh"
 #include "rld_internal.cuh"
 #include "rld_kernels.cuh"
 
@@ -128,7 +129,7 @@ struct rld_handle {
   cudaStream_t st = nullptr;
   cublasHandle_t cublas = nullptr;
   cusolverDnHandle_t solver = nullptr;
-  ncclComm_t comm = nullptr;
+  std::unique_ptr<rld::Comm> comm;   // world > 1: NCCL or virtual shards (comm.cu)
   std::string last_error;
   rld::Resident res;
   rld::Work wk;
@@ -173,8 +174,7 @@ void set_device(rld_handle* h) { RLD_CUDA(cudaSetDevice(h->device)); }
 // --- collectives (row shards).  world == 1: no-ops. --------------------------
 void allreduce_sum(rld_handle* h, double* buf, int64_t count) {
   if (h->world == 1 || count <= 0) return;
-  ncclResult_t r = ncclAllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, h->comm, h->st);
-  if (r != ncclSuccess) fail(RLD_ERR_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+  h->comm->allreduce_sum(buf, count, h->st);
 }
 
 // Bitwise OR of the host copies of the status flags over ranks.  Flags raised on
@@ -187,8 +187,7 @@ void allreduce_flags(rld_handle* h, int* hflags, int count) {
   DevBuf& d = h->wk.flagbuf;
   d.reserve(sizeof(int) * bits.size());
   RLD_CUDA(cudaMemcpyAsync(d.ptr, bits.data(), sizeof(int) * bits.size(), cudaMemcpyHostToDevice, h->st));
-  ncclResult_t r = ncclAllReduce(d.ptr, d.ptr, bits.size(), ncclInt32, ncclMax, h->comm, h->st);
-  if (r != ncclSuccess) fail(RLD_ERR_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+  h->comm->allreduce_max(d.as<int>(), (int64_t)bits.size(), h->st);
   RLD_CUDA(cudaMemcpyAsync(bits.data(), d.ptr, sizeof(int) * bits.size(), cudaMemcpyDeviceToHost, h->st));
   RLD_CUDA(cudaStreamSynchronize(h->st));
   for (int i = 0; i < count; ++i) {
@@ -363,8 +362,7 @@ void gather_rows(rld_handle* h, const double* local, int64_t m, double* full) {
   if (r.rows > 0)
     RLD_CUDA(cudaMemcpy2DAsync(snd, sizeof(double) * L, local, sizeof(double) * r.rows, sizeof(double) * r.rows, m,
                                cudaMemcpyDeviceToDevice, h->st));
-  ncclResult_t e = ncclAllGather(snd, rcv, (size_t)(m * L), ncclDouble, h->comm, h->st);
-  if (e != ncclSuccess) fail(RLD_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(e));
+  h->comm->allgather(snd, rcv, m * L, h->st);
   relayout_gathered(rcv, h->world, m, L, r.n, full, h->st);
 }
 
@@ -493,11 +491,12 @@ bool cholqr_gemm_enabled() {
   return on;
 }
 
-// Householder QR of Y (col-major n x w, single shard), Q with positive R
-// diagonal -- the same Q CGS2 produces -- and the reference's rank test
-// |R_ii| < rtol |Y_i| (src/linalg.py:177-178).
+// Householder QR of Y (col-major n x w, local rows), Q with positive R diagonal -- the same Q
+// CGS2 produces -- and the reference's rank test |R_ii| < rtol |Y_i| (src/linalg.py:177-178).
+// Row shards (world > 1): TSQR -- local Householder QR Y_g = Q_g R_g, all-gather of the R_g,
+// one replicated QR of the stacked [R_0; ...; R_{G-1}] = Q_s R, local Q = Q_g Q_s[g] -- so the
+// rank test sees the global R, exactly as on one GPU (up to rounding).
 void qr_householder(rld_handle* h, int64_t n, int w, double* Y, double rtol, int* flags) {
-  if (h->world != 1) fail(RLD_ERR_RANK_DEFICIENT, "ill-conditioned sketch needs Householder QR (single GPU only)");
   Work& wk = h->wk;
   wk.gdiag.reserve(sizeof(double) * 2 * w);
   wk.G.reserve(sizeof(double) * std::max<int64_t>((int64_t)w * w, 2 * w));
@@ -507,12 +506,47 @@ void qr_householder(rld_handle* h, int64_t n, int w, double* Y, double rtol, int
   int* info = wk.ints.as<int>() + 1;
   rows_dot(w, n, Y, n, Y, n, norms2, wk.scratch, h->st, nullptr);
   int l1 = 0, l2 = 0;
+  if (h->world == 1) {
+    RLD_CUSOLVER(cusolverDnDgeqrf_bufferSize(h->solver, (int)n, w, Y, (int)n, &l1));
+    RLD_CUSOLVER(cusolverDnDorgqr_bufferSize(h->solver, (int)n, w, w, Y, (int)n, tau, &l2));
+    wk.solver_work.reserve(sizeof(double) * std::max(std::max(l1, l2), 1));
+    RLD_CUSOLVER(cusolverDnDgeqrf(h->solver, (int)n, w, Y, (int)n, tau, wk.solver_work.as<double>(), l1, info));
+    householder_check(w, Y, n, norms2, rtol, sgn, flags, h->st);
+    RLD_CUSOLVER(cusolverDnDorgqr(h->solver, (int)n, w, w, Y, (int)n, tau, wk.solver_work.as<double>(), l2, info));
+    scale_cols_colmajor(n, w, n, sgn, Y, h->st);
+    return;
+  }
+  if (n < w) fail(RLD_ERR_NOT_SUPPORTED, "TSQR needs at least w = " + std::to_string(w) + " rows per shard");
+  allreduce_sum(h, norms2, w);
+  const int G = h->world;
+  const int64_t gw = (int64_t)G * w, ww = (int64_t)w * w;
+  wk.gsend.reserve(sizeof(double) * ww);
+  wk.grecv.reserve(sizeof(double) * ww * G);
+  wk.scratch2.reserve(sizeof(double) * std::max<int64_t>(gw * w, n * w));
+  wk.qtile.reserve(sizeof(double) * gw * w);
+  double* S = wk.qtile.as<double>();
+  // local factor
   RLD_CUSOLVER(cusolverDnDgeqrf_bufferSize(h->solver, (int)n, w, Y, (int)n, &l1));
   RLD_CUSOLVER(cusolverDnDorgqr_bufferSize(h->solver, (int)n, w, w, Y, (int)n, tau, &l2));
-  wk.solver_work.reserve(sizeof(double) * std::max(std::max(l1, l2), 1));
-  RLD_CUSOLVER(cusolverDnDgeqrf(h->solver, (int)n, w, Y, (int)n, tau, wk.solver_work.as<double>(), l1, info));
-  householder_check(w, Y, n, norms2, rtol, sgn, flags, h->st);
-  RLD_CUSOLVER(cusolverDnDorgqr(h->solver, (int)n, w, w, Y, (int)n, tau, wk.solver_work.as<double>(), l2, info));
+  int l3 = 0, l4 = 0;
+  RLD_CUSOLVER(cusolverDnDgeqrf_bufferSize(h->solver, (int)gw, w, S, (int)gw, &l3));
+  RLD_CUSOLVER(cusolverDnDorgqr_bufferSize(h->solver, (int)gw, w, w, S, (int)gw, tau, &l4));
+  wk.solver_work.reserve(sizeof(double) * std::max(std::max(std::max(l1, l2), std::max(l3, l4)), 1));
+  double* work = wk.solver_work.as<double>();
+  RLD_CUSOLVER(cusolverDnDgeqrf(h->solver, (int)n, w, Y, (int)n, tau, work, std::max(l1, l2), info));
+  copy_upper(w, Y, n, wk.gsend.as<double>(), h->st);
+  RLD_CUSOLVER(cusolverDnDorgqr(h->solver, (int)n, w, w, Y, (int)n, tau, work, std::max(l1, l2), info));
+  // stacked R factors, replicated QR
+  h->comm->allgather(wk.gsend.as<double>(), wk.grecv.as<double>(), ww, h->st);
+  relayout_gathered(wk.grecv.as<double>(), G, w, w, gw, S, h->st);   // (G w) x w column-major
+  RLD_CUSOLVER(cusolverDnDgeqrf(h->solver, (int)gw, w, S, (int)gw, tau, work, std::max(l3, l4), info));
+  householder_check(w, S, gw, norms2, rtol, sgn, flags, h->st);
+  RLD_CUSOLVER(cusolverDnDorgqr(h->solver, (int)gw, w, w, S, (int)gw, tau, work, std::max(l3, l4), info));
+  // Q_local = Q_g Q_s[g], then the sign fix
+  double* out = wk.scratch2.as<double>();
+  RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)n, w, w, &ONE, Y, (int)n, S + (int64_t)h->rank * w,
+                         (int)gw, &ZERO, out, (int)n));
+  copy_doubles(n * (int64_t)w, out, Y, h->st);
   scale_cols_colmajor(n, w, n, sgn, Y, h->st);
 }
 
@@ -677,8 +711,7 @@ void global_argmax(rld_handle* h, const double* d, double* pv) {
   wk.gsend.reserve(sizeof(double) * 2);
   wk.grecv.reserve(sizeof(double) * 2 * h->world);
   argmax_first(r.rows, d, r.row0, wk.gsend.as<double>(), wk.scratch, h->st);
-  ncclResult_t e = ncclAllGather(wk.gsend.ptr, wk.grecv.ptr, 2, ncclDouble, h->comm, h->st);
-  if (e != ncclSuccess) fail(RLD_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(e));
+  h->comm->allgather(wk.gsend.as<double>(), wk.grecv.as<double>(), 2, h->st);
   pick_first_max(h->world, wk.grecv.as<double>(), pv, h->st);   // ranks hold increasing row ranges
 }
 
@@ -1214,6 +1247,7 @@ int guarded(rld_handle* h, F&& f) {
     return RLD_OK;
   } catch (const Error& e) {
     if (h) h->last_error = e.msg;
+    if (h && h->comm) h->comm->abort(e.msg);   // the other ranks fail instead of waiting on this one
     return e.code;
   } catch (const std::bad_alloc&) {
     if (h) h->last_error = "host allocation failed";
@@ -1266,11 +1300,16 @@ int rld_create(const rld_device_set* ds, rld_handle** out) {
     RLD_CUDA(cudaEventCreateWithFlags(&h->efork, cudaEventDisableTiming));
     RLD_CUDA(cudaEventCreateWithFlags(&h->ejoin, cudaEventDisableTiming));
     if (h->world > 1) {
-      if (!ds || !ds->nccl_id) fail(RLD_ERR_INVALID_ARGUMENT, "nccl_id required for world_size > 1");
-      ncclUniqueId id;
-      memcpy(&id, ds->nccl_id, sizeof id);
-      ncclResult_t r = ncclCommInitRank(&h->comm, h->world, id, h->rank);
-      if (r != ncclSuccess) fail(RLD_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+      if (ds->comm_kind == RLD_COMM_THREADS) {
+        if (!ds->group) fail(RLD_ERR_INVALID_ARGUMENT, "group required for RLD_COMM_THREADS");
+        h->comm = make_thread_comm(ds->group, h->rank);
+        if (h->comm->world != h->world) fail(RLD_ERR_INVALID_ARGUMENT, "group size differs from world_size");
+      } else if (ds->comm_kind == RLD_COMM_NCCL) {
+        if (!ds->nccl_id) fail(RLD_ERR_INVALID_ARGUMENT, "nccl_id required for world_size > 1");
+        h->comm = make_nccl_comm(ds->nccl_id, h->rank, h->world);
+      } else {
+        fail(RLD_ERR_INVALID_ARGUMENT, "unknown comm_kind");
+      }
     }
   });
   if (rc != RLD_OK) {
@@ -1289,7 +1328,7 @@ void rld_destroy(rld_handle* h) {
   cudaSetDevice(h->device);
   if (h->st) cudaStreamSynchronize(h->st);
   h->res.Kbuf.release();
-  if (h->comm) ncclCommDestroy(h->comm);
+  h->comm.reset();
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
   if (h->st2) cudaStreamSynchronize(h->st2), cudaStreamDestroy(h->st2);

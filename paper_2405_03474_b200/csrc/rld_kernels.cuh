@@ -67,6 +67,7 @@ void cholqr_check(int w, const double* R, const double* gdiag, const int* info, 
                   cudaStream_t st);
 void householder_check(int w, const double* R, int64_t ldr, const double* norms2, double rtol, double* sgn,
                        int* flags, cudaStream_t st);
+void copy_upper(int w, const double* src, int64_t lds, double* dst, cudaStream_t st);
 void diag_copy(int w, const double* G, double* d, cudaStream_t st);
 void top_eigvecs(int w, int k, const double* V, const double* theta, double* Vtop, double* theta_top,
                  cudaStream_t st);

@@ -449,6 +449,15 @@ __global__ void householder_check_kernel(int w, const double* __restrict__ R, in
   sgn[i] = rii < 0.0 ? -1.0 : 1.0;
 }
 
+// dst (w x w, ld w, column-major) = upper triangle of src (ld lds), zeros below
+__global__ void copy_upper_kernel(int w, const double* __restrict__ src, int64_t lds, double* __restrict__ dst) {
+  const int64_t total = (int64_t)w * w;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / w), r = (int)(e % w);
+    dst[e] = r <= c ? src[(int64_t)c * lds + r] : 0.0;
+  }
+}
+
 __global__ void diag_copy_kernel(int w, const double* __restrict__ G, double* __restrict__ d) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < w) d[i] = G[(int64_t)i * w + i];
@@ -647,6 +656,12 @@ void cholqr_check(int w, const double* R, const double* gdiag, const int* info, 
   cholqr_check_kernel<<<(unsigned)ceil_div(std::max(w, 1), 128), 128, 0, st>>>(w, R, gdiag, info, rtol, flags);
   RLD_LAUNCH_CHECK();
 }
+void copy_upper(int w, const double* src, int64_t lds, double* dst, cudaStream_t st) {
+  const int64_t total = (int64_t)w * w;
+  copy_upper_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 1024), 256, 0, st>>>(w, src, lds, dst);
+  RLD_LAUNCH_CHECK();
+}
+
 void householder_check(int w, const double* R, int64_t ldr, const double* norms2, double rtol, double* sgn,
                        int* flags, cudaStream_t st) {
   householder_check_kernel<<<(unsigned)ceil_div(std::max(w, 1), 128), 128, 0, st>>>(w, R, ldr, norms2, rtol, sgn,

@@ -247,17 +247,21 @@ class ResidentMatrix:
     ``bench.py`` times.  Owns its own librld handle."""
 
     def __init__(self, M, dtype: str = "fp64", path: str = "auto", device: int | None = None,
-                 shard: bool | None = None):
+                 shard: bool | None = None, session=None):
         """``shard`` (default: True under torch.distributed with world size > 1)
         joins the process-wide NCCL session and keeps only this rank's rows of K;
-        ``shard=False`` gives an independent single-GPU replica."""
-        from ._session import Session, dist_world, session
+        ``shard=False`` gives an independent single-GPU replica.  ``session`` binds an
+        explicit session (a virtual-shard rank of ``parallel.VirtualShards``)."""
+        from ._session import Session, dist_world
+        from ._session import session as process_session
 
         rank, world, local = dist_world()
         if shard is None:
             shard = world > 1
-        if shard and world > 1:
-            self.sess = session()
+        if session is not None:
+            self.sess = session
+        elif shard and world > 1:
+            self.sess = process_session()
         else:
             self.sess = Session(local if device is None else device)
         self.dtype = dtype

@@ -42,3 +42,71 @@ def broadcast_nccl_id() -> bytes:
     else:
         dist.broadcast(buf, 0)
     return bytes(buf.numpy().tobytes())
+
+
+class VirtualShards:
+    """G row shards of one estimate in ONE process (RLD_COMM_THREADS): one librld handle per
+    rank, each driven by its own host thread, collectives through device staging slots with
+    host barriers (comm.cu) -- no kernel waits on another rank.  Runs the world > 1 code paths
+    of the library on a single GPU (tests, and ``bench.py --virtual-shards``); production
+    multi-GPU runs use one process per GPU over NCCL instead.
+
+        with VirtualShards(3) as vs:
+            results = vs.run(lambda: rstar_logdet(M, cfg))     # one LogDetEstimate per rank
+    """
+
+    def __init__(self, world_size: int, device: int = 0):
+        from . import _native as N
+        from ._session import Session
+
+        if world_size < 1:
+            raise ValueError("world_size must be >= 1")
+        self.world_size = world_size
+        self.group = N.VirtualGroup(world_size)
+        self.sessions = [Session(device, r, world_size, group=self.group) for r in range(world_size)]
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
+
+    def close(self):
+        for s in self.sessions:
+            s.handle.close()
+        self.sessions = []
+        self.group.close()
+
+    def run(self, fn, *args):
+        """fn(*args) on every rank concurrently, each in a thread bound to its rank's session
+        (``fn`` may take the rank's Session as a keyword ``session`` if it declares one).
+        Returns the per-rank results; re-raises the first root-cause error (a rank whose
+        failure aborted the group makes the others fail with 'virtual group aborted')."""
+        import inspect
+        import threading
+
+        from ._session import worker_session
+
+        out = [None] * self.world_size
+        errs = [None] * self.world_size
+        wants = "session" in inspect.signature(fn).parameters
+
+        def body(r):
+            try:
+                with worker_session(sess=self.sessions[r]):
+                    out[r] = fn(*args, session=self.sessions[r]) if wants else fn(*args)
+            except BaseException as e:  # noqa: BLE001 - collected and re-raised below
+                errs[r] = e
+
+        ths = [threading.Thread(target=body, args=(r,)) for r in range(self.world_size)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        real = [e for e in errs if e is not None and "virtual group aborted" not in str(e)]
+        if real:
+            raise real[0]
+        if any(e is not None for e in errs):
+            raise next(e for e in errs if e is not None)
+        return out

@@ -71,6 +71,27 @@ __global__ void dfma_kernel(int iters, double seed, double* out) {
   if (s == 12345.0) out[0] = s;
 }
 
+// FP64 tensor cores: independent chains of mma.sync m8n8k4 f64 (256 FMA each)
+__global__ void dmma_kernel(int iters, double seed, double* out) {
+  double c[CHAINS][2];
+  const double a = seed + threadIdx.x * 1e-9, b = 0.999999;
+#pragma unroll
+  for (int k = 0; k < CHAINS; ++k) c[k][0] = c[k][1] = 1e-3 * k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int k = 0; k < CHAINS; ++k)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                     : "+d"(c[k][0]), "+d"(c[k][1])
+                     : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < CHAINS; ++k) s += c[k][0] + c[k][1];
+  if (s == 12345.0) out[0] = s;
+}
+
 template <int OP>   // 0 ex2.approx.ftz, 1 sqrt.approx.ftz
 __global__ void mufu_kernel(int iters, float seed, float* out) {
   float a[CHAINS];
@@ -183,6 +204,13 @@ int main() {
   {
     float ms = best_ms([&] { dfma_kernel<<<blocks, threads>>>(iters / 4, 1.0, dd); });
     printf(" \"dfma_tflops\": %.2f,\n", 2 * ops / 4 / (ms * 1e-3) / 1e12);
+  }
+  {
+    // per warp: iters * 4 * CHAINS DMMAs of 8 x 8 x 4 FMAs
+    const int dit = iters / 16;
+    float ms = best_ms([&] { dmma_kernel<<<blocks, threads>>>(dit, 1.0, dd); });
+    const double fl = (double)blocks * (threads / 32) * dit * 4 * CHAINS * 2.0 * 8 * 8 * 4;
+    printf(" \"dmma_tflops\": %.2f,\n", fl / (ms * 1e-3) / 1e12);
   }
   {
     float ms = best_ms([&] { mufu_kernel<0><<<blocks, threads>>>(iters / 4, 0.5f, fo); });

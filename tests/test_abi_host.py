@@ -33,7 +33,7 @@ def test_library_loads_and_exports_every_symbol():
     lib = N.load()
     for name in declared_symbols():
         assert hasattr(lib, name), name
-    assert lib.rld_abi_version() == N.ABI_VERSION == 3
+    assert lib.rld_abi_version() == N.ABI_VERSION == 4
 
 
 def test_library_is_sm100a():
@@ -53,6 +53,7 @@ int main(void) {
   O(rld_problem, data) O(rld_problem, ld) O(rld_config, probe_key) O(rld_config, omega_key)
   O(rld_config, diag_floor) O(rld_result, per_probe) O(rld_result, phase_ms) O(rld_inputs, memory)
   O(rld_config, estimator) O(rld_result, clamped_eigs) O(rld_config, precond_scale) O(rld_config, precond_key)
+  O(rld_device_set, comm_kind) O(rld_device_set, nccl_id) O(rld_device_set, group)
   return 0;
 }
 """
