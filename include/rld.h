@@ -161,7 +161,7 @@ typedef struct rld_result {
   double phase_ms[8];     /* [0] K build [1] sketch+QR [2] projected eig [3] precond factors
                              [4] Lanczos [5] shifted solves + Hutchinson [6] collectives [7] total */
   int32_t clamped_eigs;   /* SLQ: Ritz values <= 0 floored before the log (src/estimators.py:113-115) */
-  int32_t reserved;
+  int32_t qr_fallback;    /* rand-svd: 1 when an ill-conditioned sketch sent the QR to Householder / TSQR */
 } rld_result;
 
 int rld_abi_version(void);

@@ -76,7 +76,7 @@ class Result(C.Structure):
     _fields_ = [("value", C.c_double), ("logdet_P", C.c_double), ("trace_term", C.c_double),
                 ("per_probe", C.POINTER(C.c_double)), ("wall_time", C.c_double), ("attempts", C.c_int32),
                 ("rank_kept", C.c_int32), ("kv_products", C.c_int32), ("kernel_launches", C.c_int32),
-                ("phase_ms", C.c_double * 8), ("clamped_eigs", C.c_int32), ("reserved", C.c_int32)]
+                ("phase_ms", C.c_double * 8), ("clamped_eigs", C.c_int32), ("qr_fallback", C.c_int32)]
 
 
 _lib = None

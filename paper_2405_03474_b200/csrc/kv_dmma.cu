@@ -14,7 +14,8 @@
 // Kernel design (one CTA = BM x BN outputs over a k range):
 //   * warp 8 is the producer: one elected lane streams BK = 16-double (128-byte) k-steps of A and
 //     of B into a 4-stage shared-memory ring with TMA (cp.async.bulk.tensor, 128-byte swizzle,
-//     out-of-range rows and columns zero-filled by the copy engine), full/empty mbarriers;
+//     out-of-range rows and columns zero-filled by the copy engine), full/empty mbarriers; a
+//     stage is released one step late (after the DMMAs that consumed its shared loads issued);
 //   * warps 0-7 each own a WM x WN slice of the tile and issue (WM/8) x (WN/8) DMMAs per 4-deep
 //     k slice; the m8n8k4 A and B fragments (8 rows x 4 consecutive k of a row-major tile) are
 //     single 8-byte shared loads, conflict-free under the 128-byte swizzle (two wavefronts per
@@ -134,6 +135,12 @@ gemm_nt_dmma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
   for (int s = 0; s < steps; ++s) {
     const int st = s % DM_STAGES;
     ptx::mbar_wait(&full[st], (s / DM_STAGES) & 1);
+    // Release the PREVIOUS stage only now.  An mbarrier arrive does not wait for this warp's
+    // outstanding shared loads (ptxas schedules it among the DMMAs that consume them), so an
+    // arrive right after the loads let the next TMA overwrite a row before its LDS had read it
+    // (rare single-row errors, worst with concurrent kernels).  Every DMMA of step s-1 -- and so
+    // every LDS it consumed -- has issued before the loop back-edge, i.e. before this point.
+    if (s > 0 && lane == 0) ptx::mbar_arrive(&empty[(s - 1) % DM_STAGES]);
     const uint32_t a_s = sbase + st * S::STAGE_BYTES;
     const uint32_t b_s = a_s + S::A_BYTES;
 #pragma unroll
@@ -149,8 +156,6 @@ gemm_nt_dmma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
 #pragma unroll
         for (int j = 0; j < S::NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
-    __syncwarp();
-    if (lane == 0) ptx::mbar_arrive(&empty[st]);
   }
 
   // ---- epilogue: C[c, i] (+ split offset); lane holds rows fr, columns 2 fk + {0, 1}

@@ -1222,6 +1222,7 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
   res->trace_term = hs[2];
   res->value = res->logdet_P + res->trace_term;
   res->attempts = po.attempts;
+  res->qr_fallback = po.householder ? 1 : 0;
   res->rank_kept = po.k > 0 ? hi[3] : 0;
   res->kv_products = products + (c->precond_kind == RLD_PRECOND_RAND_SVD || c->precond_kind == RLD_PRECOND_RAND_SVD_SCALED
                                      ? (c->precond_iters + 1) * po.attempts : 0);

@@ -80,6 +80,7 @@ class LogDetEstimate:
     rank_kept: int = 0
     attempts: int = 1
     path: str = "stored"      # where K lived for this estimate: "stored" in HBM or "on_the_fly"
+    qr_fallback: bool = False  # the sketch QR fell back from Cholesky-QR to Householder (TSQR when sharded)
 
 
 def _sketch_width(cfg: EstimatorConfig, n: int) -> int:
@@ -179,7 +180,7 @@ def _result(res: N.Result, per: np.ndarray, start: float, path: str = "stored") 
     return LogDetEstimate(res.value, res.logdet_P, res.trace_term, per, time.perf_counter() - start,
                           clamped_eigs=int(res.clamped_eigs), device_time=res.wall_time, phase_ms=tuple(res.phase_ms),
                           kv_products=res.kv_products, kernel_launches=res.kernel_launches, rank_kept=res.rank_kept,
-                          attempts=res.attempts, path=path)
+                          attempts=res.attempts, path=path, qr_fallback=bool(res.qr_fallback))
 
 
 def rstar_logdet(M, cfg: EstimatorConfig, probes=None, omega=None) -> LogDetEstimate:
