@@ -2,7 +2,10 @@
 UNMODIFIED reference ``ratlogdet.rstar_logdet`` with ``PreconditionerConfig(kind, ...)``
 (src/precond.py:201-267), run in this container only.
 
-Usage:  OPENBLAS_NUM_THREADS=1 python tests/golden/make_golden_precond.py
+Usage:  OPENBLAS_NUM_THREADS=1 python tests/golden/make_golden_precond.py [wellposed]
+
+``wellposed`` writes golden_precond_wellposed.json: the partial-Cholesky kinds on K + diag(offsets)
+with distinct offsets, so the greedy pivots have no near-ties and the cases pin to 1e-6.
 """
 
 from __future__ import annotations
@@ -27,7 +30,41 @@ KINDS = ("identity", "diagonal", "rank-one", "partial-cholesky", "partial-choles
          "trunc-svd-scaled", "rand-svd", "rand-svd-scaled")
 
 
+def diag_offsets(n, seed=7):
+    """Distinct diagonal offsets that make the partial-Cholesky pivots well posed: with the kernel's
+    constant diagonal every first pivot is an n-way tie (np.argmax picks index 0, a 1e-15
+    perturbation picks another), so the plain-kernel cases below screen at ~1e-2."""
+    return np.random.default_rng(seed).uniform(0.0, 0.05, n)
+
+
+def wellposed_cases():
+    out = []
+    for idx, n, rank, scale in [(1, 768, 48, 5e-3), (3, 1024, 64, 5e-3)]:
+        wl = baseline(idx, n=n)
+        spec = ratlogdet.KernelSpec(wl.spec.family, wl.spec.amplitude, wl.spec.length_scale, wl.spec.jitter)
+        M = ratlogdet.build_covariance(spec, wl.points) + np.diag(diag_offsets(n))
+        for kind in ("partial-cholesky", "partial-cholesky-scaled"):
+            cfg = ratlogdet.EstimatorConfig("r3", 8, 20, "rademacher",
+                                            ratlogdet.PreconditionerConfig(kind, rank, 5, scale), seed=0)
+            est = ratlogdet.rstar_logdet(M, cfg)
+            g = np.random.default_rng(12345)
+            E = g.standard_normal(M.shape)
+            E = 0.5 * (E + E.T)
+            pert = ratlogdet.rstar_logdet(M * (1.0 + 1e-15 * E), cfg).value
+            rec = dict(name=f"{kind}_wellposed_{wl.name}_n{n}", kind=kind, config_index=idx, n=n, rank=rank,
+                       num_iters=5, scale=scale, num_probes=8, algorithm="r3", seed=0, diag_offsets_seed=7,
+                       diag_offsets_max=0.05, value=est.value, logdet_P=est.logdet_P, trace_term=est.trace_term,
+                       per_probe=[float(x) for x in est.per_probe_values],
+                       screen=abs(pert - est.value) / abs(est.value))
+            print(rec["name"], rec["value"], rec["logdet_P"], "screen", rec["screen"], flush=True)
+            out.append(rec)
+    return out
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "wellposed":
+        (HERE / "golden_precond_wellposed.json").write_text(json.dumps(wellposed_cases(), indent=1))
+        return
     out = []
     for idx, n, rank, scale in [(1, 768, 48, 5e-3), (3, 1024, 64, 5e-3)]:
         wl = baseline(idx, n=n)
