@@ -186,6 +186,121 @@ __global__ void dmma_split_reduce_kernel(const double* __restrict__ part, int sp
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// "Expand" products: C (q x N) = beta C + S^T X, S: p x q column-major (small), X: p x N rows layout
+// (long N = the points).  The basis changes / low-rank expansions of the preconditioner
+// (Q R^-1 of the CholQR, A = Q^T U_top, U = A W / sqrt(lambda): src/precond.py:96-99, 191-193;
+// src/linalg.py:159-180) and the Woodbury apply w += U (h o U^T w) (src/precond.py:102-115).
+// m8n8k4 with M = the q side (fragment rows of the S tile, 128-byte swizzle as above) and N = the
+// long side; the X tile arrives as 8-column TMA boxes [BK][8] (64-byte rows, no swizzle), so a
+// B fragment (4 consecutive k rows x 8 consecutive columns) is 256 contiguous bytes: conflict-free.
+// No split over p (p <= a few thousand): deterministic, one pass.
+constexpr int EX_BN = 128;   // columns of X / C per CTA
+
+template <int BQ>
+struct ExShape {
+  static constexpr int WARPS_Q = BQ >= 64 ? 2 : 1;
+  static constexpr int WARPS_N = DM_MMA_WARPS / WARPS_Q;
+  static constexpr int WQ = BQ / WARPS_Q;           // 32
+  static constexpr int WN = EX_BN / WARPS_N;        // 32 (BQ 64) or 16 (BQ 32)
+  static constexpr int MT = WQ / 8, NT = WN / 8;
+  static constexpr int S_BYTES = BQ * DM_BK * 8;
+  static constexpr int X_BYTES = EX_BN * DM_BK * 8;
+  static constexpr int STAGE_BYTES = S_BYTES + X_BYTES;
+  static constexpr int SMEM = DM_STAGES * STAGE_BYTES + 1024 + 2 * DM_STAGES * 8;
+  static_assert(S_BYTES % 1024 == 0, "S tile must keep 1024-byte alignment");
+};
+
+template <int BQ>
+__global__ void __launch_bounds__(DM_THREADS, 2)
+gemm_expand_dmma_kernel(const __grid_constant__ CUtensorMap mapS, const __grid_constant__ CUtensorMap mapX, int64_t p,
+                        int64_t q, int64_t N, double* __restrict__ C, int64_t ldc, double alpha, double beta) {
+  using S = ExShape<BQ>;
+  extern __shared__ __align__(1024) unsigned char ex_smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(ex_smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + DM_STAGES * S::STAGE_BYTES);
+  uint64_t* empty = full + DM_STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t j0 = (int64_t)blockIdx.x * EX_BN;
+  const int64_t b0 = (int64_t)blockIdx.y * BQ;
+  const int steps = (int)ceil_div(p, DM_BK);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < DM_STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], DM_MMA_WARPS);
+    }
+    ptx::fence_mbarrier_init();
+  }
+  __syncthreads();
+
+  if (warp == DM_MMA_WARPS) {   // ---- producer: one S box + EX_BN / 8 X boxes per k-step
+    if (ptx::elect_one()) {
+      ptx::tma_prefetch_desc(&mapS);
+      ptx::tma_prefetch_desc(&mapX);
+      for (int s = 0; s < steps; ++s) {
+        const int st = s % DM_STAGES;
+        if (s >= DM_STAGES) ptx::mbar_wait(&empty[st], ((s / DM_STAGES) - 1) & 1);
+        unsigned char* dst = smem + st * S::STAGE_BYTES;
+        ptx::mbar_arrive_expect_tx(&full[st], S::STAGE_BYTES);
+        const int32_t kc = s * DM_BK;
+        ptx::tma_load_2d(dst, &mapS, &full[st], kc, (int32_t)b0);
+#pragma unroll 1
+        for (int g = 0; g < EX_BN / 8; ++g)
+          ptx::tma_load_2d(dst + S::S_BYTES + g * DM_BK * 64, &mapX, &full[st], (int32_t)(j0 + 8 * g), kc);
+      }
+    }
+    return;
+  }
+
+  const int wq0 = (warp / S::WARPS_N) * S::WQ;
+  const int wn0 = (warp % S::WARPS_N) * S::WN;
+  const int fr = lane >> 2, fk = lane & 3;
+  double acc[S::MT][S::NT][2];
+#pragma unroll
+  for (int i = 0; i < S::MT; ++i)
+#pragma unroll
+    for (int j = 0; j < S::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const uint32_t sbase = ptx::smem_u32(smem);
+  for (int s = 0; s < steps; ++s) {
+    const int st = s % DM_STAGES;
+    ptx::mbar_wait(&full[st], (s / DM_STAGES) & 1);
+    if (s > 0 && lane == 0) ptx::mbar_arrive(&empty[(s - 1) % DM_STAGES]);   // see gemm_nt_dmma_kernel
+    const uint32_t s_s = sbase + st * S::STAGE_BYTES;
+    const uint32_t x_s = s_s + S::S_BYTES;
+#pragma unroll
+    for (int kk = 0; kk < DM_BK / 4; ++kk) {
+      const int k = kk * 4 + fk;
+      double a[S::MT], b[S::NT];
+#pragma unroll
+      for (int i = 0; i < S::MT; ++i) a[i] = lds_f64(s_s + sw128(wq0 + i * 8 + fr, k));
+#pragma unroll
+      for (int j = 0; j < S::NT; ++j) {
+        const int g = (wn0 + j * 8) >> 3;   // 8-column box
+        b[j] = lds_f64(x_s + (uint32_t)(g * DM_BK * 64 + k * 64 + fr * 8));
+      }
+#pragma unroll
+      for (int i = 0; i < S::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < S::NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+  // C[b][j]: lane holds row fr, columns 2 fk + {0, 1}
+#pragma unroll
+  for (int i = 0; i < S::MT; ++i) {
+    const int64_t b = b0 + wq0 + i * 8 + fr;
+    if (b >= q) continue;
+#pragma unroll
+    for (int j = 0; j < S::NT; ++j) {
+      const int64_t c = j0 + wn0 + j * 8 + 2 * fk;
+      double* o = C + b * ldc + c;
+      if (c < N) o[0] = beta == 0.0 ? alpha * acc[i][j][0] : fma(beta, o[0], alpha * acc[i][j][0]);
+      if (c + 1 < N) o[1] = beta == 0.0 ? alpha * acc[i][j][1] : fma(beta, o[1], alpha * acc[i][j][1]);
+    }
+  }
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -286,6 +401,37 @@ bool aligned16(const void* ptr, int64_t ld) {
 
 }  // namespace
 
+// rows x cols float64 row-major, box {8, box_rows}, no swizzle (64-byte rows)
+CUtensorMap map_f64_b8(const double* base, int64_t cols, int64_t rows, int64_t ld, int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  cuuint32_t box[2] = {8, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(RLD_ERR_CUDA, "cuTensorMapEncodeTiled (f64 x8) failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+template <int BQ>
+void launch_expand(const double* Sm, int64_t lds, int64_t p, int64_t q, const double* X, int64_t ldx, int64_t N,
+                   double* C, int64_t ldc, double alpha, double beta, cudaStream_t st) {
+  using S = ExShape<BQ>;
+  static bool attr = false;
+  if (!attr) {
+    RLD_CUDA(cudaFuncSetAttribute(gemm_expand_dmma_kernel<BQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM));
+    attr = true;
+  }
+  const CUtensorMap ms = map_f64(Sm, p, q, lds, BQ);       // S^T as q rows of p
+  const CUtensorMap mx = map_f64_b8(X, N, p, ldx, DM_BK);   // X: p rows of N
+  dim3 grid((unsigned)ceil_div(N, EX_BN), (unsigned)ceil_div(q, BQ), 1);
+  if (grid.y > 65535u) fail(RLD_ERR_NOT_SUPPORTED, "gemm_expand_f64: q too large");
+  gemm_expand_dmma_kernel<BQ><<<grid, DM_THREADS, S::SMEM, st>>>(ms, mx, p, q, N, C, ldc, alpha, beta);
+  RLD_LAUNCH_CHECK();
+}
+
 bool gemm_nt_f64_ok(const double* A, int64_t lda, const double* B, int64_t ldb) {
   return aligned16(A, lda) && aligned16(B, ldb);
 }
@@ -319,6 +465,22 @@ void gemm_nt_f64(const double* A, int64_t lda, int64_t p, const double* B, int64
     case 32: launch_nt<128, 32>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st); break;
     default: launch_nt<128, 16>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st); break;
   }
+}
+
+// C (q x N, ld ldc, rows layout) = beta C + alpha S^T X; S: p x q column-major (ld lds), X: p x N
+// rows layout (ld ldx).  S and X rows 16-byte aligned (gemm_nt_f64_ok(S, lds, X, ldx)).
+void gemm_expand_f64(const double* Sm, int64_t lds, int64_t p, int64_t q, const double* X, int64_t ldx, int64_t N,
+                     double* C, int64_t ldc, double alpha, double beta, cudaStream_t st) {
+  if (q <= 0 || N <= 0) return;
+  if (p <= 0) {
+    if (beta != 1.0) fail(RLD_ERR_NOT_SUPPORTED, "gemm_expand_f64 with p = 0 needs beta = 1");
+    return;
+  }
+  if (!gemm_nt_f64_ok(Sm, lds, X, ldx)) fail(RLD_ERR_NOT_SUPPORTED, "gemm_expand_f64 needs 16-byte aligned rows");
+  if (q <= 32)
+    launch_expand<32>(Sm, lds, p, q, X, ldx, N, C, ldc, alpha, beta, st);
+  else
+    launch_expand<64>(Sm, lds, p, q, X, ldx, N, C, ldc, alpha, beta, st);
 }
 
 }  // namespace rld

@@ -384,25 +384,37 @@ bool fused_enabled_for(int64_t s, int k) {
   return on && lanczos_fused_fits(s, k);
 }
 
-// G (w x w, full) = Y^T Y for the rows x w column-major block.  The rows are cut
-// into fixed chunks, one DGEMM per chunk in a strided batch (FP64 tensor cores,
-// enough CTAs to fill the GPU; a single SYRK has only ~w^2/2048 output tiles),
-// then the chunk Grams are summed in fixed order (deterministic).
+// ---- float64 products of the estimate outside K x V, on the FP64 tensor cores (kv_dmma.cu).
+// Both operands' rows must start 16-byte aligned (even leading dimensions: every BASELINE shape);
+// otherwise -- odd n or an odd shard offset -- the same product runs on cuBLAS.
+//
+// nt_f64: C (q x p, ld ldc) = beta C + A B^T for A: p x n, B: q x n (rows layout); in column-major
+// terms C = A^T B.  The Grams, projections and U^T W of the preconditioner and its apply.
+void nt_f64(rld_handle* h, const double* A, int64_t lda, int64_t p, const double* B, int64_t ldb, int64_t q, int64_t n,
+            double* C, int64_t ldc, double beta = 0.0) {
+  if (gemm_nt_f64_ok(A, lda, B, ldb)) {
+    gemm_nt_f64(A, lda, p, B, ldb, q, n, C, ldc, beta, h->wk.gram_scratch, h->st);
+    return;
+  }
+  RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, (int)p, (int)q, (int)n, &ONE, A, (int)lda, B, (int)ldb,
+                         &beta, C, (int)ldc));
+}
+
+// ex_f64: C (q x N rows layout, ld ldc) = beta C + alpha S^T X for S: p x q column-major, X: p x N
+// rows layout; in column-major terms C = X S.  Basis changes and low-rank expansions.
+void ex_f64(rld_handle* h, const double* S, int64_t lds, int64_t p, int64_t q, const double* X, int64_t ldx, int64_t N,
+            double* C, int64_t ldc, double alpha = 1.0, double beta = 0.0) {
+  if (gemm_nt_f64_ok(S, lds, X, ldx)) {
+    gemm_expand_f64(S, lds, p, q, X, ldx, N, C, ldc, alpha, beta, h->st);
+    return;
+  }
+  RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)N, (int)q, (int)p, &alpha, X, (int)ldx, S, (int)lds,
+                         &beta, C, (int)ldc));
+}
+
+// G (w x w, full) = Y^T Y for the rows x w column-major block (fixed-order split-k, deterministic).
 void gram_blas(rld_handle* h, int64_t rows, int w, const double* Y, int64_t ldy, double* G) {
-  Work& wk = h->wk;
-  const int64_t chunk = std::max<int64_t>(512, ceil_div(rows, 16));
-  const int64_t nb = ceil_div(rows, chunk);
-  const int64_t full = rows / chunk;   // equal chunks in the batch; a ragged tail gets its own GEMM
-  wk.gram_scratch.reserve(sizeof(double) * (size_t)w * w * nb);
-  double* P = wk.gram_scratch.as<double>();
-  if (full > 0)
-    RLD_CUBLAS(cublasDgemmStridedBatched(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, w, w, (int)chunk, &ONE, Y, (int)ldy,
-                                         chunk, Y, (int)ldy, chunk, &ZERO, P, w, (int64_t)w * w, (int)full));
-  const int64_t tail = rows - full * chunk;
-  if (tail > 0)
-    RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, w, w, (int)tail, &ONE, Y + full * chunk, (int)ldy,
-                           Y + full * chunk, (int)ldy, &ZERO, P + (size_t)full * w * w, w));
-  sum_blocks(nb, (int64_t)w * w, P, G, h->st);
+  nt_f64(h, Y, ldy, w, Y, ldy, w, rows, G, w);
 }
 
 // In-place row orthonormalisation of the w x n block Y (col-major n x w), two
@@ -436,16 +448,24 @@ void cholqr2(rld_handle* h, int64_t n, int w, double* Y, int* flags, int passes 
   Work& wk = h->wk;
   wk.G.reserve(sizeof(double) * w * w);
   wk.gdiag.reserve(sizeof(double) * w);
+  wk.rinv.reserve(sizeof(double) * w * w);
   double* G = wk.G.as<double>();
+  double* Ri = wk.rinv.as<double>();
   int* info = wk.ints.as<int>() + 1;
   for (int pass = 0; pass < passes; ++pass) {
     gram_blas(h, n, w, Y, n, G);
     allreduce_sum(h, G, (int64_t)w * w);
     if (pass == 0) diag_copy(w, G, wk.gdiag.as<double>(), h->st);
-    potrf_upper(h, w, G, info);
+    const bool have_rinv = potrf_upper(h, w, G, info, Ri);
     if (pass == 0) cholqr_check(w, G, wk.gdiag.as<double>(), info, 1e-6, flags, h->st);
-    RLD_CUBLAS(cublasDtrsm(h->cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
-                           (int)n, w, &ONE, G, w, Y, (int)n));
+    if (have_rinv && n > 0) {   // Y <- Y R^-1 through a scratch copy (the expand kernel is out of place)
+      wk.scratch2.reserve(sizeof(double) * n * w);
+      copy_doubles(n * (int64_t)w, Y, wk.scratch2.as<double>(), h->st);
+      ex_f64(h, Ri, w, w, w, wk.scratch2.as<double>(), n, n, Y, n);
+    } else {
+      RLD_CUBLAS(cublasDtrsm(h->cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
+                             (int)n, w, &ONE, G, w, Y, (int)n));
+    }
   }
 }
 
@@ -476,8 +496,7 @@ void cholqr_gemm(rld_handle* h, int64_t n, int w, double* src, double* dst, int*
       RLD_CUBLAS(cublasDtrsm(h->cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, w,
                              w, &ONE, G, w, Ri, w));
     }
-    RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)n, w, w, &ONE, cur, (int)n, Ri, w, &ZERO, out,
-                           (int)n));
+    ex_f64(h, Ri, w, w, w, cur, n, n, out, n);   // out = cur R^-1
     cur = out;
   }
   if (cur != dst) copy_doubles(n * (int64_t)w, cur, dst, h->st);
@@ -544,8 +563,7 @@ void qr_householder(rld_handle* h, int64_t n, int w, double* Y, double rtol, int
   RLD_CUSOLVER(cusolverDnDorgqr(h->solver, (int)gw, w, w, S, (int)gw, tau, work, std::max(l3, l4), info));
   // Q_local = Q_g Q_s[g], then the sign fix
   double* out = wk.scratch2.as<double>();
-  RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)n, w, w, &ONE, Y, (int)n, S + (int64_t)h->rank * w,
-                         (int)gw, &ZERO, out, (int)n));
+  ex_f64(h, S + (int64_t)h->rank * w, gw, w, w, Y, n, n, out, n);
   copy_doubles(n * (int64_t)w, out, Y, h->st);
   scale_cols_colmajor(n, w, n, sgn, Y, h->st);
 }
@@ -568,7 +586,7 @@ void syevd(rld_handle* h, int k, double* A, double* evals) {
     double* G = sp;
     double* Z2 = sp + kk;
     double* defect = sp + 2 * kk;
-    RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, k, k, k, &ONE, Z, k, Z, k, &ZERO, G, k));
+    nt_f64(h, Z, k, k, Z, k, k, k, G, k);   // G = Z^T Z
     orth_defect(k, G, defect, h->st);
     double hd = 0.0;
     RLD_CUDA(cudaMemcpyAsync(&hd, defect, sizeof(double), cudaMemcpyDeviceToHost, h->st));
@@ -580,14 +598,12 @@ void syevd(rld_handle* h, int k, double* A, double* evals) {
       double* cur = Z;
       double* nxt = Z2;
       for (int it = 0; it < steps; ++it) {
-        if (it > 0)
-          RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, k, k, k, &ONE, cur, k, cur, k, &ZERO, G, k));
+        if (it > 0) nt_f64(h, cur, k, k, cur, k, k, k, G, k);
         copy_doubles((int64_t)kk, cur, nxt, h->st);
-        RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, k, k, k, &HALF_NEG, cur, k, G, k, &THREE_HALF,
-                               nxt, k));
+        ex_f64(h, G, k, k, k, cur, k, k, nxt, k, HALF_NEG, THREE_HALF);   // nxt = 1.5 Z - 0.5 Z G
         std::swap(cur, nxt);
       }
-      RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, k, k, k, &ONE, Q, k, cur, k, &ZERO, A, k));
+      ex_f64(h, cur, k, k, k, Q, k, k, A, k);   // A = Q Z
       return;
     }
     if (getenv("RLD_TRI_EIG_DEBUG")) fprintf(stderr, "rld: tri_eigh fallback to DSYEVD (k = %d, defect %.2e)\n", k, hd);
@@ -684,8 +700,7 @@ int lowrank_randsvd(rld_handle* h, const rld_config* c, const rld_inputs* in, Pr
   wk.C.reserve(sizeof(double) * std::max<int64_t>((int64_t)w * w, (int64_t)k * k));
   double* B = wk.C.as<double>();
   const double* Ql = Y + r.row0;  // col-major n x w, local rows start at row0
-  RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, w, w, (int)nl, &ONE, Ql, (int)n, Z, (int)nl, &ZERO, B,
-                         w));
+  nt_f64(h, Ql, n, w, Z, nl, w, nl, B, w);   // B = Q_l^T (K Q^T)_l
   allreduce_sum(h, B, (int64_t)w * w);
   wk.theta.reserve(sizeof(double) * w);
   syevd(h, w, B, wk.theta.as<double>());                  // src/precond.py:190
@@ -695,8 +710,7 @@ int lowrank_randsvd(rld_handle* h, const rld_config* c, const rld_inputs* in, Pr
   // A = (Q^T U_top) sqrt(max(theta, 0))  (src/precond.py:191-193, 264)
   wk.A.reserve(sizeof(double) * nl * k);
   double* A = wk.A.as<double>();
-  RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nl, k, w, &ONE, Ql, (int)n, wk.Vtop.as<double>(),
-                         w, &ZERO, A, (int)nl));
+  ex_f64(h, wk.Vtop.as<double>(), w, w, k, Ql, n, nl, A, nl);   // A = Q_l V_top
   return k;
 }
 
@@ -924,8 +938,7 @@ PrecondOut build_preconditioner(rld_handle* h, const rld_config* c, const rld_in
   double* hv = wk.hgg.as<double>();
   sqrt_factors(k, c->keep_rtol, wk.lam.as<double>(), C, hv, hv + k, hv + 2 * k, wk.ints.as<int>() + 3, st);
   // U (n_local x k) into Z (no longer needed)
-  RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nl, k, k, &ONE, A, (int)nl, C, k, &ZERO, Z,
-                         (int)nl));
+  ex_f64(h, C, k, k, k, A, nl, nl, Z, nl);   // U = A W lambda^-1/2
   if (side) RLD_CUDA(cudaStreamWaitEvent(st, h->join, 0));
   out.k = k;
   return out;
@@ -1055,16 +1068,13 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
   copy_doubles(s * nl, wv, x, st);
   copy_doubles(s * nl, wv, p, st);
   if (k > 0) {
-    RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, k, (int)s, (int)nl, &ONE, U, (int)nl, wv, (int)nl,
-                           &ZERO, T, k));
+    nt_f64(h, U, nl, k, wv, nl, s, nl, T, k);                    // T = U^T q0
     allreduce_sum(h, T, (int64_t)k * s);
     copy_doubles((int64_t)k * s, T, Tg, st);
     scale_rows_colmajor(k, s, k, hv + k, false, Tg, st);       // g
     scale_rows_colmajor(k, s, k, hv + 2 * k, false, T, st);    // gamma
-    RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nl, (int)s, k, &ONE, U, (int)nl, Tg, k, &ONE, x,
-                           (int)nl));
-    RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nl, (int)s, k, &ONE, U, (int)nl, T, k, &ONE, p,
-                           (int)nl));
+    ex_f64(h, Tg, k, k, s, U, nl, nl, x, nl, 1.0, 1.0);        // x += U (g o T)
+    ex_f64(h, T, k, k, s, U, nl, nl, p, nl, 1.0, 1.0);         // p += U (gamma o T)
   }
   scale_rows_colmajor(nl, s, nl, sqrt_base, true, x, st);
   scale_rows_colmajor(nl, s, nl, sqrt_base, false, p, st);
@@ -1122,11 +1132,9 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
       fa.j = j;
       lanczos_fused_residual(fa, st);
       if (k > 0) {   // w += U (h o (U^T w))
-        RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, k, (int)s, (int)nl, &ONE, U, (int)nl, wv,
-                               (int)nl, &ZERO, T, k));
+        nt_f64(h, U, nl, k, wv, nl, s, nl, T, k);
         scale_rows_colmajor(k, s, k, hv, false, T, st);
-        RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nl, (int)s, k, &ONE, U, (int)nl, T, k, &ONE,
-                               wv, (int)nl));
+        ex_f64(h, T, k, k, s, U, nl, nl, wv, nl, 1.0, 1.0);
       }
       lanczos_fused_finish(fa, st);
       continue;
@@ -1163,12 +1171,10 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
     }
     lanczos_residual(s, nl, j, t, KX, alpha, beta, p, pp, sqrt_base, u, wv, st, !reorth);
     if (k > 0) {
-      RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, k, (int)s, (int)nl, &ONE, U, (int)nl, wv, (int)nl,
-                             &ZERO, T, k));
+      nt_f64(h, U, nl, k, wv, nl, s, nl, T, k);                 // T = U^T w
       allreduce_sum(h, T, (int64_t)k * s);
       scale_rows_colmajor(k, s, k, hv, false, T, st);         // h = 1/(1+lam) - 1
-      RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nl, (int)s, k, &ONE, U, (int)nl, T, k, &ONE,
-                             wv, (int)nl));
+      ex_f64(h, T, k, k, s, U, nl, nl, wv, nl, 1.0, 1.0);     // w += U (h o T)
     }
     scale_rows_colmajor(nl, s, nl, sqrt_base, true, wv, st);  // z = P^-1 u
     if (reorth) {

@@ -131,6 +131,10 @@ void kv_product(const KvOperand& op, int64_t m, const double* V, int64_t ldv, do
 bool gemm_nt_f64_ok(const double* A, int64_t lda, const double* B, int64_t ldb);
 void gemm_nt_f64(const double* A, int64_t lda, int64_t p, const double* B, int64_t ldb, int64_t q, int64_t n,
                  double* C, int64_t ldc, double beta, DevBuf& partial, cudaStream_t st);
+// C (q x N, rows layout) = beta C + alpha S^T X for S: p x q column-major (small), X: p x N rows
+// layout (the expansions U T, Q R^-1, Q^T V of the preconditioner and its Woodbury apply).
+void gemm_expand_f64(const double* S, int64_t lds, int64_t p, int64_t q, const double* X, int64_t ldx, int64_t N,
+                     double* C, int64_t ldc, double alpha, double beta, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // RNG
