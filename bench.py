@@ -76,8 +76,9 @@ def parse():
     ap.add_argument("--mode", choices=["sharded", "replicas"], default="sharded",
                     help="multi-GPU: row-shard one estimate (default) or run independent replicas")
     ap.add_argument("--no-extra", action="store_true", help="skip the extra config-3 fp32 measurement")
-    ap.add_argument("--cpu-sample-n", type=int, default=16384,
-                    help="n of the CPU sample (extrapolated by n^2 to the workload's n)")
+    ap.add_argument("--cpu-sample-n", type=int, default=None,
+                    help="n of the CPU sample (extrapolated by n^2 to the workload's n); default: the largest "
+                         "n <= 16384 whose K reference steps fit in ~200 s")
     return ap.parse_args()
 
 
@@ -227,6 +228,9 @@ def cpu_sample(wl, args):
 
     cfg = wl.config
     ns = args.cpu_sample_n
+    if ns is None:   # ~25 s per n = 16384 sample on the GPU box's 16 host cores (r02 measurement)
+        ns = int(16384 * min(1.0, (200.0 / (25.0 * max(1, args.steps))) ** 0.5)) // 1024 * 1024
+        ns = max(4096, min(16384, ns))
     if wl.n <= ns:
         return replace(wl, config=replace(cfg, dtype="fp64")), 1.0, "the full workload"
     idx = int(wl.name.replace("config", ""))
@@ -270,7 +274,7 @@ def run_reference(args):
     arm_config = workload_config(wl)
     sw, factor, label = cpu_sample(wl, args)
     warm = min(args.warmup, 1)
-    steps = max(1, min(args.steps, 2 if factor > 1 else 3))
+    steps = max(1, args.steps)   # exactly K steps, each a bounded sample (cpu_sample)
     for _ in range(warm):
         cpu_estimate(sw, threads)
     times = [cpu_estimate(sw, threads)[0] * factor for _ in range(steps)]

@@ -1,0 +1,23 @@
+"""A few float64 stored K.V products at one BASELINE shape (for ncu): config 3 (n = 65536), m = s or w."""
+import argparse
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2405_03474_b200 as rld  # noqa: E402
+from paper_2405_03474_b200.workloads import baseline  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=3)
+ap.add_argument("--m", type=int, default=64)
+ap.add_argument("--reps", type=int, default=3)
+a = ap.parse_args()
+wl = baseline(a.config)
+R = rld.ResidentMatrix(rld.KernelMatrix(wl.spec, wl.points), dtype="fp64", path="stored")
+V = torch.randn(a.m, wl.n, dtype=torch.float64, device="cuda")
+for _ in range(a.reps):
+    R.kv_apply(V)
+torch.cuda.synchronize()
+print("ok")
