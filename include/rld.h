@@ -209,6 +209,30 @@ int rld_build_covariance(rld_handle* h, const rld_problem* problem, void* out, i
  * rld_prepare).  Stream-ordered: enqueued on rld_stream(h), not synchronised. */
 int rld_kv_apply(rld_handle* h, int64_t m, const double* V, double* Y);
 
+/* build_preconditioner(M, cfg, rng) on its own (src/precond.py:236-267) for the resident problem:
+ * the preconditioner fields of `cfg` (kind, rank, num_iters, scale, diag_floor, keep_rtol,
+ * omega_key / precond_key streams; the estimator fields are ignored).  The factors stay in the
+ * handle (until the next prepare or estimate) for rld_precond_apply.  Errors as rld_logdet. */
+typedef struct rld_precond_info {
+  double log_det;          /* log det P (src/precond.py:69-80) */
+  int32_t rank;            /* columns of the low-rank factor A (k; < rank when partial Cholesky runs out) */
+  int32_t rank_kept;       /* columns of U kept by the 1e-14 filter (src/precond.py:97) */
+  int32_t attempts;        /* sketch attempts (rand-svd: 2 after a RankDeficient retry) */
+  int32_t qr_fallback;     /* 1 when the sketch QR fell back to Householder / TSQR */
+  int32_t kernel_launches;
+  int32_t reserved;
+} rld_precond_info;
+int rld_precond_build(rld_handle* h, const rld_config* cfg, const rld_inputs* inputs, rld_precond_info* info);
+
+typedef enum rld_precond_op {
+  RLD_SOLVE_SQRT = 0,    /* N^-1 z   (Preconditioner.solve_sqrt,   src/precond.py:102-108) */
+  RLD_SOLVE_SQRT_T = 1,  /* N^-T x   (Preconditioner.solve_sqrt_t, src/precond.py:110-115) */
+  RLD_SOLVE = 2          /* P^-1 u = N^-T N^-1 u */
+} rld_precond_op;
+/* Y = op(V) for m rows V (m x n float64, device) with the last preconditioner build; one GPU.
+ * Stream-ordered on rld_stream(h) and synchronised before returning. */
+int rld_precond_apply(rld_handle* h, int32_t op, int64_t m, const double* V, double* Y);
+
 /* Rng(seed).child(...).rademacher((rows, n)) -- src/linalg.py:84-85, on the
  * device from the stream's Philox key; `out` is device float64, rows x n. */
 int rld_rademacher(rld_handle* h, const uint64_t key[2], int64_t rows, int64_t n, double* out);

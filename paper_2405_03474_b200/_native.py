@@ -42,7 +42,14 @@ EXPORTS = (
     "rld_abi_version", "rld_create", "rld_destroy", "rld_last_error", "rld_logdet", "rld_prepare",
     "rld_logdet_resident", "rld_build_covariance", "rld_kv_apply", "rld_rademacher", "rld_exact_logdet", "rld_dense_cholesky", "rld_dense_eigh",
     "rld_nccl_unique_id", "rld_stream", "rld_normal", "rld_chi_radii", "rld_vgroup_create", "rld_vgroup_destroy",
+    "rld_precond_build", "rld_precond_apply",
 )
+SOLVE_SQRT, SOLVE_SQRT_T, SOLVE = 0, 1, 2
+
+
+class PrecondInfo(C.Structure):
+    _fields_ = [("log_det", C.c_double), ("rank", C.c_int32), ("rank_kept", C.c_int32), ("attempts", C.c_int32),
+                ("qr_fallback", C.c_int32), ("kernel_launches", C.c_int32), ("reserved", C.c_int32)]
 
 
 class DeviceSet(C.Structure):
@@ -116,6 +123,8 @@ def load() -> C.CDLL:
         lib.rld_nccl_unique_id.argtypes = [C.c_void_p]
         lib.rld_stream.argtypes = [H]
         lib.rld_stream.restype = C.c_void_p
+        lib.rld_precond_build.argtypes = [H, C.POINTER(Config), C.POINTER(Inputs), C.POINTER(PrecondInfo)]
+        lib.rld_precond_apply.argtypes = [H, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p]
         lib.rld_vgroup_create.argtypes = [C.c_int32, C.POINTER(C.c_void_p)]
         lib.rld_vgroup_destroy.argtypes = [C.c_void_p]
         lib.rld_vgroup_destroy.restype = None

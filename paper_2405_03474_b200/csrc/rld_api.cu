@@ -15,6 +15,8 @@
 #include <cstring>
 #include <new>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "comm.cuh"
 #include "rld_internal.cuh"
 #include "rld_kernels.cuh"
@@ -25,6 +27,12 @@ thread_local int g_launches = 0;
 std::atomic<int> g_live_handles{0};  // own kernel launches (RLD_LAUNCH_CHECK)
 
 [[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+// NVTX phase ranges (nsys / ncu --nvtx): a no-op unless a tool injects itself
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
   if (e == cudaSuccess) return;
@@ -113,7 +121,6 @@ struct Work {
   DevBuf gsend, grecv;   // row-shard all-gather staging
   DevBuf qbasis, pbasis, coef;   // reorthogonalised Lanczos: bases (t x s x rows) and coefficients
   DevBuf endw, radii;            // normal-orthogonal probes: stream position, chi radii
-  DevBuf lz_dotp, lz_dotp2;      // fused Lanczos step: per-chunk dot partials
   DevBuf rinv;                   // CholQR: explicit R^-1
   DevBuf eig_scratch;            // one-cluster eigensolver: V and singular values
   DevBuf flagbuf;        // flag OR over ranks
@@ -130,6 +137,7 @@ struct rld_handle {
   cublasHandle_t cublas = nullptr;
   cusolverDnHandle_t solver = nullptr;
   std::unique_ptr<rld::Comm> comm;   // world > 1: NCCL or virtual shards (comm.cu)
+  int precond_k = -1;                 // columns of U of the last preconditioner build (-1: none)
   std::string last_error;
   rld::Resident res;
   rld::Work wk;
@@ -198,6 +206,7 @@ void allreduce_flags(rld_handle* h, int* hflags, int count) {
 
 // ----------------------------------------------------------------------------
 void prepare(rld_handle* h, const rld_problem* p) {
+  NvtxRange nv("rld:prepare (K rows / points to HBM)");
   if (!p) fail(RLD_ERR_INVALID_ARGUMENT, "problem is NULL");
   if (p->n < 1) fail(RLD_ERR_INVALID_ARGUMENT, "n must be >= 1");
   if (p->dtype != RLD_FP64 && p->dtype != RLD_FP32) fail(RLD_ERR_INVALID_ARGUMENT, "dtype must be fp64 or fp32");
@@ -205,6 +214,7 @@ void prepare(rld_handle* h, const rld_problem* p) {
   Resident& r = h->res;
   r.ready = false;
   r.tiled = false;
+  h->precond_k = -1;
   r.source = p->source;
   r.dtype = p->dtype;
   r.n = p->n;
@@ -370,19 +380,12 @@ void gather_rows(rld_handle* h, const double* local, int64_t m, double* full) {
 // Y (m x rows) = V (m x n full) K^T restricted to the local rows.  tc_mode 1 =
 // single-pass TF32 on the tensor cores (power-iteration sketch products only),
 // 3 = 3xTF32 (everything whose value enters the estimate directly).
-void kv(rld_handle* h, int64_t m, const double* Vfull, double* Y, int tc_mode = 3, bool presplit = false) {
+void kv(rld_handle* h, int64_t m, const double* Vfull, double* Y, int tc_mode = 3) {
   KvOperand op = h->res.op();
   op.tc_mode = tc_mode;
-  kv_product(op, m, Vfull, op.n, Y, op.rows, h->wk.kv, h->st, nullptr, presplit);
+  kv_product(op, m, Vfull, op.n, Y, op.rows, h->wk.kv, h->st, nullptr);
 }
 
-// The fused Lanczos step (lanczos_fused.cu) covers one GPU, the three-term recurrence (no
-// reorthogonalisation) and s <= 64 probes.  Opt-in (RLD_FUSED_LANCZOS=1): it measured no faster
-// than the separate kernels at config 2 (19.43 vs 19.32 ms per estimate).
-bool fused_enabled_for(int64_t s, int k) {
-  static const bool on = getenv("RLD_FUSED_LANCZOS") && getenv("RLD_FUSED_LANCZOS")[0] == '1';
-  return on && lanczos_fused_fits(s, k);
-}
 
 // ---- float64 products of the estimate outside K x V, on the FP64 tensor cores (kv_dmma.cu).
 // Both operands' rows must start 16-byte aligned (even leading dimensions: every BASELINE shape);
@@ -570,9 +573,6 @@ void qr_householder(rld_handle* h, int64_t n, int w, double* Y, double rtol, int
 
 void syevd(rld_handle* h, int k, double* A, double* evals) {
   Work& wk = h->wk;
-  // the preconditioner's B and C are positive semi-definite: one-cluster Jacobi for k <= 288 when
-  // opted in (RLD_SMALL_EIG=1; slower than DSYEVD, kept for measurement)
-  if (small_eigh(k, A, evals, wk.eig_scratch, nullptr, h->st)) return;
   // tridiagonalisation + multisection + inverse iteration (tri_eig.cu) for k <= 288, then
   // Newton-Schulz orthogonalisation of T's eigenvectors, Z <- 1.5 Z - 0.5 Z (Z^T Z) (symmetric in
   // the columns; the defect E = Z^T Z - I goes to ~0.75 E^2 per step), and the back-transformation,
@@ -944,7 +944,87 @@ PrecondOut build_preconditioner(rld_handle* h, const rld_config* c, const rld_in
   return out;
 }
 
+// build_preconditioner's argument checks (src/precond.py:47-55, 176-177, 241-242)
+void validate_precond(const rld_config* c, int64_t n) {
+  if (c->precond_rank < 0) fail(RLD_ERR_INVALID_ARGUMENT, "rank must be >= 0");
+  if (c->precond_iters < 1) fail(RLD_ERR_INVALID_ARGUMENT, "num_iters must be >= 1");
+  const int pk = c->precond_kind;
+  if (pk != RLD_PRECOND_IDENTITY && pk != RLD_PRECOND_DIAGONAL && pk != RLD_PRECOND_RANK_ONE && c->precond_rank > n)
+    fail(RLD_ERR_INVALID_ARGUMENT, "rank " + std::to_string(c->precond_rank) + " exceeds dimension " + std::to_string(n));
+  const bool randsvd = pk == RLD_PRECOND_RAND_SVD || pk == RLD_PRECOND_RAND_SVD_SCALED;
+  if (randsvd && c->precond_rank < 1)   // randomized_range_svd (src/precond.py:176-177)
+    fail(RLD_ERR_INVALID_ARGUMENT, "rank must be in 1.." + std::to_string(n) + ", got " + std::to_string(c->precond_rank));
+  if (!(c->precond_scale > 0) && (pk == RLD_PRECOND_RAND_SVD_SCALED || pk == RLD_PRECOND_PARTIAL_CHOLESKY_SCALED ||
+                                  pk == RLD_PRECOND_TRUNC_SVD_SCALED))
+    fail(RLD_ERR_INVALID_ARGUMENT, "scale must be positive");
+}
+
+// rld_precond_build: build_preconditioner(M, cfg, rng) on its own (src/precond.py:236-267), the
+// factors staying in the handle for rld_precond_apply; log det P and the kept rank read back.
+void precond_build(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_precond_info* out) {
+  NvtxRange nv("rld:precond_build");
+  Resident& r = h->res;
+  if (!r.ready) fail(RLD_ERR_INVALID_ARGUMENT, "no resident problem (call rld_prepare)");
+  if (!c || !out) fail(RLD_ERR_INVALID_ARGUMENT, "config / info is NULL");
+  rld_inputs none{};
+  if (!in) in = &none;
+  validate_precond(c, r.n);
+  Work& wk = h->wk;
+  wk.ints.reserve(sizeof(int) * 16);
+  wk.scal.reserve(sizeof(double) * 16);
+  RLD_CUDA(cudaMemsetAsync(wk.ints.ptr, 0, sizeof(int) * 8, h->st));
+  g_launches = 0;
+  const PrecondOut po = build_preconditioner(h, c, in);
+  double hs[2];
+  int hi[8];
+  RLD_CUDA(cudaMemcpyAsync(hs, wk.scal.ptr, sizeof hs, cudaMemcpyDeviceToHost, h->st));
+  RLD_CUDA(cudaMemcpyAsync(hi, wk.ints.ptr, sizeof hi, cudaMemcpyDeviceToHost, h->st));
+  RLD_CUDA(cudaStreamSynchronize(h->st));
+  int fl[1] = {hi[0]};
+  allreduce_flags(h, fl, 1);
+  if (fl[0] & RLD_FLAG_NOT_PD) fail(RLD_ERR_NOT_POSITIVE_DEFINITE, "Matrix is not positive definite (inner Cholesky)");
+  if (fl[0] & 8) fail(RLD_ERR_INVALID_ARGUMENT, "base diagonal must be strictly positive");
+  h->precond_k = po.k;
+  out->log_det = hs[0] + hs[1];
+  out->rank = po.k;
+  out->rank_kept = po.k > 0 ? hi[3] : 0;
+  out->attempts = po.attempts;
+  out->qr_fallback = po.householder ? 1 : 0;
+  out->kernel_launches = g_launches;
+}
+
+// rld_precond_apply: Y = op(V) for m rows V (m x n, device) with the factors of the last
+// preconditioner build: N^-1 (solve_sqrt, src/precond.py:102-108), N^-T (solve_sqrt_t,
+// src/precond.py:110-115) or P^-1 = N^-T N^-1.  One GPU.
+void precond_apply(rld_handle* h, int32_t op, int64_t m, const double* V, double* Y) {
+  if (h->precond_k < 0) fail(RLD_ERR_INVALID_ARGUMENT, "no preconditioner built (call rld_precond_build)");
+  if (h->world != 1) fail(RLD_ERR_NOT_SUPPORTED, "rld_precond_apply is single-GPU");
+  if (m < 1 || !V || !Y) fail(RLD_ERR_INVALID_ARGUMENT, "bad precond_apply arguments");
+  if (op < RLD_SOLVE_SQRT || op > RLD_SOLVE) fail(RLD_ERR_INVALID_ARGUMENT, "unknown precond op");
+  Work& wk = h->wk;
+  cudaStream_t st = h->st;
+  const int64_t n = h->res.n;
+  const int k = h->precond_k;
+  const double* U = wk.Z.as<double>();
+  const double* hv = wk.hgg.as<double>();
+  const double* sqrt_base = wk.sqrt_base.as<double>();
+  DevBuf& T = wk.Tg;
+  T.reserve(sizeof(double) * std::max<int64_t>(1, (int64_t)k * m));
+  copy_doubles(m * n, V, Y, st);
+  // N^-1 z = w + U (g o U^T w), w = z / sqrt(base);  N^-T x = (x + U (g o U^T x)) / sqrt(base);
+  // P^-1 u = (w + U (h o U^T w)) / sqrt(base), w = u / sqrt(base)
+  if (op != RLD_SOLVE_SQRT_T) scale_rows_colmajor(n, m, n, sqrt_base, true, Y, st);
+  if (k > 0) {
+    nt_f64(h, U, n, k, Y, n, m, n, T.as<double>(), k);
+    scale_rows_colmajor(k, m, k, op == RLD_SOLVE ? hv : hv + k, false, T.as<double>(), st);
+    ex_f64(h, T.as<double>(), k, k, m, U, n, n, Y, n, 1.0, 1.0);
+  }
+  if (op != RLD_SOLVE_SQRT) scale_rows_colmajor(n, m, n, sqrt_base, true, Y, st);
+  RLD_CUDA(cudaStreamSynchronize(st));
+}
+
 void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_result* res) {
+  NvtxRange nv("rld:estimate");
   Resident& r = h->res;
   if (!r.ready) fail(RLD_ERR_INVALID_ARGUMENT, "no resident problem (call rld_prepare or rld_logdet)");
   if (!c) fail(RLD_ERR_INVALID_ARGUMENT, "config is NULL");
@@ -966,15 +1046,7 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
   const int64_t n = r.n, nl = r.rows;
   const int64_t s = c->num_probes;
   const int t = (int)std::min<int64_t>(c->lanczos_iters, n);   // src/estimators.py:62
-  const int pk = c->precond_kind;
-  if (pk != RLD_PRECOND_IDENTITY && pk != RLD_PRECOND_DIAGONAL && pk != RLD_PRECOND_RANK_ONE && c->precond_rank > n)
-    fail(RLD_ERR_INVALID_ARGUMENT, "rank " + std::to_string(c->precond_rank) + " exceeds dimension " + std::to_string(n));
-  const bool randsvd = pk == RLD_PRECOND_RAND_SVD || pk == RLD_PRECOND_RAND_SVD_SCALED;
-  if (randsvd && c->precond_rank < 1)   // randomized_range_svd (src/precond.py:176-177)
-    fail(RLD_ERR_INVALID_ARGUMENT, "rank must be in 1.." + std::to_string(n) + ", got " + std::to_string(c->precond_rank));
-  if (!(c->precond_scale > 0) && (pk == RLD_PRECOND_RAND_SVD_SCALED || pk == RLD_PRECOND_PARTIAL_CHOLESKY_SCALED ||
-                                  pk == RLD_PRECOND_TRUNC_SVD_SCALED))
-    fail(RLD_ERR_INVALID_ARGUMENT, "scale must be positive");
+  validate_precond(c, n);
   cudaStream_t st = h->st;
   Work& wk = h->wk;
   wk.ints.reserve(sizeof(int) * (8 + 2 * s));
@@ -984,14 +1056,18 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
   RLD_CUDA(cudaEventRecord(h->ev[0], st));
 
   // ---- preconditioner
+  nvtxRangePushA("rld:preconditioner (sketch, QR, eigensolves, factors)");
   const PrecondOut po = build_preconditioner(h, c, in);
+  h->precond_k = po.k;
   RLD_CUDA(cudaEventRecord(h->ev[1], st));
   const int k = po.k;
   const double* U = wk.Z.as<double>();
   const double* hv = wk.hgg.as<double>();
   const double* sqrt_base = wk.sqrt_base.as<double>();
 
+  nvtxRangePop();
   // ---- probes (src/estimators.py:64)
+  nvtxRangePushA("rld:probes + Lanczos");
   wk.probes.reserve(sizeof(double) * s * nl);
   double* Zp = wk.probes.as<double>();
   if (in->probes) {
@@ -1103,42 +1179,7 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
     Pb = wk.pbasis.as<double>();
   }
   int products = 0;
-  const bool fused = h->world == 1 && !slq && !reorth && fused_enabled_for(s, k);
-  LanczosFusedArgs fa;
-  if (fused) {
-    const int64_t nch = ceil_div(nl, 128);
-    wk.lz_dotp.reserve(sizeof(double) * nch * s);
-    wk.lz_dotp2.reserve(sizeof(double) * nch * s);
-    KvOperand op = r.op();
-    op.tc_mode = 3;
-    static const bool presplit_on = !(getenv("RLD_FUSED_PRESPLIT") && getenv("RLD_FUSED_PRESPLIT")[0] == '0');
-    if (!presplit_on || !kv_tc_b_layout(op, s, wk.kv, fa.bl)) fa.bl = TcBLayout{};
-    fa.n = nl; fa.m = (int)s; fa.t = t; fa.rtol = c->breakdown_rtol;
-    fa.dotp = wk.lz_dotp.as<double>(); fa.dotp2 = wk.lz_dotp2.as<double>();
-    fa.live = live; fa.live_rw = live; fa.size = size;
-    fa.alpha = alpha; fa.beta = beta; fa.beta_ref = beta_ref;
-    fa.KX = KX; fa.sqrt_base = sqrt_base;
-    fa.p = p; fa.pp = pp; fa.u = u; fa.w = wv; fa.x = x;
-  }
   for (int j = 0; j < t; ++j) {
-    if (fused) {
-      kv(h, s, x, KX, 3, j > 0 && fa.bl.bhi != nullptr);   // x_j's operand written by the previous step
-      ++products;
-      lanczos_chunk_dots(nl, (int)s, x, KX, wk.lz_dotp.as<double>(), st);
-      if (j == t - 1) {
-        lanczos_alpha_chunks((int)s, nl, j, t, wk.lz_dotp.as<double>(), live, alpha, st);
-        break;
-      }
-      fa.j = j;
-      lanczos_fused_residual(fa, st);
-      if (k > 0) {   // w += U (h o (U^T w))
-        nt_f64(h, U, nl, k, wv, nl, s, nl, T, k);
-        scale_rows_colmajor(k, s, k, hv, false, T, st);
-        ex_f64(h, T, k, k, s, U, nl, nl, wv, nl, 1.0, 1.0);
-      }
-      lanczos_fused_finish(fa, st);
-      continue;
-    }
     if (slq || reorth) copy_doubles(s * nl, x, Qb + (size_t)j * s * nl, st);
     if (reorth) copy_doubles(s * nl, p, Pb + (size_t)j * s * nl, st);
     const double* xin = x;                                // one GPU: the local rows are the full rows
@@ -1198,6 +1239,8 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
     lanczos_advance(s, nl, j, t, beta, live, u, wv, p, pp, x, st);
   }
   RLD_CUDA(cudaEventRecord(h->ev[2], st));
+  nvtxRangePop();
+  NvtxRange nv_solves("rld:shifted solves + Hutchinson");
   if (slq)   // Gauss quadrature of log on each probe's T (src/estimators.py:110-116)
     slq_epilogue(s, t, alpha, beta, size, norms, 1e-300, per_probe, scal + 2, ints + 6, flags, st);
   else
@@ -1404,6 +1447,16 @@ int rld_build_covariance(rld_handle* h, const rld_problem* p, void* out, int32_t
     }
     RLD_CUDA(cudaStreamSynchronize(h->st));
   });
+}
+
+int rld_precond_build(rld_handle* h, const rld_config* cfg, const rld_inputs* inputs, rld_precond_info* info) {
+  if (!h) return RLD_ERR_INVALID_ARGUMENT;
+  return guarded(h, [&] { precond_build(h, cfg, inputs, info); });
+}
+
+int rld_precond_apply(rld_handle* h, int32_t op, int64_t m, const double* V, double* Y) {
+  if (!h) return RLD_ERR_INVALID_ARGUMENT;
+  return guarded(h, [&] { precond_apply(h, op, m, V, Y); });
 }
 
 int rld_kv_apply(rld_handle* h, int64_t m, const double* V, double* Y) {

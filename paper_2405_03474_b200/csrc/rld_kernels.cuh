@@ -17,29 +17,6 @@ enum : int {
 void normalize_rows(int64_t m, int64_t n, const double* z, const double* nrm2, double* norms, double* q,
                     cudaStream_t st);
 
-// Fused one-GPU Lanczos step (lanczos_fused.cu): everything between two K x X products.
-struct LanczosFusedArgs {
-  int64_t n = 0;
-  int m = 0, k = 0, j = 0, t = 0;
-  double rtol = 0.0;
-  const double* dotp = nullptr;    // [ceil(n/128)][m] chunk partials of x . K x
-  double* dotp2 = nullptr;         // [ceil(n/128)][m] chunk partials of u . z (out)
-  const int* live = nullptr;
-  int* live_rw = nullptr;
-  int* size = nullptr;
-  double *alpha = nullptr, *beta = nullptr, *beta_ref = nullptr;
-  const double *KX = nullptr, *sqrt_base = nullptr;
-  double *p = nullptr, *pp = nullptr, *u = nullptr, *w = nullptr, *x = nullptr;
-  TcBLayout bl;                    // bl.bhi == nullptr: no tensor-core operand to prepare
-};
-bool lanczos_fused_fits(int64_t s, int k);
-void lanczos_chunk_dots(int64_t n, int m, const double* a, const double* b, double* dotp, cudaStream_t st);
-void lanczos_alpha_chunks(int m, int64_t n, int j, int t, const double* dotp, const int* live, double* alpha,
-                          cudaStream_t st);
-// alpha_j + residual u, w = u / sqrt(base)   |   (w += U T by the caller)   |   z = w / sqrt(base),
-// beta_j, advance (and the next B operand)
-void lanczos_fused_residual(const LanczosFusedArgs& a, cudaStream_t st);
-void lanczos_fused_finish(const LanczosFusedArgs& a, cudaStream_t st);
 // u = KX - alpha_j p - beta_{j-1} p_prev (or u = KX when !three_term: the residual is then
 // reorthogonalised against the whole basis, src/lanczos.py:58-62); w = u / sqrt_base
 void lanczos_residual(int64_t m, int64_t n, int j, int t, const double* KX, const double* alpha,
@@ -80,11 +57,6 @@ void chol_logdet(int k, const double* L, const int* info, double* out, int* flag
 // out of range (caller falls back to cuSOLVER).  small_chol.cu
 // With Rinv != nullptr also writes R^-1 (upper, n x n, ld n, lower part zero).
 bool small_potrf_upper(int n, double* G, int ld, int* info, cudaStream_t st, double* Rinv = nullptr);
-// Eigenpairs of a symmetric positive semi-definite n x n matrix (n <= 288) on one 16-CTA cluster
-// (one-sided block Jacobi, small_eig.cu): eigenvalues ascending into w, eigenvectors over A
-// (column j <-> w[j]), as DSYEVD returns them up to signs.  false if n is out of range or the
-// solver is not enabled (opt-in RLD_SMALL_EIG=1: measured ~10x slower than DSYEVD).
-bool small_eigh(int n, double* A, double* w, DevBuf& scratch, int* sweeps, cudaStream_t st);
 // Eigen-decomposition of a symmetric n x n matrix (3 <= n <= 288) up to the last two steps
 // (tri_eig.cu): eigenvalues ascending into w; Z (n x n) = eigenvectors of the tridiagonal T from
 // inverse iteration (orthogonal up to eps |T| / gap: the caller runs one Cholesky-QR pass) and

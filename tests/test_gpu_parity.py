@@ -763,38 +763,6 @@ def test_dense_eigh_matches_lapack(rld, n, spectrum):
         assert np.linalg.norm(Pg - Pr) <= 1e-9
 
 
-def test_dense_eigh_cluster_jacobi_opt_in(rld):
-    """The opt-in one-cluster Jacobi eigensolver (RLD_SMALL_EIG=1, read once per process, so in a
-    subprocess) against LAPACK on a decaying and a degenerate spectrum."""
-    import os
-    import subprocess
-    import sys
-    from pathlib import Path
-
-    code = r"""
-import sys
-sys.path.insert(0, %r)
-sys.path.insert(0, %r)
-import numpy as np
-from test_gpu_parity import _dense_eigh
-for n, lam in [(266, np.logspace(7, -3, 266)), (64, np.repeat([5.0, 2.0, 2.0, 0.5], 16))]:
-    g = np.random.default_rng(n)
-    Q, _ = np.linalg.qr(g.standard_normal((n, n)))
-    A = (Q * lam) @ Q.T
-    A = (A + A.T) / 2
-    w, V = _dense_eigh(A)
-    wr = np.linalg.eigh(A)[0]
-    s = np.max(np.abs(wr))
-    assert np.max(np.abs(w - wr)) <= 1e-11 * s, (n, np.max(np.abs(w - wr)))
-    assert np.linalg.norm(V.T @ V - np.eye(n)) <= 1e-11 * np.sqrt(n)
-    assert np.linalg.norm((V * w) @ V.T - A) <= 1e-11 * np.linalg.norm(A)
-print("ok")
-""" % (str(Path(__file__).resolve().parent.parent), str(Path(__file__).resolve().parent))
-    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, RLD_SMALL_EIG="1"), capture_output=True,
-                       text=True, timeout=600)
-    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
-
-
 def test_tri_eigh_fallback_and_dsyevd_path(rld):
     """tri_eig.cu hands degenerate unreduced blocks to DSYEVD (reported with RLD_TRI_EIG_DEBUG=1)
     and keeps a well-separated spectrum; RLD_TRI_EIG=0 (DSYEVD always) agrees to rounding.  Flags
@@ -837,9 +805,8 @@ print("res", *out)
     np.testing.assert_allclose(a[3], b[3], rtol=1e-12)
 
 
-def test_opt_in_fused_lanczos_and_cholqr_paths_agree(rld):
-    """The opt-in / alternative one-GPU paths (RLD_FUSED_LANCZOS=1: fused Lanczos step with the
-    pre-split tensor-core operand; RLD_CHOLQR_GEMM=0: DTRSM CholQR; RLD_TC_CG2=0: single-CTA
+def test_alternative_paths_agree(rld):
+    """The alternative one-GPU paths (RLD_CHOLQR_GEMM=0: DTRSM CholQR; RLD_TC_CG2=0: single-CTA
     products; RLD_TRI_EIG=0: cuSOLVER DSYEVD instead of tri_eig.cu) give the default estimate to
     fp32 accuracy (flags are read once: subprocesses)."""
     import json
@@ -860,7 +827,7 @@ for idx, n in [(1, 1024), (2, 4096)]:
 print(json.dumps(out))
 """ % str(Path(__file__).resolve().parent.parent)
     runs = {}
-    for name, env in [("default", {}), ("fused", {"RLD_FUSED_LANCZOS": "1"}), ("trsm", {"RLD_CHOLQR_GEMM": "0"}),
+    for name, env in [("default", {}), ("trsm", {"RLD_CHOLQR_GEMM": "0"}),
                       ("single_cta", {"RLD_TC_CG2": "0"}), ("dsyevd", {"RLD_TRI_EIG": "0"})]:
         r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
                            timeout=600)
