@@ -98,3 +98,42 @@ def test_fp64_product_misaligned_operand(rld):
     K = O.covariance_block(wl.spec.family, wl.spec.amplitude, wl.spec.length_scale, wl.spec.jitter, wl.points)
     ref = V.cpu().numpy() @ K.T
     assert np.max(np.abs(Y - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+def test_fp64_product_under_concurrency(rld):
+    """Several handles issue DMMA products from their own host threads at once; every product is
+    checked against torch float64 (this stress found a shared-memory stage released before its
+    loads completed: rare single-row errors; compute-sanitizer is closed on this pool)."""
+    import threading
+
+    import torch
+
+    from paper_2405_03474_b200._session import worker_session
+    from paper_2405_03474_b200.workloads import baseline
+
+    wl = baseline(1)
+    M = rld.KernelMatrix(wl.spec, wl.points)
+    K = rld.build_covariance(wl.spec, wl.points, dtype="fp64")
+    torch.cuda.synchronize()
+    bad = []
+
+    def body(j):
+        with worker_session() as s:
+            R = rld.ResidentMatrix(M, dtype="fp64", path="stored", session=s)
+            g = torch.Generator(device="cuda").manual_seed(j)
+            for it in range(25):
+                m = (16, 74, 80, 266, 3)[(it + j) % 5]
+                V = torch.randn(m, wl.n, dtype=torch.float64, device="cuda", generator=g)
+                Y = R.kv_apply(V)
+                ref = V @ K.T
+                torch.cuda.synchronize()
+                e = float((Y - ref).abs().max() / ref.abs().max())
+                if e > 1e-13:
+                    bad.append((j, it, m, e))
+
+    ths = [threading.Thread(target=body, args=(j,)) for j in range(4)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not bad, bad[:5]
