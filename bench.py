@@ -92,7 +92,7 @@ def load_peaks():
 
 def load_pipe_peaks():
     """Measured compute-pipe peaks of this pool's B200 (scripts/pipe_peaks.cu, committed)."""
-    p = ROOT / "profiles" / "r01_pipe_peaks.json"
+    p = ROOT / "profiles" / "r02_pipe_peaks.json"
     return json.loads(p.read_text()) if p.exists() else {}
 
 
