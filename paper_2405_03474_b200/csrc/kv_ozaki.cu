@@ -1,0 +1,371 @@
+// Float64-accurate K x V on the INT8 tensor cores (tcgen05 kind::i8): exact integer slicing
+// ("Ozaki scheme").  The stored-K product of the float64 estimate (src/estimators.py:72,
+// src/precond.py:186, 189) at 3-4x the FP64 (DMMA) peak.
+//
+// Slicing (exact, deterministic):
+//   each row i of K gets sigma_i = 2^e with max_j |K_ij| < sigma_i <= 2 max_j |K_ij|, each vector c
+//   of V gets tau_c likewise; x = K_ij / sigma_i in (-1, 1) is cut into S = 8 signed 7-bit digits,
+//   d_s = trunc(128 r_s), r_{s+1} = 128 r_s - d_s (every step exact in float64):
+//       K_ij = sigma_i (sum_s d_s 2^{-7 (s+1)} + r_8 2^{-56}),   |d_s| <= 127,  |r_8| < 1.
+//   Then (K V^T)_ic = sigma_i tau_c sum_{s+t <= 7} 2^{-7 (s+t+2)} sum_j d_s[i,j] e_t[c,j] + err,
+//   36 int8 x int8 products accumulated EXACTLY in int32, combined in float64.  The dropped digits
+//   and slice pairs bound |err| <= ~2^-52 sigma_i tau_c per term of the j-sum: the float64 GEMM's
+//   own rounding level, scaled by the row / column maxima instead of the entries.
+//
+// Kernel (one CTA per SM, 256 threads; grid = column passes x row tiles x k splits):
+//   warp 0  producer: per 32-column k-step ONE bulk copy (TMA engine) of all 8 K slices' tile
+//           (8 x 128 rows x 32 B = 32 KB) and one of all 8 V slices' (8 x 64 vectors x 32 B), both
+//           stored pre-swizzled in the k-step-tiled global image (a 3-D TMA box with 32-byte rows
+//           moved 1536 32-byte rows per step and bound the product), 4-stage ring;
+//   warp 1  MMA issuer (one thread): the 36 slice pairs of a k-step as 12 tcgen05.mma kind::i8
+//           M = 128, K = 32, N = 64..256 from shared-memory descriptors -- A slice s against the
+//           stacked V slices 0..7-s, pair (s, t) landing in the int32 TMEM accumulator of its
+//           diagonal d = s + t (8 x 64 columns = all 512) -- and a commit frees the stage;
+//   warp 2  TMEM owner;
+//   warps 4-7 drain: after the CTA's k range (<= 16384 columns: the int32 bound, 8 pairs x 127^2 x
+//           16384 < 2^31) they read the 8 accumulators (thread = row), form sum_d 2^{-7(d+2)} I_d
+//           in float64, scale by sigma_i tau_c and store.
+// k splits (at least n / 16384 of them) write float64 partials that a fixed-order reduce adds
+// (deterministic).
+#include <cuda.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "rld_internal.cuh"
+#include "tc_ptx.cuh"
+
+namespace rld {
+
+namespace {
+
+constexpr int OZ_S = 8;             // digits per operand
+constexpr int OZ_DIAG = 8;          // diagonals d = s + t kept: 0 .. 7 (36 pairs)
+constexpr int OZ_BM = 128;          // K rows per tile (UMMA M)
+constexpr int OZ_BN = 64;           // vectors per column pass (UMMA N)
+constexpr int OZ_BK = 32;           // int8 columns per k-step (UMMA K for kind::i8, one 32-byte row)
+constexpr int OZ_STAGES = 4;
+constexpr int64_t OZ_KMAX = 16384;  // columns per CTA: 8 pairs x 127^2 x 16384 < 2^31 (exact int32)
+constexpr int OZ_THREADS = 256;
+constexpr uint32_t OZ_A_SLICE = OZ_BM * OZ_BK;            // 4 KB
+constexpr uint32_t OZ_B_SLICE = OZ_BN * OZ_BK;            // 2 KB
+constexpr uint32_t OZ_A_BYTES = OZ_S * OZ_A_SLICE;        // 32 KB
+constexpr uint32_t OZ_STAGE = OZ_A_BYTES + OZ_S * OZ_B_SLICE;   // 48 KB
+constexpr int OZ_SMEM = OZ_STAGES * OZ_STAGE + 1024 + 256;
+constexpr uint32_t OZ_TMEM_COLS = OZ_DIAG * OZ_BN;        // 512
+
+// UMMA shared-memory descriptor: K-major operand, 32-byte swizzle atoms (8 rows x 32 B), 8-row
+// groups 256 B apart -- the layout TMA writes for a box with a 32-byte inner dimension and
+// CU_TENSOR_MAP_SWIZZLE_32B.
+__device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);   // start address
+  d |= (uint64_t)1 << 16;                    // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(256 >> 4) << 32;           // stride byte offset: 8 rows x 32 B
+  d |= (uint64_t)1 << 46;                    // descriptor version (sm100)
+  d |= (uint64_t)6 << 61;                    // layout: SWIZZLE_32B
+  return d;
+}
+
+// kind::i8 instruction descriptor: D s32, A and B s8, K-major, M = 128, N
+constexpr uint32_t idesc_i8(int M, int N) {
+  return (2u << 4)                       // c_format S32
+         | (1u << 7)                     // a_format S8 (signed)
+         | (1u << 10)                    // b_format S8
+         | ((uint32_t)(N >> 3) << 17)    // n_dim
+         | ((uint32_t)(M >> 4) << 24);   // m_dim
+}
+
+__device__ __forceinline__ void mma_i8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   ptx::smem_u32(smem_dst)),
+               "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(ptx::smem_u32(bar))
+               : "memory");
+}
+
+// ---------------------------------------------------------------------------------------------
+// Slicing.  Global layout = the shared-memory image of one k-step: for tile t (TR rows) and k-step
+// ks (32 columns) the 8 slices' [TR][32]-byte tiles are contiguous, ((t KS + ks) 8 + s) TR 32 bytes,
+// each already in the 32-byte-swizzle order (Swizzle<1,4,3>: the two 16-byte halves of a row swap
+// in rows 4..7 of every 8-row atom) the UMMA descriptor expects -- so a stage is ONE bulk copy.
+// Rows >= rows and columns >= n are zero.
+
+// scale[row] = sigma = 2^e with max_j |A_row,j| < sigma <= 2 max (1 for an all-zero row)
+__global__ void ozaki_scale_kernel(const double* __restrict__ A, int64_t lda, int64_t n, double* __restrict__ scale) {
+  const int64_t row = blockIdx.x;
+  const double* a = A + row * lda;
+  double mx = 0.0;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) mx = fmax(mx, fabs(a[j]));
+  __shared__ double red[32];
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
+    int e = 0;
+    if (mx > 0.0) frexp(mx, &e);            // mx = f 2^e, f in [0.5, 1)
+    scale[row] = mx > 0.0 ? ldexp(1.0, e) : 1.0;
+  }
+}
+
+// one thread per (padded row, column) of the tiled image: 8 exact 7-bit digits of A / sigma
+template <int TR>
+__global__ void ozaki_digits_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int64_t n,
+                                    const double* __restrict__ scale, int64_t KS, int8_t* __restrict__ q) {
+  const int64_t total = ceil_div(rows, TR) * TR * KS * OZ_BK;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % OZ_BK);
+    const int64_t ks = (e / OZ_BK) % KS;
+    const int64_t row = e / (OZ_BK * KS);
+    const int64_t t = row / TR;
+    const int i = (int)(row % TR);
+    const int64_t j = ks * OZ_BK + c;
+    double r = (row < rows && j < n) ? A[row * lda + j] / scale[row] : 0.0;   // exact: power of two
+    const uint32_t o = (uint32_t)(i * OZ_BK + c);
+    const uint32_t phys = o ^ (((o >> 7) & 1u) << 4);
+    int8_t* base = q + (t * KS + ks) * (int64_t)OZ_S * TR * OZ_BK + phys;
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s) {
+      const double x = r * 128.0;           // exact
+      const double d = trunc(x);            // |d| <= 127
+      r = x - d;                            // exact
+      base[(int64_t)s * TR * OZ_BK] = (int8_t)(int)d;
+    }
+  }
+}
+
+__global__ void oz_split_reduce_kernel(const double* __restrict__ part, int splits, int64_t stride, int64_t m,
+                                       int64_t rows, double* __restrict__ out, int64_t ldo) {
+  const int64_t total = m * rows;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < splits; ++k) s += part[k * stride + e];
+    out[(e / rows) * ldo + e % rows] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, int64_t KS,
+                const double* __restrict__ sigma, const double* __restrict__ tau, int64_t rows, int64_t m, int64_t n,
+                int64_t kchunk, double* __restrict__ out, int64_t ldo, int64_t split_stride) {
+  extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OZ_STAGES * OZ_STAGE);
+  uint64_t* empty = full + OZ_STAGES;
+  uint64_t* accfull = empty + OZ_STAGES;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t col0 = (int64_t)blockIdx.x * OZ_BN;
+  const int64_t row0 = (int64_t)blockIdx.y * OZ_BM;
+  const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
+  const int64_t kend = min64(n, kbeg + kchunk);
+  const int steps = (int)ceil_div(max64(kend - kbeg, 0), OZ_BK);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < OZ_STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    ptx::mbar_init(accfull, 1);
+    ptx::fence_mbarrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tmem_holder, OZ_TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {   // ---- producer: one bulk copy of the A image and one of the B image per k-step
+    if (ptx::elect_one()) {
+      const int8_t* ga = Aq + ((int64_t)blockIdx.y * KS + kbeg / OZ_BK) * OZ_A_BYTES;
+      const int8_t* gb = Bq + ((int64_t)blockIdx.x * KS + kbeg / OZ_BK) * (OZ_STAGE - OZ_A_BYTES);
+      for (int s = 0; s < steps; ++s) {
+        const int st = s % OZ_STAGES;
+        if (s >= OZ_STAGES) ptx::mbar_wait(&empty[st], ((s / OZ_STAGES) - 1) & 1);
+        unsigned char* dst = smem + st * OZ_STAGE;
+        ptx::mbar_arrive_expect_tx(&full[st], OZ_STAGE);
+        bulk_load(dst, ga + (int64_t)s * OZ_A_BYTES, OZ_A_BYTES, &full[st]);
+        bulk_load(dst + OZ_A_BYTES, gb + (int64_t)s * (OZ_STAGE - OZ_A_BYTES), OZ_STAGE - OZ_A_BYTES, &full[st]);
+      }
+    }
+  } else if (warp == 1) {   // ---- MMA issuer
+    if (ptx::elect_one()) {
+      const uint32_t sbase = ptx::smem_u32(smem);
+      for (int s = 0; s < steps; ++s) {
+        const int st = s % OZ_STAGES;
+        ptx::mbar_wait(&full[st], (uint32_t)((s / OZ_STAGES) & 1));
+        ptx::tc_fence_after();
+        const uint32_t a0 = sbase + st * OZ_STAGE;
+        const uint32_t b0 = a0 + OZ_A_BYTES;
+        // A slice sa against the stacked B slices 0 .. 7 - sa at once: the accumulators of the
+        // diagonals d = sa + t are adjacent TMEM column blocks, so one N = 64 (8 - sa) product
+        // (in N <= 256 pieces) covers the whole row of pairs -- 12 MMAs per k-step instead of 36
+        // N = 64 ones, and the A operand is read from shared memory once per piece
+#pragma unroll
+        for (int sa = 0; sa < OZ_S; ++sa) {
+          const uint64_t adesc = desc_sw32(a0 + sa * OZ_A_SLICE);
+          const uint32_t acc = (s > 0 || sa > 0) ? 1u : 0u;
+#pragma unroll
+          for (int t0 = 0; t0 < OZ_DIAG - sa; t0 += 4) {
+            const int nb = (OZ_DIAG - sa - t0) < 4 ? (OZ_DIAG - sa - t0) : 4;   // B slices in this piece
+            mma_i8_ss(tmem + (uint32_t)((sa + t0) * OZ_BN), adesc, desc_sw32(b0 + t0 * OZ_B_SLICE),
+                      idesc_i8(OZ_BM, nb * OZ_BN), acc);
+          }
+        }
+        ptx::tc_commit(&empty[st]);   // the stage is free once these MMAs have read it
+      }
+      if (steps > 0) ptx::tc_commit(accfull);
+    }
+  } else if (warp >= 4) {   // ---- drains: thread = row (TMEM lane); one drain (k range <= OZ_KMAX)
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const int64_t r = row0 + row;
+    double* o = out + (int64_t)blockIdx.z * split_stride;
+    if (steps > 0) {
+      ptx::mbar_wait_sleep(accfull, 0);
+      ptx::tc_fence_after();
+    }
+    const double sg = (r < rows) ? sigma[r] : 0.0;
+#pragma unroll 1
+    for (int c0 = 0; c0 < OZ_BN; c0 += 32) {
+      double part[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) part[e] = 0.0;
+      if (steps > 0) {
+#pragma unroll 1
+        for (int d = OZ_DIAG - 1; d >= 0; --d) {   // small terms first
+          const double w = __longlong_as_double((long long)(1023 - 7 * (d + 2)) << 52);   // 2^{-7(d+2)}
+          uint32_t v[32];
+          ptx::tmem_ld_32x32b_x32(tmem + lane_base + (uint32_t)(d * OZ_BN + c0), v);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) part[e] = fma(w, (double)(int32_t)v[e], part[e]);
+        }
+      }
+      if (r < rows) {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int64_t cc = col0 + c0 + e;
+          if (cc < m) o[cc * ldo + r] = part[e] * sg * tau[cc];
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) ptx::tmem_dealloc(tmem, OZ_TMEM_COLS);
+}
+
+int oz_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    RLD_CUDA(cudaGetDevice(&dev));
+    RLD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return sms;
+}
+
+}  // namespace
+
+int64_t ozaki_bytes(int64_t rows, int64_t n, int tile_rows) {
+  return ceil_div(rows, tile_rows) * tile_rows * ceil_div(n, OZ_BK) * OZ_BK * OZ_S;
+}
+
+bool fp64_product_ozaki() {
+  static const bool on = [] {
+    const char* e = getenv("RLD_FP64_PRODUCT");
+    return e && std::string(e) == "ozaki";
+  }();
+  return on;
+}
+
+void ozaki_slice(const double* A, int64_t lda, int64_t rows, int64_t n, int tile_rows, int8_t* q, double* scale,
+                 cudaStream_t st) {
+  if (rows <= 0) return;
+  if (rows > 2147483647LL) fail(RLD_ERR_NOT_SUPPORTED, "ozaki_slice: too many rows");
+  ozaki_scale_kernel<<<(unsigned)rows, 256, 0, st>>>(A, lda, n, scale);
+  RLD_LAUNCH_CHECK();
+  const int64_t KS = ceil_div(n, OZ_BK);
+  const int64_t total = ceil_div(rows, tile_rows) * tile_rows * KS * OZ_BK;
+  const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)oz_sms() * 16);
+  if (tile_rows == OZ_BM)
+    ozaki_digits_kernel<OZ_BM><<<blocks, 256, 0, st>>>(A, lda, rows, n, scale, KS, q);
+  else if (tile_rows == OZ_BN)
+    ozaki_digits_kernel<OZ_BN><<<blocks, 256, 0, st>>>(A, lda, rows, n, scale, KS, q);
+  else
+    fail(RLD_ERR_INVALID_ARGUMENT, "ozaki_slice: tile rows must be 128 (K) or 64 (V)");
+  RLD_LAUNCH_CHECK();
+}
+
+// Y (m x rows, ld ldy) = V K^T with K given by its sliced image Kq (ozaki_slice, 128-row tiles) and
+// row scales; V (m x n float64 rows, ld ldv) is sliced here (64-vector tiles) into ws.oz_vq.
+void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int64_t n, const double* V, int64_t ldv,
+                      int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st) {
+  if (m <= 0 || rows <= 0) return;
+  ws.oz_vq.reserve((size_t)ozaki_bytes(m, n, OZ_BN));
+  ws.oz_tau.reserve(sizeof(double) * m);
+  ozaki_slice(V, ldv, m, n, OZ_BN, ws.oz_vq.as<int8_t>(), ws.oz_tau.as<double>(), st);
+  static bool attr = false;
+  if (!attr) {
+    RLD_CUDA(cudaFuncSetAttribute(ozaki_kv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM));
+    attr = true;
+  }
+  const int64_t KS = ceil_div(n, OZ_BK);
+  const int64_t passes = ceil_div(m, OZ_BN), tiles = ceil_div(rows, OZ_BM);
+  const int64_t units0 = passes * tiles;
+  const int64_t slots = oz_sms();
+  // k splits: every CTA <= OZ_KMAX columns (exact int32), >= 64 k-steps; the fewest splits whose
+  // CTA count fills >= 95 % of whole waves
+  const int64_t min_s = ceil_div(n, OZ_KMAX);
+  const int64_t max_s = std::max<int64_t>(min_s, n / (OZ_BK * 64));
+  int64_t splits = min_s;
+  double best = 0.0;
+  for (int64_t s = min_s; s <= std::min<int64_t>(max_s, min_s + 64); ++s) {
+    const int64_t u = units0 * s, waves = ceil_div(u, slots);
+    const double eff = (double)u / (double)(waves * slots);
+    if (eff > best + 1e-9) {
+      best = eff;
+      splits = s;
+    }
+    if (eff >= 0.95 && waves >= 2) break;
+  }
+  const int64_t kchunk = ceil_div(ceil_div(n, splits), OZ_BK) * OZ_BK;
+  splits = ceil_div(n, kchunk);
+  dim3 grid((unsigned)passes, (unsigned)tiles, (unsigned)splits);
+  if (grid.y > 65535u || grid.z > 65535u) fail(RLD_ERR_NOT_SUPPORTED, "kv_product_ozaki: grid too large");
+  const int8_t* Bq = ws.oz_vq.as<int8_t>();
+  if (splits == 1) {
+    ozaki_kv_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(Kq, Bq, KS, ksigma, ws.oz_tau.as<double>(), rows, m, n, kchunk,
+                                                      Y, ldy, 0);
+    RLD_LAUNCH_CHECK();
+    return;
+  }
+  const int64_t stride = m * rows;
+  ws.partial.reserve(sizeof(double) * stride * splits);
+  ozaki_kv_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(Kq, Bq, KS, ksigma, ws.oz_tau.as<double>(), rows, m, n, kchunk,
+                                                    ws.partial.as<double>(), rows, stride);
+  RLD_LAUNCH_CHECK();
+  const int blocks = (int)std::min<int64_t>(ceil_div(stride, 256), slots * 8);
+  oz_split_reduce_kernel<<<blocks, 256, 0, st>>>(ws.partial.as<double>(), (int)splits, stride, m, rows, Y, ldy);
+  RLD_LAUNCH_CHECK();
+}
+
+}  // namespace rld

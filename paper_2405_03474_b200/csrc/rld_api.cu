@@ -93,6 +93,8 @@ struct Resident {
   DevBuf X;                  // points n x d
   DevBuf pts4;               // points split to n x 8 fp32 hi/lo (d <= 4; tensor-core on-the-fly tiles)
   DevBuf diag;               // local diagonal of K (float64)
+  DevBuf Kq, ksigma;         // float64 K as exact int8 slices (RLD_FP64_PRODUCT=ozaki, kv_ozaki.cu)
+  bool kq_ready = false;
   KernelParams kp{};
 
   KvOperand op() const {
@@ -104,6 +106,10 @@ struct Resident {
     o.pts4 = (source == RLD_SOURCE_POINTS && d <= 4) ? pts4.as<float>() : nullptr;
     o.kp = kp;
     o.dtype = dtype;
+    if (kq_ready && path != RLD_PATH_ON_THE_FLY) {
+      o.kq = Kq.as<int8_t>();
+      o.ksigma = ksigma.as<double>();
+    }
     o.n = n;
     o.row0 = row0;
     o.rows = rows;
@@ -338,6 +344,15 @@ void prepare(rld_handle* h, const rld_problem* p) {
       diag_of_dense(r.rows, r.row0, r.K, r.ldk, p->dtype, r.diag.as<double>(), st);
   } else {
     fail(RLD_ERR_INVALID_ARGUMENT, "unknown source");
+  }
+  r.kq_ready = false;
+  if (r.path == RLD_PATH_STORED && r.dtype == RLD_FP64 && fp64_product_ozaki() && r.rows > 0) {
+    // exact int8 slices of the stored float64 rows for the INT8 tensor-core product (kv_ozaki.cu)
+    r.Kq.reserve((size_t)ozaki_bytes(r.rows, r.n, 128));
+    r.ksigma.reserve(sizeof(double) * r.rows);
+    ozaki_slice(static_cast<const double*>(r.K), r.ldk, r.rows, r.n, 128, r.Kq.as<int8_t>(), r.ksigma.as<double>(),
+                st);
+    r.kq_ready = true;
   }
   RLD_CUDA(cudaStreamSynchronize(st));
   r.ready = true;

@@ -88,6 +88,8 @@ struct KvOperand {
   const float* pts4 = nullptr;  // points as n x 8 fp32 (hi x,y,z,w; lo x,y,z,w) for the tensor-core on-the-fly path, d <= 4
   KernelParams kp{};
   int dtype = RLD_FP64;      // product arithmetic
+  const int8_t* kq = nullptr;      // float64 K as 8 exact int8 slices, k-step-tiled image (kv_ozaki.cu), or null
+  const double* ksigma = nullptr;  // per-row power-of-two scales of the slices
   int64_t n = 0;             // columns of K (global order)
   int64_t row0 = 0;          // first global row held locally
   int64_t rows = 0;          // local rows
@@ -101,6 +103,7 @@ struct KvWorkspace {
   DevBuf tc_partial;  // stream-K partial accumulators
   DevBuf tc_sync;     // epoch-barrier counters of the tensor-core kernel
   cublasHandle_t blas = nullptr;   // the handle's cuBLAS (bound to the same stream): fp64 stored K
+  DevBuf oz_vq, oz_tau;            // int8 slices of V and their column scales (kv_ozaki.cu)
 };
 
 bool kv_tc_supported(const KvOperand& op);
@@ -135,6 +138,15 @@ void gemm_nt_f64(const double* A, int64_t lda, int64_t p, const double* B, int64
 // layout (the expansions U T, Q R^-1, Q^T V of the preconditioner and its Woodbury apply).
 void gemm_expand_f64(const double* S, int64_t lds, int64_t p, int64_t q, const double* X, int64_t ldx, int64_t N,
                      double* C, int64_t ldc, double alpha, double beta, cudaStream_t st);
+
+// Float64-accurate products on the INT8 tensor cores (kv_ozaki.cu): exact 8 x 7-bit slicing.
+int64_t ozaki_bytes(int64_t rows, int64_t n, int tile_rows);   // size of a sliced image (tiles of 128 / 64 rows)
+void ozaki_slice(const double* A, int64_t lda, int64_t rows, int64_t n, int tile_rows, int8_t* q, double* scale,
+                 cudaStream_t st);
+void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int64_t n, const double* V, int64_t ldv,
+                      int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st);
+// Which float64 stored-K product runs: RLD_FP64_PRODUCT = "ozaki" (int8 slices) or "dmma".
+bool fp64_product_ozaki();
 
 // ---------------------------------------------------------------------------
 // RNG
