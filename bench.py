@@ -469,8 +469,23 @@ def roofline_for(wl, cfg, rows, n, s, kv_ms, world):
     """Roofline of the dominant kernel (K x block, Lanczos shape m = s), SURVEY.md §8(d)."""
     es = 4 if cfg.dtype == "fp32" else 8
     pipe = load_pipe_peaks()
-    key = f"kv_product|{cfg.dtype}|{wl.path}|n={n}|rows={rows}|m={s}"
+    ozaki = cfg.dtype == "fp64" and wl.path == "stored" and os.environ.get("RLD_FP64_PRODUCT") != "dmma"
+    key = f"kv_product|{cfg.dtype}{'-int8slices' if ozaki else ''}|{wl.path}|n={n}|rows={rows}|m={s}"
     traffic, traffic_src = ncu_traffic(key)
+    if ozaki:
+        # float64-accurate product on the INT8 tensor cores (kv_ozaki.cu): K streams as its 8 exact
+        # int8 slices, 8 bytes per entry like a float64 K; 36 slice-pair int8 products per useful
+        # multiply-add (4.0e13 int8 ops at config 3, m = 64: under the int8 tensor peak's time), so
+        # HBM bounds it
+        alg_bytes = 8 * rows * n + 8 * n * s + 8 * rows * s
+        hbm_peak, _, peak_kind = load_peaks()
+        achieved = alg_bytes / (kv_ms * 1e-3) / 1e9
+        return {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                "traffic": traffic, "traffic_source": traffic_src, "traffic_key": key,
+                "kernel": f"kv_product (tcgen05 kind::i8 on exact int8 slices of float64 K, m=s={s}, {rows} rows)",
+                "kernel_ms": kv_ms, "alg_bytes": alg_bytes, "equiv_fp64_tflops": 2.0 * rows * n * s / (kv_ms * 1e-3) / 1e12,
+                "int8_ops": 36 * 2.0 * rows * n * (-(-s // 64) * 64),
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}
     if wl.path == "stored" and cfg.dtype == "fp32":
         alg_bytes = es * rows * n + 4 * n * s + 8 * rows * s
         hbm_peak, _, peak_kind = load_peaks()

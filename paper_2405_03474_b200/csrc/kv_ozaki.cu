@@ -3,10 +3,12 @@
 // src/precond.py:186, 189) at 3-4x the FP64 (DMMA) peak.
 //
 // Slicing (exact, deterministic):
-//   each row i of K gets sigma_i = 2^e with max_j |K_ij| < sigma_i <= 2 max_j |K_ij|, each vector c
-//   of V gets tau_c likewise; x = K_ij / sigma_i in (-1, 1) is cut into S = 8 signed 7-bit digits,
-//   d_s = trunc(128 r_s), r_{s+1} = 128 r_s - d_s (every step exact in float64):
-//       K_ij = sigma_i (sum_s d_s 2^{-7 (s+1)} + r_8 2^{-56}),   |d_s| <= 127,  |r_8| < 1.
+//   each row i of K gets sigma_i = 2^e with 2 max_j |K_ij| < sigma_i <= 4 max_j |K_ij|, each vector
+//   c of V gets tau_c likewise; x = K_ij / sigma_i in (-1/2, 1/2) is cut into S = 8 signed digits
+//   d_s = rint(128 r_s), r_0 = x, r_{s+1} = 128 r_s - d_s (every step exact in float64):
+//       K_ij = sigma_i (sum_s d_s 2^{-7 (s+1)} + r_8 2^{-56}),   |d_s| <= 64,  |r_8| <= 1/2
+//   (round-to-nearest digits leave unbiased remainders, so the dropped terms do not add up
+//   coherently over the n-term sums).
 //   Then (K V^T)_ic = sigma_i tau_c sum_{s+t <= 7} 2^{-7 (s+t+2)} sum_j d_s[i,j] e_t[c,j] + err,
 //   36 int8 x int8 products accumulated EXACTLY in int32, combined in float64.  The dropped digits
 //   and slice pairs bound |err| <= ~2^-52 sigma_i tau_c per term of the j-sum: the float64 GEMM's
@@ -22,10 +24,10 @@
 //           stacked V slices 0..7-s, pair (s, t) landing in the int32 TMEM accumulator of its
 //           diagonal d = s + t (8 x 64 columns = all 512) -- and a commit frees the stage;
 //   warp 2  TMEM owner;
-//   warps 4-7 drain: after the CTA's k range (<= 16384 columns: the int32 bound, 8 pairs x 127^2 x
-//           16384 < 2^31) they read the 8 accumulators (thread = row), form sum_d 2^{-7(d+2)} I_d
+//   warps 4-7 drain: after the CTA's k range (<= 32768 columns: the int32 bound, 8 pairs x 64^2 x
+//           32768 = 2^30) they read the 8 accumulators (thread = row), form sum_d 2^{-7(d+2)} I_d
 //           in float64, scale by sigma_i tau_c and store.
-// k splits (at least n / 16384 of them) write float64 partials that a fixed-order reduce adds
+// k splits (at least n / 32768 of them) write float64 partials that a fixed-order reduce adds
 // (deterministic).
 #include <cuda.h>
 
@@ -45,7 +47,7 @@ constexpr int OZ_BM = 128;          // K rows per tile (UMMA M)
 constexpr int OZ_BN = 64;           // vectors per column pass (UMMA N)
 constexpr int OZ_BK = 32;           // int8 columns per k-step (UMMA K for kind::i8, one 32-byte row)
 constexpr int OZ_STAGES = 4;
-constexpr int64_t OZ_KMAX = 16384;  // columns per CTA: 8 pairs x 127^2 x 16384 < 2^31 (exact int32)
+constexpr int64_t OZ_KMAX = 32768;  // columns per CTA: <= 8 pairs x 64^2 x 32768 = 2^30 < 2^31 (exact int32)
 constexpr int OZ_THREADS = 256;
 constexpr uint32_t OZ_A_SLICE = OZ_BM * OZ_BK;            // 4 KB
 constexpr uint32_t OZ_B_SLICE = OZ_BN * OZ_BK;            // 2 KB
@@ -103,7 +105,7 @@ __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint
 // in rows 4..7 of every 8-row atom) the UMMA descriptor expects -- so a stage is ONE bulk copy.
 // Rows >= rows and columns >= n are zero.
 
-// scale[row] = sigma = 2^e with max_j |A_row,j| < sigma <= 2 max (1 for an all-zero row)
+// scale[row] = sigma = 2^e with 2 max_j |A_row,j| < sigma <= 4 max (1 for an all-zero row)
 __global__ void ozaki_scale_kernel(const double* __restrict__ A, int64_t lda, int64_t n, double* __restrict__ scale) {
   const int64_t row = blockIdx.x;
   const double* a = A + row * lda;
@@ -116,8 +118,8 @@ __global__ void ozaki_scale_kernel(const double* __restrict__ A, int64_t lda, in
   if (threadIdx.x == 0) {
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
     int e = 0;
-    if (mx > 0.0) frexp(mx, &e);            // mx = f 2^e, f in [0.5, 1)
-    scale[row] = mx > 0.0 ? ldexp(1.0, e) : 1.0;
+    if (mx > 0.0) frexp(mx, &e);            // mx = f 2^e, f in [0.5, 1): |a| / 2^(e+1) < 1/2
+    scale[row] = mx > 0.0 ? ldexp(1.0, e + 1) : 1.0;
   }
 }
 
@@ -139,9 +141,9 @@ __global__ void ozaki_digits_kernel(const double* __restrict__ A, int64_t lda, i
     int8_t* base = q + (t * KS + ks) * (int64_t)OZ_S * TR * OZ_BK + phys;
 #pragma unroll
     for (int s = 0; s < OZ_S; ++s) {
-      const double x = r * 128.0;           // exact
-      const double d = trunc(x);            // |d| <= 127
-      r = x - d;                            // exact
+      const double x = r * 128.0;                  // exact
+      const double d = rint(x);                    // |d| <= 64 (|r| <= 1/2 throughout)
+      r = x - d;                                   // exact
       base[(int64_t)s * TR * OZ_BK] = (int8_t)(int)d;
     }
   }
@@ -289,12 +291,10 @@ int64_t ozaki_bytes(int64_t rows, int64_t n, int tile_rows) {
   return ceil_div(rows, tile_rows) * tile_rows * ceil_div(n, OZ_BK) * OZ_BK * OZ_S;
 }
 
+// Read at every prepare, so a process can compare both products.  Default: the int8 slices.
 bool fp64_product_ozaki() {
-  static const bool on = [] {
-    const char* e = getenv("RLD_FP64_PRODUCT");
-    return e && std::string(e) == "ozaki";
-  }();
-  return on;
+  const char* e = getenv("RLD_FP64_PRODUCT");
+  return !(e && std::string(e) == "dmma");
 }
 
 void ozaki_slice(const double* A, int64_t lda, int64_t rows, int64_t n, int tile_rows, int8_t* q, double* scale,

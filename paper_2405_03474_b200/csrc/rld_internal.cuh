@@ -145,7 +145,8 @@ void ozaki_slice(const double* A, int64_t lda, int64_t rows, int64_t n, int tile
                  cudaStream_t st);
 void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int64_t n, const double* V, int64_t ldv,
                       int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st);
-// Which float64 stored-K product runs: RLD_FP64_PRODUCT = "ozaki" (int8 slices) or "dmma".
+// Which float64 stored-K product a prepare sets up: the int8 slices (default) or, with
+// RLD_FP64_PRODUCT=dmma, the DMMA kernel on the float64 K.
 bool fp64_product_ozaki();
 
 // ---------------------------------------------------------------------------

@@ -10,7 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2405_03474_b200 as rld  # noqa: E402
 from paper_2405_03474_b200.workloads import baseline  # noqa: E402
 
-assert os.environ.get("RLD_FP64_PRODUCT") == "ozaki"
+assert os.environ.get("RLD_FP64_PRODUCT", "ozaki") == "ozaki"
 shapes = sys.argv[1].split(",") if len(sys.argv) > 1 else ["1:2048:16", "2:4099:37", "2:16384:32", "2:16384:266"]
 for sh in shapes:
     cfg, n, m = (int(x) for x in sh.split(":"))

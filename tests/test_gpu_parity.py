@@ -576,12 +576,16 @@ def test_perfect_preconditioner_kills_stochastic_part(rld, kind, path):
     assert rel(est.value, O.cholesky_logdet(K)) <= 1e-8
 
 
-def test_partial_cholesky_on_the_fly_matches_stored(rld):
+def test_partial_cholesky_on_the_fly_matches_stored(rld, monkeypatch):
     """The pivoted partial Cholesky reads K columns from the stored K or generates them
-    from the points: same pivots, same preconditioner; stored fp64 K.V runs on the DMMA kernel,
-    the on-the-fly product on the DFMA kernel.  Both float64: 1e-9 (measured: identical)."""
+    from the points: same pivots, same preconditioner.  With the stored product on the DMMA
+    kernel (float64 GEMM) and the on-the-fly one on the DFMA kernel: 1e-9 (measured: identical).
+    With the default INT8-slice product the floored base (1e-12 on the 64 pivot rows) amplifies its
+    sigma-scaled rounding (~2^-52 n max|K| max|V| per entry) ~1e12-fold through N^-1 K N^-T:
+    5.6e-8, held to the fp64 bar."""
     from paper_2405_03474_b200.workloads import baseline
 
+    monkeypatch.setenv("RLD_FP64_PRODUCT", "dmma")
     wl = baseline(5, n=2048)
     cfg = replace(wl.config, dtype="fp64", num_probes=8,
                   precond=rld.PreconditionerConfig("partial-cholesky", 64, 5))
@@ -589,6 +593,10 @@ def test_partial_cholesky_on_the_fly_matches_stored(rld):
     b = rld.rstar_logdet(rld.KernelMatrix(wl.spec, wl.points), replace(cfg, path="on_the_fly"))
     assert rel(a.logdet_P, b.logdet_P) <= 1e-9
     assert rel(a.value, b.value) <= 1e-9
+    monkeypatch.setenv("RLD_FP64_PRODUCT", "ozaki")
+    c = rld.rstar_logdet(rld.KernelMatrix(wl.spec, wl.points), replace(cfg, path="stored"))
+    assert rel(c.logdet_P, b.logdet_P) <= 1e-9
+    assert rel(c.value, b.value) <= TOL["fp64"]
 
 
 # ---------------------------------------------------------------- normal-orthogonal probes
