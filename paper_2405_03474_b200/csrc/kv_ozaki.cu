@@ -123,29 +123,43 @@ __global__ void ozaki_scale_kernel(const double* __restrict__ A, int64_t lda, in
   }
 }
 
-// one thread per (padded row, column) of the tiled image: 8 exact 7-bit digits of A / sigma
+// one thread per (padded row, 16-column half of a k-step): 8 exact digits of 16 entries of A / sigma,
+// written as one 16-byte store per slice (the half lands at byte 16 h ^ 16 in rows 4..7 of an atom)
 template <int TR>
 __global__ void ozaki_digits_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int64_t n,
                                     const double* __restrict__ scale, int64_t KS, int8_t* __restrict__ q) {
-  const int64_t total = ceil_div(rows, TR) * TR * KS * OZ_BK;
+  const int64_t total = ceil_div(rows, TR) * TR * KS * 2;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(e % OZ_BK);
-    const int64_t ks = (e / OZ_BK) % KS;
-    const int64_t row = e / (OZ_BK * KS);
-    const int64_t t = row / TR;
-    const int i = (int)(row % TR);
-    const int64_t j = ks * OZ_BK + c;
-    double r = (row < rows && j < n) ? A[row * lda + j] / scale[row] : 0.0;   // exact: power of two
-    const uint32_t o = (uint32_t)(i * OZ_BK + c);
+    // h fastest, then the tile row: a warp writes 512 contiguous bytes of one slice image per store
+    const int h = (int)(e & 1);
+    const int i = (int)((e >> 1) % TR);
+    const int64_t rest = (e >> 1) / TR;
+    const int64_t ks = rest % KS;
+    const int64_t t = rest / KS;
+    const int64_t row = t * TR + i;
+    const int64_t j0 = ks * OZ_BK + 16 * h;
+    const double inv = row < rows ? 1.0 / scale[row] : 0.0;   // a power of two: exact
+    uint32_t w[OZ_S][4];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int64_t j = j0 + k;
+      double r = (row < rows && j < n) ? A[row * lda + j] * inv : 0.0;
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) {
+        const double x = r * 128.0;   // exact
+        const double d = rint(x);     // |d| <= 64 (|r| <= 1/2 throughout)
+        r = x - d;                    // exact
+        const uint32_t b = (uint32_t)(uint8_t)(int8_t)(int)d;
+        if ((k & 3) == 0) w[s][k >> 2] = b;
+        else w[s][k >> 2] |= b << (8 * (k & 3));
+      }
+    }
+    const uint32_t o = (uint32_t)(i * OZ_BK + 16 * h);
     const uint32_t phys = o ^ (((o >> 7) & 1u) << 4);
     int8_t* base = q + (t * KS + ks) * (int64_t)OZ_S * TR * OZ_BK + phys;
 #pragma unroll
-    for (int s = 0; s < OZ_S; ++s) {
-      const double x = r * 128.0;                  // exact
-      const double d = rint(x);                    // |d| <= 64 (|r| <= 1/2 throughout)
-      r = x - d;                                   // exact
-      base[(int64_t)s * TR * OZ_BK] = (int8_t)(int)d;
-    }
+    for (int s = 0; s < OZ_S; ++s)
+      *reinterpret_cast<uint4*>(base + (int64_t)s * TR * OZ_BK) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
   }
 }
 
@@ -304,7 +318,7 @@ void ozaki_slice(const double* A, int64_t lda, int64_t rows, int64_t n, int tile
   ozaki_scale_kernel<<<(unsigned)rows, 256, 0, st>>>(A, lda, n, scale);
   RLD_LAUNCH_CHECK();
   const int64_t KS = ceil_div(n, OZ_BK);
-  const int64_t total = ceil_div(rows, tile_rows) * tile_rows * KS * OZ_BK;
+  const int64_t total = ceil_div(rows, tile_rows) * tile_rows * KS * 2;
   const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)oz_sms() * 16);
   if (tile_rows == OZ_BM)
     ozaki_digits_kernel<OZ_BM><<<blocks, 256, 0, st>>>(A, lda, rows, n, scale, KS, q);
