@@ -34,6 +34,7 @@
 #include <algorithm>
 #include <mutex>
 
+#include "rld_device.cuh"
 #include "rld_internal.cuh"
 #include "tc_ptx.cuh"
 
@@ -138,12 +139,13 @@ __global__ void ozaki_digits_kernel(const double* __restrict__ A, int64_t lda, i
     const int64_t t = rest / KS;
     const int64_t row = t * TR + i;
     const int64_t j0 = ks * OZ_BK + 16 * h;
-    const double inv = row < rows ? 1.0 / scale[row] : 0.0;   // a power of two: exact
+    int ee = 0;
+    if (row < rows) frexp(scale[row], &ee);   // sigma = 2^(ee-1): x = a 2^(1-ee), exact (ldexp: no overflow)
     uint32_t w[OZ_S][4];
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
       const int64_t j = j0 + k;
-      double r = (row < rows && j < n) ? A[row * lda + j] * inv : 0.0;
+      double r = (row < rows && j < n) ? ldexp(A[row * lda + j], 1 - ee) : 0.0;
 #pragma unroll
       for (int s = 0; s < OZ_S; ++s) {
         const double x = r * 128.0;   // exact
@@ -161,6 +163,72 @@ __global__ void ozaki_digits_kernel(const double* __restrict__ A, int64_t lda, i
     for (int s = 0; s < OZ_S; ++s)
       *reinterpret_cast<uint4*>(base + (int64_t)s * TR * OZ_BK) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
   }
+}
+
+// The same sliced image straight from the points (stored float64 path, no float64 K in HBM): the
+// entries are kgen.cu's float64 values (direct differences, kernel_value_f64, exact diagonal) and
+// every row's maximum is the diagonal a^2 + jitter (a stationary kernel: |K_ij| <= a^2), so sigma is
+// known up front.  Bitwise the slices of the stored float64 K.
+__global__ void ozaki_points_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, int64_t row0,
+                                    int64_t rows, int64_t KS, int8_t* __restrict__ q) {
+  constexpr int TR = OZ_BM;
+  const int d = kp.d;
+  int ee = 0;
+  frexp(kp.diag > 0.0 ? kp.diag : 1.0, &ee);   // diag = f 2^ee: sigma = 2^(ee+1), x = v 2^-(ee+1)
+  const int sh = -(ee + 1);
+  const int64_t total = ceil_div(rows, TR) * TR * KS * 2;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int h = (int)(e & 1);
+    const int i = (int)((e >> 1) % TR);
+    const int64_t rest = (e >> 1) / TR;
+    const int64_t ks = rest % KS;
+    const int64_t t = rest / KS;
+    const int64_t row = t * TR + i;
+    const int64_t gi = row0 + row;
+    const int64_t j0 = ks * OZ_BK + 16 * h;
+    double xi[RLD_MAX_DIM];
+#pragma unroll 4
+    for (int k = 0; k < d; ++k) xi[k] = row < rows ? X[gi * d + k] : 0.0;
+    uint32_t w[OZ_S][4];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int64_t j = j0 + k;
+      double v = 0.0;
+      if (row < rows && j < n) {
+        if (j == gi) {
+          v = kp.diag;
+        } else {
+          double r2 = 0.0;
+          for (int c = 0; c < d; ++c) {
+            const double df = xi[c] - X[j * d + c];
+            r2 = fma(df, df, r2);
+          }
+          v = kernel_value_f64(kp, r2);
+        }
+      }
+      double r = ldexp(v, sh);
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) {
+        const double x = r * 128.0;
+        const double dg = rint(x);
+        r = x - dg;
+        const uint32_t b = (uint32_t)(uint8_t)(int8_t)(int)dg;
+        if ((k & 3) == 0) w[s][k >> 2] = b;
+        else w[s][k >> 2] |= b << (8 * (k & 3));
+      }
+    }
+    const uint32_t o = (uint32_t)(i * OZ_BK + 16 * h);
+    const uint32_t phys = o ^ (((o >> 7) & 1u) << 4);
+    int8_t* base = q + (t * KS + ks) * (int64_t)OZ_S * TR * OZ_BK + phys;
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s)
+      *reinterpret_cast<uint4*>(base + (int64_t)s * TR * OZ_BK) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+  }
+}
+
+__global__ void oz_fill_kernel(int64_t rows, double v, double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < rows) out[i] = v;
 }
 
 __global__ void oz_split_reduce_kernel(const double* __restrict__ part, int splits, int64_t stride, int64_t m,
@@ -326,6 +394,21 @@ void ozaki_slice(const double* A, int64_t lda, int64_t rows, int64_t n, int tile
     ozaki_digits_kernel<OZ_BN><<<blocks, 256, 0, st>>>(A, lda, rows, n, scale, KS, q);
   else
     fail(RLD_ERR_INVALID_ARGUMENT, "ozaki_slice: tile rows must be 128 (K) or 64 (V)");
+  RLD_LAUNCH_CHECK();
+}
+
+void ozaki_slice_points(const double* X, int64_t n, const KernelParams& kp, int64_t row0, int64_t rows, int8_t* q,
+                        double* scale, cudaStream_t st) {
+  if (rows <= 0) return;
+  if (kp.d > RLD_MAX_DIM) fail(RLD_ERR_NOT_SUPPORTED, "ozaki_slice_points: d > 32");
+  int ee = 0;
+  frexp(kp.diag > 0.0 ? kp.diag : 1.0, &ee);
+  oz_fill_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, st>>>(rows, ldexp(1.0, ee + 1), scale);
+  RLD_LAUNCH_CHECK();
+  const int64_t KS = ceil_div(n, OZ_BK);
+  const int64_t total = ceil_div(rows, OZ_BM) * OZ_BM * KS * 2;
+  const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)oz_sms() * 16);
+  ozaki_points_kernel<<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q);
   RLD_LAUNCH_CHECK();
 }
 

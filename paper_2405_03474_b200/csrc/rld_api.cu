@@ -220,6 +220,7 @@ void prepare(rld_handle* h, const rld_problem* p) {
   Resident& r = h->res;
   r.ready = false;
   r.tiled = false;
+  r.kq_ready = false;
   h->precond_k = -1;
   r.source = p->source;
   r.dtype = p->dtype;
@@ -261,7 +262,19 @@ void prepare(rld_handle* h, const rld_problem* p) {
       pad_points(r.X.as<double>(), p->n, p->d, scale, r.pts4.as<float>(), st);
     }
     if (r.path == RLD_PATH_STORED) {
-      if (p->dtype == RLD_FP64) {
+      if (p->dtype == RLD_FP64 && fp64_product_ozaki()) {
+        // float64 products on exact int8 slices generated straight from the points (kv_ozaki.cu):
+        // no float64 K in HBM (column reads and rebuilds go back to the points)
+        r.K = nullptr;
+        r.ldk = 0;
+        if (r.rows > 0) {
+          r.Kq.reserve((size_t)ozaki_bytes(r.rows, p->n, 128));
+          r.ksigma.reserve(sizeof(double) * r.rows);
+          ozaki_slice_points(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.Kq.as<int8_t>(), r.ksigma.as<double>(),
+                             st);
+        }
+        r.kq_ready = r.rows > 0;
+      } else if (p->dtype == RLD_FP64) {
         r.ldk = ceil_div(p->n, 4) * 4;
         r.Kbuf.reserve(sizeof(double) * r.rows * r.ldk);
         r.K = r.Kbuf.ptr;
@@ -345,8 +358,7 @@ void prepare(rld_handle* h, const rld_problem* p) {
   } else {
     fail(RLD_ERR_INVALID_ARGUMENT, "unknown source");
   }
-  r.kq_ready = false;
-  if (r.path == RLD_PATH_STORED && r.dtype == RLD_FP64 && fp64_product_ozaki() && r.rows > 0) {
+  if (!r.kq_ready && r.K && r.path == RLD_PATH_STORED && r.dtype == RLD_FP64 && fp64_product_ozaki() && r.rows > 0) {
     // exact int8 slices of the stored float64 rows for the INT8 tensor-core product (kv_ozaki.cu)
     r.Kq.reserve((size_t)ozaki_bytes(r.rows, r.n, 128));
     r.ksigma.reserve(sizeof(double) * r.rows);
@@ -797,7 +809,7 @@ int lowrank_truncsvd(rld_handle* h, const rld_config* c) {
   DevBuf L, W;
   L.reserve(sizeof(double) * n * n);
   W.reserve(sizeof(double) * n);
-  if (r.path == RLD_PATH_ON_THE_FLY)
+  if (r.path == RLD_PATH_ON_THE_FLY || !r.K)
     build_kernel_rows<double>(r.X.as<double>(), n, r.kp, 0, n, L.as<double>(), n, st);
   else if (r.tiled)
     untile_to_f64(static_cast<const float*>(r.K), n, n, L.as<double>(), n, st);
@@ -1539,7 +1551,7 @@ int rld_exact_logdet(rld_handle* h, double* value) {
     const int64_t n = r.n;
     DevBuf L;
     L.reserve(sizeof(double) * n * n);
-    if (r.path == RLD_PATH_ON_THE_FLY) {
+    if (r.path == RLD_PATH_ON_THE_FLY || !r.K) {
       build_kernel_rows<double>(r.X.as<double>(), n, r.kp, 0, n, L.as<double>(), n, h->st);
     } else {
       if (r.tiled)

@@ -143,6 +143,9 @@ void gemm_expand_f64(const double* S, int64_t lds, int64_t p, int64_t q, const d
 int64_t ozaki_bytes(int64_t rows, int64_t n, int tile_rows);   // size of a sliced image (tiles of 128 / 64 rows)
 void ozaki_slice(const double* A, int64_t lda, int64_t rows, int64_t n, int tile_rows, int8_t* q, double* scale,
                  cudaStream_t st);
+// the same image straight from the points (no float64 K): stationary kernel, row max = diagonal
+void ozaki_slice_points(const double* X, int64_t n, const KernelParams& kp, int64_t row0, int64_t rows, int8_t* q,
+                        double* scale, cudaStream_t st);
 void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int64_t n, const double* V, int64_t ldv,
                       int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st);
 // Which float64 stored-K product a prepare sets up: the int8 slices (default) or, with

@@ -156,3 +156,18 @@ def test_fp64_product_under_concurrency(rld, fp64_product):
     for t in ths:
         t.join()
     assert not bad, bad[:5]
+
+
+def test_int8_slices_from_points_equal_slices_from_K(rld, monkeypatch):
+    """Stored float64 from the points slices K straight from the points (no float64 K in HBM); from
+    a dense device K built by build_covariance it slices the stored rows: same entries, same row
+    scales (the diagonal), so the two estimates are bit-identical."""
+    from paper_2405_03474_b200.workloads import baseline
+
+    monkeypatch.setenv("RLD_FP64_PRODUCT", "ozaki")
+    for idx in (1, 2):
+        wl = baseline(idx, n=3000, rank=64, num_probes=8, dtype="fp64")
+        a = rld.rstar_logdet(rld.KernelMatrix(wl.spec, wl.points), replace(wl.config, path="stored"))
+        K = rld.build_covariance(wl.spec, wl.points, dtype="fp64")
+        b = rld.rstar_logdet(K, wl.config)
+        assert a.value == b.value, (idx, a.value, b.value)
