@@ -103,8 +103,8 @@ class Session:
             raise ValueError(f"unknown path {path!r}")
         n = M.n
         rows = -(-n // self.world_size)
-        # fp64 stores K and (default product) its 8 int8 slices: 16 bytes per entry
-        es = (8 if os.environ.get("RLD_FP64_PRODUCT") == "dmma" else 16) if dtype == "fp64" else 4
+        # fp64 from points: the float64 K or (default product) its 8 int8 slices, 8 bytes per entry
+        es = 8 if dtype == "fp64" else 4
         return "stored" if rows * n * es <= 0.5 * hbm_bytes(self.device) else "on_the_fly"
 
     def problem_for(self, M, dtype: str, path: str = "auto"):
