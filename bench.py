@@ -485,6 +485,8 @@ def roofline_for(wl, cfg, rows, n, s, kv_ms, world):
                 "kernel": f"kv_product (tcgen05 kind::i8 on exact int8 slices of float64 K, m=s={s}, {rows} rows)",
                 "kernel_ms": kv_ms, "alg_bytes": alg_bytes, "equiv_fp64_tflops": 2.0 * rows * n * s / (kv_ms * 1e-3) / 1e12,
                 "int8_ops": 36 * 2.0 * rows * n * (-(-s // 64) * 64),
+                "int8_tensor_frac": 36 * 2.0 * rows * n * (-(-s // 64) * 64) / (kv_ms * 1e-3) / 1e12
+                / pipe.get("i8_ss_n128", {}).get("tops", 4555.6),
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}
     if wl.path == "stored" and cfg.dtype == "fp32":
         alg_bytes = es * rows * n + 4 * n * s + 8 * rows * s

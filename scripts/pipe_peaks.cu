@@ -158,6 +158,51 @@ __global__ void __launch_bounds__(128) mma_kernel(int iters, long long* out) {
   if (threadIdx.x < 32) ptx::tmem_dealloc(tmem, 512);
 }
 
+// tcgen05 kind::i8 (s8 x s8 -> s32), M = 128, K = 32, A and B from shared memory (32-byte swizzle
+// descriptors as kv_ozaki.cu), N = 64 / 128 / 256
+__device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(256 >> 4) << 32) | ((uint64_t)1 << 46) |
+         ((uint64_t)6 << 61);
+}
+
+template <int N>
+__global__ void __launch_bounds__(128) mma_i8_kernel(int iters, long long* out) {
+  __shared__ __align__(1024) uint8_t sm[128 * 32 + 256 * 32];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t holder;
+  for (int i = threadIdx.x; i < (int)sizeof(sm) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u;
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_mbarrier_init();
+  }
+  if (threadIdx.x < 32) ptx::tmem_alloc(&holder, 512);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = holder;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint64_t ad = desc_sw32(ptx::smem_u32(sm)), bd = desc_sw32(ptx::smem_u32(sm + 128 * 32));
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (uint32_t)(k & 1) * 256u),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(1u)
+            : "memory");
+    }
+    ptx::tc_commit(&bar);
+    ptx::mbar_wait(&bar, 0);
+    if (blockIdx.x == 0) out[0] = clock64() - t0;
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) ptx::tmem_dealloc(tmem, 512);
+}
+
 template <typename F>
 float best_ms(F launch) {
   cudaEvent_t e0, e1;
@@ -234,7 +279,18 @@ int main() {
   mma(mma_kernel<256, false>, 256, "tf32_ss_n256", false);
   mma(mma_kernel<64, true>, 64, "tf32_ts_n64", false);
   mma(mma_kernel<128, true>, 128, "tf32_ts_n128", false);
-  mma(mma_kernel<256, true>, 256, "tf32_ts_n256", true);
+  mma(mma_kernel<256, true>, 256, "tf32_ts_n256", false);
+  auto mma8 = [&](auto kern, int N, const char* name, bool last) {
+    float ms = best_ms([&] { kern<<<sms, 128>>>(mi, lo); });
+    long long cyc = 0;
+    cudaMemcpy(&cyc, lo, 8, cudaMemcpyDeviceToHost);
+    const double ops = (double)sms * mi * 4 * 2.0 * 128 * N * 32;
+    printf(" \"%s\": {\"tops\": %.1f, \"cycles_per_mma\": %.1f}%s\n", name, ops / (ms * 1e-3) / 1e12,
+           (double)cyc / (mi * 4.0), last ? "" : ",");
+  };
+  mma8(mma_i8_kernel<64>, 64, "i8_ss_n64", false);
+  mma8(mma_i8_kernel<128>, 128, "i8_ss_n128", false);
+  mma8(mma_i8_kernel<256>, 256, "i8_ss_n256", true);
   printf("}\n");
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
