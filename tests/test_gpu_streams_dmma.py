@@ -171,3 +171,32 @@ def test_int8_slices_from_points_equal_slices_from_K(rld, monkeypatch):
         K = rld.build_covariance(wl.spec, wl.points, dtype="fp64")
         b = rld.rstar_logdet(K, wl.config)
         assert a.value == b.value, (idx, a.value, b.value)
+
+
+@pytest.mark.parametrize("n,m", [(1, 1), (5, 2), (31, 3), (33, 1), (130, 70), (257, 129)])
+def test_int8_slices_edge_cases(rld, monkeypatch, n, m):
+    """The INT8-slice product on an arbitrary dense float64 matrix (signed entries, an all-zero row,
+    rows scaled by 1e120 and 1e-150) and vectors including an all-zero one and huge / tiny
+    ones: the slice error bound |err_ic| <= 2^-50 n max_j |A_ij| max_j |V_cj| holds entrywise, the
+    zero row / vector give exact zeros, nothing overflows."""
+    import torch
+
+    monkeypatch.setenv("RLD_FP64_PRODUCT", "ozaki")
+    g = np.random.default_rng(n * 1000 + m)
+    A = g.standard_normal((n, n)) * np.exp(g.uniform(-5, 5, (n, n)))
+    A[n // 2] = 0.0
+    if n > 3:
+        A[1] *= 1e120
+        A[2] *= 1e-150
+    R = rld.ResidentMatrix(A, dtype="fp64")
+    V = g.standard_normal((m, n))
+    V[0] = 0.0
+    if m > 2:
+        V[1] *= 1e120
+        V[2] *= 1e-150
+    Y = R.kv_apply(torch.from_numpy(V).cuda()).cpu().numpy()
+    ref = V @ A.T
+    assert np.all(np.isfinite(Y))
+    assert np.all(Y[0] == 0.0) and np.all(Y[:, n // 2] == 0.0)
+    bound = 2.0 ** -50 * n * np.outer(np.abs(V).max(axis=1), np.abs(A).max(axis=1))
+    assert np.all(np.abs(Y - ref) <= bound + 1e-300)
