@@ -367,11 +367,10 @@ template <int BM, int BN>
 void launch_nt(const double* A, int64_t lda, int64_t p, const double* B, int64_t ldb, int64_t q, int64_t n,
                double* C, int64_t ldc, double beta, DevBuf& partial, cudaStream_t st) {
   using S = DmmaShape<BM, BN>;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [&] {
     RLD_CUDA(cudaFuncSetAttribute(gemm_nt_dmma_kernel<BM, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM));
-    attr = true;
-  }
+  });
   const CUtensorMap ma = map_f64(A, n, p, lda, BM);
   const CUtensorMap mb = map_f64(B, n, q, ldb, BN);
   const int64_t tiles = ceil_div(p, BM) * ceil_div(q, BN);
@@ -419,11 +418,10 @@ template <int BQ>
 void launch_expand(const double* Sm, int64_t lds, int64_t p, int64_t q, const double* X, int64_t ldx, int64_t N,
                    double* C, int64_t ldc, double alpha, double beta, cudaStream_t st) {
   using S = ExShape<BQ>;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [&] {
     RLD_CUDA(cudaFuncSetAttribute(gemm_expand_dmma_kernel<BQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM));
-    attr = true;
-  }
+  });
   const CUtensorMap ms = map_f64(Sm, p, q, lds, BQ);       // S^T as q rows of p
   const CUtensorMap mx = map_f64_b8(X, N, p, ldx, DM_BK);   // X: p rows of N
   dim3 grid((unsigned)ceil_div(N, EX_BN), (unsigned)ceil_div(q, BQ), 1);

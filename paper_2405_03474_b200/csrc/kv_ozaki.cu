@@ -420,11 +420,10 @@ void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int6
   ws.oz_vq.reserve((size_t)ozaki_bytes(m, n, OZ_BN));
   ws.oz_tau.reserve(sizeof(double) * m);
   ozaki_slice(V, ldv, m, n, OZ_BN, ws.oz_vq.as<int8_t>(), ws.oz_tau.as<double>(), st);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [&] {
     RLD_CUDA(cudaFuncSetAttribute(ozaki_kv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM));
-    attr = true;
-  }
+  });
   const int64_t KS = ceil_div(n, OZ_BK);
   const int64_t passes = ceil_div(m, OZ_BN), tiles = ceil_div(rows, OZ_BM);
   const int64_t units0 = passes * tiles;

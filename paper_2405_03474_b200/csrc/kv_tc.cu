@@ -892,7 +892,16 @@ void launch_tc(const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap&
   p.tmem_cols = Sh::TMEM_COLS;
   const size_t smem = (size_t)p.sa * Sh::A_REGION + (size_t)p.sb * BST + extra;
   auto kern = kv_tc_kernel<MODE, NT, OTF, DIM, FAM, CG2>;
-  RLD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // the opt-in maximum once per device (not the launch's own size: another host thread could lower
+  // the attribute between this thread's set and launch)
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [&] {
+    int dev = 0, optin = 0;
+    RLD_CUDA(cudaGetDevice(&dev));
+    RLD_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    RLD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  });
+  if (smem > 232448) fail(RLD_ERR_NOT_SUPPORTED, "kv_tc: shared memory request above the sm_100 limit");
   if constexpr (CG2) {   // CTA pairs: clusters of two on one TPC
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)grid);

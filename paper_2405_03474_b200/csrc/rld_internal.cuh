@@ -39,6 +39,18 @@ extern thread_local int g_launches;
 // barrier (a spin on CTAs that another kernel's blocks could keep off the SMs).
 extern std::atomic<int> g_live_handles;
 
+// Run `f` once per CUDA device (kernel attributes such as the dynamic shared-memory limit are per
+// device); safe from several host threads (f is idempotent, so a concurrent double call is harmless).
+template <typename F>
+void once_per_device(std::atomic<uint64_t>& done, F&& f) {
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice", __FILE__, __LINE__);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  f();
+  done.fetch_or(bit, std::memory_order_acq_rel);
+}
+
 // Grow-only device buffer.
 struct DevBuf {
   void* ptr = nullptr;

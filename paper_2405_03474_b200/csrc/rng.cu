@@ -361,12 +361,11 @@ void normal_rows(const uint64_t key[2], int64_t rows, int64_t n, int64_t col0, i
   int* entry = naccs + nchunks * EMAX;
   int64_t* base = reinterpret_cast<int64_t*>(entry + nchunks + (nchunks & 1));
   const size_t smem = sizeof(ChunkSmem);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [&] {
     RLD_CUDA(cudaFuncSetAttribute(zig_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     RLD_CUDA(cudaFuncSetAttribute(zig_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  });
   zig_chunk_kernel<<<(unsigned)nchunks, ZT, smem, st>>>(key[0], key[1], exits, naccs, dflags);
   RLD_LAUNCH_CHECK();
   zig_link_kernel<<<1, ZL, 0, st>>>(nchunks, count, exits, naccs, entry, base, dflags);

@@ -329,12 +329,11 @@ bool small_potrf_upper(int n, double* G, int ld, int* info, cudaStream_t st, dou
     const size_t tail = std::max((size_t)nn * (NB + 1), (size_t)NB * NB * ((nn + NB - 1) / NB));
     return sizeof(double) * ((size_t)3 * NB * (NB + 1) + 3 * NB + (size_t)CMAX * (NB + 1)) + sizeof(double) * tail;
   };
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_set{0};
+  once_per_device(attr_set, [&] {
     RLD_CUDA(cudaFuncSetAttribute(chol_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem_for(SMALL_CHOL_MAX)));
-    attr_set = true;
-  }
+  });
   const size_t smem = smem_for(n);
   static const bool profile = getenv("RLD_CHOL_PROFILE") != nullptr;
   long long* prof = nullptr;

@@ -621,14 +621,13 @@ bool tri_eigh(int n, const double* A, double* w, DevBuf& scratch, double** Zout,
   double* Z = V + nn;
   double* Q = Z + nn;
   double* work = Q + nn;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [&] {
     RLD_CUDA(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     RLD_CUDA(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)tridiag_smem()));
     RLD_CUDA(cudaFuncSetAttribute(inviter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)inviter_smem(TNMAX)));
-    attr = true;
-  }
+  });
   {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(TCL);
