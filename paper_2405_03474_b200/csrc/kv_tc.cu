@@ -49,6 +49,7 @@
 #include "rld_device.cuh"
 #include "rld_internal.cuh"
 #include "tc_ptx.cuh"
+#include "kv_sched.cuh"
 
 namespace rld {
 
@@ -57,23 +58,8 @@ namespace {
 constexpr int TC_BM = 128;          // K rows per tile (UMMA M)
 constexpr int TC_BK = 32;           // fp32 k-elements per step (one 128-byte swizzle row)
 constexpr int TC_THREADS = 640;   // 20 warps: TMA, 2 MMA, TMEM owner, 4 CP converters, 4 DP drains (CP + DP = 4)
-constexpr int GROUP = 4;            // k-steps accumulated in TMEM before the register flush
 constexpr int NABUF_MAX = 8;        // pipeline stages = TMEM A-operand buffers: as many as the 512 columns leave (<= 8)
 constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4;  // 16 KB
-
-// Work schedule of one CTA (G CTAs per column pass).  Phase 1: R = tiles / G full
-// rounds -- CTA c takes tile c + r G over all k-steps, so every CTA sweeps the B
-// operand (V) in the same k order at about the same time and L2 serves the reuse
-// (with per-CTA stream-K ranges the CTAs sat at unrelated k offsets and re-read B
-// from HBM once per tile: ~8.8 TB per config-5 product).  Phase 2: the remaining
-// tiles' (tile, k-step) space is cut into G equal contiguous ranges ("stream-K"),
-// whose per-CTA partial tiles kv_tc_reduce adds in fixed order.
-struct Sched {
-  int ks, G, R;          // k-steps per tile, CTAs per pass, full rounds
-  int64_t tail_total;    // (tiles - R G) * ks
-  __host__ __device__ int64_t tail_beg(int64_t c) const { return c * tail_total / G; }
-  __host__ __device__ int64_t tail_end(int64_t c) const { return (c + 1) * tail_total / G; }
-};
 
 // CTA b works on column pass b % npass over stream-K range b / npass.
 struct TcParams {
@@ -105,40 +91,6 @@ struct TcParams {
   float la2;                   // log2(amplitude^2), folded into the exponent
 };
 
-__device__ __forceinline__ float fast_exp2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-__device__ __forceinline__ float fast_sqrt(float x) {   // MUFU; sqrt(0) = 0
-  float y;
-  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-// packed FP32x2 helpers (sm_100 FADD2 / FMUL2 / FFMA2), lanes = (lo 32 bits, hi 32 bits)
-__device__ __forceinline__ uint64_t pk(float a, float b) {
-  return (uint64_t)__float_as_uint(a) | ((uint64_t)__float_as_uint(b) << 32);
-}
-__device__ __forceinline__ float pk_lo(uint64_t v) { return __uint_as_float((uint32_t)v); }
-__device__ __forceinline__ float pk_hi(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
-__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
-  uint64_t d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
-  uint64_t d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-
 // Two K entries from packed scaled squared distances (src/kernels.py:40-46), float32:
 // RBF a^2 2^(-r2') with r2' = r^2 log2(e) / (2 l^2); Matern-5/2 a^2 (1 + u + u^2/3) e^-u
 // with u = sqrt(r2') = sqrt(5) r / l.  a^2 is folded into the exponent (la2 = log2 a^2).
@@ -153,101 +105,6 @@ __device__ __forceinline__ uint64_t kernel_pair(const TcParams& p, uint64_t r2) 
   const uint64_t t = fma2(u, pk(-1.4426950408889634f, -1.4426950408889634f), pk(p.la2, p.la2));
   return mul2(poly, pk(fast_exp2(pk_lo(t)), fast_exp2(pk_hi(t))));
 }
-
-__host__ __device__ __forceinline__ int64_t cta_of_step(int64_t x, int64_t total, int64_t G) {
-  // the CTA whose range [c*total/G, (c+1)*total/G) contains step x
-  return ((x + 1) * G - 1) / total;
-}
-
-// Walks a CTA's steps with running 32-bit counters (no divisions in the loops:
-// the pipeline warps run this once per k-step, inside their critical loops, and
-// each role pays only for the counters it uses: GRP = group boundaries (MMA),
-// BR = a second ring (the converters walk the A-source ring in (s, ph) and the
-// B / TMEM-buffer ring in (sb, phb))).
-template <bool GRP, bool BR>
-struct StepIter {
-  int v, vend;           // step index (== pipeline slot j) and end: [0, R ks) phase 1, then the tail range
-  int ks, kstep, tile, s, S, G, R, round;
-  int tail_next, tail_k0;   // where the tail range starts (tile, k-step)
-  uint32_t ph;
-  int gpos = 0;          // GRP: position in the accumulation group
-  int sb = 0, SB = 1;    // BR: second ring
-  uint32_t phb = 0;
-  __device__ __forceinline__ StepIter(const Sched& sc, int64_t cta, int S_, int SB_ = 1)
-      : v(0), ks(sc.ks), kstep(0), s(0), S(S_), G(sc.G), R(sc.R), round(0), ph(0), SB(SB_) {
-    const int64_t tb = sc.tail_beg(cta), te = sc.tail_end(cta);
-    vend = R * ks + (int)(te - tb);
-    tail_next = R * G + (int)(tb / ks);
-    tail_k0 = (int)(tb - (int64_t)(tb / ks) * ks);
-    if (R > 0) {
-      tile = (int)cta;
-    } else {
-      tile = tail_next;
-      kstep = tail_k0;
-    }
-  }
-  __device__ __forceinline__ bool valid() const { return v < vend; }
-  __device__ __forceinline__ bool in_tail() const { return round >= R; }
-  __device__ __forceinline__ bool group_start() const { return gpos == 0; }
-  __device__ __forceinline__ bool seg_end() const { return v + 1 == vend || kstep + 1 == ks; }
-  __device__ __forceinline__ bool group_end() const { return seg_end() || gpos + 1 == GROUP; }
-  __device__ __forceinline__ void next() {
-    if (GRP) gpos = group_end() ? 0 : gpos + 1;
-    ++v;
-    if (++kstep == ks) {
-      kstep = 0;
-      if (round < R) {
-        if (++round < R) {
-          tile += G;
-        } else {   // phase 1 done: continue in the tail range
-          tile = tail_next;
-          kstep = tail_k0;
-        }
-      } else {
-        ++tile;
-      }
-    }
-    if (++s == S) {
-      s = 0;
-      ph ^= 1;
-    }
-    if (BR && ++sb == SB) {
-      sb = 0;
-      phb ^= 1;
-    }
-  }
-};
-
-// Segment (tile, first step, steps) iteration for the drain warps: one call per
-// segment instead of one StepIter advance per k-step.
-struct SegIter {
-  int64_t cta;
-  const Sched* sc;
-  int r;                 // phase-1 round, then R for the tail
-  int64_t x, xe;         // tail-space position and end
-  __device__ __forceinline__ SegIter(const Sched& s, int64_t c) : cta(c), sc(&s), r(0) {
-    x = s.tail_beg(c);
-    xe = s.tail_end(c);
-  }
-  // next segment: tile, its length in k-steps and its partial-sum slot; false when done
-  __device__ __forceinline__ bool next(int& tile, int& len, int& seg) {
-    if (r < sc->R) {
-      tile = (int)cta + r * sc->G;
-      len = sc->ks;
-      seg = 0;
-      ++r;
-      return true;
-    }
-    if (x >= xe) return false;
-    const int64_t u = x / sc->ks;
-    const int64_t x0 = u * sc->ks;
-    tile = sc->R * sc->G + (int)u;
-    len = (int)(std::min<int64_t>(xe, x0 + sc->ks) - x);
-    seg = (int)(cta - cta_of_step(x0, sc->tail_total, sc->G));
-    x += len;
-    return true;
-  }
-};
 
 // 16 on-the-fly K entries of one converter thread: its row x 16 column points of
 // the stage (columns [e0, e0 + 16) of the k-step), split into tf32 hi + lo.
@@ -829,9 +686,7 @@ __global__ void kv_tc_split(const double* __restrict__ V, int64_t ldv, int64_t m
 
 // ---------------------------------------------------------------- host side
 
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+}  // namespace
 
 EncodeTiledFn encode_fn() {
   static EncodeTiledFn fn = nullptr;
@@ -874,6 +729,8 @@ int max_smem_optin() {
   RLD_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   return v;
 }
+
+namespace {
 
 template <int MODE, int NT, bool OTF, int DIM, int FAM, bool CG2 = false>
 void launch_tc(const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl, TcParams p, int64_t grid,
@@ -1049,6 +906,10 @@ bool kv_tc_b_layout(const KvOperand& op, int64_t m, KvWorkspace& ws, TcBLayout& 
 
 void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, int64_t ldv, double* Y, int64_t ldy,
                    KvWorkspace& ws, cudaStream_t st, bool presplit) {
+  if (op.K == nullptr && !presplit && kv_otf_f16_enabled()) {
+    kv_product_otf16(op, m, V, ldv, Y, ldy, ws, st);
+    return;
+  }
   const int64_t n = op.n, rows = op.rows;
   const int ks = (int)ceil_div(n, TC_BK);
   int npass = 0, width = 0;

@@ -256,7 +256,7 @@ void prepare(rld_handle* h, const rld_problem* p) {
     r.diag.reserve(sizeof(double) * std::max<int64_t>(1, r.rows));
     fill_doubles(r.rows, r.kp.diag, r.diag.as<double>(), st);
     if (p->d <= 4) {
-      r.pts4.reserve(sizeof(float) * 8 * ceil_div(p->n, 32) * 32);
+      r.pts4.reserve(sizeof(float) * otf_points_floats(p->n));
       // coordinates pre-scaled so the tile generator's r^2 is the kernel argument
       const double scale = p->family == RLD_MATERN52 ? r.kp.s5_over_l : std::sqrt(r.kp.inv_2l2 * 1.4426950408889634);
       pad_points(r.X.as<double>(), p->n, p->d, scale, r.pts4.as<float>(), st);

@@ -116,9 +116,16 @@ struct KvWorkspace {
   DevBuf tc_sync;     // epoch-barrier counters of the tensor-core kernel
   cublasHandle_t blas = nullptr;   // the handle's cuBLAS (bound to the same stream): fp64 stored K
   DevBuf oz_vq, oz_tau;            // int8 slices of V and their column scales (kv_ozaki.cu)
+  DevBuf otf_vmax;                 // per-vector max |V| of the fp16 on-the-fly product (kv_otf.cu)
 };
 
 bool kv_tc_supported(const KvOperand& op);
+// On-the-fly float32 product on the kind::f16 tensor cores (kv_otf.cu; default, RLD_OTF_KIND=tf32
+// selects the 3xTF32 kernel).  Points in op.pts4 padded to otf_points_floats(n) floats.
+bool kv_otf_f16_enabled();
+int64_t otf_points_floats(int64_t n);
+void kv_product_otf16(const KvOperand& op, int64_t m, const double* V, int64_t ldv, double* Y, int64_t ldy,
+                      KvWorkspace& ws, cudaStream_t st);
 // presplit: the B operand (tf32 hi / lo of V in the k-step blocked layout) was already written
 // into ws.bhi / ws.blo by the caller (see kv_tc_b_layout); V is then unused.
 void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, int64_t ldv, double* Y, int64_t ldy,

@@ -962,7 +962,7 @@ void sum_blocks(int64_t nb, int64_t count, const double* in, double* out, cudaSt
 }
 
 void pad_points(const double* X, int64_t n, int d, double scale, float* pts8, cudaStream_t st) {
-  RLD_CUDA(cudaMemsetAsync(pts8, 0, sizeof(float) * 8 * ceil_div(n, 32) * 32, st));
+  RLD_CUDA(cudaMemsetAsync(pts8, 0, sizeof(float) * otf_points_floats(n), st));
   pad_points_kernel<<<(unsigned)ceil_div(4 * n, 256), 256, 0, st>>>(X, n, d, scale, pts8);
   RLD_LAUNCH_CHECK();
 }
