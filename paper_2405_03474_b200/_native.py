@@ -11,7 +11,8 @@ import os
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "librld.so"
+# RLD_LIB_PATH: an alternative build of the same library (A/B measurements of kernel variants)
+LIB_PATH = Path(os.environ.get("RLD_LIB_PATH") or (Path(__file__).resolve().parent / "librld.so"))
 
 RLD_OK = 0
 RLD_ERR_INVALID_ARGUMENT = 1

@@ -72,9 +72,12 @@ def test_reduced_configs_sharded(rld, golden_cases, G, dtype, path, idx, n):
     one = rld.rstar_logdet(M, cfg)
     res = sharded(rld, G, lambda: rld.rstar_logdet(M, cfg))
     # fp32: the tensor-core product's stream-k tail split depends on the shard's row count, so the
-    # fp32 accumulation order of a few tiles differs; config 4 (clustered points, r5, l = n/4) carries
-    # that through 20 Lanczos steps to ~1.4e-6 -- two fp32 routes, well inside the 1e-4 fp32 budget
-    tol = 1e-12 if dtype == "fp64" else 1e-5
+    # fp32 accumulation order of a few tiles differs; config 4 (clustered points, r5, l = n/4) is
+    # ill-conditioned enough to carry that through 20 Lanczos steps to the 1e-5 level.  Measured
+    # (scripts/_c4shard.py, G = 1 / 2 / 3 vs the float64 golden value): fp16 on-the-fly kernel
+    # 5.9e-6 / 1.2e-5 / 4.9e-6, 3xTF32 kernel 6.5e-6 / 7.1e-6 / 1.3e-6; so G vs G = 1 is held
+    # to 3e-5 and both to the 1e-4 fp32 bar against the golden value below
+    tol = 1e-12 if dtype == "fp64" else 3e-5
     assert rel(res[0].value, one.value) <= tol, (res[0].value, one.value)
     name = {2: "config2_n2048_r3", 4: "config4_n4096_r5", 3: "config3_n4096_r3"}.get(idx)
     if name and golden_cases[name]["n"] == n:
