@@ -92,8 +92,11 @@ def load_peaks():
 
 def load_pipe_peaks():
     """Measured compute-pipe peaks of this pool's B200 (scripts/pipe_peaks.cu, committed)."""
-    p = ROOT / "profiles" / "r02_pipe_peaks.json"
-    return json.loads(p.read_text()) if p.exists() else {}
+    for name in ("r02c_pipe_peaks.json", "r02_pipe_peaks.json"):
+        p = ROOT / "profiles" / name
+        if p.exists():
+            return json.loads(p.read_text())
+    return {}
 
 
 class ClockSampler:
@@ -258,9 +261,11 @@ def workload_config(wl, world=1, sharded=False):
     es = 4 if cfg.dtype == "fp32" else 8
     return {"workload": f"{wl.name}: n={n} {wl.spec.family} d={wl.points.shape[1]} ell={wl.spec.length_scale} "
                         f"noise={wl.spec.jitter} {cfg.algorithm} l={cfg.precond.rank} s={s} "
-                        f"{cfg.probe_kind} t={cfg.lanczos_iters} q={cfg.precond.num_iters} stored K "
-                        f"({cfg.dtype})",
-            "l2": "inputs larger than L2 (K = %.2f GB)" % (es * n * n / 1e9),
+                        f"{cfg.probe_kind} t={cfg.lanczos_iters} q={cfg.precond.num_iters} "
+                        f"{'on-the-fly' if wl.path == 'on_the_fly' else 'stored'} K ({cfg.dtype})",
+            "l2": ("inputs larger than L2 (K = %.2f GB)" % (es * n * n / 1e9)) if wl.path != "on_the_fly" else
+                  ("K never stored; the float64 probe / sketch blocks (%.0f MB .. %.0f MB) exceed L2"
+                   % (8 * n * s / 1e6, 8 * n * min(cfg.precond.rank + 10, n) / 1e6)),
             "parallelism": (f"rows{world}" if sharded else f"replicas{world}") if world > 1 else "single"}
 
 
@@ -450,6 +455,10 @@ def run_ours(args):
     if args.config == 3 and cfg.dtype == "fp64" and not args.no_extra:
         line["extra_fp32"] = extra_fp32(args, rld, world, sharded, per_step)
 
+    # ---- extra: config 4 at full n on the fly (fp32, fp16 3-term tensor-core products)
+    if args.config == 3 and cfg.dtype == "fp64" and not args.no_extra and world == 1:
+        line["extra_otf"] = extra_otf(rld)
+
     # ---- CPU baseline (rank 0, N = 1 only)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -580,6 +589,78 @@ def extra_fp32(args, rld, world, sharded, per_step):
     out = {"value": per_step * K / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms / K, "dtype": "f32",
            "config": workload_config(wl, world, sharded),
            "roofline": roofline_for(wl, cfg, r1 - r0, wl.n, cfg.num_probes, k0.elapsed_time(k1) / 10, world),
+           "parity": parity_vs_golden(wl, est.value)}
+    del R
+    torch.cuda.empty_cache()
+    return out
+
+
+def roofline_otf(wl, n, m, kv_ms, nt):
+    """On-the-fly product (csrc/kv_otf.cu): per K entry 3 fp16 tensor products of width NT (the
+    padded pass width), 1 (RBF) or 2 (Matern: sqrt + ex2) MUFU ops, and the FP32-pipe generation
+    work; each pipe's minimum time at its measured peak, the largest is the bound."""
+    pipe = load_pipe_peaks()
+    entries = float(n) * n
+    passes = -(-m // nt)
+    # the tensor ceiling at the MMA width the kernel issues (N = 64 MMAs take 44.6 cycles, not 32)
+    pk_name = f"f16_ts_n{max(64, min(nt, 128)) if nt != 32 else 64}"
+    f16_peak = pipe.get(pk_name, {}).get("tflops", 2230.0)
+    f16_src = f"profiles pipe peaks {pk_name} (measured)" if pk_name in pipe else "nominal 2.25 PF/s"
+    tensor_work = 3 * 2.0 * entries * passes * nt
+    mufu_ops = entries * passes * (1 if wl.spec.family == "rbf" else 2)
+    mufu_peak = pipe.get("mufu_ex2_gops", 4630.0)
+    t_tensor = tensor_work / (f16_peak * 1e12)
+    t_mufu = mufu_ops / (mufu_peak * 1e9)
+    bound, t_min = ("tensor", t_tensor) if t_tensor >= t_mufu else ("mufu", t_mufu)
+    key = f"kv_product|fp32-f16|on_the_fly|n={n}|rows={n}|m={m}"
+    traffic, traffic_src = ncu_traffic(key)
+    return {"bound": bound, "achieved": (tensor_work if bound == "tensor" else mufu_ops) / (kv_ms * 1e-3)
+            / (1e12 if bound == "tensor" else 1e9),
+            "peak": f16_peak if bound == "tensor" else mufu_peak, "unit": "TFLOP/s" if bound == "tensor" else "Gop/s",
+            "frac": t_min / (kv_ms * 1e-3), "tensor_frac": t_tensor / (kv_ms * 1e-3),
+            "mufu_frac": t_mufu / (kv_ms * 1e-3), "traffic": traffic, "traffic_source": traffic_src,
+            "traffic_key": key, "kernel": f"kv_otf (tcgen05 kind::f16, 3 fp16 products, on the fly, m={m}, NT={nt})",
+            "kernel_ms": kv_ms, "tensor_work_flops": tensor_work, "mufu_ops": mufu_ops,
+            "useful_tflops": 2.0 * entries * m / (kv_ms * 1e-3) / 1e12,
+            "peak_source": f"{f16_src}; MUFU mufu_ex2_gops (measured)"}
+
+
+def extra_otf(rld):
+    """BASELINE config 4 at full n = 262144, K tiles generated on the fly (fp32): 2 timed
+    estimates after 1 warm-up, and the K.V product at the Lanczos shape (m = 64), CUDA events."""
+    import torch
+
+    from paper_2405_03474_b200.workloads import baseline
+
+    wl = baseline(4)
+    cfg = wl.config
+    R = rld.ResidentMatrix(rld.KernelMatrix(wl.spec, wl.points), dtype="fp32", path="on_the_fly")
+    st = torch.cuda.ExternalStream(R.sess.handle.stream)
+    est = R.estimate(cfg)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    K = 2
+    e0.record(st)
+    for _ in range(K):
+        est = R.estimate(cfg)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / K
+    m = cfg.num_probes
+    V = torch.randn(m, wl.n, dtype=torch.float64, device="cuda")
+    R.kv_apply(V)
+    torch.cuda.synchronize()
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record(st)
+    for _ in range(10):
+        R.kv_apply(V)
+    k1.record(st)
+    torch.cuda.synchronize()
+    nt = 32 if m <= 32 else (64 if m <= 64 else 128)
+    out = {"value": 1e3 / ms, "unit": UNIT, "ms_per_step": ms, "dtype": "f32",
+           "config": workload_config(wl, 1, False),
+           "phase_ms_last_step": {"precond": est.phase_ms[1], "lanczos": est.phase_ms[4]},
+           "roofline": roofline_otf(wl, wl.n, m, k0.elapsed_time(k1) / 10, nt),
            "parity": parity_vs_golden(wl, est.value)}
     del R
     torch.cuda.empty_cache()

@@ -115,7 +115,7 @@ __global__ void mufu_kernel(int iters, float seed, float* out) {
 }
 
 // One issuing thread per CTA, one CTA per SM, back-to-back MMAs into one accumulator.
-template <int N, bool TS>
+template <int N, bool TS, bool F16 = false>
 __global__ void __launch_bounds__(128) mma_kernel(int iters, long long* out) {
   __shared__ __align__(1024) uint8_t bsm[256 * 128];
   __shared__ uint64_t bar;
@@ -132,13 +132,21 @@ __global__ void __launch_bounds__(128) mma_kernel(int iters, long long* out) {
   ptx::tc_fence_after();
   const uint32_t tmem = holder;
   if (threadIdx.x == 0) {
-    const uint32_t idesc = ptx::idesc_tf32(128, N);
+    // kind::f16 (fp16 in, f32 accumulate, K = 16): a_format = b_format = 0
+    const uint32_t idesc = F16 ? ((1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24))
+                               : ptx::idesc_tf32(128, N);
     const uint64_t bd = ptx::smem_desc_sw128(ptx::smem_u32(bsm));
     const long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        if (TS) {
+        if (TS && F16) {
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+              "r"(tmem + 256 + 8 * k), "l"(bd + 2 * k), "r"(idesc), "r"(1u)
+              : "memory");
+        } else if (TS) {
           ptx::mma_tf32_ts(tmem, tmem + 256 + 8 * k, bd + 2 * k, idesc, 1u);
         } else {
           asm volatile(
@@ -280,6 +288,17 @@ int main() {
   mma(mma_kernel<64, true>, 64, "tf32_ts_n64", false);
   mma(mma_kernel<128, true>, 128, "tf32_ts_n128", false);
   mma(mma_kernel<256, true>, 256, "tf32_ts_n256", false);
+  auto mmah = [&](auto kern, int N, const char* name) {   // kind::f16: K = 16 per MMA
+    float ms = best_ms([&] { kern<<<sms, 128>>>(mi, lo); });
+    long long cyc = 0;
+    cudaMemcpy(&cyc, lo, 8, cudaMemcpyDeviceToHost);
+    const double fl = (double)sms * mi * 4 * 2.0 * 128 * N * 16;
+    printf(" \"%s\": {\"tflops\": %.1f, \"cycles_per_mma\": %.1f},\n", name, fl / (ms * 1e-3) / 1e12,
+           (double)cyc / (mi * 4.0));
+  };
+  mmah(mma_kernel<64, true, true>, 64, "f16_ts_n64");
+  mmah(mma_kernel<128, true, true>, 128, "f16_ts_n128");
+  mmah(mma_kernel<256, true, true>, 256, "f16_ts_n256");
   auto mma8 = [&](auto kern, int N, const char* name, bool last) {
     float ms = best_ms([&] { kern<<<sms, 128>>>(mi, lo); });
     long long cyc = 0;
