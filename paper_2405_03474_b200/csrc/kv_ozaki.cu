@@ -245,7 +245,7 @@ __global__ void oz_split_reduce_kernel(const double* __restrict__ part, int spli
 __global__ void __launch_bounds__(OZ_THREADS, 1)
 ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, int64_t KS,
                 const double* __restrict__ sigma, const double* __restrict__ tau, int64_t rows, int64_t m, int64_t n,
-                int64_t kchunk, double* __restrict__ out, int64_t ldo, int64_t split_stride) {
+                int64_t kchunk, double* __restrict__ out, int64_t ldo, int64_t split_stride, int nd) {
   extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -279,13 +279,15 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
     if (ptx::elect_one()) {
       const int8_t* ga = Aq + ((int64_t)blockIdx.y * KS + kbeg / OZ_BK) * OZ_A_BYTES;
       const int8_t* gb = Bq + ((int64_t)blockIdx.x * KS + kbeg / OZ_BK) * (OZ_STAGE - OZ_A_BYTES);
+      // only the first nd slices of each operand take part (a contiguous prefix of the k-step image)
+      const uint32_t abytes = (uint32_t)nd * OZ_A_SLICE, bbytes = (uint32_t)nd * OZ_B_SLICE;
       for (int s = 0; s < steps; ++s) {
         const int st = s % OZ_STAGES;
         if (s >= OZ_STAGES) ptx::mbar_wait(&empty[st], ((s / OZ_STAGES) - 1) & 1);
         unsigned char* dst = smem + st * OZ_STAGE;
-        ptx::mbar_arrive_expect_tx(&full[st], OZ_STAGE);
-        bulk_load(dst, ga + (int64_t)s * OZ_A_BYTES, OZ_A_BYTES, &full[st]);
-        bulk_load(dst + OZ_A_BYTES, gb + (int64_t)s * (OZ_STAGE - OZ_A_BYTES), OZ_STAGE - OZ_A_BYTES, &full[st]);
+        ptx::mbar_arrive_expect_tx(&full[st], abytes + bbytes);
+        bulk_load(dst, ga + (int64_t)s * OZ_A_BYTES, abytes, &full[st]);
+        bulk_load(dst + OZ_A_BYTES, gb + (int64_t)s * (OZ_STAGE - OZ_A_BYTES), bbytes, &full[st]);
       }
     }
   } else if (warp == 1) {   // ---- MMA issuer
@@ -303,11 +305,13 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
         // N = 64 ones, and the A operand is read from shared memory once per piece
 #pragma unroll
         for (int sa = 0; sa < OZ_S; ++sa) {
+          if (sa >= nd) break;
           const uint64_t adesc = desc_sw32(a0 + sa * OZ_A_SLICE);
           const uint32_t acc = (s > 0 || sa > 0) ? 1u : 0u;
 #pragma unroll
           for (int t0 = 0; t0 < OZ_DIAG - sa; t0 += 4) {
-            const int nb = (OZ_DIAG - sa - t0) < 4 ? (OZ_DIAG - sa - t0) : 4;   // B slices in this piece
+            if (t0 >= nd - sa) break;
+            const int nb = (nd - sa - t0) < 4 ? (nd - sa - t0) : 4;   // B slices in this piece
             mma_i8_ss(tmem + (uint32_t)((sa + t0) * OZ_BN), adesc, desc_sw32(b0 + t0 * OZ_B_SLICE),
                       idesc_i8(OZ_BM, nb * OZ_BN), acc);
           }
@@ -334,7 +338,7 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
       for (int e = 0; e < 32; ++e) part[e] = 0.0;
       if (steps > 0) {
 #pragma unroll 1
-        for (int d = OZ_DIAG - 1; d >= 0; --d) {   // small terms first
+        for (int d = nd - 1; d >= 0; --d) {   // small terms first
           const double w = __longlong_as_double((long long)(1023 - 7 * (d + 2)) << 52);   // 2^{-7(d+2)}
           uint32_t v[32];
           ptx::tmem_ld_32x32b_x32(tmem + lane_base + (uint32_t)(d * OZ_BN + c0), v);
@@ -415,8 +419,9 @@ void ozaki_slice_points(const double* X, int64_t n, const KernelParams& kp, int6
 // Y (m x rows, ld ldy) = V K^T with K given by its sliced image Kq (ozaki_slice, 128-row tiles) and
 // row scales; V (m x n float64 rows, ld ldv) is sliced here (64-vector tiles) into ws.oz_vq.
 void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int64_t n, const double* V, int64_t ldv,
-                      int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st) {
+                      int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st, int diags) {
   if (m <= 0 || rows <= 0) return;
+  if (diags < 1 || diags > OZ_DIAG) fail(RLD_ERR_INVALID_ARGUMENT, "kv_product_ozaki: diagonals must be 1..8");
   ws.oz_vq.reserve((size_t)ozaki_bytes(m, n, OZ_BN));
   ws.oz_tau.reserve(sizeof(double) * m);
   ozaki_slice(V, ldv, m, n, OZ_BN, ws.oz_vq.as<int8_t>(), ws.oz_tau.as<double>(), st);
@@ -450,14 +455,14 @@ void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int6
   const int8_t* Bq = ws.oz_vq.as<int8_t>();
   if (splits == 1) {
     ozaki_kv_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(Kq, Bq, KS, ksigma, ws.oz_tau.as<double>(), rows, m, n, kchunk,
-                                                      Y, ldy, 0);
+                                                      Y, ldy, 0, diags);
     RLD_LAUNCH_CHECK();
     return;
   }
   const int64_t stride = m * rows;
   ws.partial.reserve(sizeof(double) * stride * splits);
   ozaki_kv_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(Kq, Bq, KS, ksigma, ws.oz_tau.as<double>(), rows, m, n, kchunk,
-                                                    ws.partial.as<double>(), rows, stride);
+                                                    ws.partial.as<double>(), rows, stride, diags);
   RLD_LAUNCH_CHECK();
   const int blocks = (int)std::min<int64_t>(ceil_div(stride, 256), slots * 8);
   oz_split_reduce_kernel<<<blocks, 256, 0, st>>>(ws.partial.as<double>(), (int)splits, stride, m, rows, Y, ldy);

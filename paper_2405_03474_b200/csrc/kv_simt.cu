@@ -246,7 +246,7 @@ void kv_product(const KvOperand& op, int64_t m, const double* V, int64_t ldv, do
     static const bool simt = getenv("RLD_FP64_SIMT") && getenv("RLD_FP64_SIMT")[0] == '1';
     const double* K = static_cast<const double*>(op.K);
     if (!simt && op.kq) {   // exact int8 slices of K on the INT8 tensor cores (kv_ozaki.cu)
-      kv_product_ozaki(op.kq, op.ksigma, op.rows, op.n, V, ldv, m, Y, ldy, ws, st);
+      kv_product_ozaki(op.kq, op.ksigma, op.rows, op.n, V, ldv, m, Y, ldy, ws, st, op.oz_diags);
       return;
     }
     if (!otf && !simt && gemm_nt_f64_ok(K, op.ldk, K, op.ldk)) {

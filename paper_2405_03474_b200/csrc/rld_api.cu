@@ -407,9 +407,10 @@ void gather_rows(rld_handle* h, const double* local, int64_t m, double* full) {
 // Y (m x rows) = V (m x n full) K^T restricted to the local rows.  tc_mode 1 =
 // single-pass TF32 on the tensor cores (power-iteration sketch products only),
 // 3 = 3xTF32 (everything whose value enters the estimate directly).
-void kv(rld_handle* h, int64_t m, const double* Vfull, double* Y, int tc_mode = 3) {
+void kv(rld_handle* h, int64_t m, const double* Vfull, double* Y, int tc_mode = 3, int oz_diags = 8) {
   KvOperand op = h->res.op();
   op.tc_mode = tc_mode;
+  op.oz_diags = oz_diags;
   kv_product(op, m, Vfull, op.n, Y, op.rows, h->wk.kv, h->st, nullptr);
 }
 
@@ -656,6 +657,19 @@ struct PrecondOut {
 // 2.7e-4 (all iterations) and 2.1e-4 (all but the last), beyond the 1e-4 fp32
 // budget, so the default is 3xTF32 everywhere; RLD_SKETCH_MODE=1 opts in to
 // single-pass TF32 for the early iterations.
+// Slice-pair diagonals of the float64 int8-slice product in the first q-1 power iterations: 6
+// (21 of the 36 pairs, dropped terms ~2^-44 of max|K| max|V| per sum term) -- those iterations only
+// steer the subspace, which the last full-precision iteration re-forms.  The last iteration,
+// B = Q K Q^T and every Lanczos product keep all 8 diagonals.  Measured on the float64 estimates
+// against the float64 golden values (config 3 / 1 / 2): 8 diagonals 5.3e-15 / 3.9e-15 / 5.2e-16,
+// 6 diagonals 5.6e-14 / 1.4e-16 / 2.1e-14 (config 3 505 -> 427 ms); DESIGN.md §3.2.
+// RLD_FP64_SKETCH_DIAGS (1..8, read per call) overrides.
+int sketch_oz_diags() {
+  const char* e = getenv("RLD_FP64_SKETCH_DIAGS");
+  const int v = e ? atoi(e) : 6;
+  return v < 1 ? 1 : (v > 8 ? 8 : v);
+}
+
 int sketch_tc_mode() {
   static const int mode = [] {
     const char* e = getenv("RLD_SKETCH_MODE");
@@ -701,7 +715,7 @@ int lowrank_randsvd(rld_handle* h, const rld_config* c, const rld_inputs* in, Pr
       RLD_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), st));
       for (int it = 0; it < c->precond_iters; ++it) {
         const bool last = it + 1 == c->precond_iters;
-        kv(h, w, Y, Z, last ? 3 : sketch_tc_mode());      // Y <- Y M      (src/precond.py:186)
+        kv(h, w, Y, Z, last ? 3 : sketch_tc_mode(), last ? 8 : sketch_oz_diags());   // Y <- Y M (src/precond.py:186)
         if (householder) {
           qr_householder(h, nl, w, Z, c->orth_rtol, flags);
           gather_rows(h, Z, w, Y);

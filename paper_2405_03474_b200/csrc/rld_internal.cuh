@@ -106,6 +106,7 @@ struct KvOperand {
   int64_t row0 = 0;          // first global row held locally
   int64_t rows = 0;          // local rows
   int tc_mode = 3;           // tensor-core product: 3 = 3xTF32 (Lanczos), 1 = 1xTF32 (sketch)
+  int oz_diags = 8;          // float64 int8-slice product: slice-pair diagonals kept (8 = all 36 pairs)
 };
 
 struct KvWorkspace {
@@ -166,7 +167,7 @@ void ozaki_slice(const double* A, int64_t lda, int64_t rows, int64_t n, int tile
 void ozaki_slice_points(const double* X, int64_t n, const KernelParams& kp, int64_t row0, int64_t rows, int8_t* q,
                         double* scale, cudaStream_t st);
 void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int64_t n, const double* V, int64_t ldv,
-                      int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st);
+                      int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st, int diags = 8);
 // Which float64 stored-K product a prepare sets up: the int8 slices (default) or, with
 // RLD_FP64_PRODUCT=dmma, the DMMA kernel on the float64 K.
 bool fp64_product_ozaki();

@@ -9,6 +9,7 @@
 """
 
 from dataclasses import replace
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -200,3 +201,29 @@ def test_int8_slices_edge_cases(rld, monkeypatch, n, m):
     assert np.all(Y[0] == 0.0) and np.all(Y[:, n // 2] == 0.0)
     bound = 2.0 ** -50 * n * np.outer(np.abs(V).max(axis=1), np.abs(A).max(axis=1))
     assert np.all(np.abs(Y - ref) <= bound + 1e-300)
+
+
+@pytest.mark.parametrize("index", [1, 2])
+def test_fp64_sketch_diagonals(rld, index, monkeypatch):
+    """The first q-1 power iterations run the int8-slice float64 product with 6 of its 8 slice-pair
+    diagonals (rld_api.cu sketch_oz_diags); the last iteration, B = Q K Q^T and the Lanczos products
+    keep all 36 pairs.  The estimate must stay float64-grade: within 1e-12 of the all-pairs run and
+    of the unmodified reference's golden value (north_star fp64 bar: 1e-6)."""
+    import json
+    from dataclasses import replace
+
+    from conftest import rel
+    from paper_2405_03474_b200.workloads import baseline
+
+    gold = {c["name"]: c for c in json.load(open(Path(__file__).parent / "golden" / "golden.json"))}[
+        f"config{index}_r3"]["value"]
+    wl = baseline(index, dtype="fp64")
+    cfg = replace(wl.config, dtype="fp64", path="stored")
+    R = rld.ResidentMatrix(rld.KernelMatrix(wl.spec, wl.points), dtype="fp64", path="stored")
+    monkeypatch.setenv("RLD_FP64_SKETCH_DIAGS", "8")
+    full = R.estimate(cfg)
+    monkeypatch.delenv("RLD_FP64_SKETCH_DIAGS")
+    default = R.estimate(cfg)
+    assert rel(default.value, full.value) <= 1e-12, (default.value, full.value)
+    assert rel(default.logdet_P, full.logdet_P) <= 1e-12
+    assert rel(default.value, gold) <= 1e-12, (default.value, gold)
