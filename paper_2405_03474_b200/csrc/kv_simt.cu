@@ -245,6 +245,10 @@ void kv_product(const KvOperand& op, int64_t m, const double* V, int64_t ldv, do
     // it is not; a K aliased from a caller's odd-pitched matrix takes this file's DFMA kernel.
     static const bool simt = getenv("RLD_FP64_SIMT") && getenv("RLD_FP64_SIMT")[0] == '1';
     const double* K = static_cast<const double*>(op.K);
+    if (!simt && op.kr && m >= CRT_MIN_M) {   // wide: modular int8 GEMMs + CRT (kv_crt.cu)
+      kv_product_crt(op.kr, op.ksigma, op.rows, op.n, V, ldv, m, Y, ldy, ws, st);
+      return;
+    }
     if (!simt && op.kq) {   // exact int8 slices of K on the INT8 tensor cores (kv_ozaki.cu)
       kv_product_ozaki(op.kq, op.ksigma, op.rows, op.n, V, ldv, m, Y, ldy, ws, st, op.oz_diags);
       return;

@@ -95,6 +95,8 @@ struct Resident {
   DevBuf diag;               // local diagonal of K (float64)
   DevBuf Kq, ksigma;         // float64 K as exact int8 slices (RLD_FP64_PRODUCT=ozaki, kv_ozaki.cu)
   bool kq_ready = false;
+  DevBuf Kr;                 // residues of K' modulo the CRT moduli (kv_crt.cu), for the wide products
+  bool kr_ready = false;
   KernelParams kp{};
 
   KvOperand op() const {
@@ -109,6 +111,7 @@ struct Resident {
     if (kq_ready && path != RLD_PATH_ON_THE_FLY) {
       o.kq = Kq.as<int8_t>();
       o.ksigma = ksigma.as<double>();
+      if (kr_ready) o.kr = Kr.as<int8_t>();
     }
     o.n = n;
     o.row0 = row0;
@@ -221,6 +224,7 @@ void prepare(rld_handle* h, const rld_problem* p) {
   r.ready = false;
   r.tiled = false;
   r.kq_ready = false;
+  r.kr_ready = false;
   h->precond_k = -1;
   r.source = p->source;
   r.dtype = p->dtype;
@@ -365,6 +369,18 @@ void prepare(rld_handle* h, const rld_problem* p) {
     ozaki_slice(static_cast<const double*>(r.K), r.ldk, r.rows, r.n, 128, r.Kq.as<int8_t>(), r.ksigma.as<double>(),
                 st);
     r.kq_ready = true;
+  }
+  if (r.kq_ready && crt_supported(r.n)) {
+    // the CRT residue image for the wide (sketch) products, where it fits beside the slices
+    const int64_t bytes = crt_bytes(r.rows, r.n);
+    size_t fr = 0, tot = 0;
+    RLD_CUDA(cudaStreamSynchronize(st));
+    RLD_CUDA(cudaMemGetInfo(&fr, &tot));
+    if ((int64_t)r.Kr.bytes >= bytes || (int64_t)fr > bytes + (int64_t)(tot / 16)) {
+      r.Kr.reserve((size_t)bytes);
+      crt_residues(r.Kq.as<int8_t>(), r.rows, r.n, r.Kr.as<int8_t>(), st);
+      r.kr_ready = true;
+    }
   }
   RLD_CUDA(cudaStreamSynchronize(st));
   r.ready = true;

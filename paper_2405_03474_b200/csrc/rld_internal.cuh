@@ -107,6 +107,7 @@ struct KvOperand {
   int64_t rows = 0;          // local rows
   int tc_mode = 3;           // tensor-core product: 3 = 3xTF32 (Lanczos), 1 = 1xTF32 (sketch)
   int oz_diags = 8;          // float64 int8-slice product: slice-pair diagonals kept (8 = all 36 pairs)
+  const int8_t* kr = nullptr;      // K' residues modulo the CRT moduli (kv_crt.cu), or null
 };
 
 struct KvWorkspace {
@@ -118,6 +119,7 @@ struct KvWorkspace {
   cublasHandle_t blas = nullptr;   // the handle's cuBLAS (bound to the same stream): fp64 stored K
   DevBuf oz_vq, oz_tau;            // int8 slices of V and their column scales (kv_ozaki.cu)
   DevBuf otf_vmax;                 // per-vector max |V| of the fp16 on-the-fly product (kv_otf.cu)
+  DevBuf crt_vmax, crt_vr, crt_out;   // CRT product (kv_crt.cu): V scales, V residues, output residues
 };
 
 bool kv_tc_supported(const KvOperand& op);
@@ -168,6 +170,14 @@ void ozaki_slice_points(const double* X, int64_t n, const KernelParams& kp, int6
                         double* scale, cudaStream_t st);
 void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int64_t n, const double* V, int64_t ldv,
                       int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st, int diags = 8);
+// Wide float64 products as 15 modular int8 GEMMs + CRT (kv_crt.cu); the residue image of K comes
+// from its slice image (crt_residues, 15 bytes per entry).
+bool crt_supported(int64_t n);
+int64_t crt_bytes(int64_t rows, int64_t n);
+void crt_residues(const int8_t* Kq, int64_t rows, int64_t n, int8_t* Kr, cudaStream_t st);
+void kv_product_crt(const int8_t* Kr, const double* ksigma, int64_t rows, int64_t n, const double* V, int64_t ldv,
+                    int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st);
+constexpr int64_t CRT_MIN_M = 96;   // narrower products (the Lanczos block) stay on the slices
 // Which float64 stored-K product a prepare sets up: the int8 slices (default) or, with
 // RLD_FP64_PRODUCT=dmma, the DMMA kernel on the float64 K.
 bool fp64_product_ozaki();
