@@ -36,24 +36,16 @@
 #include "rld_device.cuh"
 #include "rld_internal.cuh"
 #include "tc_ptx.cuh"
+#include "crt_common.cuh"
 
 namespace rld {
 
 namespace {
 
-constexpr int CRT_L = 15;           // moduli used
 constexpr int CRT_BM = 128, CRT_BK = 32;
 constexpr int CRT_KB = 4;           // k-steps per stage
 constexpr int CRT_THREADS = 256;
-constexpr int CRT_SLICES = 7;       // slices of K forming K' (49 bits)
 constexpr int CRT_KBITS_X100 = 4802;   // log2 max|K'| * 100 (|K'| < 64 sum_k 128^k < 2^48.02)
-__host__ __device__ constexpr int crt_mod(int l) {
-  // pairwise coprime, largest first: 2^8, 3.5.17, 11.23, 251, 13.19, 241, 239, 233, 229, 227, 223, 7.31, 211, 199, 197
-  return l == 0 ? 256 : l == 1 ? 255 : l == 2 ? 253 : l == 3 ? 251 : l == 4 ? 247 : l == 5 ? 241 : l == 6 ? 239
-       : l == 7 ? 233 : l == 8 ? 229 : l == 9 ? 227 : l == 10 ? 223 : l == 11 ? 217 : l == 12 ? 211 : l == 13 ? 199
-       : 197;
-}
-
 struct CrtConst {
   int coef[CRT_SLICES][CRT_L];   // 128^{6-s} mod p_l
   int u[CRT_L];                  // (P / p_l)^-1 mod p_l
@@ -101,14 +93,6 @@ CrtConst make_consts() {
 const CrtConst& consts() {
   static const CrtConst c = make_consts();
   return c;
-}
-
-// symmetric residue of an int32 x modulo p (odd p: [-(p-1)/2, (p-1)/2]; p = 256: [-128, 127])
-__device__ __forceinline__ int sym_mod(int x, int p) {
-  int r = x % p;
-  if (r > (p - 1) / 2) r -= p;
-  if (r < -(p / 2)) r += p;
-  return r;
 }
 
 __device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr) {

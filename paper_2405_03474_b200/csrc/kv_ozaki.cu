@@ -37,6 +37,7 @@
 #include "rld_device.cuh"
 #include "rld_internal.cuh"
 #include "tc_ptx.cuh"
+#include "crt_common.cuh"
 
 namespace rld {
 
@@ -169,29 +170,38 @@ __global__ void ozaki_digits_kernel(const double* __restrict__ A, int64_t lda, i
 // entries are kgen.cu's float64 values (direct differences, kernel_value_f64, exact diagonal) and
 // every row's maximum is the diagonal a^2 + jitter (a stationary kernel: |K_ij| <= a^2), so sigma is
 // known up front.  Bitwise the slices of the stored float64 K.
-__global__ void ozaki_points_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, int64_t row0,
-                                    int64_t rows, int64_t KS, int8_t* __restrict__ q) {
+// Kr != null: also the CRT residue image (kv_crt.cu) of K' = sum_{s<7} d_s 128^{6-s}, same
+// swizzled position, ((t L + l) KS + ks) 4096 + phys -- in the same pass (no second read of the
+// 34 GB slice image).  Thread = EL consecutive columns of one row (EL = 8: 80 registers, 3 CTAs per
+// SM; 16 columns per thread held 128 registers and ran at 25 % occupancy, latency-bound).
+template <bool CRT, int EL, int DMAX>
+__global__ void __launch_bounds__(256)
+ozaki_points_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, int64_t row0,
+                    int64_t rows, int64_t KS, int8_t* __restrict__ q, int8_t* __restrict__ Kr) {
   constexpr int TR = OZ_BM;
+  constexpr int PARTS = OZ_BK / EL;          // threads per (row, k-step)
+  constexpr int W = EL / 4;                  // 32-bit words per slice
   const int d = kp.d;
   int ee = 0;
   frexp(kp.diag > 0.0 ? kp.diag : 1.0, &ee);   // diag = f 2^ee: sigma = 2^(ee+1), x = v 2^-(ee+1)
-  const int sh = -(ee + 1);
-  const int64_t total = ceil_div(rows, TR) * TR * KS * 2;
+  const double scl = ldexp(1.0, -(ee + 1));    // exact power of two
+  const int64_t total = ceil_div(rows, TR) * TR * KS * PARTS;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int h = (int)(e & 1);
-    const int i = (int)((e >> 1) % TR);
-    const int64_t rest = (e >> 1) / TR;
+    const int h = (int)(e % PARTS);
+    const int i = (int)((e / PARTS) % TR);
+    const int64_t rest = (e / PARTS) / TR;
     const int64_t ks = rest % KS;
     const int64_t t = rest / KS;
     const int64_t row = t * TR + i;
     const int64_t gi = row0 + row;
-    const int64_t j0 = ks * OZ_BK + 16 * h;
-    double xi[RLD_MAX_DIM];
-#pragma unroll 4
-    for (int k = 0; k < d; ++k) xi[k] = row < rows ? X[gi * d + k] : 0.0;
-    uint32_t w[OZ_S][4];
+    const int64_t j0 = ks * OZ_BK + EL * h;
+    double xi[DMAX];   // DMAX = 4: registers (d <= 4), else local memory
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
+    for (int k = 0; k < DMAX; ++k) xi[k] = (k < d && row < rows) ? X[gi * d + k] : 0.0;
+    uint32_t w[OZ_S][W];
+    long long kq[EL];   // CRT: K' of the EL entries
+#pragma unroll
+    for (int k = 0; k < EL; ++k) {
       const int64_t j = j0 + k;
       double v = 0.0;
       if (row < rows && j < n) {
@@ -199,30 +209,78 @@ __global__ void ozaki_points_kernel(const double* __restrict__ X, int64_t n, Ker
           v = kp.diag;
         } else {
           double r2 = 0.0;
-          for (int c = 0; c < d; ++c) {
-            const double df = xi[c] - X[j * d + c];
-            r2 = fma(df, df, r2);
+#pragma unroll
+          for (int c = 0; c < DMAX; ++c) {
+            if (c < d) {
+              const double df = xi[c] - X[j * d + c];
+              r2 = fma(df, df, r2);
+            }
           }
           v = kernel_value_f64(kp, r2);
         }
       }
-      double r = ldexp(v, sh);
+      double r = v * scl;
+      double kd = 0.0;   // K' (exact in float64: |K'| < 2^48.02)
 #pragma unroll
       for (int s = 0; s < OZ_S; ++s) {
         const double x = r * 128.0;
         const double dg = rint(x);
         r = x - dg;
+        if (CRT && s < CRT_SLICES) kd = fma(kd, 128.0, dg);
         const uint32_t b = (uint32_t)(uint8_t)(int8_t)(int)dg;
         if ((k & 3) == 0) w[s][k >> 2] = b;
         else w[s][k >> 2] |= b << (8 * (k & 3));
       }
+      if (CRT) kq[k] = __double2ll_rn(kd);
     }
-    const uint32_t o = (uint32_t)(i * OZ_BK + 16 * h);
+    const uint32_t o = (uint32_t)(i * OZ_BK + EL * h);
     const uint32_t phys = o ^ (((o >> 7) & 1u) << 4);
     int8_t* base = q + (t * KS + ks) * (int64_t)OZ_S * TR * OZ_BK + phys;
 #pragma unroll
-    for (int s = 0; s < OZ_S; ++s)
-      *reinterpret_cast<uint4*>(base + (int64_t)s * TR * OZ_BK) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+    for (int s = 0; s < OZ_S; ++s) {
+      if (W == 4)
+        *reinterpret_cast<uint4*>(base + (int64_t)s * TR * OZ_BK) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+      else
+        *reinterpret_cast<uint2*>(base + (int64_t)s * TR * OZ_BK) = make_uint2(w[s][0], w[s][1]);
+    }
+    if (CRT) {
+      // residues on the FP32 pipe: K' = a 2^36 + b 2^24 + c 2^12 + d (|a| < 2^12.02, 0 <= b, c, d < 2^12);
+      // acc = a (2^36 mod p) + b (2^24 mod p) + c (2^12 mod p) + d with symmetric constants (|.| <= 128)
+      // is an exact fp32 integer (|acc| < 2^21); r = acc - p rint(acc / p) (rint by the 1.5 2^23
+      // magic add: exact for odd p, whose residues never tie) and its int8 byte is the low byte of
+      // r + 1.5 2^23 (for p = 256 a tie gives +-128, the same class mod 256)
+      float fa[EL], fb[EL], fc[EL], fd[EL];
+#pragma unroll
+      for (int k = 0; k < EL; ++k) {
+        const long long kk = kq[k];
+        fa[k] = (float)(int)(kk >> 36);
+        fb[k] = (float)(int)((kk >> 24) & 0xFFF);
+        fc[k] = (float)(int)((kk >> 12) & 0xFFF);
+        fd[k] = (float)(int)(kk & 0xFFF);
+      }
+      constexpr float MAGIC = 12582912.0f;
+#pragma unroll
+      for (int l = 0; l < CRT_L; ++l) {
+        const int p = crt_mod(l);
+        const float A = (float)crt_pow2_sym(36, p), B = (float)crt_pow2_sym(24, p), C = (float)crt_pow2_sym(12, p);
+        const float pf = (float)p, inv = 1.0f / (float)p;
+        uint32_t wv[W];
+#pragma unroll
+        for (int k = 0; k < EL; ++k) {
+          const float acc = fmaf(fa[k], A, fmaf(fb[k], B, fmaf(fc[k], C, fd[k])));
+          const float qq = fmaf(acc, inv, MAGIC) - MAGIC;
+          const float rr = fmaf(-qq, pf, acc);
+          const uint32_t b8 = __float_as_uint(rr + MAGIC) & 0xFFu;
+          if ((k & 3) == 0) wv[k >> 2] = b8;
+          else wv[k >> 2] |= b8 << (8 * (k & 3));
+        }
+        int8_t* dst = Kr + ((t * CRT_L + l) * KS + ks) * (int64_t)TR * OZ_BK + phys;
+        if (W == 4)
+          *reinterpret_cast<uint4*>(dst) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        else
+          *reinterpret_cast<uint2*>(dst) = make_uint2(wv[0], wv[1]);
+      }
+    }
   }
 }
 
@@ -402,7 +460,7 @@ void ozaki_slice(const double* A, int64_t lda, int64_t rows, int64_t n, int tile
 }
 
 void ozaki_slice_points(const double* X, int64_t n, const KernelParams& kp, int64_t row0, int64_t rows, int8_t* q,
-                        double* scale, cudaStream_t st) {
+                        double* scale, cudaStream_t st, int8_t* Kr) {
   if (rows <= 0) return;
   if (kp.d > RLD_MAX_DIM) fail(RLD_ERR_NOT_SUPPORTED, "ozaki_slice_points: d > 32");
   int ee = 0;
@@ -410,9 +468,16 @@ void ozaki_slice_points(const double* X, int64_t n, const KernelParams& kp, int6
   oz_fill_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, st>>>(rows, ldexp(1.0, ee + 1), scale);
   RLD_LAUNCH_CHECK();
   const int64_t KS = ceil_div(n, OZ_BK);
-  const int64_t total = ceil_div(rows, OZ_BM) * OZ_BM * KS * 2;
+  const int64_t total = ceil_div(rows, OZ_BM) * OZ_BM * KS * 4;
   const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)oz_sms() * 16);
-  ozaki_points_kernel<<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q);
+  if (Kr && kp.d <= 4)
+    ozaki_points_kernel<true, 8, 4><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, Kr);
+  else if (Kr)
+    ozaki_points_kernel<true, 8, RLD_MAX_DIM><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, Kr);
+  else if (kp.d <= 4)
+    ozaki_points_kernel<false, 8, 4><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, nullptr);
+  else
+    ozaki_points_kernel<false, 8, RLD_MAX_DIM><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, nullptr);
   RLD_LAUNCH_CHECK();
 }
 

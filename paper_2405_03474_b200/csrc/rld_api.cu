@@ -274,8 +274,21 @@ void prepare(rld_handle* h, const rld_problem* p) {
         if (r.rows > 0) {
           r.Kq.reserve((size_t)ozaki_bytes(r.rows, p->n, 128));
           r.ksigma.reserve(sizeof(double) * r.rows);
+          // the CRT residue image for the wide (sketch) products in the same pass, where it fits
+          int8_t* kr = nullptr;
+          if (crt_supported(p->n)) {
+            const int64_t bytes = crt_bytes(r.rows, p->n);
+            size_t fr = 0, tot = 0;
+            RLD_CUDA(cudaStreamSynchronize(st));
+            RLD_CUDA(cudaMemGetInfo(&fr, &tot));
+            if ((int64_t)r.Kr.bytes >= bytes || (int64_t)fr > bytes + (int64_t)(tot / 16)) {
+              r.Kr.reserve((size_t)bytes);
+              kr = r.Kr.as<int8_t>();
+            }
+          }
           ozaki_slice_points(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.Kq.as<int8_t>(), r.ksigma.as<double>(),
-                             st);
+                             st, kr);
+          r.kr_ready = kr != nullptr;
         }
         r.kq_ready = r.rows > 0;
       } else if (p->dtype == RLD_FP64) {
@@ -370,7 +383,7 @@ void prepare(rld_handle* h, const rld_problem* p) {
                 st);
     r.kq_ready = true;
   }
-  if (r.kq_ready && crt_supported(r.n)) {
+  if (r.kq_ready && !r.kr_ready && crt_supported(r.n)) {
     // the CRT residue image for the wide (sketch) products, where it fits beside the slices
     const int64_t bytes = crt_bytes(r.rows, r.n);
     size_t fr = 0, tot = 0;

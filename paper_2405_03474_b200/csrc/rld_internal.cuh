@@ -166,8 +166,9 @@ int64_t ozaki_bytes(int64_t rows, int64_t n, int tile_rows);   // size of a slic
 void ozaki_slice(const double* A, int64_t lda, int64_t rows, int64_t n, int tile_rows, int8_t* q, double* scale,
                  cudaStream_t st);
 // the same image straight from the points (no float64 K): stationary kernel, row max = diagonal
+// Kr != null: also K's CRT residue image (kv_crt.cu), crt_bytes(rows, n) bytes
 void ozaki_slice_points(const double* X, int64_t n, const KernelParams& kp, int64_t row0, int64_t rows, int8_t* q,
-                        double* scale, cudaStream_t st);
+                        double* scale, cudaStream_t st, int8_t* Kr = nullptr);
 void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int64_t n, const double* V, int64_t ldv,
                       int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st, int diags = 8);
 // Wide float64 products as 15 modular int8 GEMMs + CRT (kv_crt.cu); the residue image of K comes
