@@ -370,6 +370,23 @@ def run_ours(args):
     torch.cuda.synchronize()
     kv_ms = k0.elapsed_time(k1) / reps
     roofline = roofline_for(wl, cfg, rows, n, s, kv_ms, world)
+    # float64 stored K: the sketch products (m = w) run on the CRT kernel and take the most time of
+    # any kernel (6 of the 26 products); their roofline is the headline one, the Lanczos product's
+    # (HBM) is kept beside it
+    roofline_lanczos = None
+    if cfg.dtype == "fp64" and wl.path == "stored" and os.environ.get("RLD_FP64_SKETCH") != "slices":
+        Vw = torch.randn(w, n, dtype=torch.float64, device="cuda")
+        for _ in range(2):
+            R.kv_apply(Vw)
+        torch.cuda.synchronize()
+        k0.record(stream)
+        for _ in range(5):
+            R.kv_apply(Vw)
+        k1.record(stream)
+        torch.cuda.synchronize()
+        roofline_lanczos = roofline
+        roofline = roofline_crt(rows, n, w, k0.elapsed_time(k1) / 5)
+        del Vw
 
     # ---- end to end through the public API (host buffers, pinned)
     e2e = None
@@ -443,6 +460,7 @@ def run_ours(args):
         "phase_ms_last_step": {"precond": phases[1], "lanczos": phases[4], "solves": phases[5]},
         "roofline": roofline,
         "clocks": clocks,
+        **({"roofline_lanczos": roofline_lanczos} if roofline_lanczos else {}),
         "estimate": est.value,
     }
     if concurrent is not None:
@@ -593,6 +611,28 @@ def extra_fp32(args, rld, world, sharded, per_step):
     del R
     torch.cuda.empty_cache()
     return out
+
+
+def roofline_crt(rows, n, w, ms):
+    """The float64 sketch product (csrc/kv_crt.cu): 15 modular int8 GEMMs (CRT), tensor-bound.  The
+    time covers the whole product call (V residues, the GEMM, the CRT reconstruction); the peak is
+    the int8 rate on random operand bytes sustained for ~4.7 s (the power-capped clock a long step
+    runs at; profiles/r02c_pipe_peaks.json)."""
+    pipe = load_pipe_peaks()
+    ops = 15 * 2.0 * rows * n * w
+    rec = pipe.get("i8_ss_n256_random_sustained", {})
+    peak, src = (rec["tops"], "profiles/r02c_pipe_peaks.json i8_ss_n256_random_sustained (measured)") if rec else (
+        pipe.get("i8_ss_n256", {}).get("tops", 4576.0), "pipe peaks i8_ss_n256 (measured, burst)")
+    ach = ops / (ms * 1e-3) / 1e12
+    key = f"kv_product|fp64-crt|stored|n={n}|rows={rows}|m={w}"
+    traffic, traffic_src = ncu_traffic(key)
+    burst = pipe.get("i8_ss_n256_random_burst", {}).get("tops")
+    return {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TOPS (int8)", "frac": ach / peak,
+            "frac_of_burst": ach / burst if burst else None, "traffic": traffic, "traffic_source": traffic_src,
+            "traffic_key": key, "alg_bytes": 15 * rows * n + 8 * n * w + 8 * rows * w,
+            "kernel": f"kv_crt (15 modular tcgen05 kind::i8 GEMMs + CRT, float64 sketch product, m=w={w}, {rows} rows)",
+            "kernel_ms": ms, "int8_ops": ops, "equiv_fp64_tflops": 2.0 * rows * n * w / (ms * 1e-3) / 1e12,
+            "peak_source": src}
 
 
 def roofline_otf(wl, n, m, kv_ms, nt):

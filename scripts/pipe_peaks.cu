@@ -173,12 +173,18 @@ __device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr) {
          ((uint64_t)6 << 61);
 }
 
-template <int N>
+// RAND: operands random bytes (the data a real int8-slice / residue product multiplies; constant
+// operands draw far less power and never meet the 1 kW cap)
+template <int N, bool RAND = false>
 __global__ void __launch_bounds__(128) mma_i8_kernel(int iters, long long* out) {
   __shared__ __align__(1024) uint8_t sm[128 * 32 + 256 * 32];
   __shared__ uint64_t bar;
   __shared__ uint32_t holder;
-  for (int i = threadIdx.x; i < (int)sizeof(sm) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u;
+  for (int i = threadIdx.x; i < (int)sizeof(sm) / 4; i += blockDim.x) {
+    uint32_t x = (uint32_t)(i + 1) * 2654435761u ^ (uint32_t)blockIdx.x * 0x9E3779B9u;
+    x ^= x >> 15; x *= 0x2c1b3c6du; x ^= x >> 12;
+    reinterpret_cast<uint32_t*>(sm)[i] = RAND ? x : 0x01010101u;
+  }
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar, 1);
     ptx::fence_mbarrier_init();
@@ -309,7 +315,27 @@ int main() {
   };
   mma8(mma_i8_kernel<64>, 64, "i8_ss_n64", false);
   mma8(mma_i8_kernel<128>, 128, "i8_ss_n128", false);
-  mma8(mma_i8_kernel<256>, 256, "i8_ss_n256", true);
+  mma8(mma_i8_kernel<256>, 256, "i8_ss_n256", false);
+  {
+    // sustained: back-to-back launches for ~4 s (the power-capped clock a long int8 step runs at)
+    float ms1 = best_ms([&] { mma_i8_kernel<256, true><<<sms, 128>>>(mi, lo); });
+    {
+      const double ops1 = (double)sms * mi * 4 * 2.0 * 128 * 256 * 32;
+      printf(" \"i8_ss_n256_random_burst\": {\"tops\": %.1f},\n", ops1 / (ms1 * 1e-3) / 1e12);
+    }
+    const int reps = (int)(4000.0f / (ms1 > 0.01f ? ms1 : 0.01f)) + 1;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    for (int r = 0; r < reps; ++r) mma_i8_kernel<256, true><<<sms, 128>>>(mi, lo);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    const double ops = (double)reps * sms * mi * 4 * 2.0 * 128 * 256 * 32;
+    printf(" \"i8_ss_n256_random_sustained\": {\"tops\": %.1f, \"seconds\": %.2f}\n", ops / (ms * 1e-3) / 1e12, ms * 1e-3);
+  }
   printf("}\n");
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
