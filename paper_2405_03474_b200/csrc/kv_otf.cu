@@ -49,7 +49,7 @@ namespace {
 constexpr int OB_M = 128;          // K rows per tile (UMMA M)
 constexpr int OB_K = 64;           // k-elements per step (one 128-byte fp16 swizzle row)
 constexpr int OTF_THREADS = 640;   // 20 warps
-constexpr uint32_t PTS_STAGE = 2048;   // 64 column points: [2][8][32] fp32
+constexpr uint32_t PTS_STAGE_POINTS = 2048;   // 64 column points: [2][8][32] fp32
 constexpr int SCALE_TOP = 13;      // scaled magnitudes in [2^13, 2^14)
 
 struct OtfParams {
@@ -64,6 +64,8 @@ struct OtfParams {
   uint32_t wait_ns;
   const float* pts;     // [ceil(n/64) * 2][8][32] pre-scaled float32 coordinates
   int64_t n, row0, rows;
+  const float* rowscale;   // stored K (DIM == 0): per local row 2^s_i with max_j |K_ij| 2^s_i in [2^13, 2^14)
+  int ks32;             // stored K: 32-column tiles per row tile of the tiled layout
   float diag;           // 2^sK (a^2 + jitter)
   float la2;            // log2(a^2) + sK
   int family;
@@ -148,6 +150,24 @@ __device__ __forceinline__ void gen32(const OtfParams& p, uint32_t pp, const uin
   }
 }
 
+// 32 stored K entries of one row (one 16 KB tile [128][32] fp32, 128-byte swizzled: chunk c of
+// row r at ((c ^ (r & 7)) << 4)) scaled by 2^s (exact) and split into fp16 head / tail words
+__device__ __forceinline__ void load32(uint32_t rowp, int row, float rs, uint32_t (&hw)[16], uint32_t (&lw)[16]) {
+  const uint64_t neg1 = pk(-1.f, -1.f), sc = pk(rs, rs);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const float4 v = ptx::lds128(rowp + (uint32_t)((c ^ (row & 7)) << 4));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint64_t kv = mul2(h == 0 ? pk(v.x, v.y) : pk(v.z, v.w), sc);
+      const uint32_t h0 = (uint32_t)kv & 0xFFFFE000u, h1 = (uint32_t)(kv >> 32) & 0xFFFFE000u;
+      const uint64_t l2 = fma2((uint64_t)h0 | ((uint64_t)h1 << 32), neg1, kv);
+      hw[2 * c + h] = f16x2(__uint_as_float(h0), __uint_as_float(h1));
+      lw[2 * c + h] = f16x2(pk_lo(l2), pk_hi(l2));
+    }
+  }
+}
+
 template <int NT>
 struct OtfShape {
   static constexpr bool STACK = NT == 32;           // [Bh; Bl] as one N = 64 operand
@@ -167,11 +187,14 @@ struct OtfShape {
   static_assert(NT % 16 == 0 && (NT / DP) % 16 == 0 && NT <= 128, "NT");
 };
 
+// DIM > 0: K tiles generated from the points; DIM == 0: stored fp32 K (tiled layout, kgen.cu), two
+// 16 KB tiles per 64-column stage, per-row power-of-two scales (the wide products of configs 2-3)
 template <int NT, int DIM, int FAM>
 __global__ void __launch_bounds__(OTF_THREADS, 1)
 kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmBh,
               const __grid_constant__ CUtensorMap tmBl, const OtfParams p) {
   using Sh = OtfShape<NT>;
+  constexpr uint32_t PTS_STAGE = DIM == 0 ? 32768u : PTS_STAGE_POINTS;
   constexpr int DW = Sh::DW, NACC = Sh::NACC;
   constexpr uint32_t B_BYTES = Sh::B_BYTES, BST = Sh::BST, ASTRIDE = Sh::ASTRIDE, A_COL0 = Sh::A_COL0;
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -231,7 +254,11 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
         ptx::mbar_wait_idle(&kempty[s], it.ph ^ 1, p.wait_mode, p.wait_ns);
         if (ptx::elect_one()) {
           ptx::mbar_arrive_expect_tx(&kfull[s], PTS_STAGE);
-          ptx::tma_load_2d(pring + (size_t)s * PTS_STAGE, &tmP, &kfull[s], 0, it.kstep * 16);
+          if (DIM == 0)   // tiles 2 kstep, 2 kstep + 1 of row tile `tile`: one 256-row box
+            ptx::tma_load_2d(pring + (size_t)s * PTS_STAGE, &tmP, &kfull[s], 0,
+                             (it.tile * p.ks32 + 2 * it.kstep) * OB_M);
+          else
+            ptx::tma_load_2d(pring + (size_t)s * PTS_STAGE, &tmP, &kfull[s], 0, it.kstep * 16);
         }
         __syncwarp();
       }
@@ -336,9 +363,10 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
       const int row = q * 32 + lane;
       const uint32_t lane_base = (uint32_t)(q * 32) << 16;
       int cur_tile = -1;
-      uint64_t xr2[DIM];
+      uint64_t xr2[DIM > 0 ? DIM : 1];
 #pragma unroll
-      for (int k = 0; k < DIM; ++k) xr2[k] = 0;
+      for (int k = 0; k < (DIM > 0 ? DIM : 1); ++k) xr2[k] = 0;
+      float rs = 0.f;   // stored K: this row's scale
       int grow = 0, wrow0 = 0;
       const int n32 = (int)p.n;
       int pend = -1;
@@ -361,10 +389,14 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
           wrow0 = (int)p.row0 + cur_tile * OB_M + q * 32;
           grow = wrow0 + lane;
           if (lr < p.rows) {
+            if (DIM == 0) {
+              rs = p.rowscale[lr];
+            } else {
 #pragma unroll
-            for (int k = 0; k < DIM; ++k) {
-              const float x = p.pts[(((int64_t)(grow >> 5) * 8 + k) << 5) + (grow & 31)];
-              xr2[k] = pk(x, x);
+              for (int k = 0; k < DIM; ++k) {
+                const float x = p.pts[(((int64_t)(grow >> 5) * 8 + k) << 5) + (grow & 31)];
+                xr2[k] = pk(x, x);
+              }
             }
           }
         }
@@ -382,11 +414,16 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           uint32_t hw[16], lw[16];
-          const uint32_t pp = ptx::smem_u32(pring + (size_t)s * PTS_STAGE) + 1024u * half;
-          const int j0 = it.kstep * OB_K + 32 * half;
-          const bool fix = (j0 < wrow0 + 32 && j0 + 32 > wrow0) || (j0 + 32 > n32);
-          if (!fix) gen32<DIM, FAM, false>(p, pp, xr2, 0, 0, 0, hw, lw);
-          else gen32<DIM, FAM, true>(p, pp, xr2, j0, grow, n32, hw, lw);
+          if constexpr (DIM == 0) {
+            load32(ptx::smem_u32(pring + (size_t)s * PTS_STAGE) + 16384u * half + (uint32_t)row * 128u, row, rs, hw,
+                   lw);
+          } else {
+            const uint32_t pp = ptx::smem_u32(pring + (size_t)s * PTS_STAGE) + 1024u * half;
+            const int j0 = it.kstep * OB_K + 32 * half;
+            const bool fix = (j0 < wrow0 + 32 && j0 + 32 > wrow0) || (j0 + 32 > n32);
+            if (!fix) gen32<DIM, FAM, false>(p, pp, xr2, 0, 0, 0, hw, lw);
+            else gen32<DIM, FAM, true>(p, pp, xr2, j0, grow, n32, hw, lw);
+          }
           if (half == 1) {   // the points stage is read: release it
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&kempty[s]);
@@ -474,7 +511,8 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
 constexpr int RED_COLS = 8;
 __global__ void __launch_bounds__(256)
 kv_otf_reduce(const float* __restrict__ P, Sched sc, int tiles, int segs, int nt, int64_t m, int64_t rows, int sK,
-              const unsigned long long* __restrict__ vmax, double* __restrict__ Y, int64_t ldy) {
+              const float* __restrict__ rowscale, const unsigned long long* __restrict__ vmax, double* __restrict__ Y,
+              int64_t ldy) {
   const int tile = blockIdx.x;
   const int r = threadIdx.x & 127;
   const int64_t i = (int64_t)tile * OB_M + r;
@@ -496,7 +534,10 @@ kv_otf_reduce(const float* __restrict__ P, Sched sc, int tiles, int segs, int nt
     for (int k = 0; k < nseg; ++k) s += (double)Pp[(size_t)k * nt * OB_M];
     const double mx = __longlong_as_double((long long)vmax[c]);
     const int ev = mx > 0.0 ? SCALE_TOP - ilogb(mx) : 0;
-    Y[(int64_t)c * ldy + i] = ldexp(s, -(sK + ev));
+    if (rowscale)
+      Y[(int64_t)c * ldy + i] = ldexp(s, -ev) / (double)rowscale[i];   // exact: powers of two
+    else
+      Y[(int64_t)c * ldy + i] = ldexp(s, -(sK + ev));
   }
 }
 
@@ -549,13 +590,19 @@ template <int NT, int DIM, int FAM>
 void launch_otf(const CUtensorMap& mP, const CUtensorMap& mBh, const CUtensorMap& mBl, OtfParams p, int64_t grid,
                 cudaStream_t st) {
   using Sh = OtfShape<NT>;
+  constexpr size_t AST = DIM == 0 ? 32768u : PTS_STAGE_POINTS;   // A-source stage: K tiles or points
   const size_t extra = 1024 + 8 * 64;   // alignment slack + barriers
   const size_t cap = (size_t)max_smem_optin() - extra;
   int sb = Sh::NABUF;
-  while (sb > 2 && cap < sb * (size_t)Sh::BST + 4 * (size_t)PTS_STAGE) --sb;
+  while (sb > 2 && cap < sb * (size_t)Sh::BST + (DIM == 0 ? 3 : 4) * AST) --sb;
   p.sb = sb;
-  p.sa = (int)std::min<size_t>(12, (cap - sb * (size_t)Sh::BST) / PTS_STAGE);
-  const size_t smem = (size_t)p.sa * PTS_STAGE + (size_t)p.sb * Sh::BST + extra;
+  p.sa = (int)std::min<size_t>(12, (cap - sb * (size_t)Sh::BST) / AST);
+  // the converter warp of step j (j % CP) reads A-ring slot j % SA: with SA a multiple of CP every
+  // slot belongs to one converter warp, so no warp can pass a kfull parity wait a whole ring phase
+  // early (SA = 3 with CP = 2 let one warp read a slot still holding the other warp's step)
+  p.sa = p.sa / Sh::CP * Sh::CP;
+  if (p.sa < Sh::CP) fail(RLD_ERR_NOT_SUPPORTED, "kv_otf: shared memory below one A stage per converter warp");
+  const size_t smem = (size_t)p.sa * AST + (size_t)p.sb * Sh::BST + extra;
   auto kern = kv_otf_kernel<NT, DIM, FAM>;
   static std::atomic<uint64_t> attr{0};
   once_per_device(attr, [&] {
@@ -577,6 +624,30 @@ void launch_otf_nt(int nt, const CUtensorMap& mP, const CUtensorMap& mBh, const 
 
 }  // namespace
 
+// Per-row scales of a tiled fp32 K: rowscale[i] = 2^s, max_j |K_ij| 2^s in [2^13, 2^14) (1 for a zero
+// row).  Thread = row; it reads the row's 32-float segment of every tile.
+__global__ void kv_rowscale_tiled(const float* __restrict__ Kt, int64_t rows, int64_t ks32, float* __restrict__ rs) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  const int64_t t = i / OB_M, r = i % OB_M;
+  float mx = 0.f;
+  for (int64_t k = 0; k < ks32; ++k) {
+    const float4* row = reinterpret_cast<const float4*>(Kt + ((t * ks32 + k) * OB_M + r) * 32);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float4 v = row[c];
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+  }
+  rs[i] = mx > 0.f ? ldexpf(1.f, SCALE_TOP - ilogbf(mx)) : 1.f;
+}
+
+void kv_rowscales(const float* Kt, int64_t rows, int64_t n, float* rs, cudaStream_t st) {
+  if (rows <= 0) return;
+  kv_rowscale_tiled<<<(unsigned)ceil_div(rows, 128), 128, 0, st>>>(Kt, rows, ceil_div(n, 32), rs);
+  RLD_LAUNCH_CHECK();
+}
+
 // The fp16 kernel is the default on-the-fly float32 product; RLD_OTF_KIND=tf32 selects the
 // 3xTF32 kernel of kv_tc.cu (read per call, for A/B measurements).
 bool kv_otf_f16_enabled() {
@@ -589,6 +660,8 @@ int64_t otf_points_floats(int64_t n) { return 8 * ceil_div(n, OB_K) * OB_K; }
 void kv_product_otf16(const KvOperand& op, int64_t m, const double* V, int64_t ldv, double* Y, int64_t ldy,
                       KvWorkspace& ws, cudaStream_t st) {
   const int64_t n = op.n, rows = op.rows;
+  const bool stored = op.K != nullptr;   // tiled fp32 K with per-row scales, else points
+  if (stored && (!op.tiled || !op.rowscale)) fail(RLD_ERR_INVALID_ARGUMENT, "kv_otf: stored K must be tiled and scaled");
   if (n >= (int64_t)1 << 31) fail(RLD_ERR_NOT_SUPPORTED, "kv_otf: n >= 2^31");
   const int ks = (int)ceil_div(n, OB_K);
   const int npass = (int)ceil_div(m, 128);
@@ -635,11 +708,13 @@ void kv_product_otf16(const KvOperand& op, int64_t m, const double* V, int64_t l
   p.wait_mode = getenv("RLD_TC_WAIT") ? atoi(getenv("RLD_TC_WAIT")) : 1;
   p.wait_ns = 256;
   p.pts = op.pts4;
+  p.rowscale = op.rowscale;
+  p.ks32 = (int)ceil_div(n, 32);
   p.n = n;
   p.row0 = op.row0;
   p.rows = rows;
   p.family = op.kp.family;
-  const int sK = SCALE_TOP - ilogb(op.kp.diag);
+  const int sK = (!stored && op.kp.diag > 0.0) ? SCALE_TOP - ilogb(op.kp.diag) : 0;
   p.diag = (float)std::ldexp(op.kp.diag, sK);
   p.la2 = (float)(std::log2(op.kp.a2) + sK);
   {
@@ -657,8 +732,12 @@ void kv_product_otf16(const KvOperand& op, int64_t m, const double* V, int64_t l
   ws.tc_partial.reserve(sizeof(float) * (size_t)npass * tiles * segs * width * OB_M);
   p.partial = ws.tc_partial.as<float>();
   // points: [ceil(n/64) * 2 * 8][32] fp32, one 2 KB box {32, 16} per k-step
-  const CUtensorMap mP = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, op.pts4, 32, (int64_t)ks * 16, 128, 32, 16,
-                                     CU_TENSOR_MAP_SWIZZLE_NONE);
+  // points: [ceil(n/64) * 2 * 8][32] fp32, one 2 KB box {32, 16} per k-step; stored K: the tiled
+  // layout as [tiles * ks32 * 128][32] fp32, one 32 KB box {32, 256} (two tiles) per k-step
+  const CUtensorMap mP = stored ? make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, op.K, 32,
+                                              (int64_t)tiles * p.ks32 * OB_M, 128, 32, 256, CU_TENSOR_MAP_SWIZZLE_128B)
+                                : make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, op.pts4, 32, (int64_t)ks * 16, 128, 32, 16,
+                                              CU_TENSOR_MAP_SWIZZLE_NONE);
   const CUtensorMap mBh = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, ws.bhi.ptr, OB_K, mp * ks, OB_K * 2, OB_K,
                                       width, CU_TENSOR_MAP_SWIZZLE_128B);
   const CUtensorMap mBl = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, ws.blo.ptr, OB_K, mp * ks, OB_K * 2, OB_K,
@@ -672,7 +751,9 @@ void kv_product_otf16(const KvOperand& op, int64_t m, const double* V, int64_t l
     p.prof = prof_buf.as<unsigned long long>();
   }
   const int d = op.kp.d;
-  if (op.kp.family == RLD_RBF) {
+  if (stored) {
+    launch_otf_nt<0, 0>(width, mP, mBh, mBl, p, grid, st);
+  } else if (op.kp.family == RLD_RBF) {
     if (d <= 2) launch_otf_nt<2, RLD_RBF>(width, mP, mBh, mBl, p, grid, st);
     else if (d == 3) launch_otf_nt<3, RLD_RBF>(width, mP, mBh, mBl, p, grid, st);
     else launch_otf_nt<4, RLD_RBF>(width, mP, mBh, mBl, p, grid, st);
@@ -698,7 +779,8 @@ void kv_product_otf16(const KvOperand& op, int64_t m, const double* V, int64_t l
             a[6] / cs, a[8] / cs, a[9] / ds, a[11] / grid / steps, a[12] / grid / steps);
   }
   const dim3 rgrid((unsigned)tiles, (unsigned)ceil_div(m, RED_COLS));
-  kv_otf_reduce<<<rgrid, 256, 0, st>>>(p.partial, sc, tiles, segs, width, m, rows, sK, vmax, Y, ldy);
+  kv_otf_reduce<<<rgrid, 256, 0, st>>>(p.partial, sc, tiles, segs, width, m, rows, sK, stored ? op.rowscale : nullptr,
+                                       vmax, Y, ldy);
   RLD_LAUNCH_CHECK();
 }
 

@@ -746,6 +746,10 @@ void launch_tc(const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap&
   while (sb > 2 && smem_cap < sb * BST + 3 * (size_t)Sh::A_REGION) --sb;
   p.sb = sb;
   p.sa = (int)std::min<size_t>(max_sa, (smem_cap - sb * BST) / Sh::A_REGION);
+  // one A-ring slot per converter warp parity (SA a multiple of CP): a slot shared by two converter
+  // warps lets the one a whole ring phase ahead pass its kfull parity wait on the other's step
+  p.sa = p.sa / Sh::CP * Sh::CP;
+  if (p.sa < Sh::CP) fail(RLD_ERR_NOT_SUPPORTED, "kv_tc: shared memory below one A stage per converter warp");
   p.tmem_cols = Sh::TMEM_COLS;
   const size_t smem = (size_t)p.sa * Sh::A_REGION + (size_t)p.sb * BST + extra;
   auto kern = kv_tc_kernel<MODE, NT, OTF, DIM, FAM, CG2>;
@@ -907,6 +911,12 @@ bool kv_tc_b_layout(const KvOperand& op, int64_t m, KvWorkspace& ws, TcBLayout& 
 void kv_product_tc(const KvOperand& op, int mode, int64_t m, const double* V, int64_t ldv, double* Y, int64_t ldy,
                    KvWorkspace& ws, cudaStream_t st, bool presplit) {
   if (op.K == nullptr && !presplit && kv_otf_f16_enabled()) {
+    kv_product_otf16(op, m, V, ldv, Y, ldy, ws, st);
+    return;
+  }
+  // wide products of a stored (tiled) fp32 K: tensor-bound, so the fp16 head / tail kernel at twice
+  // the tf32 rate; the HBM-bound Lanczos block (m <= 64) stays on 3xTF32
+  if (op.K && op.tiled && op.rowscale && m > 64 && mode == 3 && !presplit && kv_otf_f16_enabled()) {
     kv_product_otf16(op, m, V, ldv, Y, ldy, ws, st);
     return;
   }

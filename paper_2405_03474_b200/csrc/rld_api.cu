@@ -97,6 +97,7 @@ struct Resident {
   bool kq_ready = false;
   DevBuf Kr;                 // residues of K' modulo the CRT moduli (kv_crt.cu), for the wide products
   bool kr_ready = false;
+  DevBuf rowscale;           // tiled fp32 K: per-row power-of-two scales (fp16 wide products, kv_otf.cu)
   KernelParams kp{};
 
   KvOperand op() const {
@@ -104,6 +105,7 @@ struct Resident {
     o.K = (path == RLD_PATH_ON_THE_FLY) ? nullptr : K;
     o.ldk = ldk;
     o.tiled = tiled;
+    o.rowscale = (tiled && path != RLD_PATH_ON_THE_FLY) ? rowscale.as<float>() : nullptr;
     o.X = X.as<double>();
     o.pts4 = (source == RLD_SOURCE_POINTS && d <= 4) ? pts4.as<float>() : nullptr;
     o.kp = kp;
@@ -382,6 +384,10 @@ void prepare(rld_handle* h, const rld_problem* p) {
     ozaki_slice(static_cast<const double*>(r.K), r.ldk, r.rows, r.n, 128, r.Kq.as<int8_t>(), r.ksigma.as<double>(),
                 st);
     r.kq_ready = true;
+  }
+  if (r.tiled && r.K && r.rows > 0) {
+    r.rowscale.reserve(sizeof(float) * r.rows);
+    kv_rowscales(static_cast<const float*>(r.K), r.rows, r.n, r.rowscale.as<float>(), st);
   }
   if (r.kq_ready && !r.kr_ready && crt_supported(r.n)) {
     // the CRT residue image for the wide (sketch) products, where it fits beside the slices

@@ -108,6 +108,7 @@ struct KvOperand {
   int tc_mode = 3;           // tensor-core product: 3 = 3xTF32 (Lanczos), 1 = 1xTF32 (sketch)
   int oz_diags = 8;          // float64 int8-slice product: slice-pair diagonals kept (8 = all 36 pairs)
   const int8_t* kr = nullptr;      // K' residues modulo the CRT moduli (kv_crt.cu), or null
+  const float* rowscale = nullptr; // tiled fp32 K: per-row power-of-two scales (kv_otf.cu stored products)
 };
 
 struct KvWorkspace {
@@ -127,6 +128,8 @@ bool kv_tc_supported(const KvOperand& op);
 // selects the 3xTF32 kernel).  Points in op.pts4 padded to otf_points_floats(n) floats.
 bool kv_otf_f16_enabled();
 int64_t otf_points_floats(int64_t n);
+// per-row scales of a tiled fp32 K for the fp16 stored products (wide products, m > 64)
+void kv_rowscales(const float* Kt, int64_t rows, int64_t n, float* rs, cudaStream_t st);
 void kv_product_otf16(const KvOperand& op, int64_t m, const double* V, int64_t ldv, double* Y, int64_t ldy,
                       KvWorkspace& ws, cudaStream_t st);
 // presplit: the B operand (tf32 hi / lo of V in the k-step blocked layout) was already written

@@ -125,3 +125,23 @@ def test_otf16_estimate_agrees_with_3xtf32(rld, index, monkeypatch):
                         probe_kind=cfg.probe_kind, k=cfg.precond.rank, q=cfg.precond.num_iters,
                         seed=cfg.seed)
     assert rel(a.value, ref.value) <= 1e-4, (a.value, ref.value)
+
+
+@pytest.mark.parametrize("n,m", [(4099, 70), (16384, 266), (19968, 128), (24960, 300), (39936, 522)])
+def test_stored_f16_wide_product(rld, n, m):
+    """Wide products (m > 64) of a stored fp32 K run on the same fp16 head / tail kernel with the K
+    tiles streamed from HBM and per-row power-of-two scales.  The shapes include whole-wave rounds
+    plus stream-K tails; (19968, 128) and (39936, 522) hung before the A-ring depth was made a
+    multiple of the converter warps (a ring slot shared by two warps).  Sampled rows against the
+    float64 product with the stored (float32-rounded) K."""
+    import torch
+
+    g = np.random.default_rng(n + m)
+    pts = g.standard_normal((n, 4))
+    spec = rld.KernelSpec("rbf", 1.0, 1.5, 1e-3)
+    R = rld.ResidentMatrix(rld.KernelMatrix(spec, pts), dtype="fp32", path="stored")
+    V = g.standard_normal((m, n)) * np.exp(g.uniform(-10, 10, (m, 1)))
+    Y = R.kv_apply(torch.from_numpy(V).cuda()).cpu().numpy()
+    for i in g.choice(n, 12, replace=False):
+        k = O.covariance_block("rbf", 1.0, 1.5, 1e-3, pts, rows=slice(i, i + 1))[0].astype(np.float32).astype(np.float64)
+        assert np.max(np.abs(Y[:, i] - V @ k) / (np.abs(V) @ np.abs(k))) <= 2e-6
