@@ -55,8 +55,10 @@ constexpr int SCALE_TOP = 13;      // scaled magnitudes in [2^13, 2^14)
 struct OtfParams {
   Sched sched;
   int mp;               // B rows per k-step block (vectors padded to npass x NT)
-  unsigned int* sync;   // phase-1 epoch barrier counters (per pass)
+  unsigned int* sync;   // phase-1 epoch barrier counters (per pass, or one for all passes)
   int sync_k;
+  int sync_all;         // stored K, several passes: one counter, so the passes' CTAs that stream the same
+                        // K tiles stay within an L2-sized window and K comes from HBM once
   int ks, tiles, npass, segs;
   int sa, sb;
   float* partial;       // [npass][tiles][segs][NT][128], scaled units
@@ -272,9 +274,9 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
           ++epoch;
           const unsigned long long e0 = prof ? clock64() : 0;
           if (lane == 0) {
-            unsigned int* ctr = p.sync + pass;
+            unsigned int* ctr = p.sync + (p.sync_all ? 0 : pass);
             atomicAdd(ctr, 1u);
-            const unsigned int target = (unsigned int)(epoch * p.sched.G);
+            const unsigned int target = (unsigned int)(epoch * p.sched.G * (p.sync_all ? p.npass : 1));
             while (*(volatile unsigned int*)ctr < target) __nanosleep(100);
             if (prof) pb[1] += clock64() - e0;
           }
@@ -593,8 +595,13 @@ void launch_otf(const CUtensorMap& mP, const CUtensorMap& mBh, const CUtensorMap
   constexpr size_t AST = DIM == 0 ? 32768u : PTS_STAGE_POINTS;   // A-source stage: K tiles or points
   const size_t extra = 1024 + 8 * 64;   // alignment slack + barriers
   const size_t cap = (size_t)max_smem_optin() - extra;
+  // stored K: 4 A stages (32 KB each) to cover HBM latency where the B stages are small enough (NT <= 96:
+  // config-2 sketch 3.0 -> 2.4 ms); at NT = 128 the fourth TMEM A buffer is worth more (4 B + 2 A
+  // stages: config-3 sketch 14 ms, 3 B + 4 A: 18 ms)
   int sb = Sh::NABUF;
-  while (sb > 2 && cap < sb * (size_t)Sh::BST + (DIM == 0 ? 3 : 4) * AST) --sb;
+  const int min_sb = (DIM == 0 && NT <= 96) ? Sh::CP + 1 : 2;
+  const size_t a_need = (DIM == 0 && NT > 96) ? 2 : 4;
+  while (sb > min_sb && cap < sb * (size_t)Sh::BST + a_need * AST) --sb;
   p.sb = sb;
   p.sa = (int)std::min<size_t>(12, (cap - sb * (size_t)Sh::BST) / AST);
   // the converter warp of step j (j % CP) reads A-ring slot j % SA: with SA a multiple of CP every
@@ -618,6 +625,12 @@ void launch_otf_nt(int nt, const CUtensorMap& mP, const CUtensorMap& mBh, const 
   switch (nt) {
     case 32: launch_otf<32, DIM, FAM>(mP, mBh, mBl, p, grid, st); break;
     case 64: launch_otf<64, DIM, FAM>(mP, mBh, mBl, p, grid, st); break;
+    case 96:
+      if constexpr (DIM == 0) {   // stored K only: tensor-bound, so less padding pays (config 2: 3 x 96 for 266)
+        launch_otf<96, DIM, FAM>(mP, mBh, mBl, p, grid, st);
+        break;
+      }
+      [[fallthrough]];
     default: launch_otf<128, DIM, FAM>(mP, mBh, mBl, p, grid, st); break;
   }
 }
@@ -666,7 +679,7 @@ void kv_product_otf16(const KvOperand& op, int64_t m, const double* V, int64_t l
   const int ks = (int)ceil_div(n, OB_K);
   const int npass = (int)ceil_div(m, 128);
   int width = (int)(ceil_div(ceil_div(m, npass), 32) * 32);
-  if (width == 96) width = 128;
+  if (width == 96 && !stored) width = 128;   // on the fly: generation-bound, passes of 96 gain nothing
   const int64_t mp = (int64_t)npass * width;
   // per-vector scales, then the fp16 head / tail operand
   ws.otf_vmax.reserve(sizeof(unsigned long long) * mp);
@@ -725,6 +738,11 @@ void kv_product_otf16(const KvOperand& op, int64_t m, const double* V, int64_t l
       return v > 0 ? (1 << pw) : 0;
     }();
     p.sync_k = (sc.R > 1 || (sc.R == 1 && sc.tail_total > 0)) && g_live_handles.load() <= 1 ? sync_k : 0;
+    // stored K in several passes: every pass streams all of K; keep the passes together (64 k-steps
+    // = 2 MB of K per CTA per epoch, ~60 MB across the wave: inside L2)
+    static const int sync_multi = getenv("RLD_OTF_SYNC_MULTI") ? atoi(getenv("RLD_OTF_SYNC_MULTI")) : 64;
+    p.sync_all = (stored && npass > 1 && p.sync_k > 0 && sync_multi > 0) ? 1 : 0;
+    if (p.sync_all) p.sync_k = sync_multi;
     ws.tc_sync.reserve(sizeof(unsigned int) * npass);
     p.sync = ws.tc_sync.as<unsigned int>();
     if (p.sync_k > 0) RLD_CUDA(cudaMemsetAsync(p.sync, 0, sizeof(unsigned int) * npass, st));
