@@ -374,7 +374,10 @@ def run_ours(args):
     # any kernel (6 of the 26 products); their roofline is the headline one, the Lanczos product's
     # (HBM) is kept beside it
     roofline_lanczos = None
-    if cfg.dtype == "fp64" and wl.path == "stored" and os.environ.get("RLD_FP64_SKETCH") != "slices":
+    stats = (C.c_int64 * 4)()
+    if cfg.dtype == "fp64" and wl.path == "stored" and R.sess.lib.rld_slice_stats(R.sess.handle.ptr, stats) == 0 \
+            and stats[0] > 0:
+        blocks, slices, pairs, crt = (int(x) for x in stats)
         Vw = torch.randn(w, n, dtype=torch.float64, device="cuda")
         for _ in range(2):
             R.kv_apply(Vw)
@@ -384,8 +387,10 @@ def run_ours(args):
             R.kv_apply(Vw)
         k1.record(stream)
         torch.cuda.synchronize()
-        roofline_lanczos = roofline
-        roofline = roofline_crt(rows, n, w, k0.elapsed_time(k1) / 5)
+        w_ms = k0.elapsed_time(k1) / 5
+        roofline_lanczos = roofline_slices(rows, n, s, kv_ms, blocks, slices, pairs, "Lanczos block m=s")
+        roofline = roofline_crt(rows, n, w, w_ms) if crt else roofline_slices(rows, n, w, w_ms, blocks, slices, pairs,
+                                                                             "sketch block m=w")
         del Vw
 
     # ---- end to end through the public API (host buffers, pinned)
@@ -611,6 +616,36 @@ def extra_fp32(args, rld, world, sharded, per_step):
     del R
     torch.cuda.empty_cache()
     return out
+
+
+def roofline_slices(rows, n, m, ms, blocks, slices, pairs, what):
+    """The float64 product on exact int8 slices (csrc/kv_ozaki.cu) with its all-zero leading slices
+    skipped (points in Morton order): algorithmic bytes = the K slices actually read (rld_slice_stats)
+    plus V in and Y out; int8 work = the slice pairs multiplied, each a 128 x 64 x 32 MMA per block
+    and 64-vector pass.  Both fractions are reported; the bound is the larger."""
+    pipe = load_pipe_peaks()
+    hbm_peak, _, peak_kind = load_peaks()
+    passes = -(-m // 64)
+    alg_bytes = 4096 * slices + 8 * n * m + 8 * rows * m
+    ops = 2.0 * 128 * 64 * 32 * pairs * passes
+    rec = pipe.get("i8_ss_n256_random_sustained", {})
+    i8_peak = rec.get("tops", pipe.get("i8_ss_n256", {}).get("tops", 4576.0))
+    t = ms * 1e-3
+    f_hbm, f_t = alg_bytes / t / 1e9 / hbm_peak, ops / t / 1e12 / i8_peak
+    key = f"kv_product|fp64-int8slices|stored|n={n}|rows={rows}|m={m}"
+    traffic, traffic_src = ncu_traffic(key)
+    common = {"traffic": traffic, "traffic_source": traffic_src, "traffic_key": key, "kernel_ms": ms,
+              "kernel": f"kv_product (tcgen05 kind::i8 on exact int8 slices of float64 K, {what}={m}, {rows} rows; "
+                        f"{slices / blocks:.2f} of 8 slices and {pairs / blocks:.1f} of 36 pairs per block after "
+                        f"skipping all-zero leading slices)",
+              "alg_bytes": alg_bytes, "int8_ops": ops, "hbm_frac": f_hbm, "int8_tensor_frac": f_t,
+              "equiv_fp64_tflops": 2.0 * rows * n * m / t / 1e12,
+              "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}); int8: profiles/r02c_pipe_peaks.json "
+                             f"i8_ss_n256_random_sustained (measured)"}
+    if f_t >= f_hbm:
+        return {"bound": "tensor", "achieved": ops / t / 1e12, "peak": i8_peak, "unit": "TOPS (int8)", "frac": f_t,
+                **common}
+    return {"bound": "hbm", "achieved": alg_bytes / t / 1e9, "peak": hbm_peak, "unit": "GB/s", "frac": f_hbm, **common}
 
 
 def roofline_crt(rows, n, w, ms):

@@ -43,7 +43,7 @@ EXPORTS = (
     "rld_abi_version", "rld_create", "rld_destroy", "rld_last_error", "rld_logdet", "rld_prepare",
     "rld_logdet_resident", "rld_build_covariance", "rld_kv_apply", "rld_rademacher", "rld_exact_logdet", "rld_dense_cholesky", "rld_dense_eigh",
     "rld_nccl_unique_id", "rld_stream", "rld_normal", "rld_chi_radii", "rld_vgroup_create", "rld_vgroup_destroy",
-    "rld_precond_build", "rld_precond_apply",
+    "rld_precond_build", "rld_precond_apply", "rld_slice_stats",
 )
 SOLVE_SQRT, SOLVE_SQRT_T, SOLVE = 0, 1, 2
 
@@ -118,6 +118,7 @@ def load() -> C.CDLL:
         lib.rld_rademacher.argtypes = [H, C.POINTER(C.c_uint64 * 2), C.c_int64, C.c_int64, C.c_void_p]
         lib.rld_normal.argtypes = [H, C.POINTER(C.c_uint64 * 2), C.c_int64, C.c_int64, C.c_void_p]
         lib.rld_exact_logdet.argtypes = [H, C.POINTER(C.c_double)]
+        lib.rld_slice_stats.argtypes = [H, C.POINTER(C.c_int64)]
         lib.rld_dense_cholesky.argtypes = [H, C.c_int32, C.c_void_p, C.POINTER(C.c_int32)]
         lib.rld_dense_eigh.argtypes = [H, C.c_int32, C.c_void_p, C.c_void_p]
         lib.rld_chi_radii.argtypes = [C.POINTER(C.c_uint64 * 2), C.c_uint64, C.c_int64, C.c_int64, C.c_void_p]

@@ -177,7 +177,7 @@ __global__ void ozaki_digits_kernel(const double* __restrict__ A, int64_t lda, i
 template <bool CRT, int EL, int DMAX>
 __global__ void __launch_bounds__(256)
 ozaki_points_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, int64_t row0,
-                    int64_t rows, int64_t KS, int8_t* __restrict__ q, int8_t* __restrict__ Kr) {
+                    int64_t rows, int64_t KS, int8_t* __restrict__ q, int8_t* __restrict__ Kr, int* __restrict__ knz) {
   constexpr int TR = OZ_BM;
   constexpr int PARTS = OZ_BK / EL;          // threads per (row, k-step)
   constexpr int W = EL / 4;                  // 32-bit words per slice
@@ -200,6 +200,7 @@ ozaki_points_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, in
     for (int k = 0; k < DMAX; ++k) xi[k] = (k < d && row < rows) ? X[gi * d + k] : 0.0;
     uint32_t w[OZ_S][W];
     long long kq[EL];   // CRT: K' of the EL entries
+    int nz = 0;         // slices from the first nonzero digit of any of the EL entries: 8 - leading zero slices
 #pragma unroll
     for (int k = 0; k < EL; ++k) {
       const int64_t j = j0 + k;
@@ -227,11 +228,17 @@ ozaki_points_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, in
         const double dg = rint(x);
         r = x - dg;
         if (CRT && s < CRT_SLICES) kd = fma(kd, 128.0, dg);
+        if (dg != 0.0 && nz < OZ_S - s) nz = OZ_S - s;
         const uint32_t b = (uint32_t)(uint8_t)(int8_t)(int)dg;
         if ((k & 3) == 0) w[s][k >> 2] = b;
         else w[s][k >> 2] |= b << (8 * (k & 3));
       }
       if (CRT) kq[k] = __double2ll_rn(kd);
+    }
+    // a warp holds 8 rows x 4 column parts of one (tile, k-step) block: reduce, one atomic per warp
+    if (knz) {
+      const int wnz = (int)__reduce_max_sync(0xffffffffu, (unsigned)nz);
+      if ((threadIdx.x & 31) == 0 && wnz > 0) atomicMax(knz + t * KS + ks, wnz);
     }
     const uint32_t o = (uint32_t)(i * OZ_BK + EL * h);
     const uint32_t phys = o ^ (((o >> 7) & 1u) << 4);
@@ -303,7 +310,8 @@ __global__ void oz_split_reduce_kernel(const double* __restrict__ part, int spli
 __global__ void __launch_bounds__(OZ_THREADS, 1)
 ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, int64_t KS,
                 const double* __restrict__ sigma, const double* __restrict__ tau, int64_t rows, int64_t m, int64_t n,
-                int64_t kchunk, double* __restrict__ out, int64_t ldo, int64_t split_stride, int nd) {
+                int64_t kchunk, double* __restrict__ out, int64_t ldo, int64_t split_stride, int nd,
+                const int* __restrict__ knz) {
   extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -332,19 +340,44 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  if (knz) {
+    // blocks skip their leading all-zero K slices, so a diagonal's first MMA can come at any k-step:
+    // the accumulators start from zero and every MMA accumulates
+    if (warp >= 4) {
+      const uint32_t lb = (uint32_t)((warp & 3) * 32) << 16;
+      uint32_t z[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) z[e] = 0u;
+#pragma unroll 1
+      for (int c = 0; c < (int)OZ_TMEM_COLS; c += 32) ptx::tmem_st_32x32b_x32(tmem + lb + (uint32_t)c, z);
+      ptx::tmem_wait_st();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+  }
+  // leading all-zero K slices of the k-th block of this CTA's range (0 without the metadata)
+  const int* kb_nz = knz ? knz + (int64_t)blockIdx.y * KS + kbeg / OZ_BK : nullptr;
+  auto lead = [&](int s) { return kb_nz ? OZ_S - kb_nz[s] : 0; };
 
   if (warp == 0) {   // ---- producer: one bulk copy of the A image and one of the B image per k-step
     if (ptx::elect_one()) {
       const int8_t* ga = Aq + ((int64_t)blockIdx.y * KS + kbeg / OZ_BK) * OZ_A_BYTES;
       const int8_t* gb = Bq + ((int64_t)blockIdx.x * KS + kbeg / OZ_BK) * (OZ_STAGE - OZ_A_BYTES);
-      // only the first nd slices of each operand take part (a contiguous prefix of the k-step image)
-      const uint32_t abytes = (uint32_t)nd * OZ_A_SLICE, bbytes = (uint32_t)nd * OZ_B_SLICE;
+      // K slices lz .. nd-1 (lz leading all-zero slices skipped) and V slices 0 .. nd-1-lz take part:
+      // contiguous ranges of the k-step image
       for (int s = 0; s < steps; ++s) {
         const int st = s % OZ_STAGES;
+        const int lz = lead(s);
         if (s >= OZ_STAGES) ptx::mbar_wait(&empty[st], ((s / OZ_STAGES) - 1) & 1);
         unsigned char* dst = smem + st * OZ_STAGE;
+        if (lz >= nd) {
+          ptx::mbar_arrive(&full[st]);
+          continue;
+        }
+        const uint32_t abytes = (uint32_t)(nd - lz) * OZ_A_SLICE, bbytes = (uint32_t)(nd - lz) * OZ_B_SLICE;
         ptx::mbar_arrive_expect_tx(&full[st], abytes + bbytes);
-        bulk_load(dst, ga + (int64_t)s * OZ_A_BYTES, abytes, &full[st]);
+        bulk_load(dst + lz * OZ_A_SLICE, ga + (int64_t)s * OZ_A_BYTES + lz * OZ_A_SLICE, abytes, &full[st]);
         bulk_load(dst + OZ_A_BYTES, gb + (int64_t)s * (OZ_STAGE - OZ_A_BYTES), bbytes, &full[st]);
       }
     }
@@ -357,6 +390,7 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
         ptx::tc_fence_after();
         const uint32_t a0 = sbase + st * OZ_STAGE;
         const uint32_t b0 = a0 + OZ_A_BYTES;
+        const int lz = lead(s);
         // A slice sa against the stacked B slices 0 .. 7 - sa at once: the accumulators of the
         // diagonals d = sa + t are adjacent TMEM column blocks, so one N = 64 (8 - sa) product
         // (in N <= 256 pieces) covers the whole row of pairs -- 12 MMAs per k-step instead of 36
@@ -364,8 +398,9 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
 #pragma unroll
         for (int sa = 0; sa < OZ_S; ++sa) {
           if (sa >= nd) break;
+          if (sa < lz) continue;
           const uint64_t adesc = desc_sw32(a0 + sa * OZ_A_SLICE);
-          const uint32_t acc = (s > 0 || sa > 0) ? 1u : 0u;
+          const uint32_t acc = (kb_nz || s > 0 || sa > 0) ? 1u : 0u;
 #pragma unroll
           for (int t0 = 0; t0 < OZ_DIAG - sa; t0 += 4) {
             if (t0 >= nd - sa) break;
@@ -460,7 +495,7 @@ void ozaki_slice(const double* A, int64_t lda, int64_t rows, int64_t n, int tile
 }
 
 void ozaki_slice_points(const double* X, int64_t n, const KernelParams& kp, int64_t row0, int64_t rows, int8_t* q,
-                        double* scale, cudaStream_t st, int8_t* Kr) {
+                        double* scale, cudaStream_t st, int8_t* Kr, int* knz) {
   if (rows <= 0) return;
   if (kp.d > RLD_MAX_DIM) fail(RLD_ERR_NOT_SUPPORTED, "ozaki_slice_points: d > 32");
   int ee = 0;
@@ -470,21 +505,23 @@ void ozaki_slice_points(const double* X, int64_t n, const KernelParams& kp, int6
   const int64_t KS = ceil_div(n, OZ_BK);
   const int64_t total = ceil_div(rows, OZ_BM) * OZ_BM * KS * 4;
   const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)oz_sms() * 16);
+  if (knz) RLD_CUDA(cudaMemsetAsync(knz, 0, sizeof(int) * ceil_div(rows, OZ_BM) * KS, st));
   if (Kr && kp.d <= 4)
-    ozaki_points_kernel<true, 8, 4><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, Kr);
+    ozaki_points_kernel<true, 8, 4><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, Kr, knz);
   else if (Kr)
-    ozaki_points_kernel<true, 8, RLD_MAX_DIM><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, Kr);
+    ozaki_points_kernel<true, 8, RLD_MAX_DIM><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, Kr, knz);
   else if (kp.d <= 4)
-    ozaki_points_kernel<false, 8, 4><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, nullptr);
+    ozaki_points_kernel<false, 8, 4><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, nullptr, knz);
   else
-    ozaki_points_kernel<false, 8, RLD_MAX_DIM><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, nullptr);
+    ozaki_points_kernel<false, 8, RLD_MAX_DIM><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, nullptr, knz);
   RLD_LAUNCH_CHECK();
 }
 
 // Y (m x rows, ld ldy) = V K^T with K given by its sliced image Kq (ozaki_slice, 128-row tiles) and
 // row scales; V (m x n float64 rows, ld ldv) is sliced here (64-vector tiles) into ws.oz_vq.
 void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int64_t n, const double* V, int64_t ldv,
-                      int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st, int diags) {
+                      int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st, int diags,
+                      const int* knz) {
   if (m <= 0 || rows <= 0) return;
   if (diags < 1 || diags > OZ_DIAG) fail(RLD_ERR_INVALID_ARGUMENT, "kv_product_ozaki: diagonals must be 1..8");
   ws.oz_vq.reserve((size_t)ozaki_bytes(m, n, OZ_BN));
@@ -520,14 +557,14 @@ void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int6
   const int8_t* Bq = ws.oz_vq.as<int8_t>();
   if (splits == 1) {
     ozaki_kv_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(Kq, Bq, KS, ksigma, ws.oz_tau.as<double>(), rows, m, n, kchunk,
-                                                      Y, ldy, 0, diags);
+                                                      Y, ldy, 0, diags, knz);
     RLD_LAUNCH_CHECK();
     return;
   }
   const int64_t stride = m * rows;
   ws.partial.reserve(sizeof(double) * stride * splits);
   ozaki_kv_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(Kq, Bq, KS, ksigma, ws.oz_tau.as<double>(), rows, m, n, kchunk,
-                                                    ws.partial.as<double>(), rows, stride, diags);
+                                                    ws.partial.as<double>(), rows, stride, diags, knz);
   RLD_LAUNCH_CHECK();
   const int blocks = (int)std::min<int64_t>(ceil_div(stride, 256), slots * 8);
   oz_split_reduce_kernel<<<blocks, 256, 0, st>>>(ws.partial.as<double>(), (int)splits, stride, m, rows, Y, ldy);

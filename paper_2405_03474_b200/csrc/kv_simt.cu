@@ -250,7 +250,7 @@ void kv_product(const KvOperand& op, int64_t m, const double* V, int64_t ldv, do
       return;
     }
     if (!simt && op.kq) {   // exact int8 slices of K on the INT8 tensor cores (kv_ozaki.cu)
-      kv_product_ozaki(op.kq, op.ksigma, op.rows, op.n, V, ldv, m, Y, ldy, ws, st, op.oz_diags);
+      kv_product_ozaki(op.kq, op.ksigma, op.rows, op.n, V, ldv, m, Y, ldy, ws, st, op.oz_diags, op.knz);
       return;
     }
     if (!otf && !simt && gemm_nt_f64_ok(K, op.ldk, K, op.ldk)) {

@@ -14,6 +14,8 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <algorithm>
+#include <vector>
 
 #include <nvtx3/nvToolsExt.h>
 
@@ -95,6 +97,10 @@ struct Resident {
   DevBuf diag;               // local diagonal of K (float64)
   DevBuf Kq, ksigma;         // float64 K as exact int8 slices (RLD_FP64_PRODUCT=ozaki, kv_ozaki.cu)
   bool kq_ready = false;
+  DevBuf perm;               // points held in Morton (Z-curve) order: perm[i] = original index of point i
+  bool permuted = false;     // (single GPU, float64 stored products: far-field slice blocks are all-zero)
+  DevBuf knz;                // per slice-image block: slices from the first nonzero one (skipped leading zeros)
+  bool knz_ready = false;
   DevBuf Kr;                 // residues of K' modulo the CRT moduli (kv_crt.cu), for the wide products
   bool kr_ready = false;
   DevBuf rowscale;           // tiled fp32 K: per-row power-of-two scales (fp16 wide products, kv_otf.cu)
@@ -113,6 +119,7 @@ struct Resident {
     if (kq_ready && path != RLD_PATH_ON_THE_FLY) {
       o.kq = Kq.as<int8_t>();
       o.ksigma = ksigma.as<double>();
+      if (knz_ready) o.knz = knz.as<int>();
       if (kr_ready) o.kr = Kr.as<int8_t>();
     }
     o.n = n;
@@ -125,6 +132,7 @@ struct Resident {
 struct Work {
   DevBuf Y, Z, A, G, gdiag, theta, Vtop, theta_top, C, inner, lam, hgg, base, sqrt_base;
   DevBuf omega, probes;
+  DevBuf ptmp, ptmp2;  // n-vector blocks moved into / out of the resident (Morton) order
   DevBuf x, p, pp, u, w, KX, T, Tg;
   DevBuf scal;     // small scalars / per-probe arrays
   DevBuf ints;     // flags, info, live, size, kept
@@ -216,6 +224,43 @@ void allreduce_flags(rld_handle* h, int* hflags, int count) {
 }
 
 // ----------------------------------------------------------------------------
+// Morton (Z-curve) order of n points in d <= 3 dimensions: 63 / d bits per coordinate over the
+// bounding box, stable in the original index
+std::vector<int> morton_order(const double* X, int64_t n, int d) {
+  const int b = 63 / d;
+  std::vector<double> lo(d, INFINITY), hi(d, -INFINITY);
+  for (int64_t i = 0; i < n; ++i)
+    for (int c = 0; c < d; ++c) {
+      lo[c] = std::min(lo[c], X[i * d + c]);
+      hi[c] = std::max(hi[c], X[i * d + c]);
+    }
+  std::vector<uint64_t> code((size_t)n);
+  const double top = std::ldexp(1.0, b) - 1.0;
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t k = 0;
+    for (int c = 0; c < d; ++c) {
+      const double span = hi[c] - lo[c];
+      const double f = span > 0 ? (X[i * d + c] - lo[c]) / span : 0.0;
+      const uint64_t q = (uint64_t)std::min(top, std::max(0.0, std::floor(f * top)));
+      for (int bit = 0; bit < b; ++bit) k |= ((q >> bit) & 1ull) << (bit * d + c);
+    }
+    code[(size_t)i] = k;
+  }
+  std::vector<int> pm((size_t)n);
+  for (int64_t i = 0; i < n; ++i) pm[(size_t)i] = (int)i;
+  std::stable_sort(pm.begin(), pm.end(), [&](int a, int c) { return code[(size_t)a] < code[(size_t)c]; });
+  return pm;
+}
+
+// Locality order for the points: the float64 stored product on int8 slices (the only one that skips
+// all-zero blocks), one GPU, d <= 3; RLD_SORT=0 keeps the given order.
+bool sort_points(const rld_handle* h, const rld_problem* p) {
+  const char* e = getenv("RLD_SORT");
+  if (e && e[0] == '0') return false;
+  return p->source == RLD_SOURCE_POINTS && p->path == RLD_PATH_STORED && p->dtype == RLD_FP64 &&
+         fp64_product_ozaki() && h->world == 1 && p->d >= 1 && p->d <= 3 && p->n < (int64_t)1 << 31;
+}
+
 void prepare(rld_handle* h, const rld_problem* p) {
   NvtxRange nv("rld:prepare (K rows / points to HBM)");
   if (!p) fail(RLD_ERR_INVALID_ARGUMENT, "problem is NULL");
@@ -227,6 +272,8 @@ void prepare(rld_handle* h, const rld_problem* p) {
   r.tiled = false;
   r.kq_ready = false;
   r.kr_ready = false;
+  r.knz_ready = false;
+  r.permuted = false;
   h->precond_k = -1;
   r.source = p->source;
   r.dtype = p->dtype;
@@ -257,8 +304,27 @@ void prepare(rld_handle* h, const rld_problem* p) {
     r.kp.diag = r.kp.a2 + p->jitter;
     const size_t xb = sizeof(double) * p->n * p->d;
     r.X.reserve(xb);
-    RLD_CUDA(cudaMemcpyAsync(r.X.ptr, p->data, xb,
-                             p->data_memory == RLD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    if (sort_points(h, p)) {
+      // float64 stored products on int8 slices: points in Morton order make the K blocks away from
+      // the diagonal small, and their leading slices all zero, which the product skips (kv_ozaki.cu).
+      // Every n-vector entering or leaving the resident frame is permuted (probes, sketch rows, the
+      // rank-one start, kv_apply / precond_apply operands); pivot ties go to the original index.
+      std::vector<double> hx((size_t)p->n * p->d), hxp((size_t)p->n * p->d);
+      RLD_CUDA(cudaMemcpyAsync(hx.data(), p->data, xb,
+                               p->data_memory == RLD_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost, st));
+      RLD_CUDA(cudaStreamSynchronize(st));
+      std::vector<int> pm = morton_order(hx.data(), p->n, p->d);
+      for (int64_t i = 0; i < p->n; ++i)
+        for (int c = 0; c < p->d; ++c) hxp[(size_t)i * p->d + c] = hx[(size_t)pm[i] * p->d + c];
+      r.perm.reserve(sizeof(int) * p->n);
+      RLD_CUDA(cudaMemcpyAsync(r.perm.ptr, pm.data(), sizeof(int) * p->n, cudaMemcpyHostToDevice, st));
+      RLD_CUDA(cudaMemcpyAsync(r.X.ptr, hxp.data(), xb, cudaMemcpyHostToDevice, st));
+      RLD_CUDA(cudaStreamSynchronize(st));   // host buffers go out of scope
+      r.permuted = true;
+    } else {
+      RLD_CUDA(cudaMemcpyAsync(r.X.ptr, p->data, xb,
+                               p->data_memory == RLD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    }
     r.diag.reserve(sizeof(double) * std::max<int64_t>(1, r.rows));
     fill_doubles(r.rows, r.kp.diag, r.diag.as<double>(), st);
     if (p->d <= 4) {
@@ -278,7 +344,8 @@ void prepare(rld_handle* h, const rld_problem* p) {
           r.ksigma.reserve(sizeof(double) * r.rows);
           // the CRT residue image for the wide (sketch) products in the same pass, where it fits
           int8_t* kr = nullptr;
-          if (crt_supported(p->n)) {
+          if (crt_supported(p->n) && !r.permuted) {   // Morton-ordered points: the slices skip their
+                                                      // all-zero blocks and beat the CRT product
             const int64_t bytes = crt_bytes(r.rows, p->n);
             size_t fr = 0, tot = 0;
             RLD_CUDA(cudaStreamSynchronize(st));
@@ -288,9 +355,11 @@ void prepare(rld_handle* h, const rld_problem* p) {
               kr = r.Kr.as<int8_t>();
             }
           }
+          r.knz.reserve(sizeof(int) * ceil_div(r.rows, 128) * ceil_div(p->n, 32));
           ozaki_slice_points(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.Kq.as<int8_t>(), r.ksigma.as<double>(),
-                             st, kr);
+                             st, kr, r.knz.as<int>());
           r.kr_ready = kr != nullptr;
+          r.knz_ready = true;
         }
         r.kq_ready = r.rows > 0;
       } else if (p->dtype == RLD_FP64) {
@@ -389,7 +458,7 @@ void prepare(rld_handle* h, const rld_problem* p) {
     r.rowscale.reserve(sizeof(float) * r.rows);
     kv_rowscales(static_cast<const float*>(r.K), r.rows, r.n, r.rowscale.as<float>(), st);
   }
-  if (r.kq_ready && !r.kr_ready && crt_supported(r.n)) {
+  if (r.kq_ready && !r.kr_ready && !r.permuted && crt_supported(r.n)) {
     // the CRT residue image for the wide (sketch) products, where it fits beside the slices
     const int64_t bytes = crt_bytes(r.rows, r.n);
     size_t fr = 0, tot = 0;
@@ -436,6 +505,17 @@ void gather_rows(rld_handle* h, const double* local, int64_t m, double* full) {
                                cudaMemcpyDeviceToDevice, h->st));
   h->comm->allgather(snd, rcv, m * L, h->st);
   relayout_gathered(rcv, h->world, m, L, r.n, full, h->st);
+}
+
+// m rows of length n into the resident point order, in place (no-op unless the points were
+// reordered at prepare: one GPU only)
+void to_resident_order(rld_handle* h, int64_t m, double* V, int64_t ld) {
+  Resident& r = h->res;
+  if (!r.permuted || m <= 0) return;
+  h->wk.ptmp.reserve(sizeof(double) * m * r.n);
+  permute_rows(m, r.n, r.perm.as<int>(), V, ld, h->wk.ptmp.as<double>(), r.n, false, h->st);
+  RLD_CUDA(cudaMemcpy2DAsync(V, sizeof(double) * ld, h->wk.ptmp.ptr, sizeof(double) * r.n, sizeof(double) * r.n, m,
+                             cudaMemcpyDeviceToDevice, h->st));
 }
 
 // Y (m x rows) = V (m x n full) K^T restricted to the local rows
@@ -692,16 +772,16 @@ struct PrecondOut {
 // 2.7e-4 (all iterations) and 2.1e-4 (all but the last), beyond the 1e-4 fp32
 // budget, so the default is 3xTF32 everywhere; RLD_SKETCH_MODE=1 opts in to
 // single-pass TF32 for the early iterations.
-// Slice-pair diagonals of the float64 int8-slice product in the first q-1 power iterations: 6
-// (21 of the 36 pairs, dropped terms ~2^-44 of max|K| max|V| per sum term) -- those iterations only
+// Slice-pair diagonals of the float64 int8-slice product in the first q-1 power iterations: 7
+// (28 of the 36 pairs, dropped terms ~2^-51 of max|K| max|V| per sum term) -- those iterations only
 // steer the subspace, which the last full-precision iteration re-forms.  The last iteration,
-// B = Q K Q^T and every Lanczos product keep all 8 diagonals.  Measured on the float64 estimates
-// against the float64 golden values (config 3 / 1 / 2): 8 diagonals 5.3e-15 / 3.9e-15 / 5.2e-16,
-// 6 diagonals 5.6e-14 / 1.4e-16 / 2.1e-14 (config 3 505 -> 427 ms); DESIGN.md §3.2.
-// RLD_FP64_SKETCH_DIAGS (1..8, read per call) overrides.
+// B = Q K Q^T and every Lanczos product keep all 8 diagonals; with a CRT residue image the wide
+// products run as modular GEMMs instead (full precision).  Measured on config 3 (Morton order,
+// slices) against the float64 golden value: 8 diagonals 5.5e-15 (350 ms), 7: 4.7e-15 (321 ms),
+// 6: 5.6e-14 (304 ms).  RLD_FP64_SKETCH_DIAGS (1..8, read per call) overrides.
 int sketch_oz_diags() {
   const char* e = getenv("RLD_FP64_SKETCH_DIAGS");
-  const int v = e ? atoi(e) : 6;
+  const int v = e ? atoi(e) : 7;
   return v < 1 ? 1 : (v > 8 ? 8 : v);
 }
 
@@ -747,6 +827,7 @@ int lowrank_randsvd(rld_handle* h, const rld_config* c, const rld_inputs* in, Pr
                                  in->memory == RLD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
       else  // numpy-exact Gaussian sketch rows, generated on the device (src/precond.py:183)
         normal_rows(okey, w, n, 0, n, n, Y, wk.rng_scratch, wk.ints.as<int>() + 5, st);
+      to_resident_order(h, w, Y, n);
       RLD_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), st));
       for (int it = 0; it < c->precond_iters; ++it) {
         const bool last = it + 1 == c->precond_iters;
@@ -794,8 +875,8 @@ int lowrank_randsvd(rld_handle* h, const rld_config* c, const rld_inputs* in, Pr
 void global_argmax(rld_handle* h, const double* d, double* pv) {
   Resident& r = h->res;
   Work& wk = h->wk;
-  if (h->world == 1) {
-    argmax_first(r.rows, d, r.row0, pv, wk.scratch, h->st);
+  if (h->world == 1) {   // ties: the smallest original index, also when the points were reordered
+    argmax_first(r.rows, d, r.row0, pv, wk.scratch, h->st, r.permuted ? r.perm.as<int>() : nullptr);
     return;
   }
   wk.gsend.reserve(sizeof(double) * 2);
@@ -899,6 +980,7 @@ int lowrank_rankone(rld_handle* h, const rld_config* c) {
   double* w = wk.Tg.as<double>();
   double* dd = wk.scal.as<double>() + 4;   // [0] v.w  [1] w.w  [2] v.v
   normal_rows(c->precond_key, 1, n, 0, n, n, vfull, wk.rng_scratch, wk.ints.as<int>() + 5, st);   // rng.normal(n)
+  to_resident_order(h, 1, vfull, n);
   rows_dot(1, n, vfull, n, vfull, n, dd + 2, wk.scratch, st, nullptr);
   scale_by(n, vfull, dd + 2, 0, st);                                   // v /= |v|
   copy_doubles(nl, vfull + r.row0, v, st);
@@ -1086,7 +1168,15 @@ void precond_apply(rld_handle* h, int32_t op, int64_t m, const double* V, double
   const double* sqrt_base = wk.sqrt_base.as<double>();
   DevBuf& T = wk.Tg;
   T.reserve(sizeof(double) * std::max<int64_t>(1, (int64_t)k * m));
-  copy_doubles(m * n, V, Y, st);
+  const bool perm = h->res.permuted;   // operands in the caller's order, factors in the resident order
+  double* const Yout = Y;
+  if (perm) {
+    wk.ptmp2.reserve(sizeof(double) * m * n);
+    Y = wk.ptmp2.as<double>();
+    permute_rows(m, n, h->res.perm.as<int>(), V, n, Y, n, false, st);
+  } else {
+    copy_doubles(m * n, V, Y, st);
+  }
   // N^-1 z = w + U (g o U^T w), w = z / sqrt(base);  N^-T x = (x + U (g o U^T x)) / sqrt(base);
   // P^-1 u = (w + U (h o U^T w)) / sqrt(base), w = u / sqrt(base)
   if (op != RLD_SOLVE_SQRT_T) scale_rows_colmajor(n, m, n, sqrt_base, true, Y, st);
@@ -1096,6 +1186,7 @@ void precond_apply(rld_handle* h, int32_t op, int64_t m, const double* V, double
     ex_f64(h, T.as<double>(), k, k, m, U, n, n, Y, n, 1.0, 1.0);
   }
   if (op != RLD_SOLVE_SQRT) scale_rows_colmajor(n, m, n, sqrt_base, true, Y, st);
+  if (perm) permute_rows(m, n, h->res.perm.as<int>(), Y, n, Yout, n, true, st);
   RLD_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -1148,8 +1239,10 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
   double* Zp = wk.probes.as<double>();
   if (in->probes) {
     load_rows(h, in->probes, in->memory, s, Zp);
+    to_resident_order(h, s, Zp, nl);
   } else if (c->probe_kind == RLD_RADEMACHER) {
     rademacher_rows(c->probe_key, s, n, r.row0, nl, nl, Zp, st);
+    to_resident_order(h, s, Zp, nl);
   } else if (c->probe_kind == RLD_NORMAL_ORTHOGONAL) {
     // src/probes.py:15-22, 36-44: block i of min(s_left, n) rows from stream (seed, (2, i)):
     // Gaussian rows, orthonormalised (CholQR = the CGS2 Q), scaled by chi(n) radii drawn from
@@ -1163,6 +1256,7 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
       double* blk = Zp + done * nl;
       const uint64_t* key = c->probe_block_keys + 2 * b;
       normal_rows(key, sb, n, r.row0, nl, nl, blk, wk.rng_scratch, wk.ints.as<int>() + 5, st, wk.endw.as<int64_t>());
+      to_resident_order(h, sb, blk, nl);
       cholqr2(h, nl, (int)sb, blk, wk.ints.as<int>(), 2);
       int64_t ew = 0;
       RLD_CUDA(cudaMemcpyAsync(&ew, wk.endw.ptr, sizeof ew, cudaMemcpyDeviceToHost, st));
@@ -1176,6 +1270,7 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
     }
   } else {  // numpy-exact Gaussian probes on the device (src/probes.py:33-34)
     normal_rows(c->probe_key, s, n, r.row0, nl, nl, Zp, wk.rng_scratch, wk.ints.as<int>() + 5, st);
+    to_resident_order(h, s, Zp, nl);
   }
 
   // ---- Lanczos state
@@ -1535,12 +1630,45 @@ int rld_precond_apply(rld_handle* h, int32_t op, int64_t m, const double* V, dou
   return guarded(h, [&] { precond_apply(h, op, m, V, Y); });
 }
 
+int rld_slice_stats(rld_handle* h, int64_t* stats) {
+  if (!h || !stats) return RLD_ERR_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    const Resident& r = h->res;
+    for (int i = 0; i < 4; ++i) stats[i] = 0;
+    if (!r.ready || !r.kq_ready) return;
+    const int64_t nb = ceil_div(r.rows, 128) * ceil_div(r.n, 32);
+    stats[0] = nb;
+    stats[3] = r.kr_ready ? 1 : 0;
+    if (!r.knz_ready) {   // no metadata: every block reads all 8 slices, 36 pairs
+      stats[1] = 8 * nb;
+      stats[2] = 36 * nb;
+      return;
+    }
+    std::vector<int> nz((size_t)nb);
+    RLD_CUDA(cudaMemcpyAsync(nz.data(), r.knz.ptr, sizeof(int) * nb, cudaMemcpyDeviceToHost, h->st));
+    RLD_CUDA(cudaStreamSynchronize(h->st));
+    for (int v : nz) {
+      stats[1] += v;
+      stats[2] += (int64_t)v * (v + 1) / 2;
+    }
+  });
+}
+
 int rld_kv_apply(rld_handle* h, int64_t m, const double* V, double* Y) {
   if (!h) return RLD_ERR_INVALID_ARGUMENT;
   return guarded(h, [&] {
     if (!h->res.ready) fail(RLD_ERR_INVALID_ARGUMENT, "no resident problem");
     if (m < 1 || !V || !Y) fail(RLD_ERR_INVALID_ARGUMENT, "bad kv_apply arguments");
-    kv(h, m, V, Y);   // stream-ordered on rld_stream(h)
+    Resident& r = h->res;
+    if (r.permuted) {   // operands in the caller's order, K in the resident (Morton) order
+      h->wk.ptmp.reserve(sizeof(double) * m * r.n);
+      h->wk.ptmp2.reserve(sizeof(double) * m * r.n);
+      permute_rows(m, r.n, r.perm.as<int>(), V, r.n, h->wk.ptmp.as<double>(), r.n, false, h->st);
+      kv(h, m, h->wk.ptmp.as<double>(), h->wk.ptmp2.as<double>());
+      permute_rows(m, r.n, r.perm.as<int>(), h->wk.ptmp2.as<double>(), r.n, Y, r.n, true, h->st);
+    } else {
+      kv(h, m, V, Y);   // stream-ordered on rld_stream(h)
+    }
   });
 }
 

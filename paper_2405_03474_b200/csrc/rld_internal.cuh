@@ -102,6 +102,7 @@ struct KvOperand {
   int dtype = RLD_FP64;      // product arithmetic
   const int8_t* kq = nullptr;      // float64 K as 8 exact int8 slices, k-step-tiled image (kv_ozaki.cu), or null
   const double* ksigma = nullptr;  // per-row power-of-two scales of the slices
+  const int* knz = nullptr;        // per (tile, k-step) block: slices from the first nonzero one (or null)
   int64_t n = 0;             // columns of K (global order)
   int64_t row0 = 0;          // first global row held locally
   int64_t rows = 0;          // local rows
@@ -170,10 +171,13 @@ void ozaki_slice(const double* A, int64_t lda, int64_t rows, int64_t n, int tile
                  cudaStream_t st);
 // the same image straight from the points (no float64 K): stationary kernel, row max = diagonal
 // Kr != null: also K's CRT residue image (kv_crt.cu), crt_bytes(rows, n) bytes
+// knz != null: per (128-row tile, 32-column k-step) block, 8 - the number of leading all-zero slices
+// (int [ceil(rows/128)][ceil(n/32)]), which the product skips
 void ozaki_slice_points(const double* X, int64_t n, const KernelParams& kp, int64_t row0, int64_t rows, int8_t* q,
-                        double* scale, cudaStream_t st, int8_t* Kr = nullptr);
+                        double* scale, cudaStream_t st, int8_t* Kr = nullptr, int* knz = nullptr);
 void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int64_t n, const double* V, int64_t ldv,
-                      int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st, int diags = 8);
+                      int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st, int diags = 8,
+                      const int* knz = nullptr);
 // Wide float64 products as 15 modular int8 GEMMs + CRT (kv_crt.cu); the residue image of K comes
 // from its slice image (crt_residues, 15 bytes per entry).
 bool crt_supported(int64_t n);

@@ -91,7 +91,11 @@ void diag_of_tiled(int64_t rows, int64_t row0, int64_t n, const float* Kt, doubl
 // preconditioner kinds beyond rand-svd (src/precond.py:201-267)
 void precond_base_scaled(int64_t n, int k, double scale, double* A, double* base, double* sqrt_base,
                          cudaStream_t st);
-void argmax_first(int64_t n, const double* d, int64_t offset, double* out, DevBuf& scratch, cudaStream_t st);
+void argmax_first(int64_t n, const double* d, int64_t offset, double* out, DevBuf& scratch, cudaStream_t st,
+                  const int* perm = nullptr);
+// m rows of length n: gather dst[c][i] = src[c][perm[i]], or scatter dst[c][perm[i]] = src[c][i]
+void permute_rows(int64_t m, int64_t n, const int* perm, const double* src, int64_t lds, double* dst, int64_t ldd,
+                  bool scatter, cudaStream_t st);
 // out = the (value, index) pair with the largest value, first on ties, of P pairs ordered by index
 void pick_first_max(int P, const double* pairs, double* out, cudaStream_t st);
 void kernel_column(int64_t rows, int64_t row0, int64_t n, int64_t p, const void* K, int64_t ldk, int kdtype,

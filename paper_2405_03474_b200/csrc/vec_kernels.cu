@@ -815,8 +815,12 @@ __global__ void base_scaled_kernel(int64_t n, int k, double scale, double* __res
 
 // first largest entry of d[0..n) (np.argmax tie rule: smallest index), one block per chunk then a final pick;
 // out[0] = value, out[1] = global index (row0 + i) as double
+// key of index j for first-max ties: j itself, or (points stored in a locality order) the original
+// index perm[j], so the pivot is the reference's np.argmax one
+__device__ __forceinline__ int64_t amax_key(const int* perm, int64_t j) { return perm ? (int64_t)perm[j] : j; }
+
 __global__ void argmax_partial_kernel(int64_t n, const double* __restrict__ d, int64_t chunk,
-                                      double* __restrict__ part) {
+                                      double* __restrict__ part, const int* __restrict__ perm) {
   __shared__ double sv[256];
   __shared__ int64_t si[256];
   const int64_t j0 = (int64_t)blockIdx.x * chunk, j1 = min64(n, j0 + chunk);
@@ -824,7 +828,7 @@ __global__ void argmax_partial_kernel(int64_t n, const double* __restrict__ d, i
   int64_t bi = -1;
   for (int64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
     const double v = d[j];
-    if (v > bv) { bv = v; bi = j; }   // strided walk visits increasing j: keeps the first max
+    if (v > bv || (perm && v == bv && amax_key(perm, j) < amax_key(perm, bi))) { bv = v; bi = j; }   // first max
   }
   sv[threadIdx.x] = bv;
   si[threadIdx.x] = bi;
@@ -833,7 +837,8 @@ __global__ void argmax_partial_kernel(int64_t n, const double* __restrict__ d, i
     if (threadIdx.x < o) {
       const double v2 = sv[threadIdx.x + o];
       const int64_t i2 = si[threadIdx.x + o];
-      if (v2 > sv[threadIdx.x] || (v2 == sv[threadIdx.x] && i2 >= 0 && (si[threadIdx.x] < 0 || i2 < si[threadIdx.x]))) {
+      if (v2 > sv[threadIdx.x] || (v2 == sv[threadIdx.x] && i2 >= 0 &&
+                                    (si[threadIdx.x] < 0 || amax_key(perm, i2) < amax_key(perm, si[threadIdx.x])))) {
         sv[threadIdx.x] = v2;
         si[threadIdx.x] = i2;
       }
@@ -845,11 +850,12 @@ __global__ void argmax_partial_kernel(int64_t n, const double* __restrict__ d, i
     part[2 * blockIdx.x + 1] = (double)si[0];
   }
 }
-__global__ void argmax_final_kernel(int P, const double* __restrict__ part, int64_t offset, double* __restrict__ out) {
+__global__ void argmax_final_kernel(int P, const double* __restrict__ part, int64_t offset, double* __restrict__ out,
+                                    const int* __restrict__ perm) {
   double bv = -INFINITY, bi = -1.0;
   for (int b = 0; b < P; ++b) {   // pairs in increasing index order: strict > keeps the first max
     const double v = part[2 * b], i = part[2 * b + 1];
-    if (i >= 0 && v > bv) { bv = v; bi = i; }
+    if (i >= 0 && (v > bv || (perm && v == bv && bi >= 0 && perm[(int64_t)i] < perm[(int64_t)bi]))) { bv = v; bi = i; }
   }
   out[0] = bv;
   out[1] = bi >= 0 ? bi + (double)offset : -1.0;
@@ -917,18 +923,19 @@ void precond_base_scaled(int64_t n, int k, double scale, double* A, double* base
       n, k, scale, A, base, sqrt_base);
   RLD_LAUNCH_CHECK();
 }
-void argmax_first(int64_t n, const double* d, int64_t offset, double* out, DevBuf& scratch, cudaStream_t st) {
+void argmax_first(int64_t n, const double* d, int64_t offset, double* out, DevBuf& scratch, cudaStream_t st,
+                  const int* perm) {
   int P = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 2048), 512));
   const int64_t chunk = ceil_div(std::max<int64_t>(n, 1), P);
   P = (int)ceil_div(std::max<int64_t>(n, 1), chunk);
   scratch.reserve(sizeof(double) * 2 * P);
-  argmax_partial_kernel<<<P, 256, 0, st>>>(n, d, chunk, scratch.as<double>());
+  argmax_partial_kernel<<<P, 256, 0, st>>>(n, d, chunk, scratch.as<double>(), perm);
   RLD_LAUNCH_CHECK();
-  argmax_final_kernel<<<1, 1, 0, st>>>(P, scratch.as<double>(), offset, out);
+  argmax_final_kernel<<<1, 1, 0, st>>>(P, scratch.as<double>(), offset, out, perm);
   RLD_LAUNCH_CHECK();
 }
 void pick_first_max(int P, const double* pairs, double* out, cudaStream_t st) {
-  argmax_final_kernel<<<1, 1, 0, st>>>(P, pairs, 0, out);
+  argmax_final_kernel<<<1, 1, 0, st>>>(P, pairs, 0, out, nullptr);
   RLD_LAUNCH_CHECK();
 }
 void kernel_column(int64_t rows, int64_t row0, int64_t n, int64_t p, const void* K, int64_t ldk, int kdtype,
@@ -972,4 +979,27 @@ void diag_of_dense(int64_t rows, int64_t row0, const void* K, int64_t ldk, int d
   RLD_LAUNCH_CHECK();
 }
 
+}  // namespace rld
+
+namespace rld {
+namespace {
+// dst[c * ldd + i] = src[c * lds + perm[i]] (gather) or dst[c * ldd + perm[i]] = src[c * lds + i] (scatter)
+__global__ void permute_rows_kernel(int64_t m, int64_t n, const int* __restrict__ perm, const double* __restrict__ src,
+                                    int64_t lds, double* __restrict__ dst, int64_t ldd, int scatter) {
+  const int64_t c = blockIdx.y;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = perm[i];
+    if (scatter) dst[c * ldd + j] = src[c * lds + i];
+    else dst[c * ldd + i] = src[c * lds + j];
+  }
+}
+}  // namespace
+
+void permute_rows(int64_t m, int64_t n, const int* perm, const double* src, int64_t lds, double* dst, int64_t ldd,
+                  bool scatter, cudaStream_t st) {
+  if (m <= 0 || n <= 0) return;
+  const dim3 g((unsigned)std::min<int64_t>(ceil_div(n, 256), 1024), (unsigned)m);
+  permute_rows_kernel<<<g, 256, 0, st>>>(m, n, perm, src, lds, dst, ldd, scatter ? 1 : 0);
+  RLD_LAUNCH_CHECK();
+}
 }  // namespace rld

@@ -166,6 +166,7 @@ def test_int8_slices_from_points_equal_slices_from_K(rld, monkeypatch):
     from paper_2405_03474_b200.workloads import baseline
 
     monkeypatch.setenv("RLD_FP64_PRODUCT", "ozaki")
+    monkeypatch.setenv("RLD_SORT", "0")   # the points path otherwise holds K in Morton order (same value to 1e-12)
     for idx in (1, 2):
         wl = baseline(idx, n=3000, rank=64, num_probes=8, dtype="fp64")
         a = rld.rstar_logdet(rld.KernelMatrix(wl.spec, wl.points), replace(wl.config, path="stored"))
@@ -205,7 +206,7 @@ def test_int8_slices_edge_cases(rld, monkeypatch, n, m):
 
 @pytest.mark.parametrize("index", [1, 2])
 def test_fp64_sketch_diagonals(rld, index, monkeypatch):
-    """The first q-1 power iterations run the int8-slice float64 product with 6 of its 8 slice-pair
+    """The first q-1 power iterations run the int8-slice float64 product with 7 of its 8 slice-pair
     diagonals (rld_api.cu sketch_oz_diags); the last iteration, B = Q K Q^T and the Lanczos products
     keep all 36 pairs.  The estimate must stay float64-grade: within 1e-12 of the all-pairs run and
     of the unmodified reference's golden value (north_star fp64 bar: 1e-6)."""
@@ -255,3 +256,75 @@ def test_fp64_crt_product(rld, n, m, monkeypatch):
     R2 = rld.ResidentMatrix(rld.KernelMatrix(spec, pts), dtype="fp64", path="stored")
     Y2 = R2.kv_apply(Vt).cpu().numpy()
     assert (np.abs(Y2 - Y) / np.where(scale > 0, scale, 1.0)).max() <= 1e-13
+
+
+def _kinds_cfg(wl, kind, probe="rademacher", alg="r3"):
+    from dataclasses import replace
+
+    from paper_2405_03474_b200.precond import PreconditionerConfig
+
+    return replace(wl.config, algorithm=alg, probe_kind=probe, dtype="fp64", path="stored",
+                   precond=PreconditionerConfig(kind, min(64, wl.config.precond.rank), 5))
+
+
+@pytest.mark.parametrize("kind,probe,alg", [("rand-svd", "rademacher", "r3"), ("rand-svd", "gaussian", "r5"),
+                                            ("partial-cholesky", "rademacher", "r3"),
+                                            ("partial-cholesky-scaled", "rademacher", "r1"),
+                                            ("rank-one", "rademacher", "r3"), ("diagonal", "normal-orthogonal", "r3"),
+                                            ("rand-svd", "rademacher", "slq")])
+def test_morton_order_is_invisible(rld, monkeypatch, kind, probe, alg):
+    """Float64 stored K from points (d <= 3, one GPU) is held in Morton order so the int8-slice
+    product can skip all-zero far-field blocks; probes, sketch rows and the rank-one start vector
+    are permuted in, pivot ties go to the original index, kv_apply / precond_apply operands are
+    permuted in and out.  Every result must match the unpermuted run (RLD_SORT=0) to 1e-12."""
+    import torch
+
+    from conftest import rel
+    from paper_2405_03474_b200.workloads import baseline
+
+    wl = baseline(1, n=1500, dtype="fp64")
+    cfg = _kinds_cfg(wl, kind, probe, "r3" if alg == "slq" else alg)
+    if alg == "slq":
+        from dataclasses import replace
+
+        cfg = replace(cfg, algorithm="slq")
+    res = {}
+    for sort in ("1", "0"):
+        monkeypatch.setenv("RLD_SORT", sort)
+        R = rld.ResidentMatrix(rld.KernelMatrix(wl.spec, wl.points), dtype="fp64", path="stored")
+        est = R.estimate(cfg)
+        V = torch.from_numpy(np.random.default_rng(5).standard_normal((3, wl.n))).cuda()
+        res[sort] = (est, R.kv_apply(V).cpu().numpy())
+    a, b = res["1"][0], res["0"][0]
+    # the plain partial-Cholesky preconditioner floors its pivot rows' base at 1e-12, so P^-1 K is
+    # ~1e12-conditioned and any change of summation order moves the trace term ~1e-6 (DESIGN.md §4:
+    # pinned at 1e-4 against the reference); everything else is float64-identical
+    tol = 1e-4 if kind == "partial-cholesky" else 1e-12
+    assert rel(a.value, b.value) <= tol, (a.value, b.value)
+    assert rel(a.logdet_P, b.logdet_P) <= 1e-12
+    if kind != "partial-cholesky":
+        np.testing.assert_allclose(a.per_probe_values, b.per_probe_values, rtol=1e-10, atol=1e-10 * abs(b.value))
+    np.testing.assert_allclose(res["1"][1], res["0"][1], rtol=1e-12, atol=1e-12 * np.abs(res["0"][1]).max())
+
+
+def test_morton_order_precond_seam(rld, monkeypatch):
+    """rld_precond_build / rld_precond_apply with reordered points: the apply operands are in the
+    caller's order (solve_sqrt / solve_sqrt_t / solve), identical to the unpermuted handle."""
+    import torch
+
+    from paper_2405_03474_b200 import precond as P
+    from paper_2405_03474_b200.linalg import Rng
+    from paper_2405_03474_b200.workloads import baseline
+
+    wl = baseline(1, n=1200, dtype="fp64")
+    V = torch.from_numpy(np.random.default_rng(9).standard_normal((wl.n, 2))).cuda()   # columns are vectors
+    out = {}
+    for sort in ("1", "0"):
+        monkeypatch.setenv("RLD_SORT", sort)
+        M = rld.KernelMatrix(wl.spec, wl.points)
+        pc = P.build_preconditioner(M, P.PreconditionerConfig("rand-svd", 48, 5), Rng(3), dtype="fp64")
+        out[sort] = (pc.log_det, pc.solve_sqrt(V).cpu().numpy(), pc.solve_sqrt_t(V).cpu().numpy(),
+                     pc.solve(V).cpu().numpy())
+    assert abs(out["1"][0] - out["0"][0]) <= 1e-12 * abs(out["0"][0])
+    for k in (1, 2, 3):
+        np.testing.assert_allclose(out["1"][k], out["0"][k], rtol=1e-11, atol=1e-12 * np.abs(out["0"][k]).max())
