@@ -67,6 +67,8 @@ struct OtfParams {
   const float* pts;     // [ceil(n/64) * 2][8][32] pre-scaled float32 coordinates
   int64_t n, row0, rows;
   const float* rowscale;   // stored K (DIM == 0): per local row 2^s_i with max_j |K_ij| 2^s_i in [2^13, 2^14)
+  const uint32_t* skip;    // on the fly: bit k of word [tile][k / 32] set = the tile's k-step k has only
+  int skip_wpt;            // exactly-zero fp16 operands (far field in Morton order): no loads, no MMAs
   int ks32;             // stored K: 32-column tiles per row tile of the tiled layout
   float diag;           // 2^sK (a^2 + jitter)
   float la2;            // log2(a^2) + sK
@@ -170,6 +172,21 @@ __device__ __forceinline__ void load32(uint32_t rowp, int row, float rs, uint32_
   }
 }
 
+// k-step `ks` of row tile `t` skipped?  Word cache per caller (consecutive k-steps share a word).
+struct SkipCache {
+  int64_t key = -1;
+  uint32_t word = 0;
+  __device__ __forceinline__ bool operator()(const OtfParams& p, int t, int ks) {
+    if (!p.skip) return false;
+    const int64_t k = (int64_t)t * p.skip_wpt + (ks >> 5);
+    if (k != key) {
+      key = k;
+      word = __ldg(p.skip + k);
+    }
+    return (word >> (ks & 31)) & 1u;
+  }
+};
+
 template <int NT>
 struct OtfShape {
   static constexpr bool STACK = NT == 32;           // [Bh; Bl] as one N = 64 operand
@@ -213,6 +230,7 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
   uint64_t* accfull = afull + SB;
   uint64_t* accempty = accfull + NACC;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accempty + NACC);
+  volatile int* grp_live = reinterpret_cast<volatile int*>(tmem_holder + 1);   // MMA warps: group has an MMA yet
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t bid = blockIdx.x;
@@ -251,9 +269,15 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
   if (StepIter<false, false>(p.sched, cta, 1).valid()) {
     if (warp == 0) {
       // ---------------- points producer
+      SkipCache skipped;
       for (StepIter<false, false> it(p.sched, cta, SA); it.valid(); it.next()) {
         const int s = it.s;
         ptx::mbar_wait_idle(&kempty[s], it.ph ^ 1, p.wait_mode, p.wait_ns);
+        if (skipped(p, it.tile, it.kstep)) {   // the slot still cycles, empty
+          if (ptx::elect_one()) ptx::mbar_arrive(&kfull[s]);
+          __syncwarp();
+          continue;
+        }
         if (ptx::elect_one()) {
           ptx::mbar_arrive_expect_tx(&kfull[s], PTS_STAGE);
           if (DIM == 0)   // tiles 2 kstep, 2 kstep + 1 of row tile `tile`: one 256-row box
@@ -268,6 +292,7 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
       // ---------------- B producer
       int64_t epoch = 0;
       unsigned long long pb[2] = {0, 0};
+      SkipCache bskipped;
       for (StepIter<false, false> it(p.sched, cta, SB); it.valid(); it.next()) {
         const int s = it.s;
         if (p.sync_k > 0 && !it.in_tail() && it.v > 0 && (it.kstep & (p.sync_k - 1)) == 0) {
@@ -285,6 +310,11 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
         const unsigned long long b0 = prof ? clock64() : 0;
         ptx::mbar_wait_idle(&bempty[s], it.ph ^ 1, p.wait_mode, p.wait_ns);
         if (prof) pb[0] += clock64() - b0;
+        if (bskipped(p, it.tile, it.kstep)) {
+          if (ptx::elect_one()) ptx::mbar_arrive(&bfull[s]);
+          __syncwarp();
+          continue;
+        }
         if (ptx::elect_one()) {
           uint8_t* st = bring + (size_t)s * BST;
           const int brow = it.kstep * p.mp + b_row0;
@@ -306,6 +336,7 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
       constexpr uint64_t LO_OFF = (uint64_t)(B_BYTES >> 4);
       int64_t gi = -1;
       unsigned long long pa[5] = {0, 0, 0, 0, 0};
+      SkipCache mskipped;
       for (StepIter<true, false> it(p.sched, cta, SB); it.valid(); it.next()) {
         const bool gstart = it.group_start(), gend = it.group_end();
         if (gstart) ++gi;
@@ -330,12 +361,18 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
           const uint32_t d = tmem + (uint32_t)(gi % NACC) * DW;
           const uint32_t a0 = tmem + A_COL0 + ASTRIDE * s;
           const uint64_t bdesc = desc0 + (uint64_t)((s * BST) >> 4);
+          // skipped k-steps issue nothing; the group's first issued MMA overwrites the accumulator
+          // (the flag travels with the baton: the other MMA warp reads it after its bar.sync)
+          const bool skip = mskipped(p, it.tile, it.kstep);
+          const bool live = gstart ? false : (*grp_live != 0);
+          __syncwarp();
           const bool leader = ptx::elect_one();
-          if (leader) {
+          if (leader) *grp_live = (live || !skip) ? 1 : 0;
+          if (leader && !skip) {
 #pragma unroll
             for (int kk = 0; kk < OB_K / 16; ++kk) {
               const uint64_t bd = bdesc + 2 * kk;   // +32 bytes = 16 fp16 along k
-              const uint32_t acc = (gstart && kk == 0) ? 0u : 1u;
+              const uint32_t acc = (!live && kk == 0) ? 0u : 1u;
               if (Sh::STACK) {
                 mma_f16_ts(d, a0 + 8 * kk, bd, idesc, acc);         // D += Kh [Vh; Vl]
                 mma_f16_ts(d, a0 + 32 + 8 * kk, bd, idesc, 1u);     // D += Kl [Vh; Vl]
@@ -381,6 +418,7 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&afull[buf]);
       };
+      SkipCache cskipped;
       StepIter<false, true> it(p.sched, cta, SA, SB);
       for (int k = 0; k < par; ++k) it.next();
       for (; it.valid(); [&] { for (int k = 0; k < Sh::CP; ++k) it.next(); }()) {
@@ -413,6 +451,13 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
         }
         ptx::tc_fence_after();
         const uint32_t ta = tmem + lane_base + A_COL0 + ASTRIDE * sb;
+        if (cskipped(p, it.tile, it.kstep)) {   // nothing to generate: release the slot, post the buffer
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&kempty[s]);
+          if (pend >= 0) post(pend);
+          pend = sb;
+          continue;
+        }
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           uint32_t hw[16], lw[16];
@@ -458,11 +503,14 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
       int64_t gi = -1;
       unsigned long long pd[2] = {0, 0};
       SegIter si(p.sched, cta);
-      int tile = 0, len = 0, seg = 0;
-      while (si.next(tile, len, seg)) {
-        for (int g0 = 0; g0 < len; g0 += GROUP) {
+      SkipCache dskipped;
+      int tile = 0, len = 0, seg = 0, k0 = 0;
+      while (si.next(tile, len, seg, k0)) {
+        for (int g0 = 0; g0 < len; g0 += p.sched.group) {
           ++gi;
           const int buf = (int)(gi % NACC);
+          bool any = !p.skip;   // a group whose k-steps were all skipped left the accumulator untouched
+          for (int k = g0; !any && k < g0 + p.sched.group && k < len; ++k) any = !dskipped(p, tile, k0 + k);
           const unsigned long long d0 = prof ? clock64() : 0;
           ptx::mbar_wait_idle(&accfull[buf], (uint32_t)((gi / NACC) & 1), p.wait_mode, p.wait_ns);
           if (prof) {
@@ -470,6 +518,7 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
             pd[1] += 1;
           }
           ptx::tc_fence_after();
+          if (any) {
 #pragma unroll
           for (int c0 = 0; c0 < HALF; c0 += 16) {
             uint32_t v[16];
@@ -485,6 +534,7 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
 #pragma unroll
               for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]);
             }
+          }
           }
           ptx::tc_fence_before();
           __syncwarp();
@@ -661,6 +711,100 @@ void kv_rowscales(const float* Kt, int64_t rows, int64_t n, float* rs, cudaStrea
   RLD_LAUNCH_CHECK();
 }
 
+// ---- far-field skip map of the on-the-fly product (points in Morton order).  Box of the points of
+// each 128-row tile and of each 64-column k-step, then per (tile, k-step) an upper bound on K from the
+// boxes' distance: a k-step whose scaled bound 2^sK K_max is below 2^-27 (4x under the 2^-25 at
+// which fp16 head and tail both round to zero) has only exactly-zero operands.
+__global__ void otf_boxes(const double* __restrict__ X, int64_t first, int64_t count, int d, int64_t group,
+                          int64_t groups, double* __restrict__ box) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= groups) return;
+  double lo[4], hi[4];
+  for (int c = 0; c < 4; ++c) {
+    lo[c] = INFINITY;
+    hi[c] = -INFINITY;
+  }
+  const int64_t a = g * group, b = min64(count, a + group);
+  for (int64_t i = a; i < b; ++i)
+    for (int c = 0; c < d; ++c) {
+      const double x = X[(first + i) * d + c];
+      lo[c] = fmin(lo[c], x);
+      hi[c] = fmax(hi[c], x);
+    }
+  for (int c = 0; c < 4; ++c) {
+    box[g * 8 + c] = lo[c];
+    box[g * 8 + 4 + c] = hi[c];
+  }
+}
+
+__global__ void otf_skip_kernel(const double* __restrict__ tbox, const double* __restrict__ kbox, int64_t tiles,
+                                int64_t ks, int wpt, int d, KernelParams kp, double thresh, int64_t row0, int64_t rows,
+                                uint32_t* __restrict__ bits) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= tiles * wpt) return;
+  const int64_t t = e / wpt;
+  const int w = (int)(e - t * wpt);
+  uint32_t word = 0;
+  for (int b = 0; b < 32; ++b) {
+    const int64_t k = (int64_t)w * 32 + b;
+    if (k >= ks) break;
+    double r2 = 0.0;
+    for (int c = 0; c < d; ++c) {
+      const double g = fmax(0.0, fmax(kbox[k * 8 + c] - tbox[t * 8 + 4 + c], tbox[t * 8 + c] - kbox[k * 8 + 4 + c]));
+      r2 += g * g;
+    }
+    // the k-step may hold a diagonal entry of these rows: never skipped (r2 = 0 there anyway)
+    const int64_t r_lo = row0 + t * 128, r_hi = row0 + min64(rows, (t + 1) * 128), c_lo = k * 64, c_hi = c_lo + 64;
+    if (r_lo < c_hi && c_lo < r_hi) continue;
+    if (kernel_value_f64(kp, r2) < thresh) word |= 1u << b;
+  }
+  bits[e] = word;
+}
+
+void otf_skip_map(const double* X, int64_t n, const KernelParams& kp, int64_t row0, int64_t rows, uint32_t* bits,
+                  DevBuf& scratch, cudaStream_t st) {
+  if (rows <= 0 || kp.d > 4) return;
+  const int64_t tiles = ceil_div(rows, OB_M), ks = ceil_div(n, OB_K);
+  const int wpt = (int)ceil_div(ks, 32);
+  scratch.reserve(sizeof(double) * 8 * (tiles + ks));
+  double* tb = scratch.as<double>();
+  double* kb = tb + 8 * tiles;
+  otf_boxes<<<(unsigned)ceil_div(tiles, 128), 128, 0, st>>>(X, row0, rows, kp.d, OB_M, tiles, tb);
+  RLD_LAUNCH_CHECK();
+  otf_boxes<<<(unsigned)ceil_div(ks, 128), 128, 0, st>>>(X, 0, n, kp.d, OB_K, ks, kb);
+  RLD_LAUNCH_CHECK();
+  const int sK = kp.diag > 0.0 ? SCALE_TOP - ilogb(kp.diag) : 0;
+  const double thresh = std::ldexp(1.0, -27 - sK);
+  otf_skip_kernel<<<(unsigned)ceil_div(tiles * wpt, 256), 256, 0, st>>>(tb, kb, tiles, ks, wpt, kp.d, kp, thresh, row0,
+                                                                        rows, bits);
+  RLD_LAUNCH_CHECK();
+}
+
+int64_t otf_skip_words(int64_t rows, int64_t n) { return ceil_div(rows, OB_M) * ceil_div(ceil_div(n, OB_K), 32); }
+
+__global__ void popc_kernel(const uint32_t* __restrict__ w, int64_t n, unsigned long long* __restrict__ out) {
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    c += __popc(w[i]);
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+// fraction of the (tile, k-step) pairs the map skips
+double otf_skip_fraction(const uint32_t* bits, int64_t rows, int64_t n, DevBuf& scratch, cudaStream_t st) {
+  const int64_t words = otf_skip_words(rows, n);
+  if (words <= 0) return 0.0;
+  scratch.reserve(sizeof(unsigned long long));
+  RLD_CUDA(cudaMemsetAsync(scratch.ptr, 0, sizeof(unsigned long long), st));
+  popc_kernel<<<(unsigned)std::min<int64_t>(ceil_div(words, 256), 1024), 256, 0, st>>>(
+      bits, words, scratch.as<unsigned long long>());
+  RLD_LAUNCH_CHECK();
+  unsigned long long c = 0;
+  RLD_CUDA(cudaMemcpyAsync(&c, scratch.ptr, sizeof c, cudaMemcpyDeviceToHost, st));
+  RLD_CUDA(cudaStreamSynchronize(st));
+  return (double)c / (double)(ceil_div(rows, OB_M) * ceil_div(n, OB_K));
+}
+
 // The fp16 kernel is the default on-the-fly float32 product; RLD_OTF_KIND=tf32 selects the
 // 3xTF32 kernel of kv_tc.cu (read per call, for A/B measurements).
 bool kv_otf_f16_enabled() {
@@ -723,6 +867,14 @@ void kv_product_otf16(const KvOperand& op, int64_t m, const double* V, int64_t l
   p.pts = op.pts4;
   p.rowscale = op.rowscale;
   p.ks32 = (int)ceil_div(n, 32);
+  p.skip = stored ? nullptr : op.otf_skip;
+  p.skip_wpt = (int)ceil_div(ks, 32);
+  // Morton order puts a row's near field (most of |Y_i|) into a few consecutive k-steps, so a TMEM
+  // group would carry nearly the whole sum through its truncating (round-toward-zero) adds: flush
+  // every k-step there (config 3 on the fly, log det P vs the float64 oracle: groups of 4: 2.6e-5,
+  // of 1: see DESIGN.md §3.4)
+  static const int grp_sorted = getenv("RLD_OTF_GROUP") ? atoi(getenv("RLD_OTF_GROUP")) : 1;
+  if (p.skip) p.sched.group = std::max(1, grp_sorted);
   p.n = n;
   p.row0 = op.row0;
   p.rows = rows;

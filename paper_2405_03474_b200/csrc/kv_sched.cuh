@@ -21,6 +21,7 @@ constexpr int GROUP = 4;            // k-steps accumulated in TMEM before the re
 // whose per-CTA partial tiles kv_tc_reduce adds in fixed order.
 struct Sched {
   int ks, G, R;          // k-steps per tile, CTAs per pass, full rounds
+  int group = GROUP;     // k-steps per TMEM accumulation group (register flush after each)
   int64_t tail_total;    // (tiles - R G) * ks
   __host__ __device__ int64_t tail_beg(int64_t c) const { return c * tail_total / G; }
   __host__ __device__ int64_t tail_end(int64_t c) const { return (c + 1) * tail_total / G; }
@@ -73,14 +74,14 @@ __host__ __device__ __forceinline__ int64_t cta_of_step(int64_t x, int64_t total
 template <bool GRP, bool BR>
 struct StepIter {
   int v, vend;           // step index (== pipeline slot j) and end: [0, R ks) phase 1, then the tail range
-  int ks, kstep, tile, s, S, G, R, round;
+  int ks, kstep, tile, s, S, G, R, round, group;
   int tail_next, tail_k0;   // where the tail range starts (tile, k-step)
   uint32_t ph;
   int gpos = 0;          // GRP: position in the accumulation group
   int sb = 0, SB = 1;    // BR: second ring
   uint32_t phb = 0;
   __device__ __forceinline__ StepIter(const Sched& sc, int64_t cta, int S_, int SB_ = 1)
-      : v(0), ks(sc.ks), kstep(0), s(0), S(S_), G(sc.G), R(sc.R), round(0), ph(0), SB(SB_) {
+      : v(0), ks(sc.ks), kstep(0), s(0), S(S_), G(sc.G), R(sc.R), round(0), group(sc.group), ph(0), SB(SB_) {
     const int64_t tb = sc.tail_beg(cta), te = sc.tail_end(cta);
     vend = R * ks + (int)(te - tb);
     tail_next = R * G + (int)(tb / ks);
@@ -96,7 +97,7 @@ struct StepIter {
   __device__ __forceinline__ bool in_tail() const { return round >= R; }
   __device__ __forceinline__ bool group_start() const { return gpos == 0; }
   __device__ __forceinline__ bool seg_end() const { return v + 1 == vend || kstep + 1 == ks; }
-  __device__ __forceinline__ bool group_end() const { return seg_end() || gpos + 1 == GROUP; }
+  __device__ __forceinline__ bool group_end() const { return seg_end() || gpos + 1 == group; }
   __device__ __forceinline__ void next() {
     if (GRP) gpos = group_end() ? 0 : gpos + 1;
     ++v;
@@ -137,10 +138,16 @@ struct SegIter {
   }
   // next segment: tile, its length in k-steps and its partial-sum slot; false when done
   __device__ __forceinline__ bool next(int& tile, int& len, int& seg) {
+    int k0;
+    return next(tile, len, seg, k0);
+  }
+  // ... and the segment's first k-step
+  __device__ __forceinline__ bool next(int& tile, int& len, int& seg, int& k0) {
     if (r < sc->R) {
       tile = (int)cta + r * sc->G;
       len = sc->ks;
       seg = 0;
+      k0 = 0;
       ++r;
       return true;
     }
@@ -150,6 +157,7 @@ struct SegIter {
     tile = sc->R * sc->G + (int)u;
     len = (int)(std::min<int64_t>(xe, x0 + sc->ks) - x);
     seg = (int)(cta - cta_of_step(x0, sc->tail_total, sc->G));
+    k0 = (int)(x - x0);
     x += len;
     return true;
   }

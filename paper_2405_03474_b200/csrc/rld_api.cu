@@ -100,6 +100,8 @@ struct Resident {
   DevBuf perm;               // points held in Morton (Z-curve) order: perm[i] = original index of point i
   bool permuted = false;     // (single GPU, float64 stored products: far-field slice blocks are all-zero)
   DevBuf knz;                // per slice-image block: slices from the first nonzero one (skipped leading zeros)
+  DevBuf otf_skip;           // on the fly (fp32, Morton order): far-field (tile, k-step) skip bits
+  bool otf_skip_ready = false;
   bool knz_ready = false;
   DevBuf Kr;                 // residues of K' modulo the CRT moduli (kv_crt.cu), for the wide products
   bool kr_ready = false;
@@ -112,6 +114,7 @@ struct Resident {
     o.ldk = ldk;
     o.tiled = tiled;
     o.rowscale = (tiled && path != RLD_PATH_ON_THE_FLY) ? rowscale.as<float>() : nullptr;
+    o.otf_skip = (otf_skip_ready && path == RLD_PATH_ON_THE_FLY) ? otf_skip.as<uint32_t>() : nullptr;
     o.X = X.as<double>();
     o.pts4 = (source == RLD_SOURCE_POINTS && d <= 4) ? pts4.as<float>() : nullptr;
     o.kp = kp;
@@ -257,8 +260,12 @@ std::vector<int> morton_order(const double* X, int64_t n, int d) {
 bool sort_points(const rld_handle* h, const rld_problem* p) {
   const char* e = getenv("RLD_SORT");
   if (e && e[0] == '0') return false;
-  return p->source == RLD_SOURCE_POINTS && p->path == RLD_PATH_STORED && p->dtype == RLD_FP64 &&
-         fp64_product_ozaki() && h->world == 1 && p->d >= 1 && p->d <= 3 && p->n < (int64_t)1 << 31;
+  // float64 stored on int8 slices (all-zero leading slices skipped) or float32 on the fly (far-field
+  // k-steps with exactly-zero fp16 operands skipped)
+  const bool slices = p->path == RLD_PATH_STORED && p->dtype == RLD_FP64 && fp64_product_ozaki();
+  const bool otf = p->path == RLD_PATH_ON_THE_FLY && p->dtype == RLD_FP32 && kv_otf_f16_enabled();
+  return p->source == RLD_SOURCE_POINTS && (slices || otf) && h->world == 1 && p->d >= 1 && p->d <= 3 &&
+         p->n < (int64_t)1 << 31;
 }
 
 void prepare(rld_handle* h, const rld_problem* p) {
@@ -274,6 +281,7 @@ void prepare(rld_handle* h, const rld_problem* p) {
   r.kr_ready = false;
   r.knz_ready = false;
   r.permuted = false;
+  r.otf_skip_ready = false;
   h->precond_k = -1;
   r.source = p->source;
   r.dtype = p->dtype;
@@ -332,6 +340,27 @@ void prepare(rld_handle* h, const rld_problem* p) {
       // coordinates pre-scaled so the tile generator's r^2 is the kernel argument
       const double scale = p->family == RLD_MATERN52 ? r.kp.s5_over_l : std::sqrt(r.kp.inv_2l2 * 1.4426950408889634);
       pad_points(r.X.as<double>(), p->n, p->d, scale, r.pts4.as<float>(), st);
+      if (r.permuted && r.path == RLD_PATH_ON_THE_FLY && p->dtype == RLD_FP32 && r.rows > 0) {
+        r.otf_skip.reserve(sizeof(uint32_t) * otf_skip_words(r.rows, p->n));
+        otf_skip_map(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.otf_skip.as<uint32_t>(), h->wk.scratch2, st);
+        // the order pays only where it skips enough: its per-k-step flushes (kv_otf.cu) cost ~13 %
+        // (config 4's clustered points skip ~nothing; config 5 skips most k-steps)
+        if (otf_skip_fraction(r.otf_skip.as<uint32_t>(), r.rows, p->n, h->wk.scratch2, st) >= 0.3) {
+          r.otf_skip_ready = true;
+        } else {   // back to the caller's order
+          std::vector<double> hx((size_t)p->n * p->d), hy((size_t)p->n * p->d);
+          std::vector<int> pm((size_t)p->n);
+          RLD_CUDA(cudaMemcpyAsync(hx.data(), r.X.ptr, xb, cudaMemcpyDeviceToHost, st));
+          RLD_CUDA(cudaMemcpyAsync(pm.data(), r.perm.ptr, sizeof(int) * p->n, cudaMemcpyDeviceToHost, st));
+          RLD_CUDA(cudaStreamSynchronize(st));
+          for (int64_t i = 0; i < p->n; ++i)
+            for (int c = 0; c < p->d; ++c) hy[(size_t)pm[i] * p->d + c] = hx[(size_t)i * p->d + c];
+          RLD_CUDA(cudaMemcpyAsync(r.X.ptr, hy.data(), xb, cudaMemcpyHostToDevice, st));
+          RLD_CUDA(cudaStreamSynchronize(st));
+          r.permuted = false;
+          pad_points(r.X.as<double>(), p->n, p->d, scale, r.pts4.as<float>(), st);
+        }
+      }
     }
     if (r.path == RLD_PATH_STORED) {
       if (p->dtype == RLD_FP64 && fp64_product_ozaki()) {

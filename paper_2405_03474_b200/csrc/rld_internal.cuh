@@ -110,6 +110,7 @@ struct KvOperand {
   int oz_diags = 8;          // float64 int8-slice product: slice-pair diagonals kept (8 = all 36 pairs)
   const int8_t* kr = nullptr;      // K' residues modulo the CRT moduli (kv_crt.cu), or null
   const float* rowscale = nullptr; // tiled fp32 K: per-row power-of-two scales (kv_otf.cu stored products)
+  const uint32_t* otf_skip = nullptr;  // on the fly: (tile, k-step) far-field skip bits (kv_otf.cu), or null
 };
 
 struct KvWorkspace {
@@ -129,6 +130,11 @@ bool kv_tc_supported(const KvOperand& op);
 // selects the 3xTF32 kernel).  Points in op.pts4 padded to otf_points_floats(n) floats.
 bool kv_otf_f16_enabled();
 int64_t otf_points_floats(int64_t n);
+// far-field skip map of the on-the-fly fp16 product (otf_skip_words(rows, n) words)
+int64_t otf_skip_words(int64_t rows, int64_t n);
+double otf_skip_fraction(const uint32_t* bits, int64_t rows, int64_t n, DevBuf& scratch, cudaStream_t st);
+void otf_skip_map(const double* X, int64_t n, const KernelParams& kp, int64_t row0, int64_t rows, uint32_t* bits,
+                  DevBuf& scratch, cudaStream_t st);
 // per-row scales of a tiled fp32 K for the fp16 stored products (wide products, m > 64)
 void kv_rowscales(const float* Kt, int64_t rows, int64_t n, float* rs, cudaStream_t st);
 void kv_product_otf16(const KvOperand& op, int64_t m, const double* V, int64_t ldv, double* Y, int64_t ldy,
