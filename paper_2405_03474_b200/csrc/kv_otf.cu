@@ -172,20 +172,130 @@ __device__ __forceinline__ void load32(uint32_t rowp, int row, float rs, uint32_
   }
 }
 
-// k-step `ks` of row tile `t` skipped?  Word cache per caller (consecutive k-steps share a word).
-struct SkipCache {
-  int64_t key = -1;
-  uint32_t word = 0;
-  __device__ __forceinline__ bool operator()(const OtfParams& p, int t, int ks) {
-    if (!p.skip) return false;
-    const int64_t k = (int64_t)t * p.skip_wpt + (ks >> 5);
-    if (k != key) {
-      key = k;
-      word = __ldg(p.skip + k);
+// First k-step >= k of row tile t below kend that the skip map keeps (kend if none).
+__device__ __forceinline__ int next_kept(const OtfParams& p, int t, int k, int kend) {
+  const uint32_t* row = p.skip + (int64_t)t * p.skip_wpt;
+  while (k < kend) {
+    const uint32_t m = ~__ldg(row + (k >> 5)) & (0xFFFFFFFFu << (k & 31));
+    if (m) {
+      const int kk = (k & ~31) + __ffs(m) - 1;
+      return kk < kend ? kk : kend;
     }
-    return (word >> (ks & 31)) & 1u;
+    k = (k & ~31) + 32;
+  }
+  return kend;
+}
+
+// The CTA's (tile, k-step) walk of StepIter (kv_sched.cuh) restricted to the k-steps the skip map
+// keeps (all of them without a map): every role walks the same sequence, so the rings, the MMA baton
+// and the accumulation groups see only kept steps.  u counts kept steps (ring slot u % S); the
+// lookahead (l*) is the next kept step, which decides segment and group ends.
+template <bool GRP, bool BR>
+struct KeptIter {
+  const OtfParams* p;
+  int ks, G, R, group;
+  int64_t vend;
+  int tail_next, tail_k0;
+  int v, kstep, tile, round;        // current kept step (raw walk position)
+  int lv, lkstep, ltile, lround;    // next kept step
+  int u = 0;
+  int s = 0, S;
+  uint32_t ph = 0;
+  int gpos = 0;
+  int sb = 0, SB = 1;
+  uint32_t phb = 0;
+  __device__ __forceinline__ KeptIter(const OtfParams& prm, int64_t cta, int S_, int SB_ = 1)
+      : p(&prm), ks(prm.sched.ks), G(prm.sched.G), R(prm.sched.R), group(prm.sched.group), S(S_), SB(SB_) {
+    const Sched& sc = prm.sched;
+    const int64_t tb = sc.tail_beg(cta), te = sc.tail_end(cta);
+    vend = (int64_t)R * ks + (te - tb);
+    tail_next = R * G + (int)(tb / ks);
+    tail_k0 = (int)(tb - (int64_t)(tb / ks) * ks);
+    v = 0;
+    round = 0;
+    if (R > 0) {
+      tile = (int)cta;
+      kstep = 0;
+    } else {
+      tile = tail_next;
+      kstep = tail_k0;
+    }
+    seek(v, kstep, tile, round);
+    lv = v; lkstep = kstep; ltile = tile; lround = round;
+    if (lv < vend) {
+      raw_next(lv, lkstep, ltile, lround);
+      seek(lv, lkstep, ltile, lround);
+    }
+  }
+  // one raw step (StepIter::next without the rings)
+  __device__ __forceinline__ void raw_next(int& v_, int& k_, int& t_, int& r_) const {
+    ++v_;
+    if (++k_ == ks) {
+      k_ = 0;
+      if (r_ < R) {
+        if (++r_ < R) {
+          t_ += G;
+        } else {
+          t_ = tail_next;
+          k_ = tail_k0;
+        }
+      } else {
+        ++t_;
+      }
+    }
+  }
+  // forward to the first kept step at or after the position
+  __device__ __forceinline__ void seek(int& v_, int& k_, int& t_, int& r_) const {
+    if (!p->skip) return;
+    while (v_ < vend) {
+      const int kend = (int)min64(ks, (int64_t)k_ + (vend - v_));   // this tile's segment ends here
+      const int k2 = next_kept(*p, t_, k_, kend);
+      v_ += k2 - k_;
+      k_ = k2;
+      if (k2 < kend) return;
+      // the rest of the segment is skipped: onto the next tile
+      --v_;
+      k_ = kend - 1;
+      raw_next(v_, k_, t_, r_);
+    }
+  }
+  __device__ __forceinline__ bool valid() const { return v < vend; }
+  __device__ __forceinline__ bool has_next() const { return lv < vend; }
+  __device__ __forceinline__ bool group_start() const { return gpos == 0; }
+  __device__ __forceinline__ bool seg_end() const { return !has_next() || ltile != tile; }
+  __device__ __forceinline__ bool group_end() const { return seg_end() || gpos + 1 == group; }
+  __device__ __forceinline__ void next() {
+    if (GRP) gpos = group_end() ? 0 : gpos + 1;
+    v = lv; kstep = lkstep; tile = ltile; round = lround;
+    if (lv < vend) {
+      raw_next(lv, lkstep, ltile, lround);
+      seek(lv, lkstep, ltile, lround);
+    }
+    ++u;
+    if (++s == S) {
+      s = 0;
+      ph ^= 1;
+    }
+    if (BR && ++sb == SB) {
+      sb = 0;
+      phb ^= 1;
+    }
   }
 };
+
+// kept k-steps of row tile t in [k0, k0 + len)
+__device__ __forceinline__ int kept_count(const OtfParams& p, int t, int k0, int len) {
+  if (!p.skip) return len;
+  const uint32_t* row = p.skip + (int64_t)t * p.skip_wpt;
+  int c = 0;
+  for (int k = k0; k < k0 + len;) {
+    const int b = k & 31, take = min(32 - b, k0 + len - k);
+    const uint32_t mask = (take == 32 ? 0xFFFFFFFFu : ((1u << take) - 1u)) << b;
+    c += __popc(~__ldg(row + (k >> 5)) & mask);
+    k += take;
+  }
+  return c;
+}
 
 template <int NT>
 struct OtfShape {
@@ -230,7 +340,6 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
   uint64_t* accfull = afull + SB;
   uint64_t* accempty = accfull + NACC;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accempty + NACC);
-  volatile int* grp_live = reinterpret_cast<volatile int*>(tmem_holder + 1);   // MMA warps: group has an MMA yet
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t bid = blockIdx.x;
@@ -266,18 +375,12 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
   const uint32_t tmem = *tmem_holder;
 
   const unsigned long long k_start = prof ? clock64() : 0;
-  if (StepIter<false, false>(p.sched, cta, 1).valid()) {
+  if (StepIter<false, false>(p.sched, cta, 1).valid()) {   // raw schedule: empty segments still get zeros
     if (warp == 0) {
       // ---------------- points producer
-      SkipCache skipped;
-      for (StepIter<false, false> it(p.sched, cta, SA); it.valid(); it.next()) {
+      for (KeptIter<false, false> it(p, cta, SA); it.valid(); it.next()) {
         const int s = it.s;
         ptx::mbar_wait_idle(&kempty[s], it.ph ^ 1, p.wait_mode, p.wait_ns);
-        if (skipped(p, it.tile, it.kstep)) {   // the slot still cycles, empty
-          if (ptx::elect_one()) ptx::mbar_arrive(&kfull[s]);
-          __syncwarp();
-          continue;
-        }
         if (ptx::elect_one()) {
           ptx::mbar_arrive_expect_tx(&kfull[s], PTS_STAGE);
           if (DIM == 0)   // tiles 2 kstep, 2 kstep + 1 of row tile `tile`: one 256-row box
@@ -292,10 +395,10 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
       // ---------------- B producer
       int64_t epoch = 0;
       unsigned long long pb[2] = {0, 0};
-      SkipCache bskipped;
-      for (StepIter<false, false> it(p.sched, cta, SB); it.valid(); it.next()) {
+      for (KeptIter<false, false> it(p, cta, SB); it.valid(); it.next()) {
         const int s = it.s;
-        if (p.sync_k > 0 && !it.in_tail() && it.v > 0 && (it.kstep & (p.sync_k - 1)) == 0) {
+        // (no epoch barrier with a skip map: the kept steps differ between CTAs)
+        if (p.sync_k > 0 && it.round < p.sched.R && it.v > 0 && (it.kstep & (p.sync_k - 1)) == 0) {
           ++epoch;
           const unsigned long long e0 = prof ? clock64() : 0;
           if (lane == 0) {
@@ -310,11 +413,6 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
         const unsigned long long b0 = prof ? clock64() : 0;
         ptx::mbar_wait_idle(&bempty[s], it.ph ^ 1, p.wait_mode, p.wait_ns);
         if (prof) pb[0] += clock64() - b0;
-        if (bskipped(p, it.tile, it.kstep)) {
-          if (ptx::elect_one()) ptx::mbar_arrive(&bfull[s]);
-          __syncwarp();
-          continue;
-        }
         if (ptx::elect_one()) {
           uint8_t* st = bring + (size_t)s * BST;
           const int brow = it.kstep * p.mp + b_row0;
@@ -336,11 +434,10 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
       constexpr uint64_t LO_OFF = (uint64_t)(B_BYTES >> 4);
       int64_t gi = -1;
       unsigned long long pa[5] = {0, 0, 0, 0, 0};
-      SkipCache mskipped;
-      for (StepIter<true, false> it(p.sched, cta, SB); it.valid(); it.next()) {
+      for (KeptIter<true, false> it(p, cta, SB); it.valid(); it.next()) {
         const bool gstart = it.group_start(), gend = it.group_end();
         if (gstart) ++gi;
-        if ((it.v & 1) == mpar) {
+        if ((it.u & 1) == mpar) {
           const int s = it.s;
           const unsigned long long t0 = prof ? clock64() : 0;
           if (gstart && gi >= NACC) ptx::mbar_wait(&accempty[gi % NACC], (uint32_t)((gi / NACC - 1) & 1));
@@ -349,7 +446,7 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
           const unsigned long long t2 = prof ? clock64() : 0;
           ptx::mbar_wait(&bfull[s], it.ph);
           const unsigned long long t3 = prof ? clock64() : 0;
-          if (it.v > 0) ptx::named_bar_sync(mpar ? 1 : 2, 64);
+          if (it.u > 0) ptx::named_bar_sync(mpar ? 1 : 2, 64);
           if (prof) {
             pa[0] += t1 - t0;
             pa[1] += t2 - t1;
@@ -361,18 +458,12 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
           const uint32_t d = tmem + (uint32_t)(gi % NACC) * DW;
           const uint32_t a0 = tmem + A_COL0 + ASTRIDE * s;
           const uint64_t bdesc = desc0 + (uint64_t)((s * BST) >> 4);
-          // skipped k-steps issue nothing; the group's first issued MMA overwrites the accumulator
-          // (the flag travels with the baton: the other MMA warp reads it after its bar.sync)
-          const bool skip = mskipped(p, it.tile, it.kstep);
-          const bool live = gstart ? false : (*grp_live != 0);
-          __syncwarp();
           const bool leader = ptx::elect_one();
-          if (leader) *grp_live = (live || !skip) ? 1 : 0;
-          if (leader && !skip) {
+          if (leader) {
 #pragma unroll
             for (int kk = 0; kk < OB_K / 16; ++kk) {
               const uint64_t bd = bdesc + 2 * kk;   // +32 bytes = 16 fp16 along k
-              const uint32_t acc = (!live && kk == 0) ? 0u : 1u;
+              const uint32_t acc = (gstart && kk == 0) ? 0u : 1u;
               if (Sh::STACK) {
                 mma_f16_ts(d, a0 + 8 * kk, bd, idesc, acc);         // D += Kh [Vh; Vl]
                 mma_f16_ts(d, a0 + 32 + 8 * kk, bd, idesc, 1u);     // D += Kl [Vh; Vl]
@@ -384,7 +475,7 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
             }
           }
           __syncwarp();
-          if (it.v + 1 < it.vend) ptx::named_bar_arrive(mpar ? 2 : 1, 64);
+          if (it.has_next()) ptx::named_bar_arrive(mpar ? 2 : 1, 64);
           if (leader) ptx::tc_commit(&bempty[s]);
         }
         if (gend) {
@@ -418,8 +509,7 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&afull[buf]);
       };
-      SkipCache cskipped;
-      StepIter<false, true> it(p.sched, cta, SA, SB);
+      KeptIter<false, true> it(p, cta, SA, SB);
       for (int k = 0; k < par; ++k) it.next();
       for (; it.valid(); [&] { for (int k = 0; k < Sh::CP; ++k) it.next(); }()) {
         const int s = it.s, sb = it.sb;
@@ -443,7 +533,7 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
         const unsigned long long c0 = prof ? clock64() : 0;
         ptx::mbar_wait(&kfull[s], it.ph);
         const unsigned long long c1 = prof ? clock64() : 0;
-        if (it.v >= SB) ptx::mbar_wait(&bempty[sb], it.phb ^ 1);   // TMEM A buffer sb free
+        if (it.u >= SB) ptx::mbar_wait(&bempty[sb], it.phb ^ 1);   // TMEM A buffer sb free
         if (prof) {
           pc[0] += c1 - c0;
           pc[1] += clock64() - c1;
@@ -451,13 +541,6 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
         }
         ptx::tc_fence_after();
         const uint32_t ta = tmem + lane_base + A_COL0 + ASTRIDE * sb;
-        if (cskipped(p, it.tile, it.kstep)) {   // nothing to generate: release the slot, post the buffer
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&kempty[s]);
-          if (pend >= 0) post(pend);
-          pend = sb;
-          continue;
-        }
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           uint32_t hw[16], lw[16];
@@ -503,14 +586,13 @@ kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ C
       int64_t gi = -1;
       unsigned long long pd[2] = {0, 0};
       SegIter si(p.sched, cta);
-      SkipCache dskipped;
       int tile = 0, len = 0, seg = 0, k0 = 0;
       while (si.next(tile, len, seg, k0)) {
-        for (int g0 = 0; g0 < len; g0 += p.sched.group) {
+        const int kept = kept_count(p, tile, k0, len);   // the MMA groups cover the kept k-steps only
+        for (int g0 = 0; g0 < kept; g0 += p.sched.group) {
           ++gi;
           const int buf = (int)(gi % NACC);
-          bool any = !p.skip;   // a group whose k-steps were all skipped left the accumulator untouched
-          for (int k = g0; !any && k < g0 + p.sched.group && k < len; ++k) any = !dskipped(p, tile, k0 + k);
+          const bool any = true;
           const unsigned long long d0 = prof ? clock64() : 0;
           ptx::mbar_wait_idle(&accfull[buf], (uint32_t)((gi / NACC) & 1), p.wait_mode, p.wait_ns);
           if (prof) {
@@ -889,7 +971,8 @@ void kv_product_otf16(const KvOperand& op, int64_t m, const double* V, int64_t l
       while (v > 1 && (1 << (pw + 1)) <= v) ++pw;
       return v > 0 ? (1 << pw) : 0;
     }();
-    p.sync_k = (sc.R > 1 || (sc.R == 1 && sc.tail_total > 0)) && g_live_handles.load() <= 1 ? sync_k : 0;
+    // (none with a skip map: the kept steps differ between CTAs, so they share no epochs)
+    p.sync_k = (sc.R > 1 || (sc.R == 1 && sc.tail_total > 0)) && g_live_handles.load() <= 1 && !p.skip ? sync_k : 0;
     // stored K in several passes: every pass streams all of K; keep the passes together (64 k-steps
     // = 2 MB of K per CTA per epoch, ~60 MB across the wave: inside L2)
     static const int sync_multi = getenv("RLD_OTF_SYNC_MULTI") ? atoi(getenv("RLD_OTF_SYNC_MULTI")) : 64;
