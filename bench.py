@@ -737,7 +737,28 @@ def extra_otf(rld):
            "phase_ms_last_step": {"precond": est.phase_ms[1], "lanczos": est.phase_ms[4]},
            "roofline": roofline_otf(wl, wl.n, m, k0.elapsed_time(k1) / 10, nt),
            "parity": parity_vs_golden(wl, est.value)}
-    del R
+    del R, V
+    torch.cuda.empty_cache()
+    # config 5's kernel and points at full n = 2^20: the K.V product at the Lanczos shape (m = 128),
+    # Morton order with the far-field k-steps skipped (a full estimate takes ~34 s: not timed here)
+    wl5 = baseline(5)
+    R5 = rld.ResidentMatrix(rld.KernelMatrix(wl5.spec, wl5.points), dtype="fp32", path="on_the_fly")
+    st5 = torch.cuda.ExternalStream(R5.sess.handle.stream)
+    V5 = torch.randn(wl5.config.num_probes, wl5.n, dtype=torch.float64, device="cuda")
+    R5.kv_apply(V5)
+    torch.cuda.synchronize()
+    k0.record(st5)
+    for _ in range(3):
+        R5.kv_apply(V5)
+    k1.record(st5)
+    torch.cuda.synchronize()
+    ms5 = k0.elapsed_time(k1) / 3
+    n5, m5 = wl5.n, wl5.config.num_probes
+    out["config5_product"] = {"workload": workload_config(wl5, 1, False)["workload"], "m": m5, "ms": ms5,
+                              "dense_equiv_tflops": 2.0 * n5 * n5 * m5 / (ms5 * 1e-3) / 1e12,
+                              "what": "K.V with K generated on the fly, points in Morton order, (tile, k-step) pairs "
+                                      "with exactly-zero fp16 operands skipped (csrc/kv_otf.cu); CUDA events"}
+    del R5, V5
     torch.cuda.empty_cache()
     return out
 
