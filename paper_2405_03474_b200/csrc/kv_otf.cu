@@ -307,7 +307,13 @@ struct OtfShape {
   static constexpr uint32_t ASTRIDE = 64;           // TMEM columns per A buffer: head 32 | tail 32
   static constexpr uint32_t A_COL0 = NACC * DW;
   static constexpr int DP = NT == 64 ? 1 : 2;       // drain warps per lane quarter
-  static constexpr int CP = 4 - DP;                 // converter warps per lane quarter
+#ifndef RLD_OTF_CP128
+#define RLD_OTF_CP128 2
+#endif
+  // converter warps per lane quarter: 3 at NT = 64 (20 warps); at NT = 128 RLD_OTF_CP128 (2: 20
+  // warps, 96 registers; 3: 24 warps, 80 registers)
+  static constexpr int CP = NT == 128 ? RLD_OTF_CP128 : 4 - DP;
+  static constexpr int THREADS = 32 * (4 + 4 * (CP + DP));
   static constexpr int NABUF = (512 - (int)A_COL0) / (int)ASTRIDE < 8 ? (512 - (int)A_COL0) / (int)ASTRIDE : 8;
   static constexpr int TMEM_NEED = (int)A_COL0 + NABUF * (int)ASTRIDE;
   static constexpr uint32_t TMEM_COLS = TMEM_NEED <= 256 ? 256 : 512;
@@ -319,7 +325,7 @@ struct OtfShape {
 // DIM > 0: K tiles generated from the points; DIM == 0: stored fp32 K (tiled layout, kgen.cu), two
 // 16 KB tiles per 64-column stage, per-row power-of-two scales (the wide products of configs 2-3)
 template <int NT, int DIM, int FAM>
-__global__ void __launch_bounds__(OTF_THREADS, 1)
+__global__ void __launch_bounds__(OtfShape<NT>::THREADS, 1)
 kv_otf_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmBh,
               const __grid_constant__ CUtensorMap tmBl, const OtfParams p) {
   using Sh = OtfShape<NT>;
@@ -747,7 +753,7 @@ void launch_otf(const CUtensorMap& mP, const CUtensorMap& mBh, const CUtensorMap
   once_per_device(attr, [&] {
     RLD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem_optin()));
   });
-  kern<<<(unsigned)grid, OTF_THREADS, smem, st>>>(mP, mBh, mBl, p);
+  kern<<<(unsigned)grid, Sh::THREADS, smem, st>>>(mP, mBh, mBl, p);
   RLD_LAUNCH_CHECK();
 }
 

@@ -226,37 +226,8 @@ void allreduce_flags(rld_handle* h, int* hflags, int count) {
   }
 }
 
-// ----------------------------------------------------------------------------
-// Morton (Z-curve) order of n points in d <= 3 dimensions: 63 / d bits per coordinate over the
-// bounding box, stable in the original index
-std::vector<int> morton_order(const double* X, int64_t n, int d) {
-  const int b = 63 / d;
-  std::vector<double> lo(d, INFINITY), hi(d, -INFINITY);
-  for (int64_t i = 0; i < n; ++i)
-    for (int c = 0; c < d; ++c) {
-      lo[c] = std::min(lo[c], X[i * d + c]);
-      hi[c] = std::max(hi[c], X[i * d + c]);
-    }
-  std::vector<uint64_t> code((size_t)n);
-  const double top = std::ldexp(1.0, b) - 1.0;
-  for (int64_t i = 0; i < n; ++i) {
-    uint64_t k = 0;
-    for (int c = 0; c < d; ++c) {
-      const double span = hi[c] - lo[c];
-      const double f = span > 0 ? (X[i * d + c] - lo[c]) / span : 0.0;
-      const uint64_t q = (uint64_t)std::min(top, std::max(0.0, std::floor(f * top)));
-      for (int bit = 0; bit < b; ++bit) k |= ((q >> bit) & 1ull) << (bit * d + c);
-    }
-    code[(size_t)i] = k;
-  }
-  std::vector<int> pm((size_t)n);
-  for (int64_t i = 0; i < n; ++i) pm[(size_t)i] = (int)i;
-  std::stable_sort(pm.begin(), pm.end(), [&](int a, int c) { return code[(size_t)a] < code[(size_t)c]; });
-  return pm;
-}
-
-// Locality order for the points: the float64 stored product on int8 slices (the only one that skips
-// all-zero blocks), one GPU, d <= 3; RLD_SORT=0 keeps the given order.
+// Locality order (Morton, morton_order_device) for the points of the products that skip exactly-zero
+// work: one GPU, d <= 3; RLD_SORT=0 keeps the given order.
 bool sort_points(const rld_handle* h, const rld_problem* p) {
   const char* e = getenv("RLD_SORT");
   if (e && e[0] == '0') return false;
@@ -317,17 +288,11 @@ void prepare(rld_handle* h, const rld_problem* p) {
       // the diagonal small, and their leading slices all zero, which the product skips (kv_ozaki.cu).
       // Every n-vector entering or leaving the resident frame is permuted (probes, sketch rows, the
       // rank-one start, kv_apply / precond_apply operands); pivot ties go to the original index.
-      std::vector<double> hx((size_t)p->n * p->d), hxp((size_t)p->n * p->d);
-      RLD_CUDA(cudaMemcpyAsync(hx.data(), p->data, xb,
-                               p->data_memory == RLD_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost, st));
-      RLD_CUDA(cudaStreamSynchronize(st));
-      std::vector<int> pm = morton_order(hx.data(), p->n, p->d);
-      for (int64_t i = 0; i < p->n; ++i)
-        for (int c = 0; c < p->d; ++c) hxp[(size_t)i * p->d + c] = hx[(size_t)pm[i] * p->d + c];
+      h->wk.ptmp.reserve(xb);   // the caller's points on the device, then sorted into r.X
+      RLD_CUDA(cudaMemcpyAsync(h->wk.ptmp.ptr, p->data, xb,
+                               p->data_memory == RLD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
       r.perm.reserve(sizeof(int) * p->n);
-      RLD_CUDA(cudaMemcpyAsync(r.perm.ptr, pm.data(), sizeof(int) * p->n, cudaMemcpyHostToDevice, st));
-      RLD_CUDA(cudaMemcpyAsync(r.X.ptr, hxp.data(), xb, cudaMemcpyHostToDevice, st));
-      RLD_CUDA(cudaStreamSynchronize(st));   // host buffers go out of scope
+      morton_order_device(h->wk.ptmp.as<double>(), p->n, p->d, r.perm.as<int>(), r.X.as<double>(), h->wk.scratch2, st);
       r.permuted = true;
     } else {
       RLD_CUDA(cudaMemcpyAsync(r.X.ptr, p->data, xb,

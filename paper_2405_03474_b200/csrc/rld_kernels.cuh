@@ -93,6 +93,8 @@ void precond_base_scaled(int64_t n, int k, double scale, double* A, double* base
                          cudaStream_t st);
 void argmax_first(int64_t n, const double* d, int64_t offset, double* out, DevBuf& scratch, cudaStream_t st,
                   const int* perm = nullptr);
+// Morton order of n device points (d <= 3): perm[i] = original index of point i, Xs the sorted points
+void morton_order_device(const double* X, int64_t n, int d, int* perm, double* Xs, DevBuf& scratch, cudaStream_t st);
 // m rows of length n: gather dst[c][i] = src[c][perm[i]], or scatter dst[c][perm[i]] = src[c][i]
 void permute_rows(int64_t m, int64_t n, const int* perm, const double* src, int64_t lds, double* dst, int64_t ldd,
                   bool scatter, cudaStream_t st);

@@ -6,6 +6,11 @@
 #include "rld_device.cuh"
 #include "rld_kernels.cuh"
 
+#include <thrust/device_ptr.h>
+#include <thrust/execution_policy.h>
+#include <thrust/sequence.h>
+#include <thrust/sort.h>
+
 namespace rld {
 
 namespace {
@@ -1000,6 +1005,89 @@ void permute_rows(int64_t m, int64_t n, const int* perm, const double* src, int6
   if (m <= 0 || n <= 0) return;
   const dim3 g((unsigned)std::min<int64_t>(ceil_div(n, 256), 1024), (unsigned)m);
   permute_rows_kernel<<<g, 256, 0, st>>>(m, n, perm, src, lds, dst, ldd, scatter ? 1 : 0);
+  RLD_LAUNCH_CHECK();
+}
+}  // namespace rld
+
+namespace rld {
+namespace {
+// per-dimension bounding box of n points (one block): box[c] = min, box[4 + c] = max
+__global__ void morton_box_kernel(const double* __restrict__ X, int64_t n, int d, double* __restrict__ box) {
+  __shared__ double lo[4][32], hi[4][32];
+  double l[4], h[4];
+  for (int c = 0; c < 4; ++c) {
+    l[c] = INFINITY;
+    h[c] = -INFINITY;
+  }
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+    for (int c = 0; c < d; ++c) {
+      const double x = X[i * d + c];
+      l[c] = fmin(l[c], x);
+      h[c] = fmax(h[c], x);
+    }
+  for (int c = 0; c < 4; ++c)
+    for (int o = 16; o > 0; o >>= 1) {
+      l[c] = fmin(l[c], __shfl_xor_sync(0xffffffffu, l[c], o));
+      h[c] = fmax(h[c], __shfl_xor_sync(0xffffffffu, h[c], o));
+    }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+    for (int c = 0; c < 4; ++c) {
+      lo[c][w] = l[c];
+      hi[c][w] = h[c];
+    }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    double a = INFINITY, b = -INFINITY;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+      a = fmin(a, lo[threadIdx.x][k]);
+      b = fmax(b, hi[threadIdx.x][k]);
+    }
+    box[threadIdx.x] = a;
+    box[4 + threadIdx.x] = b;
+  }
+}
+
+// Z-curve code: 63 / d bits per coordinate over the box, interleaved
+__global__ void morton_code_kernel(const double* __restrict__ X, int64_t n, int d, const double* __restrict__ box,
+                                   unsigned long long* __restrict__ code, int* __restrict__ idx) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int b = 63 / d;
+  const double top = ldexp(1.0, b) - 1.0;
+  unsigned long long k = 0;
+  for (int c = 0; c < d; ++c) {
+    const double span = box[4 + c] - box[c];
+    const double f = span > 0 ? (X[i * d + c] - box[c]) / span : 0.0;
+    const unsigned long long q = (unsigned long long)fmin(top, fmax(0.0, floor(f * top)));
+    for (int bit = 0; bit < b; ++bit) k |= ((q >> bit) & 1ull) << (bit * d + c);
+  }
+  code[i] = k;
+  idx[i] = (int)i;
+}
+
+__global__ void gather_points_kernel(const double* __restrict__ X, int64_t n, int d, const int* __restrict__ perm,
+                                     double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * d) return;
+  const int64_t i = e / d;
+  out[e] = X[(int64_t)perm[i] * d + (e - i * d)];
+}
+}  // namespace
+
+// Morton (Z-curve) order of n device points (d <= 3), stable: perm[i] = original index of point i;
+// Xs = the points in that order.  scratch holds the codes.
+void morton_order_device(const double* X, int64_t n, int d, int* perm, double* Xs, DevBuf& scratch, cudaStream_t st) {
+  scratch.reserve(sizeof(unsigned long long) * (n + 1) + sizeof(double) * 8);
+  double* box = scratch.as<double>();
+  unsigned long long* code = reinterpret_cast<unsigned long long*>(box + 8);
+  morton_box_kernel<<<1, 1024, 0, st>>>(X, n, d, box);
+  RLD_LAUNCH_CHECK();
+  morton_code_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(X, n, d, box, code, perm);
+  RLD_LAUNCH_CHECK();
+  thrust::stable_sort_by_key(thrust::cuda::par.on(st), thrust::device_pointer_cast(code),
+                             thrust::device_pointer_cast(code + n), thrust::device_pointer_cast(perm));
+  gather_points_kernel<<<(unsigned)ceil_div(n * d, 256), 256, 0, st>>>(X, n, d, perm, Xs);
   RLD_LAUNCH_CHECK();
 }
 }  // namespace rld
