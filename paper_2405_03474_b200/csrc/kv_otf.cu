@@ -1026,8 +1026,13 @@ void kv_product_otf16(const KvOperand& op, int64_t m, const double* V, int64_t l
     RLD_CUDA(cudaMemcpyAsync(h.data(), prof_buf.ptr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, st));
     RLD_CUDA(cudaStreamSynchronize(st));
     double a[16] = {0};
-    for (int64_t c = 0; c < grid; ++c)
+    double tmax = 0.0, tmin = 1e300;
+    for (int64_t c = 0; c < grid; ++c) {
       for (int k = 0; k < 16; ++k) a[k] += (double)h[c * 16 + k];
+      tmax = std::max(tmax, (double)h[c * 16 + 13]);
+      tmin = std::min(tmin, (double)h[c * 16 + 13]);
+    }
+    fprintf(stderr, "[kv_otf prof] CTA cycles: min %.3g avg %.3g max %.3g\n", tmin, a[13] / grid, tmax);
     const double ms = a[4] > 0 ? a[4] : 1, cs = a[7] > 0 ? a[7] : 1, ds = a[10] > 0 ? a[10] : 1;
     const double steps = (double)total * npass / grid;   // k-steps per CTA
     fprintf(stderr,

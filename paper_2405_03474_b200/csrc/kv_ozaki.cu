@@ -5,8 +5,8 @@
 // Slicing (exact, deterministic):
 //   each row i of K gets sigma_i = 2^e with 2 max_j |K_ij| < sigma_i <= 4 max_j |K_ij|, each vector
 //   c of V gets tau_c likewise; x = K_ij / sigma_i in (-1/2, 1/2) is cut into S = 8 signed digits
-//   d_s = rint(128 r_s), r_0 = x, r_{s+1} = 128 r_s - d_s (every step exact in float64):
-//       K_ij = sigma_i (sum_s d_s 2^{-7 (s+1)} + r_8 2^{-56}),   |d_s| <= 64,  |r_8| <= 1/2
+//   of the integer rint(x 2^56) (digits8: balanced base 128, d_7..d_1 in [-64, 63], d_0 in [-64, 64]):
+//       K_ij = sigma_i (sum_s d_s 2^{-7 (s+1)} + rho 2^{-56}),   |d_s| <= 64,  |rho| <= 1/2
 //   (round-to-nearest digits leave unbiased remainders, so the dropped terms do not add up
 //   coherently over the n-term sums).
 //   Then (K V^T)_ic = sigma_i tau_c sum_{s+t <= 7} 2^{-7 (s+t+2)} sum_j d_s[i,j] e_t[c,j] + err,
@@ -107,6 +107,27 @@ __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint
 // in rows 4..7 of every 8-row atom) the UMMA descriptor expects -- so a stage is ONE bulk copy.
 // Rows >= rows and columns >= n are zero.
 
+// The 8 signed base-128 digits of x (|x| < 1/2): K = rint(x 2^56) (x 2^56 is exact in float64 or
+// rounds once; |K| < 2^55), then balanced digits from the bottom, d_s in [-64, 63] for s = 7..1 and
+// the top d_0 = what remains, in [-64, 64]:  x = sum_s d_s 2^{-7(s+1)} + rho 2^-56, |rho| <= 1/2.
+// Integer work on the ALU pipe (one F2I per entry): the float64 rint recursion it replaces kept the
+// XU pipe busy with 8 rounds and 8 conversions per entry.  Also returns K' = sum_{s<7} d_s 128^{6-s}
+// (the CRT integer, kv_crt.cu) and 8 - the number of leading zero digits.
+__device__ __forceinline__ void digits8(double x, int (&d)[OZ_S], long long& kprime, int& nz) {
+  long long k = __double2ll_rn(x * 72057594037927936.0);   // x 2^56
+  nz = 0;
+#pragma unroll
+  for (int s = OZ_S - 1; s >= 1; --s) {
+    const int dd = (int)((k + 64) & 127) - 64;
+    d[s] = dd;
+    k = (k - dd) >> 7;   // exact
+    if (s == OZ_S - 1) kprime = k;
+    if (dd != 0) nz = OZ_S - s;
+  }
+  d[0] = (int)k;
+  if (k != 0) nz = OZ_S;
+}
+
 // scale[row] = sigma = 2^e with 2 max_j |A_row,j| < sigma <= 4 max (1 for an all-zero row)
 __global__ void ozaki_scale_kernel(const double* __restrict__ A, int64_t lda, int64_t n, double* __restrict__ scale) {
   const int64_t row = blockIdx.x;
@@ -146,13 +167,14 @@ __global__ void ozaki_digits_kernel(const double* __restrict__ A, int64_t lda, i
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
       const int64_t j = j0 + k;
-      double r = (row < rows && j < n) ? ldexp(A[row * lda + j], 1 - ee) : 0.0;
+      const double r = (row < rows && j < n) ? ldexp(A[row * lda + j], 1 - ee) : 0.0;
+      int dg[OZ_S];
+      long long kp;
+      int nzk;
+      digits8(r, dg, kp, nzk);
 #pragma unroll
       for (int s = 0; s < OZ_S; ++s) {
-        const double x = r * 128.0;   // exact
-        const double d = rint(x);     // |d| <= 64 (|r| <= 1/2 throughout)
-        r = x - d;                    // exact
-        const uint32_t b = (uint32_t)(uint8_t)(int8_t)(int)d;
+        const uint32_t b = (uint32_t)(uint8_t)(int8_t)dg[s];
         if ((k & 3) == 0) w[s][k >> 2] = b;
         else w[s][k >> 2] |= b << (8 * (k & 3));
       }
@@ -220,20 +242,18 @@ ozaki_points_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, in
           v = kernel_value_f64(kp, r2);
         }
       }
-      double r = v * scl;
-      double kd = 0.0;   // K' (exact in float64: |K'| < 2^48.02)
+      int dg[OZ_S];
+      long long kp;
+      int nzk;
+      digits8(v * scl, dg, kp, nzk);
+      if (nzk > nz) nz = nzk;
 #pragma unroll
       for (int s = 0; s < OZ_S; ++s) {
-        const double x = r * 128.0;
-        const double dg = rint(x);
-        r = x - dg;
-        if (CRT && s < CRT_SLICES) kd = fma(kd, 128.0, dg);
-        if (dg != 0.0 && nz < OZ_S - s) nz = OZ_S - s;
-        const uint32_t b = (uint32_t)(uint8_t)(int8_t)(int)dg;
+        const uint32_t b = (uint32_t)(uint8_t)(int8_t)dg[s];
         if ((k & 3) == 0) w[s][k >> 2] = b;
         else w[s][k >> 2] |= b << (8 * (k & 3));
       }
-      if (CRT) kq[k] = __double2ll_rn(kd);
+      if (CRT) kq[k] = kp;
     }
     // a warp holds 8 rows x 4 column parts of one (tile, k-step) block: reduce, one atomic per warp
     if (knz) {
