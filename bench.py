@@ -481,6 +481,7 @@ def run_ours(args):
     # ---- extra: config 4 at full n on the fly (fp32, fp16 3-term tensor-core products)
     if args.config == 3 and cfg.dtype == "fp64" and not args.no_extra and world == 1:
         line["extra_otf"] = extra_otf(rld)
+        line["extra_e2e_dense"] = extra_e2e_dense(rld)
 
     # ---- CPU baseline (rank 0, N = 1 only)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -759,6 +760,63 @@ def extra_otf(rld):
                               "what": "K.V with K generated on the fly, points in Morton order, (tile, k-step) pairs "
                                       "with exactly-zero fp16 operands skipped (csrc/kv_otf.cu); CUDA events"}
     del R5, V5
+    torch.cuda.empty_cache()
+    return out
+
+
+def extra_e2e_dense(rld):
+    """The reference's callers pass a dense float64 M: BASELINE config 2 (n = 16384, 2.15 GB) from
+    pinned host memory through rld_logdet every step -- the H2D copy, the int8 slice image and CRT
+    residues of M, the estimate and the read-back are all inside the timed region (CUDA events on
+    the handle's stream; 1 warm-up, 3 steps)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2405_03474_b200 import _native as N
+    from paper_2405_03474_b200._session import Session
+    from paper_2405_03474_b200.estimators import make_config
+    from paper_2405_03474_b200.workloads import baseline
+
+    wl = baseline(2, dtype="fp64")
+    cfg = replace(wl.config, dtype="fp64", path="stored")
+    Kd = rld.build_covariance(wl.spec, wl.points, dtype="fp64")
+    Kh = torch.empty(Kd.shape, dtype=torch.float64, pin_memory=True)
+    Kh.copy_(Kd)
+    del Kd
+    torch.cuda.empty_cache()
+    sess = Session()
+    prob, keep = sess.problem_for(Kh, "fp64", "stored")
+    c = make_config(cfg, wl.n)
+    inp = N.Inputs()
+    inp.memory = N.HOST
+    per = np.empty(cfg.num_probes)
+    res = N.Result()
+    res.per_probe = per.ctypes.data_as(C.POINTER(C.c_double))
+
+    def step():
+        sess.handle.check(sess.lib.rld_logdet(sess.handle.ptr, C.byref(prob), C.byref(c), C.byref(inp), C.byref(res)),
+                          "rld_logdet")
+
+    step()
+    stream = torch.cuda.ExternalStream(sess.handle.stream)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    K = 3
+    for _ in range(K):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / K
+    out = {"value": 1e3 / ms, "unit": UNIT, "ms_per_step": ms, "dtype": "f64",
+           "config": {"workload": workload_config(wl, 1, False)["workload"].replace("stored K", "dense host M"),
+                      "input": "dense float64 M (2.15 GB) in pinned host memory, copied every step"},
+           "h2d_bytes_per_step": int(8 * wl.n * wl.n), "d2h_bytes_per_step": int(8 * (cfg.num_probes + 3)),
+           "phase_ms_last_step": {"precond": res.phase_ms[1], "lanczos": res.phase_ms[4],
+                                  "h2d_and_prepare": ms - res.phase_ms[7]},
+           "parity": parity_vs_golden(replace(wl, config=cfg), res.value)}
+    del keep, Kh
     torch.cuda.empty_cache()
     return out
 
