@@ -23,7 +23,14 @@ namespace rld {
 namespace {
 
 namespace cg = cooperative_groups;
-constexpr int TCL = 16, TT = 256, TNMAX = 288, TRPC = TNMAX / TCL;   // 18 rows per CTA
+constexpr int TCL = 16, TT = 256, TNMAX = 288;
+// Two instantiations: n <= 288 (256 threads, 18 rows per CTA) and n <= 544 (192 threads, 34 rows
+// per CTA: 148 KB of rows + the per-warp v / w slots + the broadcast columns fill the 227 KB)
+constexpr int TNMAX_L = 544, TT_L = 192;
+template <int NMAX, int TTH>
+constexpr size_t tridiag_smem_t() {
+  return sizeof(double) * ((size_t)((NMAX + TCL - 1) / TCL) * NMAX + (size_t)(TTH / 32) * 2 * NMAX + 4 * (size_t)NMAX);
+}
 
 // sqrt and reciprocal on the per-column chain from the MUFU approximations plus two Newton steps
 // (~1 ulp): the IEEE FP64 sqrt / division sequences are several times longer.  Normal inputs only
@@ -52,18 +59,20 @@ __device__ __forceinline__ double rcp_nr(double x) {
 // rows (the rank-2 update) from a per-warp shared slot.  Owners broadcast p = tau A v and their
 // raw entries of the next column through DSMEM; the next column is rebuilt locally from them.
 // (0.63 ms vs 0.89 ms for the block-barrier version at n = 266: scripts/tridiag_bench3.cu.)
-__global__ void __launch_bounds__(TT)
+template <int NMAX, int TTH>
+__global__ void __launch_bounds__(TTH)
 tridiag_kernel(int n, const double* __restrict__ A, double* __restrict__ d, double* __restrict__ e,
                double* __restrict__ tau_out, double* __restrict__ V) {
-  constexpr int K = TNMAX / 32, W = TT / 32;
+  constexpr int K = NMAX / 32, W = TTH / 32, TT = TTH, TNMAX = NMAX, TRPC = (NMAX + TCL - 1) / TCL;
+  static_assert(NMAX % 32 == 0, "NMAX must be a multiple of 32");
   cg::cluster_group cl = cg::this_cluster();
   const int r = (int)cl.block_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   extern __shared__ double sm[];
   double (*rows)[TNMAX] = reinterpret_cast<double (*)[TNMAX]>(sm);                  // [TRPC][TNMAX]
   double (*vw)[2][TNMAX] = reinterpret_cast<double (*)[2][TNMAX]>(sm + TRPC * TNMAX);  // [W][2][TNMAX]
-  __shared__ double col[2][TNMAX];   // raw broadcast column (before this column's correction)
-  __shared__ double pv[2][TNMAX];    // broadcast p = tau A v
+  double (*col)[TNMAX] = reinterpret_cast<double (*)[TNMAX]>(sm + (TRPC + 2 * W) * TNMAX);  // [2][TNMAX] raw broadcast column
+  double (*pv)[TNMAX] = col + 2;     // [2][TNMAX] broadcast p = tau A v
   const int nr = (n - r + TCL - 1) / TCL;
   for (int q = 0; q < nr; ++q)
     for (int c = tid; c < n; c += TT) rows[q][c] = A[(size_t)(r + q * TCL) * n + c];
@@ -313,7 +322,8 @@ __global__ void bisect_kernel(int n, const double* __restrict__ d, const double*
   if (lane == 0) lam[k] = 0.5 * (lo + hi) / sc;
 }
 
-constexpr int IV_T = 16;   // eigenvalues (threads) per inverse-iteration CTA
+// eigenvalues (threads) per inverse-iteration CTA: 16 for n <= 288, 8 above (the per-thread
+// factors take 5 n doubles of shared memory)
 
 // eigenvector k of T by inverse iteration on the unreduced block of T that owns eigenvalue k
 // (LAPACK dstein style).  Ownership (only when T splits): the eigenvalues within +-delta of lam[k]
@@ -324,6 +334,7 @@ constexpr int IV_T = 16;   // eigenvalues (threads) per inverse-iteration CTA
 // the block.  The factors and the iterate live in shared memory, interleaved over the CTA's 16
 // threads ([field][row][thread]: conflict-free), so the serial recurrences run at shared-memory
 // latency.
+template <int IV_T>
 __global__ void __launch_bounds__(IV_T)
 inviter_kernel(int n, const double* __restrict__ d, const double* __restrict__ e, const double* __restrict__ lam,
                double* __restrict__ Z) {
@@ -452,19 +463,19 @@ inviter_kernel(int n, const double* __restrict__ d, const double* __restrict__ e
 #undef PB
 }
 
-size_t tridiag_smem() { return sizeof(double) * ((size_t)TRPC * TNMAX + (size_t)(TT / 32) * 2 * TNMAX); }
-
-size_t inviter_smem(int n) {
-  return sizeof(double) * (3 * (size_t)n + (size_t)5 * n * IV_T) + sizeof(unsigned) * ((n + 31) / 32) * IV_T;
+size_t inviter_smem(int n, int iv_t) {
+  return sizeof(double) * (3 * (size_t)n + (size_t)5 * n * iv_t) + sizeof(unsigned) * ((n + 31) / 32) * iv_t;
 }
 
 // Compact-WY factors of the reflectors in chunks of FQ_C (LAPACK dlarft, forward / columnwise):
 // H_j0 ... H_{j0+C-1} = I - V_c T_c V_c^T with T_c upper triangular, T_jj = tau_j,
 // T[0:j, j] = -tau_j T[0:j, 0:j] (V_c^T v_j)[0:j].  One CTA per chunk.
 constexpr int FQ_C = 16;
+template <int TNMAX>
 __global__ void __launch_bounds__(TT)
 wy_t_kernel(int n, const double* __restrict__ V, const double* __restrict__ tau, double* __restrict__ Tout) {
-  __shared__ double vs[FQ_C][TNMAX];
+  extern __shared__ double vs_dyn[];
+  double (*vs)[TNMAX] = reinterpret_cast<double (*)[TNMAX]>(vs_dyn);   // [FQ_C][TNMAX]
   __shared__ double g[FQ_C][FQ_C + 1];
   __shared__ double tt[FQ_C][FQ_C + 1];
   const int j0 = blockIdx.x * FQ_C;
@@ -508,9 +519,11 @@ wy_t_kernel(int n, const double* __restrict__ V, const double* __restrict__ tau,
 // independent (their butterfly reductions interleave) instead of one serial reduction per
 // reflector.  Each warp carries FQ_R rows; V_c and T_c are staged in shared memory for the CTA.
 constexpr int FQ_R = 2;
+template <int TNMAX>
 __global__ void __launch_bounds__(TT)
 formq_kernel(int n, const double* __restrict__ V, const double* __restrict__ Tw, double* __restrict__ Q) {
-  __shared__ double vs[FQ_C][TNMAX];
+  extern __shared__ double vs_dyn[];
+  double (*vs)[TNMAX] = reinterpret_cast<double (*)[TNMAX]>(vs_dyn);   // [FQ_C][TNMAX]
   __shared__ double ts[FQ_C][FQ_C];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int row0 = (blockIdx.x * (TT / 32) + warp) * FQ_R;
@@ -600,6 +613,51 @@ __global__ void __launch_bounds__(1024) orth_defect_kernel(int n, const double* 
   }
 }
 
+template <int NMAX, int TTH, int IVT>
+void tri_eigh_launch(int n, const double* A, double* w, double* d, double* e, double* tau, double* V, double* Z,
+                     double* Q, double* Tw, cudaStream_t st, cudaStream_t st2, cudaEvent_t fork, cudaEvent_t join) {
+  constexpr size_t tsm = tridiag_smem_t<NMAX, TTH>();
+  const size_t vsm = sizeof(double) * FQ_C * NMAX;
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [&] {
+    RLD_CUDA(cudaFuncSetAttribute(tridiag_kernel<NMAX, TTH>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    RLD_CUDA(cudaFuncSetAttribute(tridiag_kernel<NMAX, TTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+    RLD_CUDA(cudaFuncSetAttribute(inviter_kernel<IVT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)inviter_smem(NMAX, IVT)));
+    RLD_CUDA(cudaFuncSetAttribute(wy_t_kernel<NMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsm));
+    RLD_CUDA(cudaFuncSetAttribute(formq_kernel<NMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsm));
+  });
+  {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(TCL);
+    cfg.blockDim = dim3(TTH);
+    cfg.dynamicSmemBytes = tsm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = TCL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    RLD_CUDA(cudaLaunchKernelEx(&cfg, tridiag_kernel<NMAX, TTH>, n, A, d, e, tau, V));
+    RLD_LAUNCH_CHECK();
+  }
+  // Q (reflectors -> WY -> rows of Q) on the side stream, overlapping the eigenvalue and
+  // eigenvector kernels of T on `st`; joined by the caller
+  RLD_CUDA(cudaEventRecord(fork, st));
+  RLD_CUDA(cudaStreamWaitEvent(st2, fork, 0));
+  wy_t_kernel<NMAX><<<(unsigned)ceil_div(n - 2, FQ_C), TT, vsm, st2>>>(n, V, tau, Tw);
+  RLD_LAUNCH_CHECK();
+  formq_kernel<NMAX><<<(unsigned)ceil_div(n, (TT / 32) * FQ_R), TT, vsm, st2>>>(n, V, Tw, Q);
+  RLD_LAUNCH_CHECK();
+  RLD_CUDA(cudaEventRecord(join, st2));
+  bisect_kernel<<<(unsigned)ceil_div(32 * (int64_t)n, 256), 256, sizeof(double) * 2 * n, st>>>(n, d, e, w);
+  RLD_LAUNCH_CHECK();
+  inviter_kernel<IVT><<<(unsigned)ceil_div(n, IVT), IVT, inviter_smem(n, IVT), st>>>(n, d, e, w, Z);
+  RLD_LAUNCH_CHECK();
+}
+
 }  // namespace
 
 void orth_defect(int n, const double* G, double* out, cudaStream_t st) {
@@ -610,7 +668,7 @@ void orth_defect(int n, const double* G, double* out, cudaStream_t st) {
 bool tri_eigh(int n, const double* A, double* w, DevBuf& scratch, double** Zout, double** Qout, double** spare,
               cudaStream_t st, cudaStream_t st2, cudaEvent_t fork, cudaEvent_t join) {
   static const int env = getenv("RLD_TRI_EIG") ? atoi(getenv("RLD_TRI_EIG")) : 1;
-  if (!env || n < 3 || n > TNMAX) return false;
+  if (!env || n < 3 || n > TNMAX_L) return false;
   // scratch: d e tau | V (n x n) | Z (n x n) | Q (n x n) | WY factors (n x n) | spare (3 n x n)
   const size_t nn = (size_t)n * n;
   scratch.reserve(sizeof(double) * (3 * (size_t)n + 7 * nn));
@@ -621,43 +679,11 @@ bool tri_eigh(int n, const double* A, double* w, DevBuf& scratch, double** Zout,
   double* Z = V + nn;
   double* Q = Z + nn;
   double* work = Q + nn;
-  static std::atomic<uint64_t> attr{0};
-  once_per_device(attr, [&] {
-    RLD_CUDA(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    RLD_CUDA(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)tridiag_smem()));
-    RLD_CUDA(cudaFuncSetAttribute(inviter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)inviter_smem(TNMAX)));
-  });
-  {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(TCL);
-    cfg.blockDim = dim3(TT);
-    cfg.dynamicSmemBytes = tridiag_smem();
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = TCL;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    RLD_CUDA(cudaLaunchKernelEx(&cfg, tridiag_kernel, n, A, d, e, tau, V));
-    RLD_LAUNCH_CHECK();
-  }
-  // Q (reflectors -> WY -> rows of Q) on the side stream, overlapping the eigenvalue and
-  // eigenvector kernels of T on `st`; joined before returning
-  RLD_CUDA(cudaEventRecord(fork, st));
-  RLD_CUDA(cudaStreamWaitEvent(st2, fork, 0));
   double* Tw = work;   // compact-WY T factors, FQ_C^2 per chunk (<= n^2 in all)
-  wy_t_kernel<<<(unsigned)ceil_div(n - 2, FQ_C), TT, 0, st2>>>(n, V, tau, Tw);
-  RLD_LAUNCH_CHECK();
-  formq_kernel<<<(unsigned)ceil_div(n, (TT / 32) * FQ_R), TT, 0, st2>>>(n, V, Tw, Q);
-  RLD_LAUNCH_CHECK();
-  RLD_CUDA(cudaEventRecord(join, st2));
-  bisect_kernel<<<(unsigned)ceil_div(32 * (int64_t)n, 256), 256, sizeof(double) * 2 * n, st>>>(n, d, e, w);
-  RLD_LAUNCH_CHECK();
-  inviter_kernel<<<(unsigned)ceil_div(n, IV_T), IV_T, inviter_smem(n), st>>>(n, d, e, w, Z);
-  RLD_LAUNCH_CHECK();
+  if (n <= TNMAX)
+    tri_eigh_launch<TNMAX, TT, 16>(n, A, w, d, e, tau, V, Z, Q, Tw, st, st2, fork, join);
+  else
+    tri_eigh_launch<TNMAX_L, TT_L, 8>(n, A, w, d, e, tau, V, Z, Q, Tw, st, st2, fork, join);
   RLD_CUDA(cudaStreamWaitEvent(st, join, 0));
   *Zout = Z;
   *Qout = Q;

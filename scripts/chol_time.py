@@ -11,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2405_03474_b200._session import session  # noqa: E402
 
 s = session()
-for n in (74, 256, 266, 522, 640):
+for n in [int(a) for a in sys.argv[1:]] or (74, 256, 266, 512, 522, 640, 1024, 2048):
     g = np.random.default_rng(n)
     X = g.standard_normal((n + 8, n))
     G0 = torch.from_numpy(X.T @ X).cuda()

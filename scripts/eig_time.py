@@ -1,4 +1,4 @@
-"""Time rld_dense_eigh (one-cluster Jacobi, or DSYEVD with RLD_SMALL_EIG=0) at the preconditioner sizes."""
+"""Time rld_dense_eigh (tri_eig.cu, or DSYEVD with RLD_TRI_EIG=0) at the preconditioner sizes (argv: sizes)."""
 import os
 import sys
 import time
@@ -10,7 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2405_03474_b200._session import session  # noqa: E402
 
 s = session()
-for n in (74, 256, 266, 288):
+for n in [int(a) for a in sys.argv[1:]] or (74, 256, 266, 288, 512, 522, 544, 1034, 2058):
     g = np.random.default_rng(n)
     Q, _ = np.linalg.qr(g.standard_normal((n, n)))
     A0 = torch.from_numpy((Q * np.logspace(4, -2, n)) @ Q.T).cuda()

@@ -729,11 +729,11 @@ def _dense_eigh(A):
     return w.cpu().numpy(), t.cpu().numpy().T   # column j of the column-major result <-> w[j]
 
 
-@pytest.mark.parametrize("n", [2, 3, 10, 64, 74, 256, 266, 288, 300])
+@pytest.mark.parametrize("n", [2, 3, 10, 64, 74, 256, 266, 288, 300, 512, 522, 544, 560])
 @pytest.mark.parametrize("spectrum", ["wishart", "decaying", "degenerate", "rank_deficient", "indefinite",
                                       "clustered", "diagonal"])
 def test_dense_eigh_matches_lapack(rld, n, spectrum):
-    """The preconditioner's symmetric eigensolver (tri_eig.cu for 3 <= n <= 288, DSYEVD otherwise
+    """The preconditioner's symmetric eigensolver (tri_eig.cu for 3 <= n <= 544, DSYEVD otherwise
     and as the fallback on degenerate unreduced blocks) against LAPACK eigh: eigenvalues,
     reconstruction, orthogonality, and the top-half spectral projector (eigenvectors are defined
     up to sign / rotation inside degenerate eigenspaces)."""
