@@ -80,8 +80,11 @@ template <int BM, int BN>
 __global__ void __launch_bounds__(DM_THREADS, DmmaShape<BM, BN>::MIN_BLOCKS)
 gemm_nt_dmma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int64_t p,
                     int64_t q, int64_t n, int64_t kchunk, double* __restrict__ out, int64_t ldo,
-                    int64_t split_stride) {
+                    int64_t split_stride, int sym) {
   using S = DmmaShape<BM, BN>;
+  // symmetric (A == B, a Gram): tiles wholly above the diagonal (every c > i) are mirrored by the
+  // reduce instead of computed
+  if (sym && (int64_t)blockIdx.x * BN >= (int64_t)blockIdx.y * BM + BM) return;
   extern __shared__ __align__(1024) unsigned char dm_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(dm_smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -173,14 +176,19 @@ gemm_nt_dmma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
   }
 }
 
-// out[c * ldo + r] = beta * out + sum_{s < splits} part[s * stride + c * p + r]   (fixed order)
+// out[c * ldo + r] = beta * out + sum_{s < splits} part[s * stride + c * p + r]   (fixed order);
+// sym_bm > 0: entries of the skipped tiles (c >= (r / sym_bm + 1) sym_bm, column tiles of sym_bn)
+// come from their mirror (r, c)
 __global__ void dmma_split_reduce_kernel(const double* __restrict__ part, int splits, int64_t stride, int64_t q,
-                                         int64_t p, double* __restrict__ out, int64_t ldo, double beta) {
+                                         int64_t p, double* __restrict__ out, int64_t ldo, double beta, int sym_bm,
+                                         int sym_bn) {
   const int64_t total = q * p;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int k = 0; k < splits; ++k) s += part[k * stride + e];
     const int64_t c = e / p, r = e % p;
+    int64_t src = e;
+    if (sym_bm > 0 && (c / sym_bn) * sym_bn >= (r / sym_bm + 1) * sym_bm) src = r * p + c;
+    double s = 0.0;
+    for (int k = 0; k < splits; ++k) s += part[k * stride + src];
     double* d = out + c * ldo + r;
     *d = beta == 0.0 ? s : beta * *d + s;
   }
@@ -365,7 +373,7 @@ int64_t choose_splits(int64_t tiles, int64_t n, int64_t slots) {
 
 template <int BM, int BN>
 void launch_nt(const double* A, int64_t lda, int64_t p, const double* B, int64_t ldb, int64_t q, int64_t n,
-               double* C, int64_t ldc, double beta, DevBuf& partial, cudaStream_t st) {
+               double* C, int64_t ldc, double beta, DevBuf& partial, cudaStream_t st, bool sym) {
   using S = DmmaShape<BM, BN>;
   static std::atomic<uint64_t> attr{0};
   once_per_device(attr, [&] {
@@ -373,24 +381,30 @@ void launch_nt(const double* A, int64_t lda, int64_t p, const double* B, int64_t
   });
   const CUtensorMap ma = map_f64(A, n, p, lda, BM);
   const CUtensorMap mb = map_f64(B, n, q, ldb, BN);
-  const int64_t tiles = ceil_div(p, BM) * ceil_div(q, BN);
+  int64_t tiles = ceil_div(p, BM) * ceil_div(q, BN);
+  if (sym) {   // computed tiles only
+    tiles = 0;
+    for (int64_t ty = 0; ty < ceil_div(p, BM); ++ty)
+      for (int64_t tx = 0; tx < ceil_div(q, BN); ++tx) tiles += (tx * BN < ty * BM + BM);
+  }
   const int64_t splits_req = choose_splits(tiles, n, (int64_t)dm_sms() * S::MIN_BLOCKS);
   const int64_t kchunk = ceil_div(ceil_div(n, splits_req), DM_BK) * DM_BK;
   const int64_t splits = ceil_div(n, kchunk);
   dim3 grid((unsigned)ceil_div(q, BN), (unsigned)ceil_div(p, BM), (unsigned)splits);
   if (grid.y > 65535u) fail(RLD_ERR_NOT_SUPPORTED, "gemm_nt_f64: too many row tiles");
-  if (splits == 1 && beta == 0.0) {
-    gemm_nt_dmma_kernel<BM, BN><<<grid, DM_THREADS, S::SMEM, st>>>(ma, mb, p, q, n, kchunk, C, ldc, 0);
+  if (splits == 1 && beta == 0.0 && !sym) {
+    gemm_nt_dmma_kernel<BM, BN><<<grid, DM_THREADS, S::SMEM, st>>>(ma, mb, p, q, n, kchunk, C, ldc, 0, 0);
     RLD_LAUNCH_CHECK();
     return;
   }
   const int64_t stride = q * p;
   partial.reserve(sizeof(double) * stride * splits);
   gemm_nt_dmma_kernel<BM, BN><<<grid, DM_THREADS, S::SMEM, st>>>(ma, mb, p, q, n, kchunk, partial.as<double>(), p,
-                                                                   stride);
+                                                                   stride, sym ? 1 : 0);
   RLD_LAUNCH_CHECK();
   const int blocks = (int)std::min<int64_t>(ceil_div(stride, 256), (int64_t)dm_sms() * 8);
-  dmma_split_reduce_kernel<<<blocks, 256, 0, st>>>(partial.as<double>(), (int)splits, stride, q, p, C, ldc, beta);
+  dmma_split_reduce_kernel<<<blocks, 256, 0, st>>>(partial.as<double>(), (int)splits, stride, q, p, C, ldc, beta,
+                                                   sym ? BM : 0, BN);
   RLD_LAUNCH_CHECK();
 }
 
@@ -455,13 +469,16 @@ void gemm_nt_f64(const double* A, int64_t lda, int64_t p, const double* B, int64
       bn = w;
     }
   }
+  // a Gram (the same block on both sides): skip the tiles above the diagonal (RLD_GRAM_SYM=0: off)
+  static const bool sym_on = !(getenv("RLD_GRAM_SYM") && getenv("RLD_GRAM_SYM")[0] == '0');
+  const bool sym = sym_on && A == B && lda == ldb && p == q;
   switch (bn) {
-    case 128: launch_nt<128, 128>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st); break;
-    case 96: launch_nt<128, 96>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st); break;
-    case 64: launch_nt<128, 64>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st); break;
-    case 48: launch_nt<128, 48>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st); break;
-    case 32: launch_nt<128, 32>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st); break;
-    default: launch_nt<128, 16>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st); break;
+    case 128: launch_nt<128, 128>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st, sym); break;
+    case 96: launch_nt<128, 96>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st, sym); break;
+    case 64: launch_nt<128, 64>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st, sym); break;
+    case 48: launch_nt<128, 48>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st, sym); break;
+    case 32: launch_nt<128, 32>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st, sym); break;
+    default: launch_nt<128, 16>(A, lda, p, B, ldb, q, n, C, ldc, beta, partial, st, sym); break;
   }
 }
 

@@ -146,6 +146,29 @@ __global__ void ozaki_scale_kernel(const double* __restrict__ A, int64_t lda, in
   }
 }
 
+// The same scales with the row split over many CTAs (the one-CTA-per-row version left most SMs idle
+// for the m = 64 Lanczos block): per-chunk maxima of |A| merged with atomicMax on their bit patterns
+// (non-negative doubles order like unsigned integers) into `bits` (zeroed), then converted in place.
+constexpr int OZ_MAX_CHUNK = 4096;
+__global__ void ozaki_rowmax_kernel(const double* __restrict__ A, int64_t lda, int64_t n,
+                                    unsigned long long* __restrict__ bits) {
+  const int64_t row = blockIdx.x;
+  const int64_t j0 = (int64_t)blockIdx.y * OZ_MAX_CHUNK, j1 = min64(n, j0 + OZ_MAX_CHUNK);
+  const double* a = A + row * lda;
+  double mx = 0.0;
+  for (int64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) mx = fmax(mx, fabs(a[j]));
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx > 0.0) atomicMax(bits + row, (unsigned long long)__double_as_longlong(mx));
+}
+__global__ void ozaki_scale_finish_kernel(int64_t rows, double* __restrict__ scale) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  const double mx = __longlong_as_double((long long)reinterpret_cast<unsigned long long*>(scale)[i]);
+  int e = 0;
+  if (mx > 0.0) frexp(mx, &e);
+  scale[i] = mx > 0.0 ? ldexp(1.0, e + 1) : 1.0;
+}
+
 // one thread per (padded row, 16-column half of a k-step): 8 exact digits of 16 entries of A / sigma,
 // written as one 16-byte store per slice (the half lands at byte 16 h ^ 16 in rows 4..7 of an atom)
 template <int TR>
@@ -162,12 +185,17 @@ __global__ void ozaki_digits_kernel(const double* __restrict__ A, int64_t lda, i
     const int64_t row = t * TR + i;
     const int64_t j0 = ks * OZ_BK + 16 * h;
     int ee = 0;
-    if (row < rows) frexp(scale[row], &ee);   // sigma = 2^(ee-1): x = a 2^(1-ee), exact (ldexp: no overflow)
+    if (row < rows) frexp(scale[row], &ee);   // sigma = 2^(ee-1): x = a 2^(1-ee), exact
+    // one multiply by the exact power of two when it is a normal double, ldexp otherwise (no
+    // overflow / underflow of the multiplier for extreme scales)
+    const bool mul = ee > -1000 && ee < 1000;
+    const double f = mul ? __longlong_as_double((long long)(1023 + 1 - ee) << 52) : 1.0;
     uint32_t w[OZ_S][4];
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
       const int64_t j = j0 + k;
-      const double r = (row < rows && j < n) ? ldexp(A[row * lda + j], 1 - ee) : 0.0;
+      const double a = (row < rows && j < n) ? A[row * lda + j] : 0.0;
+      const double r = mul ? a * f : ldexp(a, 1 - ee);
       int dg[OZ_S];
       long long kp;
       int nzk;
@@ -316,13 +344,33 @@ __global__ void oz_fill_kernel(int64_t rows, double v, double* __restrict__ out)
   if (i < rows) out[i] = v;
 }
 
+// row c = blockIdx.y (grid-stride over m), columns grid-stride over x; pairs of doubles when the
+// rows and the output pitch allow 16-byte accesses
 __global__ void oz_split_reduce_kernel(const double* __restrict__ part, int splits, int64_t stride, int64_t m,
                                        int64_t rows, double* __restrict__ out, int64_t ldo) {
-  const int64_t total = m * rows;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int k = 0; k < splits; ++k) s += part[k * stride + e];
-    out[(e / rows) * ldo + e % rows] = s;
+  const bool v2 = (rows % 2 == 0) && (ldo % 2 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) &&
+                  ((reinterpret_cast<uintptr_t>(part) & 15) == 0) && (stride % 2 == 0);
+  for (int64_t c = blockIdx.y; c < m; c += gridDim.y) {
+    const double* pc = part + c * rows;
+    double* oc = out + c * ldo;
+    if (v2) {
+      for (int64_t r = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); r < rows;
+           r += 2 * (int64_t)gridDim.x * blockDim.x) {
+        double2 s = make_double2(0.0, 0.0);
+        for (int k = 0; k < splits; ++k) {
+          const double2 v = *reinterpret_cast<const double2*>(pc + k * stride + r);
+          s.x += v.x;
+          s.y += v.y;
+        }
+        *reinterpret_cast<double2*>(oc + r) = s;
+      }
+    } else {
+      for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int k = 0; k < splits; ++k) s += pc[k * stride + r];
+        oc[r] = s;
+      }
+    }
   }
 }
 
@@ -331,7 +379,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, int64_t KS,
                 const double* __restrict__ sigma, const double* __restrict__ tau, int64_t rows, int64_t m, int64_t n,
                 int64_t kchunk, double* __restrict__ out, int64_t ldo, int64_t split_stride, int nd,
-                const int* __restrict__ knz) {
+                const int* __restrict__ knz, int probe) {
   extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -395,6 +443,10 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
           ptx::mbar_arrive(&full[st]);
           continue;
         }
+        if (probe == 2) {   // RLD_OZ_PROBE=2 (measurement only): no loads, the MMAs read stale stages
+          ptx::mbar_arrive(&full[st]);
+          continue;
+        }
         const uint32_t abytes = (uint32_t)(nd - lz) * OZ_A_SLICE, bbytes = (uint32_t)(nd - lz) * OZ_B_SLICE;
         ptx::mbar_arrive_expect_tx(&full[st], abytes + bbytes);
         bulk_load(dst + lz * OZ_A_SLICE, ga + (int64_t)s * OZ_A_BYTES + lz * OZ_A_SLICE, abytes, &full[st]);
@@ -417,7 +469,7 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
         // N = 64 ones, and the A operand is read from shared memory once per piece
 #pragma unroll
         for (int sa = 0; sa < OZ_S; ++sa) {
-          if (sa >= nd) break;
+          if (sa >= nd || probe == 1) break;   // RLD_OZ_PROBE=1 (measurement only): loads, no MMAs
           if (sa < lz) continue;
           const uint64_t adesc = desc_sw32(a0 + sa * OZ_A_SLICE);
           const uint32_t acc = (kb_nz || s > 0 || sa > 0) ? 1u : 0u;
@@ -500,7 +552,15 @@ void ozaki_slice(const double* A, int64_t lda, int64_t rows, int64_t n, int tile
                  cudaStream_t st) {
   if (rows <= 0) return;
   if (rows > 2147483647LL) fail(RLD_ERR_NOT_SUPPORTED, "ozaki_slice: too many rows");
-  ozaki_scale_kernel<<<(unsigned)rows, 256, 0, st>>>(A, lda, n, scale);
+  if (rows <= 65535) {
+    RLD_CUDA(cudaMemsetAsync(scale, 0, sizeof(double) * rows, st));
+    ozaki_rowmax_kernel<<<dim3((unsigned)rows, (unsigned)ceil_div(std::max<int64_t>(n, 1), OZ_MAX_CHUNK)), 256, 0, st>>>(
+        A, lda, n, reinterpret_cast<unsigned long long*>(scale));
+    RLD_LAUNCH_CHECK();
+    ozaki_scale_finish_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, st>>>(rows, scale);
+  } else {
+    ozaki_scale_kernel<<<(unsigned)rows, 256, 0, st>>>(A, lda, n, scale);
+  }
   RLD_LAUNCH_CHECK();
   const int64_t KS = ceil_div(n, OZ_BK);
   const int64_t total = ceil_div(rows, tile_rows) * tile_rows * KS * 2;
@@ -575,19 +635,22 @@ void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int6
   dim3 grid((unsigned)passes, (unsigned)tiles, (unsigned)splits);
   if (grid.y > 65535u || grid.z > 65535u) fail(RLD_ERR_NOT_SUPPORTED, "kv_product_ozaki: grid too large");
   const int8_t* Bq = ws.oz_vq.as<int8_t>();
+  const char* pe = getenv("RLD_OZ_PROBE");   // kernel-phase probe for measurement, never set in production
+  const int probe = pe ? atoi(pe) : 0;
   if (splits == 1) {
     ozaki_kv_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(Kq, Bq, KS, ksigma, ws.oz_tau.as<double>(), rows, m, n, kchunk,
-                                                      Y, ldy, 0, diags, knz);
+                                                      Y, ldy, 0, diags, knz, probe);
     RLD_LAUNCH_CHECK();
     return;
   }
   const int64_t stride = m * rows;
   ws.partial.reserve(sizeof(double) * stride * splits);
   ozaki_kv_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(Kq, Bq, KS, ksigma, ws.oz_tau.as<double>(), rows, m, n, kchunk,
-                                                    ws.partial.as<double>(), rows, stride, diags, knz);
+                                                    ws.partial.as<double>(), rows, stride, diags, knz, probe);
   RLD_LAUNCH_CHECK();
-  const int blocks = (int)std::min<int64_t>(ceil_div(stride, 256), slots * 8);
-  oz_split_reduce_kernel<<<blocks, 256, 0, st>>>(ws.partial.as<double>(), (int)splits, stride, m, rows, Y, ldy);
+  const unsigned gy = (unsigned)std::min<int64_t>(m, 65535);
+  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 512), slots * 8 / gy + 1));
+  oz_split_reduce_kernel<<<dim3(gx, gy), 256, 0, st>>>(ws.partial.as<double>(), (int)splits, stride, m, rows, Y, ldy);
   RLD_LAUNCH_CHECK();
 }
 

@@ -191,6 +191,177 @@ tridiag_kernel(int n, const double* __restrict__ A, double* __restrict__ d, doub
 }
 
 
+// Variant with ONE set of v / w slots per CTA (double-buffered by column parity) instead of one per
+// warp, so the shared memory that held the per-warp copies goes to more warps (fewer rows per warp
+// on the latency-bound per-column chain), and two rows per warp iteration (independent dot
+// products and butterflies interleave).  Warp 0 writes the slots; the cluster barrier publishes
+// v, one block barrier per column publishes w before the rank-2 update.
+template <int NMAX, int TTH>
+constexpr size_t tridiag2_smem_t() {
+  return sizeof(double) * ((size_t)((NMAX + TCL - 1) / TCL) * NMAX + 8 * (size_t)NMAX);
+}
+
+template <int NMAX, int TTH>
+__global__ void __launch_bounds__(TTH)
+tridiag2_kernel(int n, const double* __restrict__ A, double* __restrict__ d, double* __restrict__ e,
+                double* __restrict__ tau_out, double* __restrict__ V) {
+  constexpr int K = NMAX / 32, W = TTH / 32, TRPC = (NMAX + TCL - 1) / TCL;
+  static_assert(NMAX % 32 == 0, "NMAX must be a multiple of 32");
+  cg::cluster_group cl = cg::this_cluster();
+  const int r = (int)cl.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  extern __shared__ double sm[];
+  double (*rows)[NMAX] = reinterpret_cast<double (*)[NMAX]>(sm);                     // [TRPC][NMAX]
+  double (*slot)[2][NMAX] = reinterpret_cast<double (*)[2][NMAX]>(sm + TRPC * NMAX);  // [parity][v, w][NMAX]
+  double (*col)[NMAX] = reinterpret_cast<double (*)[NMAX]>(sm + (TRPC + 4) * NMAX);   // [2][NMAX] raw column
+  double (*pv)[NMAX] = col + 2;                                                      // [2][NMAX] p = tau A v
+  const int nr = (n - r + TCL - 1) / TCL;
+  for (int q = 0; q < nr; ++q)
+    for (int c = tid; c < n; c += TTH) rows[q][c] = A[(size_t)(r + q * TCL) * n + c];
+  for (int c = tid; c < 4 * NMAX; c += TTH) (&slot[0][0][0])[c] = 0.0;
+  __syncthreads();
+  for (int q = tid; q < nr; q += TTH) {
+    const int i = r + q * TCL;
+    for (int dst = 0; dst < TCL; ++dst) *cl.map_shared_rank(&col[0][i], dst) = rows[q][0];
+  }
+  cl.sync();
+  double x[K], v[K], w[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int c = lane + 32 * k;
+    x[k] = c < n ? col[0][c] : 0.0;
+  }
+  double pvj = 0.0, pwj = 0.0;
+  for (int j = 0; j < n - 2; ++j) {
+    const int b = j & 1;
+    const double* vp = slot[b ^ 1][0];   // the previous column's v', w'
+    const double* wp = slot[b ^ 1][1];
+    double s0 = 0.0, s1 = 0.0;   // two chains: the per-column path is latency-bound
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (lane + 32 * k > j) {
+        if (k & 1) s1 = fma(x[k], x[k], s1);
+        else s0 = fma(x[k], x[k], s0);
+      }
+    const double sig = warp_sum(s0 + s1);
+    const double x0 = col[b][j + 1] - (vp[j + 1] * pwj + wp[j + 1] * pvj);
+    const double dj = col[b][j] - (vp[j] * pwj + wp[j] * pvj);
+    const double alpha = -copysign(sig > 1e-300 ? sqrt_nr(sig) : sqrt(sig), x0);
+    const double vtv = sig - x0 * x0 + (x0 - alpha) * (x0 - alpha);
+    const double tau = vtv > 1e-300 ? 2.0 * rcp_nr(vtv) : (vtv > 0.0 ? 2.0 / vtv : 0.0);
+    const double vj1 = x0 - alpha;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int c = lane + 32 * k;
+      v[k] = (c <= j) ? 0.0 : (c == j + 1 ? vj1 : x[k]);
+      if (warp == 0) slot[b][0][c] = v[k];
+    }
+    if (r == 0 && warp == 0) {
+      if (lane == 0) {
+        d[j] = dj;
+        e[j] = (tau > 0.0) ? alpha : x0;
+        tau_out[j] = tau;
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int c = lane + 32 * k;
+        if (c < n) V[(size_t)j * n + c] = v[k];
+      }
+    }
+    // own rows i > j, two per iteration: p_i = tau (row_i . v), broadcast with the raw entry of
+    // the next column
+    for (int q = warp; q < nr; q += 2 * W) {
+      const int q2 = q + W;
+      const int i1 = r + q * TCL, i2 = r + q2 * TCL;
+      const bool a1 = i1 > j, a2 = q2 < nr && i2 > j;
+      if (!a1 && !a2) continue;
+      double acc1 = 0.0, acc2 = 0.0, acc3 = 0.0, acc4 = 0.0;
+      const double* r1 = rows[q];
+      const double* r2 = rows[a2 ? q2 : q];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int c = lane + 32 * k;
+        if (c > j && c < n) {
+          if (k & 1) {
+            acc3 = fma(r1[c], v[k], acc3);
+            acc4 = fma(r2[c], v[k], acc4);
+          } else {
+            acc1 = fma(r1[c], v[k], acc1);
+            acc2 = fma(r2[c], v[k], acc2);
+          }
+        }
+      }
+      acc1 += acc3;
+      acc2 += acc4;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc1 += __shfl_xor_sync(0xffffffffu, acc1, o);
+        acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
+      }
+      if (lane < TCL) {
+        if (a1) {
+          *cl.map_shared_rank(&pv[b][i1], lane) = tau * acc1;
+          *cl.map_shared_rank(&col[b ^ 1][i1], lane) = r1[j + 1];
+        }
+        if (a2) {
+          *cl.map_shared_rank(&pv[b][i2], lane) = tau * acc2;
+          *cl.map_shared_rank(&col[b ^ 1][i2], lane) = r2[j + 1];
+        }
+      }
+    }
+    cl.sync();
+    double kap0 = 0.0, kap1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int c = lane + 32 * k;
+      w[k] = (c > j && c < n) ? pv[b][c] : 0.0;
+      if (k & 1) kap1 = fma(w[k], v[k], kap1);
+      else kap0 = fma(w[k], v[k], kap0);
+    }
+    const double kk = 0.5 * tau * warp_sum(kap0 + kap1);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      w[k] = fma(-kk, v[k], w[k]);
+      if (warp == 0) slot[b][1][lane + 32 * k] = w[k];
+    }
+    const double wj1 = fma(-kk, vj1, pv[b][j + 1]);
+    pvj = vj1;
+    pwj = wj1;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int c = lane + 32 * k;
+      x[k] = (c > j && c < n) ? col[b ^ 1][c] - (v[k] * wj1 + w[k] * vj1) : 0.0;
+    }
+    __syncthreads();   // w in the slot
+    const double* vs = slot[b][0];
+    const double* ws = slot[b][1];
+    for (int q = warp; q < nr; q += W) {
+      const int i = r + q * TCL;
+      if (i <= j) continue;
+      const double vi = vs[i], wi = ws[i];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int c = lane + 32 * k;
+        if (c > j && c < n) rows[q][c] -= vi * w[k] + wi * v[k];
+      }
+    }
+  }
+  if (n >= 3) {
+    const int b = (n - 2) & 1;
+    const double* vp = slot[b ^ 1][0];
+    const double* wp = slot[b ^ 1][1];
+    const double a = col[b][n - 2] - (vp[n - 2] * pwj + wp[n - 2] * pvj);
+    const double bb = col[b][n - 1] - (vp[n - 1] * pwj + wp[n - 1] * pvj);
+    if (r == 0 && tid == 0) {
+      d[n - 2] = a;
+      e[n - 2] = bb;
+    }
+  }
+  __syncthreads();   // row n - 1 was last updated by its owner warp
+  if ((n - 1) % TCL == r && tid == 0) d[n - 1] = rows[(n - 1) / TCL][n - 1];
+}
+
+
 // T splits between i and i + 1 when e_i^2 <= eps^2 |d_i d_{i+1}| (LAPACK dstebz's test): the
 // coupling is treated as zero by both the eigenvalue and the eigenvector kernels
 __device__ __forceinline__ bool split_at(const double* d, const double* e, int i) {
@@ -613,15 +784,25 @@ __global__ void __launch_bounds__(1024) orth_defect_kernel(int n, const double* 
   }
 }
 
-template <int NMAX, int TTH, int IVT>
+// RLD_TRIDIAG: 1 = per-warp slots (tridiag_kernel), 2 = per-CTA slots with more warps
+// (tridiag2_kernel); default: 1 for n <= 288, 2 above
+int tridiag_variant(int n) {
+  static const int v = getenv("RLD_TRIDIAG") ? atoi(getenv("RLD_TRIDIAG")) : 0;
+  return v ? v : (n <= TNMAX ? 1 : 2);   // measured: 1.00 vs 1.18 ms at n = 266, 3.54 vs 3.24 ms at 522
+}
+
+template <int NMAX, int TTH, int IVT, int TTH2>
 void tri_eigh_launch(int n, const double* A, double* w, double* d, double* e, double* tau, double* V, double* Z,
                      double* Q, double* Tw, cudaStream_t st, cudaStream_t st2, cudaEvent_t fork, cudaEvent_t join) {
   constexpr size_t tsm = tridiag_smem_t<NMAX, TTH>();
+  constexpr size_t tsm2 = tridiag2_smem_t<NMAX, TTH2>();
   const size_t vsm = sizeof(double) * FQ_C * NMAX;
   static std::atomic<uint64_t> attr{0};
   once_per_device(attr, [&] {
     RLD_CUDA(cudaFuncSetAttribute(tridiag_kernel<NMAX, TTH>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     RLD_CUDA(cudaFuncSetAttribute(tridiag_kernel<NMAX, TTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+    RLD_CUDA(cudaFuncSetAttribute(tridiag2_kernel<NMAX, TTH2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    RLD_CUDA(cudaFuncSetAttribute(tridiag2_kernel<NMAX, TTH2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm2));
     RLD_CUDA(cudaFuncSetAttribute(inviter_kernel<IVT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)inviter_smem(NMAX, IVT)));
     RLD_CUDA(cudaFuncSetAttribute(wy_t_kernel<NMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsm));
@@ -629,9 +810,10 @@ void tri_eigh_launch(int n, const double* A, double* w, double* d, double* e, do
   });
   {
     cudaLaunchConfig_t cfg{};
+    const bool v2 = tridiag_variant(n) == 2;
     cfg.gridDim = dim3(TCL);
-    cfg.blockDim = dim3(TTH);
-    cfg.dynamicSmemBytes = tsm;
+    cfg.blockDim = dim3(v2 ? TTH2 : TTH);
+    cfg.dynamicSmemBytes = v2 ? tsm2 : tsm;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -640,7 +822,10 @@ void tri_eigh_launch(int n, const double* A, double* w, double* d, double* e, do
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    RLD_CUDA(cudaLaunchKernelEx(&cfg, tridiag_kernel<NMAX, TTH>, n, A, d, e, tau, V));
+    if (v2)
+      RLD_CUDA(cudaLaunchKernelEx(&cfg, tridiag2_kernel<NMAX, TTH2>, n, A, d, e, tau, V));
+    else
+      RLD_CUDA(cudaLaunchKernelEx(&cfg, tridiag_kernel<NMAX, TTH>, n, A, d, e, tau, V));
     RLD_LAUNCH_CHECK();
   }
   // Q (reflectors -> WY -> rows of Q) on the side stream, overlapping the eigenvalue and
@@ -681,9 +866,9 @@ bool tri_eigh(int n, const double* A, double* w, DevBuf& scratch, double** Zout,
   double* work = Q + nn;
   double* Tw = work;   // compact-WY T factors, FQ_C^2 per chunk (<= n^2 in all)
   if (n <= TNMAX)
-    tri_eigh_launch<TNMAX, TT, 16>(n, A, w, d, e, tau, V, Z, Q, Tw, st, st2, fork, join);
+    tri_eigh_launch<TNMAX, TT, 16, 512>(n, A, w, d, e, tau, V, Z, Q, Tw, st, st2, fork, join);
   else
-    tri_eigh_launch<TNMAX_L, TT_L, 8>(n, A, w, d, e, tau, V, Z, Q, Tw, st, st2, fork, join);
+    tri_eigh_launch<TNMAX_L, TT_L, 8, 384>(n, A, w, d, e, tau, V, Z, Q, Tw, st, st2, fork, join);
   RLD_CUDA(cudaStreamWaitEvent(st, join, 0));
   *Zout = Z;
   *Qout = Q;

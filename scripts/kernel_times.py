@@ -40,3 +40,19 @@ all_us = sum(tot.values()) / a.reps
 print(f"phases {[round(x, 3) for x in est.phase_ms]}  kernel-sum/estimate {all_us:.1f} us")
 for name, us in sorted(tot.items(), key=lambda kv: -kv[1])[: a.top]:
     print(f"{us / a.reps:9.1f} us {cnt[name] / a.reps:6.1f}x  {name[:110]}")
+
+# device idle gaps of the last estimate: intervals with no kernel / copy running (union over streams)
+evs = sorted([(ev.time_range.start, ev.time_range.end, ev.name) for ev in prof.events()
+              if ev.device_type == torch.autograd.DeviceType.CUDA], key=lambda x: x[0])
+per = len(evs) // a.reps
+last = evs[-per:]
+gaps, cur_end, prev = [], last[0][1], last[0][2]
+for s0, e0, nm in last[1:]:
+    if s0 > cur_end:
+        gaps.append((s0 - cur_end, prev[:60], nm[:60]))
+    if e0 > cur_end:
+        cur_end, prev = e0, nm
+span = last[-1][1] - last[0][0]
+print(f"last estimate: span {span / 1e3:.2f} ms, idle {sum(g[0] for g in gaps) / 1e3:.2f} ms in {len(gaps)} gaps")
+for g in sorted(gaps, reverse=True)[:15]:
+    print(f"  gap {g[0]:8.1f} us  after {g[1]}  before {g[2]}")
