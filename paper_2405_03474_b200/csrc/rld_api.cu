@@ -570,12 +570,63 @@ void gram_blas(rld_handle* h, int64_t rows, int w, const double* Y, int64_t ldy,
 // Upper Cholesky of the w x w fp64 matrix G (ld w): the one-cluster kernel for w <= 640
 // (small_chol.cu), cuSOLVER potrf above that.  RLD_SMALL_CHOL=0 forces cuSOLVER.
 // Returns true when R^-1 was written to `rinv` as well (only the one-cluster kernel does).
+// Above 640: 2 x 2 block recursion on the same kernels (no cuSOLVER on the default path):
+//   R11 = chol(G11) with X11 = R11^-1 (the cluster kernel, or this recursion), R12 = X11^T G12 (DMMA
+//   nt), S = G22 - R12^T R12 (DMMA nt, symmetric), R22 = chol(S) with X22, and when R^-1 is wanted
+//   X12 = -X11 R12 X22 (two DMMA expands).  The leading block is a multiple of 32 columns (half of
+//   n), so every sub-factorisation is itself <= 640 or recursed.  info as potrf: first failing pivot.
+// G column-major (ld), upper part read and written; X (if not null) n x n, ld n, upper part.
+void blocked_potrf_upper(rld_handle* h, int n, double* G, int64_t ld, int* info, double* X) {
+  cudaStream_t st = h->st;
+  const int n1 = (n / 2 + 31) / 32 * 32, n2 = n - n1;
+  double *x11 = nullptr, *x22 = nullptr, *r12 = nullptr, *t = nullptr;
+  int* inf = nullptr;
+  RLD_CUDA(cudaMallocAsync(&x11, sizeof(double) * n1 * n1, st));
+  RLD_CUDA(cudaMallocAsync(&r12, sizeof(double) * n1 * n2, st));
+  RLD_CUDA(cudaMallocAsync(&t, sizeof(double) * std::max<int64_t>((int64_t)n2 * n2, (int64_t)n1 * n2), st));
+  RLD_CUDA(cudaMallocAsync(&inf, sizeof(int) * 2, st));
+  if (X) RLD_CUDA(cudaMallocAsync(&x22, sizeof(double) * n2 * n2, st));
+  auto sub = [&](int m, double* A, int64_t lda, int* i, double* Xs) {
+    if (!small_potrf_upper(m, A, (int)lda, i, st, Xs)) blocked_potrf_upper(h, m, A, lda, i, Xs);
+  };
+  sub(n1, G, ld, inf, x11);
+  // R12 = X11^T G12  (n1 x n2), then into the upper right block of G
+  nt_f64(h, x11, n1, n1, G + (int64_t)n1 * ld, ld, n2, n1, r12, n1);
+  RLD_CUDA(cudaMemcpy2DAsync(G + (int64_t)n1 * ld, sizeof(double) * ld, r12, sizeof(double) * n1, sizeof(double) * n1,
+                             n2, cudaMemcpyDeviceToDevice, st));
+  // S = G22 - R12^T R12
+  nt_f64(h, r12, n1, n2, r12, n1, n2, n1, t, n2);
+  double* G22 = G + (int64_t)n1 * ld + n1;
+  sub_block(n2, n2, t, n2, G22, ld, st);
+  sub(n2, G22, ld, inf + 1, x22);
+  combine_info(info, inf, inf + 1, n1, st);
+  if (X) {
+    // X = [[X11, -X11 R12 X22], [0, X22]]
+    RLD_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * (size_t)n * n, st));
+    RLD_CUDA(cudaMemcpy2DAsync(X, sizeof(double) * n, x11, sizeof(double) * n1, sizeof(double) * n1, n1,
+                               cudaMemcpyDeviceToDevice, st));
+    RLD_CUDA(cudaMemcpy2DAsync(X + (int64_t)n1 * n + n1, sizeof(double) * n, x22, sizeof(double) * n2,
+                               sizeof(double) * n2, n2, cudaMemcpyDeviceToDevice, st));
+    ex_f64(h, x22, n2, n2, n2, r12, n1, n1, t, n1);                    // T = R12 X22  (n1 x n2)
+    ex_f64(h, t, n1, n1, n2, x11, n1, n1, X + (int64_t)n1 * n, n, -1.0);   // X12 = -X11 T
+  }
+  RLD_CUDA(cudaFreeAsync(x11, st));
+  RLD_CUDA(cudaFreeAsync(r12, st));
+  RLD_CUDA(cudaFreeAsync(t, st));
+  RLD_CUDA(cudaFreeAsync(inf, st));
+  if (x22) RLD_CUDA(cudaFreeAsync(x22, st));
+}
+
 bool potrf_upper(rld_handle* h, int w, double* G, int* info, double* rinv = nullptr) {
   static const bool small = [] {
     const char* e = getenv("RLD_SMALL_CHOL");
     return !(e && e[0] == '0');
   }();
   if (small && small_potrf_upper(w, G, w, info, h->st, rinv)) return rinv != nullptr;
+  if (small && w > 640 && (w % 2) == 0) {   // the DMMA kernels need 16-byte aligned columns
+    blocked_potrf_upper(h, w, G, w, info, rinv);
+    return rinv != nullptr;
+  }
   Work& wk = h->wk;
   int lwork = 0;
   RLD_CUSOLVER(cusolverDnDpotrf_bufferSize(h->solver, CUBLAS_FILL_MODE_UPPER, w, G, w, &lwork));

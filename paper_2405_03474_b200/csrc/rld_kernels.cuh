@@ -38,6 +38,8 @@ void scale_rows_colmajor(int64_t rows, int64_t cols, int64_t ld, const double* f
                          cudaStream_t st);
 void scale_cols_colmajor(int64_t rows, int64_t cols, int64_t ld, const double* f, double* a, cudaStream_t st);
 void copy_doubles(int64_t count, const double* s, double* d, cudaStream_t st);
+void sub_block(int64_t rows, int64_t cols, const double* T, int64_t ldt, double* G, int64_t ldg, cudaStream_t st);
+void combine_info(int* info, const int* i1, const int* i2, int n1, cudaStream_t st);
 void fill_doubles(int64_t count, double v, double* d, cudaStream_t st);
 
 void cholqr_check(int w, const double* R, const double* gdiag, const int* info, double rtol, int* flags,

@@ -4,7 +4,7 @@
 // (src/precond.py:75-80).  cuSOLVER's potrf at these sizes is a chain of ~20 small kernels
 // (0.21 ms at n = 256, 0.27 ms at 266); this is one launch.
 //
-// Right-looking, 32-column panels, CL CTAs of one cluster; column j belongs to CTA j % CL.
+// Right-looking, 32-column panels, CL = 16 CTAs of one cluster; column j belongs to CTA j % CL.
 // Per panel p (rows/cols [k0, k1)):
 //   1. every CTA loads the diagonal block from global, applies the previous panel's update to
 //      it redundantly (owners skip those columns), and factors it in one warp with the columns
@@ -24,11 +24,10 @@ namespace rld {
 
 namespace {
 
-constexpr int CL = 8;            // CTAs per cluster
+// CTAs per cluster: 16 (non-portable; RLD_CHOL_CL=8 for the portable size)
 constexpr int NB = 32;           // panel width
 constexpr int THREADS = 256;
 constexpr int SMALL_CHOL_MAX = 640;
-constexpr int CMAX = (SMALL_CHOL_MAX + CL - 1) / CL;   // columns per CTA
 
 // Global-memory writes of one CTA become visible to the others: gpu-scope fence, then the
 // cluster barrier (release / acquire); the reads after it go to L2 (ld.global.cg).
@@ -104,7 +103,8 @@ __device__ __forceinline__ void factor_block(double* Ds, double* Ri, double* Rv,
   if (bad >= 0 && lane == 0) Ri[0] = -1.0 - (double)bad;
 }
 
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(THREADS)
+template <int CL>
+__global__ void __launch_bounds__(THREADS)
 chol_upper_kernel(int n, double* __restrict__ G, int ld, int* __restrict__ info, double* __restrict__ X,
                   long long* __restrict__ prof) {
   extern __shared__ double sm[];
@@ -115,6 +115,7 @@ chol_upper_kernel(int n, double* __restrict__ G, int ld, int* __restrict__ info,
   double* Ri = Dn + NB * LDB;       // NB: 1 / R_ii
   double* rowbuf = Ri + NB;         // 2 x NB: pivot-row broadcast of the diagonal factorisation
   double* Gs = rowbuf + 2 * NB;     // CMAX x LDB: this CTA's columns of the panel rows (step 2 input)
+  constexpr int CMAX = (SMALL_CHOL_MAX + CL - 1) / CL;
   double* Pt = Gs + CMAX * LDB;     // n x LDB: panel row, Pt[j * LDB + m] = R[k0 + m, j]
   const int cta = (int)blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -325,21 +326,43 @@ chol_upper_kernel(int n, double* __restrict__ G, int ld, int* __restrict__ info,
 bool small_potrf_upper(int n, double* G, int ld, int* info, cudaStream_t st, double* Rinv) {
   if (n < 1 || n > SMALL_CHOL_MAX) return false;
   // the panel-row buffer doubles as the R^-1 column blocks (ceil(n / 32) 32 x 32 blocks)
-  auto smem_for = [](int nn) {
+  auto smem_for = [](int nn, int cl) {
+    const size_t cmax = (size_t)(SMALL_CHOL_MAX + cl - 1) / cl;
     const size_t tail = std::max((size_t)nn * (NB + 1), (size_t)NB * NB * ((nn + NB - 1) / NB));
-    return sizeof(double) * ((size_t)3 * NB * (NB + 1) + 3 * NB + (size_t)CMAX * (NB + 1)) + sizeof(double) * tail;
+    return sizeof(double) * ((size_t)3 * NB * (NB + 1) + 3 * NB + cmax * (NB + 1)) + sizeof(double) * tail;
   };
   static std::atomic<uint64_t> attr_set{0};
   once_per_device(attr_set, [&] {
-    RLD_CUDA(cudaFuncSetAttribute(chol_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem_for(SMALL_CHOL_MAX)));
+    RLD_CUDA(cudaFuncSetAttribute(chol_upper_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem_for(SMALL_CHOL_MAX, 8)));
+    RLD_CUDA(cudaFuncSetAttribute(chol_upper_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem_for(SMALL_CHOL_MAX, 16)));
+    RLD_CUDA(cudaFuncSetAttribute(chol_upper_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   });
-  const size_t smem = smem_for(n);
+  // RLD_CHOL_CL=8/16 forces the cluster size (measurement)
+  static const int cl_env = getenv("RLD_CHOL_CL") ? atoi(getenv("RLD_CHOL_CL")) : 0;
+  const int cl = cl_env == 8 || cl_env == 16 ? cl_env : 16;   // 16: 255 vs 314 us at n = 522, 120 vs 129 at 266
+  const size_t smem = smem_for(n, cl);
   static const bool profile = getenv("RLD_CHOL_PROFILE") != nullptr;
   long long* prof = nullptr;
   if (profile) RLD_CUDA(cudaMallocAsync(&prof, 8 * sizeof(long long), st)), RLD_CUDA(cudaMemsetAsync(prof, 0, 64, st));
   if (Rinv) RLD_CUDA(cudaMemsetAsync(Rinv, 0, sizeof(double) * (size_t)n * n, st));
-  chol_upper_kernel<<<CL, THREADS, smem, st>>>(n, G, ld, info, Rinv, prof);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(cl);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (cl == 16)
+    RLD_CUDA(cudaLaunchKernelEx(&cfg, chol_upper_kernel<16>, n, G, ld, info, Rinv, prof));
+  else
+    RLD_CUDA(cudaLaunchKernelEx(&cfg, chol_upper_kernel<8>, n, G, ld, info, Rinv, prof));
   RLD_LAUNCH_CHECK();
   if (profile) {
     long long hp[8];

@@ -420,6 +420,33 @@ void copy_doubles(int64_t count, const double* s, double* d, cudaStream_t st) {
   copy_kernel<<<grid_for(count), 256, 0, st>>>(count, s, d);
   RLD_LAUNCH_CHECK();
 }
+namespace {
+__global__ void sub_block_kernel(int64_t rows, int64_t cols, const double* __restrict__ T, int64_t ldt,
+                                 double* __restrict__ G, int64_t ldg) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / rows, r = e - c * rows;
+    G[c * ldg + r] -= T[c * ldt + r];
+  }
+}
+__global__ void combine_info_kernel(int* __restrict__ info, const int* __restrict__ i1, const int* __restrict__ i2,
+                                    int n1) {
+  const int a = *i1, b = *i2;
+  *info = a != 0 ? a : (b != 0 ? n1 + b : 0);
+}
+}  // namespace
+
+// G (column-major, ld ldg) -= T (ld ldt) over a rows x cols block
+void sub_block(int64_t rows, int64_t cols, const double* T, int64_t ldt, double* G, int64_t ldg, cudaStream_t st) {
+  if (rows * cols <= 0) return;
+  sub_block_kernel<<<grid_for(rows * cols), 256, 0, st>>>(rows, cols, T, ldt, G, ldg);
+  RLD_LAUNCH_CHECK();
+}
+// info = i1 (first failing pivot of the leading block) or n1 + i2 (trailing block), 0 on success
+void combine_info(int* info, const int* i1, const int* i2, int n1, cudaStream_t st) {
+  combine_info_kernel<<<1, 1, 0, st>>>(info, i1, i2, n1);
+  RLD_LAUNCH_CHECK();
+}
+
 void fill_doubles(int64_t count, double v, double* d, cudaStream_t st) {
   if (count <= 0) return;
   fill_kernel<<<grid_for(count), 256, 0, st>>>(count, v, d);

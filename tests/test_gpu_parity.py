@@ -649,11 +649,11 @@ def _dense_cholesky(G):
     return np.tril(t.cpu().numpy()), info.value   # device column-major upper R = tril of the row-major view
 
 
-@pytest.mark.parametrize("n", [1, 5, 31, 32, 33, 64, 100, 255, 266, 522, 640, 700])
+@pytest.mark.parametrize("n", [1, 5, 31, 32, 33, 64, 100, 255, 266, 522, 640, 700, 1024, 1034, 2058])
 @pytest.mark.parametrize("spectrum", ["wishart", "decaying"])
 def test_dense_cholesky_matches_lapack(rld, n, spectrum):
-    """One-cluster Cholesky (n <= 640) / cuSOLVER potrf (above) vs LAPACK: the Gram factor of
-    CholQR and the inner factor of src/precond.py:75-80."""
+    """One-cluster Cholesky (n <= 640) / its 2 x 2 block recursion on the DMMA kernels (above) vs
+    LAPACK: the Gram factor of CholQR and the inner factor of src/precond.py:75-80."""
     g = np.random.default_rng(n)
     if spectrum == "wishart":
         X = g.standard_normal((n + 8, n))
@@ -669,7 +669,8 @@ def test_dense_cholesky_matches_lapack(rld, n, spectrum):
     assert np.linalg.norm(L - Lref) <= 1e-10 * np.linalg.norm(Lref)
 
 
-@pytest.mark.parametrize("n,bad", [(1, 0), (40, 0), (40, 5), (266, 37), (266, 265), (522, 300), (700, 650)])
+@pytest.mark.parametrize("n,bad", [(1, 0), (40, 0), (40, 5), (266, 37), (266, 265), (522, 300), (700, 650),
+                                   (700, 100), (1034, 900), (2058, 1500), (2058, 3)])
 def test_dense_cholesky_reports_first_bad_pivot(rld, n, bad):
     """info = 1-based index of the first non-positive pivot (LAPACK potrf), which the CholQR weak
     test and the NotPositiveDefinite check read."""
