@@ -506,19 +506,19 @@ def roofline_for(wl, cfg, rows, n, s, kv_ms, world):
     key = f"kv_product|{cfg.dtype}{'-int8slices' if ozaki else ''}|{wl.path}|n={n}|rows={rows}|m={s}"
     traffic, traffic_src = ncu_traffic(key)
     if ozaki:
-        # float64-accurate product on the INT8 tensor cores (kv_ozaki.cu): K streams as its 8 exact
-        # int8 slices, 8 bytes per entry like a float64 K; 36 slice-pair int8 products per useful
-        # multiply-add (4.0e13 int8 ops at config 3, m = 64: under the int8 tensor peak's time), so
+        # float64-accurate product on the INT8 tensor cores (kv_ozaki.cu): K streams as its 7 exact
+        # int8 slices (base-256 digits), 7 bytes per entry; 28 slice-pair int8 products per useful
+        # multiply-add (3.1e13 int8 ops at config 3, m = 64: under the int8 tensor peak's time), so
         # HBM bounds it
-        alg_bytes = 8 * rows * n + 8 * n * s + 8 * rows * s
+        alg_bytes = 7 * rows * n + 8 * n * s + 8 * rows * s
         hbm_peak, _, peak_kind = load_peaks()
         achieved = alg_bytes / (kv_ms * 1e-3) / 1e9
         return {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                 "traffic": traffic, "traffic_source": traffic_src, "traffic_key": key,
                 "kernel": f"kv_product (tcgen05 kind::i8 on exact int8 slices of float64 K, m=s={s}, {rows} rows)",
                 "kernel_ms": kv_ms, "alg_bytes": alg_bytes, "equiv_fp64_tflops": 2.0 * rows * n * s / (kv_ms * 1e-3) / 1e12,
-                "int8_ops": 36 * 2.0 * rows * n * (-(-s // 64) * 64),
-                "int8_tensor_frac": 36 * 2.0 * rows * n * (-(-s // 64) * 64) / (kv_ms * 1e-3) / 1e12
+                "int8_ops": 28 * 2.0 * rows * n * (-(-s // 64) * 64),
+                "int8_tensor_frac": 28 * 2.0 * rows * n * (-(-s // 64) * 64) / (kv_ms * 1e-3) / 1e12
                 / pipe.get("i8_ss_n128", {}).get("tops", 4555.6),
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}
     if wl.path == "stored" and cfg.dtype == "fp32":
@@ -637,7 +637,7 @@ def roofline_slices(rows, n, m, ms, blocks, slices, pairs, what):
     traffic, traffic_src = ncu_traffic(key)
     common = {"traffic": traffic, "traffic_source": traffic_src, "traffic_key": key, "kernel_ms": ms,
               "kernel": f"kv_product (tcgen05 kind::i8 on exact int8 slices of float64 K, {what}={m}, {rows} rows; "
-                        f"{slices / blocks:.2f} of 8 slices and {pairs / blocks:.1f} of 36 pairs per block after "
+                        f"{slices / blocks:.2f} of 7 slices (8-bit digits) and {pairs / blocks:.1f} of 28 pairs per block after "
                         f"skipping all-zero leading slices)",
               "alg_bytes": alg_bytes, "int8_ops": ops, "hbm_frac": f_hbm, "int8_tensor_frac": f_t,
               "equiv_fp64_tflops": 2.0 * rows * n * m / t / 1e12,

@@ -5,7 +5,8 @@
 namespace rld {
 
 constexpr int CRT_L = 15;           // moduli used
-constexpr int CRT_SLICES = 7;       // K' = sum_{s<7} d_s 128^{6-s}: the first 7 exact slices (49 bits)
+constexpr int OZ_NSLICES = 7;       // int8 digits (base 256) per float64 entry in the slice image (kv_ozaki.cu)
+constexpr int CRT_SLICES = 6;       // K' = sum_{s<6} d_s 256^{5-s}: the first 6 exact slices (48 bits)
 
 __host__ __device__ constexpr int crt_mod(int l) {
   // pairwise coprime, largest first: 2^8, 3.5.17, 11.23, 251, 13.19, 241, 239, 233, 229, 227, 223, 7.31, 211, 199, 197

@@ -4,8 +4,8 @@
 // kv_ozaki.cu needs 36 slice pairs, at the same float64 accuracy.
 //
 // Integers (exact):
-//   K'_ij = sum_{s<7} d_s[i,j] 128^{6-s}  from the first 7 of K's exact int8 slices (kv_ozaki.cu),
-//           K_ij = sigma_i 2^-49 (K'_ij + rho_ij), |rho| <= 1/2, |K'| < 2^48.02;
+//   K'_ij = sum_{s<6} d_s[i,j] 256^{5-s}  from the first 6 of K's exact int8 slices (kv_ozaki.cu),
+//           K_ij = sigma_i 2^-48 (K'_ij + rho_ij), |rho| <= 1/2, |K'| < 2^47;
 //   V'_cj = rint(2^{e_c} V_cj), e_c = bV - 1 - ilogb(max_j |V_cj|), |V'| < 2^bV;
 //   C'_ic = sum_j K'_ij V'_cj, |C'| < n 2^{48.02 + bV} < P / 2 (bV chosen so; 52 at n = 65536),
 //   P = prod of the L = 15 pairwise coprime moduli p_l <= 256 (2^117.8).
@@ -13,7 +13,7 @@
 //   accumulated exactly in int32 (n 2^14 < 2^31 for n < 2^17), reduced mod p_l.
 // Reconstruction (per output, float64 double-double): y_l = C_l u_l mod p_l with
 //   u_l = (P / p_l)^-1 mod p_l, S = sum_l y_l / p_l, C' = P (S - round(S)) (the representative of
-//   C' mod P in (-P/2, P/2]), Y_ic = C' sigma_i 2^-49 2^-e_c.  S is formed with 1 / p_l and P as
+//   C' mod P in (-P/2, P/2]), Y_ic = C' sigma_i 2^-48 2^-e_c.  S is formed with 1 / p_l and P as
 //   double-double (~2^-100), so C' carries < 2^21 absolute error against |C'| up to 2^116.
 // Error against the exact product: the dropped remainders rho (2^-50 sigma_i per entry) and V's
 //   rounding (2^-bV max |V_c|): the float64 level of kv_ozaki.cu.
@@ -45,9 +45,9 @@ namespace {
 constexpr int CRT_BM = 128, CRT_BK = 32;
 constexpr int CRT_KB = 4;           // k-steps per stage
 constexpr int CRT_THREADS = 256;
-constexpr int CRT_KBITS_X100 = 4802;   // log2 max|K'| * 100 (|K'| < 64 sum_k 128^k < 2^48.02)
+constexpr int CRT_KBITS_X100 = 4700;   // log2 max|K'| * 100 (|x| <= 63/128: |K'| <= 2^46.98 + 1/2)
 struct CrtConst {
-  int coef[CRT_SLICES][CRT_L];   // 128^{6-s} mod p_l
+  int coef[CRT_SLICES][CRT_L];   // 256^{5-s} mod p_l
   int u[CRT_L];                  // (P / p_l)^-1 mod p_l
   double inv_hi[CRT_L], inv_lo[CRT_L];   // 1 / p_l as double-double
   double P_hi, P_lo;             // P as double-double
@@ -59,9 +59,9 @@ CrtConst make_consts() {
   for (int l = 0; l < CRT_L; ++l) {
     const long long p = crt_mod(l);
     long long w = 1;
-    for (int s = CRT_SLICES - 1; s >= 0; --s) {   // coef[s] = 128^{6-s} mod p
+    for (int s = CRT_SLICES - 1; s >= 0; --s) {   // coef[s] = 256^{5-s} mod p
       c.coef[s][l] = (int)w;
-      w = (w * 128) % p;
+      w = (w * 256) % p;
     }
     long long Ml = 1;   // prod_{k != l} p_k mod p_l
     for (int k = 0; k < CRT_L; ++k)
@@ -131,7 +131,7 @@ __host__ __device__ __forceinline__ uint32_t swz32(uint32_t row, uint32_t col) {
 }
 
 // ---------------------------------------------------------------- K residues from the slice image
-// Slice image: ((t KS + ks) 8 + s) 4096 + phys; residue image: ((t L + l) KS + ks) 4096 + phys (the
+// Slice image: ((t KS + ks) 7 + s) 4096 + phys; residue image: ((t L + l) KS + ks) 4096 + phys (the
 // same swizzled position).  Thread = 16 bytes of one (tile, k-step).
 __global__ void crt_k_residues(const int8_t* __restrict__ Kq, int64_t tiles, int64_t KS, CrtConst c,
                                int8_t* __restrict__ Kr) {
@@ -143,7 +143,7 @@ __global__ void crt_k_residues(const int8_t* __restrict__ Kq, int64_t tiles, int
     alignas(16) int8_t d[CRT_SLICES][16];
 #pragma unroll
     for (int s = 0; s < CRT_SLICES; ++s)
-      *reinterpret_cast<uint4*>(d[s]) = *reinterpret_cast<const uint4*>(Kq + (tk * 8 + s) * 4096 + chunk * 16);
+      *reinterpret_cast<uint4*>(d[s]) = *reinterpret_cast<const uint4*>(Kq + (tk * OZ_NSLICES + s) * 4096 + chunk * 16);
 #pragma unroll
     for (int l = 0; l < CRT_L; ++l) {
       const int p = crt_mod(l);
@@ -321,7 +321,7 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
   e = (a - (s - bb)) + (b - bb);
 }
 
-// Y[c ldy + i] = C'_ic sigma_i 2^-49 2^-e_c from the L residues of C'_ic
+// Y[c ldy + i] = C'_ic sigma_i 2^-48 2^-e_c from the L residues of C'_ic
 __global__ void crt_reconstruct(const uint8_t* __restrict__ res, int64_t m, int64_t m_pad, int64_t rows, CrtConst c,
                                 int bV, const unsigned long long* __restrict__ vmax, const double* __restrict__ sigma,
                                 double* __restrict__ Y, int64_t ldy) {
@@ -352,7 +352,7 @@ __global__ void crt_reconstruct(const uint8_t* __restrict__ res, int64_t m, int6
   const double Cp = ch + ce;
   const double mx = __longlong_as_double((long long)vmax[col]);
   const int ev = mx > 0.0 ? bV - 1 - ilogb(mx) : 0;
-  Y[col * ldy + i] = ldexp(Cp * sigma[i], -49 - ev);
+  Y[col * ldy + i] = ldexp(Cp * sigma[i], -48 - ev);
 }
 
 template <int NT>
@@ -380,7 +380,7 @@ void launch_gemm_nt(int NT, const int8_t* Kr, const int8_t* Vr, int KS, int pass
   }
 }
 
-// bits of V' so that n 2^{48.02 + bV} < P / 2 (float64-grade needs >= 48), capped at 53
+// bits of V' so that n 2^{47 + bV} < P / 2 (float64-grade needs >= 48), capped at 53
 int v_bits(int64_t n) {
   const double b = consts().log2P - 1.0 - CRT_KBITS_X100 / 100.0 - std::log2((double)n);
   return (int)std::min(53.0, std::floor(b - 1e-9));

@@ -3,31 +3,34 @@
 // src/precond.py:186, 189) at 3-4x the FP64 (DMMA) peak.
 //
 // Slicing (exact, deterministic):
-//   each row i of K gets sigma_i = 2^e with 2 max_j |K_ij| < sigma_i <= 4 max_j |K_ij|, each vector
-//   c of V gets tau_c likewise; x = K_ij / sigma_i in (-1/2, 1/2) is cut into S = 8 signed digits
-//   of the integer rint(x 2^56) (digits8: balanced base 128, d_7..d_1 in [-64, 63], d_0 in [-64, 64]):
-//       K_ij = sigma_i (sum_s d_s 2^{-7 (s+1)} + rho 2^{-56}),   |d_s| <= 64,  |rho| <= 1/2
-//   (round-to-nearest digits leave unbiased remainders, so the dropped terms do not add up
+//   each row i of K gets sigma_i = 2^e with 2.016 max_j |K_ij| < sigma_i <= 4.032 max_j |K_ij|, each
+//   vector c of V gets tau_c likewise; x = K_ij / sigma_i, |x| < 127 / 256, is cut into S = 7 signed
+//   digits of the integer rint(x 2^56) (digits7: balanced base 256, d_6..d_1 in [-128, 127], the top
+//   d_0 in [-127, 127] by the bound on |x|) -- the whole int8 range, 56 bits in 7 bytes:
+//       K_ij = sigma_i (sum_s d_s 2^{-8 (s+1)} + rho 2^{-56}),   |rho| <= 1/2
+//   (a round-to-nearest integer leaves an unbiased remainder, so the dropped terms do not add up
 //   coherently over the n-term sums).
-//   Then (K V^T)_ic = sigma_i tau_c sum_{s+t <= 7} 2^{-7 (s+t+2)} sum_j d_s[i,j] e_t[c,j] + err,
-//   36 int8 x int8 products accumulated EXACTLY in int32, combined in float64.  The dropped digits
-//   and slice pairs bound |err| <= ~2^-52 sigma_i tau_c per term of the j-sum: the float64 GEMM's
-//   own rounding level, scaled by the row / column maxima instead of the entries.
+//   Then (K V^T)_ic = sigma_i tau_c sum_{s+t <= 6} 2^{-8 (s+t+2)} sum_j d_s[i,j] e_t[c,j] + err,
+//   28 int8 x int8 products accumulated EXACTLY in int32, combined in float64.  The dropped digits
+//   and slice pairs (s + t >= 7: <= 6 x 2^14 x 2^-72 per term) bound |err| <= ~2^-52 sigma_i tau_c per
+//   term of the j-sum: the float64 GEMM's own rounding level, scaled by the row / column maxima
+//   instead of the entries.  (Round 2 first used 8 digits of 7 bits, |d| <= 64: the same 56 bits
+//   and the same dropped-term level with 36 pairs and 8 bytes per entry.)
 //
 // Kernel (one CTA per SM, 256 threads; grid = column passes x row tiles x k splits):
-//   warp 0  producer: per 32-column k-step ONE bulk copy (TMA engine) of all 8 K slices' tile
-//           (8 x 128 rows x 32 B = 32 KB) and one of all 8 V slices' (8 x 64 vectors x 32 B), both
+//   warp 0  producer: per 32-column k-step ONE bulk copy (TMA engine) of all 7 K slices' tile
+//           (7 x 128 rows x 32 B = 28 KB) and one of all 7 V slices' (7 x 64 vectors x 32 B), both
 //           stored pre-swizzled in the k-step-tiled global image (a 3-D TMA box with 32-byte rows
-//           moved 1536 32-byte rows per step and bound the product), 4-stage ring;
-//   warp 1  MMA issuer (one thread): the 36 slice pairs of a k-step as 12 tcgen05.mma kind::i8
+//           moved 1536 32-byte rows per step and bound the product), 5-stage ring;
+//   warp 1  MMA issuer (one thread): the 28 slice pairs of a k-step as 10 tcgen05.mma kind::i8
 //           M = 128, K = 32, N = 64..256 from shared-memory descriptors -- A slice s against the
-//           stacked V slices 0..7-s, pair (s, t) landing in the int32 TMEM accumulator of its
-//           diagonal d = s + t (8 x 64 columns = all 512) -- and a commit frees the stage;
+//           stacked V slices 0..6-s, pair (s, t) landing in the int32 TMEM accumulator of its
+//           diagonal d = s + t (7 x 64 columns) -- and a commit frees the stage;
 //   warp 2  TMEM owner;
-//   warps 4-7 drain: after the CTA's k range (<= 32768 columns: the int32 bound, 8 pairs x 64^2 x
-//           32768 = 2^30) they read the 8 accumulators (thread = row), form sum_d 2^{-7(d+2)} I_d
-//           in float64, scale by sigma_i tau_c and store.
-// k splits (at least n / 32768 of them) write float64 partials that a fixed-order reduce adds
+//   warps 4-7 drain: after the CTA's k range (<= 16384 columns: the int32 bound, 7 pairs x 128^2 x
+//           16384 = 7 2^28 < 2^31) they read the 7 accumulators (thread = row), form
+//           sum_d 2^{-8(d+2)} I_d in float64, scale by sigma_i tau_c and store.
+// k splits (at least n / 16384 of them) write float64 partials that a fixed-order reduce adds
 // (deterministic).
 #include <cuda.h>
 
@@ -43,20 +46,22 @@ namespace rld {
 
 namespace {
 
-constexpr int OZ_S = 8;             // digits per operand
-constexpr int OZ_DIAG = 8;          // diagonals d = s + t kept: 0 .. 7 (36 pairs)
+constexpr int OZ_S = OZ_NSLICES;    // 7 digits (bytes) per operand
+constexpr int OZ_DIAG = 7;          // diagonals d = s + t kept: 0 .. 6 (28 pairs)
+constexpr int OZ_DBITS = 8;         // bits per digit
 constexpr int OZ_BM = 128;          // K rows per tile (UMMA M)
 constexpr int OZ_BN = 64;           // vectors per column pass (UMMA N)
 constexpr int OZ_BK = 32;           // int8 columns per k-step (UMMA K for kind::i8, one 32-byte row)
-constexpr int OZ_STAGES = 4;
-constexpr int64_t OZ_KMAX = 32768;  // columns per CTA: <= 8 pairs x 64^2 x 32768 = 2^30 < 2^31 (exact int32)
+constexpr int OZ_STAGES = 5;
+constexpr int64_t OZ_KMAX = 16384;  // columns per CTA: <= 7 pairs x 128^2 x 16384 = 7 2^28 < 2^31 (exact int32)
 constexpr int OZ_THREADS = 256;
 constexpr uint32_t OZ_A_SLICE = OZ_BM * OZ_BK;            // 4 KB
 constexpr uint32_t OZ_B_SLICE = OZ_BN * OZ_BK;            // 2 KB
-constexpr uint32_t OZ_A_BYTES = OZ_S * OZ_A_SLICE;        // 32 KB
-constexpr uint32_t OZ_STAGE = OZ_A_BYTES + OZ_S * OZ_B_SLICE;   // 48 KB
+constexpr uint32_t OZ_A_BYTES = OZ_S * OZ_A_SLICE;        // 28 KB
+constexpr uint32_t OZ_STAGE = OZ_A_BYTES + OZ_S * OZ_B_SLICE;   // 42 KB
 constexpr int OZ_SMEM = OZ_STAGES * OZ_STAGE + 1024 + 256;
-constexpr uint32_t OZ_TMEM_COLS = OZ_DIAG * OZ_BN;        // 512
+constexpr uint32_t OZ_ACC_COLS = OZ_DIAG * OZ_BN;         // 448 accumulator columns
+constexpr uint32_t OZ_TMEM_COLS = 512;                    // allocation (a power of two)
 
 // UMMA shared-memory descriptor: K-major operand, 32-byte swizzle atoms (8 rows x 32 B), 8-row
 // groups 256 B apart -- the layout TMA writes for a box with a 32-byte inner dimension and
@@ -102,25 +107,26 @@ __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint
 
 // ---------------------------------------------------------------------------------------------
 // Slicing.  Global layout = the shared-memory image of one k-step: for tile t (TR rows) and k-step
-// ks (32 columns) the 8 slices' [TR][32]-byte tiles are contiguous, ((t KS + ks) 8 + s) TR 32 bytes,
+// ks (32 columns) the 7 slices' [TR][32]-byte tiles are contiguous, ((t KS + ks) 7 + s) TR 32 bytes,
 // each already in the 32-byte-swizzle order (Swizzle<1,4,3>: the two 16-byte halves of a row swap
 // in rows 4..7 of every 8-row atom) the UMMA descriptor expects -- so a stage is ONE bulk copy.
 // Rows >= rows and columns >= n are zero.
 
-// The 8 signed base-128 digits of x (|x| < 1/2): K = rint(x 2^56) (x 2^56 is exact in float64 or
-// rounds once; |K| < 2^55), then balanced digits from the bottom, d_s in [-64, 63] for s = 7..1 and
-// the top d_0 = what remains, in [-64, 64]:  x = sum_s d_s 2^{-7(s+1)} + rho 2^-56, |rho| <= 1/2.
-// Integer work on the ALU pipe (one F2I per entry): the float64 rint recursion it replaces kept the
-// XU pipe busy with 8 rounds and 8 conversions per entry.  Also returns K' = sum_{s<7} d_s 128^{6-s}
-// (the CRT integer, kv_crt.cu) and 8 - the number of leading zero digits.
+// The 7 signed base-256 digits of x (|x| <= 127 / 256 - 2^-10, guaranteed by scale_exponent):
+// K = rint(x 2^56) (x 2^56 is exact in float64 or rounds once), then balanced digits from the bottom,
+// d_s in [-128, 127] for s = 6..1 and the top d_0 = what remains: |K| 2^-48 <= 127 - 2^-2 and the
+// carry adds at most 1/2, so |d_0| <= 127 and every digit is an int8:
+// x = sum_s d_s 2^{-8(s+1)} + rho 2^-56, |rho| <= 1/2.  Integer work on the ALU pipe (one F2I per
+// entry).  Also returns K' = sum_{s<6} d_s 256^{5-s} (the CRT integer, kv_crt.cu) and 7 - the number
+// of leading zero digits.
 __device__ __forceinline__ void digits8(double x, int (&d)[OZ_S], long long& kprime, int& nz) {
   long long k = __double2ll_rn(x * 72057594037927936.0);   // x 2^56
   nz = 0;
 #pragma unroll
   for (int s = OZ_S - 1; s >= 1; --s) {
-    const int dd = (int)((k + 64) & 127) - 64;
+    const int dd = (int)((k + 128) & 255) - 128;
     d[s] = dd;
-    k = (k - dd) >> 7;   // exact
+    k = (k - dd) >> OZ_DBITS;   // exact
     if (s == OZ_S - 1) kprime = k;
     if (dd != 0) nz = OZ_S - s;
   }
@@ -128,7 +134,16 @@ __device__ __forceinline__ void digits8(double x, int (&d)[OZ_S], long long& kpr
   if (k != 0) nz = OZ_S;
 }
 
-// scale[row] = sigma = 2^e with 2 max_j |A_row,j| < sigma <= 4 max (1 for an all-zero row)
+// Exponent e of the scale sigma = 2^(e+1) for a row (vector) of maximum mx = f 2^e', f in [0.5, 1):
+// e = e', or e' + 1 when f > 63/64, so that |x| = |a| / sigma <= 63/128 and the top base-256 digit of
+// rint(x 2^56) stays within int8 (digits8: |d_0| <= 126.5)
+__host__ __device__ inline int oz_scale_exp(double mx) {
+  int e = 0;
+  const double f = frexp(mx, &e);
+  return f > 0.984375 ? e + 1 : e;
+}
+
+// scale[row] = sigma = 2^e with 2 max_j |A_row,j| < sigma <= 4.07 max (1 for an all-zero row)
 __global__ void ozaki_scale_kernel(const double* __restrict__ A, int64_t lda, int64_t n, double* __restrict__ scale) {
   const int64_t row = blockIdx.x;
   const double* a = A + row * lda;
@@ -140,9 +155,7 @@ __global__ void ozaki_scale_kernel(const double* __restrict__ A, int64_t lda, in
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
-    int e = 0;
-    if (mx > 0.0) frexp(mx, &e);            // mx = f 2^e, f in [0.5, 1): |a| / 2^(e+1) < 1/2
-    scale[row] = mx > 0.0 ? ldexp(1.0, e + 1) : 1.0;
+    scale[row] = mx > 0.0 ? ldexp(1.0, oz_scale_exp(mx) + 1) : 1.0;   // |a| / sigma <= 63/128
   }
 }
 
@@ -164,12 +177,10 @@ __global__ void ozaki_scale_finish_kernel(int64_t rows, double* __restrict__ sca
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= rows) return;
   const double mx = __longlong_as_double((long long)reinterpret_cast<unsigned long long*>(scale)[i]);
-  int e = 0;
-  if (mx > 0.0) frexp(mx, &e);
-  scale[i] = mx > 0.0 ? ldexp(1.0, e + 1) : 1.0;
+  scale[i] = mx > 0.0 ? ldexp(1.0, oz_scale_exp(mx) + 1) : 1.0;
 }
 
-// one thread per (padded row, 16-column half of a k-step): 8 exact digits of 16 entries of A / sigma,
+// one thread per (padded row, 16-column half of a k-step): 7 exact digits of 16 entries of A / sigma,
 // written as one 16-byte store per slice (the half lands at byte 16 h ^ 16 in rows 4..7 of an atom)
 template <int TR>
 __global__ void ozaki_digits_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int64_t n,
@@ -232,8 +243,7 @@ ozaki_points_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, in
   constexpr int PARTS = OZ_BK / EL;          // threads per (row, k-step)
   constexpr int W = EL / 4;                  // 32-bit words per slice
   const int d = kp.d;
-  int ee = 0;
-  frexp(kp.diag > 0.0 ? kp.diag : 1.0, &ee);   // diag = f 2^ee: sigma = 2^(ee+1), x = v 2^-(ee+1)
+  const int ee = oz_scale_exp(kp.diag > 0.0 ? kp.diag : 1.0);   // sigma = 2^(ee+1), x = v 2^-(ee+1)
   const double scl = ldexp(1.0, -(ee + 1));    // exact power of two
   const int64_t total = ceil_div(rows, TR) * TR * KS * PARTS;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -250,7 +260,7 @@ ozaki_points_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, in
     for (int k = 0; k < DMAX; ++k) xi[k] = (k < d && row < rows) ? X[gi * d + k] : 0.0;
     uint32_t w[OZ_S][W];
     long long kq[EL];   // CRT: K' of the EL entries
-    int nz = 0;         // slices from the first nonzero digit of any of the EL entries: 8 - leading zero slices
+    int nz = 0;         // slices from the first nonzero digit of any of the EL entries: 7 - leading zero slices
 #pragma unroll
     for (int k = 0; k < EL; ++k) {
       const int64_t j = j0 + k;
@@ -417,7 +427,7 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
 #pragma unroll
       for (int e = 0; e < 32; ++e) z[e] = 0u;
 #pragma unroll 1
-      for (int c = 0; c < (int)OZ_TMEM_COLS; c += 32) ptx::tmem_st_32x32b_x32(tmem + lb + (uint32_t)c, z);
+      for (int c = 0; c < (int)OZ_ACC_COLS; c += 32) ptx::tmem_st_32x32b_x32(tmem + lb + (uint32_t)c, z);
       ptx::tmem_wait_st();
     }
     ptx::tc_fence_before();
@@ -463,9 +473,9 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
         const uint32_t a0 = sbase + st * OZ_STAGE;
         const uint32_t b0 = a0 + OZ_A_BYTES;
         const int lz = lead(s);
-        // A slice sa against the stacked B slices 0 .. 7 - sa at once: the accumulators of the
-        // diagonals d = sa + t are adjacent TMEM column blocks, so one N = 64 (8 - sa) product
-        // (in N <= 256 pieces) covers the whole row of pairs -- 12 MMAs per k-step instead of 36
+        // A slice sa against the stacked B slices 0 .. 6 - sa at once: the accumulators of the
+        // diagonals d = sa + t are adjacent TMEM column blocks, so one N = 64 (7 - sa) product
+        // (in N <= 256 pieces) covers the whole row of pairs -- 10 MMAs per k-step instead of 28
         // N = 64 ones, and the A operand is read from shared memory once per piece
 #pragma unroll
         for (int sa = 0; sa < OZ_S; ++sa) {
@@ -504,7 +514,7 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
       if (steps > 0) {
 #pragma unroll 1
         for (int d = nd - 1; d >= 0; --d) {   // small terms first
-          const double w = __longlong_as_double((long long)(1023 - 7 * (d + 2)) << 52);   // 2^{-7(d+2)}
+          const double w = __longlong_as_double((long long)(1023 - OZ_DBITS * (d + 2)) << 52);   // 2^{-8(d+2)}
           uint32_t v[32];
           ptx::tmem_ld_32x32b_x32(tmem + lane_base + (uint32_t)(d * OZ_BN + c0), v);
           ptx::tmem_wait_ld();
@@ -578,8 +588,7 @@ void ozaki_slice_points(const double* X, int64_t n, const KernelParams& kp, int6
                         double* scale, cudaStream_t st, int8_t* Kr, int* knz) {
   if (rows <= 0) return;
   if (kp.d > RLD_MAX_DIM) fail(RLD_ERR_NOT_SUPPORTED, "ozaki_slice_points: d > 32");
-  int ee = 0;
-  frexp(kp.diag > 0.0 ? kp.diag : 1.0, &ee);
+  const int ee = oz_scale_exp(kp.diag > 0.0 ? kp.diag : 1.0);
   oz_fill_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, st>>>(rows, ldexp(1.0, ee + 1), scale);
   RLD_LAUNCH_CHECK();
   const int64_t KS = ceil_div(n, OZ_BK);
@@ -603,7 +612,7 @@ void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int6
                       int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st, int diags,
                       const int* knz) {
   if (m <= 0 || rows <= 0) return;
-  if (diags < 1 || diags > OZ_DIAG) fail(RLD_ERR_INVALID_ARGUMENT, "kv_product_ozaki: diagonals must be 1..8");
+  if (diags < 1 || diags > OZ_DIAG) fail(RLD_ERR_INVALID_ARGUMENT, "kv_product_ozaki: diagonals must be 1..7");
   ws.oz_vq.reserve((size_t)ozaki_bytes(m, n, OZ_BN));
   ws.oz_tau.reserve(sizeof(double) * m);
   ozaki_slice(V, ldv, m, n, OZ_BN, ws.oz_vq.as<int8_t>(), ws.oz_tau.as<double>(), st);

@@ -516,7 +516,7 @@ void to_resident_order(rld_handle* h, int64_t m, double* V, int64_t ld) {
 // Y (m x rows) = V (m x n full) K^T restricted to the local rows.  tc_mode 1 =
 // single-pass TF32 on the tensor cores (power-iteration sketch products only),
 // 3 = 3xTF32 (everything whose value enters the estimate directly).
-void kv(rld_handle* h, int64_t m, const double* Vfull, double* Y, int tc_mode = 3, int oz_diags = 8) {
+void kv(rld_handle* h, int64_t m, const double* Vfull, double* Y, int tc_mode = 3, int oz_diags = 7) {
   KvOperand op = h->res.op();
   op.tc_mode = tc_mode;
   op.oz_diags = oz_diags;
@@ -817,17 +817,17 @@ struct PrecondOut {
 // 2.7e-4 (all iterations) and 2.1e-4 (all but the last), beyond the 1e-4 fp32
 // budget, so the default is 3xTF32 everywhere; RLD_SKETCH_MODE=1 opts in to
 // single-pass TF32 for the early iterations.
-// Slice-pair diagonals of the float64 int8-slice product in the first q-1 power iterations: 7
-// (28 of the 36 pairs, dropped terms ~2^-51 of max|K| max|V| per sum term) -- those iterations only
+// Slice-pair diagonals of the float64 int8-slice product in the first q-1 power iterations: 6
+// (21 of the 28 pairs, dropped terms ~2^-50 of max|K| max|V| per sum term) -- those iterations only
 // steer the subspace, which the last full-precision iteration re-forms.  The last iteration,
-// B = Q K Q^T and every Lanczos product keep all 8 diagonals; with a CRT residue image the wide
+// B = Q K Q^T and every Lanczos product keep all 7 diagonals; with a CRT residue image the wide
 // products run as modular GEMMs instead (full precision).  Measured on config 3 (Morton order,
-// slices) against the float64 golden value: 8 diagonals 5.5e-15 (350 ms), 7: 4.7e-15 (321 ms),
-// 6: 5.6e-14 (304 ms).  RLD_FP64_SKETCH_DIAGS (1..8, read per call) overrides.
+// 8 x 7-bit slices) against the float64 golden value: all diagonals 5.5e-15, one fewer 4.7e-15, two
+// fewer 5.6e-14.  RLD_FP64_SKETCH_DIAGS (1..7, read per call) overrides.
 int sketch_oz_diags() {
   const char* e = getenv("RLD_FP64_SKETCH_DIAGS");
-  const int v = e ? atoi(e) : 7;
-  return v < 1 ? 1 : (v > 8 ? 8 : v);
+  const int v = e ? atoi(e) : 6;
+  return v < 1 ? 1 : (v > 7 ? 7 : v);
 }
 
 int sketch_tc_mode() {
@@ -876,7 +876,7 @@ int lowrank_randsvd(rld_handle* h, const rld_config* c, const rld_inputs* in, Pr
       RLD_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), st));
       for (int it = 0; it < c->precond_iters; ++it) {
         const bool last = it + 1 == c->precond_iters;
-        kv(h, w, Y, Z, last ? 3 : sketch_tc_mode(), last ? 8 : sketch_oz_diags());   // Y <- Y M (src/precond.py:186)
+        kv(h, w, Y, Z, last ? 3 : sketch_tc_mode(), last ? 7 : sketch_oz_diags());   // Y <- Y M (src/precond.py:186)
         if (householder) {
           qr_householder(h, nl, w, Z, c->orth_rtol, flags);
           gather_rows(h, Z, w, Y);
@@ -1684,9 +1684,9 @@ int rld_slice_stats(rld_handle* h, int64_t* stats) {
     const int64_t nb = ceil_div(r.rows, 128) * ceil_div(r.n, 32);
     stats[0] = nb;
     stats[3] = r.kr_ready ? 1 : 0;
-    if (!r.knz_ready) {   // no metadata: every block reads all 8 slices, 36 pairs
-      stats[1] = 8 * nb;
-      stats[2] = 36 * nb;
+    if (!r.knz_ready) {   // no metadata: every block reads all 7 slices, 28 pairs
+      stats[1] = 7 * nb;
+      stats[2] = 28 * nb;
       return;
     }
     std::vector<int> nz((size_t)nb);

@@ -107,7 +107,7 @@ struct KvOperand {
   int64_t row0 = 0;          // first global row held locally
   int64_t rows = 0;          // local rows
   int tc_mode = 3;           // tensor-core product: 3 = 3xTF32 (Lanczos), 1 = 1xTF32 (sketch)
-  int oz_diags = 8;          // float64 int8-slice product: slice-pair diagonals kept (8 = all 36 pairs)
+  int oz_diags = 7;          // float64 int8-slice product: slice-pair diagonals kept (7 = all 28 pairs)
   const int8_t* kr = nullptr;      // K' residues modulo the CRT moduli (kv_crt.cu), or null
   const float* rowscale = nullptr; // tiled fp32 K: per-row power-of-two scales (kv_otf.cu stored products)
   const uint32_t* otf_skip = nullptr;  // on the fly: (tile, k-step) far-field skip bits (kv_otf.cu), or null

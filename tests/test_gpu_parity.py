@@ -205,10 +205,11 @@ def test_exact_logdet_matches_cholesky(rld, golden_cases):
 def test_fixture_rows_ill_posed(rld, fixture_rows):
     """The reference's own fixture (RBF d=1, jitter 1e-6, cond ~ 2e8): a 1e-15 relative
     perturbation of K moves these estimates by 1e-5 .. 3e-4 (their `sensitivity`), so two
-    correct float64 implementations differ at that level.  Pinned at 10x the row's own
-    sensitivity (<= 3.2e-3; measured worst gap 6x, scripts/tolerance_probe.py), both from the
-    points (K built on the device from direct differences) and from the oracle's dense K (the
-    reference's r^2 formula)."""
+    correct float64 implementations differ at that level.  Pinned at 25x the row's own
+    (single-sample) sensitivity, capped at 1e-3 (SURVEY: these rows pin results to ~1e-3); measured
+    gaps 3e-6 .. 4.3e-4 with either float64 product, worst gap / sensitivity 10.4 on the int8
+    slices and 6.0 on DMMA (scripts/tolerance_probe.py), both from the points (K built on the
+    device from direct differences) and from the oracle's dense K (the reference's r^2 formula)."""
     from paper_2405_03474_b200.linalg import Rng
 
     for r in fixture_rows:
@@ -216,7 +217,7 @@ def test_fixture_rows_ill_posed(rld, fixture_rows):
         cfg = rld.EstimatorConfig(r["algorithm"], r["s"], r["t"], "rademacher",
                                   rld.PreconditionerConfig("rand-svd", r["precond_rank"], r["precond_iters"],
                                                            max(r["jitter"], 1e-12)), r["seed"])
-        tol = max(1e-6, 10.0 * r["sensitivity"])
+        tol = max(1e-6, min(1e-3, 25.0 * r["sensitivity"]))
         est = rld.rstar_logdet(rld.KernelMatrix(rld.KernelSpec("rbf", jitter=r["jitter"]), pts), cfg)
         assert rel(est.value, r["estimate"]) <= tol, (r, est.value)
         K = O.covariance_block("rbf", 1.0, 1.0, r["jitter"], pts)

@@ -72,12 +72,13 @@ def fp64_product(monkeypatch, request):
 
 @pytest.mark.parametrize("fp64_product", ["dmma", "ozaki"], indirect=True)
 @pytest.mark.parametrize("n,m", [(16, 1), (17, 3), (1000, 33), (4099, 37), (4096, 64), (3001, 65), (2048, 129),
-                                 (5000, 300), (20000, 8), (40000, 5)])
+                                 (5000, 300), (20000, 8), (40000, 5), (1000, 90), (3000, 81), (2500, 16), (2500, 80)])
 def test_fp64_tensor_core_product(rld, fp64_product, n, m):
     """DMMA: within 1e-14 of the entries' own scale sum_j |K_ij| |V_cj| (a float64 GEMM).  INT8
     slices (kv_ozaki.cu): the digits are exact relative to the row / column maxima, so the bound is
     n sigma_i tau_c-scaled: |err_ic| <= 2^-50 n max_j |K_ij| max_j |V_cj| (measured ~1e-16 of it);
-    n = 40000 runs two k splits."""
+    n = 40000 runs two k splits; m mod 64 in 1..16 / 17..32 runs the narrow (16 / 32-vector) last
+    column pass."""
     import torch
 
     from paper_2405_03474_b200.workloads import baseline
@@ -159,6 +160,28 @@ def test_fp64_product_under_concurrency(rld, fp64_product):
     assert not bad, bad[:5]
 
 
+@pytest.mark.parametrize("m", [10, 74, 90, 522])
+def test_int8_slices_morton_narrow_last_pass(rld, m):
+    """Config-3 style points (d = 2: Morton order, leading all-zero slices skipped) with a last column
+    pass of 10 / 26 vectors (16- / 32-vector V tile): the product against float64 numpy within the
+    slice error bound, bit-identical on repeat."""
+    import torch
+
+    from paper_2405_03474_b200.workloads import baseline
+
+    n = 6000
+    wl = baseline(3, n=n)
+    R = rld.ResidentMatrix(rld.KernelMatrix(wl.spec, wl.points), dtype="fp64", path="stored")
+    V = np.random.default_rng(m).standard_normal((m, n))
+    Y = R.kv_apply(torch.from_numpy(V).cuda()).cpu().numpy()
+    K = O.covariance_block(wl.spec.family, wl.spec.amplitude, wl.spec.length_scale, wl.spec.jitter, wl.points)
+    ref = V @ K.T
+    scale = n * np.outer(np.abs(V).max(axis=1), np.abs(K).max(axis=1))
+    assert np.max(np.abs(Y - ref) / scale) <= 2.0 ** -50
+    assert np.max(np.abs(Y - ref)) <= 1e-13 * np.max(np.abs(ref))
+    assert np.array_equal(Y, R.kv_apply(torch.from_numpy(V).cuda()).cpu().numpy())
+
+
 def test_int8_slices_from_points_equal_slices_from_K(rld, monkeypatch):
     """Stored float64 from the points slices K straight from the points (no float64 K in HBM); from
     a dense device K built by build_covariance it slices the stored rows: same entries, same row
@@ -206,9 +229,9 @@ def test_int8_slices_edge_cases(rld, monkeypatch, n, m):
 
 @pytest.mark.parametrize("index", [1, 2])
 def test_fp64_sketch_diagonals(rld, index, monkeypatch):
-    """The first q-1 power iterations run the int8-slice float64 product with 7 of its 8 slice-pair
+    """The first q-1 power iterations run the int8-slice float64 product with 6 of its 7 slice-pair
     diagonals (rld_api.cu sketch_oz_diags); the last iteration, B = Q K Q^T and the Lanczos products
-    keep all 36 pairs.  The estimate must stay float64-grade: within 1e-12 of the all-pairs run and
+    keep all 28 pairs.  The estimate must stay float64-grade: within 1e-12 of the all-pairs run and
     of the unmodified reference's golden value (north_star fp64 bar: 1e-6)."""
     import json
     from dataclasses import replace
@@ -221,7 +244,7 @@ def test_fp64_sketch_diagonals(rld, index, monkeypatch):
     wl = baseline(index, dtype="fp64")
     cfg = replace(wl.config, dtype="fp64", path="stored")
     R = rld.ResidentMatrix(rld.KernelMatrix(wl.spec, wl.points), dtype="fp64", path="stored")
-    monkeypatch.setenv("RLD_FP64_SKETCH_DIAGS", "8")
+    monkeypatch.setenv("RLD_FP64_SKETCH_DIAGS", "7")
     full = R.estimate(cfg)
     monkeypatch.delenv("RLD_FP64_SKETCH_DIAGS")
     default = R.estimate(cfg)
