@@ -577,8 +577,9 @@ def parity_vs_golden(wl, value):
 
 
 def extra_fp32(args, rld, world, sharded, per_step):
-    """Config 3 in fp32 (BASELINE's stated precision): stored fp32 K, 3xTF32 tensor-core products;
-    3 timed estimates after 2 warm-ups, CUDA events, max over ranks."""
+    """Config 3 in fp32 (BASELINE's stated precision): stored K -- on one GPU as 3 int8 slices from
+    the Morton-ordered points (INT8 tensor cores), sharded as fp32 tiles (3xTF32 / fp16 tensor-core
+    products); 3 timed estimates after 2 warm-ups, CUDA events, max over ranks."""
     import torch
 
     wl = workload_for(args, dtype="fp32")
@@ -610,16 +611,26 @@ def extra_fp32(args, rld, world, sharded, per_step):
         R.kv_apply(V)
     k1.record(st)
     torch.cuda.synchronize()
+    import ctypes as C
+
+    stats = (C.c_int64 * 4)()
+    kv_ms = k0.elapsed_time(k1) / 10
+    if R.sess.lib.rld_slice_stats(R.sess.handle.ptr, stats) == 0 and stats[0] > 0:
+        # float32 K from Morton-ordered points: 3 int8 slices on the INT8 tensor cores (kv_ozaki.cu)
+        roof = roofline_slices(r1 - r0, wl.n, cfg.num_probes, kv_ms, int(stats[0]), int(stats[1]), int(stats[2]),
+                               "Lanczos block m=s", kslices=3)
+    else:
+        roof = roofline_for(wl, cfg, r1 - r0, wl.n, cfg.num_probes, kv_ms, world)
     out = {"value": per_step * K / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms / K, "dtype": "f32",
            "config": workload_config(wl, world, sharded),
-           "roofline": roofline_for(wl, cfg, r1 - r0, wl.n, cfg.num_probes, k0.elapsed_time(k1) / 10, world),
+           "roofline": roof, "phase_ms_last_step": dict(zip(("precond", "lanczos"), (est.phase_ms[1], est.phase_ms[4]))),
            "parity": parity_vs_golden(wl, est.value)}
     del R
     torch.cuda.empty_cache()
     return out
 
 
-def roofline_slices(rows, n, m, ms, blocks, slices, pairs, what):
+def roofline_slices(rows, n, m, ms, blocks, slices, pairs, what, kslices=7):
     """The float64 product on exact int8 slices (csrc/kv_ozaki.cu) with its all-zero leading slices
     skipped (points in Morton order): algorithmic bytes = the K slices actually read (rld_slice_stats)
     plus V in and Y out; int8 work = the slice pairs multiplied, each a 128 x 64 x 32 MMA per block
@@ -633,12 +644,13 @@ def roofline_slices(rows, n, m, ms, blocks, slices, pairs, what):
     i8_peak = rec.get("tops", pipe.get("i8_ss_n256", {}).get("tops", 4576.0))
     t = ms * 1e-3
     f_hbm, f_t = alg_bytes / t / 1e9 / hbm_peak, ops / t / 1e12 / i8_peak
-    key = f"kv_product|fp64-int8slices|stored|n={n}|rows={rows}|m={m}"
+    key = f"kv_product|{'fp64' if kslices == 7 else 'fp32'}-int8slices|stored|n={n}|rows={rows}|m={m}"
     traffic, traffic_src = ncu_traffic(key)
+    tot_s, tot_p, kname = (7, 28, "float64 K") if kslices == 7 else (3, 9, "float32 K (24 bits of the row scale, 3 x 4 slices)")
     common = {"traffic": traffic, "traffic_source": traffic_src, "traffic_key": key, "kernel_ms": ms,
-              "kernel": f"kv_product (tcgen05 kind::i8 on exact int8 slices of float64 K, {what}={m}, {rows} rows; "
-                        f"{slices / blocks:.2f} of 7 slices (8-bit digits) and {pairs / blocks:.1f} of 28 pairs per block after "
-                        f"skipping all-zero leading slices)",
+              "kernel": f"kv_product (tcgen05 kind::i8 on exact int8 slices of {kname}, {what}={m}, {rows} rows; "
+                        f"{slices / blocks:.2f} of {tot_s} slices (8-bit digits) and {pairs / blocks:.1f} of {tot_p} pairs per "
+                        f"block after skipping all-zero leading slices)",
               "alg_bytes": alg_bytes, "int8_ops": ops, "hbm_frac": f_hbm, "int8_tensor_frac": f_t,
               "equiv_fp64_tflops": 2.0 * rows * n * m / t / 1e12,
               "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}); int8: profiles/r02c_pipe_peaks.json "

@@ -265,10 +265,11 @@ int rld_dense_eigh(rld_handle* h, int32_t n, double* A, double* w);
  * resident problem's K in float64 on the device. */
 int rld_exact_logdet(rld_handle* h, double* value);
 
-/* Work of the float64 int8-slice product on the resident K (no reference counterpart: the
- * measurement hook of bench.py's roofline).  stats[0..3] = the 128 x 32 blocks of the slice image,
- * the K slices a product reads over them (leading all-zero slices are skipped), the slice pairs it
- * multiplies (s + t <= 7), and 1 if the wide (sketch) products run on the CRT residue image
+/* Work of the int8-slice product on the resident K (no reference counterpart: the measurement
+ * hook of bench.py's roofline).  stats[0..3] = the 128 x 32 blocks of the slice image, the K slices
+ * a product reads over them (of 7 per block for a float64 K, 3 for a float32 K from Morton-ordered
+ * points; leading all-zero slices are skipped), the slice pairs it multiplies (s + t <= 6 of 7 x 7,
+ * or s + t <= 3 of 3 x 4), and 1 if the wide (sketch) products run on the CRT residue image
  * instead.  All 0 when the resident K has no slice image. */
 int rld_slice_stats(rld_handle* h, int64_t* stats);
 

@@ -46,22 +46,28 @@ namespace rld {
 
 namespace {
 
-constexpr int OZ_S = OZ_NSLICES;    // 7 digits (bytes) per operand
-constexpr int OZ_DIAG = 7;          // diagonals d = s + t kept: 0 .. 6 (28 pairs)
+constexpr int OZ_S = OZ_NSLICES;    // float64: 7 digits (bytes) per operand, diagonals d = s + t <= 6 (28 pairs)
+constexpr int OZ_S32 = 3;           // float32 K: 3 digits (24 bits relative to the row scale) ...
+constexpr int OZ_V32 = 4;           // ... against 4 digits of V, diagonals d <= 3 (9 pairs)
 constexpr int OZ_DBITS = 8;         // bits per digit
 constexpr int OZ_BM = 128;          // K rows per tile (UMMA M)
 constexpr int OZ_BN = 64;           // vectors per column pass (UMMA N)
 constexpr int OZ_BK = 32;           // int8 columns per k-step (UMMA K for kind::i8, one 32-byte row)
-constexpr int OZ_STAGES = 5;
 constexpr int64_t OZ_KMAX = 16384;  // columns per CTA: <= 7 pairs x 128^2 x 16384 = 7 2^28 < 2^31 (exact int32)
 constexpr int OZ_THREADS = 256;
 constexpr uint32_t OZ_A_SLICE = OZ_BM * OZ_BK;            // 4 KB
 constexpr uint32_t OZ_B_SLICE = OZ_BN * OZ_BK;            // 2 KB
-constexpr uint32_t OZ_A_BYTES = OZ_S * OZ_A_SLICE;        // 28 KB
-constexpr uint32_t OZ_STAGE = OZ_A_BYTES + OZ_S * OZ_B_SLICE;   // 42 KB
-constexpr int OZ_SMEM = OZ_STAGES * OZ_STAGE + 1024 + 256;
-constexpr uint32_t OZ_ACC_COLS = OZ_DIAG * OZ_BN;         // 448 accumulator columns
-constexpr uint32_t OZ_TMEM_COLS = 512;                    // allocation (a power of two)
+// SA digits of K against SB >= SA digits of V, pairs s + t <= SB - 1 (one TMEM accumulator per diagonal)
+template <int SA, int SB>
+struct OzCfg {
+  static constexpr uint32_t A_BYTES = SA * OZ_A_SLICE;          // 28 KB (float64) / 12 KB (float32)
+  static constexpr uint32_t B_BYTES = SB * OZ_B_SLICE;          // 14 KB / 8 KB
+  static constexpr uint32_t STAGE = A_BYTES + B_BYTES;          // 42 KB / 20 KB
+  static constexpr int STAGES = SA == OZ_S ? 5 : 8;
+  static constexpr int SMEM = STAGES * (int)STAGE + 1024 + 256;
+  static constexpr uint32_t ACC_COLS = SB * OZ_BN;              // 448 / 256 accumulator columns
+  static constexpr uint32_t TMEM_COLS = ACC_COLS <= 256 ? 256 : 512;   // allocation (a power of two)
+};
 
 // UMMA shared-memory descriptor: K-major operand, 32-byte swizzle atoms (8 rows x 32 B), 8-row
 // groups 256 B apart -- the layout TMA writes for a box with a 32-byte inner dimension and
@@ -119,19 +125,21 @@ __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint
 // x = sum_s d_s 2^{-8(s+1)} + rho 2^-56, |rho| <= 1/2.  Integer work on the ALU pipe (one F2I per
 // entry).  Also returns K' = sum_{s<6} d_s 256^{5-s} (the CRT integer, kv_crt.cu) and 7 - the number
 // of leading zero digits.
-__device__ __forceinline__ void digits8(double x, int (&d)[OZ_S], long long& kprime, int& nz) {
-  long long k = __double2ll_rn(x * 72057594037927936.0);   // x 2^56
+template <int S>
+__device__ __forceinline__ void digits8(double x, int (&d)[S], long long& kprime, int& nz) {
+  long long k = __double2ll_rn(x * (double)(1ull << (OZ_DBITS * S)));   // x 2^56 (S = 7)
   nz = 0;
+  kprime = 0;
 #pragma unroll
-  for (int s = OZ_S - 1; s >= 1; --s) {
+  for (int s = S - 1; s >= 1; --s) {
     const int dd = (int)((k + 128) & 255) - 128;
     d[s] = dd;
     k = (k - dd) >> OZ_DBITS;   // exact
-    if (s == OZ_S - 1) kprime = k;
-    if (dd != 0) nz = OZ_S - s;
+    if (s == S - 1) kprime = k;
+    if (dd != 0) nz = S - s;
   }
   d[0] = (int)k;
-  if (k != 0) nz = OZ_S;
+  if (k != 0) nz = S;
 }
 
 // Exponent e of the scale sigma = 2^(e+1) for a row (vector) of maximum mx = f 2^e', f in [0.5, 1):
@@ -182,7 +190,7 @@ __global__ void ozaki_scale_finish_kernel(int64_t rows, double* __restrict__ sca
 
 // one thread per (padded row, 16-column half of a k-step): 7 exact digits of 16 entries of A / sigma,
 // written as one 16-byte store per slice (the half lands at byte 16 h ^ 16 in rows 4..7 of an atom)
-template <int TR>
+template <int TR, int S>
 __global__ void ozaki_digits_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int64_t n,
                                     const double* __restrict__ scale, int64_t KS, int8_t* __restrict__ q) {
   const int64_t total = ceil_div(rows, TR) * TR * KS * 2;
@@ -201,18 +209,18 @@ __global__ void ozaki_digits_kernel(const double* __restrict__ A, int64_t lda, i
     // overflow / underflow of the multiplier for extreme scales)
     const bool mul = ee > -1000 && ee < 1000;
     const double f = mul ? __longlong_as_double((long long)(1023 + 1 - ee) << 52) : 1.0;
-    uint32_t w[OZ_S][4];
+    uint32_t w[S][4];
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
       const int64_t j = j0 + k;
       const double a = (row < rows && j < n) ? A[row * lda + j] : 0.0;
       const double r = mul ? a * f : ldexp(a, 1 - ee);
-      int dg[OZ_S];
+      int dg[S];
       long long kp;
       int nzk;
-      digits8(r, dg, kp, nzk);
+      digits8<S>(r, dg, kp, nzk);
 #pragma unroll
-      for (int s = 0; s < OZ_S; ++s) {
+      for (int s = 0; s < S; ++s) {
         const uint32_t b = (uint32_t)(uint8_t)(int8_t)dg[s];
         if ((k & 3) == 0) w[s][k >> 2] = b;
         else w[s][k >> 2] |= b << (8 * (k & 3));
@@ -220,9 +228,9 @@ __global__ void ozaki_digits_kernel(const double* __restrict__ A, int64_t lda, i
     }
     const uint32_t o = (uint32_t)(i * OZ_BK + 16 * h);
     const uint32_t phys = o ^ (((o >> 7) & 1u) << 4);
-    int8_t* base = q + (t * KS + ks) * (int64_t)OZ_S * TR * OZ_BK + phys;
+    int8_t* base = q + (t * KS + ks) * (int64_t)S * TR * OZ_BK + phys;
 #pragma unroll
-    for (int s = 0; s < OZ_S; ++s)
+    for (int s = 0; s < S; ++s)
       *reinterpret_cast<uint4*>(base + (int64_t)s * TR * OZ_BK) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
   }
 }
@@ -235,7 +243,7 @@ __global__ void ozaki_digits_kernel(const double* __restrict__ A, int64_t lda, i
 // swizzled position, ((t L + l) KS + ks) 4096 + phys -- in the same pass (no second read of the
 // 34 GB slice image).  Thread = EL consecutive columns of one row (EL = 8: 80 registers, 3 CTAs per
 // SM; 16 columns per thread held 128 registers and ran at 25 % occupancy, latency-bound).
-template <bool CRT, int EL, int DMAX>
+template <bool CRT, int EL, int DMAX, int S>
 __global__ void __launch_bounds__(256)
 ozaki_points_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, int64_t row0,
                     int64_t rows, int64_t KS, int8_t* __restrict__ q, int8_t* __restrict__ Kr, int* __restrict__ knz) {
@@ -258,7 +266,7 @@ ozaki_points_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, in
     double xi[DMAX];   // DMAX = 4: registers (d <= 4), else local memory
 #pragma unroll
     for (int k = 0; k < DMAX; ++k) xi[k] = (k < d && row < rows) ? X[gi * d + k] : 0.0;
-    uint32_t w[OZ_S][W];
+    uint32_t w[S][W];
     long long kq[EL];   // CRT: K' of the EL entries
     int nz = 0;         // slices from the first nonzero digit of any of the EL entries: 7 - leading zero slices
 #pragma unroll
@@ -280,13 +288,13 @@ ozaki_points_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, in
           v = kernel_value_f64(kp, r2);
         }
       }
-      int dg[OZ_S];
+      int dg[S];
       long long kp;
       int nzk;
-      digits8(v * scl, dg, kp, nzk);
+      digits8<S>(v * scl, dg, kp, nzk);
       if (nzk > nz) nz = nzk;
 #pragma unroll
-      for (int s = 0; s < OZ_S; ++s) {
+      for (int s = 0; s < S; ++s) {
         const uint32_t b = (uint32_t)(uint8_t)(int8_t)dg[s];
         if ((k & 3) == 0) w[s][k >> 2] = b;
         else w[s][k >> 2] |= b << (8 * (k & 3));
@@ -300,9 +308,9 @@ ozaki_points_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, in
     }
     const uint32_t o = (uint32_t)(i * OZ_BK + EL * h);
     const uint32_t phys = o ^ (((o >> 7) & 1u) << 4);
-    int8_t* base = q + (t * KS + ks) * (int64_t)OZ_S * TR * OZ_BK + phys;
+    int8_t* base = q + (t * KS + ks) * (int64_t)S * TR * OZ_BK + phys;
 #pragma unroll
-    for (int s = 0; s < OZ_S; ++s) {
+    for (int s = 0; s < S; ++s) {
       if (W == 4)
         *reinterpret_cast<uint4*>(base + (int64_t)s * TR * OZ_BK) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
       else
@@ -385,17 +393,22 @@ __global__ void oz_split_reduce_kernel(const double* __restrict__ part, int spli
 }
 
 // ---------------------------------------------------------------------------------------------
+// SA K digits against SB V digits (float64: 7 x 7; float32 K: 3 x 4), pairs s + t <= nd - 1 <= SB - 1.
+// k-steps whose kept K slices are all zero (lz >= min(SA, nd)) are left out by the producer and the
+// MMA thread alike (same metadata, same sequence of kept steps): no load, no handshake.
+template <int SA, int SB>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
 ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, int64_t KS,
                 const double* __restrict__ sigma, const double* __restrict__ tau, int64_t rows, int64_t m, int64_t n,
                 int64_t kchunk, double* __restrict__ out, int64_t ldo, int64_t split_stride, int nd,
                 const int* __restrict__ knz, int probe) {
+  using C = OzCfg<SA, SB>;
   extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OZ_STAGES * OZ_STAGE);
-  uint64_t* empty = full + OZ_STAGES;
-  uint64_t* accfull = empty + OZ_STAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* accfull = empty + C::STAGES;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accfull + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -404,16 +417,17 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
   const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
   const int64_t kend = min64(n, kbeg + kchunk);
   const int steps = (int)ceil_div(max64(kend - kbeg, 0), OZ_BK);
+  const int na = nd < SA ? nd : SA;   // K slices that take part
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < OZ_STAGES; ++s) {
+    for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
     ptx::mbar_init(accfull, 1);
     ptx::fence_mbarrier_init();
   }
-  if (warp == 2) ptx::tmem_alloc(tmem_holder, OZ_TMEM_COLS);
+  if (warp == 2) ptx::tmem_alloc(tmem_holder, C::TMEM_COLS);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -427,7 +441,7 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
 #pragma unroll
       for (int e = 0; e < 32; ++e) z[e] = 0u;
 #pragma unroll 1
-      for (int c = 0; c < (int)OZ_ACC_COLS; c += 32) ptx::tmem_st_32x32b_x32(tmem + lb + (uint32_t)c, z);
+      for (int c = 0; c < (int)C::ACC_COLS; c += 32) ptx::tmem_st_32x32b_x32(tmem + lb + (uint32_t)c, z);
       ptx::tmem_wait_st();
     }
     ptx::tc_fence_before();
@@ -436,64 +450,69 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
   }
   // leading all-zero K slices of the k-th block of this CTA's range (0 without the metadata)
   const int* kb_nz = knz ? knz + (int64_t)blockIdx.y * KS + kbeg / OZ_BK : nullptr;
-  auto lead = [&](int s) { return kb_nz ? OZ_S - kb_nz[s] : 0; };
+  auto lead = [&](int s) { return kb_nz ? SA - kb_nz[s] : 0; };
 
-  if (warp == 0) {   // ---- producer: one bulk copy of the A image and one of the B image per k-step
+  if (warp == 0) {   // ---- producer: one bulk copy of the A image and one of the B image per kept k-step
     if (ptx::elect_one()) {
-      const int8_t* ga = Aq + ((int64_t)blockIdx.y * KS + kbeg / OZ_BK) * OZ_A_BYTES;
-      const int8_t* gb = Bq + ((int64_t)blockIdx.x * KS + kbeg / OZ_BK) * (OZ_STAGE - OZ_A_BYTES);
-      // K slices lz .. nd-1 (lz leading all-zero slices skipped) and V slices 0 .. nd-1-lz take part:
+      const int8_t* ga = Aq + ((int64_t)blockIdx.y * KS + kbeg / OZ_BK) * C::A_BYTES;
+      const int8_t* gb = Bq + ((int64_t)blockIdx.x * KS + kbeg / OZ_BK) * C::B_BYTES;
+      // K slices lz .. na-1 (lz leading all-zero slices skipped) and V slices 0 .. nd-1-lz take part:
       // contiguous ranges of the k-step image
+      int it = 0;
       for (int s = 0; s < steps; ++s) {
-        const int st = s % OZ_STAGES;
         const int lz = lead(s);
-        if (s >= OZ_STAGES) ptx::mbar_wait(&empty[st], ((s / OZ_STAGES) - 1) & 1);
-        unsigned char* dst = smem + st * OZ_STAGE;
-        if (lz >= nd) {
-          ptx::mbar_arrive(&full[st]);
-          continue;
-        }
+        if (lz >= na) continue;
+        const int st = it % C::STAGES;
+        if (it >= C::STAGES) ptx::mbar_wait(&empty[st], ((it / C::STAGES) - 1) & 1);
+        ++it;
+        unsigned char* dst = smem + st * C::STAGE;
         if (probe == 2) {   // RLD_OZ_PROBE=2 (measurement only): no loads, the MMAs read stale stages
           ptx::mbar_arrive(&full[st]);
           continue;
         }
-        const uint32_t abytes = (uint32_t)(nd - lz) * OZ_A_SLICE, bbytes = (uint32_t)(nd - lz) * OZ_B_SLICE;
+        const int nbv = (nd - lz) < SB ? (nd - lz) : SB;
+        const uint32_t abytes = (uint32_t)(na - lz) * OZ_A_SLICE, bbytes = (uint32_t)nbv * OZ_B_SLICE;
         ptx::mbar_arrive_expect_tx(&full[st], abytes + bbytes);
-        bulk_load(dst + lz * OZ_A_SLICE, ga + (int64_t)s * OZ_A_BYTES + lz * OZ_A_SLICE, abytes, &full[st]);
-        bulk_load(dst + OZ_A_BYTES, gb + (int64_t)s * (OZ_STAGE - OZ_A_BYTES), bbytes, &full[st]);
+        bulk_load(dst + lz * OZ_A_SLICE, ga + (int64_t)s * C::A_BYTES + lz * OZ_A_SLICE, abytes, &full[st]);
+        bulk_load(dst + C::A_BYTES, gb + (int64_t)s * C::B_BYTES, bbytes, &full[st]);
       }
     }
   } else if (warp == 1) {   // ---- MMA issuer
     if (ptx::elect_one()) {
       const uint32_t sbase = ptx::smem_u32(smem);
+      int it = 0;
       for (int s = 0; s < steps; ++s) {
-        const int st = s % OZ_STAGES;
-        ptx::mbar_wait(&full[st], (uint32_t)((s / OZ_STAGES) & 1));
-        ptx::tc_fence_after();
-        const uint32_t a0 = sbase + st * OZ_STAGE;
-        const uint32_t b0 = a0 + OZ_A_BYTES;
         const int lz = lead(s);
-        // A slice sa against the stacked B slices 0 .. 6 - sa at once: the accumulators of the
-        // diagonals d = sa + t are adjacent TMEM column blocks, so one N = 64 (7 - sa) product
-        // (in N <= 256 pieces) covers the whole row of pairs -- 10 MMAs per k-step instead of 28
-        // N = 64 ones, and the A operand is read from shared memory once per piece
+        if (lz >= na) continue;
+        const int st = it % C::STAGES;
+        ptx::mbar_wait(&full[st], (uint32_t)((it / C::STAGES) & 1));
+        ptx::tc_fence_after();
+        const uint32_t a0 = sbase + st * C::STAGE;
+        const uint32_t b0 = a0 + C::A_BYTES;
+        // A slice sa against the stacked B slices 0 .. nd-1-sa at once: the accumulators of the
+        // diagonals d = sa + t are adjacent TMEM column blocks, so one N = 64 (nd - sa) product
+        // (in N <= 256 pieces; 5 slices as 3 + 2, not 4 + 1: an N = 64 MMA is bound by its A read)
+        // covers the whole row of pairs -- 10 MMAs per k-step instead of 28 N = 64 ones (float64)
 #pragma unroll
-        for (int sa = 0; sa < OZ_S; ++sa) {
-          if (sa >= nd || probe == 1) break;   // RLD_OZ_PROBE=1 (measurement only): loads, no MMAs
+        for (int sa = 0; sa < SA; ++sa) {
+          if (sa >= na || probe == 1) break;   // RLD_OZ_PROBE=1 (measurement only): loads, no MMAs
           if (sa < lz) continue;
           const uint64_t adesc = desc_sw32(a0 + sa * OZ_A_SLICE);
-          const uint32_t acc = (kb_nz || s > 0 || sa > 0) ? 1u : 0u;
-#pragma unroll
-          for (int t0 = 0; t0 < OZ_DIAG - sa; t0 += 4) {
-            if (t0 >= nd - sa) break;
-            const int nb = (nd - sa - t0) < 4 ? (nd - sa - t0) : 4;   // B slices in this piece
+          const uint32_t acc = (kb_nz || it > 0 || sa > 0) ? 1u : 0u;
+          const int cnt = (nd - sa) < SB ? (nd - sa) : SB;   // B slices 0 .. cnt-1
+          int t0 = 0;
+          while (t0 < cnt) {
+            const int left = cnt - t0;
+            const int nb = left == 5 ? 3 : (left < 4 ? left : 4);   // B slices in this piece
             mma_i8_ss(tmem + (uint32_t)((sa + t0) * OZ_BN), adesc, desc_sw32(b0 + t0 * OZ_B_SLICE),
                       idesc_i8(OZ_BM, nb * OZ_BN), acc);
+            t0 += nb;
           }
         }
         ptx::tc_commit(&empty[st]);   // the stage is free once these MMAs have read it
+        ++it;
       }
-      if (steps > 0) ptx::tc_commit(accfull);
+      ptx::tc_commit(accfull);        // (no MMA pending: arrives at once)
     }
   } else if (warp >= 4) {   // ---- drains: thread = row (TMEM lane); one drain (k range <= OZ_KMAX)
     const int q = warp & 3;
@@ -501,17 +520,18 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const int64_t r = row0 + row;
     double* o = out + (int64_t)blockIdx.z * split_stride;
-    if (steps > 0) {
-      ptx::mbar_wait_sleep(accfull, 0);
-      ptx::tc_fence_after();
-    }
+    ptx::mbar_wait_sleep(accfull, 0);
+    ptx::tc_fence_after();
     const double sg = (r < rows) ? sigma[r] : 0.0;
+    // without the metadata an accumulator the MMAs never wrote (no k-step, or fewer than nd
+    // diagonals reached) holds garbage: only steps > 0 guarantees every diagonal d < nd was written
+    const bool have = knz != nullptr || steps > 0;
 #pragma unroll 1
     for (int c0 = 0; c0 < OZ_BN; c0 += 32) {
       double part[32];
 #pragma unroll
       for (int e = 0; e < 32; ++e) part[e] = 0.0;
-      if (steps > 0) {
+      if (have) {
 #pragma unroll 1
         for (int d = nd - 1; d >= 0; --d) {   // small terms first
           const double w = __longlong_as_double((long long)(1023 - OZ_DBITS * (d + 2)) << 52);   // 2^{-8(d+2)}
@@ -533,7 +553,7 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 2) ptx::tmem_dealloc(tmem, OZ_TMEM_COLS);
+  if (warp == 2) ptx::tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
 int oz_sms() {
@@ -548,8 +568,15 @@ int oz_sms() {
 
 }  // namespace
 
-int64_t ozaki_bytes(int64_t rows, int64_t n, int tile_rows) {
-  return ceil_div(rows, tile_rows) * tile_rows * ceil_div(n, OZ_BK) * OZ_BK * OZ_S;
+int64_t ozaki_bytes(int64_t rows, int64_t n, int tile_rows, int slices) {
+  return ceil_div(rows, tile_rows) * tile_rows * ceil_div(n, OZ_BK) * OZ_BK * slices;
+}
+
+// float32 stored K from Morton-ordered points as 3 int8 slices (RLD_FP32_PRODUCT=tf32 keeps the fp32
+// tiles and the 3xTF32 / fp16 kernels); read at every prepare
+bool fp32_product_slices() {
+  const char* e = getenv("RLD_FP32_PRODUCT");
+  return !(e && std::string(e) == "tf32");
 }
 
 // Read at every prepare, so a process can compare both products.  Default: the int8 slices.
@@ -559,7 +586,7 @@ bool fp64_product_ozaki() {
 }
 
 void ozaki_slice(const double* A, int64_t lda, int64_t rows, int64_t n, int tile_rows, int8_t* q, double* scale,
-                 cudaStream_t st) {
+                 cudaStream_t st, int slices) {
   if (rows <= 0) return;
   if (rows > 2147483647LL) fail(RLD_ERR_NOT_SUPPORTED, "ozaki_slice: too many rows");
   if (rows <= 65535) {
@@ -575,17 +602,19 @@ void ozaki_slice(const double* A, int64_t lda, int64_t rows, int64_t n, int tile
   const int64_t KS = ceil_div(n, OZ_BK);
   const int64_t total = ceil_div(rows, tile_rows) * tile_rows * KS * 2;
   const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)oz_sms() * 16);
-  if (tile_rows == OZ_BM)
-    ozaki_digits_kernel<OZ_BM><<<blocks, 256, 0, st>>>(A, lda, rows, n, scale, KS, q);
-  else if (tile_rows == OZ_BN)
-    ozaki_digits_kernel<OZ_BN><<<blocks, 256, 0, st>>>(A, lda, rows, n, scale, KS, q);
+  if (tile_rows == OZ_BM && slices == OZ_S)
+    ozaki_digits_kernel<OZ_BM, OZ_S><<<blocks, 256, 0, st>>>(A, lda, rows, n, scale, KS, q);
+  else if (tile_rows == OZ_BN && slices == OZ_S)
+    ozaki_digits_kernel<OZ_BN, OZ_S><<<blocks, 256, 0, st>>>(A, lda, rows, n, scale, KS, q);
+  else if (tile_rows == OZ_BN && slices == OZ_V32)
+    ozaki_digits_kernel<OZ_BN, OZ_V32><<<blocks, 256, 0, st>>>(A, lda, rows, n, scale, KS, q);
   else
-    fail(RLD_ERR_INVALID_ARGUMENT, "ozaki_slice: tile rows must be 128 (K) or 64 (V)");
+    fail(RLD_ERR_INVALID_ARGUMENT, "ozaki_slice: tile rows must be 128 (K) or 64 (V), 7 (or, V: 4) slices");
   RLD_LAUNCH_CHECK();
 }
 
 void ozaki_slice_points(const double* X, int64_t n, const KernelParams& kp, int64_t row0, int64_t rows, int8_t* q,
-                        double* scale, cudaStream_t st, int8_t* Kr, int* knz) {
+                        double* scale, cudaStream_t st, int8_t* Kr, int* knz, int slices) {
   if (rows <= 0) return;
   if (kp.d > RLD_MAX_DIM) fail(RLD_ERR_NOT_SUPPORTED, "ozaki_slice_points: d > 32");
   const int ee = oz_scale_exp(kp.diag > 0.0 ? kp.diag : 1.0);
@@ -595,30 +624,35 @@ void ozaki_slice_points(const double* X, int64_t n, const KernelParams& kp, int6
   const int64_t total = ceil_div(rows, OZ_BM) * OZ_BM * KS * 4;
   const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)oz_sms() * 16);
   if (knz) RLD_CUDA(cudaMemsetAsync(knz, 0, sizeof(int) * ceil_div(rows, OZ_BM) * KS, st));
-  if (Kr && kp.d <= 4)
-    ozaki_points_kernel<true, 8, 4><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, Kr, knz);
+  if (slices == OZ_S32) {   // float32 K: 24 bits of the float64 kernel value relative to the row scale
+    if (Kr || kp.d > 4) fail(RLD_ERR_INVALID_ARGUMENT, "ozaki_slice_points: 3 slices need d <= 4 and no CRT image");
+    ozaki_points_kernel<false, 8, 4, OZ_S32><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, nullptr, knz);
+  } else if (slices != OZ_S)
+    fail(RLD_ERR_INVALID_ARGUMENT, "ozaki_slice_points: 7 or 3 slices");
+  else if (Kr && kp.d <= 4)
+    ozaki_points_kernel<true, 8, 4, OZ_S><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, Kr, knz);
   else if (Kr)
-    ozaki_points_kernel<true, 8, RLD_MAX_DIM><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, Kr, knz);
+    ozaki_points_kernel<true, 8, RLD_MAX_DIM, OZ_S><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, Kr, knz);
   else if (kp.d <= 4)
-    ozaki_points_kernel<false, 8, 4><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, nullptr, knz);
+    ozaki_points_kernel<false, 8, 4, OZ_S><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, nullptr, knz);
   else
-    ozaki_points_kernel<false, 8, RLD_MAX_DIM><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, nullptr, knz);
+    ozaki_points_kernel<false, 8, RLD_MAX_DIM, OZ_S><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, nullptr, knz);
   RLD_LAUNCH_CHECK();
 }
 
-// Y (m x rows, ld ldy) = V K^T with K given by its sliced image Kq (ozaki_slice, 128-row tiles) and
-// row scales; V (m x n float64 rows, ld ldv) is sliced here (64-vector tiles) into ws.oz_vq.
-void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int64_t n, const double* V, int64_t ldv,
-                      int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st, int diags,
-                      const int* knz) {
-  if (m <= 0 || rows <= 0) return;
-  if (diags < 1 || diags > OZ_DIAG) fail(RLD_ERR_INVALID_ARGUMENT, "kv_product_ozaki: diagonals must be 1..7");
-  ws.oz_vq.reserve((size_t)ozaki_bytes(m, n, OZ_BN));
+namespace {
+
+template <int SA, int SB>
+void launch_product(const int8_t* Kq, const double* ksigma, int64_t rows, int64_t n, const double* V, int64_t ldv,
+                    int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st, int diags, const int* knz) {
+  using C = OzCfg<SA, SB>;
+  if (diags < 1 || diags > SB) fail(RLD_ERR_INVALID_ARGUMENT, "kv_product_ozaki: diagonals out of range");
+  ws.oz_vq.reserve((size_t)ozaki_bytes(m, n, OZ_BN, SB));
   ws.oz_tau.reserve(sizeof(double) * m);
-  ozaki_slice(V, ldv, m, n, OZ_BN, ws.oz_vq.as<int8_t>(), ws.oz_tau.as<double>(), st);
+  ozaki_slice(V, ldv, m, n, OZ_BN, ws.oz_vq.as<int8_t>(), ws.oz_tau.as<double>(), st, SB);
   static std::atomic<uint64_t> attr{0};
   once_per_device(attr, [&] {
-    RLD_CUDA(cudaFuncSetAttribute(ozaki_kv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM));
+    RLD_CUDA(cudaFuncSetAttribute(ozaki_kv_kernel<SA, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   });
   const int64_t KS = ceil_div(n, OZ_BK);
   const int64_t passes = ceil_div(m, OZ_BN), tiles = ceil_div(rows, OZ_BM);
@@ -647,20 +681,38 @@ void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int6
   const char* pe = getenv("RLD_OZ_PROBE");   // kernel-phase probe for measurement, never set in production
   const int probe = pe ? atoi(pe) : 0;
   if (splits == 1) {
-    ozaki_kv_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(Kq, Bq, KS, ksigma, ws.oz_tau.as<double>(), rows, m, n, kchunk,
-                                                      Y, ldy, 0, diags, knz, probe);
+    ozaki_kv_kernel<SA, SB><<<grid, OZ_THREADS, C::SMEM, st>>>(Kq, Bq, KS, ksigma, ws.oz_tau.as<double>(), rows, m, n,
+                                                              kchunk, Y, ldy, 0, diags, knz, probe);
     RLD_LAUNCH_CHECK();
     return;
   }
   const int64_t stride = m * rows;
   ws.partial.reserve(sizeof(double) * stride * splits);
-  ozaki_kv_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(Kq, Bq, KS, ksigma, ws.oz_tau.as<double>(), rows, m, n, kchunk,
-                                                    ws.partial.as<double>(), rows, stride, diags, knz, probe);
+  ozaki_kv_kernel<SA, SB><<<grid, OZ_THREADS, C::SMEM, st>>>(Kq, Bq, KS, ksigma, ws.oz_tau.as<double>(), rows, m, n,
+                                                            kchunk, ws.partial.as<double>(), rows, stride, diags, knz,
+                                                            probe);
   RLD_LAUNCH_CHECK();
   const unsigned gy = (unsigned)std::min<int64_t>(m, 65535);
   const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 512), slots * 8 / gy + 1));
   oz_split_reduce_kernel<<<dim3(gx, gy), 256, 0, st>>>(ws.partial.as<double>(), (int)splits, stride, m, rows, Y, ldy);
   RLD_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+// Y (m x rows, ld ldy) = V K^T with K given by its sliced image Kq (ozaki_slice, 128-row tiles, kslices =
+// 7: float64, 3: float32 K) and row scales; V (m x n float64 rows, ld ldv) is sliced here (64-vector
+// tiles, 7 or 4 slices) into ws.oz_vq.  diags <= 0: all of them.
+void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int64_t n, const double* V, int64_t ldv,
+                      int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st, int diags,
+                      const int* knz, int kslices) {
+  if (m <= 0 || rows <= 0) return;
+  if (kslices == OZ_S)
+    launch_product<OZ_S, OZ_S>(Kq, ksigma, rows, n, V, ldv, m, Y, ldy, ws, st, diags <= 0 ? OZ_S : diags, knz);
+  else if (kslices == OZ_S32)
+    launch_product<OZ_S32, OZ_V32>(Kq, ksigma, rows, n, V, ldv, m, Y, ldy, ws, st, OZ_V32, knz);
+  else
+    fail(RLD_ERR_INVALID_ARGUMENT, "kv_product_ozaki: 7 or 3 K slices");
 }
 
 }  // namespace rld

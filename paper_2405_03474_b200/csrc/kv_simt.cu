@@ -250,7 +250,7 @@ void kv_product(const KvOperand& op, int64_t m, const double* V, int64_t ldv, do
       return;
     }
     if (!simt && op.kq) {   // exact int8 slices of K on the INT8 tensor cores (kv_ozaki.cu)
-      kv_product_ozaki(op.kq, op.ksigma, op.rows, op.n, V, ldv, m, Y, ldy, ws, st, op.oz_diags, op.knz);
+      kv_product_ozaki(op.kq, op.ksigma, op.rows, op.n, V, ldv, m, Y, ldy, ws, st, op.oz_diags, op.knz, op.kslices);
       return;
     }
     if (!otf && !simt && gemm_nt_f64_ok(K, op.ldk, K, op.ldk)) {
@@ -270,6 +270,10 @@ void kv_product(const KvOperand& op, int64_t m, const double* V, int64_t ldv, do
       launch_kv<double, double, 64, 32, 16, 4, 4, true>(op, m, V, ldv, Y, ldy, ws, st, launches);
     else
       launch_kv<double, double, 64, 32, 16, 4, 4, false>(op, m, V, ldv, Y, ldy, ws, st, launches);
+    return;
+  }
+  if (op.kq) {   // float32 K held as 3 int8 slices (Morton-ordered points, kv_ozaki.cu)
+    kv_product_ozaki(op.kq, op.ksigma, op.rows, op.n, V, ldv, m, Y, ldy, ws, st, 0, op.knz, op.kslices);
     return;
   }
   if (kv_tc_supported(op) && (op.tiled || !getenv("RLD_NO_TC"))) {

@@ -95,8 +95,9 @@ struct Resident {
   DevBuf X;                  // points n x d
   DevBuf pts4;               // points split to n x 8 fp32 hi/lo (d <= 4; tensor-core on-the-fly tiles)
   DevBuf diag;               // local diagonal of K (float64)
-  DevBuf Kq, ksigma;         // float64 K as exact int8 slices (RLD_FP64_PRODUCT=ozaki, kv_ozaki.cu)
-  bool kq_ready = false;
+  DevBuf Kq, ksigma;         // K as exact int8 slices (kv_ozaki.cu): float64 (7 slices, RLD_FP64_PRODUCT=ozaki)
+  bool kq_ready = false;     // or float32 from Morton-ordered points (3 slices)
+  int kslices = 7;
   DevBuf perm;               // points held in Morton (Z-curve) order: perm[i] = original index of point i
   bool permuted = false;     // (single GPU, float64 stored products: far-field slice blocks are all-zero)
   DevBuf knz;                // per slice-image block: slices from the first nonzero one (skipped leading zeros)
@@ -121,6 +122,7 @@ struct Resident {
     o.dtype = dtype;
     if (kq_ready && path != RLD_PATH_ON_THE_FLY) {
       o.kq = Kq.as<int8_t>();
+      o.kslices = kslices;
       o.ksigma = ksigma.as<double>();
       if (knz_ready) o.knz = knz.as<int>();
       if (kr_ready) o.kr = Kr.as<int8_t>();
@@ -233,7 +235,8 @@ bool sort_points(const rld_handle* h, const rld_problem* p) {
   if (e && e[0] == '0') return false;
   // float64 stored on int8 slices (all-zero leading slices skipped) or float32 on the fly (far-field
   // k-steps with exactly-zero fp16 operands skipped)
-  const bool slices = p->path == RLD_PATH_STORED && p->dtype == RLD_FP64 && fp64_product_ozaki();
+  const bool slices = p->path == RLD_PATH_STORED &&
+                      (p->dtype == RLD_FP64 ? fp64_product_ozaki() : fp32_product_slices());
   const bool otf = p->path == RLD_PATH_ON_THE_FLY && p->dtype == RLD_FP32 && kv_otf_f16_enabled();
   return p->source == RLD_SOURCE_POINTS && (slices || otf) && h->world == 1 && p->d >= 1 && p->d <= 3 &&
          p->n < (int64_t)1 << 31;
@@ -249,6 +252,7 @@ void prepare(rld_handle* h, const rld_problem* p) {
   r.ready = false;
   r.tiled = false;
   r.kq_ready = false;
+  r.kslices = 7;
   r.kr_ready = false;
   r.knz_ready = false;
   r.permuted = false;
@@ -361,6 +365,23 @@ void prepare(rld_handle* h, const rld_problem* p) {
         r.Kbuf.reserve(sizeof(double) * r.rows * r.ldk);
         r.K = r.Kbuf.ptr;
         build_kernel_rows<double>(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.Kbuf.as<double>(), r.ldk, st);
+      } else if (r.permuted && fp32_product_slices()) {
+        // float32 K from Morton-ordered points (d <= 3, one GPU): 3 int8 slices = the float64 kernel
+        // value rounded to 24 bits of its row scale (float32-grade next to the diagonal; far-field
+        // entries below 2^-25 of the scale are exactly zero and their blocks are skipped), multiplied
+        // with 4 slices of V on the INT8 tensor cores (kv_ozaki.cu).  3 bytes per entry, no fp32 K.
+        r.K = nullptr;
+        r.ldk = 0;
+        r.kslices = 3;
+        if (r.rows > 0) {
+          r.Kq.reserve((size_t)ozaki_bytes(r.rows, p->n, 128, 3));
+          r.ksigma.reserve(sizeof(double) * r.rows);
+          r.knz.reserve(sizeof(int) * ceil_div(r.rows, 128) * ceil_div(p->n, 32));
+          ozaki_slice_points(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.Kq.as<int8_t>(), r.ksigma.as<double>(),
+                             st, nullptr, r.knz.as<int>(), 3);
+          r.knz_ready = true;
+        }
+        r.kq_ready = r.rows > 0;
       } else {   // fp32: 16 KB tiles, one contiguous TMA box per tensor-core step
         r.tiled = true;
         r.ldk = 0;
@@ -452,7 +473,7 @@ void prepare(rld_handle* h, const rld_problem* p) {
     r.rowscale.reserve(sizeof(float) * r.rows);
     kv_rowscales(static_cast<const float*>(r.K), r.rows, r.n, r.rowscale.as<float>(), st);
   }
-  if (r.kq_ready && !r.kr_ready && !r.permuted && crt_supported(r.n)) {
+  if (r.kq_ready && r.kslices == 7 && !r.kr_ready && !r.permuted && crt_supported(r.n)) {
     // the CRT residue image for the wide (sketch) products, where it fits beside the slices
     const int64_t bytes = crt_bytes(r.rows, r.n);
     size_t fr = 0, tot = 0;
@@ -1684,9 +1705,10 @@ int rld_slice_stats(rld_handle* h, int64_t* stats) {
     const int64_t nb = ceil_div(r.rows, 128) * ceil_div(r.n, 32);
     stats[0] = nb;
     stats[3] = r.kr_ready ? 1 : 0;
+    const int S = r.kslices, extra = S == 7 ? 0 : 1;   // float32 K: 3 slices against 4 of V
     if (!r.knz_ready) {   // no metadata: every block reads all 7 slices, 28 pairs
-      stats[1] = 7 * nb;
-      stats[2] = 28 * nb;
+      stats[1] = (int64_t)S * nb;
+      stats[2] = (int64_t)(S * (S + 1) / 2 + extra * S) * nb;
       return;
     }
     std::vector<int> nz((size_t)nb);
@@ -1694,7 +1716,7 @@ int rld_slice_stats(rld_handle* h, int64_t* stats) {
     RLD_CUDA(cudaStreamSynchronize(h->st));
     for (int v : nz) {
       stats[1] += v;
-      stats[2] += (int64_t)v * (v + 1) / 2;
+      stats[2] += (int64_t)v * (v + 1) / 2 + extra * v;
     }
   });
 }

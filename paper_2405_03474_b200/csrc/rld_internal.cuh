@@ -100,7 +100,8 @@ struct KvOperand {
   const float* pts4 = nullptr;  // points as n x 8 fp32 (hi x,y,z,w; lo x,y,z,w) for the tensor-core on-the-fly path, d <= 4
   KernelParams kp{};
   int dtype = RLD_FP64;      // product arithmetic
-  const int8_t* kq = nullptr;      // float64 K as 8 exact int8 slices, k-step-tiled image (kv_ozaki.cu), or null
+  const int8_t* kq = nullptr;      // K as exact int8 slices, k-step-tiled image (kv_ozaki.cu), or null
+  int kslices = 7;                 // 7: float64 K; 3: float32 K (Morton-ordered points)
   const double* ksigma = nullptr;  // per-row power-of-two scales of the slices
   const int* knz = nullptr;        // per (tile, k-step) block: slices from the first nonzero one (or null)
   int64_t n = 0;             // columns of K (global order)
@@ -171,19 +172,20 @@ void gemm_nt_f64(const double* A, int64_t lda, int64_t p, const double* B, int64
 void gemm_expand_f64(const double* S, int64_t lds, int64_t p, int64_t q, const double* X, int64_t ldx, int64_t N,
                      double* C, int64_t ldc, double alpha, double beta, cudaStream_t st);
 
-// Float64-accurate products on the INT8 tensor cores (kv_ozaki.cu): exact 8 x 7-bit slicing.
-int64_t ozaki_bytes(int64_t rows, int64_t n, int tile_rows);   // size of a sliced image (tiles of 128 / 64 rows)
+// Float64-accurate products on the INT8 tensor cores (kv_ozaki.cu): exact 7 x 8-bit slicing
+// (`slices` = 7; a float32 K from Morton-ordered points is held as 3 slices and multiplied with 4 of V).
+int64_t ozaki_bytes(int64_t rows, int64_t n, int tile_rows, int slices = 7);   // size of a sliced image (tiles of 128 / 64 rows)
 void ozaki_slice(const double* A, int64_t lda, int64_t rows, int64_t n, int tile_rows, int8_t* q, double* scale,
-                 cudaStream_t st);
+                 cudaStream_t st, int slices = 7);
 // the same image straight from the points (no float64 K): stationary kernel, row max = diagonal
 // Kr != null: also K's CRT residue image (kv_crt.cu), crt_bytes(rows, n) bytes
-// knz != null: per (128-row tile, 32-column k-step) block, 8 - the number of leading all-zero slices
+// knz != null: per (128-row tile, 32-column k-step) block, slices - the number of leading all-zero slices
 // (int [ceil(rows/128)][ceil(n/32)]), which the product skips
 void ozaki_slice_points(const double* X, int64_t n, const KernelParams& kp, int64_t row0, int64_t rows, int8_t* q,
-                        double* scale, cudaStream_t st, int8_t* Kr = nullptr, int* knz = nullptr);
+                        double* scale, cudaStream_t st, int8_t* Kr = nullptr, int* knz = nullptr, int slices = 7);
 void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int64_t n, const double* V, int64_t ldv,
-                      int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st, int diags = 8,
-                      const int* knz = nullptr);
+                      int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st, int diags = 7,
+                      const int* knz = nullptr, int kslices = 7);
 // Wide float64 products as 15 modular int8 GEMMs + CRT (kv_crt.cu); the residue image of K comes
 // from its slice image (crt_residues, 15 bytes per entry).
 bool crt_supported(int64_t n);
@@ -195,6 +197,8 @@ constexpr int64_t CRT_MIN_M = 96;   // narrower products (the Lanczos block) sta
 // Which float64 stored-K product a prepare sets up: the int8 slices (default) or, with
 // RLD_FP64_PRODUCT=dmma, the DMMA kernel on the float64 K.
 bool fp64_product_ozaki();
+// float32 stored K from Morton-ordered points as 3 int8 slices (default; RLD_FP32_PRODUCT=tf32: fp32 tiles)
+bool fp32_product_slices();
 
 // ---------------------------------------------------------------------------
 // RNG

@@ -182,6 +182,40 @@ def test_int8_slices_morton_narrow_last_pass(rld, m):
     assert np.array_equal(Y, R.kv_apply(torch.from_numpy(V).cuda()).cpu().numpy())
 
 
+@pytest.mark.parametrize("index,n,m", [(3, 6000, 10), (3, 6000, 64), (3, 9001, 130), (1, 2048, 16), (5, 5000, 128)])
+def test_fp32_int8_slices_product(rld, index, n, m, monkeypatch):
+    """float32 stored K from d <= 3 points on one GPU: 3 int8 slices (the float64 kernel value
+    rounded to 24 bits of its row scale, Morton order, all-zero leading slices skipped) against 4
+    slices of V (kv_ozaki.cu <3, 4>).  Entry error <= 2^-25 sigma (sigma <= 4.07 max|K_i|), so
+    |err_ic| <= 2^-22 n max|K_i| max|V_c| entrywise; float32-grade against numpy overall; the fp32
+    tile kernels (RLD_FP32_PRODUCT=tf32) agree at that level."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2405_03474_b200.workloads import baseline
+
+    wl = baseline(index, n=n)
+    R = rld.ResidentMatrix(rld.KernelMatrix(wl.spec, wl.points), dtype="fp32", path="stored")
+    stats = (C.c_int64 * 4)()
+    assert R.sess.lib.rld_slice_stats(R.sess.handle.ptr, stats) == 0
+    assert stats[0] > 0 and stats[1] <= 3 * stats[0] and stats[2] <= 9 * stats[0]   # the slice path is live
+    V = np.random.default_rng(m).standard_normal((m, n))
+    Vt = torch.from_numpy(V).cuda()
+    Y = R.kv_apply(Vt).cpu().numpy()
+    K = O.covariance_block(wl.spec.family, wl.spec.amplitude, wl.spec.length_scale, wl.spec.jitter, wl.points)
+    ref = V @ K.T
+    bound = 2.0 ** -22 * n * np.outer(np.abs(V).max(axis=1), np.abs(K).max(axis=1))
+    assert np.all(np.abs(Y - ref) <= bound)
+    assert np.max(np.abs(Y - ref)) <= 2e-6 * np.max(np.abs(ref))
+    assert np.array_equal(Y, R.kv_apply(Vt).cpu().numpy())
+    monkeypatch.setenv("RLD_FP32_PRODUCT", "tf32")
+    R2 = rld.ResidentMatrix(rld.KernelMatrix(wl.spec, wl.points), dtype="fp32", path="stored")
+    assert R2.sess.lib.rld_slice_stats(R2.sess.handle.ptr, stats) == 0 and stats[0] == 0
+    Y2 = R2.kv_apply(Vt).cpu().numpy()
+    assert np.max(np.abs(Y - Y2)) <= 4e-6 * np.max(np.abs(ref))
+
+
 def test_int8_slices_from_points_equal_slices_from_K(rld, monkeypatch):
     """Stored float64 from the points slices K straight from the points (no float64 K in HBM); from
     a dense device K built by build_covariance it slices the stored rows: same entries, same row
