@@ -64,6 +64,8 @@ struct OzCfg {
   static constexpr uint32_t B_BYTES = SB * OZ_B_SLICE;          // 14 KB / 8 KB
   static constexpr uint32_t STAGE = A_BYTES + B_BYTES;          // 42 KB / 20 KB
   static constexpr int STAGES = SA == OZ_S ? 5 : 8;
+  // columns per CTA, exact in int32: <= min(SA, SB) pairs per diagonal x 128^2 x KMAX < 2^31
+  static constexpr int64_t KMAX = SA == OZ_S ? OZ_KMAX : 2 * OZ_KMAX;
   static constexpr int SMEM = STAGES * (int)STAGE + 1024 + 256;
   static constexpr uint32_t ACC_COLS = SB * OZ_BN;              // 448 / 256 accumulator columns
   static constexpr uint32_t TMEM_COLS = ACC_COLS <= 256 ? 256 : 512;   // allocation (a power of two)
@@ -432,9 +434,10 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
-  if (knz) {
-    // blocks skip their leading all-zero K slices, so a diagonal's first MMA can come at any k-step:
-    // the accumulators start from zero and every MMA accumulates
+  {
+    // blocks skip their leading all-zero K slices, so a diagonal's first MMA can come at any k-step
+    // (and the MMAs of a step are issued smallest first): the accumulators start from zero and every
+    // MMA accumulates
     if (warp >= 4) {
       const uint32_t lb = (uint32_t)((warp & 3) * 32) << 16;
       uint32_t z[32];
@@ -448,9 +451,14 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
     __syncthreads();
     ptx::tc_fence_after();
   }
-  // leading all-zero K slices of the k-th block of this CTA's range (0 without the metadata)
+  // leading all-zero K slices of the k-th block of this CTA's range (0 without the metadata), staged
+  // in shared memory: the producer and the MMA thread walk it step by step (a global read per step
+  // would put an L2 latency on each of their iterations)
+  __shared__ uint8_t s_lead[C::KMAX / OZ_BK];
   const int* kb_nz = knz ? knz + (int64_t)blockIdx.y * KS + kbeg / OZ_BK : nullptr;
-  auto lead = [&](int s) { return kb_nz ? SA - kb_nz[s] : 0; };
+  for (int i = threadIdx.x; i < steps; i += OZ_THREADS) s_lead[i] = kb_nz ? (uint8_t)(SA - kb_nz[i]) : (uint8_t)0;
+  __syncthreads();
+  auto lead = [&](int s) { return (int)s_lead[s]; };
 
   if (warp == 0) {   // ---- producer: one bulk copy of the A image and one of the B image per kept k-step
     if (ptx::elect_one()) {
@@ -486,28 +494,26 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
         if (lz >= na) continue;
         const int st = it % C::STAGES;
         ptx::mbar_wait(&full[st], (uint32_t)((it / C::STAGES) & 1));
-        ptx::tc_fence_after();
         const uint32_t a0 = sbase + st * C::STAGE;
         const uint32_t b0 = a0 + C::A_BYTES;
         // A slice sa against the stacked B slices 0 .. nd-1-sa at once: the accumulators of the
         // diagonals d = sa + t are adjacent TMEM column blocks, so one N = 64 (nd - sa) product
         // (in N <= 256 pieces; 5 slices as 3 + 2, not 4 + 1: an N = 64 MMA is bound by its A read)
-        // covers the whole row of pairs -- 10 MMAs per k-step instead of 28 N = 64 ones (float64)
+        // covers the whole row of pairs -- 10 MMAs per k-step instead of 28 N = 64 ones (float64).
+        // Last slice first: the widest MMAs (sa = lz: N up to 448) go out last, so the tensor pipe
+        // still has ~250 cycles queued while this thread commits and waits for the next stage (the
+        // pipe accepts only a couple of MMAs ahead: with the narrow ones last it ran dry every step).
 #pragma unroll
-        for (int sa = 0; sa < SA; ++sa) {
-          if (sa >= na || probe == 1) break;   // RLD_OZ_PROBE=1 (measurement only): loads, no MMAs
-          if (sa < lz) continue;
+        for (int sa = SA - 1; sa >= 0; --sa) {
+          if (sa >= na || sa < lz || probe == 1) continue;   // RLD_OZ_PROBE=1 (measurement only): loads, no MMAs
           const uint64_t adesc = desc_sw32(a0 + sa * OZ_A_SLICE);
-          const uint32_t acc = (kb_nz || it > 0 || sa > 0) ? 1u : 0u;
-          const int cnt = (nd - sa) < SB ? (nd - sa) : SB;   // B slices 0 .. cnt-1
-          int t0 = 0;
-          while (t0 < cnt) {
-            const int left = cnt - t0;
-            const int nb = left == 5 ? 3 : (left < 4 ? left : 4);   // B slices in this piece
-            mma_i8_ss(tmem + (uint32_t)((sa + t0) * OZ_BN), adesc, desc_sw32(b0 + t0 * OZ_B_SLICE),
-                      idesc_i8(OZ_BM, nb * OZ_BN), acc);
-            t0 += nb;
-          }
+          constexpr uint32_t acc = 1u;
+          const int cnt = (nd - sa) < SB ? (nd - sa) : SB;   // B slices 0 .. cnt-1, in at most two pieces
+          const int first = cnt == 5 ? 3 : (cnt < 4 ? cnt : 4);
+          mma_i8_ss(tmem + (uint32_t)(sa * OZ_BN), adesc, desc_sw32(b0), idesc_i8(OZ_BM, first * OZ_BN), acc);
+          if (cnt > first)
+            mma_i8_ss(tmem + (uint32_t)((sa + first) * OZ_BN), adesc, desc_sw32(b0 + first * OZ_B_SLICE),
+                      idesc_i8(OZ_BM, (cnt - first) * OZ_BN), acc);
         }
         ptx::tc_commit(&empty[st]);   // the stage is free once these MMAs have read it
         ++it;
@@ -523,9 +529,7 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
     ptx::mbar_wait_sleep(accfull, 0);
     ptx::tc_fence_after();
     const double sg = (r < rows) ? sigma[r] : 0.0;
-    // without the metadata an accumulator the MMAs never wrote (no k-step, or fewer than nd
-    // diagonals reached) holds garbage: only steps > 0 guarantees every diagonal d < nd was written
-    const bool have = knz != nullptr || steps > 0;
+    const bool have = true;   // the accumulators are zeroed up front
 #pragma unroll 1
     for (int c0 = 0; c0 < OZ_BN; c0 += 32) {
       double part[32];
@@ -660,7 +664,7 @@ void launch_product(const int8_t* Kq, const double* ksigma, int64_t rows, int64_
   const int64_t slots = oz_sms();
   // k splits: every CTA <= OZ_KMAX columns (exact int32), >= 64 k-steps; the fewest splits whose
   // CTA count fills >= 95 % of whole waves
-  const int64_t min_s = ceil_div(n, OZ_KMAX);
+  const int64_t min_s = ceil_div(n, C::KMAX);
   const int64_t max_s = std::max<int64_t>(min_s, n / (OZ_BK * 64));
   int64_t splits = min_s;
   double best = 0.0;

@@ -12,7 +12,8 @@ import paper_2405_03474_b200 as rld  # noqa: E402
 from paper_2405_03474_b200.workloads import baseline  # noqa: E402
 
 wl = baseline(3)
-R = rld.ResidentMatrix(rld.KernelMatrix(wl.spec, wl.points), dtype="fp64", path="stored")
+DT = os.environ.get("RLD_PROBE_DTYPE", "fp64")   # fp32: the 3 x 4-slice product of a float32 K
+R = rld.ResidentMatrix(rld.KernelMatrix(wl.spec, wl.points), dtype=DT, path="stored")
 for m in [int(a) for a in sys.argv[1:]] or (64, 522):
     V = torch.randn(m, wl.n, dtype=torch.float64, device="cuda")
     for _ in range(2):
@@ -24,5 +25,5 @@ for m in [int(a) for a in sys.argv[1:]] or (64, 522):
         torch.cuda.synchronize()
     ts = [ev.device_time for ev in prof.events() if ev.device_type == torch.autograd.DeviceType.CUDA
           and "ozaki_kv_kernel" in ev.name]
-    print(f"probe={os.environ.get('RLD_OZ_PROBE', '0')} m={m}: ozaki_kv_kernel {sum(ts) / len(ts) / 1e3:.3f} ms "
+    print(f"{DT} probe={os.environ.get('RLD_OZ_PROBE', '0')} m={m}: ozaki_kv_kernel {sum(ts) / len(ts) / 1e3:.3f} ms "
           f"(n={len(ts)})", flush=True)
