@@ -34,6 +34,9 @@
 // (deterministic).
 #include <cuda.h>
 
+#include <thrust/execution_policy.h>
+#include <thrust/scan.h>
+
 #include <algorithm>
 #include <mutex>
 
@@ -58,16 +61,24 @@ constexpr int OZ_THREADS = 256;
 constexpr uint32_t OZ_A_SLICE = OZ_BM * OZ_BK;            // 4 KB
 constexpr uint32_t OZ_B_SLICE = OZ_BN * OZ_BK;            // 2 KB
 // SA digits of K against SB >= SA digits of V, pairs s + t <= SB - 1 (one TMEM accumulator per diagonal)
-template <int SA, int SB>
+// BN vectors per column pass: 64, or 128 for the wide products of the float32 variant (4 x 128 = all
+// 512 TMEM columns: half as many (CTA, k-step) handshakes per product)
+template <int SA, int SB, int BN = OZ_BN>
 struct OzCfg {
   static constexpr uint32_t A_BYTES = SA * OZ_A_SLICE;          // 28 KB (float64) / 12 KB (float32)
-  static constexpr uint32_t B_BYTES = SB * OZ_B_SLICE;          // 14 KB / 8 KB
-  static constexpr uint32_t STAGE = A_BYTES + B_BYTES;          // 42 KB / 20 KB
-  static constexpr int STAGES = SA == OZ_S ? 5 : 8;
+  static constexpr uint32_t B_SLICE = BN * OZ_BK;               // 2 KB / 4 KB (BN = 128)
+  static constexpr uint32_t B_BYTES = SB * B_SLICE;             // 14 KB / 8 KB / 16 KB
+  static constexpr int PC = 256 / BN;                           // V slices per MMA piece (N <= 256)
+  // kept k-steps per pipeline stage (one mbarrier handshake and one commit per stage): the float32
+  // variant's steps carry one to three small MMAs and are bound by that handshake, so it groups 2
+  static constexpr int GROUP = SA == OZ_S ? 1 : (BN == OZ_BN ? 3 : 2);
+  static constexpr uint32_t STEP = A_BYTES + B_BYTES;           // 42 KB / 20 KB
+  static constexpr uint32_t STAGE = GROUP * STEP;
+  static constexpr int STAGES = SA == OZ_S ? 5 : 3;
   // columns per CTA, exact in int32: <= min(SA, SB) pairs per diagonal x 128^2 x KMAX < 2^31
   static constexpr int64_t KMAX = SA == OZ_S ? OZ_KMAX : 2 * OZ_KMAX;
   static constexpr int SMEM = STAGES * (int)STAGE + 1024 + 256;
-  static constexpr uint32_t ACC_COLS = SB * OZ_BN;              // 448 / 256 accumulator columns
+  static constexpr uint32_t ACC_COLS = SB * BN;                 // 448 / 256 / 512 accumulator columns
   static constexpr uint32_t TMEM_COLS = ACC_COLS <= 256 ? 256 : 512;   // allocation (a power of two)
 };
 
@@ -248,7 +259,8 @@ __global__ void ozaki_digits_kernel(const double* __restrict__ A, int64_t lda, i
 template <bool CRT, int EL, int DMAX, int S>
 __global__ void __launch_bounds__(256)
 ozaki_points_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, int64_t row0,
-                    int64_t rows, int64_t KS, int8_t* __restrict__ q, int8_t* __restrict__ Kr, int* __restrict__ knz) {
+                    int64_t rows, int64_t KS, int8_t* __restrict__ q, int8_t* __restrict__ Kr, int* __restrict__ knz,
+                    const uint32_t* __restrict__ koff) {
   constexpr int TR = OZ_BM;
   constexpr int PARTS = OZ_BK / EL;          // threads per (row, k-step)
   constexpr int W = EL / 4;                  // 32-bit words per slice
@@ -265,6 +277,14 @@ ozaki_points_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, in
     const int64_t row = t * TR + i;
     const int64_t gi = row0 + row;
     const int64_t j0 = ks * OZ_BK + EL * h;
+    // sparse image (koff): knz is an INPUT, the slices kept of this block (a bound from the point
+    // boxes, ozaki_sparse_plan); a block keeping none is neither evaluated nor stored.  Uniform over
+    // the 512 consecutive threads of a block, so whole warps leave together.
+    int keep = S;
+    if (koff) {
+      keep = knz[t * KS + ks];
+      if (keep == 0) continue;
+    }
     double xi[DMAX];   // DMAX = 4: registers (d <= 4), else local memory
 #pragma unroll
     for (int k = 0; k < DMAX; ++k) xi[k] = (k < d && row < rows) ? X[gi * d + k] : 0.0;
@@ -304,15 +324,18 @@ ozaki_points_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, in
       if (CRT) kq[k] = kp;
     }
     // a warp holds 8 rows x 4 column parts of one (tile, k-step) block: reduce, one atomic per warp
-    if (knz) {
+    if (knz && !koff) {
       const int wnz = (int)__reduce_max_sync(0xffffffffu, (unsigned)nz);
       if ((threadIdx.x & 31) == 0 && wnz > 0) atomicMax(knz + t * KS + ks, wnz);
     }
     const uint32_t o = (uint32_t)(i * OZ_BK + EL * h);
     const uint32_t phys = o ^ (((o >> 7) & 1u) << 4);
-    int8_t* base = q + (t * KS + ks) * (int64_t)S * TR * OZ_BK + phys;
+    // dense: all S slices of the block; sparse: its last `keep` slices at slice offset koff[block]
+    int8_t* base = koff ? q + ((int64_t)koff[t * KS + ks] - (S - keep)) * (int64_t)(TR * OZ_BK) + phys
+                        : q + (t * KS + ks) * (int64_t)S * TR * OZ_BK + phys;
 #pragma unroll
     for (int s = 0; s < S; ++s) {
+      if (s < S - keep) continue;
       if (W == 4)
         *reinterpret_cast<uint4*>(base + (int64_t)s * TR * OZ_BK) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
       else
@@ -359,6 +382,51 @@ ozaki_points_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, in
   }
 }
 
+// ---- plan of a SPARSE slice image (float32 K, points in Morton order): boxes of the points of each
+// 128-row tile and each 32-column k-step, then per (tile, k-step) block an upper bound on |K| from
+// the boxes' distance and from it how many of the S = 3 slices can be nonzero (the balanced digits
+// of k = rint(x 2^24): none when |k| < 1/2, only the last when |k| <= 127, the last two when
+// |k| <= 32639).  A block keeps that many trailing slices; an exclusive scan gives their offsets.
+__global__ void oz_boxes_kernel(const double* __restrict__ X, int64_t first, int64_t count, int d, int64_t group,
+                                int64_t groups, double* __restrict__ box) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= groups) return;
+  double lo[4], hi[4];
+  for (int c = 0; c < 4; ++c) {
+    lo[c] = INFINITY;
+    hi[c] = -INFINITY;
+  }
+  const int64_t a = g * group, b = min64(count, a + group);
+  for (int64_t i = a; i < b; ++i)
+    for (int c = 0; c < d; ++c) {
+      const double x = X[(first + i) * d + c];
+      lo[c] = fmin(lo[c], x);
+      hi[c] = fmax(hi[c], x);
+    }
+  for (int c = 0; c < 4; ++c) {
+    box[g * 8 + c] = lo[c];
+    box[g * 8 + 4 + c] = hi[c];
+  }
+}
+
+__global__ void oz_keep_kernel(const double* __restrict__ tbox, const double* __restrict__ kbox, int64_t tiles,
+                               int64_t KS, int d, KernelParams kp, double scl, int64_t row0, int64_t rows,
+                               int* __restrict__ keep) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= tiles * KS) return;
+  const int64_t t = e / KS, k = e - t * KS;
+  double r2 = 0.0;
+  for (int c = 0; c < d; ++c) {
+    const double g = fmax(0.0, fmax(kbox[k * 8 + c] - tbox[t * 8 + 4 + c], tbox[t * 8 + c] - kbox[k * 8 + 4 + c]));
+    r2 += g * g;
+  }
+  // a block holding a diagonal entry of its rows: bounded by the diagonal a^2 + jitter
+  const int64_t r_lo = row0 + t * OZ_BM, r_hi = row0 + min64(rows, (t + 1) * OZ_BM), c_lo = k * OZ_BK, c_hi = c_lo + OZ_BK;
+  const double kmax = (r_lo < c_hi && c_lo < r_hi) ? kp.diag : kernel_value_f64(kp, r2 * (1.0 - 1e-12));
+  const double km = kmax * scl * (1.0 + 1e-9);   // >= |rint(x 2^24)| of every entry of the block
+  keep[e] = km < 0.49 ? 0 : (km < 126.5 ? 1 : (km < 32638.0 ? 2 : 3));
+}
+
 __global__ void oz_fill_kernel(int64_t rows, double v, double* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < rows) out[i] = v;
@@ -398,13 +466,13 @@ __global__ void oz_split_reduce_kernel(const double* __restrict__ part, int spli
 // SA K digits against SB V digits (float64: 7 x 7; float32 K: 3 x 4), pairs s + t <= nd - 1 <= SB - 1.
 // k-steps whose kept K slices are all zero (lz >= min(SA, nd)) are left out by the producer and the
 // MMA thread alike (same metadata, same sequence of kept steps): no load, no handshake.
-template <int SA, int SB>
+template <int SA, int SB, int BN>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
 ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, int64_t KS,
                 const double* __restrict__ sigma, const double* __restrict__ tau, int64_t rows, int64_t m, int64_t n,
                 int64_t kchunk, double* __restrict__ out, int64_t ldo, int64_t split_stride, int nd,
-                const int* __restrict__ knz, int probe) {
-  using C = OzCfg<SA, SB>;
+                const int* __restrict__ knz, int probe, const uint32_t* __restrict__ koff) {
+  using C = OzCfg<SA, SB, BN>;
   extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -414,7 +482,7 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accfull + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t col0 = (int64_t)blockIdx.x * OZ_BN;
+  const int64_t col0 = (int64_t)blockIdx.x * BN;
   const int64_t row0 = (int64_t)blockIdx.y * OZ_BM;
   const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
   const int64_t kend = min64(n, kbeg + kchunk);
@@ -454,11 +522,31 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
   // leading all-zero K slices of the k-th block of this CTA's range (0 without the metadata), staged
   // in shared memory: the producer and the MMA thread walk it step by step (a global read per step
   // would put an L2 latency on each of their iterations)
+  // The k-steps with a kept K slice are compacted into a list (warp 3) that both walk: fully skipped
+  // steps cost nothing.  Sparse image (koff, float32 K): the slice offset of every block as well.
   __shared__ uint8_t s_lead[C::KMAX / OZ_BK];
+  __shared__ uint16_t s_kept[C::KMAX / OZ_BK];
+  __shared__ uint32_t s_off[SA == OZ_S ? 1 : C::KMAX / OZ_BK];
+  __shared__ int s_cnt;
   const int* kb_nz = knz ? knz + (int64_t)blockIdx.y * KS + kbeg / OZ_BK : nullptr;
-  for (int i = threadIdx.x; i < steps; i += OZ_THREADS) s_lead[i] = kb_nz ? (uint8_t)(SA - kb_nz[i]) : (uint8_t)0;
+  for (int i = threadIdx.x; i < steps; i += OZ_THREADS) {
+    s_lead[i] = kb_nz ? (uint8_t)(SA - kb_nz[i]) : (uint8_t)0;
+    if (SA != OZ_S && koff) s_off[i] = koff[(int64_t)blockIdx.y * KS + kbeg / OZ_BK + i];
+  }
   __syncthreads();
-  auto lead = [&](int s) { return (int)s_lead[s]; };
+  if (warp == 3) {
+    int cnt = 0;
+    for (int b0 = 0; b0 < steps; b0 += 32) {
+      const int i = b0 + lane;
+      const bool kp_ = i < steps && (int)s_lead[i] < na;
+      const unsigned mk = __ballot_sync(0xffffffffu, kp_);
+      if (kp_) s_kept[cnt + __popc(mk & ((1u << lane) - 1u))] = (uint16_t)i;
+      cnt += __popc(mk);
+    }
+    if (lane == 0) s_cnt = cnt;
+  }
+  __syncthreads();
+  const int kept = s_cnt;
 
   if (warp == 0) {   // ---- producer: one bulk copy of the A image and one of the B image per kept k-step
     if (ptx::elect_one()) {
@@ -466,35 +554,53 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
       const int8_t* gb = Bq + ((int64_t)blockIdx.x * KS + kbeg / OZ_BK) * C::B_BYTES;
       // K slices lz .. na-1 (lz leading all-zero slices skipped) and V slices 0 .. nd-1-lz take part:
       // contiguous ranges of the k-step image
-      int it = 0;
-      for (int s = 0; s < steps; ++s) {
-        const int lz = lead(s);
-        if (lz >= na) continue;
-        const int st = it % C::STAGES;
-        if (it >= C::STAGES) ptx::mbar_wait(&empty[st], ((it / C::STAGES) - 1) & 1);
-        ++it;
-        unsigned char* dst = smem + st * C::STAGE;
+      const int groups = (kept + C::GROUP - 1) / C::GROUP;
+      for (int g = 0; g < groups; ++g) {
+        const int st = g % C::STAGES;
+        if (g >= C::STAGES) ptx::mbar_wait(&empty[st], ((g / C::STAGES) - 1) & 1);
         if (probe == 2) {   // RLD_OZ_PROBE=2 (measurement only): no loads, the MMAs read stale stages
           ptx::mbar_arrive(&full[st]);
           continue;
         }
-        const int nbv = (nd - lz) < SB ? (nd - lz) : SB;
-        const uint32_t abytes = (uint32_t)(na - lz) * OZ_A_SLICE, bbytes = (uint32_t)nbv * OZ_B_SLICE;
-        ptx::mbar_arrive_expect_tx(&full[st], abytes + bbytes);
-        bulk_load(dst + lz * OZ_A_SLICE, ga + (int64_t)s * C::A_BYTES + lz * OZ_A_SLICE, abytes, &full[st]);
-        bulk_load(dst + C::A_BYTES, gb + (int64_t)s * C::B_BYTES, bbytes, &full[st]);
+        uint32_t bytes = 0;
+#pragma unroll
+        for (int j = 0; j < C::GROUP; ++j) {
+          const int it = g * C::GROUP + j;
+          if (it >= kept) break;
+          const int lz = s_lead[s_kept[it]];
+          const int nbv = (nd - lz) < SB ? (nd - lz) : SB;
+          bytes += (uint32_t)(na - lz) * OZ_A_SLICE + (uint32_t)nbv * C::B_SLICE;
+        }
+        ptx::mbar_arrive_expect_tx(&full[st], bytes);
+#pragma unroll
+        for (int j = 0; j < C::GROUP; ++j) {
+          const int it = g * C::GROUP + j;
+          if (it >= kept) break;
+          const int s = s_kept[it];
+          const int lz = s_lead[s];
+          unsigned char* dst = smem + st * C::STAGE + j * C::STEP;
+          const int nbv = (nd - lz) < SB ? (nd - lz) : SB;
+          const uint32_t abytes = (uint32_t)(na - lz) * OZ_A_SLICE, bbytes = (uint32_t)nbv * C::B_SLICE;
+          const int8_t* asrc = (SA != OZ_S && koff) ? Aq + (int64_t)s_off[s] * OZ_A_SLICE   // the kept suffix
+                                                    : ga + (int64_t)s * C::A_BYTES + lz * OZ_A_SLICE;
+          bulk_load(dst + lz * OZ_A_SLICE, asrc, abytes, &full[st]);
+          bulk_load(dst + C::A_BYTES, gb + (int64_t)s * C::B_BYTES, bbytes, &full[st]);
+        }
       }
     }
   } else if (warp == 1) {   // ---- MMA issuer
     if (ptx::elect_one()) {
       const uint32_t sbase = ptx::smem_u32(smem);
-      int it = 0;
-      for (int s = 0; s < steps; ++s) {
-        const int lz = lead(s);
-        if (lz >= na) continue;
-        const int st = it % C::STAGES;
-        ptx::mbar_wait(&full[st], (uint32_t)((it / C::STAGES) & 1));
-        const uint32_t a0 = sbase + st * C::STAGE;
+      const int groups = (kept + C::GROUP - 1) / C::GROUP;
+      for (int g = 0; g < groups; ++g) {
+        const int st = g % C::STAGES;
+        ptx::mbar_wait(&full[st], (uint32_t)((g / C::STAGES) & 1));
+#pragma unroll
+        for (int j = 0; j < C::GROUP; ++j) {
+        const int it = g * C::GROUP + j;
+        if (it >= kept) break;
+        const int lz = s_lead[s_kept[it]];
+        const uint32_t a0 = sbase + st * C::STAGE + j * C::STEP;
         const uint32_t b0 = a0 + C::A_BYTES;
         // A slice sa against the stacked B slices 0 .. nd-1-sa at once: the accumulators of the
         // diagonals d = sa + t are adjacent TMEM column blocks, so one N = 64 (nd - sa) product
@@ -509,14 +615,14 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
           const uint64_t adesc = desc_sw32(a0 + sa * OZ_A_SLICE);
           constexpr uint32_t acc = 1u;
           const int cnt = (nd - sa) < SB ? (nd - sa) : SB;   // B slices 0 .. cnt-1, in at most two pieces
-          const int first = cnt == 5 ? 3 : (cnt < 4 ? cnt : 4);
-          mma_i8_ss(tmem + (uint32_t)(sa * OZ_BN), adesc, desc_sw32(b0), idesc_i8(OZ_BM, first * OZ_BN), acc);
+          const int first = (C::PC == 4 && cnt == 5) ? 3 : (cnt < C::PC ? cnt : C::PC);
+          mma_i8_ss(tmem + (uint32_t)(sa * BN), adesc, desc_sw32(b0), idesc_i8(OZ_BM, first * BN), acc);
           if (cnt > first)
-            mma_i8_ss(tmem + (uint32_t)((sa + first) * OZ_BN), adesc, desc_sw32(b0 + first * OZ_B_SLICE),
-                      idesc_i8(OZ_BM, (cnt - first) * OZ_BN), acc);
+            mma_i8_ss(tmem + (uint32_t)((sa + first) * BN), adesc, desc_sw32(b0 + first * C::B_SLICE),
+                      idesc_i8(OZ_BM, (cnt - first) * BN), acc);
+        }
         }
         ptx::tc_commit(&empty[st]);   // the stage is free once these MMAs have read it
-        ++it;
       }
       ptx::tc_commit(accfull);        // (no MMA pending: arrives at once)
     }
@@ -531,7 +637,7 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
     const double sg = (r < rows) ? sigma[r] : 0.0;
     const bool have = true;   // the accumulators are zeroed up front
 #pragma unroll 1
-    for (int c0 = 0; c0 < OZ_BN; c0 += 32) {
+    for (int c0 = 0; c0 < BN; c0 += 32) {
       double part[32];
 #pragma unroll
       for (int e = 0; e < 32; ++e) part[e] = 0.0;
@@ -540,7 +646,7 @@ ozaki_kv_kernel(const int8_t* __restrict__ Aq, const int8_t* __restrict__ Bq, in
         for (int d = nd - 1; d >= 0; --d) {   // small terms first
           const double w = __longlong_as_double((long long)(1023 - OZ_DBITS * (d + 2)) << 52);   // 2^{-8(d+2)}
           uint32_t v[32];
-          ptx::tmem_ld_32x32b_x32(tmem + lane_base + (uint32_t)(d * OZ_BN + c0), v);
+          ptx::tmem_ld_32x32b_x32(tmem + lane_base + (uint32_t)(d * BN + c0), v);
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int e = 0; e < 32; ++e) part[e] = fma(w, (double)(int32_t)v[e], part[e]);
@@ -612,13 +718,43 @@ void ozaki_slice(const double* A, int64_t lda, int64_t rows, int64_t n, int tile
     ozaki_digits_kernel<OZ_BN, OZ_S><<<blocks, 256, 0, st>>>(A, lda, rows, n, scale, KS, q);
   else if (tile_rows == OZ_BN && slices == OZ_V32)
     ozaki_digits_kernel<OZ_BN, OZ_V32><<<blocks, 256, 0, st>>>(A, lda, rows, n, scale, KS, q);
+  else if (tile_rows == 128 && slices == OZ_V32)
+    ozaki_digits_kernel<128, OZ_V32><<<blocks, 256, 0, st>>>(A, lda, rows, n, scale, KS, q);
   else
     fail(RLD_ERR_INVALID_ARGUMENT, "ozaki_slice: tile rows must be 128 (K) or 64 (V), 7 (or, V: 4) slices");
   RLD_LAUNCH_CHECK();
 }
 
+// Plan of the sparse 3-slice image of the local rows' float32 K (points X in Morton order, d <= 4):
+// keep[block] = slices kept (0..3, a bound from the point boxes), koff[block] = their slice offset
+// (exclusive scan).  Returns the number of slices kept in all (bytes = 4096 x that).
+int64_t ozaki_sparse_plan(const double* X, int64_t n, const KernelParams& kp, int64_t row0, int64_t rows, int* keep,
+                          uint32_t* koff, DevBuf& scratch, cudaStream_t st) {
+  if (rows <= 0) return 0;
+  if (kp.d > 4) fail(RLD_ERR_NOT_SUPPORTED, "ozaki_sparse_plan: d > 4");
+  const int64_t tiles = ceil_div(rows, OZ_BM), KS = ceil_div(n, OZ_BK), nb = tiles * KS;
+  scratch.reserve(sizeof(double) * 8 * (tiles + KS));
+  double* tb = scratch.as<double>();
+  double* kb = tb + 8 * tiles;
+  oz_boxes_kernel<<<(unsigned)ceil_div(tiles, 128), 128, 0, st>>>(X, row0, rows, kp.d, OZ_BM, tiles, tb);
+  RLD_LAUNCH_CHECK();
+  oz_boxes_kernel<<<(unsigned)ceil_div(KS, 128), 128, 0, st>>>(X, 0, n, kp.d, OZ_BK, KS, kb);
+  RLD_LAUNCH_CHECK();
+  const int ee = oz_scale_exp(kp.diag > 0.0 ? kp.diag : 1.0);   // sigma = 2^(ee+1), as ozaki_slice_points
+  const double scl = ldexp(1.0, OZ_DBITS * OZ_S32 - (ee + 1));
+  oz_keep_kernel<<<(unsigned)ceil_div(nb, 256), 256, 0, st>>>(tb, kb, tiles, KS, kp.d, kp, scl, row0, rows, keep);
+  RLD_LAUNCH_CHECK();
+  thrust::exclusive_scan(thrust::cuda::par.on(st), keep, keep + nb, koff, 0u);
+  uint32_t last_off = 0;
+  int last_keep = 0;
+  RLD_CUDA(cudaMemcpyAsync(&last_off, koff + nb - 1, sizeof last_off, cudaMemcpyDeviceToHost, st));
+  RLD_CUDA(cudaMemcpyAsync(&last_keep, keep + nb - 1, sizeof last_keep, cudaMemcpyDeviceToHost, st));
+  RLD_CUDA(cudaStreamSynchronize(st));
+  return (int64_t)last_off + last_keep;
+}
+
 void ozaki_slice_points(const double* X, int64_t n, const KernelParams& kp, int64_t row0, int64_t rows, int8_t* q,
-                        double* scale, cudaStream_t st, int8_t* Kr, int* knz, int slices) {
+                        double* scale, cudaStream_t st, int8_t* Kr, int* knz, int slices, const uint32_t* koff) {
   if (rows <= 0) return;
   if (kp.d > RLD_MAX_DIM) fail(RLD_ERR_NOT_SUPPORTED, "ozaki_slice_points: d > 32");
   const int ee = oz_scale_exp(kp.diag > 0.0 ? kp.diag : 1.0);
@@ -627,39 +763,42 @@ void ozaki_slice_points(const double* X, int64_t n, const KernelParams& kp, int6
   const int64_t KS = ceil_div(n, OZ_BK);
   const int64_t total = ceil_div(rows, OZ_BM) * OZ_BM * KS * 4;
   const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)oz_sms() * 16);
-  if (knz) RLD_CUDA(cudaMemsetAsync(knz, 0, sizeof(int) * ceil_div(rows, OZ_BM) * KS, st));
+  if (koff && (slices != OZ_S32 || !knz)) fail(RLD_ERR_INVALID_ARGUMENT, "ozaki_slice_points: sparse image needs 3 slices and its plan");
+  if (knz && !koff) RLD_CUDA(cudaMemsetAsync(knz, 0, sizeof(int) * ceil_div(rows, OZ_BM) * KS, st));
   if (slices == OZ_S32) {   // float32 K: 24 bits of the float64 kernel value relative to the row scale
     if (Kr || kp.d > 4) fail(RLD_ERR_INVALID_ARGUMENT, "ozaki_slice_points: 3 slices need d <= 4 and no CRT image");
-    ozaki_points_kernel<false, 8, 4, OZ_S32><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, nullptr, knz);
+    ozaki_points_kernel<false, 8, 4, OZ_S32><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, nullptr, knz, koff);
   } else if (slices != OZ_S)
     fail(RLD_ERR_INVALID_ARGUMENT, "ozaki_slice_points: 7 or 3 slices");
   else if (Kr && kp.d <= 4)
-    ozaki_points_kernel<true, 8, 4, OZ_S><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, Kr, knz);
+    ozaki_points_kernel<true, 8, 4, OZ_S><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, Kr, knz, nullptr);
   else if (Kr)
-    ozaki_points_kernel<true, 8, RLD_MAX_DIM, OZ_S><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, Kr, knz);
+    ozaki_points_kernel<true, 8, RLD_MAX_DIM, OZ_S><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, Kr, knz, nullptr);
   else if (kp.d <= 4)
-    ozaki_points_kernel<false, 8, 4, OZ_S><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, nullptr, knz);
+    ozaki_points_kernel<false, 8, 4, OZ_S><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, nullptr, knz, nullptr);
   else
-    ozaki_points_kernel<false, 8, RLD_MAX_DIM, OZ_S><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, nullptr, knz);
+    ozaki_points_kernel<false, 8, RLD_MAX_DIM, OZ_S><<<blocks, 256, 0, st>>>(X, n, kp, row0, rows, KS, q, nullptr, knz,
+                                                                             nullptr);
   RLD_LAUNCH_CHECK();
 }
 
 namespace {
 
-template <int SA, int SB>
+template <int SA, int SB, int BN>
 void launch_product(const int8_t* Kq, const double* ksigma, int64_t rows, int64_t n, const double* V, int64_t ldv,
-                    int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st, int diags, const int* knz) {
-  using C = OzCfg<SA, SB>;
+                    int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st, int diags, const int* knz,
+                    const uint32_t* koff) {
+  using C = OzCfg<SA, SB, BN>;
   if (diags < 1 || diags > SB) fail(RLD_ERR_INVALID_ARGUMENT, "kv_product_ozaki: diagonals out of range");
-  ws.oz_vq.reserve((size_t)ozaki_bytes(m, n, OZ_BN, SB));
+  ws.oz_vq.reserve((size_t)ozaki_bytes(m, n, BN, SB));
   ws.oz_tau.reserve(sizeof(double) * m);
-  ozaki_slice(V, ldv, m, n, OZ_BN, ws.oz_vq.as<int8_t>(), ws.oz_tau.as<double>(), st, SB);
+  ozaki_slice(V, ldv, m, n, BN, ws.oz_vq.as<int8_t>(), ws.oz_tau.as<double>(), st, SB);
   static std::atomic<uint64_t> attr{0};
   once_per_device(attr, [&] {
-    RLD_CUDA(cudaFuncSetAttribute(ozaki_kv_kernel<SA, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    RLD_CUDA(cudaFuncSetAttribute(ozaki_kv_kernel<SA, SB, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   });
   const int64_t KS = ceil_div(n, OZ_BK);
-  const int64_t passes = ceil_div(m, OZ_BN), tiles = ceil_div(rows, OZ_BM);
+  const int64_t passes = ceil_div(m, BN), tiles = ceil_div(rows, OZ_BM);
   const int64_t units0 = passes * tiles;
   const int64_t slots = oz_sms();
   // k splits: every CTA <= OZ_KMAX columns (exact int32), >= 64 k-steps; the fewest splits whose
@@ -685,16 +824,16 @@ void launch_product(const int8_t* Kq, const double* ksigma, int64_t rows, int64_
   const char* pe = getenv("RLD_OZ_PROBE");   // kernel-phase probe for measurement, never set in production
   const int probe = pe ? atoi(pe) : 0;
   if (splits == 1) {
-    ozaki_kv_kernel<SA, SB><<<grid, OZ_THREADS, C::SMEM, st>>>(Kq, Bq, KS, ksigma, ws.oz_tau.as<double>(), rows, m, n,
-                                                              kchunk, Y, ldy, 0, diags, knz, probe);
+    ozaki_kv_kernel<SA, SB, BN><<<grid, OZ_THREADS, C::SMEM, st>>>(Kq, Bq, KS, ksigma, ws.oz_tau.as<double>(), rows, m, n,
+                                                              kchunk, Y, ldy, 0, diags, knz, probe, koff);
     RLD_LAUNCH_CHECK();
     return;
   }
   const int64_t stride = m * rows;
   ws.partial.reserve(sizeof(double) * stride * splits);
-  ozaki_kv_kernel<SA, SB><<<grid, OZ_THREADS, C::SMEM, st>>>(Kq, Bq, KS, ksigma, ws.oz_tau.as<double>(), rows, m, n,
+  ozaki_kv_kernel<SA, SB, BN><<<grid, OZ_THREADS, C::SMEM, st>>>(Kq, Bq, KS, ksigma, ws.oz_tau.as<double>(), rows, m, n,
                                                             kchunk, ws.partial.as<double>(), rows, stride, diags, knz,
-                                                            probe);
+                                                            probe, koff);
   RLD_LAUNCH_CHECK();
   const unsigned gy = (unsigned)std::min<int64_t>(m, 65535);
   const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 512), slots * 8 / gy + 1));
@@ -709,12 +848,15 @@ void launch_product(const int8_t* Kq, const double* ksigma, int64_t rows, int64_
 // tiles, 7 or 4 slices) into ws.oz_vq.  diags <= 0: all of them.
 void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int64_t n, const double* V, int64_t ldv,
                       int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st, int diags,
-                      const int* knz, int kslices) {
+                      const int* knz, int kslices, const uint32_t* koff) {
   if (m <= 0 || rows <= 0) return;
+  if (koff && (kslices != OZ_S32 || !knz)) fail(RLD_ERR_INVALID_ARGUMENT, "kv_product_ozaki: sparse image needs 3 slices");
   if (kslices == OZ_S)
-    launch_product<OZ_S, OZ_S>(Kq, ksigma, rows, n, V, ldv, m, Y, ldy, ws, st, diags <= 0 ? OZ_S : diags, knz);
-  else if (kslices == OZ_S32)
-    launch_product<OZ_S32, OZ_V32>(Kq, ksigma, rows, n, V, ldv, m, Y, ldy, ws, st, OZ_V32, knz);
+    launch_product<OZ_S, OZ_S, OZ_BN>(Kq, ksigma, rows, n, V, ldv, m, Y, ldy, ws, st, diags <= 0 ? OZ_S : diags, knz, nullptr);
+  else if (kslices == OZ_S32 && m <= 96)
+    launch_product<OZ_S32, OZ_V32, OZ_BN>(Kq, ksigma, rows, n, V, ldv, m, Y, ldy, ws, st, OZ_V32, knz, koff);
+  else if (kslices == OZ_S32)   // wide products: 128 vectors per pass
+    launch_product<OZ_S32, OZ_V32, 128>(Kq, ksigma, rows, n, V, ldv, m, Y, ldy, ws, st, OZ_V32, knz, koff);
   else
     fail(RLD_ERR_INVALID_ARGUMENT, "kv_product_ozaki: 7 or 3 K slices");
 }

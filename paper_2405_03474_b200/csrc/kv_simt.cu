@@ -273,7 +273,7 @@ void kv_product(const KvOperand& op, int64_t m, const double* V, int64_t ldv, do
     return;
   }
   if (op.kq) {   // float32 K held as 3 int8 slices (Morton-ordered points, kv_ozaki.cu)
-    kv_product_ozaki(op.kq, op.ksigma, op.rows, op.n, V, ldv, m, Y, ldy, ws, st, 0, op.knz, op.kslices);
+    kv_product_ozaki(op.kq, op.ksigma, op.rows, op.n, V, ldv, m, Y, ldy, ws, st, 0, op.knz, op.kslices, op.koff);
     return;
   }
   if (kv_tc_supported(op) && (op.tiled || !getenv("RLD_NO_TC"))) {

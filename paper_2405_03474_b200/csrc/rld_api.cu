@@ -96,8 +96,11 @@ struct Resident {
   DevBuf pts4;               // points split to n x 8 fp32 hi/lo (d <= 4; tensor-core on-the-fly tiles)
   DevBuf diag;               // local diagonal of K (float64)
   DevBuf Kq, ksigma;         // K as exact int8 slices (kv_ozaki.cu): float64 (7 slices, RLD_FP64_PRODUCT=ozaki)
-  bool kq_ready = false;     // or float32 from Morton-ordered points (3 slices)
+  bool kq_ready = false;     // or float32 from Morton-ordered points (3 slices, sparse image)
   int kslices = 7;
+  DevBuf koff;               // sparse 3-slice image: slice offset of every block (kv_ozaki.cu)
+  bool koff_ready = false;
+  bool cached = false;       // on-the-fly float32 problem whose sparse slice image fits in HBM: served from it
   DevBuf perm;               // points held in Morton (Z-curve) order: perm[i] = original index of point i
   bool permuted = false;     // (single GPU, float64 stored products: far-field slice blocks are all-zero)
   DevBuf knz;                // per slice-image block: slices from the first nonzero one (skipped leading zeros)
@@ -120,9 +123,10 @@ struct Resident {
     o.pts4 = (source == RLD_SOURCE_POINTS && d <= 4) ? pts4.as<float>() : nullptr;
     o.kp = kp;
     o.dtype = dtype;
-    if (kq_ready && path != RLD_PATH_ON_THE_FLY) {
+    if (kq_ready && (path != RLD_PATH_ON_THE_FLY || cached)) {
       o.kq = Kq.as<int8_t>();
       o.kslices = kslices;
+      if (koff_ready) o.koff = koff.as<uint32_t>();
       o.ksigma = ksigma.as<double>();
       if (knz_ready) o.knz = knz.as<int>();
       if (kr_ready) o.kr = Kr.as<int8_t>();
@@ -242,7 +246,8 @@ bool sort_points(const rld_handle* h, const rld_problem* p) {
          p->n < (int64_t)1 << 31;
 }
 
-void prepare(rld_handle* h, const rld_problem* p) {
+// plain: the points as given (no Morton order, no slice image): rld_build_covariance's upload
+void prepare(rld_handle* h, const rld_problem* p, bool plain = false) {
   NvtxRange nv("rld:prepare (K rows / points to HBM)");
   if (!p) fail(RLD_ERR_INVALID_ARGUMENT, "problem is NULL");
   if (p->n < 1) fail(RLD_ERR_INVALID_ARGUMENT, "n must be >= 1");
@@ -252,6 +257,8 @@ void prepare(rld_handle* h, const rld_problem* p) {
   r.ready = false;
   r.tiled = false;
   r.kq_ready = false;
+  r.koff_ready = false;
+  r.cached = false;
   r.kslices = 7;
   r.kr_ready = false;
   r.knz_ready = false;
@@ -287,7 +294,7 @@ void prepare(rld_handle* h, const rld_problem* p) {
     r.kp.diag = r.kp.a2 + p->jitter;
     const size_t xb = sizeof(double) * p->n * p->d;
     r.X.reserve(xb);
-    if (sort_points(h, p)) {
+    if (!plain && sort_points(h, p)) {
       // float64 stored products on int8 slices: points in Morton order make the K blocks away from
       // the diagonal small, and their leading slices all zero, which the product skips (kv_ozaki.cu).
       // Every n-vector entering or leaving the resident frame is permuted (probes, sketch rows, the
@@ -309,7 +316,43 @@ void prepare(rld_handle* h, const rld_problem* p) {
       // coordinates pre-scaled so the tile generator's r^2 is the kernel argument
       const double scale = p->family == RLD_MATERN52 ? r.kp.s5_over_l : std::sqrt(r.kp.inv_2l2 * 1.4426950408889634);
       pad_points(r.X.as<double>(), p->n, p->d, scale, r.pts4.as<float>(), st);
-      if (r.permuted && r.path == RLD_PATH_ON_THE_FLY && p->dtype == RLD_FP32 && r.rows > 0) {
+      if (r.permuted && p->dtype == RLD_FP32 && fp32_product_slices() && r.rows > 0) {
+        // float32 K from Morton-ordered points (d <= 3, one GPU) as a SPARSE image of 3 int8 slices:
+        // the float64 kernel value rounded to 24 bits of its row scale (float32-grade next to the
+        // diagonal; far-field entries below 2^-25 of the scale are exactly zero), only the slices a
+        // bound from the point boxes allows to be nonzero are evaluated and stored, and the product
+        // multiplies them with 4 slices of V on the INT8 tensor cores (kv_ozaki.cu <3, 4>).  A
+        // stored problem always takes it (<= 3 bytes per entry, no fp32 K); an on-the-fly problem
+        // when the image leaves a quarter of HBM free (config 4: clustered points, most blocks
+        // empty), and is then served from HBM instead of regenerating K for every product.
+        const int64_t nb = ceil_div(r.rows, 128) * ceil_div(p->n, 32);
+        r.knz.reserve(sizeof(int) * nb);
+        r.koff.reserve(sizeof(uint32_t) * nb);
+        const int64_t kept = ozaki_sparse_plan(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.knz.as<int>(),
+                                               r.koff.as<uint32_t>(), h->wk.scratch2, st);
+        const int64_t bytes = std::max<int64_t>(kept, 1) * 4096;
+        bool take = r.path == RLD_PATH_STORED;
+        const char* ce = getenv("RLD_OTF_CACHE");   // 0: always regenerate K on the fly (read per prepare)
+        if (!take && !(ce && ce[0] == '0')) {
+          size_t fr = 0, tot = 0;
+          RLD_CUDA(cudaMemGetInfo(&fr, &tot));
+          // room for the estimate's workspaces: ~6 blocks of w x n float64 at the largest BASELINE
+          // sketch width (w = 2058; the configuration is not known at prepare) and 8 GB of slack
+          const int64_t need = 6 * 2058 * p->n * (int64_t)sizeof(double) + ((int64_t)8 << 30);
+          (void)tot;
+          take = kept < ((int64_t)1 << 32) && bytes + need <= (int64_t)fr + (int64_t)r.Kq.bytes;
+        }
+        if (take) {
+          r.Kq.reserve((size_t)bytes);
+          r.ksigma.reserve(sizeof(double) * r.rows);
+          ozaki_slice_points(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.Kq.as<int8_t>(), r.ksigma.as<double>(),
+                             st, nullptr, r.knz.as<int>(), 3, r.koff.as<uint32_t>());
+          r.kslices = 3;
+          r.kq_ready = r.knz_ready = r.koff_ready = true;
+          r.cached = r.path == RLD_PATH_ON_THE_FLY;
+        }
+      }
+      if (!r.kq_ready && r.permuted && r.path == RLD_PATH_ON_THE_FLY && p->dtype == RLD_FP32 && r.rows > 0) {
         r.otf_skip.reserve(sizeof(uint32_t) * otf_skip_words(r.rows, p->n));
         otf_skip_map(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.otf_skip.as<uint32_t>(), h->wk.scratch2, st);
         // the order pays only where it skips enough: its per-k-step flushes (kv_otf.cu) cost ~13 %
@@ -365,23 +408,9 @@ void prepare(rld_handle* h, const rld_problem* p) {
         r.Kbuf.reserve(sizeof(double) * r.rows * r.ldk);
         r.K = r.Kbuf.ptr;
         build_kernel_rows<double>(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.Kbuf.as<double>(), r.ldk, st);
-      } else if (r.permuted && fp32_product_slices()) {
-        // float32 K from Morton-ordered points (d <= 3, one GPU): 3 int8 slices = the float64 kernel
-        // value rounded to 24 bits of its row scale (float32-grade next to the diagonal; far-field
-        // entries below 2^-25 of the scale are exactly zero and their blocks are skipped), multiplied
-        // with 4 slices of V on the INT8 tensor cores (kv_ozaki.cu).  3 bytes per entry, no fp32 K.
+      } else if (r.kq_ready) {   // float32 K held as the sparse 3-slice image built above: no fp32 K
         r.K = nullptr;
         r.ldk = 0;
-        r.kslices = 3;
-        if (r.rows > 0) {
-          r.Kq.reserve((size_t)ozaki_bytes(r.rows, p->n, 128, 3));
-          r.ksigma.reserve(sizeof(double) * r.rows);
-          r.knz.reserve(sizeof(int) * ceil_div(r.rows, 128) * ceil_div(p->n, 32));
-          ozaki_slice_points(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.Kq.as<int8_t>(), r.ksigma.as<double>(),
-                             st, nullptr, r.knz.as<int>(), 3);
-          r.knz_ready = true;
-        }
-        r.kq_ready = r.rows > 0;
       } else {   // fp32: 16 KB tiles, one contiguous TMA box per tensor-core step
         r.tiled = true;
         r.ldk = 0;
@@ -1659,8 +1688,8 @@ int rld_build_covariance(rld_handle* h, const rld_problem* p, void* out, int32_t
     if (!out) fail(RLD_ERR_INVALID_ARGUMENT, "out is NULL");
     if (h->world != 1) fail(RLD_ERR_NOT_SUPPORTED, "build_covariance is single-GPU");
     rld_problem q = *p;
-    q.path = RLD_PATH_ON_THE_FLY;  // upload points only
-    prepare(h, &q);
+    q.path = RLD_PATH_ON_THE_FLY;  // upload points only, in the caller's order
+    prepare(h, &q, true);
     Resident& r = h->res;
     const size_t es = p->dtype == RLD_FP64 ? 8 : 4;
     if (out_memory == RLD_DEVICE) {

@@ -102,6 +102,7 @@ struct KvOperand {
   int dtype = RLD_FP64;      // product arithmetic
   const int8_t* kq = nullptr;      // K as exact int8 slices, k-step-tiled image (kv_ozaki.cu), or null
   int kslices = 7;                 // 7: float64 K; 3: float32 K (Morton-ordered points)
+  const uint32_t* koff = nullptr;  // sparse 3-slice image: slice offset of every block's kept slices
   const double* ksigma = nullptr;  // per-row power-of-two scales of the slices
   const int* knz = nullptr;        // per (tile, k-step) block: slices from the first nonzero one (or null)
   int64_t n = 0;             // columns of K (global order)
@@ -182,10 +183,16 @@ void ozaki_slice(const double* A, int64_t lda, int64_t rows, int64_t n, int tile
 // knz != null: per (128-row tile, 32-column k-step) block, slices - the number of leading all-zero slices
 // (int [ceil(rows/128)][ceil(n/32)]), which the product skips
 void ozaki_slice_points(const double* X, int64_t n, const KernelParams& kp, int64_t row0, int64_t rows, int8_t* q,
-                        double* scale, cudaStream_t st, int8_t* Kr = nullptr, int* knz = nullptr, int slices = 7);
+                        double* scale, cudaStream_t st, int8_t* Kr = nullptr, int* knz = nullptr, int slices = 7,
+                        const uint32_t* koff = nullptr);
+// sparse 3-slice image of a float32 K (Morton-ordered points): per block the slices kept (a bound from
+// the point boxes) and their slice offsets; returns the slices kept in all (4096 bytes each).  The
+// image is then written by ozaki_slice_points(..., knz = keep, slices = 3, koff)
+int64_t ozaki_sparse_plan(const double* X, int64_t n, const KernelParams& kp, int64_t row0, int64_t rows, int* keep,
+                          uint32_t* koff, DevBuf& scratch, cudaStream_t st);
 void kv_product_ozaki(const int8_t* Kq, const double* ksigma, int64_t rows, int64_t n, const double* V, int64_t ldv,
                       int64_t m, double* Y, int64_t ldy, KvWorkspace& ws, cudaStream_t st, int diags = 7,
-                      const int* knz = nullptr, int kslices = 7);
+                      const int* knz = nullptr, int kslices = 7, const uint32_t* koff = nullptr);
 // Wide float64 products as 15 modular int8 GEMMs + CRT (kv_crt.cu); the residue image of K comes
 // from its slice image (crt_residues, 15 bytes per entry).
 bool crt_supported(int64_t n);

@@ -29,6 +29,13 @@ def rld():
     return rld
 
 
+@pytest.fixture(autouse=True)
+def _no_slice_cache(monkeypatch):
+    """These tests are about the on-the-fly kernel: keep d <= 3 problems from being served from the
+    cached sparse int8-slice image (rld_api.cu prepare; tests/test_gpu_streams_dmma.py covers that)."""
+    monkeypatch.setenv("RLD_OTF_CACHE", "0")
+
+
 def _product(rld, spec, pts, V, kind=None, monkeypatch=None):
     import torch
 

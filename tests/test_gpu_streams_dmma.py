@@ -216,6 +216,32 @@ def test_fp32_int8_slices_product(rld, index, n, m, monkeypatch):
     assert np.max(np.abs(Y - Y2)) <= 4e-6 * np.max(np.abs(ref))
 
 
+@pytest.mark.parametrize("index,n", [(4, 6000), (3, 5000), (5, 4099)])
+def test_on_the_fly_fp32_served_from_cached_slices(rld, index, n, monkeypatch):
+    """An on-the-fly float32 problem from d <= 3 points whose sparse 3-slice image fits in HBM is
+    served from that image (config 4: clustered points, most blocks empty): the same image and
+    kernels as the stored path, so estimates are bit-identical to it; RLD_OTF_CACHE=0 regenerates K
+    per product (kv_otf.cu) and agrees at the float32 level."""
+    import ctypes as C
+
+    from paper_2405_03474_b200.workloads import baseline
+
+    wl = baseline(index, n=n, rank=64, num_probes=8, dtype="fp32")
+    M = rld.KernelMatrix(wl.spec, wl.points)
+    stats = (C.c_int64 * 4)()
+    R = rld.ResidentMatrix(M, dtype="fp32", path="on_the_fly")
+    assert R.sess.lib.rld_slice_stats(R.sess.handle.ptr, stats) == 0 and stats[0] > 0
+    assert stats[1] <= 3 * stats[0]
+    a = R.estimate(replace(wl.config, path="on_the_fly"))
+    b = rld.ResidentMatrix(M, dtype="fp32", path="stored").estimate(replace(wl.config, path="stored"))
+    assert a.value == b.value and a.logdet_P == b.logdet_P
+    monkeypatch.setenv("RLD_OTF_CACHE", "0")
+    R0 = rld.ResidentMatrix(M, dtype="fp32", path="on_the_fly")
+    assert R0.sess.lib.rld_slice_stats(R0.sess.handle.ptr, stats) == 0 and stats[0] == 0
+    c = R0.estimate(replace(wl.config, path="on_the_fly"))
+    assert rel(a.value, c.value) <= 1e-5, (a.value, c.value)
+
+
 def test_int8_slices_from_points_equal_slices_from_K(rld, monkeypatch):
     """Stored float64 from the points slices K straight from the points (no float64 K in HBM); from
     a dense device K built by build_covariance it slices the stored rows: same entries, same row
