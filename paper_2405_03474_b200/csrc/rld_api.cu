@@ -506,7 +506,13 @@ void prepare(rld_handle* h, const rld_problem* p, bool plain = false) {
     // the CRT residue image for the wide (sketch) products, where it fits beside the slices
     const int64_t bytes = crt_bytes(r.rows, r.n);
     size_t fr = 0, tot = 0;
-    RLD_CUDA(cudaStreamSynchronize(st));
+    if (!r.kq_ready && r.Kq.bytes > ((size_t)1 << 30)) {
+    // a large slice image of an earlier problem (grow-only buffers) would starve this one's workspaces
+    r.Kq.release();
+    r.koff.release();
+    r.knz.release();
+  }
+  RLD_CUDA(cudaStreamSynchronize(st));
     RLD_CUDA(cudaMemGetInfo(&fr, &tot));
     if ((int64_t)r.Kr.bytes >= bytes || (int64_t)fr > bytes + (int64_t)(tot / 16)) {
       r.Kr.reserve((size_t)bytes);
