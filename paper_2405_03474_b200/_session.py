@@ -103,7 +103,8 @@ class Session:
             raise ValueError(f"unknown path {path!r}")
         n = M.n
         rows = -(-n // self.world_size)
-        # fp64 from points: the float64 K or (default product) its 8 int8 slices, 8 bytes per entry
+        # fp64 from points: the float64 K (8 bytes per entry) or, by default, its 7 int8 slices; fp32: 4-byte
+        # tiles or at most 3 int8 slices
         es = 8 if dtype == "fp64" else 4
         return "stored" if rows * n * es <= 0.5 * hbm_bytes(self.device) else "on_the_fly"
 
