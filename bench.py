@@ -13,21 +13,27 @@ A step is one full estimate (preconditioner build + s-probe Lanczos +
 multishift solves + Hutchinson mean) -- the reference's timer scope
 (src/estimators.py:81-96).
 
-* ``value``: estimates/s with K, the sketch rows and the probes resident in HBM
-  (K = 1.07 GB fp32 > 126 MB L2, so every product streams K from HBM), CUDA
-  events on the handle's stream around exactly K steps, max over ranks.
+* ``value``: estimates/s with K resident in HBM (float64: 30 GB of int8 slices, far
+  larger than the 126 MB L2, so every product streams K from HBM), CUDA events on
+  the handle's stream around exactly K steps, max over ranks.
 * ``e2e``: the same metric through the C ABI call the public API makes, with host
   buffers -- every step uploads the points from pinned memory, builds K on the
   GPU, regenerates the reference's probe / sketch streams on the GPU, runs the
   estimate and reads the result back.
-* ``roofline``: the dominant kernel (the K x block product, Lanczos shape),
-  timed live with CUDA events.  float64: FP64 tensor cores (DMMA), algorithmic
-  flops 2 n^2 s per launch against the measured DMMA peak; float32 stored:
+* ``roofline``: the dominant kernel, timed live with CUDA events.  float64 stored
+  (default): the int8-slice product at the sketch shape m = w (tensor-bound against
+  the sustained int8 rate; work from rld_slice_stats), with the same kernel at the
+  Lanczos shape m = s beside it (``roofline_lanczos``: HBM-bound on the slices
+  read); RLD_FP64_PRODUCT=dmma: DMMA against the measured DMMA peak; float32 tiles:
   HBM, algorithmic bytes 4 n^2 (K) + 4 n s (operand) + 8 n s (result).
+* extra keys: ``extra_fp32`` (config 3 in fp32: K as 3 int8 slices), ``extra_otf``
+  (config 4 at full n, path on_the_fly, served from the cached sparse slice image;
+  the on-the-fly kernel's own roofline beside it; config 5's product at n = 2^20),
+  ``extra_e2e_dense`` (a dense float64 host M through rld_logdet).
 * ``cpu_baseline``: the oracle port (float64 numpy restatement of the
   reference, per-probe loop like the reference) on this host's cores.  The
   reference's dense K does not fit host RAM at n = 65536, so the
-  sample is the same configuration at n = 16384, extrapolated by n^2 (labelled).
+  sample is the same configuration at n ~ 14336, extrapolated by n^2 (labelled).
 * ``--impl reference``: that CPU implementation is the timed arm.
 
 Multi-GPU (torchrun, one process per GPU): by default the rows of K and of every
