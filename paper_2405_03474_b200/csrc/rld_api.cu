@@ -102,7 +102,7 @@ struct Resident {
   bool koff_ready = false;
   bool cached = false;       // on-the-fly float32 problem whose sparse slice image fits in HBM: served from it
   DevBuf perm;               // points held in Morton (Z-curve) order: perm[i] = original index of point i
-  bool permuted = false;     // (single GPU, float64 stored products: far-field slice blocks are all-zero)
+  bool permuted = false;     // (every rank alike; far-field slice blocks are then all-zero and skipped)
   DevBuf knz;                // per slice-image block: slices from the first nonzero one (skipped leading zeros)
   DevBuf otf_skip;           // on the fly (fp32, Morton order): far-field (tile, k-step) skip bits
   bool otf_skip_ready = false;
@@ -233,7 +233,7 @@ void allreduce_flags(rld_handle* h, int* hflags, int count) {
 }
 
 // Locality order (Morton, morton_order_device) for the points of the products that skip exactly-zero
-// work: one GPU, d <= 3; RLD_SORT=0 keeps the given order.
+// work: d <= 3; RLD_SORT=0 keeps the given order.
 bool sort_points(const rld_handle* h, const rld_problem* p) {
   const char* e = getenv("RLD_SORT");
   if (e && e[0] == '0') return false;
@@ -242,8 +242,8 @@ bool sort_points(const rld_handle* h, const rld_problem* p) {
   const bool slices = p->path == RLD_PATH_STORED &&
                       (p->dtype == RLD_FP64 ? fp64_product_ozaki() : fp32_product_slices());
   const bool otf = p->path == RLD_PATH_ON_THE_FLY && p->dtype == RLD_FP32 && kv_otf_f16_enabled();
-  return p->source == RLD_SOURCE_POINTS && (slices || otf) && h->world == 1 && p->d >= 1 && p->d <= 3 &&
-         p->n < (int64_t)1 << 31;
+  // (every rank sorts all n points the same way; its rows are a block of the sorted order)
+  return p->source == RLD_SOURCE_POINTS && (slices || otf) && p->d >= 1 && p->d <= 3 && p->n < (int64_t)1 << 31;
 }
 
 // plain: the points as given (no Morton order, no slice image): rld_build_covariance's upload
@@ -316,8 +316,8 @@ void prepare(rld_handle* h, const rld_problem* p, bool plain = false) {
       // coordinates pre-scaled so the tile generator's r^2 is the kernel argument
       const double scale = p->family == RLD_MATERN52 ? r.kp.s5_over_l : std::sqrt(r.kp.inv_2l2 * 1.4426950408889634);
       pad_points(r.X.as<double>(), p->n, p->d, scale, r.pts4.as<float>(), st);
-      if (r.permuted && p->dtype == RLD_FP32 && fp32_product_slices() && r.rows > 0) {
-        // float32 K from Morton-ordered points (d <= 3, one GPU) as a SPARSE image of 3 int8 slices:
+      if (r.permuted && p->dtype == RLD_FP32 && fp32_product_slices()) {   // (collective: ranks without rows too)
+        // float32 K from Morton-ordered points (d <= 3) as a SPARSE image of 3 int8 slices:
         // the float64 kernel value rounded to 24 bits of its row scale (float32-grade next to the
         // diagonal; far-field entries below 2^-25 of the scale are exactly zero), only the slices a
         // bound from the point boxes allows to be nonzero are evaluated and stored, and the product
@@ -326,10 +326,10 @@ void prepare(rld_handle* h, const rld_problem* p, bool plain = false) {
         // when the image leaves a quarter of HBM free (config 4: clustered points, most blocks
         // empty), and is then served from HBM instead of regenerating K for every product.
         const int64_t nb = ceil_div(r.rows, 128) * ceil_div(p->n, 32);
-        r.knz.reserve(sizeof(int) * nb);
-        r.koff.reserve(sizeof(uint32_t) * nb);
+        r.knz.reserve(sizeof(int) * std::max<int64_t>(nb, 1));
+        r.koff.reserve(sizeof(uint32_t) * std::max<int64_t>(nb, 1));
         const int64_t kept = ozaki_sparse_plan(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.knz.as<int>(),
-                                               r.koff.as<uint32_t>(), h->wk.scratch2, st);
+                                               r.koff.as<uint32_t>(), h->wk.scratch2, st);   // 0 without rows
         const int64_t bytes = std::max<int64_t>(kept, 1) * 4096;
         bool take = r.path == RLD_PATH_STORED;
         const char* ce = getenv("RLD_OTF_CACHE");   // 0: always regenerate K on the fly (read per prepare)
@@ -342,23 +342,34 @@ void prepare(rld_handle* h, const rld_problem* p, bool plain = false) {
           (void)tot;
           take = kept < ((int64_t)1 << 32) && bytes + need <= (int64_t)fr + (int64_t)r.Kq.bytes;
         }
+        if (h->world > 1 && r.path == RLD_PATH_ON_THE_FLY) {   // all ranks serve from the image, or none
+          int no = take ? 0 : 1;
+          allreduce_flags(h, &no, 1);
+          take = no == 0;
+        }
         if (take) {
           r.Kq.reserve((size_t)bytes);
-          r.ksigma.reserve(sizeof(double) * r.rows);
+          r.ksigma.reserve(sizeof(double) * std::max<int64_t>(r.rows, 1));
           ozaki_slice_points(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.Kq.as<int8_t>(), r.ksigma.as<double>(),
                              st, nullptr, r.knz.as<int>(), 3, r.koff.as<uint32_t>());
           r.kslices = 3;
-          r.kq_ready = r.knz_ready = r.koff_ready = true;
+          r.kq_ready = r.knz_ready = r.koff_ready = r.rows > 0;
           r.cached = r.path == RLD_PATH_ON_THE_FLY;
         }
       }
-      if (!r.kq_ready && r.permuted && r.path == RLD_PATH_ON_THE_FLY && p->dtype == RLD_FP32 && r.rows > 0) {
-        r.otf_skip.reserve(sizeof(uint32_t) * otf_skip_words(r.rows, p->n));
-        otf_skip_map(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.otf_skip.as<uint32_t>(), h->wk.scratch2, st);
-        // the order pays only where it skips enough: its per-k-step flushes (kv_otf.cu) cost ~13 %
-        // (config 4's clustered points skip ~nothing; config 5 skips most k-steps)
-        if (otf_skip_fraction(r.otf_skip.as<uint32_t>(), r.rows, p->n, h->wk.scratch2, st) >= 0.3) {
-          r.otf_skip_ready = true;
+      if (!r.cached && !(r.kq_ready && r.path == RLD_PATH_STORED) && r.permuted && r.path == RLD_PATH_ON_THE_FLY &&
+          p->dtype == RLD_FP32) {
+        int thin = 0;
+        if (r.rows > 0) {
+          r.otf_skip.reserve(sizeof(uint32_t) * otf_skip_words(r.rows, p->n));
+          otf_skip_map(r.X.as<double>(), p->n, r.kp, r.row0, r.rows, r.otf_skip.as<uint32_t>(), h->wk.scratch2, st);
+          // the order pays only where it skips enough: its per-k-step flushes (kv_otf.cu) cost ~13 %
+          // (config 4's clustered points skip ~nothing; config 5 skips most k-steps)
+          thin = otf_skip_fraction(r.otf_skip.as<uint32_t>(), r.rows, p->n, h->wk.scratch2, st) >= 0.3 ? 0 : 1;
+        }
+        if (h->world > 1) allreduce_flags(h, &thin, 1);   // one order for all ranks
+        if (!thin) {
+          r.otf_skip_ready = r.rows > 0;
         } else {   // back to the caller's order
           std::vector<double> hx((size_t)p->n * p->d), hy((size_t)p->n * p->d);
           std::vector<int> pm((size_t)p->n);
@@ -982,9 +993,10 @@ void global_argmax(rld_handle* h, const double* d, double* pv) {
   }
   wk.gsend.reserve(sizeof(double) * 2);
   wk.grecv.reserve(sizeof(double) * 2 * h->world);
-  argmax_first(r.rows, d, r.row0, wk.gsend.as<double>(), wk.scratch, h->st);
+  const int* perm = r.permuted ? r.perm.as<int>() : nullptr;   // ties: the smallest ORIGINAL index
+  argmax_first(r.rows, d, r.row0, wk.gsend.as<double>(), wk.scratch, h->st, perm ? perm + r.row0 : nullptr);
   h->comm->allgather(wk.gsend.as<double>(), wk.grecv.as<double>(), 2, h->st);
-  pick_first_max(h->world, wk.grecv.as<double>(), pv, h->st);   // ranks hold increasing row ranges
+  pick_first_max(h->world, wk.grecv.as<double>(), pv, h->st, perm);   // ranks hold increasing row ranges
 }
 
 // Rank-k pivoted partial Cholesky with greedy largest-diagonal pivoting (src/precond.py:215-228):
@@ -1338,9 +1350,27 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
   nvtxRangePushA("rld:probes + Lanczos");
   wk.probes.reserve(sizeof(double) * s * nl);
   double* Zp = wk.probes.as<double>();
-  if (in->probes) {
+  // sharded with the points in Morton order: a rank's rows are scattered through the caller's order,
+  // so the probes are generated (or loaded) at full length and this rank's rows gathered from them
+  const bool gather_local = h->world > 1 && r.permuted;
+  double* Zfull = nullptr;
+  if (gather_local) {
+    wk.ptmp2.reserve(sizeof(double) * s * n);
+    Zfull = wk.ptmp2.as<double>();
+  }
+  auto local_rows = [&](int64_t m, const double* full, double* out) {
+    permute_rows(m, nl, r.perm.as<int>() + r.row0, full, n, out, nl, false, st);
+  };
+  if (in->probes && gather_local) {
+    RLD_CUDA(cudaMemcpyAsync(Zfull, in->probes, sizeof(double) * s * n,
+                             in->memory == RLD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    local_rows(s, Zfull, Zp);
+  } else if (in->probes) {
     load_rows(h, in->probes, in->memory, s, Zp);
     to_resident_order(h, s, Zp, nl);
+  } else if (c->probe_kind == RLD_RADEMACHER && gather_local) {
+    rademacher_rows(c->probe_key, s, n, 0, n, n, Zfull, st);
+    local_rows(s, Zfull, Zp);
   } else if (c->probe_kind == RLD_RADEMACHER) {
     rademacher_rows(c->probe_key, s, n, r.row0, nl, nl, Zp, st);
     to_resident_order(h, s, Zp, nl);
@@ -1356,8 +1386,13 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
       const int64_t sb = std::min<int64_t>(s - done, n);
       double* blk = Zp + done * nl;
       const uint64_t* key = c->probe_block_keys + 2 * b;
-      normal_rows(key, sb, n, r.row0, nl, nl, blk, wk.rng_scratch, wk.ints.as<int>() + 5, st, wk.endw.as<int64_t>());
-      to_resident_order(h, sb, blk, nl);
+      if (gather_local) {
+        normal_rows(key, sb, n, 0, n, n, Zfull, wk.rng_scratch, wk.ints.as<int>() + 5, st, wk.endw.as<int64_t>());
+        local_rows(sb, Zfull, blk);
+      } else {
+        normal_rows(key, sb, n, r.row0, nl, nl, blk, wk.rng_scratch, wk.ints.as<int>() + 5, st, wk.endw.as<int64_t>());
+        to_resident_order(h, sb, blk, nl);
+      }
       cholqr2(h, nl, (int)sb, blk, wk.ints.as<int>(), 2);
       int64_t ew = 0;
       RLD_CUDA(cudaMemcpyAsync(&ew, wk.endw.ptr, sizeof ew, cudaMemcpyDeviceToHost, st));
@@ -1369,6 +1404,9 @@ void run_estimate(rld_handle* h, const rld_config* c, const rld_inputs* in, rld_
       RLD_CUDA(cudaStreamSynchronize(st));   // rad goes out of scope
       done += sb;
     }
+  } else if (gather_local) {
+    normal_rows(c->probe_key, s, n, 0, n, n, Zfull, wk.rng_scratch, wk.ints.as<int>() + 5, st);
+    local_rows(s, Zfull, Zp);
   } else {  // numpy-exact Gaussian probes on the device (src/probes.py:33-34)
     normal_rows(c->probe_key, s, n, r.row0, nl, nl, Zp, wk.rng_scratch, wk.ints.as<int>() + 5, st);
     to_resident_order(h, s, Zp, nl);
@@ -1762,7 +1800,20 @@ int rld_kv_apply(rld_handle* h, int64_t m, const double* V, double* Y) {
     if (!h->res.ready) fail(RLD_ERR_INVALID_ARGUMENT, "no resident problem");
     if (m < 1 || !V || !Y) fail(RLD_ERR_INVALID_ARGUMENT, "bad kv_apply arguments");
     Resident& r = h->res;
-    if (r.permuted) {   // operands in the caller's order, K in the resident (Morton) order
+    if (r.permuted && h->world > 1) {
+      // sharded: the product's rows come out in the resident order; gather them, undo the order and
+      // hand back this rank's rows [row0, row0 + rows) of the caller's order
+      h->wk.ptmp.reserve(sizeof(double) * m * r.n);
+      h->wk.ptmp2.reserve(sizeof(double) * m * r.n);
+      permute_rows(m, r.n, r.perm.as<int>(), V, r.n, h->wk.ptmp.as<double>(), r.n, false, h->st);
+      h->wk.KX.reserve(sizeof(double) * m * std::max<int64_t>(r.rows, 1));
+      kv(h, m, h->wk.ptmp.as<double>(), h->wk.KX.as<double>());
+      gather_rows(h, h->wk.KX.as<double>(), m, h->wk.ptmp2.as<double>());
+      permute_rows(m, r.n, r.perm.as<int>(), h->wk.ptmp2.as<double>(), r.n, h->wk.ptmp.as<double>(), r.n, true, h->st);
+      if (r.rows > 0)
+        RLD_CUDA(cudaMemcpy2DAsync(Y, sizeof(double) * r.rows, h->wk.ptmp.as<double>() + r.row0, sizeof(double) * r.n,
+                                   sizeof(double) * r.rows, m, cudaMemcpyDeviceToDevice, h->st));
+    } else if (r.permuted) {   // operands in the caller's order, K in the resident (Morton) order
       h->wk.ptmp.reserve(sizeof(double) * m * r.n);
       h->wk.ptmp2.reserve(sizeof(double) * m * r.n);
       permute_rows(m, r.n, r.perm.as<int>(), V, r.n, h->wk.ptmp.as<double>(), r.n, false, h->st);

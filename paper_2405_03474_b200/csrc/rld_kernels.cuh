@@ -101,7 +101,8 @@ void morton_order_device(const double* X, int64_t n, int d, int* perm, double* X
 void permute_rows(int64_t m, int64_t n, const int* perm, const double* src, int64_t lds, double* dst, int64_t ldd,
                   bool scatter, cudaStream_t st);
 // out = the (value, index) pair with the largest value, first on ties, of P pairs ordered by index
-void pick_first_max(int P, const double* pairs, double* out, cudaStream_t st);
+// perm != null: equal values go to the pair whose (global resident) index has the smallest perm[]
+void pick_first_max(int P, const double* pairs, double* out, cudaStream_t st, const int* perm = nullptr);
 void kernel_column(int64_t rows, int64_t row0, int64_t n, int64_t p, const void* K, int64_t ldk, int kdtype,
                    bool tiled, const double* X, const KernelParams& kp, double* out, cudaStream_t st);
 void pchol_update(int64_t rows, const double* col, const double* dp, double* Cj, double* d, cudaStream_t st);

@@ -966,8 +966,8 @@ void argmax_first(int64_t n, const double* d, int64_t offset, double* out, DevBu
   argmax_final_kernel<<<1, 1, 0, st>>>(P, scratch.as<double>(), offset, out, perm);
   RLD_LAUNCH_CHECK();
 }
-void pick_first_max(int P, const double* pairs, double* out, cudaStream_t st) {
-  argmax_final_kernel<<<1, 1, 0, st>>>(P, pairs, 0, out, nullptr);
+void pick_first_max(int P, const double* pairs, double* out, cudaStream_t st, const int* perm) {
+  argmax_final_kernel<<<1, 1, 0, st>>>(P, pairs, 0, out, perm);
   RLD_LAUNCH_CHECK();
 }
 void kernel_column(int64_t rows, int64_t row0, int64_t n, int64_t p, const void* K, int64_t ldk, int kdtype,

@@ -60,6 +60,11 @@ def test_config1_sharded_matches_single_and_reference(rld, golden_cases, G, alg)
 @pytest.mark.parametrize("G,dtype,path,idx,n", [
     (2, "fp32", "stored", 2, 4096), (3, "fp32", "on_the_fly", 4, 4096), (2, "fp64", "on_the_fly", 3, 4096),
     (4, "fp64", "stored", 5, 4097),
+    # points in Morton order on every rank (d <= 3): float64 slices with skipped leading slices and
+    # Gaussian probes gathered from full-length streams, the sparse float32 slice image (stored and
+    # serving an on-the-fly problem), ragged last shards
+    (2, "fp64", "stored", 3, 4096), (3, "fp32", "stored", 3, 4099), (2, "fp32", "on_the_fly", 5, 4096),
+    (3, "fp64", "stored", 4, 3000),
 ])
 def test_reduced_configs_sharded(rld, golden_cases, G, dtype, path, idx, n):
     """fp32 / fp64, stored / on the fly, odd n with a ragged last shard."""
@@ -157,23 +162,48 @@ def test_ill_conditioned_sketch_takes_tsqr(rld):
     assert rel(res[0].value, one.value) <= 1e-12
 
 
-def test_resident_sharded_kv_apply(rld):
-    """Each rank's K.V holds its own rows of the single-GPU product."""
+@pytest.mark.parametrize("idx,dtype", [(2, "fp64"), (3, "fp64"), (3, "fp32")])
+def test_resident_sharded_kv_apply(rld, idx, dtype):
+    """Each rank's K.V holds its own rows (of the caller's order) of the single-GPU product; config 3's
+    d = 2 points sit in Morton order on every rank (gather, undo the order, own rows back)."""
     import torch
 
     from paper_2405_03474_b200.parallel import VirtualShards, shard_bounds
     from paper_2405_03474_b200.workloads import baseline
 
-    wl = baseline(2, n=3001)
+    wl = baseline(idx, n=3001)
     M = rld.KernelMatrix(wl.spec, wl.points)
-    one = rld.ResidentMatrix(M, dtype="fp64", path="stored")
+    one = rld.ResidentMatrix(M, dtype=dtype, path="stored")
     V = torch.randn(7, wl.n, dtype=torch.float64, device="cuda")
     Y = one.kv_apply(V)
     G = 3
+    import ctypes as C
+
+    def body(session):
+        R = rld.ResidentMatrix(M, dtype=dtype, path="stored", session=session)
+        st = (C.c_int64 * 4)()
+        assert session.lib.rld_slice_stats(session.handle.ptr, st) == 0
+        return R.kv_apply(V), tuple(st)
+
     with VirtualShards(G) as vs:
-        parts = vs.run(lambda session: rld.ResidentMatrix(M, dtype="fp64", path="stored", session=session)
-                       .kv_apply(V))
-    for r, Yr in enumerate(parts):
+        parts = vs.run(body)
+    for r, (Yr, st) in enumerate(parts):
+        if idx == 3:   # Morton order is live on every rank: leading all-zero slices are skipped
+            assert st[0] > 0 and st[1] < (7 if dtype == "fp64" else 3) * st[0], st
         r0, r1 = shard_bounds(wl.n, G, r)
-        # the k-split of the DMMA product depends on the rows per shard: rounding-level differences
+        # the k-split of the product depends on the rows per shard: rounding-level differences (the
+        # integer slice products are exact: only the float64 split reduce can differ)
         assert torch.allclose(Yr, Y[:, r0:r1], rtol=0, atol=1e-13 * float(Y.abs().max()))
+
+
+def test_normal_orthogonal_probes_sharded_morton(rld):
+    """Normal-orthogonal probe blocks (Gaussian rows, CholQR, chi radii) with the points in Morton
+    order on every rank: G = 2 against G = 1."""
+    from paper_2405_03474_b200.workloads import baseline
+
+    wl = baseline(1, n=1500, rank=32, num_probes=12)
+    cfg = replace(wl.config, probe_kind="normal-orthogonal", dtype="fp64")
+    M = rld.KernelMatrix(wl.spec, wl.points)
+    one = rld.rstar_logdet(M, cfg)
+    res = sharded(rld, 2, lambda: rld.rstar_logdet(M, cfg))
+    assert rel(res[0].value, one.value) <= 1e-11, (res[0].value, one.value)
