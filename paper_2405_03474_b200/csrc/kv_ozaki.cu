@@ -790,6 +790,24 @@ void launch_product(const int8_t* Kq, const double* ksigma, int64_t rows, int64_
                     const uint32_t* koff) {
   using C = OzCfg<SA, SB, BN>;
   if (diags < 1 || diags > SB) fail(RLD_ERR_INVALID_ARGUMENT, "kv_product_ozaki: diagonals out of range");
+  const int64_t KS = ceil_div(n, OZ_BK);
+  const int64_t passes = ceil_div(m, BN), tiles = ceil_div(rows, OZ_BM);
+  {
+    // the float64 partials of the k splits (>= n / KMAX of them) take splits x m x rows x 8 bytes:
+    // beyond 20 GB (wide products at n >= 2^19) the vectors go through in groups of whole passes
+    const int64_t s0 = ceil_div(n, C::KMAX);
+    const int64_t per_pass = s0 > 1 ? s0 * BN * rows * (int64_t)sizeof(double) : 0;
+    const char* ce = getenv("RLD_OZ_PARTIAL_MB");   // (tests: a small cap exercises the grouping)
+    const int64_t cap = ce ? (int64_t)atol(ce) << 20 : (int64_t)20 << 30;
+    const int64_t fit = per_pass > 0 ? std::max<int64_t>(1, cap / per_pass) : passes;
+    if (passes > fit) {
+      for (int64_t p0 = 0; p0 < passes; p0 += fit) {
+        const int64_t c0 = p0 * BN, mc = std::min<int64_t>(m - c0, fit * BN);
+        launch_product<SA, SB, BN>(Kq, ksigma, rows, n, V + c0 * ldv, ldv, mc, Y + c0 * ldy, ldy, ws, st, diags, knz, koff);
+      }
+      return;
+    }
+  }
   ws.oz_vq.reserve((size_t)ozaki_bytes(m, n, BN, SB));
   ws.oz_tau.reserve(sizeof(double) * m);
   ozaki_slice(V, ldv, m, n, BN, ws.oz_vq.as<int8_t>(), ws.oz_tau.as<double>(), st, SB);
@@ -797,14 +815,14 @@ void launch_product(const int8_t* Kq, const double* ksigma, int64_t rows, int64_
   once_per_device(attr, [&] {
     RLD_CUDA(cudaFuncSetAttribute(ozaki_kv_kernel<SA, SB, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   });
-  const int64_t KS = ceil_div(n, OZ_BK);
-  const int64_t passes = ceil_div(m, BN), tiles = ceil_div(rows, OZ_BM);
   const int64_t units0 = passes * tiles;
   const int64_t slots = oz_sms();
   // k splits: every CTA <= OZ_KMAX columns (exact int32), >= 64 k-steps; the fewest splits whose
   // CTA count fills >= 95 % of whole waves
   const int64_t min_s = ceil_div(n, C::KMAX);
-  const int64_t max_s = std::max<int64_t>(min_s, n / (OZ_BK * 64));
+  // (more splits than the range needs only while their partials stay under 8 GB)
+  const int64_t mem_s = std::max<int64_t>(min_s, ((int64_t)8 << 30) / std::max<int64_t>(1, m * rows * (int64_t)sizeof(double)));
+  const int64_t max_s = std::min(mem_s, std::max<int64_t>(min_s, n / (OZ_BK * 64)));
   int64_t splits = min_s;
   double best = 0.0;
   for (int64_t s = min_s; s <= std::min<int64_t>(max_s, min_s + 64); ++s) {

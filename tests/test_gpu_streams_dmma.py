@@ -242,6 +242,25 @@ def test_on_the_fly_fp32_served_from_cached_slices(rld, index, n, monkeypatch):
     assert rel(a.value, c.value) <= 1e-5, (a.value, c.value)
 
 
+@pytest.mark.parametrize("dtype,index,n,m", [("fp64", 2, 40000, 300), ("fp32", 3, 70000, 300)])
+def test_slice_product_in_pass_groups(rld, dtype, index, n, m, monkeypatch):
+    """The k splits' float64 partials take splits x m x rows x 8 bytes; past a cap (20 GB: wide products
+    at n >= 2^19) the vectors go through in groups of whole column passes.  A 1 MB cap forces one pass
+    per launch here: same product (the integer sums are exact; the float64 split reduce is the same)."""
+    import torch
+
+    from paper_2405_03474_b200.workloads import baseline
+
+    monkeypatch.setenv("RLD_FP64_SKETCH", "slices")   # (no CRT for the wide float64 product)
+    wl = baseline(index, n=n)
+    R = rld.ResidentMatrix(rld.KernelMatrix(wl.spec, wl.points), dtype=dtype, path="stored")
+    V = torch.from_numpy(np.random.default_rng(0).standard_normal((m, n))).cuda()
+    Y = R.kv_apply(V)
+    monkeypatch.setenv("RLD_OZ_PARTIAL_MB", "1")
+    Y1 = R.kv_apply(V)
+    assert float((Y - Y1).abs().max()) <= 1e-13 * float(Y.abs().max())
+
+
 def test_int8_slices_from_points_equal_slices_from_K(rld, monkeypatch):
     """Stored float64 from the points slices K straight from the points (no float64 K in HBM); from
     a dense device K built by build_covariance it slices the stored rows: same entries, same row
