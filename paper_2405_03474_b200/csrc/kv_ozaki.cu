@@ -138,21 +138,43 @@ __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint
 // x = sum_s d_s 2^{-8(s+1)} + rho 2^-56, |rho| <= 1/2.  Integer work on the ALU pipe (one F2I per
 // entry).  Also returns K' = sum_{s<6} d_s 256^{5-s} (the CRT integer, kv_crt.cu) and 7 - the number
 // of leading zero digits.
+// 32-bit arithmetic: the 64-bit integer is never formed for the digits.  hi = rint(x 2^24) and
+// lo = rint((x 2^24 - hi) 2^32) (the difference is exact in float64) give the same integer
+// hi 2^32 + lo = rint(x 2^56); the low three digits come from lo, the other four from
+// hi 256 + (what is left of lo) -- about half the ALU work of the 64-bit shifts and masks it replaces
+// (the slicing of K from the points is bound by this integer work, not by its float64 exp).
+template <int NB>
+__device__ __forceinline__ void low_digits(int& v, int* d_top_down_end) {   // NB digits from the bottom of v
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    const int dd = ((v + 128) & 255) - 128;
+    *(d_top_down_end - i) = dd;
+    v = (v - dd) >> 8;   // exact (arithmetic shift)
+  }
+}
 template <int S>
 __device__ __forceinline__ void digits8(double x, int (&d)[S], long long& kprime, int& nz) {
-  long long k = __double2ll_rn(x * (double)(1ull << (OZ_DBITS * S)));   // x 2^56 (S = 7)
-  nz = 0;
+  nz = 0;        // (the callers that need it derive it from the packed slices)
   kprime = 0;
-#pragma unroll
-  for (int s = S - 1; s >= 1; --s) {
-    const int dd = (int)((k + 128) & 255) - 128;
-    d[s] = dd;
-    k = (k - dd) >> OZ_DBITS;   // exact
-    if (s == S - 1) kprime = k;
-    if (dd != 0) nz = S - s;
+  if constexpr (S <= 4) {   // |x 2^(8 S)| <= 63/128 2^32 < 2^31
+    int v = __double2int_rn(x * (double)(1ull << (OZ_DBITS * S)));
+    low_digits<S - 1>(v, &d[S - 1]);
+    d[0] = v;
+  } else {
+    static_assert(S == 7, "7 digits: 3 + 4 bytes");
+    const int hi = __double2int_rn(x * 16777216.0);                       // rint(x 2^24), |hi| < 2^23
+    const double r = fma(x, 16777216.0, -(double)hi);                     // exact, |r| <= 1/2
+    const long long lo = __double2ll_rn(r * 4294967296.0);                // |lo| <= 2^31
+    const int d6 = (((int)lo + 128) & 255) - 128;
+    const long long l1 = (lo - d6) >> 8;                                  // |l1| <= 2^23
+    int v = (int)l1;
+    d[6] = d6;
+    low_digits<2>(v, &d[5]);                                              // d5, d4; |v| <= 128 left
+    kprime = ((long long)hi << 24) + l1;                                  // (K - d6) / 256: the CRT integer
+    int u = hi * 256 + v;                                                 // |u| < 2^31
+    low_digits<3>(u, &d[3]);                                              // d3, d2, d1
+    d[0] = u;
   }
-  d[0] = (int)k;
-  if (k != 0) nz = S;
 }
 
 // Exponent e of the scale sigma = 2^(e+1) for a row (vector) of maximum mx = f 2^e', f in [0.5, 1):
@@ -314,7 +336,6 @@ ozaki_points_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, in
       long long kp;
       int nzk;
       digits8<S>(v * scl, dg, kp, nzk);
-      if (nzk > nz) nz = nzk;
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         const uint32_t b = (uint32_t)(uint8_t)(int8_t)dg[s];
@@ -322,6 +343,14 @@ ozaki_points_kernel(const double* __restrict__ X, int64_t n, KernelParams kp, in
         else w[s][k >> 2] |= b << (8 * (k & 3));
       }
       if (CRT) kq[k] = kp;
+    }
+    // slices from the first one with a nonzero digit in any of this thread's EL entries
+#pragma unroll
+    for (int sl = S - 1; sl >= 0; --sl) {
+      uint32_t any = 0;
+#pragma unroll
+      for (int q4 = 0; q4 < W; ++q4) any |= w[sl][q4];
+      if (any) nz = S - sl;
     }
     // a warp holds 8 rows x 4 column parts of one (tile, k-step) block: reduce, one atomic per warp
     if (knz && !koff) {
