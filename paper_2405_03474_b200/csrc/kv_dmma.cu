@@ -222,7 +222,7 @@ struct ExShape {
 template <int BQ>
 __global__ void __launch_bounds__(DM_THREADS, 2)
 gemm_expand_dmma_kernel(const __grid_constant__ CUtensorMap mapS, const __grid_constant__ CUtensorMap mapX, int64_t p,
-                        int64_t q, int64_t N, double* __restrict__ C, int64_t ldc, double alpha, double beta) {
+                        int64_t q, int64_t N, double* __restrict__ C, int64_t ldc, double alpha, double beta, int tri) {
   using S = ExShape<BQ>;
   extern __shared__ __align__(1024) unsigned char ex_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -232,7 +232,9 @@ gemm_expand_dmma_kernel(const __grid_constant__ CUtensorMap mapS, const __grid_c
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t j0 = (int64_t)blockIdx.x * EX_BN;
   const int64_t b0 = (int64_t)blockIdx.y * BQ;
-  const int steps = (int)ceil_div(p, DM_BK);
+  // tri: S is upper triangular (S[k][b] = 0 for k > b, the R^-1 of CholQR): this tile of output rows
+  // b0 .. b0 + BQ - 1 only needs k < b0 + BQ
+  const int steps = (int)ceil_div(tri ? min64(p, b0 + BQ) : p, DM_BK);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < DM_STAGES; ++s) {
@@ -430,7 +432,7 @@ CUtensorMap map_f64_b8(const double* base, int64_t cols, int64_t rows, int64_t l
 
 template <int BQ>
 void launch_expand(const double* Sm, int64_t lds, int64_t p, int64_t q, const double* X, int64_t ldx, int64_t N,
-                   double* C, int64_t ldc, double alpha, double beta, cudaStream_t st) {
+                   double* C, int64_t ldc, double alpha, double beta, cudaStream_t st, bool tri) {
   using S = ExShape<BQ>;
   static std::atomic<uint64_t> attr{0};
   once_per_device(attr, [&] {
@@ -440,7 +442,7 @@ void launch_expand(const double* Sm, int64_t lds, int64_t p, int64_t q, const do
   const CUtensorMap mx = map_f64_b8(X, N, p, ldx, DM_BK);   // X: p rows of N
   dim3 grid((unsigned)ceil_div(N, EX_BN), (unsigned)ceil_div(q, BQ), 1);
   if (grid.y > 65535u) fail(RLD_ERR_NOT_SUPPORTED, "gemm_expand_f64: q too large");
-  gemm_expand_dmma_kernel<BQ><<<grid, DM_THREADS, S::SMEM, st>>>(ms, mx, p, q, N, C, ldc, alpha, beta);
+  gemm_expand_dmma_kernel<BQ><<<grid, DM_THREADS, S::SMEM, st>>>(ms, mx, p, q, N, C, ldc, alpha, beta, tri ? 1 : 0);
   RLD_LAUNCH_CHECK();
 }
 
@@ -485,7 +487,7 @@ void gemm_nt_f64(const double* A, int64_t lda, int64_t p, const double* B, int64
 // C (q x N, ld ldc, rows layout) = beta C + alpha S^T X; S: p x q column-major (ld lds), X: p x N
 // rows layout (ld ldx).  S and X rows 16-byte aligned (gemm_nt_f64_ok(S, lds, X, ldx)).
 void gemm_expand_f64(const double* Sm, int64_t lds, int64_t p, int64_t q, const double* X, int64_t ldx, int64_t N,
-                     double* C, int64_t ldc, double alpha, double beta, cudaStream_t st) {
+                     double* C, int64_t ldc, double alpha, double beta, cudaStream_t st, bool tri_upper) {
   if (q <= 0 || N <= 0) return;
   if (p <= 0) {
     if (beta != 1.0) fail(RLD_ERR_NOT_SUPPORTED, "gemm_expand_f64 with p = 0 needs beta = 1");
@@ -493,9 +495,9 @@ void gemm_expand_f64(const double* Sm, int64_t lds, int64_t p, int64_t q, const 
   }
   if (!gemm_nt_f64_ok(Sm, lds, X, ldx)) fail(RLD_ERR_NOT_SUPPORTED, "gemm_expand_f64 needs 16-byte aligned rows");
   if (q <= 32)
-    launch_expand<32>(Sm, lds, p, q, X, ldx, N, C, ldc, alpha, beta, st);
+    launch_expand<32>(Sm, lds, p, q, X, ldx, N, C, ldc, alpha, beta, st, tri_upper);
   else
-    launch_expand<64>(Sm, lds, p, q, X, ldx, N, C, ldc, alpha, beta, st);
+    launch_expand<64>(Sm, lds, p, q, X, ldx, N, C, ldc, alpha, beta, st, tri_upper);
 }
 
 }  // namespace rld

@@ -610,9 +610,9 @@ void nt_f64(rld_handle* h, const double* A, int64_t lda, int64_t p, const double
 // ex_f64: C (q x N rows layout, ld ldc) = beta C + alpha S^T X for S: p x q column-major, X: p x N
 // rows layout; in column-major terms C = X S.  Basis changes and low-rank expansions.
 void ex_f64(rld_handle* h, const double* S, int64_t lds, int64_t p, int64_t q, const double* X, int64_t ldx, int64_t N,
-            double* C, int64_t ldc, double alpha = 1.0, double beta = 0.0) {
+            double* C, int64_t ldc, double alpha = 1.0, double beta = 0.0, bool tri_upper = false) {
   if (gemm_nt_f64_ok(S, lds, X, ldx)) {
-    gemm_expand_f64(S, lds, p, q, X, ldx, N, C, ldc, alpha, beta, h->st);
+    gemm_expand_f64(S, lds, p, q, X, ldx, N, C, ldc, alpha, beta, h->st, tri_upper);
     return;
   }
   RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)N, (int)q, (int)p, &alpha, X, (int)ldx, S, (int)lds,
@@ -719,7 +719,7 @@ void cholqr2(rld_handle* h, int64_t n, int w, double* Y, int* flags, int passes 
     if (have_rinv && n > 0) {   // Y <- Y R^-1 through a scratch copy (the expand kernel is out of place)
       wk.scratch2.reserve(sizeof(double) * n * w);
       copy_doubles(n * (int64_t)w, Y, wk.scratch2.as<double>(), h->st);
-      ex_f64(h, Ri, w, w, w, wk.scratch2.as<double>(), n, n, Y, n);
+      ex_f64(h, Ri, w, w, w, wk.scratch2.as<double>(), n, n, Y, n, 1.0, 0.0, true);   // (R^-1 upper triangular)
     } else {
       RLD_CUBLAS(cublasDtrsm(h->cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
                              (int)n, w, &ONE, G, w, Y, (int)n));
@@ -754,7 +754,7 @@ void cholqr_gemm(rld_handle* h, int64_t n, int w, double* src, double* dst, int*
       RLD_CUBLAS(cublasDtrsm(h->cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, w,
                              w, &ONE, G, w, Ri, w));
     }
-    ex_f64(h, Ri, w, w, w, cur, n, n, out, n);   // out = cur R^-1
+    ex_f64(h, Ri, w, w, w, cur, n, n, out, n, 1.0, 0.0, true);   // out = cur R^-1 (upper triangular: half the k loop)
     cur = out;
   }
   if (cur != dst) copy_doubles(n * (int64_t)w, cur, dst, h->st);

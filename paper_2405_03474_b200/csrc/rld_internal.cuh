@@ -171,7 +171,8 @@ void gemm_nt_f64(const double* A, int64_t lda, int64_t p, const double* B, int64
 // C (q x N, rows layout) = beta C + alpha S^T X for S: p x q column-major (small), X: p x N rows
 // layout (the expansions U T, Q R^-1, Q^T V of the preconditioner and its Woodbury apply).
 void gemm_expand_f64(const double* S, int64_t lds, int64_t p, int64_t q, const double* X, int64_t ldx, int64_t N,
-                     double* C, int64_t ldc, double alpha, double beta, cudaStream_t st);
+                     double* C, int64_t ldc, double alpha, double beta, cudaStream_t st, bool tri_upper = false);
+// tri_upper: S is upper triangular (S[k][b] = 0 for k > b): the k loop of an output tile stops at its last row
 
 // Float64-accurate products on the INT8 tensor cores (kv_ozaki.cu): exact 7 x 8-bit slicing
 // (`slices` = 7; a float32 K from Morton-ordered points is held as 3 slices and multiplied with 4 of V).
