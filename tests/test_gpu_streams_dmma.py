@@ -261,6 +261,31 @@ def test_slice_product_in_pass_groups(rld, dtype, index, n, m, monkeypatch):
     assert float((Y - Y1).abs().max()) <= 1e-13 * float(Y.abs().max())
 
 
+@pytest.mark.parametrize("n", [1, 2, 5, 31, 33, 129, 257])
+def test_slice_paths_tiny_and_ragged_n(rld, n):
+    """d <= 3 points at tiny and ragged n through every path that may hold K as slices (float64 7-slice
+    image; float32 sparse 3-slice image, stored and serving an on-the-fly problem): products against
+    numpy, and a float32 estimate runs."""
+    import torch
+
+    g = np.random.default_rng(n)
+    for d in (1, 2, 3):
+        pts = g.uniform(0, 1, (n, d))
+        spec = rld.KernelSpec("matern52", 1.0, 0.3, 1e-2)
+        K = O.covariance_block("matern52", 1.0, 0.3, 1e-2, pts)
+        V = g.standard_normal((3, n))
+        ref = V @ K.T
+        for dtype in ("fp32", "fp64"):
+            for path in ("stored", "on_the_fly"):
+                R = rld.ResidentMatrix(rld.KernelMatrix(spec, pts), dtype=dtype, path=path)
+                Y = R.kv_apply(torch.from_numpy(V).cuda()).cpu().numpy()
+                err = np.max(np.abs(Y - ref)) / max(np.max(np.abs(ref)), 1e-300)
+                assert err <= (1e-5 if dtype == "fp32" else 1e-12), (d, dtype, path, err)
+        cfg = rld.EstimatorConfig("r3", min(4, n), 20, "rademacher",
+                                  rld.PreconditionerConfig("rand-svd", min(8, n), 2, 1e-12), 1, dtype="fp32")
+        assert np.isfinite(rld.rstar_logdet(rld.KernelMatrix(spec, pts), cfg).value)
+
+
 def test_int8_slices_from_points_equal_slices_from_K(rld, monkeypatch):
     """Stored float64 from the points slices K straight from the points (no float64 K in HBM); from
     a dense device K built by build_covariance it slices the stored rows: same entries, same row
