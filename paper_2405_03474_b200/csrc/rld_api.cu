@@ -720,7 +720,7 @@ void cholqr2(rld_handle* h, int64_t n, int w, double* Y, int* flags, int passes 
       wk.scratch2.reserve(sizeof(double) * n * w);
       copy_doubles(n * (int64_t)w, Y, wk.scratch2.as<double>(), h->st);
       ex_f64(h, Ri, w, w, w, wk.scratch2.as<double>(), n, n, Y, n, 1.0, 0.0, true);   // (R^-1 upper triangular)
-    } else {
+    } else if (n > 0) {   // (a rank without rows has nothing to change)
       RLD_CUBLAS(cublasDtrsm(h->cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
                              (int)n, w, &ONE, G, w, Y, (int)n));
     }
