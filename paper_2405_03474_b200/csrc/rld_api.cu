@@ -269,6 +269,8 @@ void prepare(rld_handle* h, const rld_problem* p, bool plain = false) {
   r.dtype = p->dtype;
   r.n = p->n;
   const int64_t L = ceil_div(p->n, h->world);
+  if (h->world > 1 && (int64_t)(h->world - 1) * L >= p->n)   // (every rank sees the same condition)
+    fail(RLD_ERR_NOT_SUPPORTED, "row sharding needs at least one row of K on every rank (n too small for this world size)");
   r.row0 = std::min<int64_t>(p->n, (int64_t)h->rank * L);
   r.rows = std::min<int64_t>(L, p->n - r.row0);
   cudaStream_t st = h->st;
@@ -599,10 +601,19 @@ void kv(rld_handle* h, int64_t m, const double* Vfull, double* Y, int tc_mode = 
 // terms C = A^T B.  The Grams, projections and U^T W of the preconditioner and its apply.
 void nt_f64(rld_handle* h, const double* A, int64_t lda, int64_t p, const double* B, int64_t ldb, int64_t q, int64_t n,
             double* C, int64_t ldc, double beta = 0.0) {
+  if (n <= 0) {   // a rank without rows: its partial is zero
+    if (beta == 0.0 && p > 0 && q > 0)
+      RLD_CUDA(cudaMemset2DAsync(C, sizeof(double) * ldc, 0, sizeof(double) * p, q, h->st));
+    return;
+  }
   if (gemm_nt_f64_ok(A, lda, B, ldb)) {
     gemm_nt_f64(A, lda, p, B, ldb, q, n, C, ldc, beta, h->wk.gram_scratch, h->st);
     return;
   }
+  if (lda < std::max<int64_t>(1, n) || ldb < std::max<int64_t>(1, n) || ldc < std::max<int64_t>(1, p))
+    fail(RLD_ERR_INVALID_ARGUMENT, "nt_f64: p " + std::to_string(p) + " q " + std::to_string(q) + " n " + std::to_string(n) +
+                                       " lda " + std::to_string(lda) + " ldb " + std::to_string(ldb) + " ldc " +
+                                       std::to_string(ldc));
   RLD_CUBLAS(cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, (int)p, (int)q, (int)n, &ONE, A, (int)lda, B, (int)ldb,
                          &beta, C, (int)ldc));
 }
@@ -611,6 +622,7 @@ void nt_f64(rld_handle* h, const double* A, int64_t lda, int64_t p, const double
 // rows layout; in column-major terms C = X S.  Basis changes and low-rank expansions.
 void ex_f64(rld_handle* h, const double* S, int64_t lds, int64_t p, int64_t q, const double* X, int64_t ldx, int64_t N,
             double* C, int64_t ldc, double alpha = 1.0, double beta = 0.0, bool tri_upper = false) {
+  if (N <= 0 || q <= 0) return;   // a rank without rows
   if (gemm_nt_f64_ok(S, lds, X, ldx)) {
     gemm_expand_f64(S, lds, p, q, X, ldx, N, C, ldc, alpha, beta, h->st, tri_upper);
     return;

@@ -711,6 +711,7 @@ void top_eigvecs(int w, int k, const double* V, const double* theta, double* Vto
 }
 void precond_base(int64_t n, int k, const double* diag, double floor_v, double* A, double* base, double* sqrt_base,
                   cudaStream_t st) {
+  if (n <= 0) return;   // a rank without rows
   base_kernel<<<(unsigned)ceil_div(n, 32), 256, 0, st>>>(n, k, diag, floor_v, A, base, sqrt_base);
   RLD_LAUNCH_CHECK();
 }

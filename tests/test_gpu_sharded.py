@@ -217,9 +217,7 @@ def test_small_sharded_morton(rld, n, G, dtype, path):
     """Small n and ragged shards with the points in Morton order on every rank (sparse float32 slice
     image, stored and serving an on-the-fly problem): G ranks against one.  The weak rank-8
     preconditioner makes this a float32-level comparison only; the float64 bar (1e-12) is held by
-    test_reduced_configs_sharded on the BASELINE configurations.  (Known limit, older than the
-    order: shards of a few dozen rows in float64, and ranks without any rows, fail in a cuBLAS
-    fallback with an illegal leading dimension.)"""
+    test_reduced_configs_sharded on the BASELINE configurations."""
     g = np.random.default_rng(n + G)
     pts = g.uniform(0, 1, (n, 2))
     M = rld.KernelMatrix(rld.KernelSpec("matern52", 1.0, 0.3, 1e-2), pts)
@@ -231,3 +229,13 @@ def test_small_sharded_morton(rld, n, G, dtype, path):
     tol = 1e-11 if dtype == "fp64" else 1e-5
     assert rel(res[0].logdet_P, one.logdet_P) <= tol, (res[0].logdet_P, one.logdet_P)
     assert abs(res[0].trace_term - one.trace_term) <= tol * max(abs(one.logdet_P), abs(one.trace_term), 1.0)
+
+
+def test_sharding_needs_a_row_per_rank(rld):
+    """n = 5 over 4 ranks leaves the last rank without rows: refused up front (NOT_SUPPORTED) on every
+    rank instead of failing somewhere inside the estimate."""
+    pts = np.random.default_rng(0).uniform(0, 1, (5, 2))
+    M = rld.KernelMatrix(rld.KernelSpec("matern52", 1.0, 0.3, 1e-2), pts)
+    cfg = rld.EstimatorConfig("r3", 4, 20, "rademacher", rld.PreconditionerConfig("rand-svd", 3, 2, 1e-12), 1)
+    with pytest.raises(Exception, match="at least one row"):
+        sharded(rld, 4, lambda: rld.rstar_logdet(M, cfg))
